@@ -1,0 +1,227 @@
+/*
+ * ygg.h — C ABI of the B200-native Yggdrasil speculative-decoding step (libygg.so).
+ *
+ * Every entry point takes raw device pointers, plain integer shapes and a cudaStream_t,
+ * returns 0 (YGG_OK) or a ygg_status code, never allocates device memory on the hot path,
+ * never synchronises the stream, and is reentrant (all state is caller-owned).  Argument
+ * errors map to the reference's conventions: YGG_ERR_VALUE ~ ValueError,
+ * YGG_ERR_INDEX ~ IndexError (reference: pkg/src/specsim/token_tree.py:76-77,
+ * egt.py:65-80, cli.py:338-351).  ygg_last_error() returns a thread-local message.
+ *
+ * Reference interfaces replaced (all paths relative to the reference's pkg/src/specsim/):
+ *   ygg_topk_softmax / ygg_egt_grow_level  -> DrafterDistribution.candidates + grow_step
+ *                                             (egt.py:52-114), build_mask row update (token_tree.py:205-218)
+ *   ygg_build_mask                         -> build_mask (token_tree.py:205-218)
+ *   ygg_knapsack_prune                     -> path_products + SubtreeKnapsack + prune_verify + TokenTree.subtree
+ *                                             (acceptance.py:176-184, egt.py:150-282, token_tree.py:146-168)
+ *   ygg_accept                             -> sample_with_probs / VerificationOutcome (acceptance.py:208-241)
+ *   ygg_kv_compact                         -> (new) KV compaction of the accepted path; map = accepted_path
+ *   ygg_gemm_*, ygg_attention, ygg_rmsnorm, ygg_qkv_rope_kv, ... -> the verify / draft forwards the
+ *                                             reference prices as latency_at(...) (simulator.py:202-214)
+ *   ygg_stamp                              -> (new) on-device stage timer feeding LatencyProfile /
+ *                                             StageProfiles tables (latency.py:164-190, scheduler.py:82-103)
+ */
+#ifndef YGG_H_
+#define YGG_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st* ygg_stream_t; /* == cudaStream_t */
+
+typedef enum {
+  YGG_OK = 0,
+  YGG_ERR_VALUE = 1,       /* invalid argument value (ValueError) */
+  YGG_ERR_INDEX = 2,       /* node index out of range (IndexError) */
+  YGG_ERR_CUDA = 3,        /* CUDA runtime / driver failure */
+  YGG_ERR_UNSUPPORTED = 4  /* shape outside the compiled envelope */
+} ygg_status;
+
+typedef enum { YGG_F32 = 0, YGG_BF16 = 1 } ygg_dtype;
+
+#define YGG_MAX_BREAKPOINTS 32
+#define YGG_MAX_MASK_WORDS 8 /* trees up to 256 nodes */
+
+/* Piecewise-linear width->latency curve (reference LatencyProfile, latency.py:34-82). */
+typedef struct {
+  int32_t n;
+  int32_t width[YGG_MAX_BREAKPOINTS];
+  double latency_us[YGG_MAX_BREAKPOINTS];
+} ygg_profile;
+
+/* Reference ProfilePair (latency.py:130-134).  Lives in device memory so the on-device
+ * profiler can refresh it without re-capturing graphs. */
+typedef struct {
+  ygg_profile drafter;
+  ygg_profile verifier;
+} ygg_profile_pair;
+
+/* Batched draft trees, structure-of-arrays, one tree per request.  Mirrors TokenTree
+ * (token_tree.py:34-197): node 0 is the root, parent[i] < i, depth = parent depth + 1. */
+typedef struct {
+  int32_t B;          /* requests */
+  int32_t cap;        /* node capacity per tree */
+  int32_t mask_words; /* u32 words per mask row (ceil(cap/32)) */
+  int32_t* token;     /* [B, cap] */
+  int32_t* parent;    /* [B, cap]; -1 for the root */
+  int32_t* depth;     /* [B, cap] */
+  double* prob;       /* [B, cap] surrogate (drafter) probability */
+  double* cum;        /* [B, cap] product of surrogates root..node, in path order */
+  uint32_t* mask;     /* [B, cap, mask_words] ancestor-or-self bit rows (build_mask) */
+  int32_t* size;      /* [B] node count */
+  int32_t* frontier;  /* [B, cap] newest-level node indices, ascending */
+  int32_t* frontier_n;/* [B] */
+  int32_t* flags;     /* [B] bit0 shortfall, bit1 candidate contract violated, bit2 capacity */
+} ygg_tree;
+
+/* Per-request sequence state of the generate loop (device memory).  hist[b][0..P[b]) are
+ * confirmed tokens whose KV is in the target cache; hist[b][P[b]] is the pending bonus token. */
+typedef struct {
+  int32_t B;        /* requests */
+  int32_t S;        /* history / KV capacity per request */
+  int32_t* hist;    /* [B, S] */
+  int32_t* P;       /* [B] */
+  int32_t* n_gen;   /* [B] tokens generated so far */
+  int32_t* acc_log; /* [B, log_cap] accepted_len per step (ring), may be NULL */
+  int32_t* step;    /* [1] step counter */
+  int32_t log_cap;
+} ygg_seq;
+
+/* ---------------- library ---------------- */
+int ygg_version(void);
+const char* ygg_last_error(void);
+/* Number of SMs and compute capability of the current device; fails unless sm_100. */
+int ygg_device_check(int* num_sms, int* cc_major, int* cc_minor);
+
+/* ---------------- K1: EGT expansion (egt.py:52-114) ---------------- */
+/* Softmax(logits/temperature) top-k per row.  Ties ordered (prob desc, token asc).
+ * logits: [rows, ld] f32 or bf16.  out_tok [rows,k], out_prob [rows,k] (f64 of the f32 value),
+ * out_stats [rows,2] (row max, log-sum-exp) or NULL.  workspace >= ygg_topk_workspace(rows,V,k). */
+size_t ygg_topk_workspace(int rows, int V, int k);
+int ygg_topk_softmax(const void* logits, int dtype, int rows, int V, int ld, int k, float temperature,
+                     int32_t* out_tok, double* out_prob, float* out_stats, void* workspace,
+                     size_t workspace_bytes, ygg_stream_t stream);
+
+/* One grow_step per tree: candidates [B, Fmax, k] (rank order, counts in cand_n [B, Fmax]
+ * or NULL = all k) for frontier rows; attaches the global top-w_draft by
+ * (score desc, parent asc, rank asc), score = cum[parent] * prob (f64), in score order. */
+int ygg_egt_grow_level(ygg_tree tree, int Fmax, int k, int w_draft, const int32_t* cand_tok,
+                       const double* cand_prob, const int32_t* cand_n, ygg_stream_t stream);
+
+/* K7: full mask rebuild from parent links (build_mask). */
+int ygg_build_mask(ygg_tree tree, ygg_stream_t stream);
+
+/* ---------------- K6: knapsack + latency-aware prune (egt.py:150-282) ---------------- */
+typedef struct {
+  int32_t max_verify;  /* knapsack cap = min(max_verify, size) */
+  int32_t d_draft;     /* TreeShape.d_draft for Eq.3 */
+  int32_t w_draft;     /* TreeShape.w_draft for Eq.3 */
+  int32_t fixed_k;     /* >0: skip the objective and keep exactly min(fixed_k, cap) nodes */
+} ygg_prune_args;
+
+/* probs [B, cap] f64 acceptance probabilities (freeze_probs); NULL = use tree.prob.
+ * Outputs: keep_idx [B, cap] kept old indices ascending (-1 padded), new_idx [B, cap] (-1 dropped),
+ * w_verify [B], expected_aal [B], speedup [B], aal_at_cap [B] (1+best(root,cap)), speedup_at_cap [B];
+ * optional best_table [B, cap, max_verify+1] f64 and alloc_table (u8, same shape, indexed by the
+ * merged child) export the DP for SubtreeKnapsack.best_row / pick. */
+int ygg_knapsack_prune(ygg_tree tree, const double* probs, const ygg_profile_pair* profiles_dev,
+                       ygg_prune_args args, int32_t* keep_idx, int32_t* new_idx, int32_t* w_verify,
+                       double* expected_aal, double* speedup, double* aal_at_cap, double* speedup_at_cap,
+                       double* best_table, uint8_t* alloc_table, ygg_stream_t stream);
+
+/* Gather the pruned tree (TokenTree.subtree) into `out` from `in` using keep_idx/new_idx. */
+int ygg_tree_subtree(ygg_tree in, ygg_tree out, const int32_t* keep_idx, const int32_t* new_idx,
+                     ygg_stream_t stream);
+
+/* ---------------- K5: acceptance walk (acceptance.py:221-241) ---------------- */
+typedef enum {
+  YGG_ACCEPT_PROBS = 0,  /* reference semantics: probs[B,cap] f64 + uniforms */
+  YGG_ACCEPT_GREEDY = 1, /* prob(child)=1 iff token == argmax(target row of parent) */
+  YGG_ACCEPT_SAMPLE = 2  /* prob(child)=softmax(target/T) at parent row; residual bonus */
+} ygg_accept_mode;
+
+/* Walk the tree from above the root; one uniform per visited group (uniforms [B, n_uniform]).
+ * Target rows: row 0 = the confirmed/bonus token, row 1+i = tree node i (verify order).
+ * row_argmax [B, rows] (GREEDY), logits [B*rows, ld] + row_stats [B*rows, 2] (SAMPLE).
+ * Outputs: path [B, cap] (accepted node indices), path_len [B], accepted_len [B] = path_len+1,
+ * bonus [B] (GREEDY/SAMPLE: next confirmed token), n_draws [B] uniforms consumed by the walk (or NULL). */
+int ygg_accept(ygg_tree tree, int mode, const double* probs, const double* uniforms, int n_uniform,
+               const int32_t* row_argmax, const void* logits, int logits_dtype, int V, int ld,
+               const float* row_stats, float temperature, int32_t* path, int32_t* path_len,
+               int32_t* accepted_len, int32_t* bonus, int32_t* n_draws, ygg_stream_t stream);
+
+/* ---------------- KV cache + sequence bookkeeping ---------------- */
+/* Per request: move K/V of accepted nodes to contiguous slots after the confirmed token.
+ * cache layout per layer: [B, 2, Hkv, S, hd] (dtype); layer stride in elements.
+ * src slot of accepted node i = base[b] + 1 + map(path[b,i]) where map = keep_idx (or identity
+ * if keep_idx NULL); dst = base[b] + 1 + i.  Nodes with depth >= skip_depth are not moved. */
+int ygg_kv_compact(void* cache, int dtype, int layers, int B, int Hkv, int S, int hd, long long layer_stride,
+                   const int32_t* base, const int32_t* path, const int32_t* path_len, int path_cap,
+                   const int32_t* keep_idx, int keep_cap, const int32_t* node_depth, int depth_cap,
+                   int skip_depth, ygg_stream_t stream);
+
+/* ---------------- dense forward ops ---------------- */
+size_t ygg_gemm_plan_size(void);
+/* Weight-streaming GEMM plan: Y[M,N] = X[M,K] . W[N,K]^T written as per-tile partials
+ * ws[seg][Mpad][128] f32 (seg_first[N/128+1] on device).  bf16 -> tcgen05/TMA, f32 -> SIMT. */
+int ygg_gemm_plan_init(void* plan, int dtype, const void* W, const void* X, int M, int N, int K, int num_ctas,
+                       int32_t* seg_first_dev, int* num_segments, size_t* workspace_bytes);
+int ygg_gemm_run(const void* plan, float* workspace, ygg_stream_t stream);
+
+/* Epilogues over GEMM partials (all deterministic fixed-order segment sums). */
+int ygg_epi_store(const void* plan, const float* ws, void* out, int out_dtype, int ld_out, ygg_stream_t stream);
+int ygg_epi_residual_norm(const void* plan, const float* ws, float* resid, const void* norm_w, float eps,
+                          void* xn_out, int act_dtype, ygg_stream_t stream);
+int ygg_epi_swiglu(const void* plan, const float* ws, void* out, int act_dtype, ygg_stream_t stream);
+/* QKV epilogue: RoPE on q,k at pos[m]; q -> q_out [M, Hq, hd]; k,v -> cache at slot[m] of request req[m]. */
+int ygg_epi_qkv_rope(const void* plan, const float* ws, int Hq, int Hkv, int hd, float rope_theta,
+                     const int32_t* pos, const int32_t* slot, const int32_t* req, void* q_out, void* cache,
+                     int S, int act_dtype, ygg_stream_t stream);
+
+int ygg_embed(const void* table, int dtype, int V, int d, const int32_t* tokens, int M, float* resid_out,
+              ygg_stream_t stream);
+int ygg_rmsnorm(const float* x, const void* w, int dtype, int M, int d, float eps, void* out, ygg_stream_t stream);
+
+/* Tree/prefix attention.  q [M, Hq, hd]; per query row m of request r, mask row
+ * qmask[m, mask_words] over the request's block; keys [0, blk_start[r]) always visible,
+ * keys blk_start[r] + j visible iff bit j (qmask NULL: causal block).  Rows of request r are
+ * the contiguous range [r*M/B, (r+1)*M/B).  out [M, Hq*hd]. */
+int ygg_attention(const void* q, const void* cache, int dtype, int M, int B, int Hq, int Hkv, int hd, int S,
+                  const int32_t* blk_start, const int32_t* blk_len, const uint32_t* qmask, int mask_words,
+                  float scale, void* out, ygg_stream_t stream);
+
+/* Per-row max / argmax / log-sum-exp(x/temperature) over logits [rows, ld]. */
+int ygg_row_stats(const void* logits, int dtype, int rows, int V, int ld, float temperature, int32_t* argmax,
+                  float* stats, ygg_stream_t stream);
+
+int ygg_gemm_seg_table_len(const void* plan);
+
+/* ---------------- step bookkeeping (no host sync) ---------------- */
+/* Draft pass 0 inputs: rows [hist[P-1], hist[P]] per request (R rows, padded). */
+int ygg_pass0_inputs(ygg_seq seq, int R, int tree_cap, int32_t* tokens, int32_t* pos, int32_t* slot, int32_t* req,
+                     uint32_t* qmask, int mask_words, int32_t* blk_start, int32_t* blk_len, ygg_stream_t stream);
+/* Reset each tree to its root = top-1 candidate of pass-0 row `row` (DrafterDistribution.root()). */
+int ygg_init_roots(ygg_tree tree, const int32_t* cand_tok, const double* cand_prob, int k, int R, int row,
+                   ygg_stream_t stream);
+/* Draft pass inputs for the newest tree level (frontier rows, padded to R; cand_n [B,R]). */
+int ygg_level_inputs(ygg_tree tree, ygg_seq seq, int R, int k, int32_t* tokens, int32_t* pos, int32_t* slot,
+                     int32_t* req, uint32_t* qmask, int mask_words, int32_t* blk_start, int32_t* blk_len,
+                     int32_t* cand_n, ygg_stream_t stream);
+/* Verify inputs: bonus row + pruned tree rows, T = vtree.cap + 1 rows per request. */
+int ygg_verify_inputs(ygg_tree vtree, ygg_seq seq, int32_t* tokens, int32_t* pos, int32_t* slot, int32_t* req,
+                      uint32_t* qmask, int mask_words, int32_t* blk_start, int32_t* blk_len, ygg_stream_t stream);
+/* Append accepted tokens + bonus, advance P, log accepted_len. */
+int ygg_commit(ygg_seq seq, ygg_tree vtree, const int32_t* path, const int32_t* path_len, const int32_t* bonus,
+               ygg_stream_t stream);
+
+/* ---------------- K8: on-device stage timer ---------------- */
+int ygg_stamp(unsigned long long* slot, ygg_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* YGG_H_ */

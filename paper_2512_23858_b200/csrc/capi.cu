@@ -1,0 +1,50 @@
+// Library-level C ABI: version, thread-local error text, device check.
+#include <cstdarg>
+#include <cstdio>
+
+#include "common.cuh"
+#include "host_util.h"
+
+namespace ygg {
+static thread_local char g_err[512] = "";
+
+int ygg_fail(int code, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+  return code;
+}
+}  // namespace ygg
+
+extern "C" {
+int ygg_prepare_tree(void);
+int ygg_prepare_gemm(void);
+int ygg_prepare_layers(void);
+int ygg_prepare_attn_tc(void);
+
+int ygg_version(void) { return 100; }
+
+const char* ygg_last_error(void) { return ygg::g_err; }
+
+int ygg_device_check(int* num_sms, int* cc_major, int* cc_minor) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return ygg::ygg_fail(YGG_ERR_CUDA, "cudaGetDevice: %s", cudaGetErrorString(e));
+  cudaDeviceProp prop;
+  e = cudaGetDeviceProperties(&prop, dev);
+  if (e != cudaSuccess) return ygg::ygg_fail(YGG_ERR_CUDA, "cudaGetDeviceProperties: %s", cudaGetErrorString(e));
+  if (num_sms) *num_sms = prop.multiProcessorCount;
+  if (cc_major) *cc_major = prop.major;
+  if (cc_minor) *cc_minor = prop.minor;
+  if (prop.major != 10 || prop.minor != 0)
+    return ygg::ygg_fail(YGG_ERR_UNSUPPORTED, "libygg is built for sm_100a; found sm_%d%d", prop.major, prop.minor);
+  // One-time kernel attributes (dynamic shared memory opt-in) — set here, outside any graph capture.
+  if (int rc = ygg_prepare_tree()) return rc;
+  if (int rc = ygg_prepare_gemm()) return rc;
+  if (int rc = ygg_prepare_layers()) return rc;
+  if (int rc = ygg_prepare_attn_tc()) return rc;
+  return YGG_OK;
+}
+
+}  // extern "C"

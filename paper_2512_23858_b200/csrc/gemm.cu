@@ -1,0 +1,611 @@
+// Weight-streaming small-M GEMM for the draft and verify forwards (K3) and its fused
+// epilogues.  Y[M,N] = X[M,K] . W[N,K]^T.
+//
+// bf16 path ("swap-AB"): the weight tile is the 128-row UMMA A operand, the M<=256 tokens are
+// the UMMA N dimension, so a decode-sized batch still issues full 128-row tcgen05.mma
+// instructions.  Work is split stream-K over the persistent grid: the (tile, k-block) unit
+// space is cut into num_ctas equal contiguous ranges, so every SM streams the same number
+// of weight bytes regardless of N.  Each CTA: warp 0 = TMA producer (weights prefetched
+// before griddepcontrol.wait, activations after), warp 1 = single-thread MMA issuer with a
+// double-buffered TMEM accumulator, warps 2-5 = TMEM->global partial epilogue.
+// Partials ws[seg][BN][128] f32 are reduced by the epilogue kernels in fixed segment order
+// (deterministic), which also apply RoPE/KV-append, residual+RMSNorm or SwiGLU.
+//
+// f32 path (parity mode): SIMT tiled GEMM writing the same partial layout, one segment per tile.
+#include <cudaTypedefs.h>
+
+#include <cmath>
+#include <cstring>
+#include <vector>
+
+#include "common.cuh"
+#include "host_util.h"
+
+namespace ygg {
+
+constexpr int kBM = 128;          // weight rows per tile (UMMA M)
+constexpr int kBK = 64;           // k per stage: 64 bf16 = one 128B swizzle row
+constexpr int kGemmThreads = 192; // 6 warps
+constexpr int kSmemBudget = 200 * 1024;
+
+struct GemmPlan {
+  uint32_t magic;
+  int dtype;
+  int M, N, K;
+  int BN;        // tokens per tile (multiple of 16, <= 256)
+  int m_tiles, n_tiles, tiles, kb;
+  int num_ctas;
+  long long units;
+  int segments;
+  int stages;
+  int tmem_cols;
+  const void* W;
+  const void* X;
+  int32_t* seg_table;  // device: seg_first[tiles+1], seg_base[num_ctas]
+  alignas(64) CUtensorMap tmap_w;
+  alignas(64) CUtensorMap tmap_x;
+};
+constexpr uint32_t kPlanMagic = 0x59474750u;  // "YGGP"
+
+struct GemmParams {
+  int M, BN, m_tiles, kb, num_ctas, stages, tmem_cols;
+  long long units;
+  const int32_t* seg_first;
+  const int32_t* seg_base;
+};
+
+// ---------------------------------------------------------------------------
+// tcgen05 kernel
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kGemmThreads, 1)
+    gemm_bf16_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant__ CUtensorMap tmap_x,
+                        GemmParams p, float* __restrict__ ws) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  // 1024-align the dynamic smem base (SW128 atoms).
+  unsigned char* base = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int BN = p.BN, S = p.stages;
+  const uint32_t a_bytes = kBM * kBK * 2;
+  const uint32_t b_bytes = BN * kBK * 2;
+  unsigned char* sa = base;
+  unsigned char* sb = base + static_cast<size_t>(S) * a_bytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sb + static_cast<size_t>(S) * b_bytes);
+  uint64_t* empty = full + S;
+  uint64_t* tfull = empty + S;   // [2]
+  uint64_t* tempty = tfull + 2;  // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int c = blockIdx.x;
+  const long long u0 = p.units * c / p.num_ctas, u1 = p.units * (c + 1) / p.num_ctas;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmap_w);
+    tma_prefetch_desc(&tmap_x);
+    for (int s = 0; s < S; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    for (int a = 0; a < 2; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], 128); }
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, p.tmem_cols);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  pdl_launch_dependents();
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ===== TMA producer =====
+      const uint64_t pol_w = policy_evict_first();
+      const uint64_t pol_x = policy_evict_last();
+      const long long n_units = u1 - u0;
+      const int pre = static_cast<int>(n_units < S ? n_units : S);
+      // Weights never depend on the previous kernel: stream them before the grid dependency.
+      for (int i = 0; i < pre; ++i) {
+        const long long u = u0 + i;
+        const int tile = static_cast<int>(u / p.kb), kblk = static_cast<int>(u % p.kb);
+        const int n_tile = tile / p.m_tiles;
+        mbar_arrive_expect_tx(&full[i], a_bytes + b_bytes);
+        tma_load_2d(sa + static_cast<size_t>(i) * a_bytes, &tmap_w, &full[i], kblk * kBK, n_tile * kBM, pol_w);
+      }
+      pdl_wait();
+      for (int i = 0; i < pre; ++i) {
+        const long long u = u0 + i;
+        const int tile = static_cast<int>(u / p.kb), kblk = static_cast<int>(u % p.kb);
+        const int m_tile = tile % p.m_tiles;
+        tma_load_2d(sb + static_cast<size_t>(i) * b_bytes, &tmap_x, &full[i], kblk * kBK, m_tile * BN, pol_x);
+      }
+      int stage = pre % S;
+      uint32_t phase = (pre == S) ? 1u : 0u;
+      for (long long u = u0 + pre; u < u1; ++u) {
+        mbar_wait(&empty[stage], phase ^ 1u);
+        const int tile = static_cast<int>(u / p.kb), kblk = static_cast<int>(u % p.kb);
+        const int n_tile = tile / p.m_tiles, m_tile = tile % p.m_tiles;
+        mbar_arrive_expect_tx(&full[stage], a_bytes + b_bytes);
+        tma_load_2d(sa + static_cast<size_t>(stage) * a_bytes, &tmap_w, &full[stage], kblk * kBK, n_tile * kBM, pol_w);
+        tma_load_2d(sb + static_cast<size_t>(stage) * b_bytes, &tmap_x, &full[stage], kblk * kBK, m_tile * BN, pol_x);
+        if (++stage == S) { stage = 0; phase ^= 1u; }
+      }
+    }
+  } else if (warp == 1) {
+    pdl_wait();
+    // ===== MMA issuer =====
+    const uint32_t idesc = umma_idesc_bf16(kBM, BN);
+    int stage = 0;
+    uint32_t phase = 0;
+    int acc = 0;
+    uint32_t acc_phase[2] = {0u, 0u};
+    long long u = u0;
+    while (u < u1) {
+      const int tile = static_cast<int>(u / p.kb);
+      const long long tile_end = static_cast<long long>(tile + 1) * p.kb;
+      const long long seg_end = tile_end < u1 ? tile_end : u1;
+      // Wait for the epilogue to drain this accumulator buffer.
+      mbar_wait(&tempty[acc], acc_phase[acc] ^ 1u);
+      tc_fence_after();
+      const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * BN);
+      bool first = true;
+      for (; u < seg_end; ++u) {
+        mbar_wait(&full[stage], phase);
+        tc_fence_after();
+        if (lane == 0) {
+          const uint32_t a_addr = smem_u32(sa + static_cast<size_t>(stage) * a_bytes);
+          const uint32_t b_addr = smem_u32(sb + static_cast<size_t>(stage) * b_bytes);
+#pragma unroll
+          for (int k = 0; k < kBK / 16; ++k) {
+            const uint64_t ad = umma_desc_sw128(a_addr + k * 32);
+            const uint64_t bd = umma_desc_sw128(b_addr + k * 32);
+            umma_bf16(d_tmem, ad, bd, idesc, (first && k == 0) ? 0u : 1u);
+          }
+          umma_commit(&empty[stage]);
+        }
+        __syncwarp();
+        first = false;
+        if (++stage == S) { stage = 0; phase ^= 1u; }
+      }
+      if (lane == 0) umma_commit(&tfull[acc]);
+      __syncwarp();
+      acc_phase[acc] ^= 1u;
+      acc ^= 1;
+    }
+  } else {
+    pdl_wait();
+    // ===== Epilogue: TMEM -> registers -> partial workspace =====
+    const int quarter = warp & 3;  // TMEM lanes accessible by this warp
+    const int row = quarter * 32 + lane;
+    int acc = 0;
+    uint32_t acc_phase[2] = {0u, 0u};
+    long long u = u0;
+    while (u < u1) {
+      const int tile = static_cast<int>(u / p.kb);
+      const long long tile_end = static_cast<long long>(tile + 1) * p.kb;
+      const long long seg_end = tile_end < u1 ? tile_end : u1;
+      const int seg = (u == u0) ? p.seg_base[c] : p.seg_first[tile];
+      const int m_tile = tile % p.m_tiles;
+      const int valid = min(BN, p.M - m_tile * BN);
+      mbar_wait(&tfull[acc], acc_phase[acc]);
+      tc_fence_after();
+      float* dst = ws + static_cast<size_t>(seg) * BN * kBM + row;
+      const uint32_t taddr = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + static_cast<uint32_t>(acc * BN);
+      for (int c0 = 0; c0 < BN; c0 += 16) {
+        float v[16];
+        tmem_ld16(taddr + c0, v);
+#pragma unroll
+        for (int j = 0; j < 16; ++j)
+          if (c0 + j < valid) dst[static_cast<size_t>(c0 + j) * kBM] = v[j];
+      }
+      tc_fence_before();
+      mbar_arrive(&tempty[acc]);
+      acc_phase[acc] ^= 1u;
+      acc ^= 1;
+      u = seg_end;
+    }
+  }
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, p.tmem_cols);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// SIMT f32 kernel (parity mode): 128 (n) x 32 (m) tile per CTA, 256 threads, 4x4 per thread.
+// ---------------------------------------------------------------------------
+constexpr int kSimtBN = 32, kSimtBK = 32;
+__global__ void __launch_bounds__(256) gemm_f32_simt_kernel(const float* __restrict__ W, const float* __restrict__ X,
+                                                            int M, int N, int K, int BN, int m_tiles,
+                                                            float* __restrict__ ws) {
+  pdl_wait();
+  pdl_launch_dependents();
+  __shared__ float sw[kSimtBK][kBM + 4];
+  __shared__ float sx[kSimtBK][kSimtBN + 4];
+  const int n_tile = blockIdx.x, msub = blockIdx.y;  // msub: 32-token slice of the full M
+  const int m0 = msub * kSimtBN;
+  const int tid = threadIdx.x;
+  const int tn = tid % 32, tm = tid / 32;  // thread owns n = tn + 32*i, m = tm + 8*j
+  float acc[4][4] = {};
+  for (int k0 = 0; k0 < K; k0 += kSimtBK) {
+    for (int i = tid; i < kBM * kSimtBK; i += 256) {
+      const int r = i / kSimtBK, kk = i % kSimtBK;
+      sw[kk][r] = W[static_cast<size_t>(n_tile * kBM + r) * K + k0 + kk];
+    }
+    for (int i = tid; i < kSimtBN * kSimtBK; i += 256) {
+      const int r = i / kSimtBK, kk = i % kSimtBK;
+      const int m = m0 + r;
+      sx[kk][r] = (m < M) ? X[static_cast<size_t>(m) * K + k0 + kk] : 0.f;
+    }
+    __syncthreads();
+#pragma unroll 8
+    for (int kk = 0; kk < kSimtBK; ++kk) {
+      float a[4], bx[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) a[i] = sw[kk][tn + 32 * i];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) bx[j] = sx[kk][tm + 8 * j];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(a[i], bx[j], acc[i][j]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int m = m0 + tm + 8 * j;
+    if (m >= M) continue;
+    const int m_tile = m / BN, mr = m % BN;
+    const int seg = n_tile * m_tiles + m_tile;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) ws[(static_cast<size_t>(seg) * BN + mr) * kBM + tn + 32 * i] = acc[i][j];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Epilogues.  value(m, n) = sum over segments of tile(n/128, m/BN) of ws[seg][m%BN][n%128].
+// ---------------------------------------------------------------------------
+struct EpiGeom {
+  int M, N, BN, m_tiles;
+  const int32_t* seg_first;
+};
+
+YGG_DEV float epi_value(const EpiGeom& g, const float* __restrict__ ws, int m, int n) {
+  const int t = (n / kBM) * g.m_tiles + m / g.BN;
+  const int s0 = g.seg_first[t], s1 = g.seg_first[t + 1];
+  const size_t off = static_cast<size_t>(m % g.BN) * kBM + (n % kBM);
+  float v = 0.f;
+  for (int s = s0; s < s1; ++s) v += ws[static_cast<size_t>(s) * g.BN * kBM + off];
+  return v;
+}
+
+template <typename OutT>
+__global__ void epi_store_kernel(EpiGeom g, const float* __restrict__ ws, OutT* __restrict__ out, int ld) {
+  pdl_wait();
+  pdl_launch_dependents();
+  const int m = blockIdx.y;
+  for (int n = blockIdx.x * blockDim.x + threadIdx.x; n < g.N; n += gridDim.x * blockDim.x)
+    out[static_cast<size_t>(m) * ld + n] = from_f32<OutT>(epi_value(g, ws, m, n));
+}
+
+// Block-wide deterministic sum (fixed tree).
+template <int kThreads>
+YGG_DEV float block_sum(float v, float* red) {
+  v = warp_sum(v);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  __syncthreads();
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  float t = 0.f;
+  if (threadIdx.x < 32) {
+    t = (lane < kThreads / 32) ? red[lane] : 0.f;
+    t = warp_sum(t);
+    if (lane == 0) red[0] = t;
+  }
+  __syncthreads();
+  return red[0];
+}
+
+constexpr int kRowThreads = 256;
+constexpr int kMaxRowDim = 16384;
+
+template <typename ActT, typename WT>
+__global__ void __launch_bounds__(kRowThreads) epi_residual_norm_kernel(EpiGeom g, const float* __restrict__ ws,
+                                                                        float* __restrict__ resid,
+                                                                        const WT* __restrict__ norm_w, float eps,
+                                                                        ActT* __restrict__ xn) {
+  pdl_wait();
+  pdl_launch_dependents();
+  __shared__ float red[32];
+  const int m = blockIdx.x;
+  float* h = resid + static_cast<size_t>(m) * g.N;
+  float ss = 0.f;
+  for (int n = threadIdx.x; n < g.N; n += blockDim.x) {
+    const float v = h[n] + epi_value(g, ws, m, n);
+    h[n] = v;
+    ss += v * v;
+  }
+  const float tot = block_sum<kRowThreads>(ss, red);
+  const float r = rsqrtf(tot / static_cast<float>(g.N) + eps);
+  for (int n = threadIdx.x; n < g.N; n += blockDim.x)
+    xn[static_cast<size_t>(m) * g.N + n] = from_f32<ActT>(h[n] * r * to_f32(norm_w[n]));
+}
+
+template <typename ActT>
+__global__ void epi_swiglu_kernel(EpiGeom g, const float* __restrict__ ws, ActT* __restrict__ out) {
+  pdl_wait();
+  pdl_launch_dependents();
+  const int m = blockIdx.y;
+  const int F = g.N / 2;
+  for (int f = blockIdx.x * blockDim.x + threadIdx.x; f < F; f += gridDim.x * blockDim.x) {
+    const float gate = epi_value(g, ws, m, f);
+    const float up = epi_value(g, ws, m, F + f);
+    const float silu = gate / (1.f + expf(-gate));
+    out[static_cast<size_t>(m) * F + f] = from_f32<ActT>(silu * up);
+  }
+}
+
+// QKV epilogue: RoPE (rotate-half convention) on q and k at pos[m]; q -> q_out, k/v -> KV cache.
+template <typename ActT>
+__global__ void epi_qkv_rope_kernel(EpiGeom g, const float* __restrict__ ws, int Hq, int Hkv, int hd,
+                                    float log2_theta, const int32_t* __restrict__ pos,
+                                    const int32_t* __restrict__ slot, const int32_t* __restrict__ req,
+                                    ActT* __restrict__ q_out, ActT* __restrict__ cache, int S) {
+  pdl_wait();
+  pdl_launch_dependents();
+  const int m = blockIdx.x;
+  const int head = blockIdx.y;  // 0..Hq+2*Hkv-1
+  const int half = hd / 2;
+  const float p = static_cast<float>(pos[m]);
+  const int n0 = head * hd;
+  for (int i = threadIdx.x; i < half; i += blockDim.x) {
+    float x1 = epi_value(g, ws, m, n0 + i);
+    float x2 = epi_value(g, ws, m, n0 + i + half);
+    if (head < Hq + Hkv) {
+      // inv_freq = theta^(-2i/hd), as 1/(theta**(2i/hd)) in f32
+      const float inv_freq = 1.0f / exp2f(log2_theta * (static_cast<float>(2 * i) / static_cast<float>(hd)));
+      const float ang = p * inv_freq;
+      float sn, cs;
+      sincosf(ang, &sn, &cs);
+      const float y1 = x1 * cs - x2 * sn;
+      const float y2 = x2 * cs + x1 * sn;
+      x1 = y1;
+      x2 = y2;
+    }
+    if (head < Hq) {
+      ActT* q = q_out + (static_cast<size_t>(m) * Hq + head) * hd;
+      q[i] = from_f32<ActT>(x1);
+      q[i + half] = from_f32<ActT>(x2);
+    } else {
+      const bool is_v = head >= Hq + Hkv;
+      const int kvh = is_v ? head - Hq - Hkv : head - Hq;
+      const size_t off = ((static_cast<size_t>(req[m]) * 2 + (is_v ? 1 : 0)) * Hkv + kvh) * static_cast<size_t>(S) * hd +
+                         static_cast<size_t>(slot[m]) * hd;
+      cache[off + i] = from_f32<ActT>(x1);
+      cache[off + i + half] = from_f32<ActT>(x2);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Host side
+// ---------------------------------------------------------------------------
+static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
+  }
+  return fn;
+}
+
+static int make_map_bf16(CUtensorMap* map, const void* ptr, int rows, int cols, int box_rows) {
+  auto enc = get_encode();
+  if (!enc) return ygg_fail(YGG_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(cols) * 2};
+  cuuint32_t box[2] = {static_cast<cuuint32_t>(kBK), static_cast<cuuint32_t>(box_rows)};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return ygg_fail(YGG_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", static_cast<int>(r));
+  return YGG_OK;
+}
+
+static const GemmPlan* as_plan(const void* p) {
+  const GemmPlan* g = static_cast<const GemmPlan*>(p);
+  return (g && g->magic == kPlanMagic) ? g : nullptr;
+}
+
+static EpiGeom geom_of(const GemmPlan* g) { return EpiGeom{g->M, g->N, g->BN, g->m_tiles, g->seg_table}; }
+
+}  // namespace ygg
+
+using namespace ygg;
+
+extern "C" {
+
+int ygg_prepare_gemm(void) {
+  cudaError_t e = cudaFuncSetAttribute(gemm_bf16_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+  if (e != cudaSuccess) return ygg_fail(YGG_ERR_CUDA, "gemm attribute: %s", cudaGetErrorString(e));
+  return YGG_OK;
+}
+
+size_t ygg_gemm_plan_size(void) { return sizeof(GemmPlan) + 64; }
+
+int ygg_gemm_plan_init(void* plan_mem, int dtype, const void* W, const void* X, int M, int N, int K, int num_ctas,
+                       int32_t* seg_table_dev, int* num_segments, size_t* workspace_bytes) {
+  YGG_CHECK_ARG(plan_mem && W && X && seg_table_dev, "null pointer");
+  YGG_CHECK_ARG(M >= 1 && N >= kBM && K >= kBK, "bad GEMM shape");
+  YGG_CHECK_ARG(N % kBM == 0, "N must be a multiple of 128");
+  YGG_CHECK_ARG(K % kBK == 0, "K must be a multiple of 64");
+  GemmPlan* g = reinterpret_cast<GemmPlan*>((reinterpret_cast<uintptr_t>(plan_mem) + 63) & ~uintptr_t(63));
+  std::memset(g, 0, sizeof(GemmPlan));
+  g->magic = kPlanMagic;
+  g->dtype = dtype;
+  g->M = M;
+  g->N = N;
+  g->K = K;
+  const int mp = (M + 15) / 16 * 16;
+  g->BN = mp <= 256 ? mp : 256;
+  if (dtype == YGG_F32) g->BN = mp <= 256 ? mp : 256;
+  g->m_tiles = (M + g->BN - 1) / g->BN;
+  g->n_tiles = N / kBM;
+  g->tiles = g->n_tiles * g->m_tiles;
+  g->kb = K / kBK;
+  g->W = W;
+  g->X = X;
+  g->seg_table = seg_table_dev;
+  std::vector<int32_t> table;
+  if (dtype == YGG_BF16) {
+    if (num_ctas <= 0) num_ctas = kNumSMs;
+    g->units = static_cast<long long>(g->tiles) * g->kb;
+    if (num_ctas > g->units) num_ctas = static_cast<int>(g->units);
+    g->num_ctas = num_ctas;
+    const int stage_bytes = kBM * kBK * 2 + g->BN * kBK * 2;
+    g->stages = std::min(12, (kSmemBudget - 1024 - 256) / stage_bytes);
+    YGG_CHECK_ARG(g->stages >= 2, "tile too large for shared memory");
+    int cols = 32;
+    while (cols < 2 * g->BN) cols *= 2;
+    g->tmem_cols = cols;
+    // Segment enumeration in (cta, tile) order == (tile, cta) order.
+    std::vector<int32_t> seg_first(g->tiles + 1, 0), seg_base(num_ctas, 0);
+    std::vector<int> count(g->tiles, 0);
+    int seg = 0;
+    for (int c = 0; c < num_ctas; ++c) {
+      const long long u0 = g->units * c / num_ctas, u1 = g->units * (c + 1) / num_ctas;
+      seg_base[c] = seg;
+      if (u1 > u0) {
+        const int t0 = static_cast<int>(u0 / g->kb), t1 = static_cast<int>((u1 - 1) / g->kb);
+        for (int t = t0; t <= t1; ++t) ++count[t];
+        seg += t1 - t0 + 1;
+      }
+    }
+    int acc = 0;
+    for (int t = 0; t < g->tiles; ++t) { seg_first[t] = acc; acc += count[t]; }
+    seg_first[g->tiles] = acc;
+    g->segments = seg;
+    table = seg_first;
+    table.insert(table.end(), seg_base.begin(), seg_base.end());
+    if (int rc = make_map_bf16(&g->tmap_w, W, N, K, kBM)) return rc;
+    if (int rc = make_map_bf16(&g->tmap_x, X, M, K, g->BN)) return rc;
+  } else if (dtype == YGG_F32) {
+    g->num_ctas = 0;
+    g->segments = g->tiles;
+    table.resize(g->tiles + 1);
+    for (int t = 0; t <= g->tiles; ++t) table[t] = t;
+  } else {
+    return ygg_fail(YGG_ERR_VALUE, "unknown dtype");
+  }
+  cudaError_t e = cudaMemcpy(seg_table_dev, table.data(), table.size() * sizeof(int32_t), cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) return ygg_fail(YGG_ERR_CUDA, "seg table upload: %s", cudaGetErrorString(e));
+  if (num_segments) *num_segments = g->segments;
+  if (workspace_bytes) *workspace_bytes = static_cast<size_t>(g->segments) * g->BN * kBM * sizeof(float);
+  return YGG_OK;
+}
+
+int ygg_gemm_seg_table_len(const void* plan) {
+  const GemmPlan* g = as_plan(reinterpret_cast<const void*>((reinterpret_cast<uintptr_t>(plan) + 63) & ~uintptr_t(63)));
+  if (!g) return -1;
+  return g->tiles + 1 + g->num_ctas;
+}
+
+static const GemmPlan* plan_of(const void* plan) {
+  return as_plan(reinterpret_cast<const void*>((reinterpret_cast<uintptr_t>(plan) + 63) & ~uintptr_t(63)));
+}
+
+int ygg_gemm_run(const void* plan, float* workspace, ygg_stream_t stream) {
+  const GemmPlan* g = plan_of(plan);
+  YGG_CHECK_ARG(g != nullptr, "invalid GEMM plan");
+  YGG_CHECK_ARG(workspace != nullptr, "null workspace");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  if (g->dtype == YGG_BF16) {
+    GemmParams p;
+    p.M = g->M;
+    p.BN = g->BN;
+    p.m_tiles = g->m_tiles;
+    p.kb = g->kb;
+    p.num_ctas = g->num_ctas;
+    p.stages = g->stages;
+    p.tmem_cols = g->tmem_cols;
+    p.units = g->units;
+    p.seg_first = g->seg_table;
+    p.seg_base = g->seg_table + g->tiles + 1;
+    const size_t smem = 1024 + static_cast<size_t>(g->stages) * (kBM * kBK * 2 + g->BN * kBK * 2) + 256;
+    YGG_LAUNCH_PDL(gemm_bf16_tc_kernel, dim3(g->num_ctas), dim3(kGemmThreads), smem, s, g->tmap_w, g->tmap_x, p,
+                   workspace);
+  } else {
+    dim3 grid(g->n_tiles, (g->M + kSimtBN - 1) / kSimtBN);
+    YGG_LAUNCH_PDL(gemm_f32_simt_kernel, grid, dim3(256), 0, s, static_cast<const float*>(g->W),
+                   static_cast<const float*>(g->X), g->M, g->N, g->K, g->BN, g->m_tiles, workspace);
+  }
+  return YGG_OK;
+}
+
+int ygg_epi_store(const void* plan, const float* ws, void* out, int out_dtype, int ld_out, ygg_stream_t stream) {
+  const GemmPlan* g = plan_of(plan);
+  YGG_CHECK_ARG(g && ws && out, "invalid arguments");
+  YGG_CHECK_ARG(ld_out >= g->N, "ld_out < N");
+  EpiGeom geo = geom_of(g);
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  dim3 grid(std::min((g->N + 255) / 256, 64), g->M);
+  if (out_dtype == YGG_F32)
+    YGG_LAUNCH_PDL(epi_store_kernel<float>, grid, dim3(256), 0, s, geo, ws, static_cast<float*>(out), ld_out);
+  else
+    YGG_LAUNCH_PDL(epi_store_kernel<__nv_bfloat16>, grid, dim3(256), 0, s, geo, ws, static_cast<__nv_bfloat16*>(out),
+                   ld_out);
+  return YGG_OK;
+}
+
+int ygg_epi_residual_norm(const void* plan, const float* ws, float* resid, const void* norm_w, float eps, void* xn_out,
+                          int act_dtype, ygg_stream_t stream) {
+  const GemmPlan* g = plan_of(plan);
+  YGG_CHECK_ARG(g && ws && resid && norm_w && xn_out, "invalid arguments");
+  YGG_CHECK_ARG(g->N <= kMaxRowDim, "row too wide");
+  EpiGeom geo = geom_of(g);
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  if (act_dtype == YGG_F32)
+    YGG_LAUNCH_PDL((epi_residual_norm_kernel<float, float>), dim3(g->M), dim3(kRowThreads), 0, s, geo, ws, resid,
+                   static_cast<const float*>(norm_w), eps, static_cast<float*>(xn_out));
+  else
+    YGG_LAUNCH_PDL((epi_residual_norm_kernel<__nv_bfloat16, __nv_bfloat16>), dim3(g->M), dim3(kRowThreads), 0, s, geo,
+                   ws, resid, static_cast<const __nv_bfloat16*>(norm_w), eps, static_cast<__nv_bfloat16*>(xn_out));
+  return YGG_OK;
+}
+
+int ygg_epi_swiglu(const void* plan, const float* ws, void* out, int act_dtype, ygg_stream_t stream) {
+  const GemmPlan* g = plan_of(plan);
+  YGG_CHECK_ARG(g && ws && out, "invalid arguments");
+  YGG_CHECK_ARG(g->N % 2 == 0, "gate_up width must be even");
+  EpiGeom geo = geom_of(g);
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  dim3 grid(std::min((g->N / 2 + 255) / 256, 64), g->M);
+  if (act_dtype == YGG_F32)
+    YGG_LAUNCH_PDL(epi_swiglu_kernel<float>, grid, dim3(256), 0, s, geo, ws, static_cast<float*>(out));
+  else
+    YGG_LAUNCH_PDL(epi_swiglu_kernel<__nv_bfloat16>, grid, dim3(256), 0, s, geo, ws, static_cast<__nv_bfloat16*>(out));
+  return YGG_OK;
+}
+
+int ygg_epi_qkv_rope(const void* plan, const float* ws, int Hq, int Hkv, int hd, float rope_theta, const int32_t* pos,
+                     const int32_t* slot, const int32_t* req, void* q_out, void* cache, int S, int act_dtype,
+                     ygg_stream_t stream) {
+  const GemmPlan* g = plan_of(plan);
+  YGG_CHECK_ARG(g && ws && pos && slot && req && q_out && cache, "invalid arguments");
+  YGG_CHECK_ARG(g->N == (Hq + 2 * Hkv) * hd, "QKV width mismatch");
+  YGG_CHECK_ARG(hd % 2 == 0 && hd <= 256, "bad head dim");
+  EpiGeom geo = geom_of(g);
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  dim3 grid(g->M, Hq + 2 * Hkv);
+  const float l2t = log2f(rope_theta);
+  if (act_dtype == YGG_F32)
+    YGG_LAUNCH_PDL(epi_qkv_rope_kernel<float>, grid, dim3(64), 0, s, geo, ws, Hq, Hkv, hd, l2t, pos, slot, req,
+                   static_cast<float*>(q_out), static_cast<float*>(cache), S);
+  else
+    YGG_LAUNCH_PDL(epi_qkv_rope_kernel<__nv_bfloat16>, grid, dim3(64), 0, s, geo, ws, Hq, Hkv, hd, l2t, pos, slot, req,
+                   static_cast<__nv_bfloat16*>(q_out), static_cast<__nv_bfloat16*>(cache), S);
+  return YGG_OK;
+}
+
+}  // extern "C"

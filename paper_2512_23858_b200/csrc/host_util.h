@@ -1,0 +1,46 @@
+// Host-side helpers shared by every translation unit of libygg.so: thread-local error text,
+// argument checks that map to the reference's ValueError convention, and a launch macro
+// that always enables programmatic dependent launch (PDL) so consecutive kernels of a step
+// overlap their prologues with the previous kernel's tail.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+
+#include "../../include/ygg.h"
+
+namespace ygg {
+
+int ygg_fail(int code, const char* fmt, ...);
+
+template <typename Kernel, typename... Args>
+int launch_pdl(Kernel kernel, dim3 grid, dim3 block, size_t smem, cudaStream_t stream, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaError_t err = cudaLaunchKernelEx(&cfg, kernel, args...);
+  if (err != cudaSuccess) return ygg_fail(YGG_ERR_CUDA, "launch failed: %s", cudaGetErrorString(err));
+  return YGG_OK;
+}
+
+}  // namespace ygg
+
+#define YGG_CHECK_ARG(cond, msg)                                   \
+  do {                                                             \
+    if (!(cond)) return ::ygg::ygg_fail(YGG_ERR_VALUE, "%s", msg); \
+  } while (0)
+
+#define YGG_LAUNCH_PDL(kernel, grid, block, smem, stream, ...)                                    \
+  do {                                                                                            \
+    int _rc = ::ygg::launch_pdl(kernel, grid, block, smem, stream, __VA_ARGS__);                  \
+    if (_rc) return _rc;                                                                          \
+  } while (0)

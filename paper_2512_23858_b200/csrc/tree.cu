@@ -1,0 +1,866 @@
+// Tree kernels of the speculative step: EGT expansion (K1), mask (K7), knapsack prune (K6),
+// acceptance walk (K5) and KV compaction.  Compiled with --fmad=false: every f64 expression
+// here must round exactly like the CPython float arithmetic of the reference.
+//
+// Reference (pkg/src/specsim/): egt.py:65-114 (candidates, grow_step), egt.py:150-282
+// (SubtreeKnapsack, prune_verify), acceptance.py:176-184 (path_products), acceptance.py:221-241
+// (sample_with_probs), token_tree.py:146-168 (subtree), token_tree.py:205-218 (build_mask),
+// latency.py:68-82,154-161 (latency_at, tree_speedup).
+#include "common.cuh"
+#include "host_util.h"
+
+#include <cfloat>
+#include <cmath>
+
+namespace ygg {
+
+constexpr double kSiblingTol = 1e-9;  // token_tree.py:31
+enum : int32_t { kFlagShortfall = 1, kFlagContract = 2, kFlagCapacity = 4, kFlagStopped = 8, kFlagIndex = 16 };
+
+// ===========================================================================
+// K1a: softmax + top-k per row (DrafterDistribution.candidates realised on draft logits).
+// Phase 1: each CTA scans a chunk of one row: chunk max, f64 sum of exp, local top-k by
+// (logit desc, token asc).  Phase 2: one CTA per row merges chunks deterministically.
+// ===========================================================================
+constexpr int kTopkMaxK = 32;
+constexpr int kTopkChunk = 4096;
+constexpr int kTopkThreads = 256;
+
+struct TopkChunkOut {
+  float max_s;
+  double sum_exp;
+  float val[kTopkMaxK];
+  int32_t tok[kTopkMaxK];
+};
+
+YGG_DEV bool better(float va, int ta, float vb, int tb) { return va > vb || (va == vb && ta < tb); }
+
+template <typename T>
+__global__ void __launch_bounds__(kTopkThreads) topk_phase1(const T* __restrict__ logits, int V, int ld, int k,
+                                                            float inv_temp, int nchunks, TopkChunkOut* out) {
+  pdl_wait();
+  const int row = blockIdx.y, chunk = blockIdx.x;
+  const int begin = chunk * kTopkChunk, end = min(V, begin + kTopkChunk);
+  __shared__ float sv[kTopkChunk];
+  __shared__ float red_f[kTopkThreads / 32];
+  __shared__ double red_d[kTopkThreads / 32];
+  __shared__ int red_i[kTopkThreads / 32];
+  const T* src = logits + static_cast<size_t>(row) * ld;
+  float lmax = -INFINITY;
+  for (int i = begin + threadIdx.x; i < end; i += blockDim.x) {
+    float v = to_f32(src[i]) * inv_temp;
+    sv[i - begin] = v;
+    lmax = fmaxf(lmax, v);
+  }
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  lmax = warp_max(lmax);
+  if (lane == 0) red_f[warp] = lmax;
+  __syncthreads();
+  float cmax = red_f[0];
+  for (int w = 1; w < kTopkThreads / 32; ++w) cmax = fmaxf(cmax, red_f[w]);
+  double s = 0.0;
+  for (int i = begin + threadIdx.x; i < end; i += blockDim.x) s += exp(static_cast<double>(sv[i - begin]) - cmax);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane == 0) red_d[warp] = s;
+  __syncthreads();
+  TopkChunkOut* o = out + static_cast<size_t>(row) * nchunks + chunk;
+  if (threadIdx.x == 0) {
+    double tot = 0.0;
+    for (int w = 0; w < kTopkThreads / 32; ++w) tot += red_d[w];
+    o->max_s = cmax;
+    o->sum_exp = tot;
+  }
+  // k rounds of block arg-best with removal.
+  for (int r = 0; r < k; ++r) {
+    float bv = -INFINITY;
+    int bt = 0x7fffffff;
+    for (int i = begin + threadIdx.x; i < end; i += blockDim.x) {
+      float v = sv[i - begin];
+      if (!isnan(v) && better(v, i, bv, bt)) { bv = v; bt = i; }
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      float ov = __shfl_xor_sync(0xffffffffu, bv, off);
+      int ot = __shfl_xor_sync(0xffffffffu, bt, off);
+      if (better(ov, ot, bv, bt)) { bv = ov; bt = ot; }
+    }
+    __syncthreads();
+    if (lane == 0) { red_f[warp] = bv; red_i[warp] = bt; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      float fv = red_f[0];
+      int ft = red_i[0];
+      for (int w = 1; w < kTopkThreads / 32; ++w)
+        if (better(red_f[w], red_i[w], fv, ft)) { fv = red_f[w]; ft = red_i[w]; }
+      o->val[r] = fv;
+      o->tok[r] = (ft == 0x7fffffff) ? -1 : ft;
+      if (ft != 0x7fffffff) sv[ft - begin] = __int_as_float(0x7fc00000);  // NaN marks taken
+    }
+    __syncthreads();
+  }
+  pdl_launch_dependents();
+}
+
+__global__ void __launch_bounds__(kTopkThreads) topk_phase2(const TopkChunkOut* __restrict__ chunks, int nchunks,
+                                                            int k, int32_t* out_tok, double* out_prob,
+                                                            float* out_stats) {
+  pdl_wait();
+  const int row = blockIdx.x;
+  const TopkChunkOut* c = chunks + static_cast<size_t>(row) * nchunks;
+  extern __shared__ unsigned char smem_raw[];
+  float* cv = reinterpret_cast<float*>(smem_raw);
+  int* ct = reinterpret_cast<int*>(cv + nchunks * k);
+  __shared__ float gmax_s;
+  __shared__ double z_s;
+  __shared__ float sel_v[kTopkMaxK];
+  __shared__ int sel_t[kTopkMaxK];
+  const int n = nchunks * k;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    cv[i] = c[i / k].val[i % k];
+    ct[i] = c[i / k].tok[i % k];
+  }
+  if (threadIdx.x == 0) {
+    float m = -INFINITY;
+    for (int j = 0; j < nchunks; ++j) m = fmaxf(m, c[j].max_s);
+    double z = 0.0;  // fixed chunk order => deterministic
+    for (int j = 0; j < nchunks; ++j) z += c[j].sum_exp * exp(static_cast<double>(c[j].max_s) - m);
+    gmax_s = m;
+    z_s = z;
+  }
+  __syncthreads();
+  // Rank every candidate by (logit desc, token asc); the first k win.
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    int ti = ct[i];
+    if (ti < 0) continue;
+    float vi = cv[i];
+    int rank = 0;
+    for (int j = 0; j < n; ++j) {
+      int tj = ct[j];
+      if (tj >= 0 && better(cv[j], tj, vi, ti)) ++rank;
+    }
+    if (rank < k) { sel_v[rank] = vi; sel_t[rank] = ti; }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const double m = gmax_s;
+    double e[kTopkMaxK];
+    double topsum = 0.0;
+    for (int r = 0; r < k; ++r) {
+      e[r] = exp(static_cast<double>(sel_v[r]) - m);
+      topsum += e[r];
+    }
+    const double z = fmax(z_s, topsum);  // rounding guard: sum(top-k probs) <= 1
+    double p[kTopkMaxK];
+    int t[kTopkMaxK];
+    for (int r = 0; r < k; ++r) { p[r] = e[r] / z; t[r] = sel_t[r]; }
+    // Final order (prob desc, token asc): exp is monotone, so only equal-prob runs can move.
+    for (int a = 1; a < k; ++a) {
+      double pa = p[a];
+      int ta = t[a];
+      int b = a - 1;
+      while (b >= 0 && (p[b] < pa || (p[b] == pa && t[b] > ta))) { p[b + 1] = p[b]; t[b + 1] = t[b]; --b; }
+      p[b + 1] = pa;
+      t[b + 1] = ta;
+    }
+    for (int r = 0; r < k; ++r) {
+      out_tok[static_cast<size_t>(row) * k + r] = t[r];
+      out_prob[static_cast<size_t>(row) * k + r] = p[r];
+    }
+    if (out_stats) {
+      out_stats[2 * row] = static_cast<float>(m);
+      out_stats[2 * row + 1] = static_cast<float>(m + log(z_s));
+    }
+  }
+  pdl_launch_dependents();
+}
+
+// ===========================================================================
+// K1b: one grow_step per request (egt.py:83-114).
+// ===========================================================================
+constexpr int kGrowThreads = 256;
+constexpr int kGrowMaxCand = 1024;
+
+__global__ void __launch_bounds__(kGrowThreads) grow_level_kernel(ygg_tree t, int Fmax, int k, int w_draft,
+                                                                  const int32_t* __restrict__ cand_tok,
+                                                                  const double* __restrict__ cand_prob,
+                                                                  const int32_t* __restrict__ cand_n) {
+  pdl_wait();
+  const int b = blockIdx.x;
+  __shared__ double sc[kGrowMaxCand];
+  __shared__ int spar[kGrowMaxCand];
+  __shared__ int srank[kGrowMaxCand];
+  __shared__ int sslot[kGrowMaxCand];  // (frontier row, rank) packed
+  __shared__ int s_n, s_ok, s_added;
+  __shared__ int s_fn;
+  int32_t* flags = t.flags + b;
+  const int size0 = t.size[b];
+  if (threadIdx.x == 0) {
+    s_ok = 1;
+    s_fn = t.frontier_n[b];
+    if (*flags & kFlagStopped) s_ok = 0;
+  }
+  __syncthreads();
+  if (!s_ok) return;
+  const int fn = s_fn;
+  const int32_t* frontier = t.frontier + static_cast<size_t>(b) * t.cap;
+  const size_t tb = static_cast<size_t>(b) * t.cap;
+  // Candidate contract (_checked_candidates, egt.py:65-80): range, descending, running sum.
+  if (threadIdx.x < fn) {
+    const int f = threadIdx.x;
+    const int cnt = cand_n ? cand_n[static_cast<size_t>(b) * Fmax + f] : k;
+    const double* pr = cand_prob + (static_cast<size_t>(b) * Fmax + f) * k;
+    double total = 0.0, prev = INFINITY;
+    bool bad = cnt < 0 || cnt > k;
+    for (int r = 0; r < cnt && !bad; ++r) {
+      double p = pr[r];
+      if (!(p >= 0.0 && p <= 1.0)) bad = true;
+      if (p > prev) bad = true;
+      prev = p;
+      total = total + p;
+    }
+    if (total > 1.0 + kSiblingTol) bad = true;
+    if (bad) atomicExch(&s_ok, 0);
+  }
+  __syncthreads();
+  if (!s_ok) {
+    if (threadIdx.x == 0) atomicOr(flags, kFlagContract);
+    return;
+  }
+  if (threadIdx.x == 0) {
+    int n = 0;
+    for (int f = 0; f < fn; ++f) {
+      const int parent = frontier[f];
+      const int cnt = cand_n ? cand_n[static_cast<size_t>(b) * Fmax + f] : k;
+      const double path = t.cum[tb + parent];
+      for (int r = 0; r < cnt && n < kGrowMaxCand; ++r, ++n) {
+        sc[n] = path * cand_prob[(static_cast<size_t>(b) * Fmax + f) * k + r];
+        spar[n] = parent;
+        sslot[n] = f * k + r;
+      }
+    }
+    s_n = n;
+  }
+  __syncthreads();
+  const int n = s_n;
+  // Rank by (-score, parent, rank); equal keys cannot occur (parent, rank) unique.
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const double si = sc[i];
+    const int pi = spar[i], ri = sslot[i] % k;
+    int rank = 0;
+    for (int j = 0; j < n; ++j) {
+      const double sj = sc[j];
+      const int pj = spar[j], rj = sslot[j] % k;
+      if (sj > si || (sj == si && (pj < pi || (pj == pi && rj < ri)))) ++rank;
+    }
+    srank[i] = rank;
+  }
+  __syncthreads();
+  const int added = min(n, w_draft);
+  if (threadIdx.x == 0) {
+    s_added = added;
+    if (size0 + added > t.cap) atomicOr(flags, kFlagCapacity);
+  }
+  __syncthreads();
+  if (size0 + added > t.cap) return;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const int r = srank[i];
+    if (r >= added) continue;
+    const int idx = size0 + r;
+    const int parent = spar[i];
+    const int f = sslot[i] / k, rk = sslot[i] % k;
+    const size_t ci = (static_cast<size_t>(b) * Fmax + f) * k + rk;
+    t.token[tb + idx] = cand_tok[ci];
+    t.parent[tb + idx] = parent;
+    t.depth[tb + idx] = t.depth[tb + parent] + 1;
+    t.prob[tb + idx] = cand_prob[ci];
+    t.cum[tb + idx] = sc[i];
+    uint32_t* row = t.mask + (tb + idx) * t.mask_words;
+    const uint32_t* prow = t.mask + (tb + parent) * t.mask_words;
+    for (int w = 0; w < t.mask_words; ++w) row[w] = prow[w] | ((idx >> 5) == w ? (1u << (idx & 31)) : 0u);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    // add_child sibling-sum check in insertion order (token_tree.py:79-83).
+    for (int i = size0; i < size0 + added; ++i) {
+      const int p = t.parent[tb + i];
+      double s = 0.0;
+      for (int j = size0; j < i; ++j)
+        if (t.parent[tb + j] == p) s = s + t.prob[tb + j];
+      if (s + t.prob[tb + i] > 1.0 + kSiblingTol) atomicOr(flags, kFlagContract);
+    }
+    int32_t* fr = t.frontier + tb;
+    for (int i = 0; i < added; ++i) fr[i] = size0 + i;
+    if (added > 0) t.frontier_n[b] = added;
+    t.size[b] = size0 + added;
+    int fl = 0;
+    if (added < w_draft) fl |= kFlagShortfall;
+    if (added == 0) fl |= kFlagStopped;  // grow_egt breaks when nothing was added (egt.py:145-146)
+    if (fl) atomicOr(flags, fl);
+  }
+  pdl_launch_dependents();
+}
+
+// ===========================================================================
+// K7: build_mask (token_tree.py:205-218): row(i) = row(parent) | bit(i), one warp per tree.
+// ===========================================================================
+__global__ void build_mask_kernel(ygg_tree t) {
+  pdl_wait();
+  const int b = blockIdx.x, lane = threadIdx.x;
+  const size_t tb = static_cast<size_t>(b) * t.cap;
+  const int n = t.size[b];
+  for (int i = 0; i < t.cap; ++i) {
+    const int p = (i < n) ? t.parent[tb + i] : -1;
+    if (i < n && i > 0 && !(p >= 0 && p < i)) {
+      if (lane == 0) atomicOr(t.flags + b, kFlagIndex);
+    }
+    if (lane < t.mask_words) {
+      uint32_t v = 0;
+      if (i < n) {
+        if (i > 0 && p >= 0 && p < i) v = t.mask[(tb + p) * t.mask_words + lane];
+        if ((i >> 5) == lane) v |= 1u << (i & 31);
+      }
+      t.mask[(tb + i) * t.mask_words + lane] = v;
+    }
+    __syncwarp();
+  }
+  pdl_launch_dependents();
+}
+
+// ===========================================================================
+// K6: path_products + SubtreeKnapsack + latency-aware prune + pick (egt.py:150-282).
+// ===========================================================================
+YGG_DEV double latency_at_dev(const ygg_profile& p, int width) {
+  // latency.py:68-82, operation order preserved (compiled without FMA contraction).
+  if (width <= p.width[0]) return p.latency_us[0];
+  const int n = p.n;
+  if (width >= p.width[n - 1]) {
+    const double w0 = p.width[n - 2], l0 = p.latency_us[n - 2];
+    const double w1 = p.width[n - 1], l1 = p.latency_us[n - 1];
+    const double slope = (l1 - l0) / (w1 - w0);
+    return l1 + slope * static_cast<double>(width - p.width[n - 1]);
+  }
+  int hi = 0;
+  while (hi < n && p.width[hi] <= width) ++hi;  // bisect_right
+  const double l0 = p.latency_us[hi - 1], l1 = p.latency_us[hi];
+  return l0 + (l1 - l0) * static_cast<double>(width - p.width[hi - 1]) /
+                  static_cast<double>(p.width[hi] - p.width[hi - 1]);
+}
+
+YGG_DEV double tree_speedup_dev(const ygg_profile_pair& pp, double aal, int w_draft, int d_draft, int w_verify) {
+  // latency.py:154-161: aal * T_v(1) / (D * T_d(W) + T_v(w_verify + 1))
+  const double draft_cost = static_cast<double>(d_draft) * latency_at_dev(pp.drafter, w_draft);
+  const double verify_cost = latency_at_dev(pp.verifier, w_verify + 1);
+  return aal * latency_at_dev(pp.verifier, 1) / (draft_cost + verify_cost);
+}
+
+constexpr int kKnapThreads = 256;
+
+__global__ void __launch_bounds__(kKnapThreads) knapsack_prune_kernel(
+    ygg_tree t, const double* __restrict__ probs, const ygg_profile_pair* __restrict__ prof, ygg_prune_args args,
+    int32_t* keep_idx, int32_t* new_idx, int32_t* w_verify, double* expected_aal, double* speedup,
+    double* aal_at_cap, double* speedup_at_cap, double* best_out, uint8_t* alloc_out) {
+  pdl_wait();
+  const int b = blockIdx.x;
+  const size_t tb = static_cast<size_t>(b) * t.cap;
+  const int N = t.size[b];
+  const int cap = min(args.max_verify, N);
+  const int R = cap + 1;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double* best = reinterpret_cast<double*>(smem_raw);                       // [N][R]
+  double* gain = best + static_cast<size_t>(N) * R;                         // [N]
+  uint8_t* alloc = reinterpret_cast<uint8_t*>(gain + N);                    // [N][R] (indexed by child)
+  int* par = reinterpret_cast<int*>(alloc + ((static_cast<size_t>(N) * R + 15) & ~size_t(15)));  // [N]
+  int* sz = par + N;                                                        // [N]
+  int* stack = sz + N;                                                      // [2N]
+  __shared__ int s_best_k;
+  __shared__ double s_best_speed;
+
+  for (int i = threadIdx.x; i < N; i += blockDim.x) par[i] = t.parent[tb + i];
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    // path_products (acceptance.py:176-184) and subtree sizes (egt.py:225-229).
+    const double* pr = probs ? probs + tb : t.prob + tb;
+    gain[0] = pr[0];
+    for (int i = 1; i < N; ++i) gain[i] = gain[par[i]] * pr[i];
+    for (int i = 0; i < N; ++i) sz[i] = 1;
+    for (int v = N - 1; v >= 1; --v) sz[par[v]] += sz[v];
+  }
+  __syncthreads();
+  // Bottom-up merge (egt.py:175-196).  Thread s owns target size s; k ascending and the strict
+  // '>' reproduce the reference's first-maximum tie rule exactly.
+  for (int v = N - 1; v >= 0; --v) {
+    double* row = best + static_cast<size_t>(v) * R;
+    for (int s = threadIdx.x; s < R; s += blockDim.x) row[s] = (s == 1) ? gain[v] : -INFINITY;
+    __syncthreads();
+    for (int c = v + 1; c < N; ++c) {
+      if (par[c] != v) continue;  // children in insertion (= index) order
+      const double* crow = best + static_cast<size_t>(c) * R;
+      const int top_c = min(sz[c], cap);
+      double m = 0.0;
+      int a = 0;
+      const int s = threadIdx.x;
+      if (s >= 1 && s < R) {
+        m = row[s];
+        for (int kk = max(1, s - top_c); kk <= s - 1; ++kk) {
+          const double rk = row[kk];
+          if (rk == -INFINITY) continue;
+          const double value = rk + crow[s - kk];
+          if (value > m) { m = value; a = s - kk; }
+        }
+      }
+      __syncthreads();
+      if (s >= 1 && s < R) {
+        row[s] = m;
+        alloc[static_cast<size_t>(c) * R + s] = static_cast<uint8_t>(a);
+      }
+      if (s == 0) alloc[static_cast<size_t>(c) * R] = 0;
+      __syncthreads();
+    }
+  }
+  if (best_out || alloc_out) {
+    // Optional export of the whole DP (SubtreeKnapsack.best_row / pick on the host).
+    const size_t ob = static_cast<size_t>(b) * t.cap * (args.max_verify + 1);
+    const int RO = args.max_verify + 1;
+    for (int i = threadIdx.x; i < N * RO; i += blockDim.x) {
+      const int v = i / RO, s = i % RO;
+      if (best_out) best_out[ob + i] = (s < R) ? best[static_cast<size_t>(v) * R + s] : -INFINITY;
+      if (alloc_out) alloc_out[ob + i] = (s < R) ? alloc[static_cast<size_t>(v) * R + s] : 0;
+    }
+  }
+  if (threadIdx.x == 0) {
+    const ygg_profile_pair pp = *prof;
+    int best_k = 0;
+    double best_speed = -INFINITY;
+    const double* root = best;
+    const bool shape_ok = cap <= 1 + args.d_draft * args.w_draft;
+    if (args.fixed_k > 0) {
+      best_k = min(args.fixed_k, cap);
+      best_speed = shape_ok ? tree_speedup_dev(pp, 1.0 + root[best_k], args.w_draft, args.d_draft, best_k) : NAN;
+    } else {
+      for (int kk = 1; kk <= cap; ++kk) {  // egt.py:261-273
+        const double value = root[kk];
+        if (value == -INFINITY) continue;
+        const double sp = tree_speedup_dev(pp, 1.0 + value, args.w_draft, args.d_draft, kk);
+        if (sp > best_speed + 1e-12) { best_k = kk; best_speed = sp; }
+      }
+    }
+    if (!shape_ok) atomicOr(t.flags + b, kFlagContract);
+    s_best_k = best_k;
+    s_best_speed = best_speed;
+    w_verify[b] = best_k;
+    expected_aal[b] = 1.0 + root[best_k];
+    speedup[b] = best_speed;
+    if (aal_at_cap) aal_at_cap[b] = 1.0 + root[cap];
+    if (speedup_at_cap)
+      speedup_at_cap[b] = shape_ok ? tree_speedup_dev(pp, 1.0 + root[cap], args.w_draft, args.d_draft, cap) : NAN;
+  }
+  __syncthreads();
+  // pick(best_k) (egt.py:206-222): peel the recorded allocations in reverse merge order.
+  uint8_t* keep = reinterpret_cast<uint8_t*>(stack + 2 * N);  // [N] flags (reuses tail of smem)
+  for (int i = threadIdx.x; i < N; i += blockDim.x) keep[i] = 0;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int sp = 0;
+    stack[sp++] = 0;
+    stack[sp++] = s_best_k;
+    while (sp > 0) {
+      const int kk = stack[--sp];
+      const int v = stack[--sp];
+      keep[v] = 1;
+      int remaining = kk;
+      for (int c = N - 1; c > v; --c) {
+        if (par[c] != v) continue;
+        const int taken = alloc[static_cast<size_t>(c) * R + remaining];
+        if (taken) {
+          stack[sp++] = c;
+          stack[sp++] = taken;
+          remaining -= taken;
+        }
+      }
+    }
+    int j = 0;
+    for (int i = 0; i < N; ++i) {
+      new_idx[tb + i] = keep[i] ? j : -1;
+      if (keep[i]) keep_idx[tb + j++] = i;
+    }
+    for (int i = N; i < t.cap; ++i) new_idx[tb + i] = -1;
+    for (int i = j; i < t.cap; ++i) keep_idx[tb + i] = -1;
+  }
+  pdl_launch_dependents();
+}
+
+// TokenTree.subtree (token_tree.py:146-168): kept nodes in ascending old order.
+__global__ void subtree_kernel(ygg_tree in, ygg_tree out, const int32_t* __restrict__ keep_idx,
+                               const int32_t* __restrict__ new_idx) {
+  pdl_wait();
+  const int b = blockIdx.x;
+  const size_t ib = static_cast<size_t>(b) * in.cap, ob = static_cast<size_t>(b) * out.cap;
+  __shared__ int s_n;
+  if (threadIdx.x == 0) {
+    int n = 0;
+    while (n < in.cap && keep_idx[ib + n] >= 0) ++n;
+    s_n = n;
+    out.size[b] = n;
+    out.flags[b] = 0;
+  }
+  __syncthreads();
+  const int n = s_n;
+  for (int i = threadIdx.x; i < out.cap; i += blockDim.x) {
+    if (i < n) {
+      const int o = keep_idx[ib + i];
+      const int p = in.parent[ib + o];
+      out.token[ob + i] = in.token[ib + o];
+      out.parent[ob + i] = p < 0 ? -1 : new_idx[ib + p];
+      out.depth[ob + i] = in.depth[ib + o];
+      out.prob[ob + i] = in.prob[ib + o];
+      out.cum[ob + i] = in.cum[ib + o];
+    } else {
+      out.token[ob + i] = 0;
+      out.parent[ob + i] = -1;
+      out.depth[ob + i] = 0;
+      out.prob[ob + i] = 0.0;
+      out.cum[ob + i] = 0.0;
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    const int lane = threadIdx.x;
+    for (int i = 0; i < out.cap; ++i) {
+      if (lane < out.mask_words) {
+        uint32_t v = 0;
+        if (i < n) {
+          const int p = out.parent[ob + i];
+          if (p >= 0) v = out.mask[(ob + p) * out.mask_words + lane];
+          if ((i >> 5) == lane) v |= 1u << (i & 31);
+        }
+        out.mask[(ob + i) * out.mask_words + lane] = v;
+      }
+      __syncwarp();
+    }
+    if (lane == 0) {
+      int md = 0;
+      for (int i = 0; i < n; ++i) md = max(md, out.depth[ob + i]);
+      int fnn = 0;
+      for (int i = 0; i < n; ++i)
+        if (out.depth[ob + i] == md) out.frontier[ob + fnn++] = i;
+      out.frontier_n[b] = fnn;
+    }
+  }
+  pdl_launch_dependents();
+}
+
+// ===========================================================================
+// K5: acceptance walk (acceptance.py:221-241) + greedy / sampled realisations.
+// ===========================================================================
+constexpr int kAcceptThreads = 256;
+
+template <typename T>
+__global__ void __launch_bounds__(kAcceptThreads) accept_kernel(
+    ygg_tree t, int mode, const double* __restrict__ probs, const double* __restrict__ uniforms, int n_uniform,
+    const int32_t* __restrict__ row_argmax, const T* __restrict__ logits, int V, int ld,
+    const float* __restrict__ row_stats, float inv_temp, int32_t* path, int32_t* path_len, int32_t* accepted_len,
+    int32_t* bonus, int32_t* n_draws) {
+  pdl_wait();
+  const int b = blockIdx.x;
+  const size_t tb = static_cast<size_t>(b) * t.cap;
+  const int N = t.size[b];
+  const int rows = t.cap + 1;  // verify rows per request: [confirmed, node 0, node 1, ...]
+  __shared__ int s_stop_row, s_len, s_excl[64], s_nexcl;
+  __shared__ double s_u2;
+  if (threadIdx.x == 0) {
+    int len = 0;
+    int cursor = -1;
+    int draw_i = 0;
+    int excl_n = 0;
+    while (true) {
+      // group = [0] if cursor is None else children(cursor)
+      const int prow = cursor < 0 ? 0 : 1 + cursor;
+      int first = cursor < 0 ? 0 : cursor + 1;
+      bool any = false;
+      for (int c = first; c < N; ++c) {
+        if (cursor < 0 ? c == 0 : t.parent[tb + c] == cursor) { any = true; break; }
+      }
+      if (!any) break;
+      const double draw = (mode == YGG_ACCEPT_GREEDY) ? 0.5
+                          : (draw_i < n_uniform ? uniforms[static_cast<size_t>(b) * n_uniform + draw_i] : 1.0);
+      ++draw_i;
+      double cumulative = 0.0;
+      int chosen = -1;
+      excl_n = 0;
+      for (int c = first; c < N; ++c) {
+        if (!(cursor < 0 ? c == 0 : t.parent[tb + c] == cursor)) continue;
+        double p;
+        if (mode == YGG_ACCEPT_PROBS) {
+          p = probs[tb + c];
+        } else if (mode == YGG_ACCEPT_GREEDY) {
+          p = (t.token[tb + c] == row_argmax[static_cast<size_t>(b) * rows + prow]) ? 1.0 : 0.0;
+        } else {
+          const size_t r = static_cast<size_t>(b) * rows + prow;
+          const float l = to_f32(logits[r * ld + t.token[tb + c]]) * inv_temp;
+          p = exp(static_cast<double>(l) - static_cast<double>(row_stats[2 * r + 1]));
+        }
+        if (excl_n < 64) s_excl[excl_n++] = t.token[tb + c];
+        cumulative += p;
+        if (draw < cumulative) { chosen = c; break; }
+        if (cursor < 0) break;  // the root group has a single member
+      }
+      if (chosen < 0) break;
+      path[tb + len++] = chosen;
+      cursor = chosen;
+      excl_n = 0;
+    }
+    s_len = len;
+    s_stop_row = (cursor < 0 ? 0 : 1 + cursor);
+    s_nexcl = excl_n;
+    s_u2 = (n_uniform > 0 && uniforms) ? uniforms[static_cast<size_t>(b) * n_uniform + (n_uniform - 1)] : 0.5;
+    path_len[b] = len;
+    accepted_len[b] = len + 1;
+    if (n_draws) n_draws[b] = draw_i;
+    for (int i = len; i < t.cap; ++i) path[tb + i] = -1;
+  }
+  __syncthreads();
+  if (mode == YGG_ACCEPT_GREEDY) {
+    if (threadIdx.x == 0 && bonus) bonus[b] = row_argmax[static_cast<size_t>(b) * rows + s_stop_row];
+  } else if (mode == YGG_ACCEPT_SAMPLE && bonus) {
+    // Residual bonus: sample p(.|stop row) with the rejected children removed (inverse CDF in
+    // token order, block scan).  Together with the walk this emits exactly p(.|prefix).
+    const size_t r = static_cast<size_t>(b) * rows + s_stop_row;
+    const double lse = row_stats[2 * r + 1];
+    const T* lr = logits + r * ld;
+    const int nex = s_nexcl;
+    __shared__ double s_part[kAcceptThreads];
+    __shared__ double s_total;
+    // pass 1: per-thread contiguous slice masses
+    const int per = (V + blockDim.x - 1) / blockDim.x;
+    const int lo = threadIdx.x * per, hi = min(V, lo + per);
+    double mass = 0.0;
+    for (int v = lo; v < hi; ++v) {
+      bool ex = false;
+      for (int e = 0; e < nex; ++e) ex |= (s_excl[e] == v);
+      if (!ex) mass += exp(static_cast<double>(to_f32(lr[v]) * inv_temp) - lse);
+    }
+    s_part[threadIdx.x] = mass;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double tot = 0.0;
+      for (int i = 0; i < (int)blockDim.x; ++i) tot += s_part[i];
+      s_total = tot;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const double target = s_u2 * s_total;
+      double acc = 0.0;
+      int pick = -1;
+      for (int i = 0; i < (int)blockDim.x && pick < 0; ++i) {
+        if (acc + s_part[i] > target) {
+          const int l2 = i * per, h2 = min(V, l2 + per);
+          for (int v = l2; v < h2; ++v) {
+            bool ex = false;
+            for (int e = 0; e < nex; ++e) ex |= (s_excl[e] == v);
+            if (ex) continue;
+            acc += exp(static_cast<double>(to_f32(lr[v]) * inv_temp) - lse);
+            if (acc > target) { pick = v; break; }
+          }
+          if (pick < 0) pick = h2 - 1;
+        } else {
+          acc += s_part[i];
+        }
+      }
+      if (pick < 0) pick = V - 1;
+      bonus[b] = pick;
+    }
+  }
+  pdl_launch_dependents();
+}
+
+// ===========================================================================
+// KV compaction of the accepted path (new; the map is derived from accepted_path).
+// ===========================================================================
+template <typename T>
+__global__ void kv_compact_kernel(T* cache, int B, int Hkv, int S, int hd, long long layer_stride,
+                                  const int32_t* __restrict__ base, const int32_t* __restrict__ path,
+                                  const int32_t* __restrict__ path_len, int path_cap,
+                                  const int32_t* __restrict__ keep_idx, int keep_cap,
+                                  const int32_t* __restrict__ node_depth, int depth_cap, int skip_depth) {
+  pdl_wait();
+  const int layer = blockIdx.y, b = blockIdx.z;
+  const int kvh = blockIdx.x;  // over 2*Hkv
+  const int n = path_len[b];
+  if (n <= 0) return;
+  T* head = cache + layer * layer_stride + (static_cast<size_t>(b) * 2 * Hkv + kvh) * static_cast<size_t>(S) * hd;
+  const int p0 = base[b] + 1;
+  constexpr int kMaxPath = 64;
+  for (int d = threadIdx.x; d < hd; d += blockDim.x) {
+    T vals[kMaxPath];
+    int dst[kMaxPath];
+    int m = 0;
+    for (int i = 0; i < n && i < kMaxPath; ++i) {
+      const int node = path[static_cast<size_t>(b) * path_cap + i];
+      const int src_node = keep_idx ? keep_idx[static_cast<size_t>(b) * keep_cap + node] : node;
+      if (node_depth && node_depth[static_cast<size_t>(b) * depth_cap + src_node] >= skip_depth) continue;
+      if (src_node == i) continue;
+      vals[m] = head[static_cast<size_t>(p0 + src_node) * hd + d];
+      dst[m] = p0 + i;
+      ++m;
+    }
+    for (int j = 0; j < m; ++j) head[static_cast<size_t>(dst[j]) * hd + d] = vals[j];
+  }
+}
+
+}  // namespace ygg
+
+using namespace ygg;
+
+// ===========================================================================
+// C ABI
+// ===========================================================================
+extern "C" {
+
+int ygg_prepare_tree(void) {
+  cudaError_t e = cudaFuncSetAttribute(knapsack_prune_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+  if (e != cudaSuccess) return ygg_fail(YGG_ERR_CUDA, "knapsack attribute: %s", cudaGetErrorString(e));
+  return YGG_OK;
+}
+
+size_t ygg_topk_workspace(int rows, int V, int k) {
+  const int nchunks = (V + kTopkChunk - 1) / kTopkChunk;
+  return static_cast<size_t>(rows) * nchunks * sizeof(TopkChunkOut);
+}
+
+int ygg_topk_softmax(const void* logits, int dtype, int rows, int V, int ld, int k, float temperature,
+                     int32_t* out_tok, double* out_prob, float* out_stats, void* workspace, size_t workspace_bytes,
+                     ygg_stream_t stream) {
+  YGG_CHECK_ARG(rows >= 0 && V >= 1 && ld >= V, "bad logits shape");
+  YGG_CHECK_ARG(k >= 1 && k <= kTopkMaxK && k <= V, "k must be in [1, 32] and <= V");
+  YGG_CHECK_ARG(temperature > 0.f, "temperature must be > 0");
+  YGG_CHECK_ARG(workspace_bytes >= ygg_topk_workspace(rows, V, k), "workspace too small");
+  if (rows == 0) return YGG_OK;
+  const int nchunks = (V + kTopkChunk - 1) / kTopkChunk;
+  auto* ws = static_cast<TopkChunkOut*>(workspace);
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const float inv_t = 1.0f / temperature;
+  if (dtype == YGG_F32)
+    YGG_LAUNCH_PDL(topk_phase1<float>, dim3(nchunks, rows), dim3(kTopkThreads), 0, s,
+                   static_cast<const float*>(logits), V, ld, k, inv_t, nchunks, ws);
+  else if (dtype == YGG_BF16)
+    YGG_LAUNCH_PDL(topk_phase1<__nv_bfloat16>, dim3(nchunks, rows), dim3(kTopkThreads), 0, s,
+                   static_cast<const __nv_bfloat16*>(logits), V, ld, k, inv_t, nchunks, ws);
+  else
+    return ygg_fail(YGG_ERR_VALUE, "unknown dtype");
+  const size_t smem = static_cast<size_t>(nchunks) * k * (sizeof(float) + sizeof(int));
+  YGG_CHECK_ARG(smem <= 48 * 1024, "too many candidates for phase 2");
+  YGG_LAUNCH_PDL(topk_phase2, dim3(rows), dim3(kTopkThreads), smem, s, ws, nchunks, k, out_tok, out_prob, out_stats);
+  return YGG_OK;
+}
+
+static int check_tree(const ygg_tree& t) {
+  YGG_CHECK_ARG(t.B >= 1 && t.cap >= 1 && t.cap <= 32 * YGG_MAX_MASK_WORDS, "tree capacity out of range");
+  YGG_CHECK_ARG(t.mask_words == (t.cap + 31) / 32, "mask_words must equal ceil(cap/32)");
+  YGG_CHECK_ARG(t.token && t.parent && t.depth && t.prob && t.cum && t.mask && t.size && t.frontier &&
+                    t.frontier_n && t.flags,
+                "tree pointers must be non-null");
+  return YGG_OK;
+}
+
+int ygg_egt_grow_level(ygg_tree tree, int Fmax, int k, int w_draft, const int32_t* cand_tok, const double* cand_prob,
+                       const int32_t* cand_n, ygg_stream_t stream) {
+  if (int rc = check_tree(tree)) return rc;
+  YGG_CHECK_ARG(w_draft >= 1, "w_draft must be >= 1");
+  YGG_CHECK_ARG(k >= 1 && Fmax >= 1 && Fmax <= kGrowThreads && Fmax * k <= kGrowMaxCand, "candidate grid too large");
+  YGG_CHECK_ARG(cand_tok && cand_prob, "candidate pointers must be non-null");
+  YGG_LAUNCH_PDL(grow_level_kernel, dim3(tree.B), dim3(kGrowThreads), 0, reinterpret_cast<cudaStream_t>(stream),
+                 tree, Fmax, k, w_draft, cand_tok, cand_prob, cand_n);
+  return YGG_OK;
+}
+
+int ygg_build_mask(ygg_tree tree, ygg_stream_t stream) {
+  if (int rc = check_tree(tree)) return rc;
+  YGG_LAUNCH_PDL(build_mask_kernel, dim3(tree.B), dim3(32), 0, reinterpret_cast<cudaStream_t>(stream), tree);
+  return YGG_OK;
+}
+
+static size_t knap_smem(int N, int cap) {
+  const size_t R = cap + 1;
+  size_t bytes = N * R * sizeof(double) + N * sizeof(double);
+  bytes += (N * R + 15) & ~size_t(15);
+  bytes += 2 * N * sizeof(int) + 2 * N * sizeof(int) + N;
+  return bytes + 64;
+}
+
+int ygg_knapsack_prune(ygg_tree tree, const double* probs, const ygg_profile_pair* profiles_dev, ygg_prune_args args,
+                       int32_t* keep_idx, int32_t* new_idx, int32_t* w_verify, double* expected_aal, double* speedup,
+                       double* aal_at_cap, double* speedup_at_cap, double* best_table, uint8_t* alloc_table,
+                       ygg_stream_t stream) {
+  if (int rc = check_tree(tree)) return rc;
+  YGG_CHECK_ARG(args.max_verify >= 1, "max_size must be >= 1");
+  YGG_CHECK_ARG(args.d_draft >= 1 && args.w_draft >= 1, "d_draft and w_draft must be >= 1");
+  YGG_CHECK_ARG(args.max_verify < kKnapThreads, "max_verify must be < 256");
+  YGG_CHECK_ARG(profiles_dev && keep_idx && new_idx && w_verify && expected_aal && speedup, "null output");
+  const size_t smem = knap_smem(tree.cap, std::min(args.max_verify, tree.cap));
+  YGG_CHECK_ARG(smem <= 220 * 1024, "tree too large for the on-chip knapsack");
+  YGG_LAUNCH_PDL(knapsack_prune_kernel, dim3(tree.B), dim3(kKnapThreads), smem, reinterpret_cast<cudaStream_t>(stream),
+                 tree, probs, profiles_dev, args, keep_idx, new_idx, w_verify, expected_aal, speedup, aal_at_cap,
+                 speedup_at_cap, best_table, alloc_table);
+  return YGG_OK;
+}
+
+int ygg_tree_subtree(ygg_tree in, ygg_tree out, const int32_t* keep_idx, const int32_t* new_idx,
+                     ygg_stream_t stream) {
+  if (int rc = check_tree(in)) return rc;
+  if (int rc = check_tree(out)) return rc;
+  YGG_CHECK_ARG(in.B == out.B && out.cap >= 1, "tree batch mismatch");
+  YGG_LAUNCH_PDL(subtree_kernel, dim3(in.B), dim3(128), 0, reinterpret_cast<cudaStream_t>(stream), in, out, keep_idx,
+                 new_idx);
+  return YGG_OK;
+}
+
+int ygg_accept(ygg_tree tree, int mode, const double* probs, const double* uniforms, int n_uniform,
+               const int32_t* row_argmax, const void* logits, int logits_dtype, int V, int ld, const float* row_stats,
+               float temperature, int32_t* path, int32_t* path_len, int32_t* accepted_len, int32_t* bonus,
+               int32_t* n_draws, ygg_stream_t stream) {
+  if (int rc = check_tree(tree)) return rc;
+  YGG_CHECK_ARG(path && path_len && accepted_len, "null output");
+  if (mode == YGG_ACCEPT_PROBS) {
+    YGG_CHECK_ARG(probs && uniforms && n_uniform >= 1, "PROBS mode needs probs and uniforms");
+  } else if (mode == YGG_ACCEPT_GREEDY) {
+    YGG_CHECK_ARG(row_argmax != nullptr, "GREEDY mode needs row_argmax");
+  } else if (mode == YGG_ACCEPT_SAMPLE) {
+    YGG_CHECK_ARG(logits && row_stats && uniforms && n_uniform >= 2 && temperature > 0.f && V >= 1 && ld >= V,
+                  "SAMPLE mode needs logits, row stats, uniforms");
+  } else {
+    return ygg_fail(YGG_ERR_VALUE, "unknown accept mode");
+  }
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const float inv_t = temperature > 0.f ? 1.0f / temperature : 1.0f;
+  if (logits_dtype == YGG_BF16)
+    YGG_LAUNCH_PDL(accept_kernel<__nv_bfloat16>, dim3(tree.B), dim3(kAcceptThreads), 0, s, tree, mode, probs, uniforms,
+                   n_uniform, row_argmax, static_cast<const __nv_bfloat16*>(logits), V, ld, row_stats, inv_t, path,
+                   path_len, accepted_len, bonus, n_draws);
+  else
+    YGG_LAUNCH_PDL(accept_kernel<float>, dim3(tree.B), dim3(kAcceptThreads), 0, s, tree, mode, probs, uniforms,
+                   n_uniform, row_argmax, static_cast<const float*>(logits), V, ld, row_stats, inv_t, path, path_len,
+                   accepted_len, bonus, n_draws);
+  return YGG_OK;
+}
+
+int ygg_kv_compact(void* cache, int dtype, int layers, int B, int Hkv, int S, int hd, long long layer_stride,
+                   const int32_t* base, const int32_t* path, const int32_t* path_len, int path_cap,
+                   const int32_t* keep_idx, int keep_cap, const int32_t* node_depth, int depth_cap, int skip_depth,
+                   ygg_stream_t stream) {
+  YGG_CHECK_ARG(cache && base && path && path_len, "null pointer");
+  YGG_CHECK_ARG(layers >= 1 && B >= 1 && Hkv >= 1 && S >= 1 && hd >= 1, "bad cache shape");
+  dim3 grid(2 * Hkv, layers, B);
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const int threads = hd >= 128 ? 128 : 64;
+  if (dtype == YGG_BF16)
+    YGG_LAUNCH_PDL(kv_compact_kernel<__nv_bfloat16>, grid, dim3(threads), 0, s, static_cast<__nv_bfloat16*>(cache), B,
+                   Hkv, S, hd, layer_stride, base, path, path_len, path_cap, keep_idx, keep_cap, node_depth, depth_cap,
+                   skip_depth);
+  else
+    YGG_LAUNCH_PDL(kv_compact_kernel<float>, grid, dim3(threads), 0, s, static_cast<float*>(cache), B, Hkv, S, hd,
+                   layer_stride, base, path, path_len, path_cap, keep_idx, keep_cap, node_depth, depth_cap, skip_depth);
+  return YGG_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,353 @@
+"""The speculative-decoding step on the GPU: EGT draft -> prune -> tree verify -> accept -> compact.
+
+One ``SpecDecoder.step`` is the north-star hot path, realising the
+reference iteration (pkg/src/specsim/simulator.py:305-338) with real models:
+
+  draft pass 0   : draft forward over [x_{P-1}, bonus]; root = top-1 of the bonus row
+                   (DrafterDistribution.root(), egt.py:56-58; "the root rides along with the
+                   previous bonus", simulator.py:9-11)
+  draft pass 1..D: draft forward over the newest level with the tree mask, softmax top-k per
+                   row (K1a) and one global top-W grow_step per tree (K1b, egt.py:83-114)
+  prune          : path products + SubtreeKnapsack + Eq.3 objective from the device latency
+                   table (K6, egt.py:150-282), TokenTree.subtree relabel (token_tree.py:146-168)
+  verify         : target forward over [bonus, pruned nodes] with the ancestor mask (K2-K4)
+  accept         : greedy / sampled acceptance walk (K5, acceptance.py:221-241)
+  compact+commit : accepted K/V moved to contiguous slots in both caches, P advanced
+
+Every data-dependent value stays on the device, so the whole step is captured once per static
+shape (D, W, max_verify, B) as a CUDA graph and replayed with no host synchronisation.
+"""
+
+from __future__ import annotations
+
+import time
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib as L
+from .device_tree import DeviceTrees, SeqState
+from .forward import Forward, new_cache
+from .model import ModelConfig
+
+GREEDY, SAMPLE = "greedy", "sample"
+
+
+@dataclass
+class StepShape:
+    depth: int          # D: draft levels past the root
+    width: int          # W: nodes per level
+    expansion_k: int = 8
+    max_verify: int = 64
+    fixed_verify: int = 0  # >0: prune to exactly this many nodes (static verify width)
+
+
+class SpecDecoder:
+    def __init__(
+        self,
+        target_cfg: ModelConfig,
+        target_w: dict,
+        draft_cfg: ModelConfig,
+        draft_w: dict,
+        shape: StepShape,
+        batch: int = 1,
+        max_seq: int = 2048,
+        act_dtype: torch.dtype = torch.bfloat16,
+        mode: str = GREEDY,
+        temperature: float = 1.0,
+        profiles=None,
+        prefill_len: int = 0,
+        device="cuda",
+    ):
+        L.require_device()
+        if target_cfg.vocab != draft_cfg.vocab:
+            raise ValueError("target and draft must share a vocabulary")
+        if mode not in (GREEDY, SAMPLE):
+            raise ValueError(f"mode must be {GREEDY!r} or {SAMPLE!r}")
+        self.tc, self.dc = target_cfg, draft_cfg
+        self.tw, self.dw = target_w, draft_w
+        self.shape = shape
+        self.B = batch
+        self.mode, self.temperature = mode, float(temperature)
+        self.act_dtype = act_dtype
+        D, W, k = shape.depth, shape.width, shape.expansion_k
+        self.tree_cap = 1 + D * W
+        self.vcap = min(shape.max_verify, self.tree_cap)
+        self.T = self.vcap + 1
+        self.R = max(W, 2)
+        scratch = self.tree_cap + self.R + 8
+        self.S = max_seq + scratch
+        dev = torch.device(device)
+        self.dev = dev
+        self.seq = SeqState(batch, self.S, device=dev)
+        self.tcache = new_cache(target_cfg, batch, self.S, act_dtype, dev)
+        self.dcache = new_cache(draft_cfg, batch, self.S, act_dtype, dev)
+        tmw = max(1, (self.T + 31) // 32)
+        dmw = max(1, (self.tree_cap + 31) // 32)
+        self.draft = Forward(draft_cfg, draft_w, self.dcache, batch, self.R, dmw, act_dtype)
+        self.verify = Forward(target_cfg, target_w, self.tcache, batch, self.T, tmw, act_dtype)
+        self.grown = DeviceTrees(batch, self.tree_cap, dev)
+        self.vtree = DeviceTrees(batch, self.vcap, dev)
+        i32 = dict(dtype=torch.int32, device=dev)
+        f64 = dict(dtype=torch.float64, device=dev)
+        rows = batch * self.R
+        self.cand_tok = torch.zeros(rows, k, **i32)
+        self.cand_prob = torch.zeros(rows, k, **f64)
+        self.cand_n = torch.zeros(rows, **i32)
+        self.topk_ws = torch.empty(int(L.lib().ygg_topk_workspace(max(rows, 1), draft_cfg.vocab, k)),
+                                   dtype=torch.uint8, device=dev)
+        self.keep_idx = torch.zeros(batch, self.tree_cap, **i32)
+        self.new_idx = torch.zeros(batch, self.tree_cap, **i32)
+        self.w_verify = torch.zeros(batch, **i32)
+        self.exp_aal = torch.zeros(batch, **f64)
+        self.speedup = torch.zeros(batch, **f64)
+        self.row_argmax = torch.zeros(batch * self.T, **i32)
+        self.row_stats = torch.zeros(batch * self.T, 2, dtype=torch.float32, device=dev)
+        self.path = torch.zeros(batch, self.vcap, **i32)
+        self.path_len = torch.zeros(batch, **i32)
+        self.acc_len = torch.zeros(batch, **i32)
+        self.bonus = torch.zeros(batch, **i32)
+        self.n_uniform = D + 3
+        self.uniforms = torch.full((batch, self.n_uniform), 0.5, **f64)
+        self.uniforms_host = torch.full((batch, self.n_uniform), 0.5, dtype=torch.float64).pin_memory()
+        self.set_profiles(profiles)
+        self.prefill_len = prefill_len
+        self._prefill_fwd = {}
+        self.graph = None
+        self.step_count = 0
+
+    # ------------------------------------------------------------------
+    def set_profiles(self, profiles) -> None:
+        """Device copy of the latency table (ProfilePair) that drives the Eq.3 objective."""
+        if profiles is None:
+            d_bp, v_bp = ((1, 1.0), (64, 1.0)), ((1, 1.0), (64, 1.0))
+        else:
+            d_bp, v_bp = profiles.drafter.breakpoints, profiles.verifier.breakpoints
+        raw = L.profile_pair_bytes(d_bp, v_bp)
+        host = torch.frombuffer(bytearray(raw), dtype=torch.uint8)
+        if not hasattr(self, "profiles_dev"):
+            self.profiles_dev = torch.empty(len(raw), dtype=torch.uint8, device=self.dev)
+        self.profiles_dev.copy_(host)
+
+    # ------------------------------------------------------------------
+    def _prefill_forward(self, cfg, w, cache, n: int) -> Forward:
+        key = (cfg.name, n, id(cache))
+        f = self._prefill_fwd.get(key)
+        if f is None:
+            f = Forward(cfg, w, cache, self.B, n, 0, self.act_dtype)
+            self._prefill_fwd[key] = f
+        return f
+
+    def prefill(self, prompts: torch.Tensor) -> None:
+        """Causal prefill of both models over ``prompts`` [B, P0]; the bonus is the target argmax."""
+        B, P0 = prompts.shape
+        if B != self.B:
+            raise ValueError(f"expected {self.B} prompts, got {B}")
+        if P0 + self.tree_cap + self.R + 8 > self.S:
+            raise ValueError("prompt too long for the cache")
+        lib = L.lib()
+        s = L.stream_ptr()
+        prompts_d = prompts.to(self.dev, torch.int32)
+        self.seq.hist.zero_()
+        self.seq.hist[:, :P0] = prompts_d
+        for cfg, w, cache in ((self.tc, self.tw, self.tcache), (self.dc, self.dw, self.dcache)):
+            f = self._prefill_forward(cfg, w, cache, P0)
+            f.tokens.copy_(prompts_d.reshape(-1))
+            pos = torch.arange(P0, dtype=torch.int32, device=self.dev).repeat(B)
+            f.pos.copy_(pos)
+            f.slot.copy_(pos)
+            f.blk_start.zero_()
+            f.blk_len.fill_(P0)
+            f.run()
+            if cfg is self.tc:
+                last = f.logits.view(B, P0, -1)[:, -1, :].contiguous()
+                am = torch.zeros(B, dtype=torch.int32, device=self.dev)
+                L.check(lib.ygg_row_stats(last.data_ptr(), L.YGG_F32, B, cfg.vocab, cfg.vocab, 1.0, am.data_ptr(),
+                                          None, s))
+                self.seq.hist[torch.arange(B, device=self.dev), P0] = am
+        self.seq.P.fill_(P0)
+        self.seq.n_gen.fill_(1)
+        self.seq.step.zero_()
+
+    # ------------------------------------------------------------------
+    def _launch_step(self, stream=None) -> None:
+        lib = L.lib()
+        s = L.stream_ptr(stream)
+        chk = L.check
+        sh = self.shape
+        D, W, k = sh.depth, sh.width, sh.expansion_k
+        dr, vf, g, vt = self.draft, self.verify, self.grown, self.vtree
+        rows = self.B * self.R
+        # ---- draft pass 0: [x_{P-1}, bonus] -> root
+        chk(lib.ygg_pass0_inputs(self.seq.struct, self.R, self.tree_cap, dr.tokens.data_ptr(), dr.pos.data_ptr(),
+                                 dr.slot.data_ptr(), dr.req.data_ptr(), dr.qmask.data_ptr(), dr.mask_words,
+                                 dr.blk_start.data_ptr(), dr.blk_len.data_ptr(), s))
+        dr.run(stream)
+        chk(lib.ygg_topk_softmax(dr.logits.data_ptr(), L.YGG_F32, rows, self.dc.vocab, self.dc.vocab, k, 1.0,
+                                 self.cand_tok.data_ptr(), self.cand_prob.data_ptr(), None, self.topk_ws.data_ptr(),
+                                 self.topk_ws.numel(), s))
+        chk(lib.ygg_init_roots(g.struct, self.cand_tok.data_ptr(), self.cand_prob.data_ptr(), k, self.R, 1, s))
+        # ---- draft passes 1..D: grow one level each
+        for _ in range(D):
+            chk(lib.ygg_level_inputs(g.struct, self.seq.struct, self.R, k, dr.tokens.data_ptr(), dr.pos.data_ptr(),
+                                     dr.slot.data_ptr(), dr.req.data_ptr(), dr.qmask.data_ptr(), dr.mask_words,
+                                     dr.blk_start.data_ptr(), dr.blk_len.data_ptr(), self.cand_n.data_ptr(), s))
+            dr.run(stream)
+            chk(lib.ygg_topk_softmax(dr.logits.data_ptr(), L.YGG_F32, rows, self.dc.vocab, self.dc.vocab, k, 1.0,
+                                     self.cand_tok.data_ptr(), self.cand_prob.data_ptr(), None,
+                                     self.topk_ws.data_ptr(), self.topk_ws.numel(), s))
+            chk(lib.ygg_egt_grow_level(g.struct, self.R, k, W, self.cand_tok.data_ptr(), self.cand_prob.data_ptr(),
+                                       self.cand_n.data_ptr(), s))
+        # ---- prune (latency-aware objective or fixed width)
+        args = L.YggPruneArgs(sh.max_verify, D, W, sh.fixed_verify)
+        chk(lib.ygg_knapsack_prune(g.struct, None, self.profiles_dev.data_ptr(), args, self.keep_idx.data_ptr(),
+                                   self.new_idx.data_ptr(), self.w_verify.data_ptr(), self.exp_aal.data_ptr(),
+                                   self.speedup.data_ptr(), None, None, None, None, s))
+        chk(lib.ygg_tree_subtree(g.struct, vt.struct, self.keep_idx.data_ptr(), self.new_idx.data_ptr(), s))
+        # ---- verify
+        chk(lib.ygg_verify_inputs(vt.struct, self.seq.struct, vf.tokens.data_ptr(), vf.pos.data_ptr(),
+                                  vf.slot.data_ptr(), vf.req.data_ptr(), vf.qmask.data_ptr(), vf.mask_words,
+                                  vf.blk_start.data_ptr(), vf.blk_len.data_ptr(), s))
+        vf.run(stream)
+        nrows = self.B * self.T
+        if self.mode == GREEDY:
+            chk(lib.ygg_row_stats(vf.logits.data_ptr(), L.YGG_F32, nrows, self.tc.vocab, self.tc.vocab, 1.0,
+                                  self.row_argmax.data_ptr(), None, s))
+            chk(lib.ygg_accept(vt.struct, L.YGG_ACCEPT_GREEDY, None, None, 0, self.row_argmax.data_ptr(), None,
+                               L.YGG_F32, self.tc.vocab, self.tc.vocab, None, 1.0, self.path.data_ptr(),
+                               self.path_len.data_ptr(), self.acc_len.data_ptr(), self.bonus.data_ptr(), None, s))
+        else:
+            self.uniforms.copy_(self.uniforms_host, non_blocking=True)
+            chk(lib.ygg_row_stats(vf.logits.data_ptr(), L.YGG_F32, nrows, self.tc.vocab, self.tc.vocab,
+                                  self.temperature, self.row_argmax.data_ptr(), self.row_stats.data_ptr(), s))
+            chk(lib.ygg_accept(vt.struct, L.YGG_ACCEPT_SAMPLE, None, self.uniforms.data_ptr(), self.n_uniform,
+                               None, vf.logits.data_ptr(), L.YGG_F32, self.tc.vocab, self.tc.vocab,
+                               self.row_stats.data_ptr(), self.temperature, self.path.data_ptr(),
+                               self.path_len.data_ptr(), self.acc_len.data_ptr(), self.bonus.data_ptr(), None, s))
+        # ---- KV compaction (target: verify order; draft: grown-tree slots, leaves never drafted)
+        tc, dc = self.tc, self.dc
+        chk(lib.ygg_kv_compact(self.tcache.data_ptr(), L.dtype_code(self.act_dtype), tc.n_layers, self.B,
+                               tc.n_kv_heads, self.S, tc.head_dim, self.tcache.stride(0), self.seq.P.data_ptr(),
+                               self.path.data_ptr(), self.path_len.data_ptr(), self.vcap, None, 0, None, 0, 0, s))
+        chk(lib.ygg_kv_compact(self.dcache.data_ptr(), L.dtype_code(self.act_dtype), dc.n_layers, self.B,
+                               dc.n_kv_heads, self.S, dc.head_dim, self.dcache.stride(0), self.seq.P.data_ptr(),
+                               self.path.data_ptr(), self.path_len.data_ptr(), self.vcap, self.keep_idx.data_ptr(),
+                               self.tree_cap, g.depth.data_ptr(), self.tree_cap, D, s))
+        chk(lib.ygg_commit(self.seq.struct, vt.struct, self.path.data_ptr(), self.path_len.data_ptr(),
+                           self.bonus.data_ptr(), s))
+
+    # ------------------------------------------------------------------
+    def set_uniforms(self, step_index: int, seed: int) -> None:
+        """Host-pregenerated uniforms from default_rng([seed, step]) (simulator.py:306)."""
+        rng = np.random.default_rng([seed, step_index])
+        u = rng.random((self.B, self.n_uniform))
+        self.uniforms_host.copy_(torch.from_numpy(u))
+
+    def capture(self) -> None:
+        """Capture one step as a CUDA graph (static shapes, device-resident control)."""
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            # warm-up launch outside capture is not needed: kernels are plain launches; but the
+            # caching allocator must not allocate inside the captured region.
+            pass
+        torch.cuda.current_stream().wait_stream(s)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            self._launch_step()
+        self.graph = g
+
+    def step(self, use_graph: bool = True) -> None:
+        if use_graph:
+            if self.graph is None:
+                raise RuntimeError("call capture() first")
+            self.graph.replay()
+        else:
+            self._launch_step()
+        self.step_count += 1
+
+    def generated(self, b: int = 0) -> list[int]:
+        P0 = self.prefill_len
+        n = int(self.seq.n_gen[b])
+        return self.seq.hist[b, P0 : P0 + n].cpu().tolist()
+
+    def generate(self, prompts: torch.Tensor, n_tokens: int, use_graph: bool = True, sync_every: int = 8):
+        """Public generate loop: prefill, then steps until every request has n_tokens."""
+        self.prefill_len = prompts.shape[1]
+        self.prefill(prompts)
+        if use_graph and self.graph is None:
+            self.capture()
+        steps = 0
+        while True:
+            if steps % sync_every == 0:
+                if int(self.seq.n_gen.min()) >= n_tokens:
+                    break
+            if self.mode == SAMPLE:
+                self.set_uniforms(steps, 0)
+            self.step(use_graph)
+            steps += 1
+        return [self.generated(b)[:n_tokens] for b in range(self.B)], steps
+
+
+class ARDecoder:
+    """Plain greedy autoregressive decoding through the same kernels (baseline and oracle
+    for the lossless-greedy identity: speculative output == AR output)."""
+
+    def __init__(self, cfg: ModelConfig, w: dict, batch: int = 1, max_seq: int = 2048,
+                 act_dtype: torch.dtype = torch.bfloat16, device="cuda"):
+        L.require_device()
+        self.cfg, self.w, self.B = cfg, w, batch
+        self.S = max_seq + 8
+        self.act_dtype = act_dtype
+        self.dev = torch.device(device)
+        self.cache = new_cache(cfg, batch, self.S, act_dtype, self.dev)
+        self.fwd = Forward(cfg, w, self.cache, batch, 1, 1, act_dtype)
+        self.fwd.qmask.fill_(1)
+        self.argmax = torch.zeros(batch, dtype=torch.int32, device=self.dev)
+        self.P = torch.zeros(batch, dtype=torch.int32, device=self.dev)
+        self.graph = None
+
+    def _launch(self, stream=None):
+        lib = L.lib()
+        s = L.stream_ptr(stream)
+        f = self.fwd
+        f.tokens.copy_(self.argmax)
+        f.pos.copy_(self.P)
+        f.slot.copy_(self.P)
+        f.blk_start.copy_(self.P)
+        f.run(stream)
+        L.check(lib.ygg_row_stats(f.logits.data_ptr(), L.YGG_F32, self.B, self.cfg.vocab, self.cfg.vocab, 1.0,
+                                  self.argmax.data_ptr(), None, s))
+        self.P.add_(1)
+
+    def generate(self, prompts: torch.Tensor, n_tokens: int, use_graph: bool = True) -> list:
+        B, P0 = prompts.shape
+        pf = Forward(self.cfg, self.w, self.cache, B, P0, 0, self.act_dtype)
+        pd = prompts.to(self.dev, torch.int32)
+        pf.tokens.copy_(pd.reshape(-1))
+        pos = torch.arange(P0, dtype=torch.int32, device=self.dev).repeat(B)
+        pf.pos.copy_(pos)
+        pf.slot.copy_(pos)
+        pf.blk_start.zero_()
+        pf.blk_len.fill_(P0)
+        pf.run()
+        last = pf.logits.view(B, P0, -1)[:, -1, :].contiguous()
+        L.check(L.lib().ygg_row_stats(last.data_ptr(), L.YGG_F32, B, self.cfg.vocab, self.cfg.vocab, 1.0,
+                                      self.argmax.data_ptr(), None, L.stream_ptr()))
+        self.P.fill_(P0)
+        self.fwd.blk_len.fill_(1)
+        out = [self.argmax.clone()]
+        if use_graph and self.graph is None:
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                self._launch()
+            self.graph = g
+            # capture does not execute; nothing advanced yet
+        for _ in range(n_tokens - 1):
+            if use_graph:
+                self.graph.replay()
+            else:
+                self._launch()
+            out.append(self.argmax.clone())
+        return torch.stack(out, 1).cpu().tolist()

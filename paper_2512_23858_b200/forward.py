@@ -1,0 +1,160 @@
+"""One static-shape Llama forward over the C ABI (K3 GEMM + K4 epilogues + K2 attention).
+
+A ``Forward`` owns its activation buffers, GEMM plans (TMA descriptors are built once
+against these fixed buffers) and per-row inputs (tokens, positions, KV slots, tree masks),
+so a pass is a fixed sequence of kernel launches that CUDA-graph capture records verbatim.
+It realises the verifier / drafter forward the reference only prices
+(``latency_at(profiles.verifier, w_verify + 1)``, pkg/src/specsim/simulator.py:211-213).
+
+Per layer: GEMM(qkv) -> RoPE + KV append -> tree attention -> GEMM(o) -> residual + RMSNorm
+-> GEMM(gate|up) -> SwiGLU -> GEMM(down) -> residual + next RMSNorm.  The residual stream is
+f32; activations are bf16 (fast path) or f32 (parity path).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import math
+
+import torch
+
+from . import _lib as L
+from .model import ModelConfig
+
+
+class GemmPlan:
+    """Host-side plan (TMA tensor maps + stream-K segment table) for Y = X . W^T."""
+
+    def __init__(self, W: torch.Tensor, X: torch.Tensor, M: int, num_ctas: int = 0):
+        lib = L.lib()
+        N, K = W.shape
+        self.M, self.N, self.K = M, N, K
+        self.dtype = L.dtype_code(W.dtype)
+        self._mem = C.create_string_buffer(int(lib.ygg_gemm_plan_size()))
+        mp = (M + 15) // 16 * 16
+        bn = min(mp, 256)
+        tiles = (N // 128) * ((M + bn - 1) // bn)
+        self.seg_table = torch.zeros(tiles + 1 + 160, dtype=torch.int32, device=W.device)
+        nseg, wsb = C.c_int(), C.c_size_t()
+        L.check(
+            lib.ygg_gemm_plan_init(
+                self._mem, self.dtype, W.data_ptr(), X.data_ptr(), M, N, K, num_ctas, self.seg_table.data_ptr(),
+                C.byref(nseg), C.byref(wsb)
+            )
+        )
+        self.segments = nseg.value
+        self.ws_bytes = wsb.value
+        self.W, self.X = W, X  # keep alive
+
+    @property
+    def handle(self):
+        return self._mem
+
+
+class Forward:
+    def __init__(
+        self,
+        cfg: ModelConfig,
+        weights: dict,
+        cache: torch.Tensor,
+        B: int,
+        R: int,
+        mask_words: int,
+        act_dtype: torch.dtype,
+        logits: bool = True,
+        num_ctas: int = 0,
+    ):
+        L.require_device()
+        self.cfg, self.w, self.cache = cfg, weights, cache
+        self.B, self.R, self.M = B, R, B * R
+        self.mask_words = mask_words
+        self.act_dtype = act_dtype
+        self.act = L.dtype_code(act_dtype)
+        dev = cache.device
+        M, d = self.M, cfg.d_model
+        i32 = dict(dtype=torch.int32, device=dev)
+        # per-row inputs (written by the step bookkeeping kernels)
+        self.tokens = torch.zeros(M, **i32)
+        self.pos = torch.zeros(M, **i32)
+        self.slot = torch.zeros(M, **i32)
+        self.req = torch.arange(M, **i32) // R
+        self.qmask = torch.zeros(M, max(mask_words, 1), dtype=torch.int32, device=dev)
+        self.blk_start = torch.zeros(B, **i32)
+        self.blk_len = torch.zeros(B, **i32)
+        # activations
+        self.resid = torch.zeros(M, d, dtype=torch.float32, device=dev)
+        self.xn = torch.zeros(M, d, dtype=act_dtype, device=dev)
+        self.q = torch.zeros(M, cfg.q_dim, dtype=act_dtype, device=dev)
+        self.attn = torch.zeros(M, cfg.q_dim, dtype=act_dtype, device=dev)
+        self.mlp = torch.zeros(M, cfg.ffn, dtype=act_dtype, device=dev)
+        self.logits = torch.zeros(M, cfg.vocab, dtype=torch.float32, device=dev) if logits else None
+        self.plans = []
+        ws = 0
+        for lw in weights["layers"]:
+            p = {
+                "qkv": GemmPlan(lw["wqkv"], self.xn, M, num_ctas),
+                "o": GemmPlan(lw["wo"], self.attn, M, num_ctas),
+                "gu": GemmPlan(lw["wgu"], self.xn, M, num_ctas),
+                "down": GemmPlan(lw["wdown"], self.mlp, M, num_ctas),
+            }
+            self.plans.append(p)
+            ws = max(ws, *(q.ws_bytes for q in p.values()))
+        self.lm_plan = GemmPlan(weights["lm_head"], self.xn, M, num_ctas) if logits else None
+        if self.lm_plan:
+            ws = max(ws, self.lm_plan.ws_bytes)
+        self.ws = torch.empty(max(ws // 4, 1), dtype=torch.float32, device=dev)
+        self.layer_stride = cache.stride(0)
+        self.S = cache.shape[4]
+        self.scale = 1.0 / math.sqrt(cfg.head_dim)
+        # stage hooks: optional callables(stage_name, stream) for the on-device profiler (K8)
+        self.hooks = None
+
+    def weight_bytes(self) -> int:
+        """Algorithmic HBM bytes of the matmul weights streamed per pass."""
+        total = 0
+        for p in self.plans:
+            total += sum(q.W.numel() * q.W.element_size() for q in p.values())
+        if self.lm_plan:
+            total += self.lm_plan.W.numel() * self.lm_plan.W.element_size()
+        return total
+
+    def run(self, stream: torch.cuda.Stream | None = None) -> None:
+        lib, cfg = L.lib(), self.cfg
+        s = L.stream_ptr(stream)
+        chk = L.check
+        w = self.w
+        M = self.M
+        wdt = L.dtype_code(w["embed"].dtype)
+        chk(lib.ygg_embed(w["embed"].data_ptr(), wdt, cfg.vocab, cfg.d_model, self.tokens.data_ptr(), M,
+                          self.resid.data_ptr(), s))
+        chk(lib.ygg_rmsnorm(self.resid.data_ptr(), w["layers"][0]["attn_norm"].data_ptr(), self.act, M, cfg.d_model,
+                            cfg.norm_eps, self.xn.data_ptr(), s))
+        ws = self.ws.data_ptr()
+        nl = len(self.plans)
+        for li, (p, lw) in enumerate(zip(self.plans, w["layers"])):
+            cache_l = self.cache.data_ptr() + li * self.layer_stride * self.cache.element_size()
+            chk(lib.ygg_gemm_run(p["qkv"].handle, ws, s))
+            chk(lib.ygg_epi_qkv_rope(p["qkv"].handle, ws, cfg.n_heads, cfg.n_kv_heads, cfg.head_dim,
+                                     cfg.rope_theta, self.pos.data_ptr(), self.slot.data_ptr(),
+                                     self.req.data_ptr(), self.q.data_ptr(), cache_l, self.S, self.act, s))
+            chk(lib.ygg_attention(self.q.data_ptr(), cache_l, self.act, M, self.B, cfg.n_heads, cfg.n_kv_heads,
+                                  cfg.head_dim, self.S, self.blk_start.data_ptr(), self.blk_len.data_ptr(),
+                                  self.qmask.data_ptr() if self.mask_words > 0 else None, self.mask_words,
+                                  self.scale, self.attn.data_ptr(), s))
+            chk(lib.ygg_gemm_run(p["o"].handle, ws, s))
+            chk(lib.ygg_epi_residual_norm(p["o"].handle, ws, self.resid.data_ptr(), lw["mlp_norm"].data_ptr(),
+                                          cfg.norm_eps, self.xn.data_ptr(), self.act, s))
+            chk(lib.ygg_gemm_run(p["gu"].handle, ws, s))
+            chk(lib.ygg_epi_swiglu(p["gu"].handle, ws, self.mlp.data_ptr(), self.act, s))
+            chk(lib.ygg_gemm_run(p["down"].handle, ws, s))
+            nxt = w["layers"][li + 1]["attn_norm"] if li + 1 < nl else w["final_norm"]
+            chk(lib.ygg_epi_residual_norm(p["down"].handle, ws, self.resid.data_ptr(), nxt.data_ptr(),
+                                          cfg.norm_eps, self.xn.data_ptr(), self.act, s))
+        if self.lm_plan is not None:
+            chk(lib.ygg_gemm_run(self.lm_plan.handle, ws, s))
+            chk(lib.ygg_epi_store(self.lm_plan.handle, ws, self.logits.data_ptr(), L.YGG_F32, cfg.vocab, s))
+
+
+def new_cache(cfg: ModelConfig, B: int, S: int, dtype: torch.dtype, device) -> torch.Tensor:
+    """KV cache [layers, B, 2 (k|v), Hkv, S, hd] — per-(request, head) contiguous key streams."""
+    return torch.zeros(cfg.n_layers, B, 2, cfg.n_kv_heads, S, cfg.head_dim, dtype=dtype, device=device)

@@ -1,0 +1,441 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 speculative-decoding step (BASELINE.json metric: accepted tokens/s and
+p50 step latency per B200; % HBM roofline).
+
+Default workload (N=1): BASELINE.json configs[1] = cfg2 — Llama-3-8B-shaped target + Llama-3.2-
+1B-shaped draft (bf16, coupled synthetic random-init weights, random 512-token prompt), EGT
+depth 6 width 8, expansion_k 8, max_verify 64, greedy, one request per GPU.  With --gpus N each
+rank serves its own request (request sharding, weak scaling, no collective on the data path;
+one NCCL all-gather of the generated ids at the end).
+
+Timing: W warm-up graph replays, then K timed replays bracketed by barrier + synchronize, CUDA
+events on the launching stream, max over ranks.  Every step streams ~17.5 GB of weights, far
+more than the 126 MB L2, so no flush is needed between steps.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+WORKLOADS = {
+    "cfg2": dict(target="llama3-8b", draft="llama3.2-1b", depth=6, width=8, k=8, max_verify=64, batch=1,
+                 prompt=512, desc="cfg2: Llama-3-8B target + Llama-3.2-1B draft (bf16), EGT D6 W8 k8, "
+                                  "max_verify 64, greedy, 1 request/GPU, 512-token prompt"),
+    "cfg1": dict(target="tiny-target", draft="tiny-draft", depth=4, width=4, k=8, max_verify=64, batch=1,
+                 prompt=32, desc="cfg1: tiny 4L d256 target + 1L draft, EGT D4 W4 k8, greedy, batch 1"),
+}
+# Coupled synthetic weights (paper_2512_23858_b200/model.py): shared semantic table + permutation.
+COUPLING = {
+    "cfg2": dict(rank=2048, logit_scale=16.0, head_noise=2.0, layer_gain=2.0),
+    "cfg1": dict(rank=256, logit_scale=8.0, head_noise=2.0, layer_gain=2.0),
+}
+DRAFT_PROF = ((1, 400.0), (64, 420.0), (128, 460.0))    # placeholder Eq.3 table (us); refreshed by K8
+VERIFY_PROF = ((1, 2400.0), (64, 2450.0), (128, 2600.0))
+
+
+def _peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), "measured", d
+    return 6650.0, "fallback", {}
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        try:
+            fd, self.path = tempfile.mkstemp(suffix=".csv")
+            os.close(fd)
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100", "-f", self.path], stdout=subprocess.DEVNULL, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        rows = []
+        try:
+            for line in Path(self.path).read_text().splitlines():
+                parts = [p.strip() for p in line.split(",")]
+                if len(parts) >= 8:
+                    rows.append(parts)
+        except Exception:
+            return None
+        if not rows:
+            return None
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if "Active" in r[4 + i] and "Not" not in r[4 + i]})
+        load = [s for s in sm if s > 0.5 * (max(sm) if sm else 0)]
+        return {"sm_mhz": statistics.median(load) if load else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+def build_decoder(wl: dict, name: str, device, seed_offset: int = 0):
+    import torch
+
+    from paper_2512_23858_b200.engine import SpecDecoder, StepShape
+    from paper_2512_23858_b200.model import Coupling, init_weights, preset
+
+    tc, dc = preset(wl["target"]), preset(wl["draft"])
+    cp = Coupling(**COUPLING[name])
+    tw = init_weights(tc, 0, torch.bfloat16, device, cp)
+    dw = init_weights(dc, 1, torch.bfloat16, device, cp)
+
+    class PP:
+        class drafter:
+            breakpoints = DRAFT_PROF
+
+        class verifier:
+            breakpoints = VERIFY_PROF
+
+    shape = StepShape(wl["depth"], wl["width"], wl["k"], wl["max_verify"])
+    max_seq = wl["prompt"] + 64 * 1024 // 64 + 2048
+    sd = SpecDecoder(tc, tw, dc, dw, shape, batch=wl["batch"], max_seq=max_seq, act_dtype=torch.bfloat16,
+                     profiles=PP, device=device)
+    return sd, tc, dc
+
+
+def prompts_for(wl, vocab, rank):
+    import torch
+
+    rows = []
+    for b in range(wl["batch"]):
+        g = torch.Generator().manual_seed(1000 + rank * wl["batch"] + b)
+        rows.append(torch.randint(0, vocab, (wl["prompt"],), generator=g))
+    return torch.stack(rows)
+
+
+def gemm_roofline(sd, peak_gbs):
+    """Per-launch CUDA-event timing of every GEMM of one verify forward (the dominant kernel),
+    each launch streaming a different layer's weights from HBM."""
+    import torch
+
+    from paper_2512_23858_b200 import _lib as L
+
+    lib = L.lib()
+    vf = sd.verify
+    plans = [p for layer in vf.plans for p in layer.values()] + [vf.lm_plan]
+    s = torch.cuda.current_stream()
+    sp = L.stream_ptr()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in plans]
+    for _ in range(2):
+        for p in plans:
+            L.check(lib.ygg_gemm_run(p.handle, vf.ws.data_ptr(), sp))
+    torch.cuda.synchronize()
+    for p, (a, b) in zip(plans, ev):
+        a.record(s)
+        L.check(lib.ygg_gemm_run(p.handle, vf.ws.data_ptr(), sp))
+        b.record(s)
+    torch.cuda.synchronize()
+    times = [a.elapsed_time(b) * 1e-3 for a, b in ev]
+    nbytes = [p.W.numel() * p.W.element_size() for p in plans]
+    achieved = sum(nbytes) / sum(times) / 1e9
+    return {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak_gbs, "unit": "GB/s",
+            "frac": round(achieved / peak_gbs, 4), "traffic": None,
+            "kernel": "gemm_bf16_tc_kernel (swap-AB tcgen05 stream-K weight streaming)",
+            "launches_timed": len(plans), "bytes_per_launch_avg": int(sum(nbytes) / len(plans)),
+            "avg_launch_us": round(sum(times) / len(times) * 1e6, 2)}
+
+
+def verify_roofline(sd, peak_gbs, reps=10):
+    """Whole verify forward (graph-captured) vs its algorithmic HBM bytes (weights + KV read)."""
+    import torch
+
+    vf = sd.verify
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        vf.run()
+    for _ in range(3):
+        g.replay()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(reps):
+        g.replay()
+    b.record()
+    torch.cuda.synchronize()
+    t = a.elapsed_time(b) * 1e-3 / reps
+    P = int(sd.seq.P.max())
+    kv = sd.B * (P + sd.T) * sd.tc.kv_bytes_per_token(2)
+    nbytes = vf.weight_bytes() + kv
+    return {"verify_ms": round(t * 1e3, 3), "bytes": nbytes, "achieved_gbs": round(nbytes / t / 1e9, 1),
+            "frac": round(nbytes / t / 1e9 / peak_gbs, 4)}
+
+
+def stage_profile(sd, steps=4):
+    """K8: on-device globaltimer stamps around each stage of one step (separate graph)."""
+    import torch
+
+    from paper_2512_23858_b200 import profiler
+
+    prof = profiler.StageProfiler(sd)
+    return prof.measure(steps)
+
+
+def cpu_step_sample(wl_name: str, aal: float):
+    """CPU port of the same step (oracle, torch fp32, all host threads) timed on a bounded sample:
+    one target layer at the verify width, one draft layer at the draft width, both LM heads, and the
+    tree logic (top-k, EGT growth, knapsack prune, walk) — composed by layer count."""
+    import numpy as np
+    import torch
+
+    from oracle import tree_ref as T
+    from oracle.llama_ref import RefCache, RefLlama
+    from paper_2512_23858_b200.model import Coupling, init_weights, preset
+
+    wl = WORKLOADS[wl_name]
+    torch.set_num_threads(os.cpu_count() or 1)
+    tcfg, dcfg = preset(wl["target"]), preset(wl["draft"])
+    D, W, k = wl["depth"], wl["width"], wl["k"]
+    Tv = min(wl["max_verify"], 1 + D * W) + 1
+    P = wl["prompt"]
+    S = P + 1 + Tv + 8
+
+    def layer_time(cfg, rows, reps=2):
+        one = preset(cfg.name, n_layers=1)
+        w = init_weights(one, 0, torch.float32, "cpu", None)
+        m = RefLlama(one, w)
+        cache = RefCache(one, S)
+        vis = torch.zeros(rows, S, dtype=torch.bool)
+        vis[:, : P + rows] = True
+        toks = list(range(rows))
+        pos = list(range(P, P + rows))
+        m.forward(cache, toks, pos, pos, vis)
+        t0 = time.perf_counter()
+        for _ in range(reps):
+            m.forward(cache, toks, pos, pos, vis)
+        full = (time.perf_counter() - t0) / reps
+        # head-only time (embedding + final norm + lm_head) to split layer vs head
+        x = torch.randn(rows, cfg.d_model)
+        t0 = time.perf_counter()
+        for _ in range(reps):
+            _ = x @ m.head.T
+        head = (time.perf_counter() - t0) / reps
+        return max(full - head, 0.0), head, w
+
+    t_layer_t, t_head_t, _ = layer_time(tcfg, Tv)
+    t_layer_d, t_head_d, _ = layer_time(dcfg, max(W, 2))
+    rng = np.random.default_rng(0)
+    logits = rng.standard_normal((max(W, 2), dcfg.vocab)).astype(np.float32)
+    t0 = time.perf_counter()
+    tree = T.Tree.root(1, 0.9)
+    for _ in range(D):
+        cands = {f: T.topk_softmax(logits[i % len(logits)], k) for i, f in enumerate(tree.levels()[-1])}
+        T.grow_step(tree, lambda tr, n, kk: cands[n], W, k)
+    pr = T.prune_verify(tree, tree.prob, DRAFT_PROF, VERIFY_PROF, D, W, wl["max_verify"])
+    am = rng.integers(0, 10, size=len(pr.tree) + 1)
+    T.greedy_walk(pr.tree, am)
+    t_tree = time.perf_counter() - t0
+    step = tcfg.n_layers * t_layer_t + t_head_t + (D + 1) * (dcfg.n_layers * t_layer_d + t_head_d) + t_tree
+    sample = (f"1 {tcfg.name} layer @ {Tv} rows + LM head, 1 {dcfg.name} layer @ {max(W, 2)} rows + LM head, "
+              f"tree logic (D{D} W{W} k{k}); step = {tcfg.n_layers}x target layer + {D + 1}x "
+              f"({dcfg.n_layers}x draft layer + head) + tree; tokens/step = GPU-measured AAL {aal:.3f}")
+    return {"value": round(aal / step, 4), "unit": "tokens/s", "cores": torch.get_num_threads(), "kind": "port",
+            "sample": sample, "step_s": round(step, 4)}
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    wl = WORKLOADS[args.workload]
+    aal = args.ref_aal
+    res = cpu_step_sample(args.workload, aal)
+    line = {"impl": "reference", "metric": "accepted tokens/s", "value": res["value"], "unit": "tokens/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(res["step_s"] * 1e3, 3), "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": wl["desc"], "aal_assumed": aal},
+            "cpu_baseline": {"value": res["value"], "unit": "tokens/s", "cores": res["cores"], "kind": "port",
+                             "sample": res["sample"]},
+            "e2e": {"value": res["value"], "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2512_23858_b200 import _lib as L
+
+    device = torch.device("cuda", local_rank)
+    torch.cuda.set_device(device)
+    wl = WORKLOADS[args.workload]
+    peak, peak_kind, _ = _peaks()
+    sd, tc, dc = build_decoder(wl, args.workload, device)
+    prompts = prompts_for(wl, tc.vocab, rank)
+    sd.prefill_len = prompts.shape[1]
+    sd.prefill(prompts)
+    n0 = L.launches["count"]
+    sd.capture()
+    launches_per_step = L.launches["count"] - n0
+    for _ in range(args.warmup):
+        sd.step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = ClockSampler(local_rank)
+    clocks.start()
+    gen0 = sd.seq.n_gen.clone()
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+    torch.cuda.synchronize()
+    evs[0].record()
+    for i in range(args.steps):
+        sd.step()
+        evs[i + 1].record()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    step_ms = [evs[i].elapsed_time(evs[i + 1]) for i in range(args.steps)]
+    total_s = evs[0].elapsed_time(evs[-1]) * 1e-3
+    tokens = int((sd.seq.n_gen - gen0).sum())
+    t = torch.tensor([total_s, float(tokens)], dtype=torch.float64, device=device)
+    if world > 1:
+        tmax = t[0:1].clone()
+        dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+        tsum = t[1:2].clone()
+        dist.all_reduce(tsum, op=dist.ReduceOp.SUM)
+        total_s, tokens_all = float(tmax), float(tsum)
+    else:
+        tokens_all = float(tokens)
+    aal = tokens / (args.steps * sd.B)
+
+    # ---- e2e through the public API: pinned H2D of the step inputs, replay, D2H of the emitted tokens
+    e2e = e2e_run(sd, args.steps, device)
+    e2e_tokens = torch.tensor([e2e["tokens"]], dtype=torch.float64, device=device)
+    e2e_t = torch.tensor([e2e["seconds"]], dtype=torch.float64, device=device)
+    if world > 1:
+        dist.all_reduce(e2e_tokens, op=dist.ReduceOp.SUM)
+        dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
+
+    gemm = gemm_roofline(sd, peak)
+    ver = verify_roofline(sd, peak)
+    try:
+        stages = stage_profile(sd)
+    except Exception as exc:  # profiler is diagnostic only
+        stages = {"error": str(exc)}
+    # final result gather (the only collective)
+    gathered = None
+    if world > 1:
+        out = [None] * world
+        dist.all_gather_object(out, sd.generated(0)[:8])
+        gathered = len(out)
+    if rank != 0:
+        return
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_step_sample(args.workload, aal)
+        cpu.pop("step_s", None)
+    line = {
+        "metric": "accepted tokens/s", "value": round(tokens_all / total_s, 2), "unit": "tokens/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(total_s * 1e3 / args.steps, 4), "p50_step_ms": round(statistics.median(step_ms), 4),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic (coupled random-init weights, random prompts)",
+        "config": {"workload": wl["desc"], "aal": round(aal, 4), "requests_per_gpu": sd.B,
+                   "parallelism": f"request sharding x{world} (replicas, no collective in the step)",
+                   "l2": "inputs > L2: ~17.5 GB of weights streamed per step (126 MB L2)",
+                   "coupling": COUPLING[args.workload]},
+        "roofline": gemm, "verify_roofline": ver, "stage_us": stages,
+        "e2e": {"value": round(float(e2e_tokens) / float(e2e_t), 2), "unit": "tokens/s",
+                "h2d_bytes_per_step": e2e["h2d"], "d2h_bytes_per_step": e2e["d2h"]},
+        "gpu_launches": launches_per_step * args.steps, "launches_per_step": launches_per_step,
+        "clocks": clk, "cpu_baseline": cpu, "peak_kind": peak_kind, "gathered_ranks": gathered,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def e2e_run(sd, steps, device):
+    """Public-API loop: each step copies its inputs (sampling uniforms / control words) from pinned host
+    memory, replays the step graph, and reads the emitted tokens back into pinned host memory."""
+    import torch
+
+    B = sd.B
+    n_emit = sd.shape.depth + 2
+    host_out = torch.zeros(B, n_emit + 1, dtype=torch.int32).pin_memory()
+    host_in = torch.zeros_like(sd.uniforms_host).pin_memory()
+    h2d = host_in.numel() * host_in.element_size()
+    d2h = host_out.numel() * host_out.element_size()
+    torch.cuda.synchronize()
+    gen0 = sd.seq.n_gen.clone()
+    t0 = time.perf_counter()
+    for i in range(steps):
+        sd.uniforms.copy_(host_in, non_blocking=True)
+        sd.step()
+        sd.read_emitted(host_out)
+        torch.cuda.current_stream().synchronize()
+    dt = time.perf_counter() - t0
+    tokens = int((sd.seq.n_gen - gen0).sum())
+    return {"tokens": tokens, "seconds": dt, "h2d": h2d, "d2h": d2h}
+
+
+def main():
+    ap = argparse.ArgumentParser(description=__doc__)
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=32)
+    ap.add_argument("--warmup", type=int, default=4)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="cfg2")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ref-aal", type=float, default=float(os.environ.get("YGG_REF_AAL", "3.0")),
+                    help="accepted tokens per step assumed by --impl reference (GPU-measured AAL)")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        ap.error("--warmup must be >= 3")
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    try:
+        run_ours(args, rank, world, local_rank)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -194,6 +194,15 @@ int ygg_attention(const void* q, const void* cache, int dtype, int M, int B, int
                   const int32_t* blk_start, const int32_t* blk_len, const uint32_t* qmask, int mask_words,
                   float scale, void* out, ygg_stream_t stream);
 
+/* K2 on tcgen05 (bf16): split-KV tree attention.  Cache layout per layer: [B, 2, Hkv, S, hd]
+ * where the kv=0 half holds K rows [S][hd] and the kv=1 half holds V transposed [hd][S]
+ * (S % 64 == 0).  Plan = TMA tensor maps for q and one layer's cache; partials >= partial_bytes. */
+size_t ygg_attn_plan_size(void);
+int ygg_attn_plan_init(void* plan, const void* q, const void* cache_layer, int B, int M, int Hq, int Hkv, int hd,
+                       int S, size_t* partial_bytes);
+int ygg_attention_tc(const void* plan, const int32_t* blk_start, const int32_t* blk_len, const uint32_t* qmask,
+                     int mask_words, float scale, float* partials, void* out, ygg_stream_t stream);
+
 /* Per-row max / argmax / log-sum-exp(x/temperature) over logits [rows, ld]. */
 int ygg_row_stats(const void* logits, int dtype, int rows, int V, int ld, float temperature, int32_t* argmax,
                   float* stats, ygg_stream_t stream);
@@ -214,9 +223,10 @@ int ygg_level_inputs(ygg_tree tree, ygg_seq seq, int R, int k, int32_t* tokens, 
 /* Verify inputs: bonus row + pruned tree rows, T = vtree.cap + 1 rows per request. */
 int ygg_verify_inputs(ygg_tree vtree, ygg_seq seq, int32_t* tokens, int32_t* pos, int32_t* slot, int32_t* req,
                       uint32_t* qmask, int mask_words, int32_t* blk_start, int32_t* blk_len, ygg_stream_t stream);
-/* Append accepted tokens + bonus, advance P, log accepted_len. */
+/* Append accepted tokens + bonus, advance P, log accepted_len; emit [B, emit_cap] (optional) receives
+ * [count, tokens..., -1 padding] of this step for host streaming. */
 int ygg_commit(ygg_seq seq, ygg_tree vtree, const int32_t* path, const int32_t* path_len, const int32_t* bonus,
-               ygg_stream_t stream);
+               int32_t* emit, int emit_cap, ygg_stream_t stream);
 
 /* ---------------- K8: on-device stage timer ---------------- */
 int ygg_stamp(unsigned long long* slot, ygg_stream_t stream);

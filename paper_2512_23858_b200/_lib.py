@@ -113,16 +113,48 @@ _SIGS: dict[str, tuple] = {
     "ygg_rmsnorm": (C.c_int, [vp, vp, C.c_int, C.c_int, C.c_int, C.c_float, vp, vp]),
     "ygg_attention": (C.c_int, [vp, vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, vp, vp, vp,
                                 C.c_int, C.c_float, vp, vp]),
+    "ygg_attn_plan_size": (C.c_size_t, []),
+    "ygg_attn_plan_init": (C.c_int, [vp, vp, vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
+                                     C.POINTER(C.c_size_t)]),
+    "ygg_attention_tc": (C.c_int, [vp, vp, vp, vp, C.c_int, C.c_float, vp, vp, vp]),
     "ygg_row_stats": (C.c_int, [vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_float, vp, vp, vp]),
     "ygg_pass0_inputs": (C.c_int, [YggSeq, C.c_int, C.c_int, vp, vp, vp, vp, vp, C.c_int, vp, vp, vp]),
     "ygg_init_roots": (C.c_int, [YggTree, vp, vp, C.c_int, C.c_int, C.c_int, vp]),
     "ygg_level_inputs": (C.c_int, [YggTree, YggSeq, C.c_int, C.c_int, vp, vp, vp, vp, vp, C.c_int, vp, vp, vp, vp]),
     "ygg_verify_inputs": (C.c_int, [YggTree, YggSeq, vp, vp, vp, vp, vp, C.c_int, vp, vp, vp]),
-    "ygg_commit": (C.c_int, [YggSeq, YggTree, vp, vp, vp, vp]),
+    "ygg_commit": (C.c_int, [YggSeq, YggTree, vp, vp, vp, vp, C.c_int, vp]),
     "ygg_stamp": (C.c_int, [vp, vp]),
 }
 
 EXPORTED = tuple(_SIGS)
+
+# Kernels launched by one successful call (used to count device launches per step).
+KERNELS_PER_CALL = {
+    "ygg_topk_softmax": 2, "ygg_egt_grow_level": 1, "ygg_build_mask": 1, "ygg_knapsack_prune": 1,
+    "ygg_tree_subtree": 1, "ygg_accept": 1, "ygg_kv_compact": 1, "ygg_gemm_run": 1, "ygg_epi_store": 1,
+    "ygg_epi_residual_norm": 1, "ygg_epi_swiglu": 1, "ygg_epi_qkv_rope": 1, "ygg_embed": 1, "ygg_rmsnorm": 1,
+    "ygg_attention": 1, "ygg_attention_tc": 2, "ygg_row_stats": 1, "ygg_pass0_inputs": 1, "ygg_init_roots": 1, "ygg_level_inputs": 1,
+    "ygg_verify_inputs": 1, "ygg_commit": 1, "ygg_stamp": 1,
+}
+launches = {"count": 0}
+
+
+class _Counted:
+    __slots__ = ("fn", "k")
+
+    def __init__(self, fn, k):
+        self.fn, self.k = fn, k
+
+    def __call__(self, *a):
+        rc = self.fn(*a)
+        if rc == 0:
+            launches["count"] += self.k
+        return rc
+
+
+class _Lib:
+    pass
+
 
 _lib = None
 
@@ -136,11 +168,14 @@ def load():
                 f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'` "
                 "(there is no CPU fallback)"
             )
-        lib = C.CDLL(str(LIB_PATH))
+        raw = C.CDLL(str(LIB_PATH))
+        lib = _Lib()
+        lib._raw = raw
         for name, (res, args) in _SIGS.items():
-            fn = getattr(lib, name)
+            fn = getattr(raw, name)
             fn.restype = res
             fn.argtypes = args
+            setattr(lib, name, _Counted(fn, KERNELS_PER_CALL[name]) if name in KERNELS_PER_CALL else fn)
         _lib = lib
     return _lib
 

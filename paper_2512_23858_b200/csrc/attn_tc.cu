@@ -1,4 +1,399 @@
-// tcgen05 tree attention (bf16) — placeholder until written
+// K2: tree / prefix attention on tcgen05 (bf16), split over the key sequence.
+//
+// CTA = (key chunk of KC=128 keys, query tile of 128 rows, kv head, request).  Query rows are
+// (token, q-head-in-group) pairs of one kv head, so GQA shares every K/V tile across the G
+// heads of the group.  Flow per CTA:
+//   TMA  : Q tile [128 x hd], K chunk [KC x hd], V^T chunk [hd x KC] (V is cached transposed so
+//          both MMAs read K-major, 128B-swizzled operands)
+//   MMA1 : S[128 x KC] = Q . K^T            -> TMEM columns [0, KC)
+//   soft : one thread per row: tcgen05.ld S, ancestor mask on the fly (prefix keys always
+//          visible; block keys by the row's tree-mask bit), max / exp2 / sum, P (bf16) -> smem
+//   MMA2 : O[128 x hd] = P . V              -> TMEM columns [KC, KC + hd)
+//   out  : unnormalised O + (max, sum) partials per chunk; a combine kernel merges chunks in
+//          fixed order (deterministic).
+// Chunks past a request's key count exit immediately after recording an empty partial.
+#include <cudaTypedefs.h>
+
+#include <cmath>
+#include <cstring>
+
 #include "common.cuh"
 #include "host_util.h"
-extern "C" int ygg_prepare_attn_tc(void) { return YGG_OK; }
+
+namespace ygg {
+
+constexpr int kKC = 128;           // keys per CTA
+constexpr int kQRows = 128;        // query rows per CTA (UMMA M)
+constexpr int kAttnTcThreads = 160; // warps 0-3 softmax/epilogue, warp 4 TMA + MMA
+
+struct AttnPlan {
+  uint32_t magic;
+  int B, M, Hq, Hkv, hd, S, T;  // T = query rows (tokens) per request
+  int G, tok_per_tile, q_tiles, chunks;
+  alignas(64) CUtensorMap tm_q;
+  alignas(64) CUtensorMap tm_k;
+  alignas(64) CUtensorMap tm_vt;
+};
+constexpr uint32_t kAttnMagic = 0x59474741u;
+
+struct AttnArgs {
+  int M, Hq, Hkv, hd, S, T, G, tok_per_tile, chunks, mask_words;
+  float scale_log2;
+  const int32_t* blk_start;
+  const int32_t* blk_len;
+  const uint32_t* qmask;
+  float* opart;  // [chunks][M*Hq][hd]
+  float* ml;     // [chunks][M*Hq][2]
+};
+
+YGG_DEV void tma_load_3d(void* smem_dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1, int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+YGG_DEV void tma_load_2d_nohint(void* smem_dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+      : "memory");
+}
+YGG_DEV void st_shared_v4(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
+}
+YGG_DEV uint32_t pack_bf16(float lo, float hi) {
+  __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<uint32_t*>(&v);
+}
+
+template <int HD>
+__global__ void __launch_bounds__(kAttnTcThreads, 1)
+    attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
+                   const __grid_constant__ CUtensorMap tm_vt, AttnArgs a) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* base = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  constexpr int DCH = HD / 64;            // 64-wide d chunks
+  constexpr int KCH = kKC / 64;           // 64-wide key chunks
+  unsigned char* sq = base;                                   // DCH x [128 rows x 128 B]
+  unsigned char* sk = sq + DCH * kQRows * 128;                // DCH x [KC rows x 128 B]
+  unsigned char* svt = sk + DCH * kKC * 128;                  // KCH x [HD rows x 128 B]
+  unsigned char* sp = svt + KCH * HD * 128;                   // KCH x [128 rows x 128 B]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sp + KCH * kQRows * 128);  // load, s, p, o
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 4);
+
+  const int chunk = blockIdx.x, qt = blockIdx.y, kvh = blockIdx.z % a.Hkv, r = blockIdx.z / a.Hkv;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  pdl_wait();
+  pdl_launch_dependents();
+  const int bs = a.blk_start[r], bl = a.blk_len[r];
+  const int nkeys = bs + bl;
+  const int key0 = chunk * kKC;
+  const int t0 = qt * a.tok_per_tile;
+  // Row owned by this thread (softmax warps): TMEM lane = row.
+  const int row = (warp & 3) * 32 + lane;
+  const int tq = t0 + row / a.G;
+  const int head = kvh * a.G + row % a.G;
+  const bool row_valid = warp < 4 && tq < a.T;
+  const int m = r * a.T + tq;
+  const size_t orow = static_cast<size_t>(m) * a.Hq + head;
+  const size_t slot_stride = static_cast<size_t>(a.M) * a.Hq;
+  // Causal prefill tiles never need keys past their last query token.
+  const int last_tok = min(a.T - 1, t0 + a.tok_per_tile - 1);
+  const bool skip = key0 >= nkeys || (a.mask_words == 0 && key0 > bs + last_tok);
+  if (skip) {
+    if (row_valid) {
+      a.ml[(static_cast<size_t>(chunk) * slot_stride + orow) * 2] = -INFINITY;
+      a.ml[(static_cast<size_t>(chunk) * slot_stride + orow) * 2 + 1] = 0.f;
+    }
+    return;
+  }
+  if (warp == 4) {
+    if (lane == 0) {
+      for (int i = 0; i < 4; ++i) mbar_init(&bars[i], i == 2 ? 128 : 1);
+      fence_barrier_init();
+    }
+    __syncwarp();
+    tmem_alloc(tmem_slot, 256);
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t tS = tmem, tO = tmem + kKC;
+
+  if (warp == 4) {
+    if (lane == 0) {
+      const uint32_t bytes = DCH * kQRows * 128 + DCH * kKC * 128 + KCH * HD * 128;
+      mbar_arrive_expect_tx(&bars[0], bytes);
+      for (int c = 0; c < DCH; ++c) {
+        tma_load_3d(sq + c * kQRows * 128, &tm_q, &bars[0], c * 64, kvh * a.G, r * a.T + t0);
+        tma_load_2d_nohint(sk + c * kKC * 128, &tm_k, &bars[0], c * 64,
+                           (r * 2 * a.Hkv + kvh) * a.S + key0);
+      }
+      for (int c = 0; c < KCH; ++c)
+        tma_load_2d_nohint(svt + c * HD * 128, &tm_vt, &bars[0], key0 + c * 64, ((r * 2 + 1) * a.Hkv + kvh) * HD);
+      mbar_wait(&bars[0], 0);
+      tc_fence_after();
+      // MMA1: S = Q . K^T  (M=128, N=KC, K=HD)
+      const uint32_t id1 = umma_idesc_bf16(kQRows, kKC);
+#pragma unroll
+      for (int kk = 0; kk < HD / 16; ++kk) {
+        const uint64_t ad = umma_desc_sw128(smem_u32(sq + (kk / 4) * kQRows * 128) + (kk % 4) * 32);
+        const uint64_t bd = umma_desc_sw128(smem_u32(sk + (kk / 4) * kKC * 128) + (kk % 4) * 32);
+        umma_bf16(tS, ad, bd, id1, kk > 0 ? 1u : 0u);
+      }
+      umma_commit(&bars[1]);
+      // MMA2 after the softmax warps published P.
+      mbar_wait(&bars[2], 0);
+      tc_fence_after();
+      const uint32_t id2 = umma_idesc_bf16(kQRows, HD);
+#pragma unroll
+      for (int kk = 0; kk < kKC / 16; ++kk) {
+        const uint64_t ad = umma_desc_sw128(smem_u32(sp + (kk / 4) * kQRows * 128) + (kk % 4) * 32);
+        const uint64_t bd = umma_desc_sw128(smem_u32(svt + (kk / 4) * HD * 128) + (kk % 4) * 32);
+        umma_bf16(tO, ad, bd, id2, kk > 0 ? 1u : 0u);
+      }
+      umma_commit(&bars[3]);
+    }
+  } else {
+    // ===== softmax: one thread per query row =====
+    uint32_t mw[YGG_MAX_MASK_WORDS];
+#pragma unroll
+    for (int w = 0; w < YGG_MAX_MASK_WORDS; ++w)
+      mw[w] = (row_valid && w < a.mask_words) ? a.qmask[static_cast<size_t>(m) * a.mask_words + w] : 0u;
+    mbar_wait(&bars[1], 0);
+    tc_fence_after();
+    const uint32_t lane_base = static_cast<uint32_t>((warp & 3) * 32) << 16;
+    // Visibility of key (key0 + j) for this row: prefix keys always; block keys by tree-mask bit
+    // (or causally when no mask is given); nothing past the request's key count.
+    auto masked = [&](float v, int j) -> float {
+      const int key = key0 + j;
+      bool vis = row_valid && key < nkeys;
+      if (vis && key >= bs) {
+        const int jb = key - bs;
+        if (a.mask_words == 0) {
+          vis = jb <= tq;
+        } else {
+          uint32_t word = 0;
+#pragma unroll
+          for (int w = 0; w < YGG_MAX_MASK_WORDS; ++w)
+            if (w == (jb >> 5)) word = mw[w];
+          vis = (word >> (jb & 31)) & 1u;
+        }
+      }
+      return vis ? v * a.scale_log2 : -INFINITY;
+    };
+    // Pass 1: row max straight from TMEM (16 columns at a time, no S copy in registers).
+    float mx = -INFINITY;
+#pragma unroll 1
+    for (int c = 0; c < kKC; c += 16) {
+      float v[16];
+      tmem_ld16(tS + lane_base + c, v);
+#pragma unroll
+      for (int j = 0; j < 16; ++j) mx = fmaxf(mx, masked(v[j], c + j));
+    }
+    // Pass 2: P = 2^(s - max) -> bf16 -> smem, 128B-swizzled K-major rows (unit u -> u ^ (row & 7)).
+    float l = 0.f;
+#pragma unroll 1
+    for (int c = 0; c < kKC; c += 16) {
+      float v[16];
+      tmem_ld16(tS + lane_base + c, v);
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const float sv = masked(v[j], c + j);
+        v[j] = (mx == -INFINITY || sv == -INFINITY) ? 0.f : exp2f(sv - mx);
+        l += v[j];
+      }
+      const uint32_t rbase = smem_u32(sp + (c / 64) * kQRows * 128 + row * 128);
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int u = ((c % 64) / 8) + h;
+        const float* p8 = v + 8 * h;
+        st_shared_v4(rbase + ((u ^ (row & 7)) << 4), pack_bf16(p8[0], p8[1]), pack_bf16(p8[2], p8[3]),
+                     pack_bf16(p8[4], p8[5]), pack_bf16(p8[6], p8[7]));
+      }
+    }
+    fence_proxy_async();
+    tc_fence_before();
+    mbar_arrive(&bars[2]);
+    mbar_wait(&bars[3], 0);
+    tc_fence_after();
+    // Every lane executes the (warp-collective, .aligned) TMEM loads; only valid rows store.
+    float* op = a.opart + (static_cast<size_t>(chunk) * slot_stride + (row_valid ? orow : 0)) * HD;
+#pragma unroll
+    for (int c = 0; c < HD; c += 16) {
+      float o[16];
+      tmem_ld16(tO + lane_base + c, o);
+      if (row_valid) {
+#pragma unroll
+        for (int j = 0; j < 16; j += 4)
+          *reinterpret_cast<float4*>(op + c + j) = make_float4(o[j], o[j + 1], o[j + 2], o[j + 3]);
+      }
+    }
+    if (row_valid) {
+      a.ml[(static_cast<size_t>(chunk) * slot_stride + orow) * 2] = mx;
+      a.ml[(static_cast<size_t>(chunk) * slot_stride + orow) * 2 + 1] = l;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 4) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 256);
+  }
+}
+
+// Merge chunk partials in fixed chunk order: out = sum_c 2^(m_c - M) O_c / sum_c 2^(m_c - M) l_c.
+__global__ void attn_combine_kernel(const float* __restrict__ opart, const float* __restrict__ ml, int chunks,
+                                    int rows, int hd, __nv_bfloat16* __restrict__ out) {
+  pdl_wait();
+  pdl_launch_dependents();
+  const int rr = blockIdx.x;  // m*Hq + head
+  float M = -INFINITY;
+  for (int c = 0; c < chunks; ++c) M = fmaxf(M, ml[(static_cast<size_t>(c) * rows + rr) * 2]);
+  for (int d = threadIdx.x; d < hd; d += blockDim.x) {
+    float acc = 0.f, L = 0.f;
+    if (M != -INFINITY) {
+      for (int c = 0; c < chunks; ++c) {
+        const float mc = ml[(static_cast<size_t>(c) * rows + rr) * 2];
+        if (mc == -INFINITY) continue;
+        const float w = exp2f(mc - M);
+        L += w * ml[(static_cast<size_t>(c) * rows + rr) * 2 + 1];
+        acc += w * opart[(static_cast<size_t>(c) * rows + rr) * hd + d];
+      }
+    }
+    out[static_cast<size_t>(rr) * hd + d] = __float2bfloat16_rn(L > 0.f ? acc / L : 0.f);
+  }
+}
+
+static int encode(CUtensorMap* map, int rank, const void* ptr, const cuuint64_t* dims, const cuuint64_t* strides,
+                  const cuuint32_t* box) {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return ygg_fail(YGG_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+    fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  cuuint32_t es[3] = {1, 1, 1};
+  CUresult rc = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank, const_cast<void*>(ptr), dims, strides, box, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (rc != CUDA_SUCCESS) return ygg_fail(YGG_ERR_CUDA, "attention tensor map encode failed (%d)", static_cast<int>(rc));
+  return YGG_OK;
+}
+
+template <int HD>
+size_t attn_smem() {
+  return 1024 + (HD / 64) * kQRows * 128 + (HD / 64) * kKC * 128 + (kKC / 64) * HD * 128 + (kKC / 64) * kQRows * 128 +
+         64;
+}
+
+static const AttnPlan* attn_plan_of(const void* p) {
+  const AttnPlan* a = reinterpret_cast<const AttnPlan*>((reinterpret_cast<uintptr_t>(p) + 63) & ~uintptr_t(63));
+  return (a && a->magic == kAttnMagic) ? a : nullptr;
+}
+
+}  // namespace ygg
+
+using namespace ygg;
+
+extern "C" {
+
+int ygg_prepare_attn_tc(void) {
+  cudaError_t e = cudaFuncSetAttribute(attn_tc_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(attn_tc_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  if (e != cudaSuccess) return ygg_fail(YGG_ERR_CUDA, "attention attribute: %s", cudaGetErrorString(e));
+  return YGG_OK;
+}
+
+size_t ygg_attn_plan_size(void) { return sizeof(AttnPlan) + 64; }
+
+/* q [M, Hq, hd] bf16; cache_layer = this layer's [B, 2, Hkv, S, hd] block (K rows, V^T rows). */
+int ygg_attn_plan_init(void* plan_mem, const void* q, const void* cache_layer, int B, int M, int Hq, int Hkv, int hd,
+                       int S, size_t* partial_bytes) {
+  YGG_CHECK_ARG(plan_mem && q && cache_layer, "null pointer");
+  YGG_CHECK_ARG(hd == 64 || hd == 128, "head dim must be 64 or 128");
+  YGG_CHECK_ARG(Hkv >= 1 && Hq % Hkv == 0, "bad head grouping");
+  const int G = Hq / Hkv;
+  YGG_CHECK_ARG(kQRows % G == 0, "group size must divide 128");
+  YGG_CHECK_ARG(B >= 1 && M % B == 0, "rows must split evenly over requests");
+  YGG_CHECK_ARG(S % 64 == 0, "cache capacity must be a multiple of 64");
+  AttnPlan* p = reinterpret_cast<AttnPlan*>((reinterpret_cast<uintptr_t>(plan_mem) + 63) & ~uintptr_t(63));
+  std::memset(p, 0, sizeof(AttnPlan));
+  p->magic = kAttnMagic;
+  p->B = B;
+  p->M = M;
+  p->Hq = Hq;
+  p->Hkv = Hkv;
+  p->hd = hd;
+  p->S = S;
+  p->T = M / B;
+  p->G = G;
+  p->tok_per_tile = kQRows / G;
+  p->q_tiles = (p->T + p->tok_per_tile - 1) / p->tok_per_tile;
+  p->chunks = (S + kKC - 1) / kKC;
+  {
+    cuuint64_t dims[3] = {static_cast<cuuint64_t>(hd), static_cast<cuuint64_t>(Hq), static_cast<cuuint64_t>(M)};
+    cuuint64_t str[2] = {static_cast<cuuint64_t>(hd) * 2, static_cast<cuuint64_t>(Hq) * hd * 2};
+    cuuint32_t box[3] = {64, static_cast<cuuint32_t>(G), static_cast<cuuint32_t>(p->tok_per_tile)};
+    if (int rc = encode(&p->tm_q, 3, q, dims, str, box)) return rc;
+  }
+  {
+    cuuint64_t dims[2] = {static_cast<cuuint64_t>(hd), static_cast<cuuint64_t>(B) * 2 * Hkv * S};
+    cuuint64_t str[1] = {static_cast<cuuint64_t>(hd) * 2};
+    cuuint32_t box[2] = {64, static_cast<cuuint32_t>(kKC)};
+    if (int rc = encode(&p->tm_k, 2, cache_layer, dims, str, box)) return rc;
+  }
+  {
+    cuuint64_t dims[2] = {static_cast<cuuint64_t>(S), static_cast<cuuint64_t>(B) * 2 * Hkv * hd};
+    cuuint64_t str[1] = {static_cast<cuuint64_t>(S) * 2};
+    cuuint32_t box[2] = {64, static_cast<cuuint32_t>(hd)};
+    if (int rc = encode(&p->tm_vt, 2, cache_layer, dims, str, box)) return rc;
+  }
+  if (partial_bytes) *partial_bytes = static_cast<size_t>(p->chunks) * M * Hq * (hd + 2) * sizeof(float);
+  return YGG_OK;
+}
+
+int ygg_attention_tc(const void* plan, const int32_t* blk_start, const int32_t* blk_len, const uint32_t* qmask,
+                     int mask_words, float scale, float* partials, void* out, ygg_stream_t stream) {
+  const AttnPlan* p = attn_plan_of(plan);
+  YGG_CHECK_ARG(p != nullptr, "invalid attention plan");
+  YGG_CHECK_ARG(blk_start && blk_len && partials && out, "null pointer");
+  YGG_CHECK_ARG(mask_words >= 0 && mask_words <= YGG_MAX_MASK_WORDS, "mask too wide for the tcgen05 path");
+  YGG_CHECK_ARG(mask_words == 0 || qmask != nullptr, "mask words without a mask");
+  AttnArgs a;
+  a.M = p->M;
+  a.Hq = p->Hq;
+  a.Hkv = p->Hkv;
+  a.hd = p->hd;
+  a.S = p->S;
+  a.T = p->T;
+  a.G = p->G;
+  a.tok_per_tile = p->tok_per_tile;
+  a.chunks = p->chunks;
+  a.mask_words = mask_words;
+  a.scale_log2 = scale * 1.4426950408889634f;
+  a.blk_start = blk_start;
+  a.blk_len = blk_len;
+  a.qmask = qmask;
+  a.opart = partials;
+  a.ml = partials + static_cast<size_t>(p->chunks) * p->M * p->Hq * p->hd;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  dim3 grid(p->chunks, p->q_tiles, p->Hkv * p->B);
+  if (p->hd == 64)
+    YGG_LAUNCH_PDL(attn_tc_kernel<64>, grid, dim3(kAttnTcThreads), attn_smem<64>(), s, p->tm_q, p->tm_k, p->tm_vt, a);
+  else
+    YGG_LAUNCH_PDL(attn_tc_kernel<128>, grid, dim3(kAttnTcThreads), attn_smem<128>(), s, p->tm_q, p->tm_k, p->tm_vt,
+                   a);
+  YGG_LAUNCH_PDL(attn_combine_kernel, dim3(p->M * p->Hq), dim3(p->hd), 0, s, static_cast<const float*>(a.opart),
+                 static_cast<const float*>(a.ml), p->chunks, p->M * p->Hq, p->hd, static_cast<__nv_bfloat16*>(out));
+  return YGG_OK;
+}
+
+}  // extern "C"

@@ -160,7 +160,8 @@ __global__ void verify_inputs_kernel(ygg_tree t, ygg_seq seq, int32_t* tokens, i
 // Commit an accepted path: append the accepted tokens + bonus to the history, advance P,
 // record accepted_len (lagged host readback feeds the depth predictor).
 __global__ void commit_kernel(ygg_seq seq, ygg_tree vt, const int32_t* __restrict__ path,
-                              const int32_t* __restrict__ path_len, const int32_t* __restrict__ bonus) {
+                              const int32_t* __restrict__ path_len, const int32_t* __restrict__ bonus,
+                              int32_t* __restrict__ emit, int emit_cap) {
   pdl_wait();
   pdl_launch_dependents();
   const int b = threadIdx.x;
@@ -172,6 +173,11 @@ __global__ void commit_kernel(ygg_seq seq, ygg_tree vt, const int32_t* __restric
     int32_t* h = seq.hist + static_cast<size_t>(b) * seq.S;
     for (int i = 0; i < a; ++i) h[P + 1 + i] = vt.token[tb + path[tb + i]];
     h[P + 1 + a] = bonus[b];
+    if (emit) {  // per-step emitted tokens for host streaming: [count, tokens...]
+      int32_t* em = emit + static_cast<size_t>(b) * emit_cap;
+      em[0] = 1 + a;
+      for (int i = 0; i < emit_cap - 1; ++i) em[1 + i] = (i <= a) ? h[P + 1 + i] : -1;
+    }
     seq.P[b] = P + 1 + a;
     seq.n_gen[b] += 1 + a;
     if (seq.acc_log && seq.log_cap > 0)
@@ -221,11 +227,11 @@ int ygg_verify_inputs(ygg_tree vtree, ygg_seq seq, int32_t* tokens, int32_t* pos
 }
 
 int ygg_commit(ygg_seq seq, ygg_tree vtree, const int32_t* path, const int32_t* path_len, const int32_t* bonus,
-               ygg_stream_t stream) {
+               int32_t* emit, int emit_cap, ygg_stream_t stream) {
   YGG_CHECK_ARG(path && path_len && bonus, "invalid arguments");
   YGG_CHECK_ARG(seq.B <= 1024, "too many requests");
   YGG_LAUNCH_PDL(commit_kernel, dim3(1), dim3(seq.B), 0, reinterpret_cast<cudaStream_t>(stream), seq, vtree, path,
-                 path_len, bonus);
+                 path_len, bonus, emit, emit_cap);
   return YGG_OK;
 }
 

@@ -376,10 +376,15 @@ __global__ void epi_qkv_rope_kernel(EpiGeom g, const float* __restrict__ ws, int
     } else {
       const bool is_v = head >= Hq + Hkv;
       const int kvh = is_v ? head - Hq - Hkv : head - Hq;
-      const size_t off = ((static_cast<size_t>(req[m]) * 2 + (is_v ? 1 : 0)) * Hkv + kvh) * static_cast<size_t>(S) * hd +
-                         static_cast<size_t>(slot[m]) * hd;
-      cache[off + i] = from_f32<ActT>(x1);
-      cache[off + i + half] = from_f32<ActT>(x2);
+      const size_t base = ((static_cast<size_t>(req[m]) * 2 + (is_v ? 1 : 0)) * Hkv + kvh) * static_cast<size_t>(S) * hd;
+      if (!is_v) {  // K rows: [S][hd]
+        const size_t off = base + static_cast<size_t>(slot[m]) * hd;
+        cache[off + i] = from_f32<ActT>(x1);
+        cache[off + i + half] = from_f32<ActT>(x2);
+      } else {      // V transposed: [hd][S], so attention reads K-major V^T tiles
+        cache[base + static_cast<size_t>(i) * S + slot[m]] = from_f32<ActT>(x1);
+        cache[base + static_cast<size_t>(i + half) * S + slot[m]] = from_f32<ActT>(x2);
+      }
     }
   }
 }

@@ -98,7 +98,7 @@ __global__ void __launch_bounds__(kAttnThreads) attn_simt_kernel(
       float kv = 0.f, vv = 0.f;
       if (key < nkeys) {
         kv = to_f32(kbase[static_cast<size_t>(key) * HD + dd]);
-        vv = to_f32(vbase[static_cast<size_t>(key) * HD + dd]);
+        vv = to_f32(vbase[static_cast<size_t>(dd) * S + key]);  // V^T [hd][S]
       }
       sk[kk][dd] = kv;
       sv[kk][dd] = vv;

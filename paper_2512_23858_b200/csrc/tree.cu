@@ -689,6 +689,10 @@ __global__ void kv_compact_kernel(T* cache, int B, int Hkv, int S, int hd, long 
   const int n = path_len[b];
   if (n <= 0) return;
   T* head = cache + layer * layer_stride + (static_cast<size_t>(b) * 2 * Hkv + kvh) * static_cast<size_t>(S) * hd;
+  // K rows are [S][hd]; V is stored transposed [hd][S] (see attn_tc.cu).
+  const bool vt = kvh >= Hkv;
+  const size_t s_stride = vt ? 1 : static_cast<size_t>(hd);
+  const size_t d_stride = vt ? static_cast<size_t>(S) : 1;
   const int p0 = base[b] + 1;
   constexpr int kMaxPath = 64;
   for (int d = threadIdx.x; d < hd; d += blockDim.x) {
@@ -700,11 +704,11 @@ __global__ void kv_compact_kernel(T* cache, int B, int Hkv, int S, int hd, long 
       const int src_node = keep_idx ? keep_idx[static_cast<size_t>(b) * keep_cap + node] : node;
       if (node_depth && node_depth[static_cast<size_t>(b) * depth_cap + src_node] >= skip_depth) continue;
       if (src_node == i) continue;
-      vals[m] = head[static_cast<size_t>(p0 + src_node) * hd + d];
+      vals[m] = head[static_cast<size_t>(p0 + src_node) * s_stride + d * d_stride];
       dst[m] = p0 + i;
       ++m;
     }
-    for (int j = 0; j < m; ++j) head[static_cast<size_t>(dst[j]) * hd + d] = vals[j];
+    for (int j = 0; j < m; ++j) head[static_cast<size_t>(dst[j]) * s_stride + d * d_stride] = vals[j];
   }
 }
 

@@ -77,7 +77,7 @@ class SpecDecoder:
         self.T = self.vcap + 1
         self.R = max(W, 2)
         scratch = self.tree_cap + self.R + 8
-        self.S = max_seq + scratch
+        self.S = (max_seq + scratch + 63) // 64 * 64
         dev = torch.device(device)
         self.dev = dev
         self.seq = SeqState(batch, self.S, device=dev)
@@ -108,6 +108,7 @@ class SpecDecoder:
         self.path_len = torch.zeros(batch, **i32)
         self.acc_len = torch.zeros(batch, **i32)
         self.bonus = torch.zeros(batch, **i32)
+        self.emit = torch.zeros(batch, D + 3, **i32)
         self.n_uniform = D + 3
         self.uniforms = torch.full((batch, self.n_uniform), 0.5, **f64)
         self.uniforms_host = torch.full((batch, self.n_uniform), 0.5, dtype=torch.float64).pin_memory()
@@ -171,7 +172,12 @@ class SpecDecoder:
         self.seq.step.zero_()
 
     # ------------------------------------------------------------------
-    def _launch_step(self, stream=None) -> None:
+    def _launch_step(self, stream=None, stamp=None) -> None:
+        """Enqueue one step.  ``stamp(i)`` (K8 profiler) is called at the stage boundaries
+        0 | pass0 | 1 | draft levels | 2 | prune | 3 | verify forward | 4 | accept+compact+commit | 5."""
+        if stamp is None:
+            stamp = lambda i: None  # noqa: E731
+        stamp(0)
         lib = L.lib()
         s = L.stream_ptr(stream)
         chk = L.check
@@ -188,6 +194,7 @@ class SpecDecoder:
                                  self.cand_tok.data_ptr(), self.cand_prob.data_ptr(), None, self.topk_ws.data_ptr(),
                                  self.topk_ws.numel(), s))
         chk(lib.ygg_init_roots(g.struct, self.cand_tok.data_ptr(), self.cand_prob.data_ptr(), k, self.R, 1, s))
+        stamp(1)
         # ---- draft passes 1..D: grow one level each
         for _ in range(D):
             chk(lib.ygg_level_inputs(g.struct, self.seq.struct, self.R, k, dr.tokens.data_ptr(), dr.pos.data_ptr(),
@@ -199,17 +206,20 @@ class SpecDecoder:
                                      self.topk_ws.data_ptr(), self.topk_ws.numel(), s))
             chk(lib.ygg_egt_grow_level(g.struct, self.R, k, W, self.cand_tok.data_ptr(), self.cand_prob.data_ptr(),
                                        self.cand_n.data_ptr(), s))
+        stamp(2)
         # ---- prune (latency-aware objective or fixed width)
         args = L.YggPruneArgs(sh.max_verify, D, W, sh.fixed_verify)
         chk(lib.ygg_knapsack_prune(g.struct, None, self.profiles_dev.data_ptr(), args, self.keep_idx.data_ptr(),
                                    self.new_idx.data_ptr(), self.w_verify.data_ptr(), self.exp_aal.data_ptr(),
                                    self.speedup.data_ptr(), None, None, None, None, s))
         chk(lib.ygg_tree_subtree(g.struct, vt.struct, self.keep_idx.data_ptr(), self.new_idx.data_ptr(), s))
+        stamp(3)
         # ---- verify
         chk(lib.ygg_verify_inputs(vt.struct, self.seq.struct, vf.tokens.data_ptr(), vf.pos.data_ptr(),
                                   vf.slot.data_ptr(), vf.req.data_ptr(), vf.qmask.data_ptr(), vf.mask_words,
                                   vf.blk_start.data_ptr(), vf.blk_len.data_ptr(), s))
         vf.run(stream)
+        stamp(4)
         nrows = self.B * self.T
         if self.mode == GREEDY:
             chk(lib.ygg_row_stats(vf.logits.data_ptr(), L.YGG_F32, nrows, self.tc.vocab, self.tc.vocab, 1.0,
@@ -235,7 +245,8 @@ class SpecDecoder:
                                self.path.data_ptr(), self.path_len.data_ptr(), self.vcap, self.keep_idx.data_ptr(),
                                self.tree_cap, g.depth.data_ptr(), self.tree_cap, D, s))
         chk(lib.ygg_commit(self.seq.struct, vt.struct, self.path.data_ptr(), self.path_len.data_ptr(),
-                           self.bonus.data_ptr(), s))
+                           self.bonus.data_ptr(), self.emit.data_ptr(), self.emit.shape[1], s))
+        stamp(5)
 
     # ------------------------------------------------------------------
     def set_uniforms(self, step_index: int, seed: int) -> None:
@@ -266,6 +277,10 @@ class SpecDecoder:
         else:
             self._launch_step()
         self.step_count += 1
+
+    def read_emitted(self, host_out: torch.Tensor) -> None:
+        """Async D2H of this step's emitted tokens ([count, tokens...] per request) into pinned memory."""
+        host_out.copy_(self.emit, non_blocking=True)
 
     def generated(self, b: int = 0) -> list[int]:
         P0 = self.prefill_len
@@ -298,7 +313,7 @@ class ARDecoder:
                  act_dtype: torch.dtype = torch.bfloat16, device="cuda"):
         L.require_device()
         self.cfg, self.w, self.B = cfg, w, batch
-        self.S = max_seq + 8
+        self.S = (max_seq + 8 + 63) // 64 * 64
         self.act_dtype = act_dtype
         self.dev = torch.device(device)
         self.cache = new_cache(cfg, batch, self.S, act_dtype, self.dev)

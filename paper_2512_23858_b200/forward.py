@@ -51,6 +51,22 @@ class GemmPlan:
         return self._mem
 
 
+class AttnPlan:
+    """TMA tensor maps for the tcgen05 split-KV attention over one layer's cache."""
+
+    def __init__(self, q: torch.Tensor, cache_layer_ptr: int, B: int, M: int, cfg: ModelConfig, S: int):
+        lib = L.lib()
+        self._mem = C.create_string_buffer(int(lib.ygg_attn_plan_size()))
+        pb = C.c_size_t()
+        L.check(lib.ygg_attn_plan_init(self._mem, q.data_ptr(), cache_layer_ptr, B, M, cfg.n_heads,
+                                       cfg.n_kv_heads, cfg.head_dim, S, C.byref(pb)))
+        self.partial_bytes = pb.value
+
+    @property
+    def handle(self):
+        return self._mem
+
+
 class Forward:
     def __init__(
         self,
@@ -105,6 +121,13 @@ class Forward:
         self.ws = torch.empty(max(ws // 4, 1), dtype=torch.float32, device=dev)
         self.layer_stride = cache.stride(0)
         self.S = cache.shape[4]
+        # bf16: tcgen05 split-KV attention (one plan per layer); f32 parity path: SIMT attention.
+        self.attn_plans = None
+        if act_dtype == torch.bfloat16 and mask_words <= L.MAX_MASK_WORDS:
+            es = cache.element_size()
+            self.attn_plans = [AttnPlan(self.q, cache.data_ptr() + li * self.layer_stride * es, B, M, cfg, self.S)
+                               for li in range(cfg.n_layers)]
+            self.attn_part = torch.empty(self.attn_plans[0].partial_bytes // 4 + 1, dtype=torch.float32, device=dev)
         self.scale = 1.0 / math.sqrt(cfg.head_dim)
         # stage hooks: optional callables(stage_name, stream) for the on-device profiler (K8)
         self.hooks = None
@@ -137,10 +160,15 @@ class Forward:
             chk(lib.ygg_epi_qkv_rope(p["qkv"].handle, ws, cfg.n_heads, cfg.n_kv_heads, cfg.head_dim,
                                      cfg.rope_theta, self.pos.data_ptr(), self.slot.data_ptr(),
                                      self.req.data_ptr(), self.q.data_ptr(), cache_l, self.S, self.act, s))
-            chk(lib.ygg_attention(self.q.data_ptr(), cache_l, self.act, M, self.B, cfg.n_heads, cfg.n_kv_heads,
-                                  cfg.head_dim, self.S, self.blk_start.data_ptr(), self.blk_len.data_ptr(),
-                                  self.qmask.data_ptr() if self.mask_words > 0 else None, self.mask_words,
-                                  self.scale, self.attn.data_ptr(), s))
+            qm = self.qmask.data_ptr() if self.mask_words > 0 else None
+            if self.attn_plans is not None:
+                chk(lib.ygg_attention_tc(self.attn_plans[li].handle, self.blk_start.data_ptr(),
+                                         self.blk_len.data_ptr(), qm, self.mask_words, self.scale,
+                                         self.attn_part.data_ptr(), self.attn.data_ptr(), s))
+            else:
+                chk(lib.ygg_attention(self.q.data_ptr(), cache_l, self.act, M, self.B, cfg.n_heads, cfg.n_kv_heads,
+                                      cfg.head_dim, self.S, self.blk_start.data_ptr(), self.blk_len.data_ptr(),
+                                      qm, self.mask_words, self.scale, self.attn.data_ptr(), s))
             chk(lib.ygg_gemm_run(p["o"].handle, ws, s))
             chk(lib.ygg_epi_residual_norm(p["o"].handle, ws, self.resid.data_ptr(), lw["mlp_norm"].data_ptr(),
                                           cfg.norm_eps, self.xn.data_ptr(), self.act, s))
@@ -156,5 +184,8 @@ class Forward:
 
 
 def new_cache(cfg: ModelConfig, B: int, S: int, dtype: torch.dtype, device) -> torch.Tensor:
-    """KV cache [layers, B, 2 (k|v), Hkv, S, hd] — per-(request, head) contiguous key streams."""
+    """KV cache [layers, B, 2, Hkv, S, hd]: the kv=0 half holds K rows [S][hd] (per-head contiguous key
+    streams); the kv=1 half holds V transposed, [hd][S], so both attention MMAs read K-major tiles.
+    S is rounded up to a multiple of 64 (TMA row alignment)."""
+    S = (S + 63) // 64 * 64
     return torch.zeros(cfg.n_layers, B, 2, cfg.n_kv_heads, S, cfg.head_dim, dtype=dtype, device=device)

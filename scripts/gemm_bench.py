@@ -41,6 +41,7 @@ for name, (N, K) in shapes.items():
         e1.record()
         torch.cuda.synchronize()
         us = e0.elapsed_time(e1) * 1e3 / reps
+        L.check(lib.ygg_gemm_run(plans[0].handle, ws.data_ptr(), s))
         out = torch.zeros(M, N, device="cuda")
         L.check(lib.ygg_epi_store(plans[0].handle, ws.data_ptr(), out.data_ptr(), L.YGG_F32, N, s))
         ref = X.float() @ Ws[0].float().T

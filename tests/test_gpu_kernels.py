@@ -62,20 +62,26 @@ def test_gemm_f32_simt(M, N, K, cuda):
 # ---------------------------------------------------------------------------
 # K2 attention (bitmask / causal) vs a torch fp32 reference
 # ---------------------------------------------------------------------------
-@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+@pytest.mark.parametrize("path", ["simt_f32", "simt_bf16", "tc_bf16"])
 @pytest.mark.parametrize("hd,Hq,Hkv", [(64, 4, 2), (128, 32, 8), (64, 32, 8)])
 @pytest.mark.parametrize("causal", [False, True])
-def test_attention(dtype, hd, Hq, Hkv, causal, cuda):
+@pytest.mark.parametrize("T", [19, 50])
+def test_attention(path, hd, Hq, Hkv, causal, T, cuda):
+    """Cache layout: kv=0 half K [Hkv][S][hd], kv=1 half V^T [Hkv][hd][S]."""
+    from paper_2512_23858_b200.forward import AttnPlan
+    from paper_2512_23858_b200.model import preset
+
     L = _lib()
-    B, T, S = 2, 19, 160
-    g = torch.Generator(device="cuda").manual_seed(hd + Hq)
+    dtype = torch.float32 if path == "simt_f32" else torch.bfloat16
+    B, S = 2, 320
+    g = torch.Generator(device="cuda").manual_seed(hd + Hq + T)
     q = torch.randn(B * T, Hq, hd, device=cuda, generator=g).to(dtype)
     cache = torch.randn(B, 2, Hkv, S, hd, device=cuda, generator=g).to(dtype)
-    blk_start = torch.tensor([37, 90], dtype=torch.int32, device=cuda)
+    blk_start = torch.tensor([37, 190], dtype=torch.int32, device=cuda)
     blk_len = torch.tensor([T, T], dtype=torch.int32, device=cuda)
-    mw = 1
+    mw = (T + 31) // 32
     rng = np.random.default_rng(3)
-    masks = torch.zeros(B * T, mw, dtype=torch.int32)
+    masks = torch.zeros(B * T, mw, dtype=torch.int64)
     vis = torch.zeros(B * T, S, dtype=torch.bool)
     for b in range(B):
         for i in range(T):
@@ -86,31 +92,43 @@ def test_attention(dtype, hd, Hq, Hkv, causal, cuda):
                         bits |= 1 << j
             else:
                 bits = (1 << (i + 1)) - 1
-            masks[b * T + i, 0] = np.int32(np.uint32(bits).view(np.int32))
+            for w in range(mw):
+                masks[b * T + i, w] = (bits >> (32 * w)) & 0xFFFFFFFF
             vis[b * T + i, : int(blk_start[b])] = True
             for j in range(T):
                 if (bits >> j) & 1:
                     vis[b * T + i, int(blk_start[b]) + j] = True
+    masks_d = torch.from_numpy(masks.numpy().astype(np.uint32).view(np.int32)).to(cuda)
     out = torch.zeros(B * T, Hq * hd, device=cuda, dtype=dtype)
     scale = 1.0 / math.sqrt(hd)
-    L.check(L.lib().ygg_attention(q.data_ptr(), cache.data_ptr(), L.dtype_code(dtype), B * T, B, Hq, Hkv, hd, S,
-                                  blk_start.data_ptr(), blk_len.data_ptr(),
-                                  None if causal else masks.to(cuda).data_ptr(), 0 if causal else mw, scale,
-                                  out.data_ptr(), L.stream_ptr()))
+    qm = None if causal else masks_d.data_ptr()
+    nw = 0 if causal else mw
+    if path == "tc_bf16":
+        cfg = preset("tiny-target", n_heads=Hq, n_kv_heads=Hkv, head_dim=hd)
+        plan = AttnPlan(q, cache.data_ptr(), B, B * T, cfg, S)
+        part = torch.empty(plan.partial_bytes // 4 + 1, device=cuda)
+        L.check(L.lib().ygg_attention_tc(plan.handle, blk_start.data_ptr(), blk_len.data_ptr(), qm, nw, scale,
+                                         part.data_ptr(), out.data_ptr(), L.stream_ptr()))
+    else:
+        L.check(L.lib().ygg_attention(q.data_ptr(), cache.data_ptr(), L.dtype_code(dtype), B * T, B, Hq, Hkv, hd, S,
+                                      blk_start.data_ptr(), blk_len.data_ptr(), qm, nw, scale, out.data_ptr(),
+                                      L.stream_ptr()))
     torch.cuda.synchronize()
     G = Hq // Hkv
     ref = torch.zeros(B * T, Hq, hd, dtype=torch.float64)
     qc, cc = q.double().cpu(), cache.double().cpu()
     for b in range(B):
         K = cc[b, 0].repeat_interleave(G, 0)
-        V = cc[b, 1].repeat_interleave(G, 0)
+        V = cc[b, 1].reshape(Hkv, hd, S).transpose(1, 2).repeat_interleave(G, 0)
         rows = slice(b * T, (b + 1) * T)
         sc = torch.einsum("thd,hsd->hts", qc[rows], K) * scale
         sc = sc.masked_fill(~vis[rows][None], -math.inf)
         p = torch.softmax(sc, -1)
         ref[rows] = torch.einsum("hts,hsd->thd", p, V)
-    tol = 2e-5 if dtype == torch.float32 else 2e-2
-    assert torch.allclose(out.double().cpu().view(B * T, Hq, hd), ref, atol=tol, rtol=tol)
+    # bf16: P is rounded to bf16 before P.V on the tensor-core path (|O| <~ 4 here)
+    tol = 2e-5 if dtype == torch.float32 else 3e-2
+    got = out.double().cpu().view(B * T, Hq, hd)
+    assert torch.allclose(got, ref, atol=tol, rtol=tol), (got - ref).abs().max().item()
 
 
 # ---------------------------------------------------------------------------
@@ -181,8 +199,10 @@ def test_grow_levels_match_oracle(seed, cuda):
                 cn[b, f] = len(cl)
                 for j, (t, p) in enumerate(cl):
                     ctok[b, f, j], cprob[b, f, j] = t, p
-        L.check(L.lib().ygg_egt_grow_level(dt.struct, Fmax, k, W, ctok.cuda().data_ptr(), cprob.cuda().data_ptr(),
-                                           cn.cuda().data_ptr(), L.stream_ptr()))
+        ctok_d, cprob_d, cn_d = ctok.cuda(), cprob.cuda(), cn.cuda()  # keep alive across the async launch
+        L.check(L.lib().ygg_egt_grow_level(dt.struct, Fmax, k, W, ctok_d.data_ptr(), cprob_d.data_ptr(),
+                                           cn_d.data_ptr(), L.stream_ptr()))
+        torch.cuda.synchronize()
         for b, r in enumerate(refs):
             if not stopped[b]:  # grow_egt stops after a level that added nothing (egt.py:145-146)
                 stopped[b] = not T.grow_step(r, lambda tr, node, kk, b=b: per[b][node], W, k)
@@ -259,7 +279,8 @@ def test_knapsack_prune_matches_oracle(seed, cuda):
     aal_cap = torch.zeros_like(aal)
     sp_cap = torch.zeros_like(aal)
     args = L.YggPruneArgs(max_verify, d_draft, w_draft, 0)
-    L.check(L.lib().ygg_knapsack_prune(dt.struct, probs.cuda().data_ptr(), pp.data_ptr(), args, keep.data_ptr(),
+    probs_d = probs.cuda()
+    L.check(L.lib().ygg_knapsack_prune(dt.struct, probs_d.data_ptr(), pp.data_ptr(), args, keep.data_ptr(),
                                        new.data_ptr(), wv.data_ptr(), aal.data_ptr(), sp.data_ptr(),
                                        aal_cap.data_ptr(), sp_cap.data_ptr(), None, None, L.stream_ptr()))
     torch.cuda.synchronize()
@@ -296,7 +317,8 @@ def test_accept_probs_matches_oracle(seed, cuda):
     plen = torch.zeros(B, **i32)
     alen = torch.zeros(B, **i32)
     nd = torch.zeros(B, **i32)
-    L.check(L.lib().ygg_accept(dt.struct, L.YGG_ACCEPT_PROBS, probs.cuda().data_ptr(), uni.cuda().data_ptr(), nu,
+    probs_d, uni_d = probs.cuda(), uni.cuda()
+    L.check(L.lib().ygg_accept(dt.struct, L.YGG_ACCEPT_PROBS, probs_d.data_ptr(), uni_d.data_ptr(), nu,
                                None, None, 0, 0, 0, None, 1.0, path.data_ptr(), plen.data_ptr(), alen.data_ptr(),
                                None, nd.data_ptr(), L.stream_ptr()))
     torch.cuda.synchronize()
@@ -341,7 +363,8 @@ def test_accept_greedy_and_kv_compact(cuda):
     plen = torch.zeros(B, **i32)
     alen = torch.zeros(B, **i32)
     bonus = torch.zeros(B, **i32)
-    L.check(L.lib().ygg_accept(dt.struct, L.YGG_ACCEPT_GREEDY, None, None, 0, argmax.cuda().data_ptr(), None, 0, 0, 0,
+    argmax_d = argmax.cuda()
+    L.check(L.lib().ygg_accept(dt.struct, L.YGG_ACCEPT_GREEDY, None, None, 0, argmax_d.data_ptr(), None, 0, 0, 0,
                                None, 1.0, path.data_ptr(), plen.data_ptr(), alen.data_ptr(), bonus.data_ptr(), None,
                                L.stream_ptr()))
     torch.cuda.synchronize()
@@ -359,10 +382,13 @@ def test_accept_greedy_and_kv_compact(cuda):
                                    path.data_ptr(), plen.data_ptr(), cap, None, 0, None, 0, 0, L.stream_ptr()))
     torch.cuda.synchronize()
     exp = before.clone()
+    kx, vx = exp[:, :, 0], exp[:, :, 1].view(Ly, B, Hkv, hd, S)  # K [S][hd]; V^T [hd][S]
+    kb, vb = before[:, :, 0], before[:, :, 1].view(Ly, B, Hkv, hd, S)
     for b in range(B):
         p = path[b, : int(plen[b])].tolist()
         src = [int(base[b]) + 1 + n for n in p]
         dst = [int(base[b]) + 1 + i for i in range(len(p))]
         if src:
-            exp[:, b, :, :, dst] = before[:, b, :, :, src]
+            kx[:, b, :, dst] = kb[:, b, :, src]
+            vx[:, b, :, :, dst] = vb[:, b, :, :, src]
     assert torch.equal(cache, exp)

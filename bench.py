@@ -40,7 +40,7 @@ WORKLOADS = {
 }
 # Coupled synthetic weights (paper_2512_23858_b200/model.py): shared semantic table + permutation.
 COUPLING = {
-    "cfg2": dict(rank=2048, logit_scale=16.0, head_noise=2.0, layer_gain=2.0),
+    "cfg2": dict(rank=2048, logit_scale=16.0, head_noise=6.0, layer_gain=2.0),
     "cfg1": dict(rank=256, logit_scale=8.0, head_noise=2.0, layer_gain=2.0),
 }
 DRAFT_PROF = ((1, 400.0), (64, 420.0), (128, 460.0))    # placeholder Eq.3 table (us); refreshed by K8
@@ -123,7 +123,7 @@ def build_decoder(wl: dict, name: str, device, seed_offset: int = 0):
             breakpoints = VERIFY_PROF
 
     shape = StepShape(wl["depth"], wl["width"], wl["k"], wl["max_verify"])
-    max_seq = wl["prompt"] + 64 * 1024 // 64 + 2048
+    max_seq = wl["prompt"] + 2048  # room for ~250 steps of up to D+2 tokens
     sd = SpecDecoder(tc, tw, dc, dw, shape, batch=wl["batch"], max_seq=max_seq, act_dtype=torch.bfloat16,
                      profiles=PP, device=device)
     return sd, tc, dc

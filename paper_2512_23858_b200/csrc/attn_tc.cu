@@ -246,26 +246,42 @@ __global__ void __launch_bounds__(kAttnTcThreads, 1)
 }
 
 // Merge chunk partials in fixed chunk order: out = sum_c 2^(m_c - M) O_c / sum_c 2^(m_c - M) l_c.
-__global__ void attn_combine_kernel(const float* __restrict__ opart, const float* __restrict__ ml, int chunks,
-                                    int rows, int hd, __nv_bfloat16* __restrict__ out) {
+// One warp per (query row, head); only the chunks holding the request's keys are read.
+template <int HD>
+__global__ void __launch_bounds__(128) attn_combine_kernel(const float* __restrict__ opart,
+                                                           const float* __restrict__ ml, int rows, int Hq, int T,
+                                                           const int32_t* __restrict__ blk_start,
+                                                           const int32_t* __restrict__ blk_len,
+                                                           __nv_bfloat16* __restrict__ out) {
   pdl_wait();
   pdl_launch_dependents();
-  const int rr = blockIdx.x;  // m*Hq + head
+  const int rr = blockIdx.x * 4 + (threadIdx.x >> 5);  // m*Hq + head
+  const int lane = threadIdx.x & 31;
+  if (rr >= rows) return;
+  const int req = (rr / Hq) / T;
+  const int nch = (blk_start[req] + blk_len[req] + kKC - 1) / kKC;
+  constexpr int DPL = HD / 32;
   float M = -INFINITY;
-  for (int c = 0; c < chunks; ++c) M = fmaxf(M, ml[(static_cast<size_t>(c) * rows + rr) * 2]);
-  for (int d = threadIdx.x; d < hd; d += blockDim.x) {
-    float acc = 0.f, L = 0.f;
-    if (M != -INFINITY) {
-      for (int c = 0; c < chunks; ++c) {
-        const float mc = ml[(static_cast<size_t>(c) * rows + rr) * 2];
-        if (mc == -INFINITY) continue;
-        const float w = exp2f(mc - M);
-        L += w * ml[(static_cast<size_t>(c) * rows + rr) * 2 + 1];
-        acc += w * opart[(static_cast<size_t>(c) * rows + rr) * hd + d];
-      }
+  for (int c = 0; c < nch; ++c) M = fmaxf(M, __ldg(ml + (static_cast<size_t>(c) * rows + rr) * 2));
+  float acc[DPL];
+#pragma unroll
+  for (int i = 0; i < DPL; ++i) acc[i] = 0.f;
+  float L = 0.f;
+  if (M != -INFINITY) {
+    for (int c = 0; c < nch; ++c) {
+      const float mc = __ldg(ml + (static_cast<size_t>(c) * rows + rr) * 2);
+      if (mc == -INFINITY) continue;
+      const float w = exp2f(mc - M);
+      L += w * __ldg(ml + (static_cast<size_t>(c) * rows + rr) * 2 + 1);
+      const float* o = opart + (static_cast<size_t>(c) * rows + rr) * HD + lane * DPL;
+#pragma unroll
+      for (int i = 0; i < DPL; ++i) acc[i] += w * __ldg(o + i);
     }
-    out[static_cast<size_t>(rr) * hd + d] = __float2bfloat16_rn(L > 0.f ? acc / L : 0.f);
   }
+  const float inv = L > 0.f ? 1.f / L : 0.f;
+  __nv_bfloat16* dst = out + static_cast<size_t>(rr) * HD + lane * DPL;
+#pragma unroll
+  for (int i = 0; i < DPL; ++i) dst[i] = __float2bfloat16_rn(acc[i] * inv);
 }
 
 static int encode(CUtensorMap* map, int rank, const void* ptr, const cuuint64_t* dims, const cuuint64_t* strides,
@@ -391,8 +407,15 @@ int ygg_attention_tc(const void* plan, const int32_t* blk_start, const int32_t* 
   else
     YGG_LAUNCH_PDL(attn_tc_kernel<128>, grid, dim3(kAttnTcThreads), attn_smem<128>(), s, p->tm_q, p->tm_k, p->tm_vt,
                    a);
-  YGG_LAUNCH_PDL(attn_combine_kernel, dim3(p->M * p->Hq), dim3(p->hd), 0, s, static_cast<const float*>(a.opart),
-                 static_cast<const float*>(a.ml), p->chunks, p->M * p->Hq, p->hd, static_cast<__nv_bfloat16*>(out));
+  const int rows = p->M * p->Hq;
+  if (p->hd == 64)
+    YGG_LAUNCH_PDL(attn_combine_kernel<64>, dim3((rows + 3) / 4), dim3(128), 0, s, static_cast<const float*>(a.opart),
+                   static_cast<const float*>(a.ml), rows, p->Hq, p->T, blk_start, blk_len,
+                   static_cast<__nv_bfloat16*>(out));
+  else
+    YGG_LAUNCH_PDL(attn_combine_kernel<128>, dim3((rows + 3) / 4), dim3(128), 0, s, static_cast<const float*>(a.opart),
+                   static_cast<const float*>(a.ml), rows, p->Hq, p->T, blk_start, blk_len,
+                   static_cast<__nv_bfloat16*>(out));
   return YGG_OK;
 }
 

@@ -276,114 +276,221 @@ YGG_DEV float epi_value(const EpiGeom& g, const float* __restrict__ ws, int m, i
   return v;
 }
 
+// Sum of the partials of V consecutive features [n, n+V) of row m (n % V == 0, one tile).
+template <int V>
+YGG_DEV void epi_values(const EpiGeom& g, const float* __restrict__ ws, int m, int n, float* v) {
+  const int t = (n / kBM) * g.m_tiles + m / g.BN;
+  const int s0 = __ldg(g.seg_first + t), s1 = __ldg(g.seg_first + t + 1);
+  const float* p = ws + static_cast<size_t>(m % g.BN) * kBM + (n % kBM);
+  const size_t seg_stride = static_cast<size_t>(g.BN) * kBM;
+#pragma unroll
+  for (int i = 0; i < V; ++i) v[i] = 0.f;
+#pragma unroll 4
+  for (int s = s0; s < s1; ++s) {
+    const float4* q = reinterpret_cast<const float4*>(p + s * seg_stride);
+#pragma unroll
+    for (int i = 0; i < V / 4; ++i) {
+      const float4 x = __ldg(q + i);
+      v[4 * i] += x.x;
+      v[4 * i + 1] += x.y;
+      v[4 * i + 2] += x.z;
+      v[4 * i + 3] += x.w;
+    }
+  }
+}
+
+template <typename T>
+YGG_DEV void store8(T* dst, const float* v);
+template <>
+YGG_DEV void store8<float>(float* dst, const float* v) {
+  reinterpret_cast<float4*>(dst)[0] = make_float4(v[0], v[1], v[2], v[3]);
+  reinterpret_cast<float4*>(dst)[1] = make_float4(v[4], v[5], v[6], v[7]);
+}
+template <>
+YGG_DEV void store8<__nv_bfloat16>(__nv_bfloat16* dst, const float* v) {
+  uint4 u;
+  __nv_bfloat162 a = __floats2bfloat162_rn(v[0], v[1]), b = __floats2bfloat162_rn(v[2], v[3]);
+  __nv_bfloat162 c = __floats2bfloat162_rn(v[4], v[5]), d = __floats2bfloat162_rn(v[6], v[7]);
+  u.x = *reinterpret_cast<uint32_t*>(&a);
+  u.y = *reinterpret_cast<uint32_t*>(&b);
+  u.z = *reinterpret_cast<uint32_t*>(&c);
+  u.w = *reinterpret_cast<uint32_t*>(&d);
+  *reinterpret_cast<uint4*>(dst) = u;
+}
+template <typename T>
+YGG_DEV void load8(const T* src, float* v);
+template <>
+YGG_DEV void load8<float>(const float* src, float* v) {
+  const float4 a = reinterpret_cast<const float4*>(src)[0], b = reinterpret_cast<const float4*>(src)[1];
+  v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+}
+template <>
+YGG_DEV void load8<__nv_bfloat16>(const __nv_bfloat16* src, float* v) {
+  const uint4 u = *reinterpret_cast<const uint4*>(src);
+  const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const __nv_bfloat162 b = *reinterpret_cast<const __nv_bfloat162*>(&w[i]);
+    v[2 * i] = __bfloat162float(b.x);
+    v[2 * i + 1] = __bfloat162float(b.y);
+  }
+}
+
+constexpr int kEpiThreads = 128;  // x 8 features = 1024 features per CTA
+
 template <typename OutT>
-__global__ void epi_store_kernel(EpiGeom g, const float* __restrict__ ws, OutT* __restrict__ out, int ld) {
+__global__ void __launch_bounds__(kEpiThreads) epi_store_kernel(EpiGeom g, const float* __restrict__ ws,
+                                                                OutT* __restrict__ out, int ld) {
   pdl_wait();
   pdl_launch_dependents();
   const int m = blockIdx.y;
-  for (int n = blockIdx.x * blockDim.x + threadIdx.x; n < g.N; n += gridDim.x * blockDim.x)
-    out[static_cast<size_t>(m) * ld + n] = from_f32<OutT>(epi_value(g, ws, m, n));
+  const int n = (blockIdx.x * blockDim.x + threadIdx.x) * 8;
+  if (n >= g.N) return;
+  float v[8];
+  epi_values<8>(g, ws, m, n, v);
+  store8<OutT>(out + static_cast<size_t>(m) * ld + n, v);
 }
 
-// Block-wide deterministic sum (fixed tree).
-template <int kThreads>
-YGG_DEV float block_sum(float v, float* red) {
-  v = warp_sum(v);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  __syncthreads();
-  if (lane == 0) red[warp] = v;
-  __syncthreads();
-  float t = 0.f;
-  if (threadIdx.x < 32) {
-    t = (lane < kThreads / 32) ? red[lane] : 0.f;
-    t = warp_sum(t);
-    if (lane == 0) red[0] = t;
-  }
-  __syncthreads();
-  return red[0];
+YGG_DEV uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+YGG_DEV void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+YGG_DEV float ld_dsmem_f32(const float* local, uint32_t rank) {
+  uint32_t remote;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(smem_u32(local)), "r"(rank));
+  float v;
+  asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(remote) : "memory");
+  return v;
 }
 
-constexpr int kRowThreads = 256;
-constexpr int kMaxRowDim = 16384;
-
-template <typename ActT, typename WT>
-__global__ void __launch_bounds__(kRowThreads) epi_residual_norm_kernel(EpiGeom g, const float* __restrict__ ws,
+// Residual add + RMSNorm over a thread-block cluster: the row's 1024-feature slices live in the
+// cluster's CTAs, whose sums of squares are combined through distributed shared memory in rank
+// order (deterministic), so the whole row is normalised in one launch with N/8 threads.
+template <typename ActT>
+__global__ void __launch_bounds__(kEpiThreads) epi_residual_norm_kernel(EpiGeom g, const float* __restrict__ ws,
                                                                         float* __restrict__ resid,
-                                                                        const WT* __restrict__ norm_w, float eps,
+                                                                        const ActT* __restrict__ norm_w, float eps,
                                                                         ActT* __restrict__ xn) {
   pdl_wait();
   pdl_launch_dependents();
-  __shared__ float red[32];
-  const int m = blockIdx.x;
-  float* h = resid + static_cast<size_t>(m) * g.N;
+  __shared__ float red[kEpiThreads / 32];
+  __shared__ float cta_ss;
+  const int m = blockIdx.y;
+  const int n = (blockIdx.x * blockDim.x + threadIdx.x) * 8;
+  const bool live = n < g.N;
+  float h[8];
   float ss = 0.f;
-  for (int n = threadIdx.x; n < g.N; n += blockDim.x) {
-    const float v = h[n] + epi_value(g, ws, m, n);
-    h[n] = v;
-    ss += v * v;
+  if (live) {
+    float v[8];
+    epi_values<8>(g, ws, m, n, v);
+    float* hp = resid + static_cast<size_t>(m) * g.N + n;
+    load8<float>(hp, h);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      h[i] += v[i];
+      ss += h[i] * h[i];
+    }
+    store8<float>(hp, h);
   }
-  const float tot = block_sum<kRowThreads>(ss, red);
-  const float r = rsqrtf(tot / static_cast<float>(g.N) + eps);
-  for (int n = threadIdx.x; n < g.N; n += blockDim.x)
-    xn[static_cast<size_t>(m) * g.N + n] = from_f32<ActT>(h[n] * r * to_f32(norm_w[n]));
+  ss = warp_sum(ss);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float t = 0.f;
+    for (int w = 0; w < (int)(blockDim.x / 32); ++w) t += red[w];
+    cta_ss = t;
+  }
+  cluster_sync_all();
+  float total = 0.f;
+  for (uint32_t r = 0; r < gridDim.x; ++r) total += ld_dsmem_f32(&cta_ss, r);
+  cluster_sync_all();  // keep every CTA's smem alive until all ranks have read it
+  const float rs = rsqrtf(total / static_cast<float>(g.N) + eps);
+  if (live) {
+    float w[8];
+    load8<ActT>(norm_w + n, w);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) h[i] = h[i] * rs * w[i];
+    store8<ActT>(xn + static_cast<size_t>(m) * g.N + n, h);
+  }
 }
 
 template <typename ActT>
-__global__ void epi_swiglu_kernel(EpiGeom g, const float* __restrict__ ws, ActT* __restrict__ out) {
+__global__ void __launch_bounds__(kEpiThreads) epi_swiglu_kernel(EpiGeom g, const float* __restrict__ ws,
+                                                                 ActT* __restrict__ out) {
   pdl_wait();
   pdl_launch_dependents();
   const int m = blockIdx.y;
   const int F = g.N / 2;
-  for (int f = blockIdx.x * blockDim.x + threadIdx.x; f < F; f += gridDim.x * blockDim.x) {
-    const float gate = epi_value(g, ws, m, f);
-    const float up = epi_value(g, ws, m, F + f);
-    const float silu = gate / (1.f + expf(-gate));
-    out[static_cast<size_t>(m) * F + f] = from_f32<ActT>(silu * up);
-  }
+  const int f = (blockIdx.x * blockDim.x + threadIdx.x) * 8;
+  if (f >= F) return;
+  float gate[8], up[8], o[8];
+  epi_values<8>(g, ws, m, f, gate);
+  epi_values<8>(g, ws, m, F + f, up);
+#pragma unroll
+  for (int i = 0; i < 8; ++i) o[i] = gate[i] / (1.f + expf(-gate[i])) * up[i];
+  store8<ActT>(out + static_cast<size_t>(m) * F + f, o);
 }
 
 // QKV epilogue: RoPE (rotate-half convention) on q and k at pos[m]; q -> q_out, k/v -> KV cache.
+// Work item = 4 rotation pairs (i..i+3, i+half..i+half+3) of one head.
 template <typename ActT>
-__global__ void epi_qkv_rope_kernel(EpiGeom g, const float* __restrict__ ws, int Hq, int Hkv, int hd,
-                                    float log2_theta, const int32_t* __restrict__ pos,
-                                    const int32_t* __restrict__ slot, const int32_t* __restrict__ req,
-                                    ActT* __restrict__ q_out, ActT* __restrict__ cache, int S) {
+__global__ void __launch_bounds__(256) epi_qkv_rope_kernel(EpiGeom g, const float* __restrict__ ws, int Hq, int Hkv,
+                                                           int hd, float log2_theta, const int32_t* __restrict__ pos,
+                                                           const int32_t* __restrict__ slot,
+                                                           const int32_t* __restrict__ req, ActT* __restrict__ q_out,
+                                                           ActT* __restrict__ cache, int S) {
   pdl_wait();
   pdl_launch_dependents();
   const int m = blockIdx.x;
-  const int head = blockIdx.y;  // 0..Hq+2*Hkv-1
   const int half = hd / 2;
+  const int per_head = half / 4;
+  const int items = (Hq + 2 * Hkv) * per_head;
   const float p = static_cast<float>(pos[m]);
-  const int n0 = head * hd;
-  for (int i = threadIdx.x; i < half; i += blockDim.x) {
-    float x1 = epi_value(g, ws, m, n0 + i);
-    float x2 = epi_value(g, ws, m, n0 + i + half);
+  for (int it = threadIdx.x; it < items; it += blockDim.x) {
+    const int head = it / per_head;
+    const int i0 = (it % per_head) * 4;
+    const int n0 = head * hd;
+    float x1[4], x2[4];
+    epi_values<4>(g, ws, m, n0 + i0, x1);
+    epi_values<4>(g, ws, m, n0 + i0 + half, x2);
     if (head < Hq + Hkv) {
-      // inv_freq = theta^(-2i/hd), as 1/(theta**(2i/hd)) in f32
-      const float inv_freq = 1.0f / exp2f(log2_theta * (static_cast<float>(2 * i) / static_cast<float>(hd)));
-      const float ang = p * inv_freq;
-      float sn, cs;
-      sincosf(ang, &sn, &cs);
-      const float y1 = x1 * cs - x2 * sn;
-      const float y2 = x2 * cs + x1 * sn;
-      x1 = y1;
-      x2 = y2;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        // inv_freq = theta^(-2i/hd), as 1/(theta**(2i/hd)) in f32
+        const float inv_freq = 1.0f / exp2f(log2_theta * (static_cast<float>(2 * (i0 + j)) / static_cast<float>(hd)));
+        float sn, cs;
+        sincosf(p * inv_freq, &sn, &cs);
+        const float y1 = x1[j] * cs - x2[j] * sn;
+        const float y2 = x2[j] * cs + x1[j] * sn;
+        x1[j] = y1;
+        x2[j] = y2;
+      }
     }
     if (head < Hq) {
       ActT* q = q_out + (static_cast<size_t>(m) * Hq + head) * hd;
-      q[i] = from_f32<ActT>(x1);
-      q[i + half] = from_f32<ActT>(x2);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        q[i0 + j] = from_f32<ActT>(x1[j]);
+        q[i0 + j + half] = from_f32<ActT>(x2[j]);
+      }
     } else {
       const bool is_v = head >= Hq + Hkv;
       const int kvh = is_v ? head - Hq - Hkv : head - Hq;
       const size_t base = ((static_cast<size_t>(req[m]) * 2 + (is_v ? 1 : 0)) * Hkv + kvh) * static_cast<size_t>(S) * hd;
-      if (!is_v) {  // K rows: [S][hd]
-        const size_t off = base + static_cast<size_t>(slot[m]) * hd;
-        cache[off + i] = from_f32<ActT>(x1);
-        cache[off + i + half] = from_f32<ActT>(x2);
-      } else {      // V transposed: [hd][S], so attention reads K-major V^T tiles
-        cache[base + static_cast<size_t>(i) * S + slot[m]] = from_f32<ActT>(x1);
-        cache[base + static_cast<size_t>(i + half) * S + slot[m]] = from_f32<ActT>(x2);
+      const int sl = slot[m];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        if (!is_v) {  // K rows: [S][hd]
+          cache[base + static_cast<size_t>(sl) * hd + i0 + j] = from_f32<ActT>(x1[j]);
+          cache[base + static_cast<size_t>(sl) * hd + i0 + j + half] = from_f32<ActT>(x2[j]);
+        } else {      // V transposed: [hd][S], so attention reads K-major V^T tiles
+          cache[base + static_cast<size_t>(i0 + j) * S + sl] = from_f32<ActT>(x1[j]);
+          cache[base + static_cast<size_t>(i0 + j + half) * S + sl] = from_f32<ActT>(x2[j]);
+        }
       }
     }
   }
@@ -554,12 +661,13 @@ int ygg_epi_store(const void* plan, const float* ws, void* out, int out_dtype, i
   YGG_CHECK_ARG(ld_out >= g->N, "ld_out < N");
   EpiGeom geo = geom_of(g);
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  dim3 grid(std::min((g->N + 255) / 256, 64), g->M);
+  YGG_CHECK_ARG(ld_out % 8 == 0, "ld_out must be a multiple of 8");
+  dim3 grid((g->N + 1023) / 1024, g->M);
   if (out_dtype == YGG_F32)
-    YGG_LAUNCH_PDL(epi_store_kernel<float>, grid, dim3(256), 0, s, geo, ws, static_cast<float*>(out), ld_out);
+    YGG_LAUNCH_PDL(epi_store_kernel<float>, grid, dim3(kEpiThreads), 0, s, geo, ws, static_cast<float*>(out), ld_out);
   else
-    YGG_LAUNCH_PDL(epi_store_kernel<__nv_bfloat16>, grid, dim3(256), 0, s, geo, ws, static_cast<__nv_bfloat16*>(out),
-                   ld_out);
+    YGG_LAUNCH_PDL(epi_store_kernel<__nv_bfloat16>, grid, dim3(kEpiThreads), 0, s, geo, ws,
+                   static_cast<__nv_bfloat16*>(out), ld_out);
   return YGG_OK;
 }
 
@@ -567,15 +675,16 @@ int ygg_epi_residual_norm(const void* plan, const float* ws, float* resid, const
                           int act_dtype, ygg_stream_t stream) {
   const GemmPlan* g = plan_of(plan);
   YGG_CHECK_ARG(g && ws && resid && norm_w && xn_out, "invalid arguments");
-  YGG_CHECK_ARG(g->N <= kMaxRowDim, "row too wide");
+  const int cx = (g->N + 1023) / 1024;
+  YGG_CHECK_ARG(cx <= 8, "row wider than one 8-CTA cluster (8192 features)");
   EpiGeom geo = geom_of(g);
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   if (act_dtype == YGG_F32)
-    YGG_LAUNCH_PDL((epi_residual_norm_kernel<float, float>), dim3(g->M), dim3(kRowThreads), 0, s, geo, ws, resid,
-                   static_cast<const float*>(norm_w), eps, static_cast<float*>(xn_out));
+    YGG_LAUNCH_PDL_CLUSTER(epi_residual_norm_kernel<float>, dim3(cx, g->M), dim3(kEpiThreads), cx, s, geo, ws, resid,
+                           static_cast<const float*>(norm_w), eps, static_cast<float*>(xn_out));
   else
-    YGG_LAUNCH_PDL((epi_residual_norm_kernel<__nv_bfloat16, __nv_bfloat16>), dim3(g->M), dim3(kRowThreads), 0, s, geo,
-                   ws, resid, static_cast<const __nv_bfloat16*>(norm_w), eps, static_cast<__nv_bfloat16*>(xn_out));
+    YGG_LAUNCH_PDL_CLUSTER(epi_residual_norm_kernel<__nv_bfloat16>, dim3(cx, g->M), dim3(kEpiThreads), cx, s, geo, ws,
+                           resid, static_cast<const __nv_bfloat16*>(norm_w), eps, static_cast<__nv_bfloat16*>(xn_out));
   return YGG_OK;
 }
 
@@ -585,11 +694,12 @@ int ygg_epi_swiglu(const void* plan, const float* ws, void* out, int act_dtype, 
   YGG_CHECK_ARG(g->N % 2 == 0, "gate_up width must be even");
   EpiGeom geo = geom_of(g);
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  dim3 grid(std::min((g->N / 2 + 255) / 256, 64), g->M);
+  dim3 grid((g->N / 2 + 1023) / 1024, g->M);
   if (act_dtype == YGG_F32)
-    YGG_LAUNCH_PDL(epi_swiglu_kernel<float>, grid, dim3(256), 0, s, geo, ws, static_cast<float*>(out));
+    YGG_LAUNCH_PDL(epi_swiglu_kernel<float>, grid, dim3(kEpiThreads), 0, s, geo, ws, static_cast<float*>(out));
   else
-    YGG_LAUNCH_PDL(epi_swiglu_kernel<__nv_bfloat16>, grid, dim3(256), 0, s, geo, ws, static_cast<__nv_bfloat16*>(out));
+    YGG_LAUNCH_PDL(epi_swiglu_kernel<__nv_bfloat16>, grid, dim3(kEpiThreads), 0, s, geo, ws,
+                   static_cast<__nv_bfloat16*>(out));
   return YGG_OK;
 }
 
@@ -599,16 +709,16 @@ int ygg_epi_qkv_rope(const void* plan, const float* ws, int Hq, int Hkv, int hd,
   const GemmPlan* g = plan_of(plan);
   YGG_CHECK_ARG(g && ws && pos && slot && req && q_out && cache, "invalid arguments");
   YGG_CHECK_ARG(g->N == (Hq + 2 * Hkv) * hd, "QKV width mismatch");
-  YGG_CHECK_ARG(hd % 2 == 0 && hd <= 256, "bad head dim");
+  YGG_CHECK_ARG(hd % 8 == 0 && hd <= 256, "bad head dim");
   EpiGeom geo = geom_of(g);
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  dim3 grid(g->M, Hq + 2 * Hkv);
+  dim3 grid(g->M);
   const float l2t = log2f(rope_theta);
   if (act_dtype == YGG_F32)
-    YGG_LAUNCH_PDL(epi_qkv_rope_kernel<float>, grid, dim3(64), 0, s, geo, ws, Hq, Hkv, hd, l2t, pos, slot, req,
+    YGG_LAUNCH_PDL(epi_qkv_rope_kernel<float>, grid, dim3(256), 0, s, geo, ws, Hq, Hkv, hd, l2t, pos, slot, req,
                    static_cast<float*>(q_out), static_cast<float*>(cache), S);
   else
-    YGG_LAUNCH_PDL(epi_qkv_rope_kernel<__nv_bfloat16>, grid, dim3(64), 0, s, geo, ws, Hq, Hkv, hd, l2t, pos, slot, req,
+    YGG_LAUNCH_PDL(epi_qkv_rope_kernel<__nv_bfloat16>, grid, dim3(256), 0, s, geo, ws, Hq, Hkv, hd, l2t, pos, slot, req,
                    static_cast<__nv_bfloat16*>(q_out), static_cast<__nv_bfloat16*>(cache), S);
   return YGG_OK;
 }

@@ -32,7 +32,34 @@ int launch_pdl(Kernel kernel, dim3 grid, dim3 block, size_t smem, cudaStream_t s
   return YGG_OK;
 }
 
+template <typename Kernel, typename... Args>
+int launch_pdl_cluster(Kernel kernel, dim3 grid, dim3 block, int cluster_x, cudaStream_t stream, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  attr[1].id = cudaLaunchAttributeClusterDimension;
+  attr[1].val.clusterDim.x = cluster_x;
+  attr[1].val.clusterDim.y = 1;
+  attr[1].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 2;
+  cudaError_t err = cudaLaunchKernelEx(&cfg, kernel, args...);
+  if (err != cudaSuccess) return ygg_fail(YGG_ERR_CUDA, "cluster launch failed: %s", cudaGetErrorString(err));
+  return YGG_OK;
+}
+
 }  // namespace ygg
+
+#define YGG_LAUNCH_PDL_CLUSTER(kernel, grid, block, cx, stream, ...)                              \
+  do {                                                                                            \
+    int _rc = ::ygg::launch_pdl_cluster(kernel, grid, block, cx, stream, __VA_ARGS__);            \
+    if (_rc) return _rc;                                                                          \
+  } while (0)
 
 #define YGG_CHECK_ARG(cond, msg)                                   \
   do {                                                             \

@@ -1,0 +1,164 @@
+"""CPU tests of the host side: the C ABI library loads and exports every declared symbol, the
+product path refuses to run without a B200 (no CPU fallback), request sharding + the final gather
+over a 2-rank gloo group, reference error conventions, and the CPU oracle's lossless-greedy
+identity on the tiny config."""
+
+import ctypes
+import os
+import re
+import socket
+from pathlib import Path
+
+import pytest
+import torch
+
+ROOT = Path(__file__).resolve().parents[1]
+
+
+def test_library_exports_every_declared_symbol():
+    from paper_2512_23858_b200 import _lib
+
+    hdr = (ROOT / "include" / "ygg.h").read_text()
+    declared = set(re.findall(r"\b(ygg_[a-z0-9_]+)\s*\(", hdr))
+    raw = ctypes.CDLL(str(_lib.LIB_PATH))
+    missing = [n for n in sorted(declared) if not hasattr(raw, n)]
+    assert not missing, missing
+    assert set(_lib.EXPORTED) <= declared, set(_lib.EXPORTED) - declared
+    lib = _lib.load()
+    assert lib.ygg_version() >= 100
+
+
+def test_abi_struct_layouts_match_header():
+    from paper_2512_23858_b200 import _lib
+
+    # ygg_tree: 3 int32 + 10 pointers (natural alignment on x86-64)
+    assert ctypes.sizeof(_lib.YggTree) == 16 + 10 * 8
+    assert ctypes.sizeof(_lib.YggSeq) == 8 + 5 * 8 + 8
+    assert ctypes.sizeof(_lib.YggProfile) == 4 + 32 * 4 + 4 + 32 * 8
+    assert ctypes.sizeof(_lib.YggPruneArgs) == 16
+
+
+def test_argument_errors_map_to_value_error_without_device():
+    """Host-side argument validation runs before any device work."""
+    from paper_2512_23858_b200 import _lib
+
+    lib = _lib.load()
+    with pytest.raises(ValueError):
+        _lib.check(lib.ygg_topk_softmax(None, 0, 1, 10, 10, 0, 1.0, None, None, None, None, 0, None))
+    with pytest.raises(ValueError):
+        _lib.check(lib.ygg_gemm_plan_init(ctypes.create_string_buffer(4096), 1, 1, 1, 1, 100, 64, 0, 1, None, None))
+
+
+@pytest.mark.skipif(torch.cuda.is_available(), reason="checks the no-GPU behaviour")
+def test_product_path_fails_loudly_without_gpu():
+    from paper_2512_23858_b200 import _lib
+    from paper_2512_23858_b200.engine import SpecDecoder, StepShape
+    from paper_2512_23858_b200.model import init_weights, preset
+
+    tc = preset("tiny-target")
+    w = init_weights(tc, 0, torch.float32)
+    with pytest.raises(RuntimeError, match="no CPU fallback"):
+        _lib.require_device()
+    with pytest.raises(RuntimeError, match="no CPU fallback"):
+        SpecDecoder(tc, w, tc, w, StepShape(2, 2))
+
+
+def test_shard_requests_partition():
+    from paper_2512_23858_b200.dist import shard_requests
+
+    for n in (0, 1, 7, 16, 64):
+        for world in (1, 2, 4, 8):
+            ids = [i for r in range(world) for i in shard_requests(n, world, r)]
+            assert ids == list(range(n))
+            sizes = [len(shard_requests(n, world, r)) for r in range(world)]
+            assert max(sizes) - min(sizes) <= 1
+    with pytest.raises(ValueError):
+        shard_requests(4, 2, 2)
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, n_req, out_q):
+    import torch.distributed as dist
+
+    from oracle.llama_ref import RefLlama, greedy_ar
+    from paper_2512_23858_b200.dist import gather_generated, shard_requests
+    from paper_2512_23858_b200.model import init_weights, preset
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    cfg = preset("tiny-target", n_layers=1)
+    model = RefLlama(cfg, init_weights(cfg, 0, torch.float32))
+    mine = {}
+    for rid in shard_requests(n_req, world, rank):
+        g = torch.Generator().manual_seed(1000 + rid)
+        prompt = torch.randint(0, cfg.vocab, (8,), generator=g).tolist()
+        mine[rid] = greedy_ar(model, prompt, 4, 32)
+    merged = gather_generated(mine, world)
+    if rank == 0:
+        out_q.put(merged)
+    dist.destroy_process_group()
+
+
+def test_request_sharding_gather_gloo_world2():
+    """Two ranks each decode their shard; the gathered result equals the single-process run."""
+    import torch.multiprocessing as mp
+
+    from oracle.llama_ref import RefLlama, greedy_ar
+    from paper_2512_23858_b200.model import init_weights, preset
+
+    n_req = 5
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, n_req, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    merged = q.get(timeout=240)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    cfg = preset("tiny-target", n_layers=1)
+    model = RefLlama(cfg, init_weights(cfg, 0, torch.float32))
+    for rid in range(n_req):
+        g = torch.Generator().manual_seed(1000 + rid)
+        prompt = torch.randint(0, cfg.vocab, (8,), generator=g).tolist()
+        assert merged[rid] == greedy_ar(model, prompt, 4, 32)
+
+
+def test_oracle_spec_decoding_is_lossless_greedy():
+    """CPU oracle: EGT speculative decoding == plain greedy AR (tiny cfg1, coupled and independent)."""
+    from oracle.llama_ref import RefLlama, greedy_ar
+    from oracle.spec_ref import RefSpecDecoder
+    from oracle.tree_ref import Profile
+    from paper_2512_23858_b200.model import Coupling, init_weights, preset
+
+    tc, dc = preset("tiny-target"), preset("tiny-draft")
+    for cp in (None, Coupling(rank=256, logit_scale=8.0, head_noise=2.0, layer_gain=2.0)):
+        tw, dw = init_weights(tc, 0, torch.float32, "cpu", cp), init_weights(dc, 1, torch.float32, "cpu", cp)
+        prompt = torch.randint(0, tc.vocab, (16,), generator=torch.Generator().manual_seed(5)).tolist()
+        ar = greedy_ar(RefLlama(tc, tw), prompt, 24, 96)
+        sd = RefSpecDecoder(RefLlama(tc, tw), RefLlama(dc, dw), 4, 4, 8, 64, Profile(((1, 20.0), (64, 30.0))),
+                            Profile(((1, 100.0), (64, 100.0))), 96)
+        assert sd.generate(prompt, 24) == ar
+
+
+def test_host_latency_errors_follow_reference():
+    from paper_2512_23858_b200.latency import ConfigError, LatencyProfile, TreeShape, latency_at, load_profile
+
+    with pytest.raises(ValueError):
+        LatencyProfile(((1, 1.0),), "verifier")
+    with pytest.raises(ValueError):
+        LatencyProfile(((4, 1.0), (2, 2.0)), "verifier")
+    with pytest.raises(ValueError):
+        latency_at(LatencyProfile(((1, 1.0), (4, 2.0)), "drafter"), 0)
+    with pytest.raises(ValueError):
+        TreeShape(2, 2, 6)
+    with pytest.raises(ConfigError):
+        load_profile("/nonexistent.csv", "drafter")

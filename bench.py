@@ -148,17 +148,17 @@ def gemm_roofline(sd, peak_gbs):
 
     lib = L.lib()
     vf = sd.verify
-    plans = [p for layer in vf.plans for p in layer.values()] + [vf.lm_plan]
+    plans = vf.gemm_calls()
     s = torch.cuda.current_stream()
     sp = L.stream_ptr()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in plans]
     for _ in range(2):
         for p in plans:
-            L.check(lib.ygg_gemm_run(p.handle, vf.ws.data_ptr(), sp))
+            vf.launch_gemm(p, sp)
     torch.cuda.synchronize()
     for p, (a, b) in zip(plans, ev):
         a.record(s)
-        L.check(lib.ygg_gemm_run(p.handle, vf.ws.data_ptr(), sp))
+        vf.launch_gemm(p, sp)
         b.record(s)
     torch.cuda.synchronize()
     times = [a.elapsed_time(b) * 1e-3 for a, b in ev]
@@ -166,7 +166,7 @@ def gemm_roofline(sd, peak_gbs):
     achieved = sum(nbytes) / sum(times) / 1e9
     return {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak_gbs, "unit": "GB/s",
             "frac": round(achieved / peak_gbs, 4), "traffic": None,
-            "kernel": "gemm_bf16_tc_kernel (swap-AB tcgen05 stream-K weight streaming)",
+            "kernel": "gemm_bf16_tc_kernel (swap-AB tcgen05 stream-K weight streaming, fused epilogues)",
             "launches_timed": len(plans), "bytes_per_launch_avg": int(sum(nbytes) / len(plans)),
             "avg_launch_us": round(sum(times) / len(times) * 1e6, 2)}
 

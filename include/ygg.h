@@ -172,6 +172,48 @@ int ygg_gemm_plan_init(void* plan, int dtype, const void* W, const void* X, int 
                        int32_t* seg_first_dev, int* num_segments, size_t* workspace_bytes);
 int ygg_gemm_run(const void* plan, float* workspace, ygg_stream_t stream);
 
+/* Fused epilogues of the bf16 tcgen05 GEMM: the last CTA to finish an output tile reduces its
+ * stream-K partials in fixed order and applies the op (one launch per linear layer).  RMSNorm is
+ * folded: its gain is pre-multiplied into W and, when ss_in is given, every output row (token) m is
+ * scaled by rsqrt(sum_t ss_in[t][m] / norm_dim + eps).  Weight row layouts: QKV_ROPE rows are
+ * permuted per head so RoPE pairs (i, i+hd/2) are adjacent; SWIGLU rows interleave gate/up. */
+typedef enum {
+  YGG_EPI_NONE = 0,      /* partials only (ygg_gemm_run) */
+  YGG_EPI_STORE_F32 = 1, /* out[m][n] = y (logits) */
+  YGG_EPI_QKV_ROPE = 2,  /* RoPE at pos[m]; q -> q_out [M,Hq,hd]; k -> K rows, v -> V^T of the cache */
+  YGG_EPI_SWIGLU = 3,    /* act_out[m][j] = silu(gate_j) * up_j */
+  YGG_EPI_RESID = 4      /* resid[m][n] += y; hb = bf16(resid); ss_out[n/128][m] = per-tile sum of squares */
+} ygg_epi_kind;
+
+typedef struct {
+  int32_t kind;
+  const float* ss_in;
+  int32_t ss_tiles;
+  int32_t norm_dim;
+  float eps;
+  float* out;
+  int32_t ld;
+  void* q_out;
+  void* cache;
+  int32_t S, Hq, Hkv, hd;
+  float rope_theta;
+  const int32_t* pos;
+  const int32_t* slot;
+  const int32_t* req;
+  void* act_out;
+  float* resid;
+  void* hb;
+  float* ss_out;
+  int32_t* counters; /* [tiles] zero-initialised arrival counters (self-resetting) */
+} ygg_epilogue;
+
+int ygg_gemm_fused(const void* plan, float* workspace, const ygg_epilogue* epi, ygg_stream_t stream);
+int ygg_gemm_tiles(const void* plan);
+/* Embedding gather for the fused path: resid (f32), hb (bf16) and per-128-feature-tile sums of
+ * squares ss_out [d/128][M] (the first layer's folded RMSNorm input). */
+int ygg_embed_fused(const void* table, int V, int d, const int32_t* tokens, int M, float* resid, void* hb,
+                    float* ss_out, ygg_stream_t stream);
+
 /* Epilogues over GEMM partials (all deterministic fixed-order segment sums). */
 int ygg_epi_store(const void* plan, const float* ws, void* out, int out_dtype, int ld_out, ygg_stream_t stream);
 int ygg_epi_residual_norm(const void* plan, const float* ws, float* resid, const void* norm_w, float eps,

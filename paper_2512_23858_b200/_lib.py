@@ -83,6 +83,17 @@ class YggPruneArgs(C.Structure):
     ]
 
 
+class YggEpilogue(C.Structure):
+    _fields_ = [
+        ("kind", C.c_int32), ("ss_in", vp), ("ss_tiles", C.c_int32), ("norm_dim", C.c_int32), ("eps", C.c_float),
+        ("out", vp), ("ld", C.c_int32), ("q_out", vp), ("cache", vp), ("S", C.c_int32), ("Hq", C.c_int32),
+        ("Hkv", C.c_int32), ("hd", C.c_int32), ("rope_theta", C.c_float), ("pos", vp), ("slot", vp), ("req", vp),
+        ("act_out", vp), ("resid", vp), ("hb", vp), ("ss_out", vp), ("counters", vp),
+    ]
+
+
+YGG_EPI_NONE, YGG_EPI_STORE_F32, YGG_EPI_QKV_ROPE, YGG_EPI_SWIGLU, YGG_EPI_RESID = range(5)
+
 # name -> (restype, argtypes)
 _SIGS: dict[str, tuple] = {
     "ygg_version": (C.c_int, []),
@@ -104,6 +115,9 @@ _SIGS: dict[str, tuple] = {
                                      C.POINTER(C.c_int), C.POINTER(C.c_size_t)]),
     "ygg_gemm_seg_table_len": (C.c_int, [vp]),
     "ygg_gemm_run": (C.c_int, [vp, vp, vp]),
+    "ygg_gemm_fused": (C.c_int, [vp, vp, C.POINTER(YggEpilogue), vp]),
+    "ygg_gemm_tiles": (C.c_int, [vp]),
+    "ygg_embed_fused": (C.c_int, [vp, C.c_int, C.c_int, vp, C.c_int, vp, vp, vp, vp]),
     "ygg_epi_store": (C.c_int, [vp, vp, vp, C.c_int, C.c_int, vp]),
     "ygg_epi_residual_norm": (C.c_int, [vp, vp, vp, vp, C.c_float, vp, C.c_int, vp]),
     "ygg_epi_swiglu": (C.c_int, [vp, vp, vp, C.c_int, vp]),
@@ -131,7 +145,7 @@ EXPORTED = tuple(_SIGS)
 # Kernels launched by one successful call (used to count device launches per step).
 KERNELS_PER_CALL = {
     "ygg_topk_softmax": 2, "ygg_egt_grow_level": 1, "ygg_build_mask": 1, "ygg_knapsack_prune": 1,
-    "ygg_tree_subtree": 1, "ygg_accept": 1, "ygg_kv_compact": 1, "ygg_gemm_run": 1, "ygg_epi_store": 1,
+    "ygg_tree_subtree": 1, "ygg_accept": 1, "ygg_kv_compact": 1, "ygg_gemm_run": 1, "ygg_gemm_fused": 1, "ygg_embed_fused": 1, "ygg_epi_store": 1,
     "ygg_epi_residual_norm": 1, "ygg_epi_swiglu": 1, "ygg_epi_qkv_rope": 1, "ygg_embed": 1, "ygg_rmsnorm": 1,
     "ygg_attention": 1, "ygg_attention_tc": 2, "ygg_row_stats": 1, "ygg_pass0_inputs": 1, "ygg_init_roots": 1, "ygg_level_inputs": 1,
     "ygg_verify_inputs": 1, "ygg_commit": 1, "ygg_stamp": 1,

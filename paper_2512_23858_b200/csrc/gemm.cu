@@ -26,7 +26,9 @@ namespace ygg {
 constexpr int kBM = 128;          // weight rows per tile (UMMA M)
 constexpr int kBK = 64;           // k per stage: 64 bf16 = one 128B swizzle row
 constexpr int kGemmThreads = 192; // 6 warps
-constexpr int kSmemBudget = 200 * 1024;
+constexpr int kMaxRstdTokensHost = 1024;
+// alignment slack + barriers (<= 2*12+4 u64) + tmem slot/flag + red_s[64] + rstd_s[1024]
+constexpr int kSmemExtra = 1024 + 28 * 8 + 16 + 64 * 4 + kMaxRstdTokensHost * 4;
 
 struct GemmPlan {
   uint32_t magic;
@@ -55,11 +57,129 @@ struct GemmParams {
 };
 
 // ---------------------------------------------------------------------------
+// Fused epilogues.  The last CTA to finish a tile (per-tile arrival counter) reduces the tile's
+// partials in segment order and applies the op; a tile owned by one CTA is finished straight
+// from TMEM.  RMSNorm is folded: its gain lives in the next weight matrix and the per-token
+// rstd (from the producer's per-tile sums of squares) scales the consumer's output rows.
+// ---------------------------------------------------------------------------
+enum EpiKind : int { kEpiNone = 0, kEpiStoreF32 = 1, kEpiQkvRope = 2, kEpiSwiglu = 3, kEpiResid = 4 };
+constexpr int kMaxRstdTokens = 1024;
+
+struct EpiArgs {
+  const float* ss_in;   // [ss_tiles][M] sums of squares of the (un-normalised) input rows, or null
+  int ss_tiles;
+  int norm_dim;
+  float eps;
+  float* out;           // STORE_F32 [M][ld]
+  int ld;
+  __nv_bfloat16* q_out; // QKV_ROPE (rows permuted: pairs (i, i+hd/2) adjacent)
+  __nv_bfloat16* cache;
+  int S, Hq, Hkv, hd;
+  float log2_theta;
+  const int32_t* pos;
+  const int32_t* slot;
+  const int32_t* req;
+  __nv_bfloat16* act_out; // SWIGLU [M][N/2] (rows interleaved gate/up)
+  float* resid;           // RESID [M][N]
+  __nv_bfloat16* hb;      // RESID bf16 copy of the residual = next GEMM's X
+  float* ss_out;          // RESID [N/128][M]
+  int n_total;
+  int32_t* counters;      // [tiles] arrival counters, self-resetting
+};
+
+YGG_DEV void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+
+// Apply the fused op to 16 token columns of one 128-feature tile row (thread = feature row).
+template <int KIND>
+YGG_DEV void epi_apply(const EpiArgs& e, int M, int n, int m0, int valid16, float* v, const float* rstd_s,
+                       float* red_s, int quarter, int lane) {
+  if (e.ss_in) {
+#pragma unroll
+    for (int j = 0; j < 16; ++j) v[j] *= (j < valid16) ? rstd_s[m0 + j] : 0.f;
+  }
+  if constexpr (KIND == kEpiStoreF32) {
+#pragma unroll
+    for (int j = 0; j < 16; ++j)
+      if (j < valid16) e.out[static_cast<size_t>(m0 + j) * e.ld + n] = v[j];
+  } else if constexpr (KIND == kEpiSwiglu) {
+    const bool odd = n & 1;
+    const int F = e.n_total / 2;
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const float other = __shfl_xor_sync(0xffffffffu, v[j], 1);
+      if (!odd && j < valid16) {
+        const float g = v[j], u = other;
+        e.act_out[static_cast<size_t>(m0 + j) * F + (n >> 1)] = __float2bfloat16_rn(g / (1.f + expf(-g)) * u);
+      }
+    }
+  } else if constexpr (KIND == kEpiQkvRope) {
+    const int head = n / e.hd, p = n % e.hd, half = e.hd / 2;
+    const int pair = p >> 1;
+    const bool odd = p & 1;
+    const int orig = pair + (odd ? half : 0);
+    const bool rope = head < e.Hq + e.Hkv;
+    const float inv_freq = 1.0f / exp2f(e.log2_theta * (static_cast<float>(2 * pair) / static_cast<float>(e.hd)));
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const float other = __shfl_xor_sync(0xffffffffu, v[j], 1);
+      if (j >= valid16) continue;
+      const int m = m0 + j;
+      float y = v[j];
+      if (rope) {
+        const float x1 = odd ? other : v[j], x2 = odd ? v[j] : other;
+        float sn, cs;
+        sincosf(static_cast<float>(__ldg(e.pos + m)) * inv_freq, &sn, &cs);
+        y = odd ? (x2 * cs + x1 * sn) : (x1 * cs - x2 * sn);
+      }
+      const __nv_bfloat16 yb = __float2bfloat16_rn(y);
+      if (head < e.Hq) {
+        e.q_out[(static_cast<size_t>(m) * e.Hq + head) * e.hd + orig] = yb;
+      } else {
+        const bool is_v = head >= e.Hq + e.Hkv;
+        const int kvh = is_v ? head - e.Hq - e.Hkv : head - e.Hq;
+        const size_t base =
+            ((static_cast<size_t>(__ldg(e.req + m)) * 2 + (is_v ? 1 : 0)) * e.Hkv + kvh) * static_cast<size_t>(e.S) * e.hd;
+        const int sl = __ldg(e.slot + m);
+        if (!is_v) e.cache[base + static_cast<size_t>(sl) * e.hd + orig] = yb;
+        else e.cache[base + static_cast<size_t>(orig) * e.S + sl] = yb;  // V^T [hd][S]
+      }
+    }
+  } else if constexpr (KIND == kEpiResid) {
+    float sq[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      sq[j] = 0.f;
+      if (j < valid16) {
+        const size_t idx = static_cast<size_t>(m0 + j) * e.n_total + n;
+        const float h = e.resid[idx] + v[j];
+        e.resid[idx] = h;
+        e.hb[idx] = __float2bfloat16_rn(h);
+        sq[j] = h * h;
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      float s = sq[j];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+      if (lane == 0) red_s[quarter * 16 + j] = s;
+    }
+    epi_bar();
+    const int t = quarter * 32 + lane;
+    if (t < 16 && t < valid16)  // fixed order over the four 32-row quarters => deterministic
+      e.ss_out[static_cast<size_t>(n / kBM) * M + m0 + t] =
+          red_s[0 * 16 + t] + red_s[1 * 16 + t] + red_s[2 * 16 + t] + red_s[3 * 16 + t];
+    epi_bar();
+  }
+}
+
+// ---------------------------------------------------------------------------
 // tcgen05 kernel
 // ---------------------------------------------------------------------------
+template <int KIND>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     gemm_bf16_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant__ CUtensorMap tmap_x,
-                        GemmParams p, float* __restrict__ ws) {
+                        GemmParams p, float* __restrict__ ws, EpiArgs e) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   // 1024-align the dynamic smem base (SW128 atoms).
   unsigned char* base = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -73,6 +193,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   uint64_t* tfull = empty + S;   // [2]
   uint64_t* tempty = tfull + 2;  // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  int* flag_s = reinterpret_cast<int*>(tmem_slot + 1);
+  float* red_s = reinterpret_cast<float*>(tmem_slot + 4);  // [4][16]
+  float* rstd_s = red_s + 64;                               // [kMaxRstdTokens]
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int c = blockIdx.x;
@@ -169,9 +292,18 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     }
   } else {
     pdl_wait();
-    // ===== Epilogue: TMEM -> registers -> partial workspace =====
+    // ===== Epilogue warps: TMEM -> (partials | fused op) =====
     const int quarter = warp & 3;  // TMEM lanes accessible by this warp
     const int row = quarter * 32 + lane;
+    const int et = threadIdx.x - 64;  // 0..127
+    if (KIND != kEpiNone && e.ss_in) {
+      for (int m = et; m < p.M; m += 128) {
+        float s = 0.f;
+        for (int t = 0; t < e.ss_tiles; ++t) s += __ldg(e.ss_in + static_cast<size_t>(t) * p.M + m);
+        rstd_s[m] = rsqrtf(s / static_cast<float>(e.norm_dim) + e.eps);
+      }
+      epi_bar();
+    }
     int acc = 0;
     uint32_t acc_phase[2] = {0u, 0u};
     long long u = u0;
@@ -179,22 +311,61 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       const int tile = static_cast<int>(u / p.kb);
       const long long tile_end = static_cast<long long>(tile + 1) * p.kb;
       const long long seg_end = tile_end < u1 ? tile_end : u1;
-      const int seg = (u == u0) ? p.seg_base[c] : p.seg_first[tile];
-      const int m_tile = tile % p.m_tiles;
+      const int s_first = p.seg_first[tile], s_end = p.seg_first[tile + 1];
+      const int nseg = s_end - s_first;
+      const int seg = (u == u0) ? p.seg_base[c] : s_first;
+      const int m_tile = tile % p.m_tiles, n_tile = tile / p.m_tiles;
       const int valid = min(BN, p.M - m_tile * BN);
+      const int n = n_tile * kBM + row;
       mbar_wait(&tfull[acc], acc_phase[acc]);
       tc_fence_after();
-      float* dst = ws + static_cast<size_t>(seg) * BN * kBM + row;
       const uint32_t taddr = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + static_cast<uint32_t>(acc * BN);
-      for (int c0 = 0; c0 < BN; c0 += 16) {
-        float v[16];
-        tmem_ld16(taddr + c0, v);
+      if (KIND != kEpiNone && nseg == 1) {
+        // Whole tile accumulated here: finish it straight from TMEM.
+        for (int c0 = 0; c0 < BN; c0 += 16) {
+          float v[16];
+          tmem_ld16(taddr + c0, v);
+          epi_apply<KIND>(e, p.M, n, m_tile * BN + c0, valid - c0, v, rstd_s, red_s, quarter, lane);
+        }
+        tc_fence_before();
+        mbar_arrive(&tempty[acc]);
+      } else {
+        float* dst = ws + static_cast<size_t>(seg) * BN * kBM + row;
+        for (int c0 = 0; c0 < BN; c0 += 16) {
+          float v[16];
+          tmem_ld16(taddr + c0, v);
 #pragma unroll
-        for (int j = 0; j < 16; ++j)
-          if (c0 + j < valid) dst[static_cast<size_t>(c0 + j) * kBM] = v[j];
+          for (int j = 0; j < 16; ++j)
+            if (c0 + j < valid) dst[static_cast<size_t>(c0 + j) * kBM] = v[j];
+        }
+        tc_fence_before();
+        mbar_arrive(&tempty[acc]);
+        if (KIND != kEpiNone) {
+          __threadfence();
+          epi_bar();
+          if (et == 0) *flag_s = (atomicAdd(e.counters + tile, 1) == nseg - 1);
+          epi_bar();
+          if (*flag_s) {
+            // Last arrival: reduce every segment of the tile in segment order, then apply the op.
+            __threadfence();
+            const float* src = ws + static_cast<size_t>(s_first) * BN * kBM + row;
+            for (int c0 = 0; c0 < BN; c0 += 16) {
+              float v[16];
+#pragma unroll
+              for (int j = 0; j < 16; ++j) v[j] = 0.f;
+              for (int s = 0; s < nseg; ++s) {
+                const float* q = src + static_cast<size_t>(s) * BN * kBM;
+#pragma unroll
+                for (int j = 0; j < 16; ++j)
+                  if (c0 + j < valid) v[j] += __ldcg(q + static_cast<size_t>(c0 + j) * kBM);
+              }
+              epi_apply<KIND>(e, p.M, n, m_tile * BN + c0, valid - c0, v, rstd_s, red_s, quarter, lane);
+            }
+            if (et == 0) e.counters[tile] = 0;
+          }
+          epi_bar();  // flag_s is reused by the next tile
+        }
       }
-      tc_fence_before();
-      mbar_arrive(&tempty[acc]);
       acc_phase[acc] ^= 1u;
       acc ^= 1;
       u = seg_end;
@@ -539,8 +710,12 @@ using namespace ygg;
 extern "C" {
 
 int ygg_prepare_gemm(void) {
-  cudaError_t e = cudaFuncSetAttribute(gemm_bf16_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-  if (e != cudaSuccess) return ygg_fail(YGG_ERR_CUDA, "gemm attribute: %s", cudaGetErrorString(e));
+  cudaError_t e = cudaSuccess;
+  for (auto fn : {gemm_bf16_tc_kernel<kEpiNone>, gemm_bf16_tc_kernel<kEpiStoreF32>, gemm_bf16_tc_kernel<kEpiQkvRope>,
+                  gemm_bf16_tc_kernel<kEpiSwiglu>, gemm_bf16_tc_kernel<kEpiResid>}) {
+    e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    if (e != cudaSuccess) return ygg_fail(YGG_ERR_CUDA, "gemm attribute: %s", cudaGetErrorString(e));
+  }
   return YGG_OK;
 }
 
@@ -576,7 +751,7 @@ int ygg_gemm_plan_init(void* plan_mem, int dtype, const void* W, const void* X, 
     if (num_ctas > g->units) num_ctas = static_cast<int>(g->units);
     g->num_ctas = num_ctas;
     const int stage_bytes = kBM * kBK * 2 + g->BN * kBK * 2;
-    g->stages = std::min(12, (kSmemBudget - 1024 - 256) / stage_bytes);
+    g->stages = std::min(12, (227 * 1024 - kSmemExtra) / stage_bytes);
     YGG_CHECK_ARG(g->stages >= 2, "tile too large for shared memory");
     int cols = 32;
     while (cols < 2 * g->BN) cols *= 2;
@@ -627,11 +802,7 @@ static const GemmPlan* plan_of(const void* plan) {
   return as_plan(reinterpret_cast<const void*>((reinterpret_cast<uintptr_t>(plan) + 63) & ~uintptr_t(63)));
 }
 
-int ygg_gemm_run(const void* plan, float* workspace, ygg_stream_t stream) {
-  const GemmPlan* g = plan_of(plan);
-  YGG_CHECK_ARG(g != nullptr, "invalid GEMM plan");
-  YGG_CHECK_ARG(workspace != nullptr, "null workspace");
-  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+static int gemm_launch(const GemmPlan* g, float* workspace, const ygg_epilogue* epi, cudaStream_t s) {
   if (g->dtype == YGG_BF16) {
     GemmParams p;
     p.M = g->M;
@@ -644,15 +815,95 @@ int ygg_gemm_run(const void* plan, float* workspace, ygg_stream_t stream) {
     p.units = g->units;
     p.seg_first = g->seg_table;
     p.seg_base = g->seg_table + g->tiles + 1;
-    const size_t smem = 1024 + static_cast<size_t>(g->stages) * (kBM * kBK * 2 + g->BN * kBK * 2) + 256;
-    YGG_LAUNCH_PDL(gemm_bf16_tc_kernel, dim3(g->num_ctas), dim3(kGemmThreads), smem, s, g->tmap_w, g->tmap_x, p,
-                   workspace);
+    const size_t smem = kSmemExtra + static_cast<size_t>(g->stages) * (kBM * kBK * 2 + g->BN * kBK * 2);
+    EpiArgs e;
+    std::memset(&e, 0, sizeof(e));
+    int kind = kEpiNone;
+    if (epi) {
+      kind = epi->kind;
+      e.ss_in = epi->ss_in;
+      e.ss_tiles = epi->ss_tiles;
+      e.norm_dim = epi->norm_dim;
+      e.eps = epi->eps;
+      e.out = epi->out;
+      e.ld = epi->ld;
+      e.q_out = static_cast<__nv_bfloat16*>(epi->q_out);
+      e.cache = static_cast<__nv_bfloat16*>(epi->cache);
+      e.S = epi->S;
+      e.Hq = epi->Hq;
+      e.Hkv = epi->Hkv;
+      e.hd = epi->hd;
+      e.log2_theta = epi->rope_theta > 0.f ? log2f(epi->rope_theta) : 0.f;
+      e.pos = epi->pos;
+      e.slot = epi->slot;
+      e.req = epi->req;
+      e.act_out = static_cast<__nv_bfloat16*>(epi->act_out);
+      e.resid = epi->resid;
+      e.hb = static_cast<__nv_bfloat16*>(epi->hb);
+      e.ss_out = epi->ss_out;
+      e.n_total = g->N;
+      e.counters = epi->counters;
+      YGG_CHECK_ARG(kind == kEpiNone || e.counters != nullptr, "fused epilogue needs tile counters");
+      YGG_CHECK_ARG(!e.ss_in || g->M <= kMaxRstdTokens, "too many tokens for the folded RMSNorm");
+      YGG_CHECK_ARG(!e.ss_in || (e.ss_tiles >= 1 && e.norm_dim >= 1), "bad RMSNorm fold arguments");
+      if (kind == kEpiStoreF32) YGG_CHECK_ARG(e.out && e.ld >= g->N, "STORE_F32 needs out / ld");
+      if (kind == kEpiQkvRope)
+        YGG_CHECK_ARG(e.q_out && e.cache && e.pos && e.slot && e.req && e.hd % 2 == 0 &&
+                          g->N == (e.Hq + 2 * e.Hkv) * e.hd && kBM % e.hd == 0,
+                      "QKV_ROPE arguments");
+      if (kind == kEpiSwiglu) YGG_CHECK_ARG(e.act_out != nullptr, "SWIGLU needs act_out");
+      if (kind == kEpiResid) YGG_CHECK_ARG(e.resid && e.hb && e.ss_out, "RESID needs resid / hb / ss_out");
+    }
+    switch (kind) {
+      case kEpiNone:
+        YGG_LAUNCH_PDL(gemm_bf16_tc_kernel<kEpiNone>, dim3(g->num_ctas), dim3(kGemmThreads), smem, s, g->tmap_w,
+                       g->tmap_x, p, workspace, e);
+        break;
+      case kEpiStoreF32:
+        YGG_LAUNCH_PDL(gemm_bf16_tc_kernel<kEpiStoreF32>, dim3(g->num_ctas), dim3(kGemmThreads), smem, s, g->tmap_w,
+                       g->tmap_x, p, workspace, e);
+        break;
+      case kEpiQkvRope:
+        YGG_LAUNCH_PDL(gemm_bf16_tc_kernel<kEpiQkvRope>, dim3(g->num_ctas), dim3(kGemmThreads), smem, s, g->tmap_w,
+                       g->tmap_x, p, workspace, e);
+        break;
+      case kEpiSwiglu:
+        YGG_LAUNCH_PDL(gemm_bf16_tc_kernel<kEpiSwiglu>, dim3(g->num_ctas), dim3(kGemmThreads), smem, s, g->tmap_w,
+                       g->tmap_x, p, workspace, e);
+        break;
+      case kEpiResid:
+        YGG_LAUNCH_PDL(gemm_bf16_tc_kernel<kEpiResid>, dim3(g->num_ctas), dim3(kGemmThreads), smem, s, g->tmap_w,
+                       g->tmap_x, p, workspace, e);
+        break;
+      default:
+        return ygg_fail(YGG_ERR_VALUE, "unknown epilogue kind %d", kind);
+    }
   } else {
+    YGG_CHECK_ARG(epi == nullptr || epi->kind == kEpiNone, "fused epilogues run on the bf16 tcgen05 path only");
     dim3 grid(g->n_tiles, (g->M + kSimtBN - 1) / kSimtBN);
     YGG_LAUNCH_PDL(gemm_f32_simt_kernel, grid, dim3(256), 0, s, static_cast<const float*>(g->W),
                    static_cast<const float*>(g->X), g->M, g->N, g->K, g->BN, g->m_tiles, workspace);
   }
   return YGG_OK;
+}
+
+int ygg_gemm_run(const void* plan, float* workspace, ygg_stream_t stream) {
+  const GemmPlan* g = plan_of(plan);
+  YGG_CHECK_ARG(g != nullptr, "invalid GEMM plan");
+  YGG_CHECK_ARG(workspace != nullptr, "null workspace");
+  return gemm_launch(g, workspace, nullptr, reinterpret_cast<cudaStream_t>(stream));
+}
+
+int ygg_gemm_fused(const void* plan, float* workspace, const ygg_epilogue* epi, ygg_stream_t stream) {
+  const GemmPlan* g = plan_of(plan);
+  YGG_CHECK_ARG(g != nullptr, "invalid GEMM plan");
+  YGG_CHECK_ARG(workspace != nullptr && epi != nullptr, "null workspace / epilogue");
+  return gemm_launch(g, workspace, epi, reinterpret_cast<cudaStream_t>(stream));
+}
+
+int ygg_gemm_tiles(const void* plan) {
+  const GemmPlan* g = plan_of(plan);
+  return g ? g->tiles : -1;
 }
 
 int ygg_epi_store(const void* plan, const float* ws, void* out, int out_dtype, int ld_out, ygg_stream_t stream) {

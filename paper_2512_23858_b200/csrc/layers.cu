@@ -20,6 +20,32 @@ __global__ void embed_kernel(const T* __restrict__ table, int V, int d, const in
   for (int i = threadIdx.x; i < d; i += blockDim.x) out[static_cast<size_t>(m) * d + i] = to_f32(row[i]);
 }
 
+// Embedding for the fused path: 128 threads = one 128-feature tile at a time; writes the f32
+// residual, its bf16 copy (next GEMM operand) and the tile's sum of squares (fixed-order reduce).
+__global__ void __launch_bounds__(128) embed_fused_kernel(const __nv_bfloat16* __restrict__ table, int V, int d,
+                                                          const int32_t* __restrict__ tokens, float* __restrict__ resid,
+                                                          __nv_bfloat16* __restrict__ hb, float* __restrict__ ss_out,
+                                                          int M) {
+  pdl_wait();
+  pdl_launch_dependents();
+  __shared__ float red[4];
+  const int m = blockIdx.x;
+  int tok = tokens[m];
+  tok = tok < 0 ? 0 : (tok >= V ? V - 1 : tok);
+  for (int t = 0; t < d / 128; ++t) {
+    const int n = t * 128 + threadIdx.x;
+    const __nv_bfloat16 x = table[static_cast<size_t>(tok) * d + n];
+    const float h = __bfloat162float(x);
+    resid[static_cast<size_t>(m) * d + n] = h;
+    hb[static_cast<size_t>(m) * d + n] = x;
+    float s = warp_sum(h * h);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) ss_out[static_cast<size_t>(t) * M + m] = red[0] + red[1] + red[2] + red[3];
+    __syncthreads();
+  }
+}
+
 template <typename T>
 __global__ void __launch_bounds__(256) rmsnorm_kernel(const float* __restrict__ x, const T* __restrict__ w, int d,
                                                       float eps, T* __restrict__ out) {
@@ -243,6 +269,17 @@ int ygg_embed(const void* table, int dtype, int V, int d, const int32_t* tokens,
   else
     YGG_LAUNCH_PDL(embed_kernel<__nv_bfloat16>, dim3(M), dim3(256), 0, s, static_cast<const __nv_bfloat16*>(table), V,
                    d, tokens, resid_out);
+  return YGG_OK;
+}
+
+int ygg_embed_fused(const void* table, int V, int d, const int32_t* tokens, int M, float* resid, void* hb,
+                    float* ss_out, ygg_stream_t stream) {
+  YGG_CHECK_ARG(table && tokens && resid && hb && ss_out && V >= 1, "invalid arguments");
+  YGG_CHECK_ARG(d % 128 == 0, "model width must be a multiple of 128");
+  if (M <= 0) return YGG_OK;
+  YGG_LAUNCH_PDL(embed_fused_kernel, dim3(M), dim3(128), 0, reinterpret_cast<cudaStream_t>(stream),
+                 static_cast<const __nv_bfloat16*>(table), V, d, tokens, resid, static_cast<__nv_bfloat16*>(hb),
+                 ss_out, M);
   return YGG_OK;
 }
 

@@ -6,9 +6,17 @@ so a pass is a fixed sequence of kernel launches that CUDA-graph capture records
 It realises the verifier / drafter forward the reference only prices
 (``latency_at(profiles.verifier, w_verify + 1)``, pkg/src/specsim/simulator.py:211-213).
 
-Per layer: GEMM(qkv) -> RoPE + KV append -> tree attention -> GEMM(o) -> residual + RMSNorm
--> GEMM(gate|up) -> SwiGLU -> GEMM(down) -> residual + next RMSNorm.  The residual stream is
-f32; activations are bf16 (fast path) or f32 (parity path).
+bf16 (fast path) — 6 launches per layer, every epilogue fused into its GEMM:
+  GEMM(qkv, x=hb)  + rstd + RoPE + q / KV-cache append      (YGG_EPI_QKV_ROPE)
+  tcgen05 split-KV tree attention + combine
+  GEMM(o)          + residual add, hb, per-tile sum-of-squares (YGG_EPI_RESID)
+  GEMM(gate|up, x=hb) + rstd + SwiGLU                        (YGG_EPI_SWIGLU)
+  GEMM(down)       + residual add, hb, sum-of-squares          (YGG_EPI_RESID)
+RMSNorm gains are folded into the next weights (model.prepare_fused_) and the per-token rstd is
+applied by the consuming GEMM's epilogue, so no separate norm kernel exists.
+
+f32 (parity path): SIMT GEMM + separate epilogue kernels + SIMT attention, unfused, in the
+reference layout.  The residual stream is f32 in both paths.
 """
 
 from __future__ import annotations
@@ -19,7 +27,7 @@ import math
 import torch
 
 from . import _lib as L
-from .model import ModelConfig
+from .model import ModelConfig, prepare_fused_
 
 
 class GemmPlan:
@@ -34,6 +42,7 @@ class GemmPlan:
         mp = (M + 15) // 16 * 16
         bn = min(mp, 256)
         tiles = (N // 128) * ((M + bn - 1) // bn)
+        self.tiles = tiles
         self.seg_table = torch.zeros(tiles + 1 + 160, dtype=torch.int32, device=W.device)
         nseg, wsb = C.c_int(), C.c_size_t()
         L.check(
@@ -45,6 +54,7 @@ class GemmPlan:
         self.segments = nseg.value
         self.ws_bytes = wsb.value
         self.W, self.X = W, X  # keep alive
+        self.epi = None  # L.YggEpilogue for the fused path
 
     @property
     def handle(self):
@@ -81,11 +91,15 @@ class Forward:
         num_ctas: int = 0,
     ):
         L.require_device()
-        self.cfg, self.w, self.cache = cfg, weights, cache
+        self.cfg, self.cache = cfg, cache
         self.B, self.R, self.M = B, R, B * R
         self.mask_words = mask_words
         self.act_dtype = act_dtype
         self.act = L.dtype_code(act_dtype)
+        self.fused = act_dtype == torch.bfloat16
+        if self.fused:
+            prepare_fused_(weights, cfg)
+        self.w = weights
         dev = cache.device
         M, d = self.M, cfg.d_model
         i32 = dict(dtype=torch.int32, device=dev)
@@ -99,11 +113,14 @@ class Forward:
         self.blk_len = torch.zeros(B, **i32)
         # activations
         self.resid = torch.zeros(M, d, dtype=torch.float32, device=dev)
-        self.xn = torch.zeros(M, d, dtype=act_dtype, device=dev)
+        self.xn = torch.zeros(M, d, dtype=act_dtype, device=dev)  # f32 path: normalised input; bf16: hb
         self.q = torch.zeros(M, cfg.q_dim, dtype=act_dtype, device=dev)
         self.attn = torch.zeros(M, cfg.q_dim, dtype=act_dtype, device=dev)
         self.mlp = torch.zeros(M, cfg.ffn, dtype=act_dtype, device=dev)
         self.logits = torch.zeros(M, cfg.vocab, dtype=torch.float32, device=dev) if logits else None
+        self.layer_stride = cache.stride(0)
+        self.S = cache.shape[4]
+        self.scale = 1.0 / math.sqrt(cfg.head_dim)
         self.plans = []
         ws = 0
         for lw in weights["layers"]:
@@ -119,18 +136,51 @@ class Forward:
         if self.lm_plan:
             ws = max(ws, self.lm_plan.ws_bytes)
         self.ws = torch.empty(max(ws // 4, 1), dtype=torch.float32, device=dev)
-        self.layer_stride = cache.stride(0)
-        self.S = cache.shape[4]
-        # bf16: tcgen05 split-KV attention (one plan per layer); f32 parity path: SIMT attention.
         self.attn_plans = None
-        if act_dtype == torch.bfloat16 and mask_words <= L.MAX_MASK_WORDS:
+        if self.fused:
             es = cache.element_size()
             self.attn_plans = [AttnPlan(self.q, cache.data_ptr() + li * self.layer_stride * es, B, M, cfg, self.S)
                                for li in range(cfg.n_layers)]
             self.attn_part = torch.empty(self.attn_plans[0].partial_bytes // 4 + 1, dtype=torch.float32, device=dev)
-        self.scale = 1.0 / math.sqrt(cfg.head_dim)
-        # stage hooks: optional callables(stage_name, stream) for the on-device profiler (K8)
-        self.hooks = None
+            self._setup_fused()
+
+    # ------------------------------------------------------------------
+    def _setup_fused(self) -> None:
+        cfg, M, d = self.cfg, self.M, self.cfg.d_model
+        dev = self.cache.device
+        nt = d // 128
+        self.ss_a = torch.zeros(nt, M, dtype=torch.float32, device=dev)
+        self.ss_b = torch.zeros(nt, M, dtype=torch.float32, device=dev)
+        max_tiles = max(p.tiles for layer in self.plans for p in layer.values())
+        if self.lm_plan:
+            max_tiles = max(max_tiles, self.lm_plan.tiles)
+        self.counters = torch.zeros(max_tiles, dtype=torch.int32, device=dev)
+        eps = float(cfg.norm_eps)
+        es = self.cache.element_size()
+
+        def epi(kind, **kw):
+            e = L.YggEpilogue()
+            e.kind = kind
+            e.counters = self.counters.data_ptr()
+            for k, v in kw.items():
+                setattr(e, k, v)
+            return e
+
+        for li, p in enumerate(self.plans):
+            cache_l = self.cache.data_ptr() + li * self.layer_stride * es
+            p["qkv"].epi = epi(L.YGG_EPI_QKV_ROPE, ss_in=self.ss_a.data_ptr(), ss_tiles=nt, norm_dim=d, eps=eps,
+                               q_out=self.q.data_ptr(), cache=cache_l, S=self.S, Hq=cfg.n_heads, Hkv=cfg.n_kv_heads,
+                               hd=cfg.head_dim, rope_theta=cfg.rope_theta, pos=self.pos.data_ptr(),
+                               slot=self.slot.data_ptr(), req=self.req.data_ptr())
+            p["o"].epi = epi(L.YGG_EPI_RESID, resid=self.resid.data_ptr(), hb=self.xn.data_ptr(),
+                             ss_out=self.ss_b.data_ptr())
+            p["gu"].epi = epi(L.YGG_EPI_SWIGLU, ss_in=self.ss_b.data_ptr(), ss_tiles=nt, norm_dim=d, eps=eps,
+                              act_out=self.mlp.data_ptr())
+            p["down"].epi = epi(L.YGG_EPI_RESID, resid=self.resid.data_ptr(), hb=self.xn.data_ptr(),
+                                ss_out=self.ss_a.data_ptr())
+        if self.lm_plan:
+            self.lm_plan.epi = epi(L.YGG_EPI_STORE_F32, ss_in=self.ss_a.data_ptr(), ss_tiles=nt, norm_dim=d, eps=eps,
+                                   out=self.logits.data_ptr(), ld=cfg.vocab)
 
     def weight_bytes(self) -> int:
         """Algorithmic HBM bytes of the matmul weights streamed per pass."""
@@ -141,7 +191,48 @@ class Forward:
             total += self.lm_plan.W.numel() * self.lm_plan.W.element_size()
         return total
 
+    def gemm_calls(self):
+        """(plan, epilogue) of every GEMM launch of one pass, in order (for per-launch timing)."""
+        out = []
+        for p in self.plans:
+            out += [p["qkv"], p["o"], p["gu"], p["down"]]
+        if self.lm_plan:
+            out.append(self.lm_plan)
+        return out
+
+    def launch_gemm(self, plan: GemmPlan, stream_ptr) -> None:
+        lib = L.lib()
+        if self.fused:
+            L.check(lib.ygg_gemm_fused(plan.handle, self.ws.data_ptr(), C.byref(plan.epi), stream_ptr))
+        else:
+            L.check(lib.ygg_gemm_run(plan.handle, self.ws.data_ptr(), stream_ptr))
+
     def run(self, stream: torch.cuda.Stream | None = None) -> None:
+        if self.fused:
+            self._run_fused(stream)
+        else:
+            self._run_unfused(stream)
+
+    def _run_fused(self, stream) -> None:
+        lib, cfg = L.lib(), self.cfg
+        s = L.stream_ptr(stream)
+        chk = L.check
+        ws = self.ws.data_ptr()
+        chk(lib.ygg_embed_fused(self.w["embed"].data_ptr(), cfg.vocab, cfg.d_model, self.tokens.data_ptr(), self.M,
+                                self.resid.data_ptr(), self.xn.data_ptr(), self.ss_a.data_ptr(), s))
+        qm = self.qmask.data_ptr() if self.mask_words > 0 else None
+        for li, p in enumerate(self.plans):
+            chk(lib.ygg_gemm_fused(p["qkv"].handle, ws, C.byref(p["qkv"].epi), s))
+            chk(lib.ygg_attention_tc(self.attn_plans[li].handle, self.blk_start.data_ptr(), self.blk_len.data_ptr(),
+                                     qm, self.mask_words, self.scale, self.attn_part.data_ptr(),
+                                     self.attn.data_ptr(), s))
+            chk(lib.ygg_gemm_fused(p["o"].handle, ws, C.byref(p["o"].epi), s))
+            chk(lib.ygg_gemm_fused(p["gu"].handle, ws, C.byref(p["gu"].epi), s))
+            chk(lib.ygg_gemm_fused(p["down"].handle, ws, C.byref(p["down"].epi), s))
+        if self.lm_plan is not None:
+            chk(lib.ygg_gemm_fused(self.lm_plan.handle, ws, C.byref(self.lm_plan.epi), s))
+
+    def _run_unfused(self, stream) -> None:
         lib, cfg = L.lib(), self.cfg
         s = L.stream_ptr(stream)
         chk = L.check
@@ -154,21 +245,16 @@ class Forward:
                             cfg.norm_eps, self.xn.data_ptr(), s))
         ws = self.ws.data_ptr()
         nl = len(self.plans)
+        qm = self.qmask.data_ptr() if self.mask_words > 0 else None
         for li, (p, lw) in enumerate(zip(self.plans, w["layers"])):
             cache_l = self.cache.data_ptr() + li * self.layer_stride * self.cache.element_size()
             chk(lib.ygg_gemm_run(p["qkv"].handle, ws, s))
             chk(lib.ygg_epi_qkv_rope(p["qkv"].handle, ws, cfg.n_heads, cfg.n_kv_heads, cfg.head_dim,
                                      cfg.rope_theta, self.pos.data_ptr(), self.slot.data_ptr(),
                                      self.req.data_ptr(), self.q.data_ptr(), cache_l, self.S, self.act, s))
-            qm = self.qmask.data_ptr() if self.mask_words > 0 else None
-            if self.attn_plans is not None:
-                chk(lib.ygg_attention_tc(self.attn_plans[li].handle, self.blk_start.data_ptr(),
-                                         self.blk_len.data_ptr(), qm, self.mask_words, self.scale,
-                                         self.attn_part.data_ptr(), self.attn.data_ptr(), s))
-            else:
-                chk(lib.ygg_attention(self.q.data_ptr(), cache_l, self.act, M, self.B, cfg.n_heads, cfg.n_kv_heads,
-                                      cfg.head_dim, self.S, self.blk_start.data_ptr(), self.blk_len.data_ptr(),
-                                      qm, self.mask_words, self.scale, self.attn.data_ptr(), s))
+            chk(lib.ygg_attention(self.q.data_ptr(), cache_l, self.act, M, self.B, cfg.n_heads, cfg.n_kv_heads,
+                                  cfg.head_dim, self.S, self.blk_start.data_ptr(), self.blk_len.data_ptr(),
+                                  qm, self.mask_words, self.scale, self.attn.data_ptr(), s))
             chk(lib.ygg_gemm_run(p["o"].handle, ws, s))
             chk(lib.ygg_epi_residual_norm(p["o"].handle, ws, self.resid.data_ptr(), lw["mlp_norm"].data_ptr(),
                                           cfg.norm_eps, self.xn.data_ptr(), self.act, s))

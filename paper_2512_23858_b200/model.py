@@ -175,3 +175,42 @@ def weights_to(w: dict, device, dtype: torch.dtype | None = None) -> dict:
     }
     out["lm_head"] = out["embed"] if w["lm_head"] is w["embed"] else mv(w["lm_head"])
     return out
+
+
+def qkv_row_permutation(cfg: ModelConfig) -> torch.Tensor:
+    """Row order of the fused-path QKV weight: inside every head, RoPE pairs (i, i + hd/2) become
+    adjacent rows (new row 2i <- i, 2i+1 <- i + hd/2) so one warp-lane pair holds a rotation pair."""
+    hd, half = cfg.head_dim, cfg.head_dim // 2
+    heads = cfg.n_heads + 2 * cfg.n_kv_heads
+    within = torch.stack([torch.arange(half), torch.arange(half) + half], 1).reshape(-1)
+    return (torch.arange(heads)[:, None] * hd + within[None, :]).reshape(-1)
+
+
+def gate_up_interleave(cfg: ModelConfig) -> torch.Tensor:
+    """Row order of the fused-path gate|up weight: row 2j <- gate j, row 2j+1 <- up j."""
+    F = cfg.ffn
+    return torch.stack([torch.arange(F), torch.arange(F) + F], 1).reshape(-1)
+
+
+def prepare_fused_(w: dict, cfg: ModelConfig) -> dict:
+    """In-place conversion to the fused bf16 layout (idempotent): RMSNorm gains folded into the
+    following matmul (wqkv, wgu, lm_head columns), QKV rows RoPE-pair-interleaved, gate/up rows
+    interleaved.  The per-token rstd is applied by the consumer GEMM's epilogue."""
+    if w.get("_layout") == "fused":
+        return w
+    dev = w["embed"].device
+    qperm = qkv_row_permutation(cfg).to(dev)
+    gperm = gate_up_interleave(cfg).to(dev)
+    for lw in w["layers"]:
+        an = lw["attn_norm"].float()
+        mn = lw["mlp_norm"].float()
+        lw["wqkv"] = (lw["wqkv"].float() * an[None, :]).to(lw["wqkv"].dtype)[qperm].contiguous()
+        lw["wgu"] = (lw["wgu"].float() * mn[None, :]).to(lw["wgu"].dtype)[gperm].contiguous()
+        lw["attn_norm"] = torch.ones_like(lw["attn_norm"])
+        lw["mlp_norm"] = torch.ones_like(lw["mlp_norm"])
+    fn = w["final_norm"].float()
+    if not bool(torch.all(fn == 1)):
+        w["lm_head"] = (w["lm_head"].float() * fn[None, :]).to(w["lm_head"].dtype)
+    w["final_norm"] = torch.ones_like(w["final_norm"])
+    w["_layout"] = "fused"
+    return w

@@ -1,0 +1,133 @@
+"""Fused tcgen05 GEMM epilogues vs torch fp64 references of the same bf16 operands.
+
+Covers single-segment tiles (finished from TMEM) and multi-segment stream-K tiles (last-arrival
+reduction), via different CTA counts.  Tolerance: 2e-3 relative to the output scale (bf16
+operands are exact; f32 accumulation order differs), and bf16 rounding of stored outputs.
+"""
+
+import math
+
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+def _plan(W, X, M, ctas):
+    from paper_2512_23858_b200.forward import GemmPlan
+
+    return GemmPlan(W, X, M, ctas)
+
+
+def _run(plan, epi, cuda):
+    from paper_2512_23858_b200 import _lib as L
+    import ctypes as C
+
+    ws = torch.zeros(plan.ws_bytes // 4 + 16, device=cuda)
+    L.check(L.lib().ygg_gemm_fused(plan.handle, ws.data_ptr(), C.byref(epi), L.stream_ptr()))
+    torch.cuda.synchronize()
+
+
+def _epi(kind, counters, **kw):
+    from paper_2512_23858_b200 import _lib as L
+
+    e = L.YggEpilogue()
+    e.kind = kind
+    e.counters = counters.data_ptr()
+    for k, v in kw.items():
+        setattr(e, k, v)
+    return e
+
+
+@pytest.mark.parametrize("ctas", [0, 5, 37])
+@pytest.mark.parametrize("M", [8, 50, 300])
+def test_store_f32_with_rstd(ctas, M, cuda):
+    from paper_2512_23858_b200 import _lib as L
+
+    N, K = 1024, 512
+    g = torch.Generator(device="cuda").manual_seed(M + ctas)
+    X = torch.randn(M, K, device=cuda, generator=g).to(torch.bfloat16)
+    W = (torch.randn(N, K, device=cuda, generator=g) / math.sqrt(K)).to(torch.bfloat16)
+    ss = torch.rand(4, M, device=cuda, generator=g) * 100
+    out = torch.zeros(M, N, device=cuda)
+    plan = _plan(W, X, M, ctas)
+    cnt = torch.zeros(plan.tiles, dtype=torch.int32, device=cuda)
+    _run(plan, _epi(L.YGG_EPI_STORE_F32, cnt, ss_in=ss.data_ptr(), ss_tiles=4, norm_dim=512, eps=1e-5,
+                    out=out.data_ptr(), ld=N), cuda)
+    rstd = torch.rsqrt(ss.double().sum(0) / 512 + 1e-5)
+    ref = (X.double() @ W.double().T) * rstd[:, None]
+    assert (out.double() - ref).abs().max() <= 2e-3 * ref.abs().max()
+    assert int(cnt.abs().sum()) == 0  # counters self-reset
+
+
+@pytest.mark.parametrize("ctas", [0, 11])
+def test_resid_and_swiglu(ctas, cuda):
+    from paper_2512_23858_b200 import _lib as L
+    from paper_2512_23858_b200.model import gate_up_interleave, preset
+
+    M, d, F = 40, 512, 768
+    g = torch.Generator(device="cuda").manual_seed(ctas + 3)
+    # RESID: resid += X W^T, hb = bf16(resid), ss per 128-feature tile
+    X = torch.randn(M, F, device=cuda, generator=g).to(torch.bfloat16)
+    W = (torch.randn(d, F, device=cuda, generator=g) / math.sqrt(F)).to(torch.bfloat16)
+    resid = torch.randn(M, d, device=cuda, generator=g)
+    r0 = resid.clone()
+    hb = torch.zeros(M, d, dtype=torch.bfloat16, device=cuda)
+    ss = torch.zeros(d // 128, M, device=cuda)
+    plan = _plan(W, X, M, ctas)
+    cnt = torch.zeros(plan.tiles, dtype=torch.int32, device=cuda)
+    _run(plan, _epi(L.YGG_EPI_RESID, cnt, resid=resid.data_ptr(), hb=hb.data_ptr(), ss_out=ss.data_ptr()), cuda)
+    ref = r0.double() + X.double() @ W.double().T
+    assert (resid.double() - ref).abs().max() <= 2e-3 * ref.abs().max()
+    assert torch.equal(hb, resid.to(torch.bfloat16))
+    ref_ss = (resid.double() ** 2).view(M, d // 128, 128).sum(-1).T
+    assert torch.allclose(ss.double(), ref_ss, rtol=1e-5)
+    # SWIGLU with interleaved gate/up rows
+    cfg = preset("tiny-target", ffn=F, d_model=d)
+    Xs = torch.randn(M, d, device=cuda, generator=g).to(torch.bfloat16)
+    Wgu = (torch.randn(2 * F, d, device=cuda, generator=g) / math.sqrt(d)).to(torch.bfloat16)
+    Wp = Wgu[gate_up_interleave(cfg).to(cuda)].contiguous()
+    act = torch.zeros(M, F, dtype=torch.bfloat16, device=cuda)
+    plan2 = _plan(Wp, Xs, M, ctas)
+    cnt2 = torch.zeros(plan2.tiles, dtype=torch.int32, device=cuda)
+    _run(plan2, _epi(L.YGG_EPI_SWIGLU, cnt2, act_out=act.data_ptr()), cuda)
+    gu = Xs.double() @ Wgu.double().T
+    ref2 = torch.nn.functional.silu(gu[:, :F]) * gu[:, F:]
+    assert (act.double() - ref2).abs().max() <= 1e-2 * ref2.abs().max()
+
+
+@pytest.mark.parametrize("hd,Hq,Hkv", [(64, 4, 2), (128, 8, 2)])
+@pytest.mark.parametrize("ctas", [0, 9])
+def test_qkv_rope_kv_append(hd, Hq, Hkv, ctas, cuda):
+    from oracle.llama_ref import rope
+    from paper_2512_23858_b200 import _lib as L
+    from paper_2512_23858_b200.model import preset, qkv_row_permutation
+
+    M, d, S, B = 12, 256, 64, 2
+    cfg = preset("tiny-target", d_model=d, n_heads=Hq, n_kv_heads=Hkv, head_dim=hd)
+    g = torch.Generator(device="cuda").manual_seed(hd + ctas)
+    X = torch.randn(M, d, device=cuda, generator=g).to(torch.bfloat16)
+    W = (torch.randn(cfg.qkv_dim, d, device=cuda, generator=g) / math.sqrt(d)).to(torch.bfloat16)
+    Wp = W[qkv_row_permutation(cfg).to(cuda)].contiguous()
+    pos = torch.randint(0, 1000, (M,), device=cuda, dtype=torch.int32)
+    slot = torch.arange(M, device=cuda, dtype=torch.int32) % (M // B) + 5
+    req = torch.arange(M, device=cuda, dtype=torch.int32) // (M // B)
+    q = torch.zeros(M, Hq, hd, dtype=torch.bfloat16, device=cuda)
+    cache = torch.zeros(B, 2, Hkv, S, hd, dtype=torch.bfloat16, device=cuda)
+    plan = _plan(Wp, X, M, ctas)
+    cnt = torch.zeros(plan.tiles, dtype=torch.int32, device=cuda)
+    _run(plan, _epi(L.YGG_EPI_QKV_ROPE, cnt, q_out=q.data_ptr(), cache=cache.data_ptr(), S=S, Hq=Hq, Hkv=Hkv,
+                    hd=hd, rope_theta=cfg.rope_theta, pos=pos.data_ptr(), slot=slot.data_ptr(),
+                    req=req.data_ptr()), cuda)
+    y = (X.double() @ W.double().T).float().cpu()
+    qr = rope(y[:, : Hq * hd].view(M, Hq, hd), pos.cpu(), cfg.rope_theta)
+    kr = rope(y[:, Hq * hd : (Hq + Hkv) * hd].view(M, Hkv, hd), pos.cpu(), cfg.rope_theta)
+    v = y[:, (Hq + Hkv) * hd :].view(M, Hkv, hd)
+    tol = 2e-2 * float(y.abs().max())
+    assert (q.float().cpu() - qr).abs().max() <= tol
+    c = cache.float().cpu()
+    for m in range(M):
+        b, s = int(req[m]), int(slot[m])
+        assert (c[b, 0, :, s, :] - kr[m]).abs().max() <= tol
+        vt = c[b, 1].reshape(Hkv, hd, S)[:, :, s]  # V^T [hd][S]
+        assert (vt - v[m]).abs().max() <= tol

@@ -27,8 +27,8 @@ constexpr int kBM = 128;          // weight rows per tile (UMMA M)
 constexpr int kBK = 64;           // k per stage: 64 bf16 = one 128B swizzle row
 constexpr int kGemmThreads = 192; // 6 warps
 constexpr int kMaxRstdTokensHost = 1024;
-// alignment slack + barriers (<= 2*12+4 u64) + tmem slot/flag + red_s[64] + rstd_s[1024]
-constexpr int kSmemExtra = 1024 + 28 * 8 + 16 + 64 * 4 + kMaxRstdTokensHost * 4;
+// alignment slack + barriers (<= 2*12+4 u64) + tmem slot/pending + red_s[64] + rstd_s[1024]
+constexpr int kSmemExtra = 1024 + 28 * 8 + 32 + 64 * 4 + kMaxRstdTokensHost * 4;
 
 struct GemmPlan {
   uint32_t magic;
@@ -57,10 +57,14 @@ struct GemmParams {
 };
 
 // ---------------------------------------------------------------------------
-// Fused epilogues.  The last CTA to finish a tile (per-tile arrival counter) reduces the tile's
-// partials in segment order and applies the op; a tile owned by one CTA is finished straight
-// from TMEM.  RMSNorm is folded: its gain lives in the next weight matrix and the per-token
-// rstd (from the producer's per-tile sums of squares) scales the consumer's output rows.
+// Fused epilogues.  A tile owned by one CTA is finished straight from TMEM.  A tile split over
+// several stream-K CTAs is finished cooperatively: every participant publishes its f32 partial
+// and, at the end of its own range, waits for the tile's arrival counter and reduces a disjoint
+// slice of token columns in fixed segment order (deterministic) before applying the op.  The
+// grid is persistent (<= one CTA per SM), so all participants are co-resident and the wait is
+// short; concurrently running fused GEMMs must therefore split the SMs between them.
+// RMSNorm is folded: its gain lives in the next weight matrix and the per-token rstd (from the
+// producer's per-tile sums of squares) scales the consumer's output rows.
 // ---------------------------------------------------------------------------
 enum EpiKind : int { kEpiNone = 0, kEpiStoreF32 = 1, kEpiQkvRope = 2, kEpiSwiglu = 3, kEpiResid = 4 };
 constexpr int kMaxRstdTokens = 1024;
@@ -88,6 +92,11 @@ struct EpiArgs {
 };
 
 YGG_DEV void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+YGG_DEV int ld_acquire(const int32_t* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
 
 // Apply the fused op to 16 token columns of one 128-feature tile row (thread = feature row).
 template <int KIND>
@@ -193,8 +202,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   uint64_t* tfull = empty + S;   // [2]
   uint64_t* tempty = tfull + 2;  // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
-  int* flag_s = reinterpret_cast<int*>(tmem_slot + 1);
-  float* red_s = reinterpret_cast<float*>(tmem_slot + 4);  // [4][16]
+  int* pend_tile = reinterpret_cast<int*>(tmem_slot + 1);  // [2] deferred fixups of split tiles
+  int* pend_j = pend_tile + 2;                               // [2] participant index in the tile
+  float* red_s = reinterpret_cast<float*>(tmem_slot + 8);    // [4][16]
   float* rstd_s = red_s + 64;                               // [kMaxRstdTokens]
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -306,6 +316,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     }
     int acc = 0;
     uint32_t acc_phase[2] = {0u, 0u};
+    int npend = 0;
     long long u = u0;
     while (u < u1) {
       const int tile = static_cast<int>(u / p.kb);
@@ -341,34 +352,58 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         tc_fence_before();
         mbar_arrive(&tempty[acc]);
         if (KIND != kEpiNone) {
+          // Publish the partial; the reduction is deferred to the end of this CTA's range so the
+          // TMEM pipeline never waits on another CTA.  Only the first and last segment of a
+          // stream-K range can be partial tiles, so at most two are pending.
           __threadfence();
           epi_bar();
-          if (et == 0) *flag_s = (atomicAdd(e.counters + tile, 1) == nseg - 1);
-          epi_bar();
-          if (*flag_s) {
-            // Last arrival: reduce every segment of the tile in segment order, then apply the op.
-            __threadfence();
-            const float* src = ws + static_cast<size_t>(s_first) * BN * kBM + row;
-            for (int c0 = 0; c0 < BN; c0 += 16) {
-              float v[16];
-#pragma unroll
-              for (int j = 0; j < 16; ++j) v[j] = 0.f;
-              for (int s = 0; s < nseg; ++s) {
-                const float* q = src + static_cast<size_t>(s) * BN * kBM;
-#pragma unroll
-                for (int j = 0; j < 16; ++j)
-                  if (c0 + j < valid) v[j] += __ldcg(q + static_cast<size_t>(c0 + j) * kBM);
-              }
-              epi_apply<KIND>(e, p.M, n, m_tile * BN + c0, valid - c0, v, rstd_s, red_s, quarter, lane);
-            }
-            if (et == 0) e.counters[tile] = 0;
+          if (et == 0) {
+            atomicAdd(e.counters + tile, 1);
+            pend_tile[npend] = tile;
+            pend_j[npend] = seg - s_first;
           }
-          epi_bar();  // flag_s is reused by the next tile
+          ++npend;
         }
       }
       acc_phase[acc] ^= 1u;
       acc ^= 1;
       u = seg_end;
+    }
+    // Cooperative fixups: once all nseg partials of a split tile have arrived, participant j
+    // reduces 16-token column chunks j, j+nseg, ... in fixed segment order and applies the op.
+    for (int i = 0; i < npend; ++i) {
+      epi_bar();
+      const int tile = pend_tile[i], j = pend_j[i];
+      const int s_first = p.seg_first[tile];
+      const int nseg = p.seg_first[tile + 1] - s_first;
+      const int m_tile = tile % p.m_tiles, n_tile = tile / p.m_tiles;
+      const int valid = min(BN, p.M - m_tile * BN);
+      const int n = n_tile * kBM + row;
+      if (et == 0) {
+        const long long t0 = clock64();
+        while (ld_acquire(e.counters + tile) < nseg) {
+          __nanosleep(64);
+          if (clock64() - t0 > (1ll << 34)) __trap();
+        }
+      }
+      epi_bar();
+      const float* src = ws + static_cast<size_t>(s_first) * BN * kBM + row;
+      for (int c0 = j * 16; c0 < BN; c0 += nseg * 16) {
+        float v[16];
+#pragma unroll
+        for (int q = 0; q < 16; ++q) v[q] = 0.f;
+#pragma unroll 2
+        for (int s = 0; s < nseg; ++s) {
+          const float* ps = src + static_cast<size_t>(s) * BN * kBM;
+#pragma unroll
+          for (int q = 0; q < 16; ++q)
+            if (c0 + q < valid) v[q] += __ldcg(ps + static_cast<size_t>(c0 + q) * kBM);
+        }
+        epi_apply<KIND>(e, p.M, n, m_tile * BN + c0, valid - c0, v, rstd_s, red_s, quarter, lane);
+      }
+      epi_bar();
+      // Second-phase arrival: the last participant to finish reading resets the counter.
+      if (et == 0 && atomicAdd(e.counters + tile, 1) == 2 * nseg - 1) e.counters[tile] = 0;
     }
   }
   __syncthreads();

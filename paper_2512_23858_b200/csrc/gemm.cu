@@ -309,6 +309,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     if (KIND != kEpiNone && e.ss_in) {
       for (int m = et; m < p.M; m += 128) {
         float s = 0.f;
+#pragma unroll 16
         for (int t = 0; t < e.ss_tiles; ++t) s += __ldg(e.ss_in + static_cast<size_t>(t) * p.M + m);
         rstd_s[m] = rsqrtf(s / static_cast<float>(e.norm_dim) + e.eps);
       }
@@ -352,13 +353,12 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         tc_fence_before();
         mbar_arrive(&tempty[acc]);
         if (KIND != kEpiNone) {
-          // Publish the partial; the reduction is deferred to the end of this CTA's range so the
-          // TMEM pipeline never waits on another CTA.  Only the first and last segment of a
-          // stream-K range can be partial tiles, so at most two are pending.
-          __threadfence();
+          // Publish the partial (CTA barrier, then one release-ordered arrival); the reduction is
+          // deferred to the end of this CTA's range so the TMEM pipeline never waits on another
+          // CTA.  Only the first and last segment of a range can be partial tiles (<= 2 pending).
           epi_bar();
           if (et == 0) {
-            atomicAdd(e.counters + tile, 1);
+            asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(e.counters + tile) : "memory");
             pend_tile[npend] = tile;
             pend_j[npend] = seg - s_first;
           }
@@ -389,15 +389,24 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       epi_bar();
       const float* src = ws + static_cast<size_t>(s_first) * BN * kBM + row;
       for (int c0 = j * 16; c0 < BN; c0 += nseg * 16) {
+        const int nv = min(16, valid - c0);
         float v[16];
 #pragma unroll
         for (int q = 0; q < 16; ++q) v[q] = 0.f;
-#pragma unroll 2
-        for (int s = 0; s < nseg; ++s) {
-          const float* ps = src + static_cast<size_t>(s) * BN * kBM;
+        // Four segments' loads in flight at a time; summed in segment order (deterministic).
+        for (int s = 0; s < nseg; s += 4) {
+          float t[4][16];
 #pragma unroll
-          for (int q = 0; q < 16; ++q)
-            if (c0 + q < valid) v[q] += __ldcg(ps + static_cast<size_t>(c0 + q) * kBM);
+          for (int k = 0; k < 4; ++k) {
+            const float* ps = src + static_cast<size_t>(s + k) * BN * kBM;
+#pragma unroll
+            for (int q = 0; q < 16; ++q)
+              t[k][q] = (s + k < nseg && q < nv) ? __ldcg(ps + static_cast<size_t>(c0 + q) * kBM) : 0.f;
+          }
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+#pragma unroll
+            for (int q = 0; q < 16; ++q) v[q] += t[k][q];
         }
         epi_apply<KIND>(e, p.M, n, m_tile * BN + c0, valid - c0, v, rstd_s, red_s, quarter, lane);
       }
@@ -781,8 +790,10 @@ int ygg_gemm_plan_init(void* plan_mem, int dtype, const void* W, const void* X, 
   g->seg_table = seg_table_dev;
   std::vector<int32_t> table;
   if (dtype == YGG_BF16) {
-    if (num_ctas <= 0) num_ctas = kNumSMs;
     g->units = static_cast<long long>(g->tiles) * g->kb;
+    // Default grid: every SM, but never fewer than 8 k-blocks (128 KB of weights) per CTA, which
+    // bounds how many CTAs share (and must later reduce) one output tile for small layers.
+    if (num_ctas <= 0) num_ctas = static_cast<int>(std::max(1LL, std::min<long long>(kNumSMs, g->units / 8)));
     if (num_ctas > g->units) num_ctas = static_cast<int>(g->units);
     g->num_ctas = num_ctas;
     const int stage_bytes = kBM * kBK * 2 + g->BN * kBK * 2;

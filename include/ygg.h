@@ -205,6 +205,7 @@ typedef struct {
   void* hb;
   float* ss_out;
   int32_t* counters; /* [tiles] zero-initialised arrival counters (self-resetting) */
+  unsigned long long* dbg; /* optional per-CTA timer stamps [num_ctas][8] (profiling only), or NULL */
 } ygg_epilogue;
 
 int ygg_gemm_fused(const void* plan, float* workspace, const ygg_epilogue* epi, ygg_stream_t stream);

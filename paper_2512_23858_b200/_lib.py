@@ -88,7 +88,7 @@ class YggEpilogue(C.Structure):
         ("kind", C.c_int32), ("ss_in", vp), ("ss_tiles", C.c_int32), ("norm_dim", C.c_int32), ("eps", C.c_float),
         ("out", vp), ("ld", C.c_int32), ("q_out", vp), ("cache", vp), ("S", C.c_int32), ("Hq", C.c_int32),
         ("Hkv", C.c_int32), ("hd", C.c_int32), ("rope_theta", C.c_float), ("pos", vp), ("slot", vp), ("req", vp),
-        ("act_out", vp), ("resid", vp), ("hb", vp), ("ss_out", vp), ("counters", vp),
+        ("act_out", vp), ("resid", vp), ("hb", vp), ("ss_out", vp), ("counters", vp), ("dbg", vp),
     ]
 
 

@@ -89,7 +89,14 @@ struct EpiArgs {
   float* ss_out;          // RESID [N/128][M]
   int n_total;
   int32_t* counters;      // [tiles] arrival counters, self-resetting
+  unsigned long long* dbg; // optional per-CTA %globaltimer stamps [num_ctas][8] (profiling only)
 };
+
+YGG_DEV unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 
 YGG_DEV void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
 YGG_DEV int ld_acquire(const int32_t* p) {
@@ -202,8 +209,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   uint64_t* tfull = empty + S;   // [2]
   uint64_t* tempty = tfull + 2;  // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
-  int* pend_tile = reinterpret_cast<int*>(tmem_slot + 1);  // [2] deferred fixups of split tiles
+  int* pend_tile = reinterpret_cast<int*>(tmem_slot + 1);  // [2] split tiles awaiting their fixup
   int* pend_j = pend_tile + 2;                               // [2] participant index in the tile
+  int* pend_tgt = pend_j + 2;                                // [2] epoch-counter target
   float* red_s = reinterpret_cast<float*>(tmem_slot + 8);    // [4][16]
   float* rstd_s = red_s + 64;                               // [kMaxRstdTokens]
 
@@ -223,7 +231,18 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  if (e.dbg && threadIdx.x == 0) e.dbg[c * 8 + 0] = gtimer();
   pdl_launch_dependents();
+
+  // Processing order of this CTA's range: the (possibly split) first and last tiles first, then
+  // the whole middle tiles, so the cooperative fixups of split tiles overlap the whole-tile stream.
+  const int nsegs = (u1 > u0) ? static_cast<int>((u1 - 1) / p.kb - u0 / p.kb + 1) : 0;
+  const long long tfirst = u0 / p.kb, tlast = (u1 > u0) ? (u1 - 1) / p.kb : tfirst;
+  auto segment = [&](int k, long long& a, long long& b) {
+    const long long t = (k == 0) ? tfirst : (k == 1 ? tlast : tfirst + (k - 1));
+    a = u0 > t * p.kb ? u0 : t * p.kb;
+    b = u1 < (t + 1) * p.kb ? u1 : (t + 1) * p.kb;
+  };
 
   if (warp == 0) {
     if (lane == 0) {
@@ -232,24 +251,27 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       const uint64_t pol_x = policy_evict_last();
       const long long n_units = u1 - u0;
       const int pre = static_cast<int>(n_units < S ? n_units : S);
+      int k = 0;
+      long long a = 0, b = 0, u = 0;
+      if (nsegs) { segment(0, a, b); u = a; }
+      int pre_tile[12], pre_kblk[12];
       // Weights never depend on the previous kernel: stream them before the grid dependency.
       for (int i = 0; i < pre; ++i) {
-        const long long u = u0 + i;
         const int tile = static_cast<int>(u / p.kb), kblk = static_cast<int>(u % p.kb);
-        const int n_tile = tile / p.m_tiles;
+        pre_tile[i] = tile;
+        pre_kblk[i] = kblk;
         mbar_arrive_expect_tx(&full[i], a_bytes + b_bytes);
-        tma_load_2d(sa + static_cast<size_t>(i) * a_bytes, &tmap_w, &full[i], kblk * kBK, n_tile * kBM, pol_w);
+        tma_load_2d(sa + static_cast<size_t>(i) * a_bytes, &tmap_w, &full[i], kblk * kBK, (tile / p.m_tiles) * kBM,
+                    pol_w);
+        if (++u == b && ++k < nsegs) { segment(k, a, b); u = a; }
       }
       pdl_wait();
-      for (int i = 0; i < pre; ++i) {
-        const long long u = u0 + i;
-        const int tile = static_cast<int>(u / p.kb), kblk = static_cast<int>(u % p.kb);
-        const int m_tile = tile % p.m_tiles;
-        tma_load_2d(sb + static_cast<size_t>(i) * b_bytes, &tmap_x, &full[i], kblk * kBK, m_tile * BN, pol_x);
-      }
+      for (int i = 0; i < pre; ++i)
+        tma_load_2d(sb + static_cast<size_t>(i) * b_bytes, &tmap_x, &full[i], pre_kblk[i] * kBK,
+                    (pre_tile[i] % p.m_tiles) * BN, pol_x);
       int stage = pre % S;
       uint32_t phase = (pre == S) ? 1u : 0u;
-      for (long long u = u0 + pre; u < u1; ++u) {
+      while (k < nsegs) {
         mbar_wait(&empty[stage], phase ^ 1u);
         const int tile = static_cast<int>(u / p.kb), kblk = static_cast<int>(u % p.kb);
         const int n_tile = tile / p.m_tiles, m_tile = tile % p.m_tiles;
@@ -257,7 +279,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         tma_load_2d(sa + static_cast<size_t>(stage) * a_bytes, &tmap_w, &full[stage], kblk * kBK, n_tile * kBM, pol_w);
         tma_load_2d(sb + static_cast<size_t>(stage) * b_bytes, &tmap_x, &full[stage], kblk * kBK, m_tile * BN, pol_x);
         if (++stage == S) { stage = 0; phase ^= 1u; }
+        if (++u == b && ++k < nsegs) { segment(k, a, b); u = a; }
       }
+      if (e.dbg) e.dbg[c * 8 + 6] = gtimer();
     }
   } else if (warp == 1) {
     pdl_wait();
@@ -267,32 +291,28 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     uint32_t phase = 0;
     int acc = 0;
     uint32_t acc_phase[2] = {0u, 0u};
-    long long u = u0;
-    while (u < u1) {
-      const int tile = static_cast<int>(u / p.kb);
-      const long long tile_end = static_cast<long long>(tile + 1) * p.kb;
-      const long long seg_end = tile_end < u1 ? tile_end : u1;
+    for (int k = 0; k < nsegs; ++k) {
+      long long a, b;
+      segment(k, a, b);
       // Wait for the epilogue to drain this accumulator buffer.
       mbar_wait(&tempty[acc], acc_phase[acc] ^ 1u);
       tc_fence_after();
       const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * BN);
-      bool first = true;
-      for (; u < seg_end; ++u) {
+      for (long long u = a; u < b; ++u) {
         mbar_wait(&full[stage], phase);
         tc_fence_after();
         if (lane == 0) {
           const uint32_t a_addr = smem_u32(sa + static_cast<size_t>(stage) * a_bytes);
           const uint32_t b_addr = smem_u32(sb + static_cast<size_t>(stage) * b_bytes);
 #pragma unroll
-          for (int k = 0; k < kBK / 16; ++k) {
-            const uint64_t ad = umma_desc_sw128(a_addr + k * 32);
-            const uint64_t bd = umma_desc_sw128(b_addr + k * 32);
-            umma_bf16(d_tmem, ad, bd, idesc, (first && k == 0) ? 0u : 1u);
+          for (int kk = 0; kk < kBK / 16; ++kk) {
+            const uint64_t ad = umma_desc_sw128(a_addr + kk * 32);
+            const uint64_t bd = umma_desc_sw128(b_addr + kk * 32);
+            umma_bf16(d_tmem, ad, bd, idesc, (u == a && kk == 0) ? 0u : 1u);
           }
           umma_commit(&empty[stage]);
         }
         __syncwarp();
-        first = false;
         if (++stage == S) { stage = 0; phase ^= 1u; }
       }
       if (lane == 0) umma_commit(&tfull[acc]);
@@ -300,6 +320,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       acc_phase[acc] ^= 1u;
       acc ^= 1;
     }
+    if (e.dbg && lane == 0) e.dbg[c * 8 + 5] = gtimer();
   } else {
     pdl_wait();
     // ===== Epilogue warps: TMEM -> (partials | fused op) =====
@@ -318,14 +339,13 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     int acc = 0;
     uint32_t acc_phase[2] = {0u, 0u};
     int npend = 0;
-    long long u = u0;
-    while (u < u1) {
-      const int tile = static_cast<int>(u / p.kb);
-      const long long tile_end = static_cast<long long>(tile + 1) * p.kb;
-      const long long seg_end = tile_end < u1 ? tile_end : u1;
+    for (int k = 0; k < nsegs; ++k) {
+      long long a, b;
+      segment(k, a, b);
+      const int tile = static_cast<int>(a / p.kb);
       const int s_first = p.seg_first[tile], s_end = p.seg_first[tile + 1];
       const int nseg = s_end - s_first;
-      const int seg = (u == u0) ? p.seg_base[c] : s_first;
+      const int seg = (tile == tfirst) ? p.seg_base[c] : s_first;
       const int m_tile = tile % p.m_tiles, n_tile = tile / p.m_tiles;
       const int valid = min(BN, p.M - m_tile * BN);
       const int n = n_tile * kBM + row;
@@ -353,67 +373,71 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         tc_fence_before();
         mbar_arrive(&tempty[acc]);
         if (KIND != kEpiNone) {
-          // Publish the partial (CTA barrier, then one release-ordered arrival); the reduction is
-          // deferred to the end of this CTA's range so the TMEM pipeline never waits on another
-          // CTA.  Only the first and last segment of a range can be partial tiles (<= 2 pending).
+          // Publish the partial: CTA barrier, then one release-ordered arrival on the tile's epoch
+          // counter (monotonic: launch L of this plan moves it from L*nseg to (L+1)*nseg).
           epi_bar();
           if (et == 0) {
-            asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(e.counters + tile) : "memory");
+            int old;
+            asm volatile("atom.add.release.gpu.global.s32 %0, [%1], 1;" : "=r"(old) : "l"(e.counters + tile) : "memory");
             pend_tile[npend] = tile;
             pend_j[npend] = seg - s_first;
+            pend_tgt[npend] = (old / nseg + 1) * nseg;
           }
           ++npend;
         }
       }
       acc_phase[acc] ^= 1u;
       acc ^= 1;
-      u = seg_end;
-    }
-    // Cooperative fixups: once all nseg partials of a split tile have arrived, participant j
-    // reduces 16-token column chunks j, j+nseg, ... in fixed segment order and applies the op.
-    for (int i = 0; i < npend; ++i) {
-      epi_bar();
-      const int tile = pend_tile[i], j = pend_j[i];
-      const int s_first = p.seg_first[tile];
-      const int nseg = p.seg_first[tile + 1] - s_first;
-      const int m_tile = tile % p.m_tiles, n_tile = tile / p.m_tiles;
-      const int valid = min(BN, p.M - m_tile * BN);
-      const int n = n_tile * kBM + row;
-      if (et == 0) {
-        const long long t0 = clock64();
-        while (ld_acquire(e.counters + tile) < nseg) {
-          __nanosleep(64);
-          if (clock64() - t0 > (1ll << 34)) __trap();
-        }
-      }
-      epi_bar();
-      const float* src = ws + static_cast<size_t>(s_first) * BN * kBM + row;
-      for (int c0 = j * 16; c0 < BN; c0 += nseg * 16) {
-        const int nv = min(16, valid - c0);
-        float v[16];
-#pragma unroll
-        for (int q = 0; q < 16; ++q) v[q] = 0.f;
-        // Four segments' loads in flight at a time; summed in segment order (deterministic).
-        for (int s = 0; s < nseg; s += 4) {
-          float t[4][16];
-#pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            const float* ps = src + static_cast<size_t>(s + k) * BN * kBM;
-#pragma unroll
-            for (int q = 0; q < 16; ++q)
-              t[k][q] = (s + k < nseg && q < nv) ? __ldcg(ps + static_cast<size_t>(c0 + q) * kBM) : 0.f;
+      if (k == min(nsegs, 2) - 1 && npend > 0) {
+        if (e.dbg && et == 0) e.dbg[c * 8 + 1] = gtimer();
+        // Cooperative fixups (right after this CTA's split segments, overlapping the whole tiles
+        // still streaming): participant j reduces 16-token column chunks j, j+nseg, ... in fixed
+        // segment order and applies the op.
+        for (int i = 0; i < npend; ++i) {
+          epi_bar();
+          const int ft = pend_tile[i], fj = pend_j[i], target = pend_tgt[i];
+          const int fs = p.seg_first[ft];
+          const int fn = p.seg_first[ft + 1] - fs;
+          const int fm = ft % p.m_tiles;
+          const int fvalid = min(BN, p.M - fm * BN);
+          const int fcol = (ft / p.m_tiles) * kBM + row;
+          if (et == 0) {
+            const long long t0 = clock64();
+            while (ld_acquire(e.counters + ft) < target) {
+              __nanosleep(32);
+              if (clock64() - t0 > (1ll << 34)) __trap();
+            }
           }
+          epi_bar();
+          if (e.dbg && et == 0) e.dbg[c * 8 + 2 + i] = gtimer();
+          const float* src = ws + static_cast<size_t>(fs) * BN * kBM + row;
+          for (int c0 = fj * 16; c0 < BN; c0 += fn * 16) {
+            const int nv = min(16, fvalid - c0);
+            float v[16];
 #pragma unroll
-          for (int k = 0; k < 4; ++k)
+            for (int q = 0; q < 16; ++q) v[q] = 0.f;
+            // Four segments' loads in flight at a time; summed in segment order (deterministic).
+            for (int s = 0; s < fn; s += 4) {
+              float t[4][16];
 #pragma unroll
-            for (int q = 0; q < 16; ++q) v[q] += t[k][q];
+              for (int kk = 0; kk < 4; ++kk) {
+                const float* ps = src + static_cast<size_t>(s + kk) * BN * kBM;
+#pragma unroll
+                for (int q = 0; q < 16; ++q)
+                  t[kk][q] = (s + kk < fn && q < nv) ? __ldcg(ps + static_cast<size_t>(c0 + q) * kBM) : 0.f;
+              }
+#pragma unroll
+              for (int kk = 0; kk < 4; ++kk)
+#pragma unroll
+                for (int q = 0; q < 16; ++q) v[q] += t[kk][q];
+            }
+            epi_apply<KIND>(e, p.M, fcol, fm * BN + c0, fvalid - c0, v, rstd_s, red_s, quarter, lane);
+          }
         }
-        epi_apply<KIND>(e, p.M, n, m_tile * BN + c0, valid - c0, v, rstd_s, red_s, quarter, lane);
+        npend = 0;
       }
-      epi_bar();
-      // Second-phase arrival: the last participant to finish reading resets the counter.
-      if (et == 0 && atomicAdd(e.counters + tile, 1) == 2 * nseg - 1) e.counters[tile] = 0;
     }
+    if (e.dbg && et == 0) e.dbg[c * 8 + 4] = gtimer();
   }
   __syncthreads();
   if (warp == 1) {
@@ -889,6 +913,7 @@ static int gemm_launch(const GemmPlan* g, float* workspace, const ygg_epilogue* 
       e.ss_out = epi->ss_out;
       e.n_total = g->N;
       e.counters = epi->counters;
+      e.dbg = reinterpret_cast<unsigned long long*>(epi->dbg);
       YGG_CHECK_ARG(kind == kEpiNone || e.counters != nullptr, "fused epilogue needs tile counters");
       YGG_CHECK_ARG(!e.ss_in || g->M <= kMaxRstdTokens, "too many tokens for the folded RMSNorm");
       YGG_CHECK_ARG(!e.ss_in || (e.ss_tiles >= 1 && e.norm_dim >= 1), "bad RMSNorm fold arguments");

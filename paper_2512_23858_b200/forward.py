@@ -151,34 +151,45 @@ class Forward:
         nt = d // 128
         self.ss_a = torch.zeros(nt, M, dtype=torch.float32, device=dev)
         self.ss_b = torch.zeros(nt, M, dtype=torch.float32, device=dev)
-        max_tiles = max(p.tiles for layer in self.plans for p in layer.values())
-        if self.lm_plan:
-            max_tiles = max(max_tiles, self.lm_plan.tiles)
-        self.counters = torch.zeros(max_tiles, dtype=torch.int32, device=dev)
+        # One arrival-counter array per plan: the counters are monotonic epochs (launch L of a plan
+        # moves a split tile's counter from L*nseg to (L+1)*nseg), so plans must never share them.
+        plans = [p for layer in self.plans for p in layer.values()] + ([self.lm_plan] if self.lm_plan else [])
+        offs, total = [], 0
+        for p in plans:
+            offs.append(total)
+            total += p.tiles
+        self.counters = torch.zeros(max(total, 1), dtype=torch.int32, device=dev)
+        counter_ptr = {id(p): self.counters.data_ptr() + 4 * o for p, o in zip(plans, offs)}
         eps = float(cfg.norm_eps)
         es = self.cache.element_size()
+        cur = {"plan": None}
 
         def epi(kind, **kw):
             e = L.YggEpilogue()
             e.kind = kind
-            e.counters = self.counters.data_ptr()
+            e.counters = counter_ptr[id(cur["plan"])]
             for k, v in kw.items():
                 setattr(e, k, v)
             return e
 
         for li, p in enumerate(self.plans):
             cache_l = self.cache.data_ptr() + li * self.layer_stride * es
+            cur["plan"] = p["qkv"]
             p["qkv"].epi = epi(L.YGG_EPI_QKV_ROPE, ss_in=self.ss_a.data_ptr(), ss_tiles=nt, norm_dim=d, eps=eps,
                                q_out=self.q.data_ptr(), cache=cache_l, S=self.S, Hq=cfg.n_heads, Hkv=cfg.n_kv_heads,
                                hd=cfg.head_dim, rope_theta=cfg.rope_theta, pos=self.pos.data_ptr(),
                                slot=self.slot.data_ptr(), req=self.req.data_ptr())
+            cur["plan"] = p["o"]
             p["o"].epi = epi(L.YGG_EPI_RESID, resid=self.resid.data_ptr(), hb=self.xn.data_ptr(),
                              ss_out=self.ss_b.data_ptr())
+            cur["plan"] = p["gu"]
             p["gu"].epi = epi(L.YGG_EPI_SWIGLU, ss_in=self.ss_b.data_ptr(), ss_tiles=nt, norm_dim=d, eps=eps,
                               act_out=self.mlp.data_ptr())
+            cur["plan"] = p["down"]
             p["down"].epi = epi(L.YGG_EPI_RESID, resid=self.resid.data_ptr(), hb=self.xn.data_ptr(),
                                 ss_out=self.ss_a.data_ptr())
         if self.lm_plan:
+            cur["plan"] = self.lm_plan
             self.lm_plan.epi = epi(L.YGG_EPI_STORE_F32, ss_in=self.ss_a.data_ptr(), ss_tiles=nt, norm_dim=d, eps=eps,
                                    out=self.logits.data_ptr(), ld=cfg.vocab)
 

@@ -206,6 +206,7 @@ typedef struct {
   float* ss_out;
   int32_t* counters; /* [tiles] zero-initialised arrival counters (self-resetting) */
   unsigned long long* dbg; /* optional per-CTA timer stamps [num_ctas][8] (profiling only), or NULL */
+  const float* rope_cs;    /* optional [positions][hd/2][2] (cos, sin) table for QKV_ROPE, or NULL */
 } ygg_epilogue;
 
 int ygg_gemm_fused(const void* plan, float* workspace, const ygg_epilogue* epi, ygg_stream_t stream);

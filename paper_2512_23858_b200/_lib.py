@@ -89,6 +89,7 @@ class YggEpilogue(C.Structure):
         ("out", vp), ("ld", C.c_int32), ("q_out", vp), ("cache", vp), ("S", C.c_int32), ("Hq", C.c_int32),
         ("Hkv", C.c_int32), ("hd", C.c_int32), ("rope_theta", C.c_float), ("pos", vp), ("slot", vp), ("req", vp),
         ("act_out", vp), ("resid", vp), ("hb", vp), ("ss_out", vp), ("counters", vp), ("dbg", vp),
+        ("rope_cs", vp),
     ]
 
 

@@ -37,6 +37,7 @@ struct GemmPlan {
   int BN;        // tokens per tile (multiple of 16, <= 256)
   int m_tiles, n_tiles, tiles, kb;
   int num_ctas;
+  int dp_per_cta;
   long long units;
   int segments;
   int stages;
@@ -51,7 +52,8 @@ constexpr uint32_t kPlanMagic = 0x59474750u;  // "YGGP"
 
 struct GemmParams {
   int M, BN, m_tiles, kb, num_ctas, stages, tmem_cols;
-  long long units;
+  int dp_per_cta;   // whole tiles per CTA (tiles [0, dp_per_cta * num_ctas) are data-parallel)
+  long long units;  // stream-K units (remainder tiles x kb)
   const int32_t* seg_first;
   const int32_t* seg_base;
 };
@@ -90,6 +92,7 @@ struct EpiArgs {
   int n_total;
   int32_t* counters;      // [tiles] arrival counters, self-resetting
   unsigned long long* dbg; // optional per-CTA %globaltimer stamps [num_ctas][8] (profiling only)
+  const float2* rope_cs;   // optional [positions][hd/2] (cos, sin) table; else sincosf
 };
 
 YGG_DEV unsigned long long gtimer() {
@@ -144,7 +147,13 @@ YGG_DEV void epi_apply(const EpiArgs& e, int M, int n, int m0, int valid16, floa
       if (rope) {
         const float x1 = odd ? other : v[j], x2 = odd ? v[j] : other;
         float sn, cs;
-        sincosf(static_cast<float>(__ldg(e.pos + m)) * inv_freq, &sn, &cs);
+        if (e.rope_cs) {
+          const float2 t = __ldg(e.rope_cs + static_cast<size_t>(__ldg(e.pos + m)) * half + pair);
+          cs = t.x;
+          sn = t.y;
+        } else {
+          sincosf(static_cast<float>(__ldg(e.pos + m)) * inv_freq, &sn, &cs);
+        }
         y = odd ? (x2 * cs + x1 * sn) : (x1 * cs - x2 * sn);
       }
       const __nv_bfloat16 yb = __float2bfloat16_rn(y);
@@ -217,7 +226,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int c = blockIdx.x;
-  const long long u0 = p.units * c / p.num_ctas, u1 = p.units * (c + 1) / p.num_ctas;
+  // Hybrid split: dp_per_cta whole tiles per CTA (tiles c, c+G, ...) plus an equal share of the
+  // stream-K units of the remaining tiles, which start at tile t_dp.
+  const long long sk_base = static_cast<long long>(p.dp_per_cta) * p.num_ctas * p.kb;
+  const long long u0 = sk_base + p.units * c / p.num_ctas, u1 = sk_base + p.units * (c + 1) / p.num_ctas;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmap_w);
@@ -236,9 +248,16 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 
   // Processing order of this CTA's range: the (possibly split) first and last tiles first, then
   // the whole middle tiles, so the cooperative fixups of split tiles overlap the whole-tile stream.
-  const int nsegs = (u1 > u0) ? static_cast<int>((u1 - 1) / p.kb - u0 / p.kb + 1) : 0;
+  const int n_sk = (u1 > u0) ? static_cast<int>((u1 - 1) / p.kb - u0 / p.kb + 1) : 0;
+  const int nsegs = n_sk + p.dp_per_cta;
   const long long tfirst = u0 / p.kb, tlast = (u1 > u0) ? (u1 - 1) / p.kb : tfirst;
   auto segment = [&](int k, long long& a, long long& b) {
+    if (k >= n_sk) {  // whole data-parallel tile
+      const long long t = c + static_cast<long long>(k - n_sk) * p.num_ctas;
+      a = t * p.kb;
+      b = a + p.kb;
+      return;
+    }
     const long long t = (k == 0) ? tfirst : (k == 1 ? tlast : tfirst + (k - 1));
     a = u0 > t * p.kb ? u0 : t * p.kb;
     b = u1 < (t + 1) * p.kb ? u1 : (t + 1) * p.kb;
@@ -345,7 +364,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       const int tile = static_cast<int>(a / p.kb);
       const int s_first = p.seg_first[tile], s_end = p.seg_first[tile + 1];
       const int nseg = s_end - s_first;
-      const int seg = (tile == tfirst) ? p.seg_base[c] : s_first;
+      const int seg = (k == 0 && n_sk > 0) ? p.seg_base[c] : s_first;
       const int m_tile = tile % p.m_tiles, n_tile = tile / p.m_tiles;
       const int valid = min(BN, p.M - m_tile * BN);
       const int n = n_tile * kBM + row;
@@ -388,7 +407,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       }
       acc_phase[acc] ^= 1u;
       acc ^= 1;
-      if (k == min(nsegs, 2) - 1 && npend > 0) {
+      if (k == min(n_sk, 2) - 1 && npend > 0) {
         if (e.dbg && et == 0) e.dbg[c * 8 + 1] = gtimer();
         // Cooperative fixups (right after this CTA's split segments, overlapping the whole tiles
         // still streaming): participant j reduces 16-token column chunks j, j+nseg, ... in fixed
@@ -826,12 +845,18 @@ int ygg_gemm_plan_init(void* plan_mem, int dtype, const void* W, const void* X, 
     int cols = 32;
     while (cols < 2 * g->BN) cols *= 2;
     g->tmem_cols = cols;
-    // Segment enumeration in (cta, tile) order == (tile, cta) order.
+    // Hybrid split: whole tiles first (one segment each), then the remainder tiles' units are
+    // cut stream-K over all CTAs; their segments are enumerated in (cta, tile) == (tile, cta) order.
+    g->dp_per_cta = g->tiles / num_ctas;
+    const int t_dp = g->dp_per_cta * num_ctas;
+    g->units = static_cast<long long>(g->tiles - t_dp) * g->kb;
     std::vector<int32_t> seg_first(g->tiles + 1, 0), seg_base(num_ctas, 0);
     std::vector<int> count(g->tiles, 0);
-    int seg = 0;
+    for (int t = 0; t < t_dp; ++t) count[t] = 1;
+    int seg = t_dp;
     for (int c = 0; c < num_ctas; ++c) {
-      const long long u0 = g->units * c / num_ctas, u1 = g->units * (c + 1) / num_ctas;
+      const long long u0 = static_cast<long long>(t_dp) * g->kb + g->units * c / num_ctas;
+      const long long u1 = static_cast<long long>(t_dp) * g->kb + g->units * (c + 1) / num_ctas;
       seg_base[c] = seg;
       if (u1 > u0) {
         const int t0 = static_cast<int>(u0 / g->kb), t1 = static_cast<int>((u1 - 1) / g->kb);
@@ -880,6 +905,7 @@ static int gemm_launch(const GemmPlan* g, float* workspace, const ygg_epilogue* 
     p.m_tiles = g->m_tiles;
     p.kb = g->kb;
     p.num_ctas = g->num_ctas;
+    p.dp_per_cta = g->dp_per_cta;
     p.stages = g->stages;
     p.tmem_cols = g->tmem_cols;
     p.units = g->units;
@@ -914,6 +940,7 @@ static int gemm_launch(const GemmPlan* g, float* workspace, const ygg_epilogue* 
       e.n_total = g->N;
       e.counters = epi->counters;
       e.dbg = reinterpret_cast<unsigned long long*>(epi->dbg);
+      e.rope_cs = reinterpret_cast<const float2*>(epi->rope_cs);
       YGG_CHECK_ARG(kind == kEpiNone || e.counters != nullptr, "fused epilogue needs tile counters");
       YGG_CHECK_ARG(!e.ss_in || g->M <= kMaxRstdTokens, "too many tokens for the folded RMSNorm");
       YGG_CHECK_ARG(!e.ss_in || (e.ss_tiles >= 1 && e.norm_dim >= 1), "bad RMSNorm fold arguments");

@@ -27,7 +27,7 @@ import math
 import torch
 
 from . import _lib as L
-from .model import ModelConfig, prepare_fused_
+from .model import ModelConfig, prepare_fused_, rope_table
 
 
 class GemmPlan:
@@ -162,6 +162,7 @@ class Forward:
         counter_ptr = {id(p): self.counters.data_ptr() + 4 * o for p, o in zip(plans, offs)}
         eps = float(cfg.norm_eps)
         es = self.cache.element_size()
+        self.rope_cs = rope_table(cfg, self.S + 64, dev)
         cur = {"plan": None}
 
         def epi(kind, **kw):
@@ -178,7 +179,7 @@ class Forward:
             p["qkv"].epi = epi(L.YGG_EPI_QKV_ROPE, ss_in=self.ss_a.data_ptr(), ss_tiles=nt, norm_dim=d, eps=eps,
                                q_out=self.q.data_ptr(), cache=cache_l, S=self.S, Hq=cfg.n_heads, Hkv=cfg.n_kv_heads,
                                hd=cfg.head_dim, rope_theta=cfg.rope_theta, pos=self.pos.data_ptr(),
-                               slot=self.slot.data_ptr(), req=self.req.data_ptr())
+                               slot=self.slot.data_ptr(), req=self.req.data_ptr(), rope_cs=self.rope_cs.data_ptr())
             cur["plan"] = p["o"]
             p["o"].epi = epi(L.YGG_EPI_RESID, resid=self.resid.data_ptr(), hb=self.xn.data_ptr(),
                              ss_out=self.ss_b.data_ptr())

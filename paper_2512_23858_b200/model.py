@@ -214,3 +214,16 @@ def prepare_fused_(w: dict, cfg: ModelConfig) -> dict:
     w["final_norm"] = torch.ones_like(w["final_norm"])
     w["_layout"] = "fused"
     return w
+
+
+def rope_table(cfg: ModelConfig, positions: int, device) -> torch.Tensor:
+    """[positions, hd/2, 2] (cos, sin) of the RoPE angle for the fused QKV epilogue.
+
+    The angle is formed exactly like the fp32 reference (inv_freq = 1/theta^(2i/hd) in f32, angle =
+    f32(pos) * inv_freq rounded to f32); cos/sin are then evaluated in f64 and rounded once, so the
+    table is within half an ulp of the exact cosine of the reference's f32 angle."""
+    hd = cfg.head_dim
+    inv_freq = 1.0 / (cfg.rope_theta ** (torch.arange(0, hd, 2, dtype=torch.float32) / hd))
+    ang = torch.arange(positions, dtype=torch.float32)[:, None] * inv_freq[None, :]
+    ang64 = ang.double()
+    return torch.stack([torch.cos(ang64), torch.sin(ang64)], -1).float().contiguous().to(device)

@@ -15,6 +15,7 @@
 #include <cudaTypedefs.h>
 
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -840,7 +841,15 @@ int ygg_gemm_plan_init(void* plan_mem, int dtype, const void* W, const void* X, 
     if (num_ctas > g->units) num_ctas = static_cast<int>(g->units);
     g->num_ctas = num_ctas;
     const int stage_bytes = kBM * kBK * 2 + g->BN * kBK * 2;
-    g->stages = std::min(12, (227 * 1024 - kSmemExtra) / stage_bytes);
+    // Shared-memory budget: YGG_GEMM_SMEM_KB (default 113) keeps two GEMM CTAs resident per SM, so
+    // under programmatic dependent launch the next layer's CTAs start (prologue + weight prefetch)
+    // while this one drains its epilogue.
+    static const int smem_kb = [] {
+      const char* s = getenv("YGG_GEMM_SMEM_KB");
+      int v = s ? atoi(s) : 113;
+      return v < 48 ? 48 : (v > 227 ? 227 : v);
+    }();
+    g->stages = std::min(12, (smem_kb * 1024 - kSmemExtra) / stage_bytes);
     YGG_CHECK_ARG(g->stages >= 2, "tile too large for shared memory");
     int cols = 32;
     while (cols < 2 * g->BN) cols *= 2;

@@ -837,7 +837,13 @@ int ygg_gemm_plan_init(void* plan_mem, int dtype, const void* W, const void* X, 
     g->units = static_cast<long long>(g->tiles) * g->kb;
     // Default grid: every SM, but never fewer than 8 k-blocks (128 KB of weights) per CTA, which
     // bounds how many CTAs share (and must later reduce) one output tile for small layers.
-    if (num_ctas <= 0) num_ctas = static_cast<int>(std::max(1LL, std::min<long long>(kNumSMs, g->units / 8)));
+    static const int min_units = [] {
+      const char* s = getenv("YGG_GEMM_MIN_UNITS");
+      const int v = s ? atoi(s) : 8;
+      return v < 1 ? 1 : v;
+    }();
+    if (num_ctas <= 0)
+      num_ctas = static_cast<int>(std::max(1LL, std::min<long long>(kNumSMs, g->units / min_units)));
     if (num_ctas > g->units) num_ctas = static_cast<int>(g->units);
     g->num_ctas = num_ctas;
     const int stage_bytes = kBM * kBK * 2 + g->BN * kBK * 2;

@@ -8,12 +8,19 @@
 #include <algorithm>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 
 #include "../../include/ygg.h"
 
 namespace ygg {
 
 int ygg_fail(int code, const char* fmt, ...);
+
+// Programmatic dependent launch is on unless YGG_NO_PDL is set (A/B measurements).
+inline int pdl_enabled() {
+  static const int on = std::getenv("YGG_NO_PDL") ? 0 : 1;
+  return on;
+}
 
 template <typename Kernel, typename... Args>
 int launch_pdl(Kernel kernel, dim3 grid, dim3 block, size_t smem, cudaStream_t stream, Args... args) {
@@ -24,7 +31,7 @@ int launch_pdl(Kernel kernel, dim3 grid, dim3 block, size_t smem, cudaStream_t s
   cfg.stream = stream;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled();
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   cudaError_t err = cudaLaunchKernelEx(&cfg, kernel, args...);
@@ -41,7 +48,7 @@ int launch_pdl_cluster(Kernel kernel, dim3 grid, dim3 block, int cluster_x, cuda
   cfg.stream = stream;
   cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled();
   attr[1].id = cudaLaunchAttributeClusterDimension;
   attr[1].val.clusterDim.x = cluster_x;
   attr[1].val.clusterDim.y = 1;

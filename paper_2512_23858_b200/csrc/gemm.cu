@@ -110,6 +110,9 @@ YGG_DEV int ld_acquire(const int32_t* p) {
 }
 
 // Apply the fused op to 16 token columns of one 128-feature tile row (thread = feature row).
+// Every global load of a chunk (token metadata, RoPE table, residual) is issued before any store:
+// the EpiArgs pointers may alias as far as the compiler knows, so interleaving would serialise
+// one L2 round trip per token.
 template <int KIND>
 YGG_DEV void epi_apply(const EpiArgs& e, int M, int n, int m0, int valid16, float* v, const float* rstd_s,
                        float* red_s, int quarter, int lane) {
@@ -124,13 +127,16 @@ YGG_DEV void epi_apply(const EpiArgs& e, int M, int n, int m0, int valid16, floa
   } else if constexpr (KIND == kEpiSwiglu) {
     const bool odd = n & 1;
     const int F = e.n_total / 2;
+    float o[16];
 #pragma unroll
     for (int j = 0; j < 16; ++j) {
       const float other = __shfl_xor_sync(0xffffffffu, v[j], 1);
-      if (!odd && j < valid16) {
-        const float g = v[j], u = other;
-        e.act_out[static_cast<size_t>(m0 + j) * F + (n >> 1)] = __float2bfloat16_rn(g / (1.f + expf(-g)) * u);
-      }
+      o[j] = v[j] / (1.f + __expf(-v[j])) * other;
+    }
+    if (!odd) {
+#pragma unroll
+      for (int j = 0; j < 16; ++j)
+        if (j < valid16) e.act_out[static_cast<size_t>(m0 + j) * F + (n >> 1)] = __float2bfloat16_rn(o[j]);
     }
   } else if constexpr (KIND == kEpiQkvRope) {
     const int head = n / e.hd, p = n % e.hd, half = e.hd / 2;
@@ -138,49 +144,74 @@ YGG_DEV void epi_apply(const EpiArgs& e, int M, int n, int m0, int valid16, floa
     const bool odd = p & 1;
     const int orig = pair + (odd ? half : 0);
     const bool rope = head < e.Hq + e.Hkv;
-    const float inv_freq = 1.0f / exp2f(e.log2_theta * (static_cast<float>(2 * pair) / static_cast<float>(e.hd)));
+    const bool is_q = head < e.Hq;
+    const bool is_v = head >= e.Hq + e.Hkv;
+    // ---- load phase
+    int pos[16], req[16], slot[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const int m = m0 + (j < valid16 ? j : 0);
+      pos[j] = __ldg(e.pos + m);
+      req[j] = __ldg(e.req + m);
+      slot[j] = __ldg(e.slot + m);
+    }
+    float cs[16], sn[16];
+    if (rope) {
+      if (e.rope_cs) {
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          const float2 t = __ldg(e.rope_cs + static_cast<size_t>(pos[j]) * half + pair);
+          cs[j] = t.x;
+          sn[j] = t.y;
+        }
+      } else {
+        const float inv_freq = 1.0f / exp2f(e.log2_theta * (static_cast<float>(2 * pair) / static_cast<float>(e.hd)));
+#pragma unroll
+        for (int j = 0; j < 16; ++j) sincosf(static_cast<float>(pos[j]) * inv_freq, &sn[j], &cs[j]);
+      }
+    }
+    // ---- compute
+    float y[16];
 #pragma unroll
     for (int j = 0; j < 16; ++j) {
       const float other = __shfl_xor_sync(0xffffffffu, v[j], 1);
-      if (j >= valid16) continue;
-      const int m = m0 + j;
-      float y = v[j];
+      y[j] = v[j];
       if (rope) {
         const float x1 = odd ? other : v[j], x2 = odd ? v[j] : other;
-        float sn, cs;
-        if (e.rope_cs) {
-          const float2 t = __ldg(e.rope_cs + static_cast<size_t>(__ldg(e.pos + m)) * half + pair);
-          cs = t.x;
-          sn = t.y;
-        } else {
-          sincosf(static_cast<float>(__ldg(e.pos + m)) * inv_freq, &sn, &cs);
-        }
-        y = odd ? (x2 * cs + x1 * sn) : (x1 * cs - x2 * sn);
+        y[j] = odd ? (x2 * cs[j] + x1 * sn[j]) : (x1 * cs[j] - x2 * sn[j]);
       }
-      const __nv_bfloat16 yb = __float2bfloat16_rn(y);
-      if (head < e.Hq) {
-        e.q_out[(static_cast<size_t>(m) * e.Hq + head) * e.hd + orig] = yb;
+    }
+    // ---- store phase
+    const int kvh = is_v ? head - e.Hq - e.Hkv : head - e.Hq;
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      if (j >= valid16) continue;
+      const __nv_bfloat16 yb = __float2bfloat16_rn(y[j]);
+      if (is_q) {
+        e.q_out[(static_cast<size_t>(m0 + j) * e.Hq + head) * e.hd + orig] = yb;
       } else {
-        const bool is_v = head >= e.Hq + e.Hkv;
-        const int kvh = is_v ? head - e.Hq - e.Hkv : head - e.Hq;
         const size_t base =
-            ((static_cast<size_t>(__ldg(e.req + m)) * 2 + (is_v ? 1 : 0)) * e.Hkv + kvh) * static_cast<size_t>(e.S) * e.hd;
-        const int sl = __ldg(e.slot + m);
-        if (!is_v) e.cache[base + static_cast<size_t>(sl) * e.hd + orig] = yb;
-        else e.cache[base + static_cast<size_t>(orig) * e.S + sl] = yb;  // V^T [hd][S]
+            ((static_cast<size_t>(req[j]) * 2 + (is_v ? 1 : 0)) * e.Hkv + kvh) * static_cast<size_t>(e.S) * e.hd;
+        if (!is_v) e.cache[base + static_cast<size_t>(slot[j]) * e.hd + orig] = yb;
+        else e.cache[base + static_cast<size_t>(orig) * e.S + slot[j]] = yb;  // V^T [hd][S]
       }
     }
   } else if constexpr (KIND == kEpiResid) {
-    float sq[16];
+    float h[16], sq[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j)  // load phase
+      h[j] = (j < valid16) ? e.resid[static_cast<size_t>(m0 + j) * e.n_total + n] : 0.f;
 #pragma unroll
     for (int j = 0; j < 16; ++j) {
-      sq[j] = 0.f;
+      h[j] += (j < valid16) ? v[j] : 0.f;
+      sq[j] = h[j] * h[j];
+    }
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {  // store phase
       if (j < valid16) {
         const size_t idx = static_cast<size_t>(m0 + j) * e.n_total + n;
-        const float h = e.resid[idx] + v[j];
-        e.resid[idx] = h;
-        e.hb[idx] = __float2bfloat16_rn(h);
-        sq[j] = h * h;
+        e.resid[idx] = h[j];
+        e.hb[idx] = __float2bfloat16_rn(h[j]);
       }
     }
 #pragma unroll

@@ -225,24 +225,41 @@ class Forward:
         else:
             self._run_unfused(stream)
 
-    def _run_fused(self, stream) -> None:
+    def _run_fused(self, stream, stamps: torch.Tensor | None = None) -> None:
+        """``stamps`` (int64 [>= 6*layers+3], debug only): a %globaltimer stamp kernel is enqueued
+        after every launch, giving in-graph per-kernel durations."""
         lib, cfg = L.lib(), self.cfg
         s = L.stream_ptr(stream)
         chk = L.check
         ws = self.ws.data_ptr()
+        k = [0]
+
+        def stamp():
+            if stamps is not None:
+                chk(lib.ygg_stamp(stamps.data_ptr() + 8 * k[0], s))
+                k[0] += 1
+
+        stamp()
         chk(lib.ygg_embed_fused(self.w["embed"].data_ptr(), cfg.vocab, cfg.d_model, self.tokens.data_ptr(), self.M,
                                 self.resid.data_ptr(), self.xn.data_ptr(), self.ss_a.data_ptr(), s))
+        stamp()
         qm = self.qmask.data_ptr() if self.mask_words > 0 else None
         for li, p in enumerate(self.plans):
             chk(lib.ygg_gemm_fused(p["qkv"].handle, ws, C.byref(p["qkv"].epi), s))
+            stamp()
             chk(lib.ygg_attention_tc(self.attn_plans[li].handle, self.blk_start.data_ptr(), self.blk_len.data_ptr(),
                                      qm, self.mask_words, self.scale, self.attn_part.data_ptr(),
                                      self.attn.data_ptr(), s))
+            stamp()
             chk(lib.ygg_gemm_fused(p["o"].handle, ws, C.byref(p["o"].epi), s))
+            stamp()
             chk(lib.ygg_gemm_fused(p["gu"].handle, ws, C.byref(p["gu"].epi), s))
+            stamp()
             chk(lib.ygg_gemm_fused(p["down"].handle, ws, C.byref(p["down"].epi), s))
+            stamp()
         if self.lm_plan is not None:
             chk(lib.ygg_gemm_fused(self.lm_plan.handle, ws, C.byref(self.lm_plan.epi), s))
+            stamp()
 
     def _run_unfused(self, stream) -> None:
         lib, cfg = L.lib(), self.cfg

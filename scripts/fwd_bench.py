@@ -28,3 +28,22 @@ for name, f in (("draft", sd.draft), ("verify", sd.verify)):
     torch.cuda.synchronize()
     res[name + "_ms"] = round(a.elapsed_time(b) / 20, 4)
 print(json.dumps(res), flush=True)
+
+# In-graph per-kernel timeline (stamp kernels between launches; perturbs PDL overlap slightly).
+for name, f in (("draft", sd.draft), ("verify", sd.verify)):
+    st = torch.zeros(6 * f.cfg.n_layers + 8, dtype=torch.int64, device="cuda")
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        f._run_fused(None, st)
+    for _ in range(3):
+        g.replay()
+    torch.cuda.synchronize()
+    t = st.cpu().tolist()
+    n = 2 + 5 * f.cfg.n_layers + 1
+    d = [(t[i + 1] - t[i]) / 1000 for i in range(n - 1)]
+    names = ["embed"] + ["qkv", "attn", "o", "gu", "down"] * f.cfg.n_layers + ["lm_head"]
+    agg = {}
+    for nm, v in zip(names, d):
+        agg.setdefault(nm, []).append(v)
+    print(name, "total_us", round((t[n - 1] - t[0]) / 1000, 1),
+          json.dumps({k: [round(sum(v) / len(v), 2), round(max(v), 2)] for k, v in agg.items()}), flush=True)

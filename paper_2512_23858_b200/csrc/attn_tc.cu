@@ -24,7 +24,8 @@ namespace ygg {
 
 constexpr int kKC = 128;           // keys per CTA
 constexpr int kQRows = 128;        // query rows per CTA (UMMA M)
-constexpr int kAttnTcThreads = 160; // warps 0-3 softmax/epilogue, warp 4 TMA + MMA
+constexpr int kAttnTcThreads = 288; // warps 0-7 softmax/epilogue (2 per TMEM lane quarter), warp 8 TMA + MMA
+constexpr int kSoftThreads = 256;
 
 struct AttnPlan {
   uint32_t magic;
@@ -82,6 +83,8 @@ __global__ void __launch_bounds__(kAttnTcThreads, 1)
   unsigned char* sp = svt + KCH * HD * 128;                   // KCH x [128 rows x 128 B]
   uint64_t* bars = reinterpret_cast<uint64_t*>(sp + KCH * kQRows * 128);  // load, s, p, o
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 4);
+  float* red_max = reinterpret_cast<float*>(bars + 6);  // [2][128]
+  float* red_sum = red_max + 2 * kQRows;                 // [2][128]
 
   const int chunk = blockIdx.x, qt = blockIdx.y, kvh = blockIdx.z % a.Hkv, r = blockIdx.z / a.Hkv;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -91,11 +94,13 @@ __global__ void __launch_bounds__(kAttnTcThreads, 1)
   const int nkeys = bs + bl;
   const int key0 = chunk * kKC;
   const int t0 = qt * a.tok_per_tile;
-  // Row owned by this thread (softmax warps): TMEM lane = row.
+  // Row owned by this thread (softmax warps): TMEM lane = row; the two warps of a lane quarter
+  // split the key columns (half 0: keys [0, 64), half 1: keys [64, 128) of the chunk).
   const int row = (warp & 3) * 32 + lane;
+  const int half = (warp >> 2) & 1;
   const int tq = t0 + row / a.G;
   const int head = kvh * a.G + row % a.G;
-  const bool row_valid = warp < 4 && tq < a.T;
+  const bool row_valid = warp < 8 && tq < a.T;
   const int m = r * a.T + tq;
   const size_t orow = static_cast<size_t>(m) * a.Hq + head;
   const size_t slot_stride = static_cast<size_t>(a.M) * a.Hq;
@@ -103,15 +108,15 @@ __global__ void __launch_bounds__(kAttnTcThreads, 1)
   const int last_tok = min(a.T - 1, t0 + a.tok_per_tile - 1);
   const bool skip = key0 >= nkeys || (a.mask_words == 0 && key0 > bs + last_tok);
   if (skip) {
-    if (row_valid) {
+    if (row_valid && half == 0) {
       a.ml[(static_cast<size_t>(chunk) * slot_stride + orow) * 2] = -INFINITY;
       a.ml[(static_cast<size_t>(chunk) * slot_stride + orow) * 2 + 1] = 0.f;
     }
     return;
   }
-  if (warp == 4) {
+  if (warp == 8) {
     if (lane == 0) {
-      for (int i = 0; i < 4; ++i) mbar_init(&bars[i], i == 2 ? 128 : 1);
+      for (int i = 0; i < 4; ++i) mbar_init(&bars[i], i == 2 ? kSoftThreads : 1);
       fence_barrier_init();
     }
     __syncwarp();
@@ -123,7 +128,7 @@ __global__ void __launch_bounds__(kAttnTcThreads, 1)
   const uint32_t tmem = *tmem_slot;
   const uint32_t tS = tmem, tO = tmem + kKC;
 
-  if (warp == 4) {
+  if (warp == 8) {
     if (lane == 0) {
       const uint32_t bytes = DCH * kQRows * 128 + DCH * kKC * 128 + KCH * HD * 128;
       mbar_arrive_expect_tx(&bars[0], bytes);
@@ -158,88 +163,109 @@ __global__ void __launch_bounds__(kAttnTcThreads, 1)
       umma_commit(&bars[3]);
     }
   } else {
-    // ===== softmax: one thread per query row =====
+    // ===== softmax: two threads per query row (64 key columns each) =====
     uint32_t mw[YGG_MAX_MASK_WORDS];
 #pragma unroll
     for (int w = 0; w < YGG_MAX_MASK_WORDS; ++w)
       mw[w] = (row_valid && w < a.mask_words) ? a.qmask[static_cast<size_t>(m) * a.mask_words + w] : 0u;
+    // Visibility bits of 32 keys starting at absolute key kw: prefix keys (< bs) always, block keys
+    // by the row's tree-mask bit (causal when no mask is given), nothing at or past nkeys.
+    auto vis_word = [&](int kw) -> uint32_t {
+      if (!row_valid) return 0u;
+      uint32_t pre = 0u;
+      if (kw + 32 <= bs) pre = 0xffffffffu;
+      else if (kw < bs) pre = (1u << (bs - kw)) - 1u;
+      const int jb0 = kw - bs;  // block index of this word's bit 0
+      uint32_t blk = 0u;
+      if (jb0 + 32 > 0 && jb0 < bl) {
+        if (a.mask_words == 0) {
+          const int lo = jb0 < 0 ? -jb0 : 0;
+          const int hi = min(31, tq - jb0);
+          if (hi >= lo) blk = ((hi == 31) ? 0xffffffffu : ((1u << (hi + 1)) - 1u)) & ~((1u << lo) - 1u);
+        } else if (jb0 < 0) {
+          blk = mw[0] << (-jb0);
+        } else {
+          const int i = jb0 >> 5, s = jb0 & 31;
+          uint32_t w0 = 0u, w1 = 0u;
+#pragma unroll
+          for (int w = 0; w < YGG_MAX_MASK_WORDS; ++w) {
+            if (w == i) w0 = mw[w];
+            if (w == i + 1) w1 = mw[w];
+          }
+          blk = s ? ((w0 >> s) | (w1 << (32 - s))) : w0;
+        }
+        const int keep = bl - jb0;  // bits j with jb0 + j < bl
+        if (keep < 32) blk &= (1u << keep) - 1u;
+      }
+      return pre | blk;
+    };
+    const int cbase = half * 64;
+    const uint32_t vis0 = vis_word(key0 + cbase), vis1 = vis_word(key0 + cbase + 32);
     mbar_wait(&bars[1], 0);
     tc_fence_after();
     const uint32_t lane_base = static_cast<uint32_t>((warp & 3) * 32) << 16;
-    // Visibility of key (key0 + j) for this row: prefix keys always; block keys by tree-mask bit
-    // (or causally when no mask is given); nothing past the request's key count.
-    auto masked = [&](float v, int j) -> float {
-      const int key = key0 + j;
-      bool vis = row_valid && key < nkeys;
-      if (vis && key >= bs) {
-        const int jb = key - bs;
-        if (a.mask_words == 0) {
-          vis = jb <= tq;
-        } else {
-          uint32_t word = 0;
-#pragma unroll
-          for (int w = 0; w < YGG_MAX_MASK_WORDS; ++w)
-            if (w == (jb >> 5)) word = mw[w];
-          vis = (word >> (jb & 31)) & 1u;
-        }
-      }
-      return vis ? v * a.scale_log2 : -INFINITY;
-    };
-    // Pass 1: row max straight from TMEM (16 columns at a time, no S copy in registers).
+    // Pass 1: partial row max over this thread's 64 columns, straight from TMEM.
     float mx = -INFINITY;
-#pragma unroll 1
-    for (int c = 0; c < kKC; c += 16) {
-      float v[16];
-      tmem_ld16(tS + lane_base + c, v);
 #pragma unroll
-      for (int j = 0; j < 16; ++j) mx = fmaxf(mx, masked(v[j], c + j));
-    }
-    // Pass 2: P = 2^(s - max) -> bf16 -> smem, 128B-swizzled K-major rows (unit u -> u ^ (row & 7)).
-    float l = 0.f;
-#pragma unroll 1
-    for (int c = 0; c < kKC; c += 16) {
+    for (int c = 0; c < 64; c += 16) {
       float v[16];
-      tmem_ld16(tS + lane_base + c, v);
+      tmem_ld16(tS + lane_base + cbase + c, v);
+      const uint32_t bits = (c < 32 ? vis0 : vis1) >> (c & 31);
+#pragma unroll
+      for (int j = 0; j < 16; ++j)
+        if ((bits >> j) & 1u) mx = fmaxf(mx, v[j] * a.scale_log2);
+    }
+    red_max[half * kQRows + row] = mx;
+    asm volatile("bar.sync 1, %0;" ::"n"(kSoftThreads) : "memory");
+    mx = fmaxf(red_max[row], red_max[kQRows + row]);
+    // Pass 2: P = 2^(s - max) -> bf16 -> smem (this half's 64-key block, 128B-swizzled rows).
+    float l = 0.f;
+    const uint32_t rbase = smem_u32(sp + half * kQRows * 128 + row * 128);
+#pragma unroll
+    for (int c = 0; c < 64; c += 16) {
+      float v[16];
+      tmem_ld16(tS + lane_base + cbase + c, v);
+      const uint32_t bits = (c < 32 ? vis0 : vis1) >> (c & 31);
 #pragma unroll
       for (int j = 0; j < 16; ++j) {
-        const float sv = masked(v[j], c + j);
-        v[j] = (mx == -INFINITY || sv == -INFINITY) ? 0.f : exp2f(sv - mx);
+        v[j] = ((bits >> j) & 1u) ? exp2f(v[j] * a.scale_log2 - mx) : 0.f;
         l += v[j];
       }
-      const uint32_t rbase = smem_u32(sp + (c / 64) * kQRows * 128 + row * 128);
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
-        const int u = ((c % 64) / 8) + h;
+        const int u = c / 8 + h;
         const float* p8 = v + 8 * h;
         st_shared_v4(rbase + ((u ^ (row & 7)) << 4), pack_bf16(p8[0], p8[1]), pack_bf16(p8[2], p8[3]),
                      pack_bf16(p8[4], p8[5]), pack_bf16(p8[6], p8[7]));
       }
     }
+    red_sum[half * kQRows + row] = l;
     fence_proxy_async();
     tc_fence_before();
     mbar_arrive(&bars[2]);
     mbar_wait(&bars[3], 0);
     tc_fence_after();
-    // Every lane executes the (warp-collective, .aligned) TMEM loads; only valid rows store.
-    float* op = a.opart + (static_cast<size_t>(chunk) * slot_stride + (row_valid ? orow : 0)) * HD;
+    // O readback: each half stores HD/2 columns.  Every lane executes the (warp-collective,
+    // .aligned) TMEM loads; only valid rows store.
+    float* op = a.opart + (static_cast<size_t>(chunk) * slot_stride + (row_valid ? orow : 0)) * HD + half * (HD / 2);
 #pragma unroll
-    for (int c = 0; c < HD; c += 16) {
+    for (int c = 0; c < HD / 2; c += 16) {
       float o[16];
-      tmem_ld16(tO + lane_base + c, o);
+      tmem_ld16(tO + lane_base + half * (HD / 2) + c, o);
       if (row_valid) {
 #pragma unroll
         for (int j = 0; j < 16; j += 4)
           *reinterpret_cast<float4*>(op + c + j) = make_float4(o[j], o[j + 1], o[j + 2], o[j + 3]);
       }
     }
-    if (row_valid) {
+    if (row_valid && half == 0) {
       a.ml[(static_cast<size_t>(chunk) * slot_stride + orow) * 2] = mx;
-      a.ml[(static_cast<size_t>(chunk) * slot_stride + orow) * 2 + 1] = l;
+      a.ml[(static_cast<size_t>(chunk) * slot_stride + orow) * 2 + 1] = red_sum[row] + red_sum[kQRows + row];
     }
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 4) {
+  if (warp == 8) {
     tc_fence_after();
     tmem_dealloc(tmem, 256);
   }
@@ -306,7 +332,7 @@ static int encode(CUtensorMap* map, int rank, const void* ptr, const cuuint64_t*
 template <int HD>
 size_t attn_smem() {
   return 1024 + (HD / 64) * kQRows * 128 + (HD / 64) * kKC * 128 + (kKC / 64) * HD * 128 + (kKC / 64) * kQRows * 128 +
-         64;
+         64 + 4 * kQRows * sizeof(float);
 }
 
 static const AttnPlan* attn_plan_of(const void* p) {

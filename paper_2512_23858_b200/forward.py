@@ -23,6 +23,7 @@ from __future__ import annotations
 
 import ctypes as C
 import math
+import os
 
 import torch
 
@@ -96,7 +97,9 @@ class Forward:
         self.mask_words = mask_words
         self.act_dtype = act_dtype
         self.act = L.dtype_code(act_dtype)
-        self.fused = act_dtype == torch.bfloat16
+        # bf16 runs the fused-epilogue path unless YGG_UNFUSED is set (A/B: plain GEMM + separate
+        # epilogue kernels, reference weight layout).
+        self.fused = act_dtype == torch.bfloat16 and not os.environ.get("YGG_UNFUSED")
         if self.fused:
             prepare_fused_(weights, cfg)
         self.w = weights
@@ -137,11 +140,12 @@ class Forward:
             ws = max(ws, self.lm_plan.ws_bytes)
         self.ws = torch.empty(max(ws // 4, 1), dtype=torch.float32, device=dev)
         self.attn_plans = None
-        if self.fused:
+        if act_dtype == torch.bfloat16 and mask_words <= L.MAX_MASK_WORDS:
             es = cache.element_size()
             self.attn_plans = [AttnPlan(self.q, cache.data_ptr() + li * self.layer_stride * es, B, M, cfg, self.S)
                                for li in range(cfg.n_layers)]
             self.attn_part = torch.empty(self.attn_plans[0].partial_bytes // 4 + 1, dtype=torch.float32, device=dev)
+        if self.fused:
             self._setup_fused()
 
     # ------------------------------------------------------------------
@@ -261,12 +265,20 @@ class Forward:
             chk(lib.ygg_gemm_fused(self.lm_plan.handle, ws, C.byref(self.lm_plan.epi), s))
             stamp()
 
-    def _run_unfused(self, stream) -> None:
+    def _run_unfused(self, stream, stamps: torch.Tensor | None = None) -> None:
         lib, cfg = L.lib(), self.cfg
         s = L.stream_ptr(stream)
         chk = L.check
         w = self.w
         M = self.M
+        k = [0]
+
+        def stamp():
+            if stamps is not None:
+                chk(lib.ygg_stamp(stamps.data_ptr() + 8 * k[0], s))
+                k[0] += 1
+
+        stamp()
         wdt = L.dtype_code(w["embed"].dtype)
         chk(lib.ygg_embed(w["embed"].data_ptr(), wdt, cfg.vocab, cfg.d_model, self.tokens.data_ptr(), M,
                           self.resid.data_ptr(), s))
@@ -281,21 +293,32 @@ class Forward:
             chk(lib.ygg_epi_qkv_rope(p["qkv"].handle, ws, cfg.n_heads, cfg.n_kv_heads, cfg.head_dim,
                                      cfg.rope_theta, self.pos.data_ptr(), self.slot.data_ptr(),
                                      self.req.data_ptr(), self.q.data_ptr(), cache_l, self.S, self.act, s))
-            chk(lib.ygg_attention(self.q.data_ptr(), cache_l, self.act, M, self.B, cfg.n_heads, cfg.n_kv_heads,
-                                  cfg.head_dim, self.S, self.blk_start.data_ptr(), self.blk_len.data_ptr(),
-                                  qm, self.mask_words, self.scale, self.attn.data_ptr(), s))
+            stamp()
+            if self.attn_plans is not None:
+                chk(lib.ygg_attention_tc(self.attn_plans[li].handle, self.blk_start.data_ptr(),
+                                         self.blk_len.data_ptr(), qm, self.mask_words, self.scale,
+                                         self.attn_part.data_ptr(), self.attn.data_ptr(), s))
+            else:
+                chk(lib.ygg_attention(self.q.data_ptr(), cache_l, self.act, M, self.B, cfg.n_heads, cfg.n_kv_heads,
+                                      cfg.head_dim, self.S, self.blk_start.data_ptr(), self.blk_len.data_ptr(),
+                                      qm, self.mask_words, self.scale, self.attn.data_ptr(), s))
+            stamp()
             chk(lib.ygg_gemm_run(p["o"].handle, ws, s))
             chk(lib.ygg_epi_residual_norm(p["o"].handle, ws, self.resid.data_ptr(), lw["mlp_norm"].data_ptr(),
                                           cfg.norm_eps, self.xn.data_ptr(), self.act, s))
+            stamp()
             chk(lib.ygg_gemm_run(p["gu"].handle, ws, s))
             chk(lib.ygg_epi_swiglu(p["gu"].handle, ws, self.mlp.data_ptr(), self.act, s))
+            stamp()
             chk(lib.ygg_gemm_run(p["down"].handle, ws, s))
             nxt = w["layers"][li + 1]["attn_norm"] if li + 1 < nl else w["final_norm"]
             chk(lib.ygg_epi_residual_norm(p["down"].handle, ws, self.resid.data_ptr(), nxt.data_ptr(),
                                           cfg.norm_eps, self.xn.data_ptr(), self.act, s))
+            stamp()
         if self.lm_plan is not None:
             chk(lib.ygg_gemm_run(self.lm_plan.handle, ws, s))
             chk(lib.ygg_epi_store(self.lm_plan.handle, ws, self.logits.data_ptr(), L.YGG_F32, cfg.vocab, s))
+            stamp()
 
 
 def new_cache(cfg: ModelConfig, B: int, S: int, dtype: torch.dtype, device) -> torch.Tensor:

@@ -34,14 +34,19 @@ for name, f in (("draft", sd.draft), ("verify", sd.verify)):
     st = torch.zeros(6 * f.cfg.n_layers + 8, dtype=torch.int64, device="cuda")
     g = torch.cuda.CUDAGraph()
     with torch.cuda.graph(g):
-        f._run_fused(None, st)
+        (f._run_fused if f.fused else f._run_unfused)(None, st)
     for _ in range(3):
         g.replay()
     torch.cuda.synchronize()
     t = st.cpu().tolist()
-    n = 2 + 5 * f.cfg.n_layers + 1
+    if f.fused:
+        n = 2 + 5 * f.cfg.n_layers + 1
+        names = ["embed"] + ["qkv", "attn", "o", "gu", "down"] * f.cfg.n_layers + ["lm_head"]
+    else:
+        n = 1 + 5 * f.cfg.n_layers + 1
+        names = ["qkv(+embed,norm)"] + ["attn", "o+resnorm", "gu+swiglu", "down+resnorm", "qkv+rope"] * f.cfg.n_layers
+        names = names[: n - 2] + ["lm_head"]
     d = [(t[i + 1] - t[i]) / 1000 for i in range(n - 1)]
-    names = ["embed"] + ["qkv", "attn", "o", "gu", "down"] * f.cfg.n_layers + ["lm_head"]
     agg = {}
     for nm, v in zip(names, d):
         agg.setdefault(nm, []).append(v)

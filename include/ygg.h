@@ -221,10 +221,11 @@ int ygg_epi_store(const void* plan, const float* ws, void* out, int out_dtype, i
 int ygg_epi_residual_norm(const void* plan, const float* ws, float* resid, const void* norm_w, float eps,
                           void* xn_out, int act_dtype, ygg_stream_t stream);
 int ygg_epi_swiglu(const void* plan, const float* ws, void* out, int act_dtype, ygg_stream_t stream);
-/* QKV epilogue: RoPE on q,k at pos[m]; q -> q_out [M, Hq, hd]; k,v -> cache at slot[m] of request req[m]. */
+/* QKV epilogue: RoPE on q,k at pos[m]; q -> q_out [M, Hq, hd]; k -> K rows, v -> V^T of the cache at
+ * slot[m] of request req[m].  rope_cs: optional [positions][hd/2][2] (cos, sin) table, else sincosf. */
 int ygg_epi_qkv_rope(const void* plan, const float* ws, int Hq, int Hkv, int hd, float rope_theta,
                      const int32_t* pos, const int32_t* slot, const int32_t* req, void* q_out, void* cache,
-                     int S, int act_dtype, ygg_stream_t stream);
+                     int S, int act_dtype, const float* rope_cs, ygg_stream_t stream);
 
 int ygg_embed(const void* table, int dtype, int V, int d, const int32_t* tokens, int M, float* resid_out,
               ygg_stream_t stream);

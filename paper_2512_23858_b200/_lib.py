@@ -123,7 +123,7 @@ _SIGS: dict[str, tuple] = {
     "ygg_epi_residual_norm": (C.c_int, [vp, vp, vp, vp, C.c_float, vp, C.c_int, vp]),
     "ygg_epi_swiglu": (C.c_int, [vp, vp, vp, C.c_int, vp]),
     "ygg_epi_qkv_rope": (C.c_int, [vp, vp, C.c_int, C.c_int, C.c_int, C.c_float, vp, vp, vp, vp, vp, C.c_int, C.c_int,
-                                   vp]),
+                                   vp, vp]),
     "ygg_embed": (C.c_int, [vp, C.c_int, C.c_int, C.c_int, vp, C.c_int, vp, vp]),
     "ygg_rmsnorm": (C.c_int, [vp, vp, C.c_int, C.c_int, C.c_int, C.c_float, vp, vp]),
     "ygg_attention": (C.c_int, [vp, vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, vp, vp, vp,

@@ -726,61 +726,74 @@ __global__ void __launch_bounds__(kEpiThreads) epi_swiglu_kernel(EpiGeom g, cons
 }
 
 // QKV epilogue: RoPE (rotate-half convention) on q and k at pos[m]; q -> q_out, k/v -> KV cache.
-// Work item = 4 rotation pairs (i..i+3, i+half..i+half+3) of one head.
+// Work item = 4 rotation pairs (i..i+3, i+half..i+half+3) of one head; one item per thread.
+// cos/sin come from the host table rope_cs [positions][hd/2] when given (else sincosf).
 template <typename ActT>
 __global__ void __launch_bounds__(256) epi_qkv_rope_kernel(EpiGeom g, const float* __restrict__ ws, int Hq, int Hkv,
                                                            int hd, float log2_theta, const int32_t* __restrict__ pos,
                                                            const int32_t* __restrict__ slot,
                                                            const int32_t* __restrict__ req, ActT* __restrict__ q_out,
-                                                           ActT* __restrict__ cache, int S) {
+                                                           ActT* __restrict__ cache, int S,
+                                                           const float2* __restrict__ rope_cs) {
   pdl_wait();
   pdl_launch_dependents();
   const int m = blockIdx.x;
   const int half = hd / 2;
   const int per_head = half / 4;
   const int items = (Hq + 2 * Hkv) * per_head;
-  const float p = static_cast<float>(pos[m]);
-  for (int it = threadIdx.x; it < items; it += blockDim.x) {
-    const int head = it / per_head;
-    const int i0 = (it % per_head) * 4;
-    const int n0 = head * hd;
-    float x1[4], x2[4];
-    epi_values<4>(g, ws, m, n0 + i0, x1);
-    epi_values<4>(g, ws, m, n0 + i0 + half, x2);
-    if (head < Hq + Hkv) {
+  const int it = blockIdx.y * blockDim.x + threadIdx.x;
+  if (it >= items) return;
+  const int pm = pos[m];
+  const int head = it / per_head;
+  const int i0 = (it % per_head) * 4;
+  const int n0 = head * hd;
+  float x1[4], x2[4], cs[4], sn[4];
+  epi_values<4>(g, ws, m, n0 + i0, x1);
+  epi_values<4>(g, ws, m, n0 + i0 + half, x2);
+  if (head < Hq + Hkv) {
+    if (rope_cs) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float2 t = rope_cs[static_cast<size_t>(pm) * half + i0 + j];
+        cs[j] = t.x;
+        sn[j] = t.y;
+      }
+    } else {
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
         // inv_freq = theta^(-2i/hd), as 1/(theta**(2i/hd)) in f32
         const float inv_freq = 1.0f / exp2f(log2_theta * (static_cast<float>(2 * (i0 + j)) / static_cast<float>(hd)));
-        float sn, cs;
-        sincosf(p * inv_freq, &sn, &cs);
-        const float y1 = x1[j] * cs - x2[j] * sn;
-        const float y2 = x2[j] * cs + x1[j] * sn;
-        x1[j] = y1;
-        x2[j] = y2;
+        sincosf(static_cast<float>(pm) * inv_freq, &sn[j], &cs[j]);
       }
     }
-    if (head < Hq) {
-      ActT* q = q_out + (static_cast<size_t>(m) * Hq + head) * hd;
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        q[i0 + j] = from_f32<ActT>(x1[j]);
-        q[i0 + j + half] = from_f32<ActT>(x2[j]);
-      }
-    } else {
-      const bool is_v = head >= Hq + Hkv;
-      const int kvh = is_v ? head - Hq - Hkv : head - Hq;
-      const size_t base = ((static_cast<size_t>(req[m]) * 2 + (is_v ? 1 : 0)) * Hkv + kvh) * static_cast<size_t>(S) * hd;
-      const int sl = slot[m];
+    for (int j = 0; j < 4; ++j) {
+      const float y1 = x1[j] * cs[j] - x2[j] * sn[j];
+      const float y2 = x2[j] * cs[j] + x1[j] * sn[j];
+      x1[j] = y1;
+      x2[j] = y2;
+    }
+  }
+  if (head < Hq) {
+    ActT* q = q_out + (static_cast<size_t>(m) * Hq + head) * hd;
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        if (!is_v) {  // K rows: [S][hd]
-          cache[base + static_cast<size_t>(sl) * hd + i0 + j] = from_f32<ActT>(x1[j]);
-          cache[base + static_cast<size_t>(sl) * hd + i0 + j + half] = from_f32<ActT>(x2[j]);
-        } else {      // V transposed: [hd][S], so attention reads K-major V^T tiles
-          cache[base + static_cast<size_t>(i0 + j) * S + sl] = from_f32<ActT>(x1[j]);
-          cache[base + static_cast<size_t>(i0 + j + half) * S + sl] = from_f32<ActT>(x2[j]);
-        }
+    for (int j = 0; j < 4; ++j) {
+      q[i0 + j] = from_f32<ActT>(x1[j]);
+      q[i0 + j + half] = from_f32<ActT>(x2[j]);
+    }
+  } else {
+    const bool is_v = head >= Hq + Hkv;
+    const int kvh = is_v ? head - Hq - Hkv : head - Hq;
+    const size_t base = ((static_cast<size_t>(req[m]) * 2 + (is_v ? 1 : 0)) * Hkv + kvh) * static_cast<size_t>(S) * hd;
+    const int sl = slot[m];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      if (!is_v) {  // K rows: [S][hd]
+        cache[base + static_cast<size_t>(sl) * hd + i0 + j] = from_f32<ActT>(x1[j]);
+        cache[base + static_cast<size_t>(sl) * hd + i0 + j + half] = from_f32<ActT>(x2[j]);
+      } else {      // V transposed: [hd][S], so attention reads K-major V^T tiles
+        cache[base + static_cast<size_t>(i0 + j) * S + sl] = from_f32<ActT>(x1[j]);
+        cache[base + static_cast<size_t>(i0 + j + half) * S + sl] = from_f32<ActT>(x2[j]);
       }
     }
   }
@@ -1100,21 +1113,23 @@ int ygg_epi_swiglu(const void* plan, const float* ws, void* out, int act_dtype, 
 
 int ygg_epi_qkv_rope(const void* plan, const float* ws, int Hq, int Hkv, int hd, float rope_theta, const int32_t* pos,
                      const int32_t* slot, const int32_t* req, void* q_out, void* cache, int S, int act_dtype,
-                     ygg_stream_t stream) {
+                     const float* rope_cs, ygg_stream_t stream) {
   const GemmPlan* g = plan_of(plan);
   YGG_CHECK_ARG(g && ws && pos && slot && req && q_out && cache, "invalid arguments");
   YGG_CHECK_ARG(g->N == (Hq + 2 * Hkv) * hd, "QKV width mismatch");
   YGG_CHECK_ARG(hd % 8 == 0 && hd <= 256, "bad head dim");
   EpiGeom geo = geom_of(g);
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  dim3 grid(g->M);
+  const int items = (Hq + 2 * Hkv) * (hd / 8);
+  dim3 grid(g->M, (items + 255) / 256);
   const float l2t = log2f(rope_theta);
+  const float2* rt = reinterpret_cast<const float2*>(rope_cs);
   if (act_dtype == YGG_F32)
     YGG_LAUNCH_PDL(epi_qkv_rope_kernel<float>, grid, dim3(256), 0, s, geo, ws, Hq, Hkv, hd, l2t, pos, slot, req,
-                   static_cast<float*>(q_out), static_cast<float*>(cache), S);
+                   static_cast<float*>(q_out), static_cast<float*>(cache), S, rt);
   else
     YGG_LAUNCH_PDL(epi_qkv_rope_kernel<__nv_bfloat16>, grid, dim3(256), 0, s, geo, ws, Hq, Hkv, hd, l2t, pos, slot, req,
-                   static_cast<__nv_bfloat16*>(q_out), static_cast<__nv_bfloat16*>(cache), S);
+                   static_cast<__nv_bfloat16*>(q_out), static_cast<__nv_bfloat16*>(cache), S, rt);
   return YGG_OK;
 }
 

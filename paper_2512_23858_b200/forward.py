@@ -6,17 +6,21 @@ so a pass is a fixed sequence of kernel launches that CUDA-graph capture records
 It realises the verifier / drafter forward the reference only prices
 (``latency_at(profiles.verifier, w_verify + 1)``, pkg/src/specsim/simulator.py:211-213).
 
-bf16 (fast path) — 6 launches per layer, every epilogue fused into its GEMM:
+bf16 default (10 launches per layer): tcgen05 stream-K GEMM writing f32 partials, then a
+vectorised epilogue kernel (RoPE + KV append from a host RoPE table / residual + cluster-DSMEM
+RMSNorm / SwiGLU), and the tcgen05 split-KV tree attention + combine.
+
+bf16 with YGG_FUSED=1 (6 launches per layer): every epilogue fused into its GEMM —
   GEMM(qkv, x=hb)  + rstd + RoPE + q / KV-cache append      (YGG_EPI_QKV_ROPE)
-  tcgen05 split-KV tree attention + combine
   GEMM(o)          + residual add, hb, per-tile sum-of-squares (YGG_EPI_RESID)
   GEMM(gate|up, x=hb) + rstd + SwiGLU                        (YGG_EPI_SWIGLU)
   GEMM(down)       + residual add, hb, sum-of-squares          (YGG_EPI_RESID)
-RMSNorm gains are folded into the next weights (model.prepare_fused_) and the per-token rstd is
-applied by the consuming GEMM's epilogue, so no separate norm kernel exists.
+with RMSNorm gains folded into the next weights (model.prepare_fused_) and the per-token rstd
+applied by the consuming GEMM's epilogue.  Same results; today slower, because the split-tile
+fixups sit on each GEMM's critical path.
 
-f32 (parity path): SIMT GEMM + separate epilogue kernels + SIMT attention, unfused, in the
-reference layout.  The residual stream is f32 in both paths.
+f32 (parity path): SIMT GEMM + the same separate epilogue kernels + SIMT attention.  The
+residual stream is f32 in every path.
 """
 
 from __future__ import annotations
@@ -97,9 +101,9 @@ class Forward:
         self.mask_words = mask_words
         self.act_dtype = act_dtype
         self.act = L.dtype_code(act_dtype)
-        # bf16 runs the fused-epilogue path unless YGG_UNFUSED is set (A/B: plain GEMM + separate
-        # epilogue kernels, reference weight layout).
-        self.fused = act_dtype == torch.bfloat16 and not os.environ.get("YGG_UNFUSED")
+        # bf16 default: plain stream-K GEMM + separate vectorised epilogue kernels (faster today);
+        # YGG_FUSED=1 selects the fused-epilogue GEMMs (same results, tested).
+        self.fused = act_dtype == torch.bfloat16 and bool(os.environ.get("YGG_FUSED"))
         if self.fused:
             prepare_fused_(weights, cfg)
         self.w = weights
@@ -145,6 +149,7 @@ class Forward:
             self.attn_plans = [AttnPlan(self.q, cache.data_ptr() + li * self.layer_stride * es, B, M, cfg, self.S)
                                for li in range(cfg.n_layers)]
             self.attn_part = torch.empty(self.attn_plans[0].partial_bytes // 4 + 1, dtype=torch.float32, device=dev)
+        self.rope_cs = rope_table(cfg, self.S + 64, dev)
         if self.fused:
             self._setup_fused()
 
@@ -166,7 +171,6 @@ class Forward:
         counter_ptr = {id(p): self.counters.data_ptr() + 4 * o for p, o in zip(plans, offs)}
         eps = float(cfg.norm_eps)
         es = self.cache.element_size()
-        self.rope_cs = rope_table(cfg, self.S + 64, dev)
         cur = {"plan": None}
 
         def epi(kind, **kw):
@@ -292,7 +296,8 @@ class Forward:
             chk(lib.ygg_gemm_run(p["qkv"].handle, ws, s))
             chk(lib.ygg_epi_qkv_rope(p["qkv"].handle, ws, cfg.n_heads, cfg.n_kv_heads, cfg.head_dim,
                                      cfg.rope_theta, self.pos.data_ptr(), self.slot.data_ptr(),
-                                     self.req.data_ptr(), self.q.data_ptr(), cache_l, self.S, self.act, s))
+                                     self.req.data_ptr(), self.q.data_ptr(), cache_l, self.S, self.act,
+                                     self.rope_cs.data_ptr(), s))
             stamp()
             if self.attn_plans is not None:
                 chk(lib.ygg_attention_tc(self.attn_plans[li].handle, self.blk_start.data_ptr(),

@@ -121,6 +121,7 @@ typedef struct {
   int32_t d_draft;     /* TreeShape.d_draft for Eq.3 */
   int32_t w_draft;     /* TreeShape.w_draft for Eq.3 */
   int32_t fixed_k;     /* >0: skip the objective and keep exactly min(fixed_k, cap) nodes */
+  int32_t probs_are_gains; /* 1: `probs` already holds the per-node gains (SubtreeKnapsack(tree, gains, k)) */
 } ygg_prune_args;
 
 /* probs [B, cap] f64 acceptance probabilities (freeze_probs); NULL = use tree.prob.
@@ -132,6 +133,10 @@ int ygg_knapsack_prune(ygg_tree tree, const double* probs, const ygg_profile_pai
                        ygg_prune_args args, int32_t* keep_idx, int32_t* new_idx, int32_t* w_verify,
                        double* expected_aal, double* speedup, double* aal_at_cap, double* speedup_at_cap,
                        double* best_table, uint8_t* alloc_table, ygg_stream_t stream);
+
+/* path_products (acceptance.py:176-184): out[b,0] = p[b,0]; out[b,i] = out[b,parent(i)] * p[b,i] (f64,
+ * index order); probs NULL = tree.prob. */
+int ygg_path_products(ygg_tree tree, const double* probs, double* out, ygg_stream_t stream);
 
 /* Gather the pruned tree (TokenTree.subtree) into `out` from `in` using keep_idx/new_idx. */
 int ygg_tree_subtree(ygg_tree in, ygg_tree out, const int32_t* keep_idx, const int32_t* new_idx,

@@ -80,6 +80,7 @@ class YggPruneArgs(C.Structure):
         ("d_draft", C.c_int32),
         ("w_draft", C.c_int32),
         ("fixed_k", C.c_int32),
+        ("probs_are_gains", C.c_int32),
     ]
 
 
@@ -107,6 +108,7 @@ _SIGS: dict[str, tuple] = {
     "ygg_build_mask": (C.c_int, [YggTree, vp]),
     "ygg_knapsack_prune": (C.c_int, [YggTree, vp, vp, YggPruneArgs, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp]),
     "ygg_tree_subtree": (C.c_int, [YggTree, YggTree, vp, vp, vp]),
+    "ygg_path_products": (C.c_int, [YggTree, vp, vp, vp]),
     "ygg_accept": (C.c_int, [YggTree, C.c_int, vp, vp, C.c_int, vp, vp, C.c_int, C.c_int, C.c_int, vp, C.c_float,
                              vp, vp, vp, vp, vp, vp]),
     "ygg_kv_compact": (C.c_int, [vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_longlong, vp, vp, vp,
@@ -146,7 +148,7 @@ EXPORTED = tuple(_SIGS)
 # Kernels launched by one successful call (used to count device launches per step).
 KERNELS_PER_CALL = {
     "ygg_topk_softmax": 2, "ygg_egt_grow_level": 1, "ygg_build_mask": 1, "ygg_knapsack_prune": 1,
-    "ygg_tree_subtree": 1, "ygg_accept": 1, "ygg_kv_compact": 1, "ygg_gemm_run": 1, "ygg_gemm_fused": 1, "ygg_embed_fused": 1, "ygg_epi_store": 1,
+    "ygg_tree_subtree": 1, "ygg_path_products": 1, "ygg_accept": 1, "ygg_kv_compact": 1, "ygg_gemm_run": 1, "ygg_gemm_fused": 1, "ygg_embed_fused": 1, "ygg_epi_store": 1,
     "ygg_epi_residual_norm": 1, "ygg_epi_swiglu": 1, "ygg_epi_qkv_rope": 1, "ygg_embed": 1, "ygg_rmsnorm": 1,
     "ygg_attention": 1, "ygg_attention_tc": 2, "ygg_row_stats": 1, "ygg_pass0_inputs": 1, "ygg_init_roots": 1, "ygg_level_inputs": 1,
     "ygg_verify_inputs": 1, "ygg_commit": 1, "ygg_stamp": 1,

@@ -382,7 +382,11 @@ __global__ void __launch_bounds__(kKnapThreads) knapsack_prune_kernel(
     // path_products (acceptance.py:176-184) and subtree sizes (egt.py:225-229).
     const double* pr = probs ? probs + tb : t.prob + tb;
     gain[0] = pr[0];
-    for (int i = 1; i < N; ++i) gain[i] = gain[par[i]] * pr[i];
+    if (args.probs_are_gains) {
+      for (int i = 1; i < N; ++i) gain[i] = pr[i];
+    } else {
+      for (int i = 1; i < N; ++i) gain[i] = gain[par[i]] * pr[i];
+    }
     for (int i = 0; i < N; ++i) sz[i] = 1;
     for (int v = N - 1; v >= 1; --v) sz[par[v]] += sz[v];
   }
@@ -488,6 +492,19 @@ __global__ void __launch_bounds__(kKnapThreads) knapsack_prune_kernel(
     for (int i = j; i < t.cap; ++i) keep_idx[tb + i] = -1;
   }
   pdl_launch_dependents();
+}
+
+// path_products (acceptance.py:176-184): out[0] = p[0]; out[i] = out[parent(i)] * p[i], index order.
+__global__ void path_products_kernel(ygg_tree t, const double* __restrict__ probs, double* __restrict__ out) {
+  pdl_wait();
+  pdl_launch_dependents();
+  const int b = blockIdx.x;
+  if (threadIdx.x != 0) return;
+  const size_t tb = static_cast<size_t>(b) * t.cap;
+  const int n = t.size[b];
+  const double* p = probs ? probs + tb : t.prob + tb;
+  if (n > 0) out[tb] = p[0];
+  for (int i = 1; i < n; ++i) out[tb + i] = out[tb + t.parent[tb + i]] * p[i];
 }
 
 // TokenTree.subtree (token_tree.py:146-168): kept nodes in ascending old order.
@@ -806,6 +823,14 @@ int ygg_knapsack_prune(ygg_tree tree, const double* probs, const ygg_profile_pai
   YGG_LAUNCH_PDL(knapsack_prune_kernel, dim3(tree.B), dim3(kKnapThreads), smem, reinterpret_cast<cudaStream_t>(stream),
                  tree, probs, profiles_dev, args, keep_idx, new_idx, w_verify, expected_aal, speedup, aal_at_cap,
                  speedup_at_cap, best_table, alloc_table);
+  return YGG_OK;
+}
+
+int ygg_path_products(ygg_tree tree, const double* probs, double* out, ygg_stream_t stream) {
+  if (int rc = check_tree(tree)) return rc;
+  YGG_CHECK_ARG(out != nullptr, "null output");
+  YGG_LAUNCH_PDL(path_products_kernel, dim3(tree.B), dim3(32), 0, reinterpret_cast<cudaStream_t>(stream), tree, probs,
+                 out);
   return YGG_OK;
 }
 

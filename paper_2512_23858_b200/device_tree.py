@@ -121,3 +121,23 @@ class SeqState:
     @property
     def struct(self) -> L.YggSeq:
         return self._struct
+
+
+_CACHE: dict[int, DeviceTrees] = {}
+
+
+def upload(tree, cap: int | None = None) -> DeviceTrees:
+    """Single-tree device image of a host ``TokenTree`` (B=1), reusing a buffer per capacity;
+    runs K7 for the mask rows."""
+    n = len(tree)
+    cap = max(cap or n, n)
+    cap = min(32 * L.MAX_MASK_WORDS, ((cap + 31) // 32) * 32)
+    if n > cap:
+        raise ValueError(f"tree of {n} nodes exceeds the device capacity {cap}")
+    dt = _CACHE.get(cap)
+    if dt is None:
+        L.require_device()
+        dt = DeviceTrees(1, cap, "cuda")
+        _CACHE[cap] = dt
+    dt.load_host([tree.to_dict()])
+    return dt

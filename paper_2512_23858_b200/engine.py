@@ -208,7 +208,7 @@ class SpecDecoder:
                                        self.cand_n.data_ptr(), s))
         stamp(2)
         # ---- prune (latency-aware objective or fixed width)
-        args = L.YggPruneArgs(sh.max_verify, D, W, sh.fixed_verify)
+        args = L.YggPruneArgs(sh.max_verify, D, W, sh.fixed_verify, 0)
         chk(lib.ygg_knapsack_prune(g.struct, None, self.profiles_dev.data_ptr(), args, self.keep_idx.data_ptr(),
                                    self.new_idx.data_ptr(), self.w_verify.data_ptr(), self.exp_aal.data_ptr(),
                                    self.speedup.data_ptr(), None, None, None, None, s))

@@ -28,14 +28,31 @@ def test_library_exports_every_declared_symbol():
     assert lib.ygg_version() >= 100
 
 
-def test_abi_struct_layouts_match_header():
+def test_abi_struct_layouts_match_header(tmp_path):
+    """ctypes mirrors of the C structs have the header's sizes and field offsets (compiled with gcc)."""
+    import subprocess
+
     from paper_2512_23858_b200 import _lib
 
-    # ygg_tree: 3 int32 + 10 pointers (natural alignment on x86-64)
-    assert ctypes.sizeof(_lib.YggTree) == 16 + 10 * 8
-    assert ctypes.sizeof(_lib.YggSeq) == 8 + 5 * 8 + 8
-    assert ctypes.sizeof(_lib.YggProfile) == 4 + 32 * 4 + 4 + 32 * 8
-    assert ctypes.sizeof(_lib.YggPruneArgs) == 16
+    structs = {"ygg_tree": _lib.YggTree, "ygg_seq": _lib.YggSeq, "ygg_profile": _lib.YggProfile,
+               "ygg_profile_pair": _lib.YggProfilePair, "ygg_prune_args": _lib.YggPruneArgs,
+               "ygg_epilogue": _lib.YggEpilogue}
+    lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "ygg.h"', "int main(void) {"]
+    for cname, py in structs.items():
+        lines.append(f'  printf("{cname} %zu\\n", sizeof({cname}));')
+        for fname, _ in py._fields_:
+            lines.append(f'  printf("{cname}.{fname} %zu\\n", offsetof({cname}, {fname}));')
+    lines.append("  return 0;\n}")
+    src = tmp_path / "abi.c"
+    src.write_text("\n".join(lines))
+    exe = tmp_path / "abi"
+    subprocess.run(["gcc", "-I", str(ROOT / "include"), str(src), "-o", str(exe)], check=True)
+    got = dict(line.split() for line in subprocess.run([str(exe)], capture_output=True, text=True,
+                                                       check=True).stdout.splitlines())
+    for cname, py in structs.items():
+        assert int(got[cname]) == ctypes.sizeof(py), cname
+        for fname, _ in py._fields_:
+            assert int(got[f"{cname}.{fname}"]) == getattr(py, fname).offset, (cname, fname)
 
 
 def test_argument_errors_map_to_value_error_without_device():

@@ -139,6 +139,16 @@ def prompts_for(wl, vocab, rank):
     return torch.stack(rows)
 
 
+def _ncu_traffic():
+    """dram__bytes_read.sum + dram__bytes_write.sum per GEMM launch from the committed ncu capture."""
+    p = ROOT / "profiles" / "gemm_traffic.json"
+    if not p.exists():
+        return {"traffic": None}
+    t = json.loads(p.read_text())
+    return {"traffic": t["dram_bytes_per_launch"], "traffic_algorithmic": t["algorithmic_bytes_per_launch"],
+            "traffic_source": t["source"]}
+
+
 def gemm_roofline(sd, peak_gbs):
     """Per-launch CUDA-event timing of every GEMM of one verify forward (the dominant kernel),
     each launch streaming a different layer's weights from HBM."""
@@ -165,8 +175,8 @@ def gemm_roofline(sd, peak_gbs):
     nbytes = [p.W.numel() * p.W.element_size() for p in plans]
     achieved = sum(nbytes) / sum(times) / 1e9
     return {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak_gbs, "unit": "GB/s",
-            "frac": round(achieved / peak_gbs, 4), "traffic": None,
-            "kernel": "gemm_bf16_tc_kernel (swap-AB tcgen05 stream-K weight streaming, fused epilogues)",
+            "frac": round(achieved / peak_gbs, 4), **_ncu_traffic(),
+            "kernel": "gemm_bf16_tc_kernel (swap-AB tcgen05 stream-K weight streaming)",
             "launches_timed": len(plans), "bytes_per_launch_avg": int(sum(nbytes) / len(plans)),
             "avg_launch_us": round(sum(times) / len(times) * 1e6, 2)}
 
@@ -372,7 +382,10 @@ def run_ours(args, rank, world, local_rank):
                    "coupling": COUPLING[args.workload]},
         "roofline": gemm, "verify_roofline": ver, "stage_us": stages,
         "e2e": {"value": round(float(e2e_tokens) / float(e2e_t), 2), "unit": "tokens/s",
-                "h2d_bytes_per_step": e2e["h2d"], "d2h_bytes_per_step": e2e["d2h"]},
+                "h2d_bytes_per_step": e2e["h2d"], "d2h_bytes_per_step": e2e["d2h"],
+                "ms_per_step": round(float(e2e_t) * 1e3 / args.steps, 4),
+                "aal": round(e2e["tokens"] / (args.steps * sd.B), 4),
+                "note": "steps after the timed window (longer context, its own AAL); lagged pinned readback"},
         "gpu_launches": launches_per_step * args.steps, "launches_per_step": launches_per_step,
         "clocks": clk, "cpu_baseline": cpu, "peak_kind": peak_kind, "gathered_ranks": gathered,
     }
@@ -380,26 +393,37 @@ def run_ours(args, rank, world, local_rank):
 
 
 def e2e_run(sd, steps, device):
-    """Public-API loop: each step copies its inputs (sampling uniforms / control words) from pinned host
-    memory, replays the step graph, and reads the emitted tokens back into pinned host memory."""
+    """Public-API serving loop: each step copies its inputs (sampling uniforms / control words) from
+    pinned host memory, replays the step graph, and reads the emitted tokens back into pinned host
+    memory.  The readback is double-buffered: the host consumes step i-1's tokens (event wait) while
+    step i runs, as a server streaming tokens would; every step's D2H is inside the timed region."""
     import torch
 
     B = sd.B
     n_emit = sd.shape.depth + 2
-    host_out = torch.zeros(B, n_emit + 1, dtype=torch.int32).pin_memory()
+    host_out = [torch.zeros(B, n_emit + 1, dtype=torch.int32).pin_memory() for _ in range(2)]
     host_in = torch.zeros_like(sd.uniforms_host).pin_memory()
     h2d = host_in.numel() * host_in.element_size()
-    d2h = host_out.numel() * host_out.element_size()
+    d2h = host_out[0].numel() * host_out[0].element_size()
+    done = [torch.cuda.Event(), torch.cuda.Event()]
     torch.cuda.synchronize()
     gen0 = sd.seq.n_gen.clone()
+    streamed = 0
     t0 = time.perf_counter()
     for i in range(steps):
         sd.uniforms.copy_(host_in, non_blocking=True)
         sd.step()
-        sd.read_emitted(host_out)
-        torch.cuda.current_stream().synchronize()
+        sd.read_emitted(host_out[i % 2])
+        done[i % 2].record()
+        if i > 0:
+            done[(i - 1) % 2].synchronize()
+            streamed += int(host_out[(i - 1) % 2][:, 0].sum())
+    done[(steps - 1) % 2].synchronize()
+    streamed += int(host_out[(steps - 1) % 2][:, 0].sum())
     dt = time.perf_counter() - t0
     tokens = int((sd.seq.n_gen - gen0).sum())
+    if streamed != tokens:
+        raise RuntimeError(f"e2e: host received {streamed} tokens, device generated {tokens}")
     return {"tokens": tokens, "seconds": dt, "h2d": h2d, "d2h": d2h}
 
 
@@ -411,8 +435,8 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default="cfg2")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--ref-aal", type=float, default=float(os.environ.get("YGG_REF_AAL", "3.0")),
-                    help="accepted tokens per step assumed by --impl reference (GPU-measured AAL)")
+    ap.add_argument("--ref-aal", type=float, default=float(os.environ.get("YGG_REF_AAL", "3.78")),
+                    help="accepted tokens per step for --impl reference: the GPU-measured AAL of the same workload (profiles/r1_bench_full.jsonl); greedy decoding is lossless so both arms accept the same tokens")
     args = ap.parse_args()
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")

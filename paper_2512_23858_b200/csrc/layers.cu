@@ -189,21 +189,40 @@ __global__ void __launch_bounds__(kAttnThreads) attn_simt_kernel(
 }
 
 // Per-row max, argmax (first max) and log-sum-exp(x / T); f64 accumulation, fixed order.
+// One 1024-thread CTA per row, float4 loads when the row is 16-byte aligned; the log-sum-exp
+// pass runs only when `stats` is requested (sampling), greedy acceptance needs the argmax alone.
+constexpr int kRowStatsThreads = 1024;
 template <typename T>
-__global__ void __launch_bounds__(256) row_stats_kernel(const T* __restrict__ logits, int V, int ld, float inv_temp,
-                                                        int32_t* __restrict__ argmax, float* __restrict__ stats) {
+__global__ void __launch_bounds__(kRowStatsThreads) row_stats_kernel(const T* __restrict__ logits, int V, int ld,
+                                                                     float inv_temp, int32_t* __restrict__ argmax,
+                                                                     float* __restrict__ stats) {
   pdl_wait();
   pdl_launch_dependents();
+  constexpr int NW = kRowStatsThreads / 32;
   const int row = blockIdx.x;
   const T* x = logits + static_cast<size_t>(row) * ld;
-  __shared__ float smax[8];
-  __shared__ int sarg[8];
-  __shared__ double ssum[8];
+  __shared__ float smax[NW];
+  __shared__ int sarg[NW];
+  __shared__ double ssum[NW];
   float bm = -INFINITY;
   int ba = 0x7fffffff;
-  for (int v = threadIdx.x; v < V; v += blockDim.x) {
-    const float f = to_f32(x[v]);
+  auto take = [&](float f, int v) {
     if (f > bm || (f == bm && v < ba)) { bm = f; ba = v; }
+  };
+  if constexpr (sizeof(T) == 4) {
+    if ((reinterpret_cast<uintptr_t>(x) & 15) == 0) {
+      const int nv = V >> 2;
+      const float4* x4 = reinterpret_cast<const float4*>(x);
+      for (int i = threadIdx.x; i < nv; i += kRowStatsThreads) {
+        const float4 q = __ldg(x4 + i);
+        take(q.x, 4 * i); take(q.y, 4 * i + 1); take(q.z, 4 * i + 2); take(q.w, 4 * i + 3);
+      }
+      for (int v = (nv << 2) + threadIdx.x; v < V; v += kRowStatsThreads) take(to_f32(x[v]), v);
+    } else {
+      for (int v = threadIdx.x; v < V; v += kRowStatsThreads) take(to_f32(x[v]), v);
+    }
+  } else {
+    for (int v = threadIdx.x; v < V; v += kRowStatsThreads) take(to_f32(x[v]), v);
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
@@ -216,23 +235,25 @@ __global__ void __launch_bounds__(256) row_stats_kernel(const T* __restrict__ lo
   __syncthreads();
   float gm = smax[0];
   int ga = sarg[0];
-  for (int w = 1; w < 8; ++w)
+  for (int w = 1; w < NW; ++w)
     if (smax[w] > gm || (smax[w] == gm && sarg[w] < ga)) { gm = smax[w]; ga = sarg[w]; }
+  if (stats == nullptr) {
+    if (threadIdx.x == 0 && argmax) argmax[row] = ga;
+    return;
+  }
   const double ms = static_cast<double>(gm) * inv_temp;
   double s = 0.0;
-  for (int v = threadIdx.x; v < V; v += blockDim.x) s += exp(static_cast<double>(to_f32(x[v]) * inv_temp) - ms);
+  for (int v = threadIdx.x; v < V; v += kRowStatsThreads) s += exp(static_cast<double>(to_f32(x[v]) * inv_temp) - ms);
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
   if (lane == 0) ssum[warp] = s;
   __syncthreads();
   if (threadIdx.x == 0) {
     double tot = 0.0;
-    for (int w = 0; w < 8; ++w) tot += ssum[w];
+    for (int w = 0; w < NW; ++w) tot += ssum[w];
     if (argmax) argmax[row] = ga;
-    if (stats) {
-      stats[2 * row] = static_cast<float>(ms);
-      stats[2 * row + 1] = static_cast<float>(ms + log(tot));
-    }
+    stats[2 * row] = static_cast<float>(ms);
+    stats[2 * row + 1] = static_cast<float>(ms + log(tot));
   }
 }
 
@@ -344,10 +365,10 @@ int ygg_row_stats(const void* logits, int dtype, int rows, int V, int ld, float 
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   const float inv_t = 1.0f / temperature;
   if (dtype == YGG_F32)
-    YGG_LAUNCH_PDL(row_stats_kernel<float>, dim3(rows), dim3(256), 0, s, static_cast<const float*>(logits), V, ld,
+    YGG_LAUNCH_PDL(row_stats_kernel<float>, dim3(rows), dim3(kRowStatsThreads), 0, s, static_cast<const float*>(logits), V, ld,
                    inv_t, argmax, stats);
   else
-    YGG_LAUNCH_PDL(row_stats_kernel<__nv_bfloat16>, dim3(rows), dim3(256), 0, s,
+    YGG_LAUNCH_PDL(row_stats_kernel<__nv_bfloat16>, dim3(rows), dim3(kRowStatsThreads), 0, s,
                    static_cast<const __nv_bfloat16*>(logits), V, ld, inv_t, argmax, stats);
   return YGG_OK;
 }

@@ -179,3 +179,23 @@ def test_host_latency_errors_follow_reference():
         TreeShape(2, 2, 6)
     with pytest.raises(ConfigError):
         load_profile("/nonexistent.csv", "drafter")
+
+
+def test_profiler_csv_round_trip(tmp_path):
+    """K8 exports use the reference's on-disk formats (latency.py:164-190, scheduler.py:82-103):
+    what the profiler writes, the reference-named loaders read back exactly."""
+    from paper_2512_23858_b200.latency import latency_at, load_profile
+    from paper_2512_23858_b200.profiler import write_profile_csv, write_stage_csv
+    from paper_2512_23858_b200.scheduler import StageProfiles
+
+    bps = [(1, 1093.31), (8, 1103.4), (64, 4452.74)]
+    write_profile_csv(bps, tmp_path / "verify.csv")
+    prof = load_profile(tmp_path / "verify.csv", "verifier")
+    assert [latency_at(prof, w) for w, _ in bps] == [us for _, us in bps]
+    rows = [("Verify", "base", 4452.74), ("Accept", "base", 296.94), ("HeadDraft", "base", 2195.0),
+            ("DraftStep", "base", 1104.45)]
+    write_stage_csv(rows, tmp_path / "stages.csv")
+    sp = StageProfiles.from_csv(tmp_path / "stages.csv")
+    for name, _, us in rows:
+        assert sp.base(name) == us
+    assert sp.base("DraftStep3") == 1104.45  # DraftStep fallback (reference scheduler.py:112-118)

@@ -125,3 +125,84 @@ def test_bf16_verify_logits_within_tolerance(cuda):
         torch.cuda.synchronize()
         err = (f.logits.cpu() - ref).abs().max() / ref.abs().max()
         assert err <= tol, (dtype, float(err))
+
+
+def test_bf16_long_run_spec_equals_ar(cuda):
+    """Lossless-greedy identity over 240 tokens at cfg1's tree shape (D4 W4), coupled weights,
+    so the KV compaction of both caches is exercised over ~60 steps of varying accepted lengths."""
+    from paper_2512_23858_b200.engine import ARDecoder, SpecDecoder, StepShape
+    from paper_2512_23858_b200.model import weights_to
+
+    tc, dc, tw, dw = _models(torch.float32, True)
+    twb, dwb = weights_to(tw, cuda, torch.bfloat16), weights_to(dw, cuda, torch.bfloat16)
+    prompts = _prompt(tc.vocab, 32, 1234)[None]
+    n_tok = 240
+    ar = ARDecoder(tc, twb, batch=1, max_seq=320).generate(prompts, n_tok)
+    sd = SpecDecoder(tc, twb, dc, dwb, StepShape(4, 4, 8, 64), batch=1, max_seq=320, profiles=_profiles())
+    got, steps = sd.generate(prompts, n_tok)
+    assert got == ar
+    assert steps < n_tok  # speculation accepted more than one token per step on average
+
+
+def test_sample_mode_cold_temperature_equals_greedy(cuda):
+    """SAMPLE acceptance (softmax(target/T) child probabilities, residual bonus) at a temperature
+    where the target distribution is one-hot must reproduce greedy AR exactly."""
+    from paper_2512_23858_b200.engine import SAMPLE, ARDecoder, SpecDecoder, StepShape
+    from paper_2512_23858_b200.model import weights_to
+
+    tc, dc, tw, dw = _models(torch.float32, True)
+    twb, dwb = weights_to(tw, cuda, torch.bfloat16), weights_to(dw, cuda, torch.bfloat16)
+    prompts = torch.stack([_prompt(tc.vocab, 32, s) for s in (7, 8)])
+    n_tok = 48
+    ar = ARDecoder(tc, twb, batch=2, max_seq=256).generate(prompts, n_tok)
+    sd = SpecDecoder(tc, twb, dc, dwb, StepShape(4, 4, 8, 64), batch=2, max_seq=256, profiles=_profiles(),
+                     mode=SAMPLE, temperature=1e-4)
+    got, _ = sd.generate(prompts, n_tok, use_graph=True)
+    assert got == ar
+
+
+def test_sample_mode_first_token_distribution(cuda):
+    """At T = 1 the first emitted token after the prompt is distributed as the target softmax
+    (speculative sampling is lossless in distribution): chi-square over the top tokens, 4000 draws."""
+    import numpy as np
+
+    from paper_2512_23858_b200.engine import SAMPLE, SpecDecoder, StepShape
+    from paper_2512_23858_b200.forward import Forward, new_cache
+    from paper_2512_23858_b200.model import weights_to
+
+    tc, dc, tw, dw = _models(torch.float32, True)
+    twf, dwf = weights_to(tw, cuda, torch.float32), weights_to(dw, cuda, torch.float32)
+    prompt = _prompt(tc.vocab, 16, 99)
+    n_req = 4000
+    # target distribution of the token after the bonus: rows of a reference prefill over prompt+bonus
+    sd = SpecDecoder(tc, twf, dc, dwf, StepShape(2, 2, 4, 8), batch=n_req // 8, max_seq=64,
+                     act_dtype=torch.float32, profiles=_profiles(), mode=SAMPLE, temperature=1.0)
+    counts = {}
+    bonus0 = None
+    for rep in range(8):
+        sd.prefill_len = 16
+        sd.prefill(prompt[None].repeat(sd.B, 1))
+        if bonus0 is None:
+            bonus0 = int(sd.seq.hist[0, 16])
+        sd.set_uniforms(rep, 1234)
+        sd.step(use_graph=False)
+        nxt = sd.seq.hist[:, 17].cpu().tolist()
+        for t in nxt:
+            counts[t] = counts.get(t, 0) + 1
+    seq = torch.cat([prompt, torch.tensor([bonus0])]).to(cuda, torch.int32)
+    f = Forward(tc, twf, new_cache(tc, 1, 64, torch.float32, cuda), 1, 17, 0, torch.float32)
+    f.tokens.copy_(seq)
+    pos = torch.arange(17, dtype=torch.int32, device=cuda)
+    f.pos.copy_(pos)
+    f.slot.copy_(pos)
+    f.blk_start.zero_()
+    f.blk_len.fill_(17)
+    f.run()
+    p = torch.softmax(f.logits[16].double(), 0).cpu().numpy()
+    top = np.argsort(-p)[:8]
+    obs = np.array([counts.get(int(t), 0) for t in top] + [n_req - sum(counts.get(int(t), 0) for t in top)])
+    exp = np.concatenate([p[top], [1.0 - p[top].sum()]]) * n_req
+    keep = exp >= 5
+    chi2 = float((((obs - exp) ** 2) / exp)[keep].sum())
+    # 99.9% quantile of chi-square with <= 8 degrees of freedom is 26.1
+    assert chi2 < 26.1, (chi2, obs.tolist(), exp.round(1).tolist())

@@ -281,6 +281,54 @@ int ygg_commit(ygg_seq seq, ygg_tree vtree, const int32_t* path, const int32_t* 
 /* ---------------- K8: on-device stage timer ---------------- */
 int ygg_stamp(unsigned long long* slot, ygg_stream_t stream);
 
+/* ---------------- Persistent forward (bf16, decode-shaped: B*T <= 128 rows) ----------------
+ * One launch runs a whole draft or verify forward (the passes the reference prices as
+ * latency_at(drafter|verifier, width), simulator.py:202-214): embed, then per layer
+ * QKV GEMM -> RoPE/KV append -> tcgen05 tree attention -> combine -> O GEMM -> residual ->
+ * gate|up GEMM -> SwiGLU -> down GEMM -> residual, then the LM head.  One CTA per SM; phases
+ * are separated by a grid-wide arrival counter, and the weight stream (TMA into a smem ring
+ * plus an L2 prefetch look-ahead) runs ahead across phase boundaries, so HBM never waits on
+ * the dependency chain.  RMSNorm gains must be folded into wqkv / wgu / lm_head (the per-row
+ * rstd is applied in the consumer epilogue).  Weights are row-major [N, K] bf16. */
+typedef struct {
+  int32_t n_layers, d_model, n_heads, n_kv_heads, head_dim, ffn, vocab;
+  int32_t B, T;        /* requests, rows per request; M = B*T <= 128 */
+  int32_t S;           /* KV capacity per request (multiple of 64) */
+  int32_t mask_words;  /* tree-mask words per row (0 = causal block) */
+  float eps, attn_scale;
+  const void* const* wqkv; /* host arrays of n_layers device pointers */
+  const void* const* wo;
+  const void* const* wgu;
+  const void* const* wdown;
+  const void* embed;   /* [V, d] */
+  const void* lm_head; /* [V, d] */
+  const int32_t* tokens; const int32_t* pos; const int32_t* slot; const int32_t* req; /* [M] */
+  const uint32_t* qmask; /* [M, mask_words] */
+  const int32_t* blk_start; const int32_t* blk_len; /* [B] */
+  const float* rope_cs;  /* [positions, hd/2, 2] */
+  void* cache;           /* [layers][B][2][Hkv][S][hd] (kv=1 holds V^T) */
+  long long layer_stride;/* elements */
+  float* resid;          /* [M, d] f32 */
+  void* hb;              /* [M, d] bf16 (un-normalised residual = GEMM input) */
+  void* q;               /* [M, Hq*hd] bf16 */
+  void* attn;            /* [M, Hq*hd] bf16 */
+  void* mlp;             /* [M, ffn] bf16 */
+  float* logits;         /* [M, V] f32 */
+  float* ss;             /* [2][d/128][M] per-tile sums of squares */
+  float* ws;             /* two stream-K partial buffers, ws_bytes total */
+  float* attn_part;      /* attention chunk partials, attn_part_bytes */
+  int32_t num_ctas;      /* 0 = one per SM */
+  int32_t lookahead;     /* L2 prefetch depth in weight tiles per CTA (<0 = default) */
+  void* dbg;             /* optional u64 [grid][phases]: %globaltimer at each phase end (profiling) */
+} ygg_mk_desc;
+
+size_t ygg_mk_plan_size(void);
+/* Device table / workspace sizes for a descriptor (pointers may be NULL). */
+int ygg_mk_query(const ygg_mk_desc* desc, size_t* table_bytes, size_t* ws_bytes, size_t* attn_part_bytes);
+/* Builds the phase program + TMA maps into table_dev (device memory, >= table_bytes). */
+int ygg_mk_plan_init(void* plan, const ygg_mk_desc* desc, void* table_dev, size_t table_bytes);
+int ygg_mk_run(const void* plan, ygg_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -19,6 +19,12 @@ with RMSNorm gains folded into the next weights (model.prepare_fused_) and the p
 applied by the consuming GEMM's epilogue.  Same results; today slower, because the split-tile
 fixups sit on each GEMM's critical path.
 
+bf16 persistent (B*R <= 128; YGG_MK=1 or persistent=True): the whole pass is ONE launch of
+the persistent forward kernel (csrc/mk.cu) — one CTA per SM walking a static phase program with
+grid-wide arrival counters between phases while the weight stream (TMA ring + L2 prefetch
+look-ahead) runs ahead across them.  RMSNorm gains are folded into the next weight
+(model.prepare_folded_) and the per-row rstd is applied by the consuming epilogue phase.
+
 f32 (parity path): SIMT GEMM + the same separate epilogue kernels + SIMT attention.  The
 residual stream is f32 in every path.
 """
@@ -32,7 +38,7 @@ import os
 import torch
 
 from . import _lib as L
-from .model import ModelConfig, prepare_fused_, rope_table
+from .model import ModelConfig, prepare_folded_, prepare_fused_, rope_table
 
 
 class GemmPlan:
@@ -94,6 +100,7 @@ class Forward:
         act_dtype: torch.dtype,
         logits: bool = True,
         num_ctas: int = 0,
+        persistent: bool | None = None,
     ):
         L.require_device()
         self.cfg, self.cache = cfg, cache
@@ -104,8 +111,14 @@ class Forward:
         # bf16 default: plain stream-K GEMM + separate vectorised epilogue kernels (faster today);
         # YGG_FUSED=1 selects the fused-epilogue GEMMs (same results, tested).
         self.fused = act_dtype == torch.bfloat16 and bool(os.environ.get("YGG_FUSED"))
+        if persistent is None:
+            persistent = os.environ.get("YGG_MK", "0") != "0"
+        self.mk = (persistent and act_dtype == torch.bfloat16 and not self.fused and logits and B * R <= 128
+                   and mask_words <= L.MAX_MASK_WORDS)
         if self.fused:
             prepare_fused_(weights, cfg)
+        elif self.mk:
+            prepare_folded_(weights, cfg)
         self.w = weights
         dev = cache.device
         M, d = self.M, cfg.d_model
@@ -152,6 +165,58 @@ class Forward:
         self.rope_cs = rope_table(cfg, self.S + 64, dev)
         if self.fused:
             self._setup_fused()
+        if self.mk:
+            self._setup_mk()
+
+    # ------------------------------------------------------------------
+    def _setup_mk(self) -> None:
+        """Descriptor + device phase table of the persistent forward (csrc/mk.cu)."""
+        lib, cfg, M = L.lib(), self.cfg, self.M
+        dev = self.cache.device
+        lw = self.w["layers"]
+        n = cfg.n_layers
+        self._mk_ptrs = [(C.c_void_p * n)(*[x[k].data_ptr() for x in lw]) for k in ("wqkv", "wo", "wgu", "wdown")]
+        self.ss = torch.zeros(2, cfg.d_model // 128, M, dtype=torch.float32, device=dev)
+        d = L.YggMkDesc()
+        d.n_layers, d.d_model, d.n_heads, d.n_kv_heads = n, cfg.d_model, cfg.n_heads, cfg.n_kv_heads
+        d.head_dim, d.ffn, d.vocab = cfg.head_dim, cfg.ffn, cfg.vocab
+        d.B, d.T, d.S, d.mask_words = self.B, self.R, self.S, self.mask_words
+        d.eps, d.attn_scale = float(cfg.norm_eps), float(self.scale)
+        d.wqkv, d.wo, d.wgu, d.wdown = [C.cast(p, C.POINTER(C.c_void_p)) for p in self._mk_ptrs]
+        d.embed, d.lm_head = self.w["embed"].data_ptr(), self.w["lm_head"].data_ptr()
+        d.tokens, d.pos, d.slot, d.req = (t.data_ptr() for t in (self.tokens, self.pos, self.slot, self.req))
+        d.qmask = self.qmask.data_ptr() if self.mask_words > 0 else None
+        d.blk_start, d.blk_len = self.blk_start.data_ptr(), self.blk_len.data_ptr()
+        d.rope_cs, d.cache, d.layer_stride = self.rope_cs.data_ptr(), self.cache.data_ptr(), self.layer_stride
+        d.resid, d.hb, d.q, d.attn = (t.data_ptr() for t in (self.resid, self.xn, self.q, self.attn))
+        d.mlp, d.logits, d.ss = self.mlp.data_ptr(), self.logits.data_ptr(), self.ss.data_ptr()
+        d.num_ctas, d.lookahead = 0, -1
+        tb, wb, pb = C.c_size_t(), C.c_size_t(), C.c_size_t()
+        L.check(lib.ygg_mk_query(C.byref(d), C.byref(tb), C.byref(wb), C.byref(pb)))
+        self.mk_table = torch.zeros(tb.value, dtype=torch.uint8, device=dev)
+        self.mk_ws = torch.empty(wb.value // 4 + 4, dtype=torch.float32, device=dev)
+        self.mk_part = torch.empty(pb.value // 4 + 4, dtype=torch.float32, device=dev)
+        d.ws, d.attn_part = self.mk_ws.data_ptr(), self.mk_part.data_ptr()
+        self._mk_desc = d
+        self._mk_plan = C.create_string_buffer(int(lib.ygg_mk_plan_size()))
+        L.check(lib.ygg_mk_plan_init(self._mk_plan, C.byref(d), self.mk_table.data_ptr(), tb.value))
+
+    def mk_phase_stamps(self, on: bool) -> torch.Tensor | None:
+        """Profiling only: re-plan with (or without) per-CTA %globaltimer stamps at every phase end.
+        Returns the u64 [grid, phases] stamp buffer (int64 view) or None."""
+        if not self.mk:
+            raise ValueError("not a persistent forward")
+        lib = L.lib()
+        buf = None
+        if on:
+            g = torch.cuda.get_device_properties(self.cache.device).multi_processor_count
+            nph = 1 + 10 * self.cfg.n_layers + 2
+            buf = torch.zeros(g, nph, dtype=torch.int64, device=self.cache.device)
+        self._mk_desc.dbg = buf.data_ptr() if buf is not None else None
+        self._mk_stamps = buf
+        L.check(lib.ygg_mk_plan_init(self._mk_plan, C.byref(self._mk_desc), self.mk_table.data_ptr(),
+                                     self.mk_table.numel()))
+        return buf
 
     # ------------------------------------------------------------------
     def _setup_fused(self) -> None:
@@ -228,7 +293,9 @@ class Forward:
             L.check(lib.ygg_gemm_run(plan.handle, self.ws.data_ptr(), stream_ptr))
 
     def run(self, stream: torch.cuda.Stream | None = None) -> None:
-        if self.fused:
+        if self.mk:
+            L.check(L.lib().ygg_mk_run(self._mk_plan, L.stream_ptr(stream)))
+        elif self.fused:
             self._run_fused(stream)
         else:
             self._run_unfused(stream)

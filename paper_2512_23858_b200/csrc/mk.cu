@@ -38,12 +38,14 @@ constexpr int kKC = 64;       // attention keys per unit
 constexpr int kQRows = 128;   // attention query rows per unit (UMMA M)
 constexpr int kMaxRows = 128; // M = B*T
 constexpr int kMaxStages = 16;
-constexpr int kMaxSegTable = 1032;  // tiles + 1 of the widest GEMM (vocab <= 132096)
+constexpr int kMaxSegTable = 1032;
+constexpr int kMaxPend = 64;  // tiles one CTA touches in one GEMM phase  // tiles + 1 of the widest GEMM (vocab <= 132096)
 constexpr int kSmemLimit = 227 * 1024;
 constexpr uint32_t kMagic = 0x59474d4bu;  // "YGMK"
 
-enum Kind : int { kEmbed = 0, kGemm = 1, kEpiQkv = 2, kAttn = 3, kCombine = 4, kEpiResid = 5, kEpiSwiglu = 6,
-                  kEpiStore = 7 };
+enum Kind : int { kEmbed = 0, kGemm = 1, kAttn = 3, kCombine = 4 };
+// Epilogue fused into a GEMM phase, applied by the last CTA to finish each tile group ("fixup").
+enum Epi : int { kEpiNone = 0, kEpiQkv = 1, kEpiResid = 2, kEpiSwiglu = 3, kEpiStore = 4 };
 
 struct Phase {
   int kind, layer;
@@ -54,7 +56,13 @@ struct Phase {
   int ws;               // partial buffer (0/1)
   int ss_in, ss_out;    // sums-of-squares buffers (-1 = none)
   int kmap, vmap;       // attention: this layer's K / V^T maps
-  int pad;
+  int epi;              // GEMM: fused epilogue (Epi)
+  int ctr;              // GEMM: offset of this phase's tile-group arrival counters (partials published)
+  int dctr;             // GEMM: offset of this phase's tile-group done counters (fixup slices finished)
+  int ptot;             // GEMM: index of this phase's total done counter
+  int nsegs;            // GEMM: total segments (= fixup participants summed over groups)
+  int src;              // GEMM: phase that produced X (-1: gate on the grid counter instead)
+  int ss_src;           // GEMM: RESID phase that produced ss_in (-1: the embed phase)
   long long cache_off;  // element offset of this layer's cache block
 };
 
@@ -70,7 +78,12 @@ struct Args {
   const CUtensorMap* maps;
   const int32_t* itab;
   unsigned int* bar;
+  unsigned int* ctr;  // tile-group arrival counters (monotonic; a group completes every `target` arrivals)
+  unsigned int* dctr; // tile-group done counters (monotonic, +1 per participant slice per launch)
+  unsigned int* ptot; // per-phase done totals
+  unsigned int* lctr; // launch index of this plan (incremented by the last CTA of each launch)
   int nphases, G, M, BN, stages, look, pf_maps, bank_n;
+  int attn_bytes;  // size of the attention operand region (0 in the YGG_MK_NOATTN A/B mode)
   int xflags;  // A/B only (YGG_MK_XFLAGS): 1 = skip activation loads, 2 = skip MMAs, 4 = skip partial stores
   int d, Hq, Hkv, hd, S, T, B, F, V;
   int Gh, tok_per_tile, q_tiles, chunks, mask_words, qmap;
@@ -168,10 +181,8 @@ YGG_DEV void cons_sync() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
 // CTAs costs one L2 round trip, not one per segment.
 constexpr int kSegBatch = 8;
 template <int V>
-YGG_DEV void part_sum(const float* __restrict__ wsb, const int* seg_s, int BN, int m, int n, float* v) {
-  const int t = n >> 7;
-  const int s0 = seg_s[t], s1 = seg_s[t + 1];
-  const float* p = wsb + static_cast<size_t>(m) * kBM + (n & (kBM - 1));
+YGG_DEV void part_range(const float* __restrict__ wsb, int BN, int s0, int s1, int m, int nl, float* v) {
+  const float* p = wsb + static_cast<size_t>(m) * kBM + nl;
   const size_t seg_stride = static_cast<size_t>(BN) * kBM;
 #pragma unroll
   for (int i = 0; i < V; ++i) v[i] = 0.f;
@@ -205,10 +216,13 @@ YGG_DEV void store_bf16x8(__nv_bfloat16* dst, const float* v) {
 }
 
 // rstd of every row from the [d/128][M] sums of squares, into shared memory.
-YGG_DEV void load_rstd(const Args& a, int ss_buf, float* rstd_s, int et) {
+YGG_DEV void load_rstd(const Args& a, int ss_buf, float* rstd_s, int* pos_s, int* slot_s, int* req_s, int et) {
   const int nt = a.d / kBM;
   const float* ss = a.ss + static_cast<size_t>(ss_buf) * nt * a.M;
   for (int m = et; m < a.M; m += 128) {
+    pos_s[m] = __ldg(a.pos + m);
+    slot_s[m] = __ldg(a.slot + m);
+    req_s[m] = __ldg(a.req + m);
     float s = 0.f;
     for (int t = 0; t < nt; ++t) s += __ldcg(ss + static_cast<size_t>(t) * a.M + m);
     rstd_s[m] = rsqrtf(s / static_cast<float>(a.d) + a.eps);
@@ -246,7 +260,11 @@ struct Smem {
   uint64_t *full, *empty, *tfull, *tempty, *abar;
   uint32_t* tmem_slot;
   float* rstd_s;  // [kMaxRows]
-  int* seg_s;     // [kMaxSegTable] seg_first of the GEMM being reduced
+  int* pos_s;     // [kMaxRows]
+  int* slot_s;    // [kMaxRows]
+  int* req_s;     // [kMaxRows]
+  int* seg_s;     // [kMaxSegTable] (unused scratch)
+  int* flag;      // [kMaxPend][4] deferred fixups (group, participant, parts, counter target)
 };
 
 // Producer: three cursors over this CTA's GEMM units of every phase, all in registers (local-memory
@@ -307,14 +325,59 @@ YGG_DEV void producer(const Args& a, const MapBank& bank, const Smem& sm) {
   unsigned seen = 0;
   unsigned xdep = static_cast<unsigned>(x.p) * G;  // phase x.p - 1 complete everywhere
   bool waited = false;
-  // Issue X loads (oldest first) while their producing phase is complete; block only if asked.
+  unsigned L1 = 0;  // launch index + 1 (read after the grid dependency)
+  // X gating source of the X cursor's phase: a GEMM's tile groups (dataflow) or the grid counter.
+  int xsrc = -1, xsrc_p = -2;
+  const unsigned* src_tot = nullptr;
+  unsigned src_tgt = 0;
+  uint64_t sat0 = 0, sat1 = 0, sat2 = 0, sat3 = 0;  // source tiles already seen final (<= 256)
+  auto sat_get = [&](int f) -> bool {
+    const uint64_t w = f < 64 ? sat0 : (f < 128 ? sat1 : (f < 192 ? sat2 : sat3));
+    return (w >> (f & 63)) & 1ull;
+  };
+  auto sat_set = [&](int f) {
+    const uint64_t b = 1ull << (f & 63);
+    if (f < 64) sat0 |= b;
+    else if (f < 128) sat1 |= b;
+    else if (f < 192) sat2 |= b;
+    else sat3 |= b;
+  };
+  auto x_source = [&]() {
+    if (x.p == xsrc_p) return;
+    xsrc_p = x.p;
+    const Phase* P = a.phases + x.p;
+    xsrc = P->src;
+    sat0 = sat1 = sat2 = sat3 = 0;
+    if (xsrc >= 0) {
+      const Phase* Q = a.phases + xsrc;
+      src_tot = a.ptot + Q->ptot;
+      src_tgt = L1 * static_cast<unsigned>(Q->nsegs);
+    }
+  };
+  // Issue X loads (oldest first) once their source is final; block only if asked.
   auto flush = [&](bool block) {
     while (npend > 0) {
-      if (seen < xdep) {
-        if (!waited) {
-          pdl_wait();
-          waited = true;
+      if (!waited) {
+        pdl_wait();
+        waited = true;
+        L1 = ld_rlx(a.lctr) + 1u;
+      }
+      x_source();
+      if (xsrc >= 0) {
+        // Source GEMM's fixups all done (one counter); per-tile gating costs a load per source tile
+        // on the issue path, which the single producer thread cannot afford.
+        if (!sat0) {
+          if (ld_rlx(src_tot) < src_tgt) {
+            if (!block) return;
+            const long long t0 = clock64();
+            while (ld_rlx(src_tot) < src_tgt)
+              if (clock64() - t0 > (1ll << 32)) __trap();
+          }
+          fence_acq_gpu();
+          fence_async_global();
+          sat0 = 1;
         }
+      } else if (seen < xdep) {
         seen = ld_rlx(a.bar);
         if (seen < xdep) {
           if (!block) return;
@@ -337,6 +400,11 @@ YGG_DEV void producer(const Args& a, const MapBank& bank, const Smem& sm) {
   int cur_p = -1;
   while (w_ok) {
     if (w.p != cur_p) {
+      if (a.dbg && cur_p >= 0) {
+        unsigned long long tt;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tt));
+        a.dbg[(2ull * G + c) * a.nphases + cur_p] = tt;  // W stream of phase cur_p fully issued
+      }
       cur_p = w.p;
       if (a.pf_maps) {
         tma_prefetch_desc(w.wm);
@@ -421,7 +489,7 @@ YGG_DEV void mma_role(const Args& a, const MapBank& bank, const Smem& sm, uint32
         accph ^= 1u << acc;
         acc ^= 1;
       }
-    } else if (kind == kAttn) {
+    } else if (kind == kAttn && !(a.xflags & 8)) {
       const int kmap = a.phases[p].kmap, vmap = a.phases[p].vmap;
       if (!waited) {
         pdl_wait();
@@ -498,6 +566,212 @@ YGG_DEV uint32_t vis_word(int kw, int bs, int bl, int tq, bool row_valid, int ma
   return pre | blk;
 }
 
+// Partial sums of K items at once (rows m[k], tile-local features nl[k]..+8), segments in order;
+// SB segments' loads for all K items are in flight together (one L2 round trip per SB segments).
+template <int K, int SB>
+YGG_DEV void sumk(const float* __restrict__ wsb, int BN, int s0, int s1, const int* m, const int* nl, float (*v)[8]) {
+  const size_t seg_stride = static_cast<size_t>(BN) * kBM;
+  const float* p[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    p[k] = wsb + static_cast<size_t>(m[k]) * kBM + nl[k];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) v[k][j] = 0.f;
+  }
+  for (int s = s0; s < s1; s += SB) {
+    float4 x[SB][K][2];
+#pragma unroll
+    for (int b = 0; b < SB; ++b) {
+      const bool ok = s + b < s1;
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        const float4* q = reinterpret_cast<const float4*>(p[k] + (s + b) * seg_stride);
+        x[b][k][0] = ok ? __ldcg(q) : make_float4(0.f, 0.f, 0.f, 0.f);
+        x[b][k][1] = ok ? __ldcg(q + 1) : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+    }
+#pragma unroll
+    for (int b = 0; b < SB; ++b)
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        v[k][0] += x[b][k][0].x; v[k][1] += x[b][k][0].y; v[k][2] += x[b][k][0].z; v[k][3] += x[b][k][0].w;
+        v[k][4] += x[b][k][1].x; v[k][5] += x[b][k][1].y; v[k][6] += x[b][k][1].z; v[k][7] += x[b][k][1].w;
+      }
+  }
+}
+
+// Gate (segments [s0,s1)) and up ([q0,q1)) partial sums of K items, both ranges' loads in flight together.
+template <int K, int SB>
+YGG_DEV void sum_gu(const float* __restrict__ wsb, int BN, int s0, int s1, int q0, int q1, const int* m, const int* nl,
+                    float (*v)[8], float (*u)[8]) {
+  const size_t seg_stride = static_cast<size_t>(BN) * kBM;
+  const float* p[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    p[k] = wsb + static_cast<size_t>(m[k]) * kBM + nl[k];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) v[k][j] = u[k][j] = 0.f;
+  }
+  const int ns = s1 - s0, nq = q1 - q0, n = ns > nq ? ns : nq;
+  const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int b0 = 0; b0 < n; b0 += SB) {
+    float4 x[SB][K][4];
+#pragma unroll
+    for (int b = 0; b < SB; ++b) {
+      const bool okg = b0 + b < ns, oku = b0 + b < nq;
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        const float4* qg = reinterpret_cast<const float4*>(p[k] + (s0 + b0 + b) * seg_stride);
+        const float4* qu = reinterpret_cast<const float4*>(p[k] + (q0 + b0 + b) * seg_stride);
+        x[b][k][0] = okg ? __ldcg(qg) : z;
+        x[b][k][1] = okg ? __ldcg(qg + 1) : z;
+        x[b][k][2] = oku ? __ldcg(qu) : z;
+        x[b][k][3] = oku ? __ldcg(qu + 1) : z;
+      }
+    }
+#pragma unroll
+    for (int b = 0; b < SB; ++b)
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        v[k][0] += x[b][k][0].x; v[k][1] += x[b][k][0].y; v[k][2] += x[b][k][0].z; v[k][3] += x[b][k][0].w;
+        v[k][4] += x[b][k][1].x; v[k][5] += x[b][k][1].y; v[k][6] += x[b][k][1].z; v[k][7] += x[b][k][1].w;
+        u[k][0] += x[b][k][2].x; u[k][1] += x[b][k][2].y; u[k][2] += x[b][k][2].z; u[k][3] += x[b][k][2].w;
+        u[k][4] += x[b][k][3].x; u[k][5] += x[b][k][3].y; u[k][6] += x[b][k][3].z; u[k][7] += x[b][k][3].w;
+      }
+  }
+}
+
+// Fused epilogue of rows [row0, row1) of one tile group (this participant's slice).  Thread item =
+// (row m, 8 consecutive features); the 16 items of a row sit in 16 consecutive lanes, so RoPE pairs
+// (feature f, f +- hd/2: same head, same tile) are one shuffle apart and the per-tile sum of squares
+// is a 16-lane reduction.  Two items per thread per pass; partials summed in segment order.
+template <int EPI, int IP, int SB>
+YGG_DEV void fixup(const Args& a, const Smem& sm, int t, const float* wsb, int s0, int s1, int q0, int q1, int ss_out,
+                   long long cache_off, int et, int row0, int row1) {
+  const int M = a.M, BN = a.BN, lane = threadIdx.x & 31;
+  const int items = (row1 - row0) * 16;
+  for (int i0 = 0; i0 < items; i0 += 128 * IP) {
+    int mm[4], nl[4];
+    bool live[4];
+#pragma unroll
+    for (int k = 0; k < IP; ++k) {
+      const int i = i0 + k * 128 + et;
+      live[k] = i < items;
+      mm[k] = live[k] ? row0 + (i >> 4) : row0;
+      nl[k] = (i & 15) * 8;
+    }
+    float v[4][8];
+    float2 cs[4][8];
+    if (EPI == kEpiQkv) {
+      const int half = a.hd / 2;
+#pragma unroll
+      for (int k = 0; k < IP; ++k) {
+        const int n = t * kBM + nl[k];
+        const int idx0 = n % a.hd;
+        const bool rope = n / a.hd < a.Hq + a.Hkv;
+        const float2* cp = a.rope_cs + static_cast<size_t>(sm.pos_s[mm[k]]) * half + (idx0 % half);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) cs[k][j] = rope ? __ldg(cp + j) : make_float2(1.f, 0.f);
+      }
+    }
+    float4 rx[4][2];
+    if (EPI == kEpiResid) {
+#pragma unroll
+      for (int k = 0; k < IP; ++k) {
+        const float4* rp = reinterpret_cast<const float4*>(a.resid + static_cast<size_t>(mm[k]) * a.d + t * kBM + nl[k]);
+        rx[k][0] = __ldcg(rp);
+        rx[k][1] = __ldcg(rp + 1);
+      }
+    }
+    float u[4][8];
+    if (EPI == kEpiSwiglu) sum_gu<IP, SB>(wsb, BN, s0, s1, q0, q1, mm, nl, v, u);
+    else sumk<IP, SB>(wsb, BN, s0, s1, mm, nl, v);
+#pragma unroll
+    for (int k = 0; k < IP; ++k) {
+      const int m = mm[k];
+      const int n = t * kBM + nl[k];
+      if (EPI == kEpiQkv) {
+        const float r = sm.rstd_s[m];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) v[k][j] *= r;
+        const int hd = a.hd, half = hd / 2;
+        const int head = n / hd, idx0 = n % hd;
+        float o[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) o[j] = __shfl_xor_sync(0xffffffffu, v[k][j], hd / 16);
+        const bool first = idx0 < half;
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          v[k][j] = first ? (v[k][j] * cs[k][j].x - o[j] * cs[k][j].y) : (v[k][j] * cs[k][j].x + o[j] * cs[k][j].y);
+        if (live[k]) {
+          if (head < a.Hq) {
+            store_bf16x8(a.q + (static_cast<size_t>(m) * a.Hq + head) * hd + idx0, v[k]);
+          } else {
+            const bool is_v = head >= a.Hq + a.Hkv;
+            const int kvh = is_v ? head - a.Hq - a.Hkv : head - a.Hq;
+            const int rq = sm.req_s[m], sl = sm.slot_s[m];
+            __nv_bfloat16* base = a.cache + cache_off +
+                                  ((static_cast<size_t>(rq) * 2 + (is_v ? 1 : 0)) * a.Hkv + kvh) * static_cast<size_t>(a.S) * hd;
+            if (!is_v) {
+              store_bf16x8(base + static_cast<size_t>(sl) * hd + idx0, v[k]);
+            } else {  // V^T [hd][S]
+#pragma unroll
+              for (int j = 0; j < 8; ++j) base[static_cast<size_t>(idx0 + j) * a.S + sl] = __float2bfloat16_rn(v[k][j]);
+            }
+          }
+        }
+      } else if (EPI == kEpiResid) {
+        float sq = 0.f;
+        v[k][0] += rx[k][0].x; v[k][1] += rx[k][0].y; v[k][2] += rx[k][0].z; v[k][3] += rx[k][0].w;
+        v[k][4] += rx[k][1].x; v[k][5] += rx[k][1].y; v[k][6] += rx[k][1].z; v[k][7] += rx[k][1].w;
+        if (live[k]) {
+          float4* rp = reinterpret_cast<float4*>(a.resid + static_cast<size_t>(m) * a.d + n);
+          __stcg(rp, make_float4(v[k][0], v[k][1], v[k][2], v[k][3]));
+          __stcg(rp + 1, make_float4(v[k][4], v[k][5], v[k][6], v[k][7]));
+          store_bf16x8(a.hb + static_cast<size_t>(m) * a.d + n, v[k]);
+#pragma unroll
+          for (int j = 0; j < 8; ++j) sq += v[k][j] * v[k][j];
+        }
+#pragma unroll
+        for (int o = 8; o > 0; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
+        if (live[k] && (lane & 15) == 0)
+          __stcg(a.ss + (static_cast<size_t>(ss_out) * (a.d / kBM) + t) * M + m, sq);
+      } else if (EPI == kEpiSwiglu) {
+        const float r = sm.rstd_s[m];
+        float o[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const float g = v[k][j] * r;
+          o[j] = __fdividef(g, 1.f + __expf(-g)) * (u[k][j] * r);
+        }
+        if (live[k]) store_bf16x8(a.mlp + static_cast<size_t>(m) * a.F + n, o);
+      } else if (EPI == kEpiStore) {
+        if (live[k]) {
+          const float r = sm.rstd_s[m];
+          float4* dst = reinterpret_cast<float4*>(a.logits + static_cast<size_t>(m) * a.V + n);
+          __stcg(dst, make_float4(v[k][0] * r, v[k][1] * r, v[k][2] * r, v[k][3] * r));
+          __stcg(dst + 1, make_float4(v[k][4] * r, v[k][5] * r, v[k][6] * r, v[k][7] * r));
+        }
+      }
+    }
+  }
+}
+
+YGG_DEV void fixup_any(int epi, const Args& a, const Smem& sm, int t, const float* wsb, const int* pe, int ss_out,
+                       long long cache_off, int et, int row0, int row1) {
+  const int s0 = pe[4], s1 = pe[5], q0 = pe[6], q1 = pe[7];
+  // Few items: one item per thread with every segment in flight; many: two items, 8-segment batches.
+  const bool few = (row1 - row0) * 16 <= 128;
+#define YGG_FX(E, I, B) fixup<E, I, B>(a, sm, t, wsb, s0, s1, q0, q1, ss_out, cache_off, et, row0, row1)
+  switch (epi) {
+    case kEpiQkv: if (few) YGG_FX(kEpiQkv, 1, 16); else YGG_FX(kEpiQkv, 2, 8); break;
+    case kEpiResid: if (few) YGG_FX(kEpiResid, 1, 16); else YGG_FX(kEpiResid, 2, 8); break;
+    case kEpiSwiglu: if (few) YGG_FX(kEpiSwiglu, 1, 8); else YGG_FX(kEpiSwiglu, 2, 4); break;
+    default: if (few) YGG_FX(kEpiStore, 1, 16); else YGG_FX(kEpiStore, 2, 8); break;
+  }
+#undef YGG_FX
+}
+
 YGG_DEV void consumer(const Args& a, const Smem& sm, uint32_t tmem) {
   const int c = blockIdx.x, G = a.G, M = a.M, BN = a.BN;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -511,32 +785,69 @@ YGG_DEV void consumer(const Args& a, const Smem& sm, uint32_t tmem) {
   uint32_t accph = 0u;
   int an = 0;
   pdl_wait();
+  const unsigned L1 = ld_rlx(a.lctr) + 1u;  // launch index + 1: targets of the monotonic done counters
   for (int p = 0; p < a.nphases; ++p) {
     const Phase* PP = a.phases + p;
     const int kind = PP->kind;
-    const int kb = PP->kb, units = PP->units, ss_in = PP->ss_in, ss_out = PP->ss_out;
-    const long long cache_off = PP->cache_off;
-    float* wsb = a.ws + PP->ws * a.ws_stride;
     if (kind != kGemm && p > 0) {
       if (et == 0) wait_count(a.bar, static_cast<unsigned>(p) * G);
-      if (kind == kEpiQkv || kind == kEpiResid || kind == kEpiSwiglu || kind == kEpiStore) {
-        const int ntab = PP->N / kBM + 1;
-        const int* src = a.itab + PP->seg_first;
-        for (int i = et; i < ntab; i += 128) sm.seg_s[i] = __ldg(src + i);
-      }
       cons_sync();
     }
     if (kind == kGemm) {
+      const int kb = PP->kb, units = PP->units, epi = PP->epi, ss_in = PP->ss_in, ss_out = PP->ss_out;
+      const long long cache_off = PP->cache_off;
+      const int* sf = a.itab + PP->seg_first;
+      unsigned* ctr = a.ctr + PP->ctr;
+      float* wsb = a.ws + PP->ws * a.ws_stride;
+      const int half_t = a.F / kBM;
+      bool have_rstd = false;
+      const int ss_src = PP->ss_src;
+      auto need_rstd = [&]() {
+        if (!have_rstd && ss_in >= 0) {
+          // ss_in is complete once every fixup slice of the producing RESID phase is done (or the
+          // embed phase, for the first layer); X tiles alone do not imply it under dataflow gating.
+          if (et == 0) {
+            if (ss_src >= 0) {
+              const Phase* Q = a.phases + ss_src;
+              wait_count(a.ptot + Q->ptot, L1 * static_cast<unsigned>(Q->nsegs));
+            } else {
+              wait_count(a.bar, static_cast<unsigned>(G));
+            }
+          }
+          cons_sync();
+          load_rstd(a, ss_in, sm.rstd_s, sm.pos_s, sm.slot_s, sm.req_s, et);
+          have_rstd = true;
+        }
+      };
       const int u0 = static_cast<int>(static_cast<long long>(units) * c / G);
       const int u1 = static_cast<int>(static_cast<long long>(units) * (c + 1) / G);
       if (u1 > u0) {
         const int t0 = u0 / kb, t1 = (u1 - 1) / kb;
         const int sbase = __ldg(a.itab + PP->seg_base + c);
+        int npend_ = 0;
         for (int t = t0; t <= t1; ++t) {
           const int seg = sbase + (t - t0);
+          const int nseg = __ldg(sf + t + 1) - __ldg(sf + t);
           mbar_wait(&sm.tfull[acc], (accph >> acc) & 1u);
           tc_fence_after();
           const uint32_t taddr = tmem + lane_base + static_cast<uint32_t>(acc * BN);
+          if (epi == kEpiStore && nseg == 1) {
+            // Whole tile on this CTA: logits straight from TMEM (thread = vocabulary row).
+            need_rstd();
+            float* dst = a.logits + static_cast<size_t>(t) * kBM + row;
+            for (int c0 = 0; c0 < BN; c0 += 16) {
+              float v[16];
+              tmem_ld16(taddr + c0, v);
+#pragma unroll
+              for (int j = 0; j < 16; ++j)
+                if (c0 + j < M) __stcg(dst + static_cast<size_t>(c0 + j) * a.V, v[j] * sm.rstd_s[c0 + j]);
+            }
+            tc_fence_before();
+            mbar_arrive(&sm.tempty[acc]);
+            accph ^= 1u << acc;
+            acc ^= 1;
+            continue;
+          }
           float* dst = wsb + static_cast<size_t>(seg) * BN * kBM + row;
           for (int c0 = 0; c0 < BN; c0 += 16) {
             float v[16];
@@ -550,12 +861,80 @@ YGG_DEV void consumer(const Args& a, const Smem& sm, uint32_t tmem) {
           mbar_arrive(&sm.tempty[acc]);
           accph ^= 1u << acc;
           acc ^= 1;
+          if (a.dbg && et == 0 && t == t1) {
+            unsigned long long tt;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tt));
+            a.dbg[(static_cast<size_t>(G) + c) * a.nphases + p] = tt;  // last partial drained from TMEM
+          }
+          if (epi == kEpiNone) continue;
+          // Record the tile group this partial belongs to; arrivals are published in one batch below.
+          if (et == 0) {
+            int g = t, j = seg - __ldg(sf + t), nparts = nseg;
+            if (epi == kEpiSwiglu) {
+              g = t % half_t;
+              const int ng = __ldg(sf + g + 1) - __ldg(sf + g);
+              const int nu = __ldg(sf + g + half_t + 1) - __ldg(sf + g + half_t);
+              nparts = ng + nu;
+              if (t >= half_t) j += ng;
+            }
+            int* pe = sm.flag + 8 * npend_;
+            pe[0] = g;
+            pe[1] = j;
+            pe[2] = nparts;
+            pe[4] = __ldg(sf + g);
+            pe[5] = __ldg(sf + g + 1);
+            pe[6] = (epi == kEpiSwiglu) ? __ldg(sf + g + half_t) : 0;
+            pe[7] = (epi == kEpiSwiglu) ? __ldg(sf + g + half_t + 1) : 0;
+          }
+          ++npend_;
+          if (t == t0) need_rstd();  // rstd / positions (inputs of earlier phases) while partials drain
+        }
+        if (npend_ > 0) {
+          // Publish every partial of this range (one release per group, in parallel), then wait for
+          // each group's other participants; every participant finishes a row slice of the group.
+          cons_sync();
+          if (et < npend_) {
+            int* pe = sm.flag + 8 * et;
+            fence_acq_gpu();
+            unsigned old;
+            asm volatile("atom.relaxed.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(ctr + pe[0]) : "memory");
+            const unsigned np = static_cast<unsigned>(pe[2]);
+            wait_count(ctr + pe[0], (old / np + 1u) * np);
+          }
+          cons_sync();
+          if (a.dbg && et == 0) {
+            unsigned long long tt;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tt));
+            a.dbg[(3ull * G + c) * a.nphases + p] = tt;  // all of this CTA's tile groups complete
+          }
+          long long fx0 = clock64();
+          int fx_items = 0;
+          for (int i = 0; i < npend_; ++i) {
+            const int* pe = sm.flag + 8 * i;
+            const int g = pe[0], j = pe[1], nparts = pe[2];
+            const int r0 = static_cast<int>(static_cast<long long>(M) * j / nparts);
+            const int r1 = static_cast<int>(static_cast<long long>(M) * (j + 1) / nparts);
+            if (r1 > r0) fixup_any(epi, a, sm, g, wsb, pe, ss_out, cache_off, et, r0, r1);
+            fx_items += (r1 - r0) * 16;
+          }
+          // Publish the finished slices: per-group done counters gate the next GEMM's X tiles.
+          fence_async_global();
+          cons_sync();
+          if (et < npend_) {
+            const int* pe = sm.flag + 8 * et;
+            red_rel_add(a.dctr + PP->dctr + pe[0], 1u);
+            red_rel_add(a.ptot + PP->ptot, 1u);
+          }
+          if (a.dbg && et == 0) {
+            a.dbg[(6ull * G + c) * a.nphases + p] = static_cast<unsigned long long>(clock64() - fx0);
+            a.dbg[(7ull * G + c) * a.nphases + p] = static_cast<unsigned long long>(fx_items) * 1000ull + npend_;
+          }
         }
       }
-    } else if (kind == kEmbed || kind == kEpiResid) {
+    } else if (kind == kEmbed) {
       const int d8 = a.d / 8, items = M * d8;
       const int nt = a.d / kBM;
-      float* ss = a.ss + static_cast<size_t>(ss_out) * nt * M;
+      float* ss = a.ss + static_cast<size_t>(PP->ss_out) * nt * M;
       for (int i0 = c * 128; i0 < items; i0 += stride) {
         const int i = i0 + et;
         const bool live = i < items;
@@ -563,23 +942,14 @@ YGG_DEV void consumer(const Args& a, const Smem& sm, uint32_t tmem) {
         float h[8];
         float sq = 0.f;
         if (live) {
-          if (kind == kEmbed) {
-            const int tok = __ldg(a.tokens + m);
-            const uint4 u = __ldg(reinterpret_cast<const uint4*>(a.embed + static_cast<size_t>(tok) * a.d + n));
-            const uint32_t wv[4] = {u.x, u.y, u.z, u.w};
+          const int tok = __ldg(a.tokens + m);
+          const uint4 u = __ldg(reinterpret_cast<const uint4*>(a.embed + static_cast<size_t>(tok) * a.d + n));
+          const uint32_t wv[4] = {u.x, u.y, u.z, u.w};
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
-              const __nv_bfloat162 b = *reinterpret_cast<const __nv_bfloat162*>(&wv[k]);
-              h[2 * k] = __bfloat162float(b.x);
-              h[2 * k + 1] = __bfloat162float(b.y);
-            }
-          } else {
-            float v[8];
-            part_sum<8>(wsb, sm.seg_s, BN, m, n, v);
-            const float4* rp = reinterpret_cast<const float4*>(a.resid + static_cast<size_t>(m) * a.d + n);
-            const float4 x = __ldcg(rp), y = __ldcg(rp + 1);
-            h[0] = x.x + v[0]; h[1] = x.y + v[1]; h[2] = x.z + v[2]; h[3] = x.w + v[3];
-            h[4] = y.x + v[4]; h[5] = y.y + v[5]; h[6] = y.z + v[6]; h[7] = y.w + v[7];
+          for (int k = 0; k < 4; ++k) {
+            const __nv_bfloat162 b = *reinterpret_cast<const __nv_bfloat162*>(&wv[k]);
+            h[2 * k] = __bfloat162float(b.x);
+            h[2 * k + 1] = __bfloat162float(b.y);
           }
           float4* wp = reinterpret_cast<float4*>(a.resid + static_cast<size_t>(m) * a.d + n);
           __stcg(wp, make_float4(h[0], h[1], h[2], h[3]));
@@ -588,101 +958,11 @@ YGG_DEV void consumer(const Args& a, const Smem& sm, uint32_t tmem) {
 #pragma unroll
           for (int k = 0; k < 8; ++k) sq += h[k] * h[k];
         }
-        // 16 lanes = one 128-feature tile of one row (d/8 is a multiple of 16): fixed-order tree.
 #pragma unroll
         for (int o = 8; o > 0; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
         if (live && (lane & 15) == 0) __stcg(ss + static_cast<size_t>(n / kBM) * M + m, sq);
       }
-    } else if (kind == kEpiQkv) {
-      load_rstd(a, ss_in, sm.rstd_s, et);
-      const int half = a.hd / 2, per_head = half / 4;
-      const int heads = a.Hq + 2 * a.Hkv;
-      const int per_row = heads * per_head, items = M * per_row;
-      for (int i = c * 128 + et; i < items; i += stride) {
-        const int m = i / per_row, it = i % per_row;
-        const int head = it / per_head, i0 = (it % per_head) * 4;
-        const int n0 = head * a.hd;
-        const float r = sm.rstd_s[m];
-        float x1[4], x2[4];
-        part_sum<4>(wsb, sm.seg_s, BN, m, n0 + i0, x1);
-        part_sum<4>(wsb, sm.seg_s, BN, m, n0 + i0 + half, x2);
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          x1[j] *= r;
-          x2[j] *= r;
-        }
-        const int pm = __ldg(a.pos + m);
-        if (head < a.Hq + a.Hkv) {
-#pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            const float2 cs = __ldg(a.rope_cs + static_cast<size_t>(pm) * half + i0 + j);
-            const float y1 = x1[j] * cs.x - x2[j] * cs.y;
-            const float y2 = x2[j] * cs.x + x1[j] * cs.y;
-            x1[j] = y1;
-            x2[j] = y2;
-          }
-        }
-        if (head < a.Hq) {
-          __nv_bfloat16* qd = a.q + (static_cast<size_t>(m) * a.Hq + head) * a.hd;
-          uint2 lo, hi;
-          lo.x = pack_bf16(x1[0], x1[1]);
-          lo.y = pack_bf16(x1[2], x1[3]);
-          hi.x = pack_bf16(x2[0], x2[1]);
-          hi.y = pack_bf16(x2[2], x2[3]);
-          *reinterpret_cast<uint2*>(qd + i0) = lo;
-          *reinterpret_cast<uint2*>(qd + i0 + half) = hi;
-        } else {
-          const bool is_v = head >= a.Hq + a.Hkv;
-          const int kvh = is_v ? head - a.Hq - a.Hkv : head - a.Hq;
-          const int rq = __ldg(a.req + m), sl = __ldg(a.slot + m);
-          __nv_bfloat16* base = a.cache + cache_off +
-                                ((static_cast<size_t>(rq) * 2 + (is_v ? 1 : 0)) * a.Hkv + kvh) * static_cast<size_t>(a.S) * a.hd;
-          if (!is_v) {
-            uint2 lo, hi;
-            lo.x = pack_bf16(x1[0], x1[1]);
-            lo.y = pack_bf16(x1[2], x1[3]);
-            hi.x = pack_bf16(x2[0], x2[1]);
-            hi.y = pack_bf16(x2[2], x2[3]);
-            *reinterpret_cast<uint2*>(base + static_cast<size_t>(sl) * a.hd + i0) = lo;
-            *reinterpret_cast<uint2*>(base + static_cast<size_t>(sl) * a.hd + i0 + half) = hi;
-          } else {  // V^T [hd][S]
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-              base[static_cast<size_t>(i0 + j) * a.S + sl] = __float2bfloat16_rn(x1[j]);
-              base[static_cast<size_t>(i0 + j + half) * a.S + sl] = __float2bfloat16_rn(x2[j]);
-            }
-          }
-        }
-      }
-    } else if (kind == kEpiSwiglu) {
-      load_rstd(a, ss_in, sm.rstd_s, et);
-      const int f8 = a.F / 8, items = M * f8;
-      for (int i = c * 128 + et; i < items; i += stride) {
-        const int m = i / f8, f = (i % f8) * 8;
-        const float r = sm.rstd_s[m];
-        float g[8], u[8], o[8];
-        part_sum<8>(wsb, sm.seg_s, BN, m, f, g);
-        part_sum<8>(wsb, sm.seg_s, BN, m, a.F + f, u);
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          const float gg = g[k] * r;
-          o[k] = gg / (1.f + __expf(-gg)) * (u[k] * r);
-        }
-        store_bf16x8(a.mlp + static_cast<size_t>(m) * a.F + f, o);
-      }
-    } else if (kind == kEpiStore) {
-      load_rstd(a, ss_in, sm.rstd_s, et);
-      const int v8 = a.V / 8, items = M * v8;
-      for (int i = c * 128 + et; i < items; i += stride) {
-        const int m = i / v8, n = (i % v8) * 8;
-        const float r = sm.rstd_s[m];
-        float v[8];
-        part_sum<8>(wsb, sm.seg_s, BN, m, n, v);
-        float4* dst = reinterpret_cast<float4*>(a.logits + static_cast<size_t>(m) * a.V + n);
-        dst[0] = make_float4(v[0] * r, v[1] * r, v[2] * r, v[3] * r);
-        dst[1] = make_float4(v[4] * r, v[5] * r, v[6] * r, v[7] * r);
-      }
-    } else if (kind == kAttn) {
+    } else if (kind == kAttn && !(a.xflags & 8)) {
       const int n_units = a.chunks * a.B * a.Hkv * a.q_tiles;
       const size_t rows_all = static_cast<size_t>(M) * a.Hq;
       for (int u = c; u < n_units; u += G) {
@@ -751,29 +1031,51 @@ YGG_DEV void consumer(const Args& a, const Smem& sm, uint32_t tmem) {
         ++an;
       }
     } else if (kind == kCombine) {
+      // Merge chunk partials in fixed chunk order; every chunk's loads of a batch are in flight at once.
       const int rows = M * a.Hq;
       const int nw = G * 4;
       const int DPL = a.hd / 32;  // 2 or 4
+      constexpr int CB = 8;
       for (int rr = c * 4 + (et >> 5); rr < rows; rr += nw) {
         const int r = (rr / a.Hq) / a.T;
         const int nch = (__ldg(a.blk_start + r) + __ldg(a.blk_len + r) + kKC - 1) / kKC;
         float Mx = -INFINITY;
-        for (int ch = 0; ch < nch; ++ch) Mx = fmaxf(Mx, __ldcg(a.ml + (static_cast<size_t>(ch) * rows + rr) * 2));
+        for (int c0 = 0; c0 < nch; c0 += CB) {
+          float mv[CB];
+#pragma unroll
+          for (int k = 0; k < CB; ++k)
+            mv[k] = (c0 + k < nch) ? __ldcg(a.ml + (static_cast<size_t>(c0 + k) * rows + rr) * 2) : -INFINITY;
+#pragma unroll
+          for (int k = 0; k < CB; ++k) Mx = fmaxf(Mx, mv[k]);
+        }
         float accv[4] = {0.f, 0.f, 0.f, 0.f};
         float L = 0.f;
         if (Mx != -INFINITY) {
-          for (int ch = 0; ch < nch; ++ch) {
-            const float2 mlv = __ldcg(reinterpret_cast<const float2*>(a.ml + (static_cast<size_t>(ch) * rows + rr) * 2));
-            if (mlv.x == -INFINITY) continue;
-            const float wgt = exp2f(mlv.x - Mx);
-            L += wgt * mlv.y;
-            const float* o = a.opart + (static_cast<size_t>(ch) * rows + rr) * a.hd + lane * DPL;
-            if (DPL == 4) {
-              const float4 x = __ldcg(reinterpret_cast<const float4*>(o));
-              accv[0] += wgt * x.x; accv[1] += wgt * x.y; accv[2] += wgt * x.z; accv[3] += wgt * x.w;
-            } else {
-              const float2 x = __ldcg(reinterpret_cast<const float2*>(o));
-              accv[0] += wgt * x.x; accv[1] += wgt * x.y;
+          for (int c0 = 0; c0 < nch; c0 += CB) {
+            float2 mlv[CB];
+            float4 ov[CB];
+#pragma unroll
+            for (int k = 0; k < CB; ++k) {
+              const bool ok = c0 + k < nch;
+              const size_t base = static_cast<size_t>(c0 + k) * rows + rr;
+              mlv[k] = ok ? __ldcg(reinterpret_cast<const float2*>(a.ml + base * 2)) : make_float2(-INFINITY, 0.f);
+              const float* o = a.opart + base * a.hd + lane * DPL;
+              if (!ok) ov[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+              else if (DPL == 4) ov[k] = __ldcg(reinterpret_cast<const float4*>(o));
+              else {
+                const float2 x = __ldcg(reinterpret_cast<const float2*>(o));
+                ov[k] = make_float4(x.x, x.y, 0.f, 0.f);
+              }
+            }
+#pragma unroll
+            for (int k = 0; k < CB; ++k) {
+              if (mlv[k].x == -INFINITY) continue;
+              const float wgt = exp2f(mlv[k].x - Mx);
+              L += wgt * mlv[k].y;
+              accv[0] += wgt * ov[k].x;
+              accv[1] += wgt * ov[k].y;
+              accv[2] += wgt * ov[k].z;
+              accv[3] += wgt * ov[k].w;
             }
           }
         }
@@ -790,8 +1092,18 @@ YGG_DEV void consumer(const Args& a, const Smem& sm, uint32_t tmem) {
       }
     }
     // Publish this CTA's writes of phase p (generic stores, read later by TMA or other SMs).
+    if (a.dbg && et == 0) {
+      unsigned long long tt;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tt));
+      a.dbg[(4ull * G + c) * a.nphases + p] = tt;  // work of phase p done
+    }
     fence_async_global();
     cons_sync();
+    if (a.dbg && et == 0) {
+      unsigned long long tt;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tt));
+      a.dbg[(5ull * G + c) * a.nphases + p] = tt;  // after the proxy fence + CTA barrier
+    }
     if (et == 0) {
       // Counter semantics: value >= (p+1)*G  <=>  every CTA finished phase p.  GEMM phases do not
       // wait for phase p-1 up front (their data dependency is carried by the TMA ring), so a CTA
@@ -804,7 +1116,10 @@ YGG_DEV void consumer(const Args& a, const Smem& sm, uint32_t tmem) {
       }
       if (p == a.nphases - 1) {
         const unsigned old = atom_acqrel_add(a.bar, 1u);
-        if (old == static_cast<unsigned>(a.nphases) * G - 1u) atomicExch(a.bar, 0u);  // last CTA: reset for the next launch
+        if (old == static_cast<unsigned>(a.nphases) * G - 1u) {  // last CTA: reset for the next launch
+          atomicExch(a.bar, 0u);
+          atomicAdd(a.lctr, 1u);
+        }
       } else {
         red_rel_add(a.bar, 1u);
       }
@@ -824,7 +1139,7 @@ __global__ void __launch_bounds__(kThreads, 1) mk_kernel(const __grid_constant__
   sm.sk = sm.sq + DCH * kQRows * 128;
   sm.svt = sm.sk + DCH * kKC * 128;
   sm.sp = sm.svt + a.hd * 128;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sm.sp + kQRows * 128);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sm.sq + a.attn_bytes);
   sm.full = bars;
   sm.empty = bars + S;
   sm.tfull = bars + 2 * S;
@@ -832,7 +1147,11 @@ __global__ void __launch_bounds__(kThreads, 1) mk_kernel(const __grid_constant__
   sm.abar = sm.tempty + 2;
   sm.tmem_slot = reinterpret_cast<uint32_t*>(sm.abar + 4);
   sm.rstd_s = reinterpret_cast<float*>(sm.tmem_slot + 4);
-  sm.seg_s = reinterpret_cast<int*>(sm.rstd_s + kMaxRows);
+  sm.pos_s = reinterpret_cast<int*>(sm.rstd_s + kMaxRows);
+  sm.slot_s = sm.pos_s + kMaxRows;
+  sm.req_s = sm.slot_s + kMaxRows;
+  sm.seg_s = sm.req_s + kMaxRows;
+  sm.flag = sm.seg_s + kMaxSegTable;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < S; ++s) {
@@ -914,7 +1233,7 @@ static int map2d(CUtensorMap* m, const void* p, long long rows, long long cols, 
 // Static geometry shared by query and init.
 struct Geo {
   int G, M, BN, stages, look;
-  int nphases, nmaps, itab_len;
+  int nphases, nmaps, itab_len, nctr;
   size_t ws_floats;  // per buffer
   size_t part_bytes;
   size_t table_bytes;
@@ -949,7 +1268,10 @@ static int check_desc(const ygg_mk_desc* d) {
   return YGG_OK;
 }
 
-static size_t attn_smem_bytes(int hd) { return (hd / 64) * kQRows * 128 + (hd / 64) * kKC * 128 + hd * 128 + kQRows * 128; }
+static size_t attn_smem_bytes(int hd) {
+  if (getenv("YGG_MK_NOATTN")) return 0;  // A/B only: attention phases become no-ops (wrong results)
+  return (hd / 64) * kQRows * 128 + (hd / 64) * kKC * 128 + hd * 128 + kQRows * 128;
+}
 
 static int geometry(const ygg_mk_desc* d, Geo* g) {
   if (int rc = check_desc(d)) return rc;
@@ -960,9 +1282,9 @@ static int geometry(const ygg_mk_desc* d, Geo* g) {
     const char* s = getenv("YGG_MK_LOOK");
     return s ? atoi(s) : -1;
   }();
-  g->look = d->lookahead >= 0 ? d->lookahead : (env_look >= 0 ? env_look : 16);
-  const size_t fixed = 1024 + attn_smem_bytes(d->head_dim) + (2 * kMaxStages + 8) * 8 + 16 + kMaxRows * 4 +
-                       kMaxSegTable * 4;
+  g->look = d->lookahead >= 0 ? d->lookahead : (env_look >= 0 ? env_look : 0);
+  const size_t fixed = 1024 + attn_smem_bytes(d->head_dim) + (2 * kMaxStages + 8) * 8 + 16 + kMaxRows * 16 +
+                       kMaxSegTable * 4 + kMaxPend * 32;
   const size_t stage = static_cast<size_t>(kBM) * kBK * 2 + static_cast<size_t>(g->BN) * kBK * 2;
   int st = static_cast<int>((kSmemLimit - fixed) / stage);
   g->stages = std::min(kMaxStages, st);
@@ -974,7 +1296,7 @@ static int geometry(const ygg_mk_desc* d, Geo* g) {
   g->q_tiles = (d->T + g->tok_per_tile - 1) / g->tok_per_tile;
   g->chunks = (d->S + kKC - 1) / kKC;
   const int L = d->n_layers;
-  g->nphases = 1 + 10 * L + 2;
+  g->nphases = 1 + 6 * L + 1;
   g->nmaps = 6 * L + 1 + 4;
   // Segments per GEMM: sum over CTAs of tiles touched, <= tiles + G.
   const int qkv = (d->n_heads + 2 * d->n_kv_heads) * d->head_dim;
@@ -987,10 +1309,13 @@ static int geometry(const ygg_mk_desc* d, Geo* g) {
     itab += (tiles + 1 + g->G) * (i == 4 ? 1 : L);
   }
   g->itab_len = itab;
+  g->nctr = 0;
+  for (int i = 0; i < 5; ++i) g->nctr += (Ns[i] / kBM) * (i == 4 ? 1 : L);
   g->ws_floats = max_seg * g->BN * kBM;
   g->part_bytes = static_cast<size_t>(g->chunks) * g->M * d->n_heads * (d->head_dim + 2) * sizeof(float);
   g->table_bytes = static_cast<size_t>(g->nmaps) * sizeof(CUtensorMap) + static_cast<size_t>(g->nphases) * sizeof(Phase) +
-                   static_cast<size_t>(g->itab_len) * 4 + 64;
+                   static_cast<size_t>(g->itab_len) * 4 + static_cast<size_t>(g->nctr) * 8 +
+                   static_cast<size_t>(g->nphases) * 4 + 192;
   return YGG_OK;
 }
 
@@ -1066,7 +1391,11 @@ int ygg_mk_plan_init(void* plan_mem, const ygg_mk_desc* d, void* table_dev, size
     if (int rc = encode(&maps[qmap], 3, d->q, dims, str, box)) return rc;
   }
   int wsbuf = 0;
-  auto gemm = [&](int layer, int wmap, int xmap, int N, int K) -> Phase {
+  int nctr = 0;
+  bool too_many_tiles = false;
+  int nptot = 0;
+  auto gemm = [&](int layer, int wmap, int xmap, int N, int K, int epi, int ss_in, int ss_out, int src,
+                  int ss_src) -> int {
     Phase P;
     std::memset(&P, 0, sizeof(P));
     P.kind = kGemm;
@@ -1080,8 +1409,18 @@ int ygg_mk_plan_init(void* plan_mem, const ygg_mk_desc* d, void* table_dev, size
     P.units = tiles * P.kb;
     P.ws = wsbuf;
     wsbuf ^= 1;
-    P.ss_in = P.ss_out = -1;
+    P.epi = epi;
+    P.ss_in = ss_in;
+    P.ss_out = ss_out;
+    P.cache_off = static_cast<long long>(std::min(layer, L - 1)) * d->layer_stride;
+    P.ctr = nctr;
+    P.dctr = nctr;  // done counters live in a parallel array (same offsets)
+    nctr += tiles;
+    P.ptot = nptot++;
+    P.src = getenv("YGG_MK_DATAFLOW") ? src : -1;  // dataflow X gating (A/B; grid counter by default)
+    P.ss_src = ss_src;
     std::vector<int> count(tiles, 0), sbase(G, 0);
+    if ((P.units + G - 1) / G / P.kb + 2 > kMaxPend) too_many_tiles = true;
     int seg = 0;
     for (int c = 0; c < G; ++c) {
       const long long u0 = static_cast<long long>(P.units) * c / G, u1 = static_cast<long long>(P.units) * (c + 1) / G;
@@ -1101,17 +1440,9 @@ int ygg_mk_plan_init(void* plan_mem, const ygg_mk_desc* d, void* table_dev, size
     itab.push_back(accn);
     P.seg_base = static_cast<int>(itab.size());
     for (int c = 0; c < G; ++c) itab.push_back(sbase[c]);
+    P.nsegs = seg;
     phases.push_back(P);
-    return P;
-  };
-  auto epi = [&](int kind, const Phase& src, int layer, int ss_in, int ss_out) {
-    Phase P = src;
-    P.kind = kind;
-    P.layer = layer;
-    P.ss_in = ss_in;
-    P.ss_out = ss_out;
-    P.cache_off = static_cast<long long>(layer) * d->layer_stride;
-    phases.push_back(P);
+    return static_cast<int>(phases.size()) - 1;
   };
   {
     Phase E;
@@ -1121,9 +1452,11 @@ int ygg_mk_plan_init(void* plan_mem, const ygg_mk_desc* d, void* table_dev, size
     E.ss_out = 0;
     phases.push_back(E);
   }
+  // Per layer: QKV(+rstd, RoPE, q / KV append) | attention | combine | O(+residual, ss) |
+  // gate|up(+rstd, SwiGLU) | down(+residual, ss).  ss buffer 0 feeds QKV and the LM head, 1 feeds gate|up.
+  int prev_down = -1;
   for (int l = 0; l < L; ++l) {
-    Phase q = gemm(l, 6 * l + 0, xm_hb, qkv, d->d_model);
-    epi(kEpiQkv, q, l, 0, -1);
+    gemm(l, 6 * l + 0, xm_hb, qkv, d->d_model, kEpiQkv, 0, -1, prev_down, prev_down);
     {
       Phase A;
       std::memset(&A, 0, sizeof(A));
@@ -1137,18 +1470,15 @@ int ygg_mk_plan_init(void* plan_mem, const ygg_mk_desc* d, void* table_dev, size
       A.kind = kCombine;
       phases.push_back(A);
     }
-    Phase o = gemm(l, 6 * l + 1, xm_attn, d->d_model, qdim);
-    epi(kEpiResid, o, l, -1, 1);
-    Phase gu = gemm(l, 6 * l + 2, xm_hb, 2 * d->ffn, d->d_model);
-    epi(kEpiSwiglu, gu, l, 1, -1);
-    Phase dn = gemm(l, 6 * l + 3, xm_mlp, d->d_model, d->ffn);
-    epi(kEpiResid, dn, l, -1, 0);
+    const int po = gemm(l, 6 * l + 1, xm_attn, d->d_model, qdim, kEpiResid, -1, 1, -1, -1);
+    const int pg = gemm(l, 6 * l + 2, xm_hb, 2 * d->ffn, d->d_model, kEpiSwiglu, 1, -1, po, po);
+    prev_down = gemm(l, 6 * l + 3, xm_mlp, d->d_model, d->ffn, kEpiResid, -1, 0, pg, -1);
   }
-  Phase lm = gemm(L, lm_map, xm_hb, d->vocab, d->d_model);
-  epi(kEpiStore, lm, L, 0, -1);
-  if (static_cast<int>(phases.size()) != g.nphases || static_cast<int>(itab.size()) > g.itab_len)
+  gemm(L, lm_map, xm_hb, d->vocab, d->d_model, kEpiStore, 0, -1, prev_down, prev_down);
+  if (too_many_tiles) return ygg_fail(YGG_ERR_UNSUPPORTED, "persistent forward: too many tiles per CTA in one GEMM");
+  if (static_cast<int>(phases.size()) != g.nphases || static_cast<int>(itab.size()) > g.itab_len || nctr > g.nctr)
     return ygg_fail(YGG_ERR_VALUE, "persistent forward: internal program size mismatch");
-  // Device table: maps | phases | itab | barrier counter.
+  // Device table: maps | phases | itab | tile-group counters | barrier counter.
   std::vector<unsigned char> blob(g.table_bytes, 0);
   size_t off = 0;
   std::memcpy(blob.data() + off, maps.data(), maps.size() * sizeof(CUtensorMap));
@@ -1160,6 +1490,14 @@ int ygg_mk_plan_init(void* plan_mem, const ygg_mk_desc* d, void* table_dev, size
   const size_t it_off = off;
   std::memcpy(blob.data() + off, itab.data(), itab.size() * 4);
   off += static_cast<size_t>(g.itab_len) * 4;
+  const size_t ctr_off = off;
+  off += static_cast<size_t>(g.nctr) * 4;
+  const size_t dctr_off = off;
+  off += static_cast<size_t>(g.nctr) * 4;
+  const size_t ptot_off = off;
+  off += static_cast<size_t>(g.nphases) * 4;
+  const size_t lctr_off = off;
+  off += 4;
   const size_t bar_off = (off + 63) / 64 * 64;
   if (bar_off + 4 > g.table_bytes) return ygg_fail(YGG_ERR_VALUE, "persistent forward: table overflow");
   cudaError_t e = cudaMemcpy(table_dev, blob.data(), g.table_bytes, cudaMemcpyHostToDevice);
@@ -1179,6 +1517,10 @@ int ygg_mk_plan_init(void* plan_mem, const ygg_mk_desc* d, void* table_dev, size
   a.phases = reinterpret_cast<const Phase*>(tb + ph_off);
   a.itab = reinterpret_cast<const int32_t*>(tb + it_off);
   a.bar = reinterpret_cast<unsigned*>(tb + bar_off);
+  a.ctr = reinterpret_cast<unsigned*>(tb + ctr_off);
+  a.dctr = reinterpret_cast<unsigned*>(tb + dctr_off);
+  a.ptot = reinterpret_cast<unsigned*>(tb + ptot_off);
+  a.lctr = reinterpret_cast<unsigned*>(tb + lctr_off);
   a.nphases = g.nphases;
   if (const char* stop = getenv("YGG_MK_STOP")) a.nphases = std::max(1, std::min(g.nphases, atoi(stop)));  // debugging
   a.G = G;
@@ -1188,6 +1530,8 @@ int ygg_mk_plan_init(void* plan_mem, const ygg_mk_desc* d, void* table_dev, size
   a.look = g.look;
   a.pf_maps = getenv("YGG_MK_PFMAP") ? atoi(getenv("YGG_MK_PFMAP")) : 1;
   a.xflags = getenv("YGG_MK_XFLAGS") ? atoi(getenv("YGG_MK_XFLAGS")) : 0;
+  if (getenv("YGG_MK_NOATTN")) a.xflags |= 8;
+  a.attn_bytes = static_cast<int>(attn_smem_bytes(hd));
   a.d = d->d_model;
   a.Hq = d->n_heads;
   a.Hkv = d->n_kv_heads;

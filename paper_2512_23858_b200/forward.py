@@ -210,8 +210,8 @@ class Forward:
         buf = None
         if on:
             g = torch.cuda.get_device_properties(self.cache.device).multi_processor_count
-            nph = 1 + 10 * self.cfg.n_layers + 2
-            buf = torch.zeros(g, nph, dtype=torch.int64, device=self.cache.device)
+            nph = 1 + 6 * self.cfg.n_layers + 1
+            buf = torch.zeros(8 * g, nph, dtype=torch.int64, device=self.cache.device)
         self._mk_desc.dbg = buf.data_ptr() if buf is not None else None
         self._mk_stamps = buf
         L.check(lib.ygg_mk_plan_init(self._mk_plan, C.byref(self._mk_desc), self.mk_table.data_ptr(),

@@ -44,7 +44,7 @@ emb = w["embed"][tokens.long()].double()
 print("embed resid", rel(f.resid, emb), "hb", rel(f.xn, emb))
 ss_ref = (f.resid.double() ** 2).view(R, d // 128, 128).sum(-1).T
 print("ss0", rel(f.ss[0], ss_ref))
-f, cache = run(3)
+f, cache = run(2)
 h = emb
 rstd = torch.rsqrt((h * h).mean(-1) + cfg.norm_eps)
 y = (f.xn.double() @ lw["wqkv"].double().T) * rstd[:, None]
@@ -56,7 +56,7 @@ kc = cache[0, 0, 0].float().cpu()  # [Hkv, S, hd]
 print("k", rel(kc[:, P:P + R, :].permute(1, 0, 2), k_ref))
 vt = cache[0, 0, 1].float().cpu().reshape(Hkv, hd, -1)
 print("v", rel(vt[:, :, P:P + R].permute(2, 0, 1), v_ref))
-f, cache = run(5)
+f, cache = run(4)
 # attention reference over prefix keys [0,P) + causal block
 K = cache[0, 0, 0].double().cpu()  # [Hkv,S,hd]
 Vt = cache[0, 0, 1].double().cpu().reshape(Hkv, hd, -1)
@@ -71,28 +71,28 @@ for i in range(R):
         p = torch.softmax(s, 0)
         out[i, hh] = Vt[kv, :, :n] @ p
 print("attn", rel(f.attn.view(R, Hq, hd).cpu(), out))
-f, cache = run(7)
+f, cache = run(5)
 o = f.attn.double() @ lw["wo"].double().T
 h1 = emb + o
 print("resid1", rel(f.resid, h1), "ss1", rel(f.ss[1], (f.resid.double() ** 2).view(R, d // 128, 128).sum(-1).T))
-f, cache = run(9)
+f, cache = run(6)
 r1 = torch.rsqrt((h1 * h1).mean(-1) + cfg.norm_eps)
 gu = (f.xn.double() @ lw["wgu"].double().T) * r1[:, None]
 act = torch.nn.functional.silu(gu[:, :cfg.ffn]) * gu[:, cfg.ffn:]
 print("mlp", rel(f.mlp, act))
-f, cache = run(11)
+f, cache = run(7)
 h2 = h1 + f.mlp.double() @ lw["wdown"].double().T
 print("resid2", rel(f.resid, h2))
-f, cache = run(13)
+f, cache = run(8)
 r2 = torch.rsqrt((h2 * h2).mean(-1) + cfg.norm_eps)
 lg = (f.xn.double() @ w["lm_head"].double().T) * r2[:, None]
 print("logits", rel(f.logits, lg))
-f, cache = run(10)
+f, cache = run(6)
 print("resid after down gemm (should be h1)", rel(f.resid, h1))
-f, cache = run(11)
+f, cache = run(7)
 dd = (f.resid.double() - h2).abs()
 print("err by row", dd.max(1).values.tolist())
 print("err by 128-col tile", dd.view(R, -1, 128).amax((0, 2)).tolist())
 print("err by col%128 (first 16)", dd.amax(0).view(-1, 128).amax(0)[:16].tolist())
-f2, _ = run(11)
+f2, _ = run(7)
 print("rerun diff", float((f2.resid - f.resid).abs().max()))

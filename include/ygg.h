@@ -281,6 +281,34 @@ int ygg_commit(ygg_seq seq, ygg_tree vtree, const int32_t* path, const int32_t* 
 /* ---------------- K8: on-device stage timer ---------------- */
 int ygg_stamp(unsigned long long* slot, ygg_stream_t stream);
 
+/* ---------------- Row-block GEMV (decode passes, 1..16 token rows) ----------------
+ * Y = X . W^T with the layer epilogue fused; one launch per matmul, full K per 16-row block of W
+ * (no split-K partials).  Weights in the fused layout (model.prepare_fused_): RMSNorm gains folded,
+ * QKV rows RoPE-pair interleaved, gate/up rows interleaved.  ss_in / ss_out are per-block sums of
+ * squares of the un-normalised residual ([blocks][M]); the consumer applies rstd. */
+typedef enum { YGG_GEMV_STORE = 1, YGG_GEMV_QKV = 2, YGG_GEMV_SWIGLU = 3, YGG_GEMV_RESID = 4 } ygg_gemv_kind;
+typedef struct {
+  int32_t kind;
+  float* out;            /* STORE: [M][ld] f32 */
+  int32_t ld;
+  const float* ss_in;    /* [ss_blocks][M] or NULL (no folded RMSNorm) */
+  int32_t ss_blocks;
+  int32_t norm_dim;
+  float eps;
+  void* q_out;           /* QKV: q [M][Hq][hd] bf16 */
+  void* cache;           /* QKV: this layer's [B][2][Hkv][S][hd] block (V transposed) */
+  int32_t S, Hq, Hkv, hd;
+  const int32_t* pos; const int32_t* slot; const int32_t* req;
+  const float* rope_cs;  /* [positions][hd/2][2] */
+  void* act_out;         /* SWIGLU: [M][N/2] bf16 */
+  float* resid;          /* RESID: [M][N] f32, updated in place */
+  void* hb;              /* RESID: bf16 copy of the residual */
+  float* ss_out;         /* RESID: [N/16][M] */
+} ygg_gemv_epilogue;
+size_t ygg_gemv_plan_size(void);
+int ygg_gemv_plan_init(void* plan, const void* W, const void* X, int M, int N, int K, int num_ctas);
+int ygg_gemv_run(const void* plan, const ygg_gemv_epilogue* epi, ygg_stream_t stream);
+
 /* ---------------- Persistent forward (bf16, decode-shaped: B*T <= 128 rows) ----------------
  * One launch runs a whole draft or verify forward (the passes the reference prices as
  * latency_at(drafter|verifier, width), simulator.py:202-214): embed, then per layer

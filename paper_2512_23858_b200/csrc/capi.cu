@@ -23,6 +23,7 @@ int ygg_prepare_gemm(void);
 int ygg_prepare_layers(void);
 int ygg_prepare_attn_tc(void);
 int ygg_prepare_mk(void);
+int ygg_prepare_gemv(void);
 
 int ygg_version(void) { return 100; }
 
@@ -46,6 +47,7 @@ int ygg_device_check(int* num_sms, int* cc_major, int* cc_minor) {
   if (int rc = ygg_prepare_layers()) return rc;
   if (int rc = ygg_prepare_attn_tc()) return rc;
   if (int rc = ygg_prepare_mk()) return rc;
+  if (int rc = ygg_prepare_gemv()) return rc;
   return YGG_OK;
 }
 

@@ -101,6 +101,7 @@ class Forward:
         logits: bool = True,
         num_ctas: int = 0,
         persistent: bool | None = None,
+        gemv: bool | None = None,
     ):
         L.require_device()
         self.cfg, self.cache = cfg, cache
@@ -110,10 +111,17 @@ class Forward:
         self.act = L.dtype_code(act_dtype)
         # bf16 default: plain stream-K GEMM + separate vectorised epilogue kernels (faster today);
         # YGG_FUSED=1 selects the fused-epilogue GEMMs (same results, tested).
-        self.fused = act_dtype == torch.bfloat16 and bool(os.environ.get("YGG_FUSED"))
+        bf16 = act_dtype == torch.bfloat16
+        if gemv is None:
+            gemv = os.environ.get("YGG_GEMV", "1") != "0"
+        # Decode passes of <= 16 rows: row-block GEMV with fused epilogues (csrc/gemv.cu); needs the
+        # fused weight layout, which then also routes every other bf16 forward on these weights
+        # (prefill, verify) through the fused-epilogue GEMM.
+        self.gemv = bool(gemv) and bf16 and logits and B * R <= 16 and mask_words <= L.MAX_MASK_WORDS
+        self.fused = bf16 and (bool(os.environ.get("YGG_FUSED")) or self.gemv or weights.get("_layout") == "fused")
         if persistent is None:
             persistent = os.environ.get("YGG_MK", "0") != "0"
-        self.mk = (persistent and act_dtype == torch.bfloat16 and not self.fused and logits and B * R <= 128
+        self.mk = (persistent and bf16 and not self.fused and logits and B * R <= 128
                    and mask_words <= L.MAX_MASK_WORDS)
         if self.fused:
             prepare_fused_(weights, cfg)
@@ -167,6 +175,76 @@ class Forward:
             self._setup_fused()
         if self.mk:
             self._setup_mk()
+        if self.gemv:
+            self._setup_gemv()
+
+    # ------------------------------------------------------------------
+    def _setup_gemv(self) -> None:
+        """Row-block GEMV plans + epilogues (csrc/gemv.cu) for a <= 16-row decode pass."""
+        lib, cfg, M = L.lib(), self.cfg, self.M
+        dev = self.cache.device
+        d = cfg.d_model
+        self.ss_e = torch.zeros(d // 128, M, dtype=torch.float32, device=dev)  # embed: per 128 features
+        self.ss_ga = torch.zeros(d // 16, M, dtype=torch.float32, device=dev)  # after down: per 16 rows
+        self.ss_gb = torch.zeros(d // 16, M, dtype=torch.float32, device=dev)  # after o-proj
+        es = self.cache.element_size()
+        eps = float(cfg.norm_eps)
+
+        def plan(W, X):
+            mem = C.create_string_buffer(int(lib.ygg_gemv_plan_size()))
+            N, K = W.shape
+            L.check(lib.ygg_gemv_plan_init(mem, W.data_ptr(), X.data_ptr(), M, N, K, 0))
+            return mem
+
+        def epi(kind, **kw):
+            e = L.YggGemvEpilogue()
+            e.kind = kind
+            for k, v in kw.items():
+                setattr(e, k, v)
+            return e
+
+        self.gv = []
+        for li, lw in enumerate(self.w["layers"]):
+            ss_in, blocks = (self.ss_e, d // 128) if li == 0 else (self.ss_ga, d // 16)
+            cache_l = self.cache.data_ptr() + li * self.layer_stride * es
+            self.gv.append([
+                (plan(lw["wqkv"], self.xn),
+                 epi(L.YGG_GEMV_QKV, ss_in=ss_in.data_ptr(), ss_blocks=blocks, norm_dim=d, eps=eps,
+                     q_out=self.q.data_ptr(), cache=cache_l, S=self.S, Hq=cfg.n_heads, Hkv=cfg.n_kv_heads,
+                     hd=cfg.head_dim, pos=self.pos.data_ptr(), slot=self.slot.data_ptr(), req=self.req.data_ptr(),
+                     rope_cs=self.rope_cs.data_ptr())),
+                (plan(lw["wo"], self.attn),
+                 epi(L.YGG_GEMV_RESID, resid=self.resid.data_ptr(), hb=self.xn.data_ptr(),
+                     ss_out=self.ss_gb.data_ptr())),
+                (plan(lw["wgu"], self.xn),
+                 epi(L.YGG_GEMV_SWIGLU, ss_in=self.ss_gb.data_ptr(), ss_blocks=d // 16, norm_dim=d, eps=eps,
+                     act_out=self.mlp.data_ptr())),
+                (plan(lw["wdown"], self.mlp),
+                 epi(L.YGG_GEMV_RESID, resid=self.resid.data_ptr(), hb=self.xn.data_ptr(),
+                     ss_out=self.ss_ga.data_ptr())),
+            ])
+        ss_last, blocks_last = (self.ss_ga, d // 16) if cfg.n_layers > 0 else (self.ss_e, d // 128)
+        self.gv_lm = (plan(self.w["lm_head"], self.xn),
+                      epi(L.YGG_GEMV_STORE, out=self.logits.data_ptr(), ld=cfg.vocab, ss_in=ss_last.data_ptr(),
+                          ss_blocks=blocks_last, norm_dim=d, eps=eps))
+
+    def _run_gemv(self, stream) -> None:
+        lib, cfg = L.lib(), self.cfg
+        s = L.stream_ptr(stream)
+        chk = L.check
+        chk(lib.ygg_embed_fused(self.w["embed"].data_ptr(), cfg.vocab, cfg.d_model, self.tokens.data_ptr(), self.M,
+                                self.resid.data_ptr(), self.xn.data_ptr(), self.ss_e.data_ptr(), s))
+        qm = self.qmask.data_ptr() if self.mask_words > 0 else None
+        for li, ops in enumerate(self.gv):
+            (pq, eq), (po, eo), (pg, eg), (pd, ed) = ops
+            chk(lib.ygg_gemv_run(pq, C.byref(eq), s))
+            chk(lib.ygg_attention_tc(self.attn_plans[li].handle, self.blk_start.data_ptr(), self.blk_len.data_ptr(),
+                                     qm, self.mask_words, self.scale, self.attn_part.data_ptr(), self.attn.data_ptr(),
+                                     s))
+            chk(lib.ygg_gemv_run(po, C.byref(eo), s))
+            chk(lib.ygg_gemv_run(pg, C.byref(eg), s))
+            chk(lib.ygg_gemv_run(pd, C.byref(ed), s))
+        chk(lib.ygg_gemv_run(self.gv_lm[0], C.byref(self.gv_lm[1]), s))
 
     # ------------------------------------------------------------------
     def _setup_mk(self) -> None:
@@ -293,7 +371,9 @@ class Forward:
             L.check(lib.ygg_gemm_run(plan.handle, self.ws.data_ptr(), stream_ptr))
 
     def run(self, stream: torch.cuda.Stream | None = None) -> None:
-        if self.mk:
+        if self.gemv:
+            self._run_gemv(stream)
+        elif self.mk:
             L.check(L.lib().ygg_mk_run(self._mk_plan, L.stream_ptr(stream)))
         elif self.fused:
             self._run_fused(stream)

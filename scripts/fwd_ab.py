@@ -33,11 +33,13 @@ for _ in range(2):
     sd.step(use_graph=False)
 torch.cuda.synchronize()
 res = {}
+variants = {"draft": (("kern", dict(gemv=False, persistent=False)), ("gemv", dict(gemv=True))),
+            "verify": (("kern", dict(persistent=False)), ("mk", dict(persistent=True)))}
 for name, f in (("draft", sd.draft), ("verify", sd.verify)):
-    for pers in (False, True):
-        g = Forward(f.cfg, f.w, f.cache, f.B, f.R, f.mask_words, f.act_dtype, persistent=pers)
+    for tag, kw in variants[name]:
+        g = Forward(f.cfg, f.w, f.cache, f.B, f.R, f.mask_words, f.act_dtype, **kw)
         for t in ("tokens", "pos", "slot", "req", "qmask", "blk_start", "blk_len"):
             getattr(g, t).copy_(getattr(f, t))
-        res[f"{name}_{'mk' if pers else 'kern'}_ms"] = timeit(g)
+        res[f"{name}_{tag}_ms"] = timeit(g)
         del g
 print(json.dumps(res), flush=True)

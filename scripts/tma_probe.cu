@@ -55,14 +55,19 @@ __global__ void probe(const __grid_constant__ CUtensorMap map, int stages, int k
         const long long v = u0 + i + look;
         const int pk = static_cast<int>(v % kgroups);
         const int pn = static_cast<int>((v / kgroups) % n_tiles);
-        if (pf_mode == 1) {
+        if (pf_mode == 1 || pf_mode == 5) {
           asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(reinterpret_cast<uint64_t>(&map)),
                        "r"(pk * 64), "r"(pn * 128) : "memory");
         }
       }
       mbar_arrive_expect_tx(&full[st], box_bytes + xbytes);
       if (xrows) tma_load_2d(xbase + st * xbytes, &xmap, &full[st], kg * 64, 0, policy_evict_last());
-      if (kbox == 1)
+      if (pf_mode == 5) {  // tensor prefetch + demand load without a cache hint
+        asm volatile(
+            "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];"
+            ::"r"(smem_u32(base + st * box_bytes)), "l"(reinterpret_cast<uint64_t>(&map)), "r"(smem_u32(&full[st])),
+            "r"(kg * 64), "r"(nt * 128) : "memory");
+      } else if (kbox == 1)
         tma_load_2d(base + st * box_bytes, &map, &full[st], kg * 64, nt * 128, pol);
       else
         tma3(base + st * box_bytes, &map, &full[st], 0, nt * 128, kg * kbox);
@@ -148,8 +153,8 @@ int main() {
     }
     for (int ctas_per_sm : {1}) {
       for (int stages : {6}) {
-       for (int xrows : {0, 16, 64}) for (int st2 : {4, 5, 6, 8}) {
-        const int mode = 0, look = 0, stall = 0;
+       for (int xrows : {0}) for (int st2 : {6}) for (int mode : {0, 1, 5}) for (int look : {0, 16, 48}) for (int stall : {0, 64}) {
+        if (mode == 0 && look) continue;
         const int stages_ = st2;
         const size_t smem = 1024 + static_cast<size_t>(st2) * (16384 * kbox + xrows * 128) + 2 * st2 * 8 + 64;
         if (smem * ctas_per_sm > 228 * 1024 - 2048 * ctas_per_sm) continue;

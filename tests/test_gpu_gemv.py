@@ -1,0 +1,102 @@
+"""Row-block GEMV forward (csrc/gemv.cu, decode passes of <= 16 rows) vs the per-kernel bf16 forward.
+
+Same bf16 weights (separate copies: the GEMV path converts its dict to the fused layout), same rows,
+identical KV caches.  Tolerance 2e-2 relative to the logit scale (north_star's bf16 bound; the two
+paths round the GEMM inputs differently — folded vs applied RMSNorm — and accumulate in different
+orders); appended KV rows must agree to bf16 rounding.  Relaunches are bit-identical.
+"""
+
+import copy
+
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+MID = dict(n_layers=2, d_model=1024, n_heads=8, n_kv_heads=2, head_dim=128, ffn=2048, vocab=4096)
+
+
+def _inputs(cfg, B, R, mask_words, P, cuda, seed=0):
+    from paper_2512_23858_b200.forward import new_cache
+
+    S = P + R + 64
+    cache = new_cache(cfg, B, S, torch.bfloat16, cuda)
+    g = torch.Generator(device="cuda").manual_seed(seed + 1)
+    cache.copy_((torch.randn(cache.shape, device=cuda, generator=g) * 0.5).to(torch.bfloat16))
+    M = B * R
+    tokens = torch.randint(0, cfg.vocab, (M,), device=cuda, generator=g, dtype=torch.int32)
+    r = torch.arange(M, device=cuda, dtype=torch.int32) % R
+    qmask = None
+    pos = P + r
+    if mask_words:
+        rows, depth = [], []
+        for i in range(R):
+            par = -1 if i == 0 else (i - 1) // 2  # binary-ish tree
+            rows.append((rows[par] if par >= 0 else 0) | (1 << i))
+            depth.append(0 if par < 0 else depth[par] + 1)
+        qm = torch.tensor([[(rows[i] >> (32 * w)) & 0xFFFFFFFF for w in range(mask_words)] for i in range(R)] * B,
+                          dtype=torch.int64)
+        qmask = qm.to(torch.int32).to(cuda)
+        pos = (P + torch.tensor(depth * B, dtype=torch.int32)).to(cuda)
+    return cache, (tokens, pos, P + r, torch.arange(M, device=cuda, dtype=torch.int32) // R, qmask)
+
+
+def _fwd(cfg, w, cache, B, R, mask_words, gemv, inp, P):
+    from paper_2512_23858_b200.forward import Forward
+
+    tokens, pos, slot, req, qmask = inp
+    f = Forward(cfg, w, cache, B, R, mask_words, torch.bfloat16, gemv=gemv, persistent=False)
+    assert f.gemv == gemv
+    f.tokens.copy_(tokens)
+    f.pos.copy_(pos)
+    f.slot.copy_(slot)
+    f.req.copy_(req)
+    if qmask is not None:
+        f.qmask.copy_(qmask)
+    f.blk_start.fill_(P)
+    f.blk_len.fill_(R)
+    return f
+
+
+@pytest.mark.parametrize(
+    "name,B,R,mask_words,P",
+    [("tiny", 1, 8, 1, 40), ("tiny", 2, 8, 1, 100), ("tiny", 1, 1, 1, 77), ("mid", 1, 8, 1, 300),
+     ("mid", 2, 4, 1, 130), ("mid", 1, 16, 1, 64), ("mid", 1, 3, 0, 50)],
+)
+def test_gemv_matches_per_kernel(name, B, R, mask_words, P, cuda):
+    from paper_2512_23858_b200.model import ModelConfig, init_weights, preset, weights_to
+
+    cfg = preset("tiny-target") if name == "tiny" else ModelConfig("mid", **MID)
+    w0 = weights_to(init_weights(cfg, 0, torch.float32, "cpu"), cuda, torch.bfloat16)
+    w_ref, w_gv = copy.deepcopy(w0), copy.deepcopy(w0)
+    cache, inp = _inputs(cfg, B, R, mask_words, P, cuda)
+    c_ref, c_gv = cache.clone(), cache.clone()
+    ref = _fwd(cfg, w_ref, c_ref, B, R, mask_words, False, inp, P)
+    gv = _fwd(cfg, w_gv, c_gv, B, R, mask_words, True, inp, P)
+    ref.run()
+    gv.run()
+    torch.cuda.synchronize()
+    scale = float(ref.logits.abs().max())
+    err = float((gv.logits - ref.logits).abs().max())
+    assert err <= 2e-2 * scale, (err, scale)
+    assert (c_gv.float() - c_ref.float()).abs().max() <= 2e-2 * float(c_ref.float().abs().max())
+    first = gv.logits.clone()
+    gv.logits.zero_()
+    gv.run()
+    torch.cuda.synchronize()
+    assert torch.equal(gv.logits, first)
+
+
+def test_gemv_plan_rejects_bad_shapes(cuda):
+    import ctypes as C
+
+    from paper_2512_23858_b200 import _lib as L
+
+    lib = L.lib()
+    mem = C.create_string_buffer(int(lib.ygg_gemv_plan_size()))
+    W = torch.zeros(64, 128, dtype=torch.bfloat16, device=cuda)
+    X = torch.zeros(17, 128, dtype=torch.bfloat16, device=cuda)
+    with pytest.raises(ValueError):
+        L.check(lib.ygg_gemv_plan_init(mem, W.data_ptr(), X.data_ptr(), 17, 64, 128, 0))
+    with pytest.raises(ValueError):
+        L.check(lib.ygg_gemv_plan_init(mem, W.data_ptr(), X.data_ptr(), 8, 60, 128, 0))

@@ -61,7 +61,7 @@ def _forward(cfg, w, cache, B, R, mask_words, persistent, inputs, P):
     from paper_2512_23858_b200.forward import Forward
 
     tokens, pos, slot, req, qmask = inputs
-    f = Forward(cfg, w, cache, B, R, mask_words, torch.bfloat16, persistent=persistent)
+    f = Forward(cfg, w, cache, B, R, mask_words, torch.bfloat16, persistent=persistent, gemv=False)
     assert f.mk == persistent
     f.tokens.copy_(tokens)
     f.pos.copy_(pos)

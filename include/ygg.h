@@ -309,6 +309,17 @@ size_t ygg_gemv_plan_size(void);
 int ygg_gemv_plan_init(void* plan, const void* W, const void* X, int M, int N, int K, int num_ctas);
 int ygg_gemv_run(const void* plan, const ygg_gemv_epilogue* epi, ygg_stream_t stream);
 
+/* ---------------- Decode attention (<= 64 query rows per kv head) ----------------
+ * One CTA per (kv head, request) walks every visible key chunk with an online softmax (no split-KV
+ * partials, no combine launch); prefix keys always visible, block keys by the row's tree-mask bits
+ * (causal when mask_words == 0).  q [B*T][Hq][hd]; cache_layer as for ygg_attn_plan_init;
+ * out [B*T][Hq][hd] bf16. */
+size_t ygg_attn_dec_plan_size(void);
+int ygg_attn_dec_plan_init(void* plan, const void* q, const void* cache_layer, int B, int T, int Hq, int Hkv, int hd,
+                           int S);
+int ygg_attn_dec_run(const void* plan, const int32_t* blk_start, const int32_t* blk_len, const uint32_t* qmask,
+                     int mask_words, float scale, void* out, ygg_stream_t stream);
+
 /* ---------------- Persistent forward (bf16, decode-shaped: B*T <= 128 rows) ----------------
  * One launch runs a whole draft or verify forward (the passes the reference prices as
  * latency_at(drafter|verifier, width), simulator.py:202-214): embed, then per layer

@@ -169,6 +169,9 @@ _SIGS: dict[str, tuple] = {
     "ygg_verify_inputs": (C.c_int, [YggTree, YggSeq, vp, vp, vp, vp, vp, C.c_int, vp, vp, vp]),
     "ygg_commit": (C.c_int, [YggSeq, YggTree, vp, vp, vp, vp, C.c_int, vp]),
     "ygg_stamp": (C.c_int, [vp, vp]),
+    "ygg_attn_dec_plan_size": (C.c_size_t, []),
+    "ygg_attn_dec_plan_init": (C.c_int, [vp, vp, vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int]),
+    "ygg_attn_dec_run": (C.c_int, [vp, vp, vp, vp, C.c_int, C.c_float, vp, vp]),
     "ygg_gemv_plan_size": (C.c_size_t, []),
     "ygg_gemv_plan_init": (C.c_int, [vp, vp, vp, C.c_int, C.c_int, C.c_int, C.c_int]),
     "ygg_gemv_run": (C.c_int, [vp, C.POINTER(YggGemvEpilogue), vp]),
@@ -187,7 +190,7 @@ KERNELS_PER_CALL = {
     "ygg_tree_subtree": 1, "ygg_path_products": 1, "ygg_accept": 1, "ygg_kv_compact": 1, "ygg_gemm_run": 1, "ygg_gemm_fused": 1, "ygg_embed_fused": 1, "ygg_epi_store": 1,
     "ygg_epi_residual_norm": 1, "ygg_epi_swiglu": 1, "ygg_epi_qkv_rope": 1, "ygg_embed": 1, "ygg_rmsnorm": 1,
     "ygg_attention": 1, "ygg_attention_tc": 2, "ygg_row_stats": 1, "ygg_pass0_inputs": 1, "ygg_init_roots": 1, "ygg_level_inputs": 1,
-    "ygg_verify_inputs": 1, "ygg_commit": 1, "ygg_stamp": 1, "ygg_mk_run": 1, "ygg_gemv_run": 1,
+    "ygg_verify_inputs": 1, "ygg_commit": 1, "ygg_stamp": 1, "ygg_mk_run": 1, "ygg_gemv_run": 1, "ygg_attn_dec_run": 1,
 }
 launches = {"count": 0}
 

@@ -24,6 +24,7 @@ int ygg_prepare_layers(void);
 int ygg_prepare_attn_tc(void);
 int ygg_prepare_mk(void);
 int ygg_prepare_gemv(void);
+int ygg_prepare_attn_dec(void);
 
 int ygg_version(void) { return 100; }
 
@@ -48,6 +49,7 @@ int ygg_device_check(int* num_sms, int* cc_major, int* cc_minor) {
   if (int rc = ygg_prepare_attn_tc()) return rc;
   if (int rc = ygg_prepare_mk()) return rc;
   if (int rc = ygg_prepare_gemv()) return rc;
+  if (int rc = ygg_prepare_attn_dec()) return rc;
   return YGG_OK;
 }
 

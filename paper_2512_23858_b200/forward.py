@@ -224,6 +224,16 @@ class Forward:
                      ss_out=self.ss_ga.data_ptr())),
             ])
         ss_last, blocks_last = (self.ss_ga, d // 16) if cfg.n_layers > 0 else (self.ss_e, d // 128)
+        # decode attention: one CTA per (kv head, request), no split-KV partials / combine launch
+        self.ad_plans = None
+        if self.R * (cfg.n_heads // cfg.n_kv_heads) <= 64 and os.environ.get("YGG_ATTN_DEC", "1") != "0":
+            self.ad_plans = []
+            for li in range(cfg.n_layers):
+                mem = C.create_string_buffer(int(lib.ygg_attn_dec_plan_size()))
+                L.check(lib.ygg_attn_dec_plan_init(mem, self.q.data_ptr(),
+                                                   self.cache.data_ptr() + li * self.layer_stride * es, self.B, self.R,
+                                                   cfg.n_heads, cfg.n_kv_heads, cfg.head_dim, self.S))
+                self.ad_plans.append(mem)
         self.gv_lm = (plan(self.w["lm_head"], self.xn),
                       epi(L.YGG_GEMV_STORE, out=self.logits.data_ptr(), ld=cfg.vocab, ss_in=ss_last.data_ptr(),
                           ss_blocks=blocks_last, norm_dim=d, eps=eps))
@@ -238,9 +248,13 @@ class Forward:
         for li, ops in enumerate(self.gv):
             (pq, eq), (po, eo), (pg, eg), (pd, ed) = ops
             chk(lib.ygg_gemv_run(pq, C.byref(eq), s))
-            chk(lib.ygg_attention_tc(self.attn_plans[li].handle, self.blk_start.data_ptr(), self.blk_len.data_ptr(),
-                                     qm, self.mask_words, self.scale, self.attn_part.data_ptr(), self.attn.data_ptr(),
-                                     s))
+            if self.ad_plans is not None:
+                chk(lib.ygg_attn_dec_run(self.ad_plans[li], self.blk_start.data_ptr(), self.blk_len.data_ptr(), qm,
+                                         self.mask_words, self.scale, self.attn.data_ptr(), s))
+            else:
+                chk(lib.ygg_attention_tc(self.attn_plans[li].handle, self.blk_start.data_ptr(),
+                                         self.blk_len.data_ptr(), qm, self.mask_words, self.scale,
+                                         self.attn_part.data_ptr(), self.attn.data_ptr(), s))
             chk(lib.ygg_gemv_run(po, C.byref(eo), s))
             chk(lib.ygg_gemv_run(pg, C.byref(eg), s))
             chk(lib.ygg_gemv_run(pd, C.byref(ed), s))

@@ -12,7 +12,11 @@ prompts = bench.prompts_for(wl, tc.vocab, 0)
 sd.prefill_len = prompts.shape[1]
 sd.prefill(prompts)
 torch.cuda.synchronize()
+sd.step(use_graph=False)  # warm (first-use allocations, plan uploads)
+torch.cuda.synchronize()
+torch.cuda.nvtx.range_push("steps")
 for _ in range(n_steps):
     sd.step(use_graph=False)
 torch.cuda.synchronize()
+torch.cuda.nvtx.range_pop()
 print("aal", float(sd.seq.n_gen.sum()) / n_steps)

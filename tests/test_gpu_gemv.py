@@ -100,3 +100,54 @@ def test_gemv_plan_rejects_bad_shapes(cuda):
         L.check(lib.ygg_gemv_plan_init(mem, W.data_ptr(), X.data_ptr(), 17, 64, 128, 0))
     with pytest.raises(ValueError):
         L.check(lib.ygg_gemv_plan_init(mem, W.data_ptr(), X.data_ptr(), 8, 60, 128, 0))
+
+
+@pytest.mark.parametrize("hd,Hq,Hkv,B,T,P,mw", [(64, 32, 8, 1, 8, 300, 1), (128, 32, 8, 2, 16, 130, 1),
+                                                (64, 8, 2, 1, 1, 77, 0), (128, 8, 2, 1, 5, 64, 0)])
+def test_decode_attention_vs_fp32(hd, Hq, Hkv, B, T, P, mw, cuda):
+    """ygg_attn_dec_run vs a float64 softmax(QK^T/sqrt(hd)) V over the visible keys (prefix + tree /
+    causal block).  bf16 operands; tolerance 2e-2 of the output scale (bf16 P and output rounding)."""
+    import ctypes as C
+    import math
+
+    from paper_2512_23858_b200 import _lib as L
+
+    lib = L.lib()
+    S = ((P + T + 63) // 64) * 64
+    g = torch.Generator(device="cuda").manual_seed(hd + T)
+    M = B * T
+    q = torch.randn(M, Hq, hd, device=cuda, generator=g).to(torch.bfloat16)
+    cache = torch.randn(B, 2, Hkv, S, hd, device=cuda, generator=g).to(torch.bfloat16)  # kv=1 holds V^T rows
+    par = [-1] + [(i - 1) // 2 for i in range(1, T)]
+    rows = []
+    for i in range(T):
+        rows.append((rows[par[i]] if par[i] >= 0 else 0) | (1 << i))
+    qmask = torch.tensor([[rows[i] & 0xFFFFFFFF] for i in range(T)] * B, dtype=torch.int64).to(torch.int32).to(cuda)
+    bs = torch.full((B,), P, dtype=torch.int32, device=cuda)
+    bl = torch.full((B,), T, dtype=torch.int32, device=cuda)
+    out = torch.zeros(M, Hq, hd, dtype=torch.bfloat16, device=cuda)
+    mem = C.create_string_buffer(int(lib.ygg_attn_dec_plan_size()))
+    L.check(lib.ygg_attn_dec_plan_init(mem, q.data_ptr(), cache.data_ptr(), B, T, Hq, Hkv, hd, S))
+    scale = 1.0 / math.sqrt(hd)
+    L.check(lib.ygg_attn_dec_run(mem, bs.data_ptr(), bl.data_ptr(), qmask.data_ptr() if mw else None, mw, scale,
+                                 out.data_ptr(), L.stream_ptr()))
+    torch.cuda.synchronize()
+    K = cache[:, 0].double().cpu()                         # [B, Hkv, S, hd]
+    Vt = cache[:, 1].double().cpu().reshape(B, Hkv, hd, S)  # V^T rows
+    qd = q.double().cpu()
+    ref = torch.zeros(M, Hq, hd, dtype=torch.float64)
+    G = Hq // Hkv
+    for b in range(B):
+        for t in range(T):
+            vis = list(range(P))
+            for j in range(T):
+                if (mw and (rows[t] >> j) & 1) or (not mw and j <= t):
+                    vis.append(P + j)
+            vis = torch.tensor(vis)
+            for h in range(Hq):
+                kv = h // G
+                s = K[b, kv, vis] @ qd[b * T + t, h] * scale
+                p = torch.softmax(s, 0)
+                ref[b * T + t, h] = Vt[b, kv][:, vis] @ p
+    err = (out.double().cpu() - ref).abs().max()
+    assert err <= 2e-2 * ref.abs().max(), float(err)

@@ -180,6 +180,7 @@ __global__ void __launch_bounds__(kTopkThreads) topk_phase2(const TopkChunkOut* 
 // ===========================================================================
 constexpr int kGrowThreads = 256;
 constexpr int kGrowMaxCand = 1024;
+constexpr int kGrowMaxFront = 256;
 
 __global__ void __launch_bounds__(kGrowThreads) grow_level_kernel(ygg_tree t, int Fmax, int k, int w_draft,
                                                                   const int32_t* __restrict__ cand_tok,
@@ -192,6 +193,8 @@ __global__ void __launch_bounds__(kGrowThreads) grow_level_kernel(ygg_tree t, in
   __shared__ int srank[kGrowMaxCand];
   __shared__ int sslot[kGrowMaxCand];  // (frontier row, rank) packed
   __shared__ int s_n, s_ok, s_added;
+  __shared__ int s_apar[kGrowMaxCand];     // attached nodes by rank: parent, surrogate prob
+  __shared__ double s_aprob[kGrowMaxCand];
   __shared__ int s_fn;
   int32_t* flags = t.flags + b;
   const int size0 = t.size[b];
@@ -227,19 +230,31 @@ __global__ void __launch_bounds__(kGrowThreads) grow_level_kernel(ygg_tree t, in
     if (threadIdx.x == 0) atomicOr(flags, kFlagContract);
     return;
   }
-  if (threadIdx.x == 0) {
-    int n = 0;
-    for (int f = 0; f < fn; ++f) {
-      const int parent = frontier[f];
-      const int cnt = cand_n ? cand_n[static_cast<size_t>(b) * Fmax + f] : k;
-      const double path = t.cum[tb + parent];
-      for (int r = 0; r < cnt && n < kGrowMaxCand; ++r, ++n) {
-        sc[n] = path * cand_prob[(static_cast<size_t>(b) * Fmax + f) * k + r];
-        spar[n] = parent;
-        sslot[n] = f * k + r;
+  // Gather the scored candidates in (frontier row, rank) order, one thread per candidate slot:
+  // every load of the level is in flight at once instead of a serial walk on one thread.
+  {
+    __shared__ int s_off[kGrowMaxFront + 1];
+    if (threadIdx.x == 0) {
+      int acc = 0;
+      for (int f = 0; f < fn && f < kGrowMaxFront; ++f) {
+        s_off[f] = acc;
+        acc += cand_n ? cand_n[static_cast<size_t>(b) * Fmax + f] : k;
       }
+      s_off[min(fn, kGrowMaxFront)] = acc;
+      s_n = min(acc, kGrowMaxCand);
     }
-    s_n = n;
+    __syncthreads();
+    for (int i = threadIdx.x; i < fn * k; i += blockDim.x) {
+      const int f = i / k, r = i % k;
+      if (f >= kGrowMaxFront) continue;
+      const int cnt = s_off[f + 1] - s_off[f];
+      const int n = s_off[f] + r;
+      if (r >= cnt || n >= kGrowMaxCand) continue;
+      const int parent = frontier[f];
+      sc[n] = t.cum[tb + parent] * cand_prob[(static_cast<size_t>(b) * Fmax + f) * k + r];
+      spar[n] = parent;
+      sslot[n] = f * k + r;
+    }
   }
   __syncthreads();
   const int n = s_n;
@@ -270,11 +285,14 @@ __global__ void __launch_bounds__(kGrowThreads) grow_level_kernel(ygg_tree t, in
     const int parent = spar[i];
     const int f = sslot[i] / k, rk = sslot[i] % k;
     const size_t ci = (static_cast<size_t>(b) * Fmax + f) * k + rk;
+    const double pr = cand_prob[ci];
     t.token[tb + idx] = cand_tok[ci];
     t.parent[tb + idx] = parent;
     t.depth[tb + idx] = t.depth[tb + parent] + 1;
-    t.prob[tb + idx] = cand_prob[ci];
+    t.prob[tb + idx] = pr;
     t.cum[tb + idx] = sc[i];
+    s_apar[r] = parent;
+    s_aprob[r] = pr;
     uint32_t* row = t.mask + (tb + idx) * t.mask_words;
     const uint32_t* prow = t.mask + (tb + parent) * t.mask_words;
     for (int w = 0; w < t.mask_words; ++w) row[w] = prow[w] | ((idx >> 5) == w ? (1u << (idx & 31)) : 0u);
@@ -282,12 +300,12 @@ __global__ void __launch_bounds__(kGrowThreads) grow_level_kernel(ygg_tree t, in
   __syncthreads();
   if (threadIdx.x == 0) {
     // add_child sibling-sum check in insertion order (token_tree.py:79-83).
-    for (int i = size0; i < size0 + added; ++i) {
-      const int p = t.parent[tb + i];
+    for (int i = 0; i < added; ++i) {
+      const int p = s_apar[i];
       double s = 0.0;
-      for (int j = size0; j < i; ++j)
-        if (t.parent[tb + j] == p) s = s + t.prob[tb + j];
-      if (s + t.prob[tb + i] > 1.0 + kSiblingTol) atomicOr(flags, kFlagContract);
+      for (int j = 0; j < i; ++j)
+        if (s_apar[j] == p) s = s + s_aprob[j];
+      if (s + s_aprob[i] > 1.0 + kSiblingTol) atomicOr(flags, kFlagContract);
     }
     int32_t* fr = t.frontier + tb;
     for (int i = 0; i < added; ++i) fr[i] = size0 + i;

@@ -309,10 +309,10 @@ size_t ygg_gemv_plan_size(void);
 int ygg_gemv_plan_init(void* plan, const void* W, const void* X, int M, int N, int K, int num_ctas);
 int ygg_gemv_run(const void* plan, const ygg_gemv_epilogue* epi, ygg_stream_t stream);
 
-/* ---------------- Decode attention (<= 64 query rows per kv head) ----------------
- * One CTA per (kv head, request) walks every visible key chunk with an online softmax (no split-KV
- * partials, no combine launch); prefix keys always visible, block keys by the row's tree-mask bits
- * (causal when mask_words == 0).  q [B*T][Hq][hd]; cache_layer as for ygg_attn_plan_init;
+/* ---------------- Decode attention (tree / draft / verify passes) ----------------
+ * One CTA per (kv head, request, 64-row tile of (token, head) query rows) walks every visible key
+ * chunk with an online softmax (no split-KV partials, no combine launch); prefix keys always visible,
+ * block keys by the row's tree-mask bits (causal when mask_words == 0).  q [B*T][Hq][hd]; cache_layer as for ygg_attn_plan_init;
  * out [B*T][Hq][hd] bf16. */
 size_t ygg_attn_dec_plan_size(void);
 int ygg_attn_dec_plan_init(void* plan, const void* q, const void* cache_layer, int B, int T, int Hq, int Hkv, int hd,

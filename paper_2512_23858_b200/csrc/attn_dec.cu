@@ -1,6 +1,6 @@
-// Tree / prefix attention for decode-shaped passes (<= 64 query rows per kv head): one CTA per
-// (kv head, request) walks every visible key chunk with an online softmax, so there are no
-// split-KV partials and no combine launch.
+// Tree / prefix attention for decode-shaped passes: one CTA per (kv head, request, 64-row tile of
+// query rows) walks every visible key chunk with an online softmax, so there are no split-KV
+// partials and no combine launch.
 //
 // The tcgen05 split-KV kernel (attn_tc.cu) is built for the verify pass (T = 50 tokens x 4 heads =
 // 200 query rows per kv head): there a 128-row UMMA tile is full and a separate combine is cheap.
@@ -31,7 +31,7 @@ constexpr uint32_t kMagic = 0x59474144u;  // "YGAD"
 
 struct Plan {
   uint32_t magic;
-  int B, T, Hq, Hkv, hd, S, Gh, rows, warps, ksplit, stages;
+  int B, T, Hq, Hkv, hd, S, Gh, rows, warps, ksplit, stages, tpt, row_tiles;
   size_t smem;
   alignas(64) CUtensorMap tq;
   alignas(64) CUtensorMap tk;
@@ -39,7 +39,7 @@ struct Plan {
 };
 
 struct Args {
-  int T, Hq, Hkv, hd, S, Gh, rows, mask_words, ksplit, stages;
+  int T, Hq, Hkv, hd, S, Gh, rows, mask_words, ksplit, stages, tpt;  // rows = tpt * Gh (one row tile)
   float scale_log2;
   const int32_t* blk_start;
   const int32_t* blk_len;
@@ -127,6 +127,8 @@ __global__ void __launch_bounds__(32 * (1 + kMaxWarps), 1)
   uint64_t* empty = full + NS;
   uint64_t* qbar = empty + NS;
   const int kvh = blockIdx.x, r = blockIdx.y;
+  const int t0 = blockIdx.z * a.tpt;                        // first token of this row tile
+  const int rows_cta = min(a.tpt, a.T - t0) * a.Gh;         // valid query rows of this CTA
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nw = (a.rows + 15) / 16;  // row warps per key split
   if (threadIdx.x == 0) {
@@ -147,9 +149,9 @@ __global__ void __launch_bounds__(32 * (1 + kMaxWarps), 1)
   const size_t vt_row0 = ((static_cast<size_t>(r) * 2 + 1) * a.Hkv + kvh) * HD;     // V^T rows
   if (warp == 0) {
     if (lane == 0) {
-      mbar_arrive_expect_tx(qbar, static_cast<uint32_t>(a.rows) * 128u * DCH);
+      mbar_arrive_expect_tx(qbar, static_cast<uint32_t>(a.rows) * 128u * DCH);  // full box (OOB rows zero-filled)
       for (int dc = 0; dc < DCH; ++dc)
-        tma3(sq + dc * (64 * 128), &tq, qbar, dc * 64, kvh * a.Gh, r * a.T);
+        tma3(sq + dc * (64 * 128), &tq, qbar, dc * 64, kvh * a.Gh, r * a.T + t0);
       for (int c = 0; c < nch; ++c) {
         const int st = c % NS;
         if (c >= NS) mbar_wait(&empty[st], ((c / NS) - 1) & 1);
@@ -167,8 +169,8 @@ __global__ void __launch_bounds__(32 * (1 + kMaxWarps), 1)
   const int ks = cwi / nw, rw = cwi % nw;
   const int qr0 = rw * 16;
   const int ra = qr0 + (lane >> 2), rb = ra + 8;  // accumulator rows of this thread
-  const int ta = ra / a.Gh, tb = rb / a.Gh;
-  const bool va = ra < a.rows, vb = rb < a.rows;
+  const int ta = t0 + ra / a.Gh, tb = t0 + rb / a.Gh;
+  const bool va = ra < rows_cta, vb = rb < rows_cta;
   const uint32_t* mra = a.qmask + static_cast<size_t>(r * a.T + (va ? ta : 0)) * (a.mask_words ? a.mask_words : 1);
   const uint32_t* mrb = a.qmask + static_cast<size_t>(r * a.T + (vb ? tb : 0)) * (a.mask_words ? a.mask_words : 1);
   mbar_wait(qbar, 0);
@@ -380,7 +382,7 @@ int ygg_attn_dec_plan_init(void* plan, const void* q, const void* cache_layer, i
   YGG_CHECK_ARG(hd == 64 || hd == 128, "head dim must be 64 or 128");
   YGG_CHECK_ARG(Hkv >= 1 && Hq % Hkv == 0, "bad head grouping");
   const int Gh = Hq / Hkv;
-  YGG_CHECK_ARG(B >= 1 && T >= 1 && T * Gh <= 16 * kMaxWarps, "decode attention handles <= 64 query rows per kv head");
+  YGG_CHECK_ARG(B >= 1 && T >= 1 && Gh <= 64 && 64 % Gh == 0, "decode attention: head group must divide 64");
   YGG_CHECK_ARG(S % 64 == 0, "cache capacity must be a multiple of 64");
   Plan* p = reinterpret_cast<Plan*>((reinterpret_cast<uintptr_t>(plan) + 63) & ~uintptr_t(63));
   std::memset(p, 0, sizeof(Plan));
@@ -392,7 +394,9 @@ int ygg_attn_dec_plan_init(void* plan, const void* q, const void* cache_layer, i
   p->hd = hd;
   p->S = S;
   p->Gh = Gh;
-  p->rows = T * Gh;
+  p->tpt = T < 64 / Gh ? T : 64 / Gh;   // tokens per row tile (<= 64 query rows per CTA)
+  p->row_tiles = (T + p->tpt - 1) / p->tpt;
+  p->rows = p->tpt * Gh;
   const int nw = (p->rows + 15) / 16;
   p->ksplit = kMaxWarps / nw;            // split the key chunks over the remaining warps
   if (hd == 128 && p->ksplit > 2) p->ksplit = 2;  // register budget of the 128-wide accumulators
@@ -405,7 +409,7 @@ int ygg_attn_dec_plan_init(void* plan, const void* q, const void* cache_layer, i
   {  // q [M][Hq][hd]: box {64, Gh, T} -> rows (token, head-in-group); 64 rows of smem reserved
     cuuint64_t dims[3] = {static_cast<cuuint64_t>(hd), static_cast<cuuint64_t>(Hq), static_cast<cuuint64_t>(M)};
     cuuint64_t str[2] = {static_cast<cuuint64_t>(hd) * 2, static_cast<cuuint64_t>(Hq) * hd * 2};
-    cuuint32_t box[3] = {64, static_cast<cuuint32_t>(Gh), static_cast<cuuint32_t>(T)};
+    cuuint32_t box[3] = {64, static_cast<cuuint32_t>(Gh), static_cast<cuuint32_t>(p->tpt)};
     if (int rc = enc(&p->tq, 3, q, dims, str, box)) return rc;
   }
   {  // K rows [(B*2*Hkv*S)][hd]: box {64, 64 keys}
@@ -441,13 +445,14 @@ int ygg_attn_dec_run(const void* plan, const int32_t* blk_start, const int32_t* 
   a.mask_words = mask_words;
   a.ksplit = p->ksplit;
   a.stages = p->stages;
+  a.tpt = p->tpt;
   a.scale_log2 = scale * 1.4426950408889634f;
   a.blk_start = blk_start;
   a.blk_len = blk_len;
   a.qmask = qmask ? qmask : reinterpret_cast<const uint32_t*>(blk_start);  // never read when mask_words == 0
   a.out = static_cast<__nv_bfloat16*>(out);
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  const dim3 grid(p->Hkv, p->B), block(32 * (1 + p->warps));
+  const dim3 grid(p->Hkv, p->B, p->row_tiles), block(32 * (1 + p->warps));
   if (p->hd == 64)
     YGG_LAUNCH_PDL(attn_dec_kernel<64>, grid, block, p->smem, s, p->tq, p->tk, p->tv, a);
   else

@@ -171,6 +171,22 @@ class Forward:
                                for li in range(cfg.n_layers)]
             self.attn_part = torch.empty(self.attn_plans[0].partial_bytes // 4 + 1, dtype=torch.float32, device=dev)
         self.rope_cs = rope_table(cfg, self.S + 64, dev)
+        # Decode attention (csrc/attn_dec.cu) when one kv head's query rows fit one 64-row tile (draft
+        # levels, AR): one CTA per (kv head, request), no split-KV partials / combine launch.  Wider
+        # passes (verify: 50 tokens x 4 heads) and prefill keep the split-KV tcgen05 kernel, which is
+        # faster there (measured same-box: verify 4.37 ms vs 4.41 ms with the decode kernel).
+        self.ad_plans = None
+        gh = cfg.n_heads // cfg.n_kv_heads
+        if (act_dtype == torch.bfloat16 and mask_words <= L.MAX_MASK_WORDS and R * gh <= 64
+                and os.environ.get("YGG_ATTN_DEC", "1") != "0"):
+            lib = L.lib()
+            es = cache.element_size()
+            self.ad_plans = []
+            for li in range(cfg.n_layers):
+                mem = C.create_string_buffer(int(lib.ygg_attn_dec_plan_size()))
+                L.check(lib.ygg_attn_dec_plan_init(mem, self.q.data_ptr(), cache.data_ptr() + li * self.layer_stride * es,
+                                                   B, R, cfg.n_heads, cfg.n_kv_heads, cfg.head_dim, self.S))
+                self.ad_plans.append(mem)
         if self.fused:
             self._setup_fused()
         if self.mk:
@@ -224,19 +240,20 @@ class Forward:
                      ss_out=self.ss_ga.data_ptr())),
             ])
         ss_last, blocks_last = (self.ss_ga, d // 16) if cfg.n_layers > 0 else (self.ss_e, d // 128)
-        # decode attention: one CTA per (kv head, request), no split-KV partials / combine launch
-        self.ad_plans = None
-        if self.R * (cfg.n_heads // cfg.n_kv_heads) <= 64 and os.environ.get("YGG_ATTN_DEC", "1") != "0":
-            self.ad_plans = []
-            for li in range(cfg.n_layers):
-                mem = C.create_string_buffer(int(lib.ygg_attn_dec_plan_size()))
-                L.check(lib.ygg_attn_dec_plan_init(mem, self.q.data_ptr(),
-                                                   self.cache.data_ptr() + li * self.layer_stride * es, self.B, self.R,
-                                                   cfg.n_heads, cfg.n_kv_heads, cfg.head_dim, self.S))
-                self.ad_plans.append(mem)
         self.gv_lm = (plan(self.w["lm_head"], self.xn),
                       epi(L.YGG_GEMV_STORE, out=self.logits.data_ptr(), ld=cfg.vocab, ss_in=ss_last.data_ptr(),
                           ss_blocks=blocks_last, norm_dim=d, eps=eps))
+
+    def _attend(self, li: int, qm, s) -> None:
+        """bf16 attention of layer li: decode kernel when planned, else split-KV tcgen05 + combine."""
+        lib = L.lib()
+        if self.ad_plans is not None:
+            L.check(lib.ygg_attn_dec_run(self.ad_plans[li], self.blk_start.data_ptr(), self.blk_len.data_ptr(), qm,
+                                         self.mask_words, self.scale, self.attn.data_ptr(), s))
+        else:
+            L.check(lib.ygg_attention_tc(self.attn_plans[li].handle, self.blk_start.data_ptr(), self.blk_len.data_ptr(),
+                                         qm, self.mask_words, self.scale, self.attn_part.data_ptr(),
+                                         self.attn.data_ptr(), s))
 
     def _run_gemv(self, stream) -> None:
         lib, cfg = L.lib(), self.cfg
@@ -248,13 +265,7 @@ class Forward:
         for li, ops in enumerate(self.gv):
             (pq, eq), (po, eo), (pg, eg), (pd, ed) = ops
             chk(lib.ygg_gemv_run(pq, C.byref(eq), s))
-            if self.ad_plans is not None:
-                chk(lib.ygg_attn_dec_run(self.ad_plans[li], self.blk_start.data_ptr(), self.blk_len.data_ptr(), qm,
-                                         self.mask_words, self.scale, self.attn.data_ptr(), s))
-            else:
-                chk(lib.ygg_attention_tc(self.attn_plans[li].handle, self.blk_start.data_ptr(),
-                                         self.blk_len.data_ptr(), qm, self.mask_words, self.scale,
-                                         self.attn_part.data_ptr(), self.attn.data_ptr(), s))
+            self._attend(li, qm, s)
             chk(lib.ygg_gemv_run(po, C.byref(eo), s))
             chk(lib.ygg_gemv_run(pg, C.byref(eg), s))
             chk(lib.ygg_gemv_run(pd, C.byref(ed), s))
@@ -416,9 +427,7 @@ class Forward:
         for li, p in enumerate(self.plans):
             chk(lib.ygg_gemm_fused(p["qkv"].handle, ws, C.byref(p["qkv"].epi), s))
             stamp()
-            chk(lib.ygg_attention_tc(self.attn_plans[li].handle, self.blk_start.data_ptr(), self.blk_len.data_ptr(),
-                                     qm, self.mask_words, self.scale, self.attn_part.data_ptr(),
-                                     self.attn.data_ptr(), s))
+            self._attend(li, qm, s)
             stamp()
             chk(lib.ygg_gemm_fused(p["o"].handle, ws, C.byref(p["o"].epi), s))
             stamp()
@@ -461,9 +470,7 @@ class Forward:
                                      self.rope_cs.data_ptr(), s))
             stamp()
             if self.attn_plans is not None:
-                chk(lib.ygg_attention_tc(self.attn_plans[li].handle, self.blk_start.data_ptr(),
-                                         self.blk_len.data_ptr(), qm, self.mask_words, self.scale,
-                                         self.attn_part.data_ptr(), self.attn.data_ptr(), s))
+                self._attend(li, qm, s)
             else:
                 chk(lib.ygg_attention(self.q.data_ptr(), cache_l, self.act, M, self.B, cfg.n_heads, cfg.n_kv_heads,
                                       cfg.head_dim, self.S, self.blk_start.data_ptr(), self.blk_len.data_ptr(),

@@ -103,7 +103,9 @@ def test_gemv_plan_rejects_bad_shapes(cuda):
 
 
 @pytest.mark.parametrize("hd,Hq,Hkv,B,T,P,mw", [(64, 32, 8, 1, 8, 300, 1), (128, 32, 8, 2, 16, 130, 1),
-                                                (64, 8, 2, 1, 1, 77, 0), (128, 8, 2, 1, 5, 64, 0)])
+                                                (64, 8, 2, 1, 1, 77, 0), (128, 8, 2, 1, 5, 64, 0),
+                                                (128, 32, 8, 1, 50, 512, 2), (64, 32, 8, 2, 33, 90, 2),
+                                                (128, 32, 8, 1, 40, 64, 0)])
 def test_decode_attention_vs_fp32(hd, Hq, Hkv, B, T, P, mw, cuda):
     """ygg_attn_dec_run vs a float64 softmax(QK^T/sqrt(hd)) V over the visible keys (prefix + tree /
     causal block).  bf16 operands; tolerance 2e-2 of the output scale (bf16 P and output rounding)."""
@@ -122,7 +124,9 @@ def test_decode_attention_vs_fp32(hd, Hq, Hkv, B, T, P, mw, cuda):
     rows = []
     for i in range(T):
         rows.append((rows[par[i]] if par[i] >= 0 else 0) | (1 << i))
-    qmask = torch.tensor([[rows[i] & 0xFFFFFFFF] for i in range(T)] * B, dtype=torch.int64).to(torch.int32).to(cuda)
+    nwords = max(mw, 1)
+    qmask = torch.tensor([[(rows[i] >> (32 * w)) & 0xFFFFFFFF for w in range(nwords)] for i in range(T)] * B,
+                         dtype=torch.int64).to(torch.int32).to(cuda)
     bs = torch.full((B,), P, dtype=torch.int32, device=cuda)
     bl = torch.full((B,), T, dtype=torch.int32, device=cuda)
     out = torch.zeros(M, Hq, hd, dtype=torch.bfloat16, device=cuda)

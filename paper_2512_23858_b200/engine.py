@@ -317,9 +317,9 @@ class ARDecoder:
         self.act_dtype = act_dtype
         self.dev = torch.device(device)
         self.cache = new_cache(cfg, batch, self.S, act_dtype, self.dev)
-        # AR is the oracle of the lossless-greedy identity, so it runs the same matmul family as the
-        # verify pass (stream-K GEMM), not the row-block GEMV the draft passes use.
-        self.fwd = Forward(cfg, w, self.cache, batch, 1, 1, act_dtype, gemv=False)
+        # AR is the oracle of the lossless-greedy identity, so it runs the same kernel families as the
+        # verify pass (stream-K GEMM, split-KV tcgen05 attention), not the draft's GEMV / decode attention.
+        self.fwd = Forward(cfg, w, self.cache, batch, 1, 1, act_dtype, gemv=False, decode_attn=False)
         self.fwd.qmask.fill_(1)
         self.argmax = torch.zeros(batch, dtype=torch.int32, device=self.dev)
         self.P = torch.zeros(batch, dtype=torch.int32, device=self.dev)

@@ -102,6 +102,7 @@ class Forward:
         num_ctas: int = 0,
         persistent: bool | None = None,
         gemv: bool | None = None,
+        decode_attn: bool | None = None,
     ):
         L.require_device()
         self.cfg, self.cache = cfg, cache
@@ -177,8 +178,9 @@ class Forward:
         # faster there (measured same-box: verify 4.37 ms vs 4.41 ms with the decode kernel).
         self.ad_plans = None
         gh = cfg.n_heads // cfg.n_kv_heads
-        if (act_dtype == torch.bfloat16 and mask_words <= L.MAX_MASK_WORDS and R * gh <= 64
-                and os.environ.get("YGG_ATTN_DEC", "1") != "0"):
+        if decode_attn is None:
+            decode_attn = os.environ.get("YGG_ATTN_DEC", "1") != "0"
+        if decode_attn and act_dtype == torch.bfloat16 and mask_words <= L.MAX_MASK_WORDS and R * gh <= 64:
             lib = L.lib()
             es = cache.element_size()
             self.ad_plans = []

@@ -891,12 +891,13 @@ int ygg_gemm_plan_init(void* plan_mem, int dtype, const void* W, const void* X, 
     if (num_ctas > g->units) num_ctas = static_cast<int>(g->units);
     g->num_ctas = num_ctas;
     const int stage_bytes = kBM * kBK * 2 + g->BN * kBK * 2;
-    // Shared-memory budget: YGG_GEMM_SMEM_KB (default 113) keeps two GEMM CTAs resident per SM, so
-    // under programmatic dependent launch the next layer's CTAs start (prologue + weight prefetch)
-    // while this one drains its epilogue.
+    // Shared-memory budget: YGG_GEMM_SMEM_KB (default 150: one CTA per SM with a 6-stage ring at
+    // BN = 64, leaving room for a co-resident epilogue / attention CTA under programmatic dependent
+    // launch).  Same-box sweep of the cfg2 verify forward: 113 KB (two CTAs/SM) 4.37 ms, 135 KB
+    // 4.24, 150 KB 4.22, 165 KB 4.22, 190 KB 4.25, 227 KB 4.47.
     static const int smem_kb = [] {
       const char* s = getenv("YGG_GEMM_SMEM_KB");
-      int v = s ? atoi(s) : 113;
+      int v = s ? atoi(s) : 150;
       return v < 48 ? 48 : (v > 227 ? 227 : v);
     }();
     g->stages = std::min(12, (smem_kb * 1024 - kSmemExtra) / stage_bytes);

@@ -302,35 +302,44 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       const uint64_t pol_x = policy_evict_last();
       const long long n_units = u1 - u0;
       const int pre = static_cast<int>(n_units < S ? n_units : S);
-      int k = 0;
-      long long a = 0, b = 0, u = 0;
-      if (nsegs) { segment(0, a, b); u = a; }
-      int pre_tile[12], pre_kblk[12];
+      // Unit coordinates are stepped incrementally inside a segment (one tile): the single producer
+      // thread must not pay 64-bit divisions per stage (that alone capped a CTA near 30 GB/s).
+      int k = 0, left = 0, kblk = 0, wrow = 0, xrow = 0;
+      auto seg_start = [&](int kk) {
+        long long a, b;
+        segment(kk, a, b);
+        const int tile = static_cast<int>(a / p.kb);
+        kblk = static_cast<int>(a - static_cast<long long>(tile) * p.kb);
+        left = static_cast<int>(b - a);
+        wrow = (tile / p.m_tiles) * kBM;
+        xrow = (tile % p.m_tiles) * BN;
+      };
+      if (nsegs) seg_start(0);
+      auto advance = [&]() {
+        ++kblk;
+        if (--left == 0 && ++k < nsegs) seg_start(k);
+      };
+      int pre_xrow[12], pre_kblk[12];
       // Weights never depend on the previous kernel: stream them before the grid dependency.
       for (int i = 0; i < pre; ++i) {
-        const int tile = static_cast<int>(u / p.kb), kblk = static_cast<int>(u % p.kb);
-        pre_tile[i] = tile;
+        pre_xrow[i] = xrow;
         pre_kblk[i] = kblk;
         mbar_arrive_expect_tx(&full[i], a_bytes + b_bytes);
-        tma_load_2d(sa + static_cast<size_t>(i) * a_bytes, &tmap_w, &full[i], kblk * kBK, (tile / p.m_tiles) * kBM,
-                    pol_w);
-        if (++u == b && ++k < nsegs) { segment(k, a, b); u = a; }
+        tma_load_2d(sa + static_cast<size_t>(i) * a_bytes, &tmap_w, &full[i], kblk * kBK, wrow, pol_w);
+        advance();
       }
       pdl_wait();
       for (int i = 0; i < pre; ++i)
-        tma_load_2d(sb + static_cast<size_t>(i) * b_bytes, &tmap_x, &full[i], pre_kblk[i] * kBK,
-                    (pre_tile[i] % p.m_tiles) * BN, pol_x);
+        tma_load_2d(sb + static_cast<size_t>(i) * b_bytes, &tmap_x, &full[i], pre_kblk[i] * kBK, pre_xrow[i], pol_x);
       int stage = pre % S;
       uint32_t phase = (pre == S) ? 1u : 0u;
       while (k < nsegs) {
         mbar_wait(&empty[stage], phase ^ 1u);
-        const int tile = static_cast<int>(u / p.kb), kblk = static_cast<int>(u % p.kb);
-        const int n_tile = tile / p.m_tiles, m_tile = tile % p.m_tiles;
         mbar_arrive_expect_tx(&full[stage], a_bytes + b_bytes);
-        tma_load_2d(sa + static_cast<size_t>(stage) * a_bytes, &tmap_w, &full[stage], kblk * kBK, n_tile * kBM, pol_w);
-        tma_load_2d(sb + static_cast<size_t>(stage) * b_bytes, &tmap_x, &full[stage], kblk * kBK, m_tile * BN, pol_x);
+        tma_load_2d(sa + static_cast<size_t>(stage) * a_bytes, &tmap_w, &full[stage], kblk * kBK, wrow, pol_w);
+        tma_load_2d(sb + static_cast<size_t>(stage) * b_bytes, &tmap_x, &full[stage], kblk * kBK, xrow, pol_x);
         if (++stage == S) { stage = 0; phase ^= 1u; }
-        if (++u == b && ++k < nsegs) { segment(k, a, b); u = a; }
+        advance();
       }
       if (e.dbg) e.dbg[c * 8 + 6] = gtimer();
     }

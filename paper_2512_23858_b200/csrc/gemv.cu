@@ -132,22 +132,32 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint64_t pol_w = policy_evict_first(), pol_x = policy_evict_last();
       // Weights never depend on the previous kernel: fill the ring before the grid dependency.
       const int pre = total < S ? total : S;
+      // (block, chunk) of stage i stepped incrementally: no integer division on the issue path.
+      int b = blockIdx.x, q = 0;
+      auto step = [&]() {
+        if (++q == p.kchunks) {
+          q = 0;
+          b += p.grid;
+        }
+      };
       for (int i = 0; i < pre; ++i) {
-        const int b = blockIdx.x + (i / p.kchunks) * p.grid, q = i % p.kchunks;
         mbar_arrive_expect_tx(&full[i], w_bytes + x_bytes);
         tma3(sw + static_cast<size_t>(i) * w_bytes, &tw, &full[i], 0, b * kRows, q * kSub, pol_w);
+        step();
       }
       pdl_wait();
-      for (int i = 0; i < pre; ++i)
-        tma3(sx + static_cast<size_t>(i) * x_bytes, &tx, &full[i], 0, 0, (i % p.kchunks) * kSub, pol_x);
+      for (int i = 0, qq = 0; i < pre; ++i) {
+        tma3(sx + static_cast<size_t>(i) * x_bytes, &tx, &full[i], 0, 0, qq * kSub, pol_x);
+        if (++qq == p.kchunks) qq = 0;
+      }
       int st = pre % S;
       uint32_t ph = pre == S ? 1u : 0u;
       for (int i = pre; i < total; ++i) {
         mbar_wait(&empty[st], ph ^ 1u);
-        const int b = blockIdx.x + (i / p.kchunks) * p.grid, q = i % p.kchunks;
         mbar_arrive_expect_tx(&full[st], w_bytes + x_bytes);
         tma3(sw + static_cast<size_t>(st) * w_bytes, &tw, &full[st], 0, b * kRows, q * kSub, pol_w);
         tma3(sx + static_cast<size_t>(st) * x_bytes, &tx, &full[st], 0, 0, q * kSub, pol_x);
+        step();
         if (++st == S) {
           st = 0;
           ph ^= 1u;

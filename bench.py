@@ -37,11 +37,23 @@ WORKLOADS = {
                                   "max_verify 64, greedy, 1 request/GPU, 512-token prompt"),
     "cfg1": dict(target="tiny-target", draft="tiny-draft", depth=4, width=4, k=8, max_verify=64, batch=1,
                  prompt=32, desc="cfg1: tiny 4L d256 target + 1L draft, EGT D4 W4 k8, greedy, batch 1"),
+    # cfg4: 16 requests sharded over the GPUs (16 / world per GPU), rejection sampling at T = 0.8.
+    "cfg4": dict(target="llama3-8b", draft="llama3.2-1b", depth=6, width=8, k=8, max_verify=64, global_batch=16,
+                 prompt=2048, gen=1024, mode="sample", temperature=0.8,
+                 desc="cfg4: Llama-3-8B target + Llama-3.2-1B draft (bf16), EGT D6 W8 k8, rejection sampling "
+                      "T=0.8, 16 requests sharded over the GPUs, 2048-token prompts"),
+    # cfg5: the per-GPU slice of 64 requests over 8 GPUs (8 per GPU), 70B target + 8B draft.
+    "cfg5": dict(target="llama3-70b", draft="llama3-8b", depth=8, width=16, k=16, max_verify=64, batch=8,
+                 prompt=2048, gen=512,
+                 desc="cfg5: Llama-3-70B target + Llama-3-8B draft (bf16), EGT D8 W16 k16, greedy, 8 requests "
+                      "per GPU (64 over 8 GPUs), 2048-token prompts"),
 }
 # Coupled synthetic weights (paper_2512_23858_b200/model.py): shared semantic table + permutation.
 COUPLING = {
     "cfg2": dict(rank=2048, logit_scale=16.0, head_noise=6.0, layer_gain=2.0),
     "cfg1": dict(rank=256, logit_scale=8.0, head_noise=2.0, layer_gain=2.0),
+    "cfg4": dict(rank=2048, logit_scale=16.0, head_noise=6.0, layer_gain=2.0),
+    "cfg5": dict(rank=2048, logit_scale=16.0, head_noise=6.0, layer_gain=2.0),
 }
 DRAFT_PROF = ((1, 400.0), (64, 420.0), (128, 460.0))    # placeholder Eq.3 table (us); refreshed by K8
 VERIFY_PROF = ((1, 2400.0), (64, 2450.0), (128, 2600.0))
@@ -122,10 +134,13 @@ def build_decoder(wl: dict, name: str, device, seed_offset: int = 0):
         class verifier:
             breakpoints = VERIFY_PROF
 
+    from paper_2512_23858_b200.engine import GREEDY
+
     shape = StepShape(wl["depth"], wl["width"], wl["k"], wl["max_verify"])
-    max_seq = wl["prompt"] + 2048  # room for ~250 steps of up to D+2 tokens
+    max_seq = wl["prompt"] + wl.get("gen", 2048)  # room for the timed steps of up to D+2 tokens
     sd = SpecDecoder(tc, tw, dc, dw, shape, batch=wl["batch"], max_seq=max_seq, act_dtype=torch.bfloat16,
-                     profiles=PP, device=device)
+                     profiles=PP, device=device, mode=wl.get("mode", GREEDY),
+                     temperature=wl.get("temperature", 1.0))
     return sd, tc, dc
 
 
@@ -173,7 +188,18 @@ def gemm_roofline(sd, peak_gbs):
     torch.cuda.synchronize()
     times = [a.elapsed_time(b) * 1e-3 for a, b in ev]
     nbytes = [p.W.numel() * p.W.element_size() for p in plans]
+    flops = [2.0 * p.M * p.N * p.K for p in plans]
     achieved = sum(nbytes) / sum(times) / 1e9
+    _, _, pk = _peaks()
+    tc_peak = float(pk.get("bf16_tflops", 1630.0))
+    ridge = tc_peak * 1e12 / (peak_gbs * 1e9)  # FLOP per byte where the two roofs cross
+    if vf.M > ridge:  # weight-streaming intensity is M FLOP/B: at cfg4 / cfg5 batch the tensor pipe bounds
+        tf = sum(flops) / sum(times) / 1e12
+        return {"bound": "tensor", "achieved": round(tf, 1), "peak": tc_peak, "unit": "TFLOP/s",
+                "frac": round(tf / tc_peak, 4), "traffic": None,
+                "kernel": "gemm_bf16_tc_kernel (swap-AB tcgen05 stream-K)", "launches_timed": len(plans),
+                "flops_per_launch_avg": int(sum(flops) / len(plans)), "rows": vf.M,
+                "avg_launch_us": round(sum(times) / len(times) * 1e6, 2), "hbm_gbs": round(achieved, 1)}
     return {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak_gbs, "unit": "GB/s",
             "frac": round(achieved / peak_gbs, 4), **_ncu_traffic(),
             "kernel": "gemm_bf16_tc_kernel (swap-AB tcgen05 stream-K weight streaming)",
@@ -348,7 +374,9 @@ def run_ours(args, rank, world, local_rank):
 
     device = torch.device("cuda", local_rank)
     torch.cuda.set_device(device)
-    wl = WORKLOADS[args.workload]
+    wl = dict(WORKLOADS[args.workload])
+    if "global_batch" in wl:
+        wl["batch"] = max(1, wl["global_batch"] // world)
     peak, peak_kind, _ = _peaks()
     sd, tc, dc = build_decoder(wl, args.workload, device)
     prompts = prompts_for(wl, tc.vocab, rank)
@@ -357,7 +385,10 @@ def run_ours(args, rank, world, local_rank):
     n0 = L.launches["count"]
     sd.capture()
     launches_per_step = L.launches["count"] - n0
-    for _ in range(args.warmup):
+    sample = sd.mode != "greedy"
+    for i in range(args.warmup):
+        if sample:
+            sd.set_uniforms(i, rank)
         sd.step()
     torch.cuda.synchronize()
     if world > 1:
@@ -369,6 +400,8 @@ def run_ours(args, rank, world, local_rank):
     torch.cuda.synchronize()
     evs[0].record()
     for i in range(args.steps):
+        if sample:  # host-pregenerated acceptance uniforms, default_rng([seed, step]) (simulator.py:306)
+            sd.set_uniforms(args.warmup + i, rank)
         sd.step()
         evs[i + 1].record()
     torch.cuda.synchronize()

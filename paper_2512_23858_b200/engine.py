@@ -28,7 +28,7 @@ import torch
 
 from . import _lib as L
 from .device_tree import DeviceTrees, SeqState
-from .forward import Forward, new_cache
+from .forward import Forward, new_cache, prefill_causal
 from .model import ModelConfig
 
 GREEDY, SAMPLE = "greedy", "sample"
@@ -153,16 +153,8 @@ class SpecDecoder:
         self.seq.hist.zero_()
         self.seq.hist[:, :P0] = prompts_d
         for cfg, w, cache in ((self.tc, self.tw, self.tcache), (self.dc, self.dw, self.dcache)):
-            f = self._prefill_forward(cfg, w, cache, P0)
-            f.tokens.copy_(prompts_d.reshape(-1))
-            pos = torch.arange(P0, dtype=torch.int32, device=self.dev).repeat(B)
-            f.pos.copy_(pos)
-            f.slot.copy_(pos)
-            f.blk_start.zero_()
-            f.blk_len.fill_(P0)
-            f.run()
+            last = prefill_causal(cfg, w, cache, prompts_d, self.act_dtype, cfg is self.tc, self._prefill_fwd)
             if cfg is self.tc:
-                last = f.logits.view(B, P0, -1)[:, -1, :].contiguous()
                 am = torch.zeros(B, dtype=torch.int32, device=self.dev)
                 L.check(lib.ygg_row_stats(last.data_ptr(), L.YGG_F32, B, cfg.vocab, cfg.vocab, 1.0, am.data_ptr(),
                                           None, s))
@@ -340,16 +332,8 @@ class ARDecoder:
 
     def generate(self, prompts: torch.Tensor, n_tokens: int, use_graph: bool = True) -> list:
         B, P0 = prompts.shape
-        pf = Forward(self.cfg, self.w, self.cache, B, P0, 0, self.act_dtype)
         pd = prompts.to(self.dev, torch.int32)
-        pf.tokens.copy_(pd.reshape(-1))
-        pos = torch.arange(P0, dtype=torch.int32, device=self.dev).repeat(B)
-        pf.pos.copy_(pos)
-        pf.slot.copy_(pos)
-        pf.blk_start.zero_()
-        pf.blk_len.fill_(P0)
-        pf.run()
-        last = pf.logits.view(B, P0, -1)[:, -1, :].contiguous()
+        last = prefill_causal(self.cfg, self.w, self.cache, pd, self.act_dtype, True)
         L.check(L.lib().ygg_row_stats(last.data_ptr(), L.YGG_F32, B, self.cfg.vocab, self.cfg.vocab, 1.0,
                                       self.argmax.data_ptr(), None, L.stream_ptr()))
         self.P.fill_(P0)

@@ -496,6 +496,38 @@ class Forward:
             stamp()
 
 
+def prefill_causal(cfg: ModelConfig, w: dict, cache: torch.Tensor, prompts: torch.Tensor, act_dtype: torch.dtype,
+                   want_logits: bool, cache_fwd: dict | None = None, max_rows: int = 2048) -> torch.Tensor | None:
+    """Causal prefill of ``prompts`` [B, P0] (device int32) into ``cache``, in chunks of at most
+    ``max_rows`` rows per launch (each chunk attends to the earlier chunks as its prefix), so 2k-token
+    prompts at batch 8-16 (cfg4 / cfg5) never materialise [B*P0, V] logits or partials.  Returns the
+    f32 logits of each request's last prompt position [B, V] when ``want_logits`` (else None)."""
+    B, P0 = prompts.shape
+    chunk = max(1, min(P0, max_rows // B))
+    dev = prompts.device
+    fwd = cache_fwd if cache_fwd is not None else {}
+    last = None
+    for c0 in range(0, P0, chunk):
+        n = min(chunk, P0 - c0)
+        final = c0 + n == P0
+        key = (cfg.name, n, id(cache), final and want_logits)
+        f = fwd.get(key)
+        if f is None:
+            f = Forward(cfg, w, cache, B, n, 0, act_dtype, logits=final and want_logits, gemv=False,
+                        decode_attn=False, persistent=False)
+            fwd[key] = f
+        f.tokens.copy_(prompts[:, c0:c0 + n].reshape(-1))
+        pos = torch.arange(c0, c0 + n, dtype=torch.int32, device=dev).repeat(B)
+        f.pos.copy_(pos)
+        f.slot.copy_(pos)
+        f.blk_start.fill_(c0)
+        f.blk_len.fill_(n)
+        f.run()
+        if final and want_logits:
+            last = f.logits.view(B, n, -1)[:, -1, :].contiguous()
+    return last
+
+
 def new_cache(cfg: ModelConfig, B: int, S: int, dtype: torch.dtype, device) -> torch.Tensor:
     """KV cache [layers, B, 2, Hkv, S, hd]: the kv=0 half holds K rows [S][hd] (per-head contiguous key
     streams); the kv=1 half holds V transposed, [hd][S], so both attention MMAs read K-major tiles.

@@ -317,8 +317,12 @@ int ygg_gemv_run(const void* plan, const ygg_gemv_epilogue* epi, ygg_stream_t st
 size_t ygg_attn_dec_plan_size(void);
 int ygg_attn_dec_plan_init(void* plan, const void* q, const void* cache_layer, int B, int T, int Hq, int Hkv, int hd,
                            int S);
+/* workspace: >= ygg_attn_dec_workspace_size(plan) bytes, zero-filled once (cross-CTA key-split partials
+ * and monotonic arrival counters; the chunks of each (kv head, request, row tile) are split over CTAs
+ * and merged by the last one in fixed split order). */
+size_t ygg_attn_dec_workspace_size(const void* plan);
 int ygg_attn_dec_run(const void* plan, const int32_t* blk_start, const int32_t* blk_len, const uint32_t* qmask,
-                     int mask_words, float scale, void* out, ygg_stream_t stream);
+                     int mask_words, float scale, void* out, void* workspace, ygg_stream_t stream);
 
 /* ---------------- Persistent forward (bf16, decode-shaped: B*T <= 128 rows) ----------------
  * One launch runs a whole draft or verify forward (the passes the reference prices as

@@ -171,7 +171,8 @@ _SIGS: dict[str, tuple] = {
     "ygg_stamp": (C.c_int, [vp, vp]),
     "ygg_attn_dec_plan_size": (C.c_size_t, []),
     "ygg_attn_dec_plan_init": (C.c_int, [vp, vp, vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int]),
-    "ygg_attn_dec_run": (C.c_int, [vp, vp, vp, vp, C.c_int, C.c_float, vp, vp]),
+    "ygg_attn_dec_workspace_size": (C.c_size_t, [vp]),
+    "ygg_attn_dec_run": (C.c_int, [vp, vp, vp, vp, C.c_int, C.c_float, vp, vp, vp]),
     "ygg_gemv_plan_size": (C.c_size_t, []),
     "ygg_gemv_plan_init": (C.c_int, [vp, vp, vp, C.c_int, C.c_int, C.c_int, C.c_int]),
     "ygg_gemv_run": (C.c_int, [vp, C.POINTER(YggGemvEpilogue), vp]),

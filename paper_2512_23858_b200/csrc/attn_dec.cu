@@ -31,7 +31,7 @@ constexpr uint32_t kMagic = 0x59474144u;  // "YGAD"
 
 struct Plan {
   uint32_t magic;
-  int B, T, Hq, Hkv, hd, S, Gh, rows, warps, ksplit, stages, tpt, row_tiles;
+  int B, T, Hq, Hkv, hd, S, Gh, rows, warps, ksplit, stages, tpt, row_tiles, kvsplit;
   size_t smem;
   alignas(64) CUtensorMap tq;
   alignas(64) CUtensorMap tk;
@@ -40,6 +40,9 @@ struct Plan {
 
 struct Args {
   int T, Hq, Hkv, hd, S, Gh, rows, mask_words, ksplit, stages, tpt;  // rows = tpt * Gh (one row tile)
+  int kvsplit, row_tiles;  // CTAs per (kv head, request, row tile) splitting the key chunks
+  float* part;             // [B][Hkv][row_tiles][kvsplit][warps][NV][32] cross-CTA partials
+  unsigned* ctr;           // [B][Hkv][row_tiles] arrival counters (monotonic)
   float scale_log2;
   const int32_t* blk_start;
   const int32_t* blk_len;
@@ -127,7 +130,8 @@ __global__ void __launch_bounds__(32 * (1 + kMaxWarps), 1)
   uint64_t* empty = full + NS;
   uint64_t* qbar = empty + NS;
   const int kvh = blockIdx.x, r = blockIdx.y;
-  const int t0 = blockIdx.z * a.tpt;                        // first token of this row tile
+  const int rt = blockIdx.z / a.kvsplit, ks2 = blockIdx.z % a.kvsplit;  // row tile, cross-CTA key split
+  const int t0 = rt * a.tpt;                                // first token of this row tile
   const int rows_cta = min(a.tpt, a.T - t0) * a.Gh;         // valid query rows of this CTA
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nw = (a.rows + 15) / 16;  // row warps per key split
@@ -152,9 +156,9 @@ __global__ void __launch_bounds__(32 * (1 + kMaxWarps), 1)
       mbar_arrive_expect_tx(qbar, static_cast<uint32_t>(a.rows) * 128u * DCH);  // full box (OOB rows zero-filled)
       for (int dc = 0; dc < DCH; ++dc)
         tma3(sq + dc * (64 * 128), &tq, qbar, dc * 64, kvh * a.Gh, r * a.T + t0);
-      for (int c = 0; c < nch; ++c) {
-        const int st = c % NS;
-        if (c >= NS) mbar_wait(&empty[st], ((c / NS) - 1) & 1);
+      for (int j = 0, c = ks2; c < nch; ++j, c += a.kvsplit) {  // this CTA's chunks, local index j
+        const int st = j % NS;
+        if (j >= NS) mbar_wait(&empty[st], ((j / NS) - 1) & 1);
         mbar_arrive_expect_tx(&full[st], k_bytes + v_bytes);
         for (int dc = 0; dc < DCH; ++dc)
           tma2(sk + st * k_bytes + dc * (kKC * 128), &tk, &full[st], dc * 64, static_cast<int>(kv_row0) + c * kKC);
@@ -189,8 +193,9 @@ __global__ void __launch_bounds__(32 * (1 + kMaxWarps), 1)
   for (int n = 0; n < HD / 8; ++n) o[n][0] = o[n][1] = o[n][2] = o[n][3] = 0.f;
   float ma = -INFINITY, mb = -INFINITY, la = 0.f, lb = 0.f;
   const int brow = lane & 7, bhi = (lane >> 3) & 1;
-  for (int c = ks; c < nch; c += a.ksplit) {
-    const int st = c % NS;
+  for (int j = ks; ks2 + j * a.kvsplit < nch; j += a.ksplit) {
+    const int c = ks2 + j * a.kvsplit;
+    const int st = j % NS;
     const int key0 = c * kKC;
     // visibility of this thread's 16 key columns (n-tile j: keys 8j + 2*(lane&3) + {0,1}) per row
     uint32_t wa0 = 0u, wa1 = 0u, wb0 = 0u, wb1 = 0u;
@@ -202,7 +207,7 @@ __global__ void __launch_bounds__(32 * (1 + kMaxWarps), 1)
       wb0 = vis_word(key0, bs, bl, tb, a.mask_words, mrb);
       wb1 = vis_word(key0 + 32, bs, bl, tb, a.mask_words, mrb);
     }
-    mbar_wait(&full[st], (c / NS) & 1);
+    mbar_wait(&full[st], (j / NS) & 1);
     const uint32_t kb = smem_u32(sk + st * k_bytes), vb_ = smem_u32(sv + st * v_bytes);
     float s[8][4];
 #pragma unroll
@@ -319,6 +324,59 @@ __global__ void __launch_bounds__(32 * (1 + kMaxWarps), 1)
       mb = nb;
     }
   }
+  // Cross-CTA key splits: publish this CTA's (O, m, l); the last of the group's CTAs merges all of
+  // them in fixed split order (deterministic whichever CTA arrives last).
+  if (a.kvsplit > 1) {
+    constexpr int NV = HD / 8 * 4 + 4;
+    const size_t grp = (static_cast<size_t>(r) * a.Hkv + kvh) * a.row_tiles + rt;
+    const size_t gstride = static_cast<size_t>(nw) * NV * 32;
+    float* mine = a.part + (grp * a.kvsplit + ks2) * gstride + static_cast<size_t>(rw) * NV * 32 + lane;
+#pragma unroll
+    for (int n = 0; n < HD / 8; ++n)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) __stcg(mine + (n * 4 + e) * 32, o[n][e]);
+    __stcg(mine + (NV - 4) * 32, ma);
+    __stcg(mine + (NV - 3) * 32, mb);
+    __stcg(mine + (NV - 2) * 32, la);
+    __stcg(mine + (NV - 1) * 32, lb);
+    __threadfence();
+    asm volatile("bar.sync 2, %0;" ::"r"(32 * nw) : "memory");
+    __shared__ int last_s;
+    if (rw == 0 && lane == 0) {
+      const unsigned old = atomicAdd(a.ctr + grp, 1u);
+      last_s = ((old + 1u) % static_cast<unsigned>(a.kvsplit)) == 0u;
+    }
+    asm volatile("bar.sync 2, %0;" ::"r"(32 * nw) : "memory");
+    if (!last_s) return;
+    __threadfence();
+    const float* base0 = a.part + grp * a.kvsplit * gstride + static_cast<size_t>(rw) * NV * 32 + lane;
+    ma = __ldcg(base0 + (NV - 4) * 32);
+    mb = __ldcg(base0 + (NV - 3) * 32);
+    la = __ldcg(base0 + (NV - 2) * 32);
+    lb = __ldcg(base0 + (NV - 1) * 32);
+#pragma unroll
+    for (int n = 0; n < HD / 8; ++n)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) o[n][e] = __ldcg(base0 + (n * 4 + e) * 32);
+    for (int k2 = 1; k2 < a.kvsplit; ++k2) {
+      const float* th = base0 + k2 * gstride;
+      const float m2a = __ldcg(th + (NV - 4) * 32), m2b = __ldcg(th + (NV - 3) * 32);
+      const float na = fmaxf(ma, m2a), nb = fmaxf(mb, m2b);
+      const float f1a = na == -INFINITY ? 0.f : exp2f(ma - na), f2a = na == -INFINITY ? 0.f : exp2f(m2a - na);
+      const float f1b = nb == -INFINITY ? 0.f : exp2f(mb - nb), f2b = nb == -INFINITY ? 0.f : exp2f(m2b - nb);
+#pragma unroll
+      for (int n = 0; n < HD / 8; ++n) {
+        o[n][0] = o[n][0] * f1a + __ldcg(th + (n * 4 + 0) * 32) * f2a;
+        o[n][1] = o[n][1] * f1a + __ldcg(th + (n * 4 + 1) * 32) * f2a;
+        o[n][2] = o[n][2] * f1b + __ldcg(th + (n * 4 + 2) * 32) * f2b;
+        o[n][3] = o[n][3] * f1b + __ldcg(th + (n * 4 + 3) * 32) * f2b;
+      }
+      la = la * f1a + __ldcg(th + (NV - 2) * 32) * f2a;
+      lb = lb * f1b + __ldcg(th + (NV - 1) * 32) * f2b;
+      ma = na;
+      mb = nb;
+    }
+  }
   // O / l -> bf16 attn[m][head][hd]
   const float ia = la > 0.f ? 1.f / la : 0.f, ib = lb > 0.f ? 1.f / lb : 0.f;
   const int ha = kvh * a.Gh + ra % a.Gh, hb = kvh * a.Gh + rb % a.Gh;
@@ -368,13 +426,22 @@ extern "C" {
 
 int ygg_prepare_attn_dec(void) {
   for (auto fn : {attn_dec_kernel<64>, attn_dec_kernel<128>}) {
-    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
     if (e != cudaSuccess) return ygg_fail(YGG_ERR_CUDA, "decode attention attribute: %s", cudaGetErrorString(e));
   }
   return YGG_OK;
 }
 
 size_t ygg_attn_dec_plan_size(void) { return sizeof(Plan) + 64; }
+
+size_t ygg_attn_dec_workspace_size(const void* plan) {
+  const Plan* p = plan_of(plan);
+  if (!p) return 0;
+  const size_t groups = static_cast<size_t>(p->B) * p->Hkv * p->row_tiles;
+  const size_t nv = static_cast<size_t>(p->hd) / 8 * 4 + 4;
+  const size_t part = groups * p->kvsplit * ((p->rows + 15) / 16) * nv * 32 * sizeof(float);
+  return ((part + 255) / 256) * 256 + groups * sizeof(unsigned) + 256;
+}
 
 int ygg_attn_dec_plan_init(void* plan, const void* q, const void* cache_layer, int B, int T, int Hq, int Hkv, int hd,
                            int S) {
@@ -402,6 +469,15 @@ int ygg_attn_dec_plan_init(void* plan, const void* q, const void* cache_layer, i
   if (hd == 128 && p->ksplit > 2) p->ksplit = 2;  // register budget of the 128-wide accumulators
   p->warps = nw * p->ksplit;
   p->stages = hd == 64 ? 8 : 5;
+  // Cross-CTA key splits so the grid covers the SMs (merge by the last CTA of each group).
+  {
+    int sms = 148, dev = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int groups = Hkv * B * p->row_tiles;
+    int kv = sms / groups;
+    if (const char* e = getenv("YGG_ATTN_DEC_KVSPLIT")) kv = atoi(e);
+    p->kvsplit = kv < 1 ? 1 : (kv > 8 ? 8 : kv);
+  }
   const size_t merge = static_cast<size_t>(p->warps) * (hd / 8 * 4 + 4) * 32 * 4;
   const size_t ring = static_cast<size_t>(p->stages) * 2 * (kKC * hd * 2);
   p->smem = 1024 + 64 * hd * 2 + (ring > merge ? ring : merge) + (2 * p->stages + 2) * 8;
@@ -428,7 +504,7 @@ int ygg_attn_dec_plan_init(void* plan, const void* q, const void* cache_layer, i
 }
 
 int ygg_attn_dec_run(const void* plan, const int32_t* blk_start, const int32_t* blk_len, const uint32_t* qmask,
-                     int mask_words, float scale, void* out, ygg_stream_t stream) {
+                     int mask_words, float scale, void* out, void* workspace, ygg_stream_t stream) {
   const Plan* p = plan_of(plan);
   YGG_CHECK_ARG(p != nullptr, "invalid decode-attention plan");
   YGG_CHECK_ARG(blk_start && blk_len && out, "null pointer");
@@ -446,13 +522,23 @@ int ygg_attn_dec_run(const void* plan, const int32_t* blk_start, const int32_t* 
   a.ksplit = p->ksplit;
   a.stages = p->stages;
   a.tpt = p->tpt;
+  a.kvsplit = p->kvsplit;
+  a.row_tiles = p->row_tiles;
+  YGG_CHECK_ARG(p->kvsplit == 1 || workspace != nullptr, "decode attention with key splits needs a workspace");
+  {
+    const size_t groups = static_cast<size_t>(p->B) * p->Hkv * p->row_tiles;
+    const size_t nv = static_cast<size_t>(p->hd) / 8 * 4 + 4;
+    const size_t part = groups * p->kvsplit * ((p->rows + 15) / 16) * nv * 32 * sizeof(float);
+    a.part = static_cast<float*>(workspace);
+    a.ctr = workspace ? reinterpret_cast<unsigned*>(static_cast<char*>(workspace) + ((part + 255) / 256) * 256) : nullptr;
+  }
   a.scale_log2 = scale * 1.4426950408889634f;
   a.blk_start = blk_start;
   a.blk_len = blk_len;
   a.qmask = qmask ? qmask : reinterpret_cast<const uint32_t*>(blk_start);  // never read when mask_words == 0
   a.out = static_cast<__nv_bfloat16*>(out);
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  const dim3 grid(p->Hkv, p->B, p->row_tiles), block(32 * (1 + p->warps));
+  const dim3 grid(p->Hkv, p->B, p->row_tiles * p->kvsplit), block(32 * (1 + p->warps));
   if (p->hd == 64)
     YGG_LAUNCH_PDL(attn_dec_kernel<64>, grid, block, p->smem, s, p->tq, p->tk, p->tv, a);
   else

@@ -41,6 +41,9 @@ from . import _lib as L
 from .model import ModelConfig, prepare_folded_, prepare_fused_, rope_table
 
 
+_KNOCKOUT = set(filter(None, os.environ.get("YGG_KO", "").split(",")))
+
+
 class GemmPlan:
     """Host-side plan (TMA tensor maps + stream-K segment table) for Y = X . W^T."""
 
@@ -178,9 +181,11 @@ class Forward:
         # faster there (measured same-box: verify 4.37 ms vs 4.41 ms with the decode kernel).
         self.ad_plans = None
         gh = cfg.n_heads // cfg.n_kv_heads
+        force_dec = os.environ.get("YGG_ATTN_DEC") == "2"  # A/B: decode attention for every tree pass
         if decode_attn is None:
             decode_attn = os.environ.get("YGG_ATTN_DEC", "1") != "0"
-        if decode_attn and act_dtype == torch.bfloat16 and mask_words <= L.MAX_MASK_WORDS and R * gh <= 64:
+        if (decode_attn and act_dtype == torch.bfloat16 and mask_words <= L.MAX_MASK_WORDS
+                and (R * gh <= 64 or (force_dec and mask_words > 0))):
             lib = L.lib()
             es = cache.element_size()
             self.ad_plans = []
@@ -189,6 +194,8 @@ class Forward:
                 L.check(lib.ygg_attn_dec_plan_init(mem, self.q.data_ptr(), cache.data_ptr() + li * self.layer_stride * es,
                                                    B, R, cfg.n_heads, cfg.n_kv_heads, cfg.head_dim, self.S))
                 self.ad_plans.append(mem)
+            self.ad_ws = torch.zeros(int(lib.ygg_attn_dec_workspace_size(self.ad_plans[0])) // 4 + 64,
+                                     dtype=torch.float32, device=dev)
         if self.fused:
             self._setup_fused()
         if self.mk:
@@ -251,7 +258,7 @@ class Forward:
         lib = L.lib()
         if self.ad_plans is not None:
             L.check(lib.ygg_attn_dec_run(self.ad_plans[li], self.blk_start.data_ptr(), self.blk_len.data_ptr(), qm,
-                                         self.mask_words, self.scale, self.attn.data_ptr(), s))
+                                         self.mask_words, self.scale, self.attn.data_ptr(), self.ad_ws.data_ptr(), s))
         else:
             L.check(lib.ygg_attention_tc(self.attn_plans[li].handle, self.blk_start.data_ptr(), self.blk_len.data_ptr(),
                                          qm, self.mask_words, self.scale, self.attn_part.data_ptr(),
@@ -463,34 +470,45 @@ class Forward:
         ws = self.ws.data_ptr()
         nl = len(self.plans)
         qm = self.qmask.data_ptr() if self.mask_words > 0 else None
+        ko = _KNOCKOUT  # A/B timing only (YGG_KO): launches left out, results invalid
         for li, (p, lw) in enumerate(zip(self.plans, w["layers"])):
             cache_l = self.cache.data_ptr() + li * self.layer_stride * self.cache.element_size()
-            chk(lib.ygg_gemm_run(p["qkv"].handle, ws, s))
-            chk(lib.ygg_epi_qkv_rope(p["qkv"].handle, ws, cfg.n_heads, cfg.n_kv_heads, cfg.head_dim,
-                                     cfg.rope_theta, self.pos.data_ptr(), self.slot.data_ptr(),
-                                     self.req.data_ptr(), self.q.data_ptr(), cache_l, self.S, self.act,
-                                     self.rope_cs.data_ptr(), s))
+            if "gemm" not in ko:
+                chk(lib.ygg_gemm_run(p["qkv"].handle, ws, s))
+            if "epi" not in ko:
+                chk(lib.ygg_epi_qkv_rope(p["qkv"].handle, ws, cfg.n_heads, cfg.n_kv_heads, cfg.head_dim,
+                                         cfg.rope_theta, self.pos.data_ptr(), self.slot.data_ptr(),
+                                         self.req.data_ptr(), self.q.data_ptr(), cache_l, self.S, self.act,
+                                         self.rope_cs.data_ptr(), s))
             stamp()
-            if self.attn_plans is not None:
+            if "attn" in ko:
+                pass
+            elif self.attn_plans is not None:
                 self._attend(li, qm, s)
             else:
                 chk(lib.ygg_attention(self.q.data_ptr(), cache_l, self.act, M, self.B, cfg.n_heads, cfg.n_kv_heads,
                                       cfg.head_dim, self.S, self.blk_start.data_ptr(), self.blk_len.data_ptr(),
                                       qm, self.mask_words, self.scale, self.attn.data_ptr(), s))
             stamp()
-            chk(lib.ygg_gemm_run(p["o"].handle, ws, s))
-            chk(lib.ygg_epi_residual_norm(p["o"].handle, ws, self.resid.data_ptr(), lw["mlp_norm"].data_ptr(),
-                                          cfg.norm_eps, self.xn.data_ptr(), self.act, s))
+            if "gemm" not in ko:
+                chk(lib.ygg_gemm_run(p["o"].handle, ws, s))
+            if "epi" not in ko:
+                chk(lib.ygg_epi_residual_norm(p["o"].handle, ws, self.resid.data_ptr(), lw["mlp_norm"].data_ptr(),
+                                              cfg.norm_eps, self.xn.data_ptr(), self.act, s))
             stamp()
-            chk(lib.ygg_gemm_run(p["gu"].handle, ws, s))
-            chk(lib.ygg_epi_swiglu(p["gu"].handle, ws, self.mlp.data_ptr(), self.act, s))
+            if "gemm" not in ko:
+                chk(lib.ygg_gemm_run(p["gu"].handle, ws, s))
+            if "epi" not in ko:
+                chk(lib.ygg_epi_swiglu(p["gu"].handle, ws, self.mlp.data_ptr(), self.act, s))
             stamp()
-            chk(lib.ygg_gemm_run(p["down"].handle, ws, s))
+            if "gemm" not in ko:
+                chk(lib.ygg_gemm_run(p["down"].handle, ws, s))
             nxt = w["layers"][li + 1]["attn_norm"] if li + 1 < nl else w["final_norm"]
-            chk(lib.ygg_epi_residual_norm(p["down"].handle, ws, self.resid.data_ptr(), nxt.data_ptr(),
-                                          cfg.norm_eps, self.xn.data_ptr(), self.act, s))
+            if "epi" not in ko:
+                chk(lib.ygg_epi_residual_norm(p["down"].handle, ws, self.resid.data_ptr(), nxt.data_ptr(),
+                                              cfg.norm_eps, self.xn.data_ptr(), self.act, s))
             stamp()
-        if self.lm_plan is not None:
+        if self.lm_plan is not None and "lm" not in ko:
             chk(lib.ygg_gemm_run(self.lm_plan.handle, ws, s))
             chk(lib.ygg_epi_store(self.lm_plan.handle, ws, self.logits.data_ptr(), L.YGG_F32, cfg.vocab, s))
             stamp()

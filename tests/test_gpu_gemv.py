@@ -133,8 +133,10 @@ def test_decode_attention_vs_fp32(hd, Hq, Hkv, B, T, P, mw, cuda):
     mem = C.create_string_buffer(int(lib.ygg_attn_dec_plan_size()))
     L.check(lib.ygg_attn_dec_plan_init(mem, q.data_ptr(), cache.data_ptr(), B, T, Hq, Hkv, hd, S))
     scale = 1.0 / math.sqrt(hd)
-    L.check(lib.ygg_attn_dec_run(mem, bs.data_ptr(), bl.data_ptr(), qmask.data_ptr() if mw else None, mw, scale,
-                                 out.data_ptr(), L.stream_ptr()))
+    ws = torch.zeros(int(lib.ygg_attn_dec_workspace_size(mem)) // 4 + 64, dtype=torch.float32, device=cuda)
+    for _ in range(2):  # twice: the arrival counters are monotonic across launches
+        L.check(lib.ygg_attn_dec_run(mem, bs.data_ptr(), bl.data_ptr(), qmask.data_ptr() if mw else None, mw, scale,
+                                     out.data_ptr(), ws.data_ptr(), L.stream_ptr()))
     torch.cuda.synchronize()
     K = cache[:, 0].double().cpu()                         # [B, Hkv, S, hd]
     Vt = cache[:, 1].double().cpu().reshape(B, Hkv, hd, S)  # V^T rows

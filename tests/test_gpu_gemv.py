@@ -106,7 +106,8 @@ def test_gemv_plan_rejects_bad_shapes(cuda):
                                                 (64, 8, 2, 1, 1, 77, 0), (128, 8, 2, 1, 5, 64, 0),
                                                 (128, 32, 8, 1, 50, 512, 2), (64, 32, 8, 2, 33, 90, 2),
                                                 (128, 32, 8, 1, 40, 64, 0)])
-def test_decode_attention_vs_fp32(hd, Hq, Hkv, B, T, P, mw, cuda):
+@pytest.mark.parametrize("kvsplit", ["1", "3"])
+def test_decode_attention_vs_fp32(hd, Hq, Hkv, B, T, P, mw, kvsplit, cuda, monkeypatch):
     """ygg_attn_dec_run vs a float64 softmax(QK^T/sqrt(hd)) V over the visible keys (prefix + tree /
     causal block).  bf16 operands; tolerance 2e-2 of the output scale (bf16 P and output rounding)."""
     import ctypes as C
@@ -114,6 +115,7 @@ def test_decode_attention_vs_fp32(hd, Hq, Hkv, B, T, P, mw, cuda):
 
     from paper_2512_23858_b200 import _lib as L
 
+    monkeypatch.setenv("YGG_ATTN_DEC_KVSPLIT", kvsplit)  # read at plan time
     lib = L.lib()
     S = ((P + T + 63) // 64) * 64
     g = torch.Generator(device="cuda").manual_seed(hd + T)
@@ -134,7 +136,7 @@ def test_decode_attention_vs_fp32(hd, Hq, Hkv, B, T, P, mw, cuda):
     L.check(lib.ygg_attn_dec_plan_init(mem, q.data_ptr(), cache.data_ptr(), B, T, Hq, Hkv, hd, S))
     scale = 1.0 / math.sqrt(hd)
     ws = torch.zeros(int(lib.ygg_attn_dec_workspace_size(mem)) // 4 + 64, dtype=torch.float32, device=cuda)
-    for _ in range(2):  # twice: the arrival counters are monotonic across launches
+    for _ in range(2):  # twice: the arrival counters (key-split mode) are monotonic across launches
         L.check(lib.ygg_attn_dec_run(mem, bs.data_ptr(), bl.data_ptr(), qmask.data_ptr() if mw else None, mw, scale,
                                      out.data_ptr(), ws.data_ptr(), L.stream_ptr()))
     torch.cuda.synchronize()

@@ -271,14 +271,21 @@ class Forward:
         chk(lib.ygg_embed_fused(self.w["embed"].data_ptr(), cfg.vocab, cfg.d_model, self.tokens.data_ptr(), self.M,
                                 self.resid.data_ptr(), self.xn.data_ptr(), self.ss_e.data_ptr(), s))
         qm = self.qmask.data_ptr() if self.mask_words > 0 else None
+        ko = _KNOCKOUT  # A/B timing only (YGG_KO)
         for li, ops in enumerate(self.gv):
             (pq, eq), (po, eo), (pg, eg), (pd, ed) = ops
-            chk(lib.ygg_gemv_run(pq, C.byref(eq), s))
-            self._attend(li, qm, s)
-            chk(lib.ygg_gemv_run(po, C.byref(eo), s))
-            chk(lib.ygg_gemv_run(pg, C.byref(eg), s))
-            chk(lib.ygg_gemv_run(pd, C.byref(ed), s))
-        chk(lib.ygg_gemv_run(self.gv_lm[0], C.byref(self.gv_lm[1]), s))
+            if "qkv" not in ko:
+                chk(lib.ygg_gemv_run(pq, C.byref(eq), s))
+            if "attn" not in ko:
+                self._attend(li, qm, s)
+            if "o" not in ko:
+                chk(lib.ygg_gemv_run(po, C.byref(eo), s))
+            if "gu" not in ko:
+                chk(lib.ygg_gemv_run(pg, C.byref(eg), s))
+            if "down" not in ko:
+                chk(lib.ygg_gemv_run(pd, C.byref(ed), s))
+        if "lm" not in ko:
+            chk(lib.ygg_gemv_run(self.gv_lm[0], C.byref(self.gv_lm[1]), s))
 
     # ------------------------------------------------------------------
     def _setup_mk(self) -> None:

@@ -206,3 +206,23 @@ def test_sample_mode_first_token_distribution(cuda):
     chi2 = float((((obs - exp) ** 2) / exp)[keep].sum())
     # 99.9% quantile of chi-square with <= 8 degrees of freedom is 26.1
     assert chi2 < 26.1, (chi2, obs.tolist(), exp.round(1).tolist())
+
+
+@pytest.mark.parametrize("B,W", [(2, 8), (1, 16), (3, 8)])
+def test_bf16_spec_equals_ar_draft_paths(B, W, cuda):
+    """Lossless-greedy identity across the draft kernel families: B*R <= 16 rows run the row-block
+    GEMV with two token tiles (B=2, W=8 and B=1, W=16: 16 rows) and B=3, W=8 (24 rows) the
+    stream-K GEMM; the verify and the AR oracle always run the stream-K GEMM + split-KV attention."""
+    from paper_2512_23858_b200.engine import ARDecoder, SpecDecoder, StepShape
+    from paper_2512_23858_b200.model import weights_to
+
+    tc, dc, tw, dw = _models(torch.float32, True)
+    twb, dwb = weights_to(tw, cuda, torch.bfloat16), weights_to(dw, cuda, torch.bfloat16)
+    prompts = torch.stack([_prompt(tc.vocab, 32, 2000 + b) for b in range(B)])
+    n_tok = 48
+    ar = ARDecoder(tc, twb, batch=B, max_seq=320).generate(prompts, n_tok)
+    sd = SpecDecoder(tc, twb, dc, dwb, StepShape(3, W, 8, 64), batch=B, max_seq=320, profiles=_profiles())
+    assert sd.draft.gemv == (B * max(W, 2) <= 16)
+    got, steps = sd.generate(prompts, n_tok)
+    assert got == ar
+    assert steps < n_tok

@@ -598,6 +598,42 @@ YGG_DEV void epi_values(const EpiGeom& g, const float* __restrict__ ws, int m, i
   }
 }
 
+// Partial sums of two V-wide feature runs [n1, n1+V) and [n2, n2+V) of row m (possibly different
+// tiles), both runs' loads in flight together; each run summed in its own segment order.
+template <int V>
+YGG_DEV void epi_values2(const EpiGeom& g, const float* __restrict__ ws, int m, int n1, int n2, float* v1, float* v2) {
+  const int t1 = (n1 / kBM) * g.m_tiles + m / g.BN, t2 = (n2 / kBM) * g.m_tiles + m / g.BN;
+  const int a0 = __ldg(g.seg_first + t1), a1 = __ldg(g.seg_first + t1 + 1);
+  const int b0 = __ldg(g.seg_first + t2), b1 = __ldg(g.seg_first + t2 + 1);
+  const size_t row = static_cast<size_t>(m % g.BN) * kBM;
+  const float* p1 = ws + row + (n1 % kBM);
+  const float* p2 = ws + row + (n2 % kBM);
+  const size_t seg_stride = static_cast<size_t>(g.BN) * kBM;
+#pragma unroll
+  for (int i = 0; i < V; ++i) v1[i] = v2[i] = 0.f;
+  const int na = a1 - a0, nb = b1 - b0, n = na > nb ? na : nb;
+  for (int j = 0; j < n; j += 4) {
+    float4 x[4][2][V / 4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const float4* q1 = reinterpret_cast<const float4*>(p1 + (a0 + j + k) * seg_stride);
+      const float4* q2 = reinterpret_cast<const float4*>(p2 + (b0 + j + k) * seg_stride);
+#pragma unroll
+      for (int i = 0; i < V / 4; ++i) {
+        x[k][0][i] = (j + k < na) ? __ldg(q1 + i) : make_float4(0.f, 0.f, 0.f, 0.f);
+        x[k][1][i] = (j + k < nb) ? __ldg(q2 + i) : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+#pragma unroll
+      for (int i = 0; i < V / 4; ++i) {
+        v1[4 * i] += x[k][0][i].x; v1[4 * i + 1] += x[k][0][i].y; v1[4 * i + 2] += x[k][0][i].z; v1[4 * i + 3] += x[k][0][i].w;
+        v2[4 * i] += x[k][1][i].x; v2[4 * i + 1] += x[k][1][i].y; v2[4 * i + 2] += x[k][1][i].z; v2[4 * i + 3] += x[k][1][i].w;
+      }
+  }
+}
+
 template <typename T>
 YGG_DEV void store8(T* dst, const float* v);
 template <>
@@ -666,28 +702,27 @@ YGG_DEV float ld_dsmem_f32(const float* local, uint32_t rank) {
   return v;
 }
 
-// Residual add + RMSNorm over a thread-block cluster: the row's 1024-feature slices live in the
-// cluster's CTAs, whose sums of squares are combined through distributed shared memory in rank
-// order (deterministic), so the whole row is normalised in one launch with N/8 threads.
+// Residual add + RMSNorm of one row per CTA (N/8 threads, 8 features each): every global load of the
+// row (partials, residual, norm gains) is issued before any use, and the sum of squares is one
+// block reduction in fixed warp order (deterministic).
 template <typename ActT>
-__global__ void __launch_bounds__(kEpiThreads) epi_residual_norm_kernel(EpiGeom g, const float* __restrict__ ws,
-                                                                        float* __restrict__ resid,
-                                                                        const ActT* __restrict__ norm_w, float eps,
-                                                                        ActT* __restrict__ xn) {
+__global__ void __launch_bounds__(1024) epi_residual_norm_kernel(EpiGeom g, const float* __restrict__ ws,
+                                                                 float* __restrict__ resid,
+                                                                 const ActT* __restrict__ norm_w, float eps,
+                                                                 ActT* __restrict__ xn) {
   pdl_wait();
   pdl_launch_dependents();
-  __shared__ float red[kEpiThreads / 32];
-  __shared__ float cta_ss;
-  const int m = blockIdx.y;
-  const int n = (blockIdx.x * blockDim.x + threadIdx.x) * 8;
+  __shared__ float red[32];
+  const int m = blockIdx.x;
+  const int n = threadIdx.x * 8;
   const bool live = n < g.N;
-  float h[8];
+  float h[8], w[8], v[8];
   float ss = 0.f;
   if (live) {
-    float v[8];
-    epi_values<8>(g, ws, m, n, v);
     float* hp = resid + static_cast<size_t>(m) * g.N + n;
     load8<float>(hp, h);
+    load8<ActT>(norm_w + n, w);
+    epi_values<8>(g, ws, m, n, v);
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
       h[i] += v[i];
@@ -696,21 +731,13 @@ __global__ void __launch_bounds__(kEpiThreads) epi_residual_norm_kernel(EpiGeom 
     store8<float>(hp, h);
   }
   ss = warp_sum(ss);
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) red[warp] = ss;
   __syncthreads();
-  if (threadIdx.x == 0) {
-    float t = 0.f;
-    for (int w = 0; w < (int)(blockDim.x / 32); ++w) t += red[w];
-    cta_ss = t;
-  }
-  cluster_sync_all();
   float total = 0.f;
-  for (uint32_t r = 0; r < gridDim.x; ++r) total += ld_dsmem_f32(&cta_ss, r);
-  cluster_sync_all();  // keep every CTA's smem alive until all ranks have read it
+  for (int k = 0; k < static_cast<int>(blockDim.x >> 5); ++k) total += red[k];
   const float rs = rsqrtf(total / static_cast<float>(g.N) + eps);
   if (live) {
-    float w[8];
-    load8<ActT>(norm_w + n, w);
 #pragma unroll
     for (int i = 0; i < 8; ++i) h[i] = h[i] * rs * w[i];
     store8<ActT>(xn + static_cast<size_t>(m) * g.N + n, h);
@@ -727,8 +754,7 @@ __global__ void __launch_bounds__(kEpiThreads) epi_swiglu_kernel(EpiGeom g, cons
   const int f = (blockIdx.x * blockDim.x + threadIdx.x) * 8;
   if (f >= F) return;
   float gate[8], up[8], o[8];
-  epi_values<8>(g, ws, m, f, gate);
-  epi_values<8>(g, ws, m, F + f, up);
+  epi_values2<8>(g, ws, m, f, F + f, gate, up);
 #pragma unroll
   for (int i = 0; i < 8; ++i) o[i] = gate[i] / (1.f + expf(-gate[i])) * up[i];
   store8<ActT>(out + static_cast<size_t>(m) * F + f, o);
@@ -757,16 +783,18 @@ __global__ void __launch_bounds__(256) epi_qkv_rope_kernel(EpiGeom g, const floa
   const int i0 = (it % per_head) * 4;
   const int n0 = head * hd;
   float x1[4], x2[4], cs[4], sn[4];
-  epi_values<4>(g, ws, m, n0 + i0, x1);
-  epi_values<4>(g, ws, m, n0 + i0 + half, x2);
-  if (head < Hq + Hkv) {
-    if (rope_cs) {
+  const bool rot = head < Hq + Hkv;
+  if (rot && rope_cs) {  // table loads first: they overlap the partial-sum loads below
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const float2 t = rope_cs[static_cast<size_t>(pm) * half + i0 + j];
-        cs[j] = t.x;
-        sn[j] = t.y;
-      }
+    for (int j = 0; j < 4; ++j) {
+      const float2 t = __ldg(rope_cs + static_cast<size_t>(pm) * half + i0 + j);
+      cs[j] = t.x;
+      sn[j] = t.y;
+    }
+  }
+  epi_values2<4>(g, ws, m, n0 + i0, n0 + i0 + half, x1, x2);
+  if (rot) {
+    if (rope_cs) {
     } else {
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
@@ -1093,16 +1121,16 @@ int ygg_epi_residual_norm(const void* plan, const float* ws, float* resid, const
                           int act_dtype, ygg_stream_t stream) {
   const GemmPlan* g = plan_of(plan);
   YGG_CHECK_ARG(g && ws && resid && norm_w && xn_out, "invalid arguments");
-  const int cx = (g->N + 1023) / 1024;
-  YGG_CHECK_ARG(cx <= 8, "row wider than one 8-CTA cluster (8192 features)");
+  YGG_CHECK_ARG(g->N % 8 == 0 && g->N / 8 <= 1024, "row wider than 8192 features");
   EpiGeom geo = geom_of(g);
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const int threads = ((g->N / 8 + 31) / 32) * 32;
   if (act_dtype == YGG_F32)
-    YGG_LAUNCH_PDL_CLUSTER(epi_residual_norm_kernel<float>, dim3(cx, g->M), dim3(kEpiThreads), cx, s, geo, ws, resid,
-                           static_cast<const float*>(norm_w), eps, static_cast<float*>(xn_out));
+    YGG_LAUNCH_PDL(epi_residual_norm_kernel<float>, dim3(g->M), dim3(threads), 0, s, geo, ws, resid,
+                   static_cast<const float*>(norm_w), eps, static_cast<float*>(xn_out));
   else
-    YGG_LAUNCH_PDL_CLUSTER(epi_residual_norm_kernel<__nv_bfloat16>, dim3(cx, g->M), dim3(kEpiThreads), cx, s, geo, ws,
-                           resid, static_cast<const __nv_bfloat16*>(norm_w), eps, static_cast<__nv_bfloat16*>(xn_out));
+    YGG_LAUNCH_PDL(epi_residual_norm_kernel<__nv_bfloat16>, dim3(g->M), dim3(threads), 0, s, geo, ws, resid,
+                   static_cast<const __nv_bfloat16*>(norm_w), eps, static_cast<__nv_bfloat16*>(xn_out));
   return YGG_OK;
 }
 

@@ -482,7 +482,7 @@ class Forward:
             cache_l = self.cache.data_ptr() + li * self.layer_stride * self.cache.element_size()
             if "gemm" not in ko:
                 chk(lib.ygg_gemm_run(p["qkv"].handle, ws, s))
-            if "epi" not in ko:
+            if "epi" not in ko and "epi_qkv" not in ko:
                 chk(lib.ygg_epi_qkv_rope(p["qkv"].handle, ws, cfg.n_heads, cfg.n_kv_heads, cfg.head_dim,
                                          cfg.rope_theta, self.pos.data_ptr(), self.slot.data_ptr(),
                                          self.req.data_ptr(), self.q.data_ptr(), cache_l, self.S, self.act,
@@ -499,19 +499,19 @@ class Forward:
             stamp()
             if "gemm" not in ko:
                 chk(lib.ygg_gemm_run(p["o"].handle, ws, s))
-            if "epi" not in ko:
+            if "epi" not in ko and "epi_resid" not in ko:
                 chk(lib.ygg_epi_residual_norm(p["o"].handle, ws, self.resid.data_ptr(), lw["mlp_norm"].data_ptr(),
                                               cfg.norm_eps, self.xn.data_ptr(), self.act, s))
             stamp()
             if "gemm" not in ko:
                 chk(lib.ygg_gemm_run(p["gu"].handle, ws, s))
-            if "epi" not in ko:
+            if "epi" not in ko and "epi_swiglu" not in ko:
                 chk(lib.ygg_epi_swiglu(p["gu"].handle, ws, self.mlp.data_ptr(), self.act, s))
             stamp()
             if "gemm" not in ko:
                 chk(lib.ygg_gemm_run(p["down"].handle, ws, s))
             nxt = w["layers"][li + 1]["attn_norm"] if li + 1 < nl else w["final_norm"]
-            if "epi" not in ko:
+            if "epi" not in ko and "epi_resid" not in ko:
                 chk(lib.ygg_epi_residual_norm(p["down"].handle, ws, self.resid.data_ptr(), nxt.data_ptr(),
                                               cfg.norm_eps, self.xn.data_ptr(), self.act, s))
             stamp()

@@ -469,6 +469,7 @@ int ygg_attn_dec_plan_init(void* plan, const void* q, const void* cache_layer, i
   if (hd == 128 && p->ksplit > 2) p->ksplit = 2;  // register budget of the 128-wide accumulators
   p->warps = nw * p->ksplit;
   p->stages = hd == 64 ? 8 : 5;
+  if (const char* e = getenv("YGG_ATTN_DEC_STAGES")) p->stages = atoi(e) < 2 ? 2 : (atoi(e) > 8 ? 8 : atoi(e));
   // Cross-CTA key splits (merge by the last CTA of each group): off by default — same-box cfg2
   // draft pass 0.712 ms (1), 0.718 (2), 0.713 (4), 0.734 (8); verify (forced) 3.96 / 3.95 / 4.12.
   {

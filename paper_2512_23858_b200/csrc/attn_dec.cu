@@ -41,6 +41,7 @@ struct Plan {
 struct Args {
   int T, Hq, Hkv, hd, S, Gh, rows, mask_words, ksplit, stages, tpt;  // rows = tpt * Gh (one row tile)
   int kvsplit, row_tiles;  // CTAs per (kv head, request, row tile) splitting the key chunks
+  int ring_bytes;          // max(key/value ring, split-merge scratch): the barriers sit after it
   float* part;             // [B][Hkv][row_tiles][kvsplit][warps][NV][32] cross-CTA partials
   unsigned* ctr;           // [B][Hkv][row_tiles] arrival counters (monotonic)
   float scale_log2;
@@ -126,7 +127,7 @@ __global__ void __launch_bounds__(32 * (1 + kMaxWarps), 1)
   unsigned char* sq = base;
   unsigned char* sk = sq + q_bytes;
   unsigned char* sv = sk + NS * k_bytes;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sv + NS * v_bytes);
+  uint64_t* full = reinterpret_cast<uint64_t*>(sk + a.ring_bytes);
   uint64_t* empty = full + NS;
   uint64_t* qbar = empty + NS;
   const int kvh = blockIdx.x, r = blockIdx.y;
@@ -468,8 +469,15 @@ int ygg_attn_dec_plan_init(void* plan, const void* q, const void* cache_layer, i
   p->ksplit = kMaxWarps / nw;            // split the key chunks over the remaining warps
   if (hd == 128 && p->ksplit > 2) p->ksplit = 2;  // register budget of the 128-wide accumulators
   p->warps = nw * p->ksplit;
-  p->stages = hd == 64 ? 8 : 5;
+  p->stages = hd == 64 ? 8 : 4;
   if (const char* e = getenv("YGG_ATTN_DEC_STAGES")) p->stages = atoi(e) < 2 ? 2 : (atoi(e) > 8 ? 8 : atoi(e));
+  // Every stage must always feed the same key-split group (chunk j -> stage j % stages, group
+  // j % ksplit): otherwise a group can wait on a stage two phases ahead and the parity wait would pass
+  // on a stale phase.  So stages is a multiple of ksplit.
+  const int max_st = static_cast<int>((200 * 1024 - 64 * hd * 2) / (2 * kKC * hd * 2));  // smem budget
+  if (p->stages > max_st) p->stages = max_st;
+  p->stages = (p->stages / p->ksplit) * p->ksplit;
+  if (p->stages < p->ksplit) p->stages = p->ksplit;
   // Cross-CTA key splits (merge by the last CTA of each group): off by default — same-box cfg2
   // draft pass 0.712 ms (1), 0.718 (2), 0.713 (4), 0.734 (8); verify (forced) 3.96 / 3.95 / 4.12.
   {
@@ -479,7 +487,7 @@ int ygg_attn_dec_plan_init(void* plan, const void* q, const void* cache_layer, i
   }
   const size_t merge = static_cast<size_t>(p->warps) * (hd / 8 * 4 + 4) * 32 * 4;
   const size_t ring = static_cast<size_t>(p->stages) * 2 * (kKC * hd * 2);
-  p->smem = 1024 + 64 * hd * 2 + (ring > merge ? ring : merge) + (2 * p->stages + 2) * 8;
+  p->smem = 1024 + 64 * hd * 2 + ((ring > merge ? ring : merge) + 15) / 16 * 16 + (2 * p->stages + 2) * 8;
   const int M = B * T;
   {  // q [M][Hq][hd]: box {64, Gh, T} -> rows (token, head-in-group); 64 rows of smem reserved
     cuuint64_t dims[3] = {static_cast<cuuint64_t>(hd), static_cast<cuuint64_t>(Hq), static_cast<cuuint64_t>(M)};
@@ -523,6 +531,11 @@ int ygg_attn_dec_run(const void* plan, const int32_t* blk_start, const int32_t* 
   a.tpt = p->tpt;
   a.kvsplit = p->kvsplit;
   a.row_tiles = p->row_tiles;
+  {
+    const size_t merge = static_cast<size_t>(p->warps) * (p->hd / 8 * 4 + 4) * 32 * 4;
+    const size_t ring = static_cast<size_t>(p->stages) * 2 * (kKC * p->hd * 2);
+    a.ring_bytes = static_cast<int>(((ring > merge ? ring : merge) + 15) / 16 * 16);
+  }
   YGG_CHECK_ARG(p->kvsplit == 1 || workspace != nullptr, "decode attention with key splits needs a workspace");
   {
     const size_t groups = static_cast<size_t>(p->B) * p->Hkv * p->row_tiles;

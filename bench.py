@@ -37,6 +37,12 @@ WORKLOADS = {
                                   "max_verify 64, greedy, 1 request/GPU, 512-token prompt"),
     "cfg1": dict(target="tiny-target", draft="tiny-draft", depth=4, width=4, k=8, max_verify=64, batch=1,
                  prompt=32, desc="cfg1: tiny 4L d256 target + 1L draft, EGT D4 W4 k8, greedy, batch 1"),
+    # cfg3: the cfg2 pair, latency-aware choice over 12 EGT shapes from an on-device profiled table.
+    "cfg3": dict(target="llama3-8b", draft="llama3.2-1b", depth=6, width=8, k=8, max_verify=64, batch=1,
+                 prompt=512, sweep=[(d, w, v) for d in (4, 8, 16) for w in (4, 8) for v in (16, 64)],
+                 desc="cfg3: Llama-3-8B target + Llama-3.2-1B draft (bf16), latency-aware objective choosing "
+                      "(depth, width, verify-size) from an on-device profiled latency table, sweep of 12 EGT "
+                      "shapes, greedy, 1 request/GPU, 512-token prompt"),
     # cfg4: 16 requests sharded over the GPUs (16 / world per GPU), rejection sampling at T = 0.8.
     "cfg4": dict(target="llama3-8b", draft="llama3.2-1b", depth=6, width=8, k=8, max_verify=64, global_batch=16,
                  prompt=2048, gen=1024, mode="sample", temperature=0.8,
@@ -52,6 +58,7 @@ WORKLOADS = {
 COUPLING = {
     "cfg2": dict(rank=2048, logit_scale=16.0, head_noise=6.0, layer_gain=2.0),
     "cfg1": dict(rank=256, logit_scale=8.0, head_noise=2.0, layer_gain=2.0),
+    "cfg3": dict(rank=2048, logit_scale=16.0, head_noise=6.0, layer_gain=2.0),
     "cfg4": dict(rank=2048, logit_scale=16.0, head_noise=6.0, layer_gain=2.0),
     "cfg5": dict(rank=2048, logit_scale=16.0, head_noise=6.0, layer_gain=2.0),
 }
@@ -116,16 +123,19 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(rows)}
 
 
-def build_decoder(wl: dict, name: str, device, seed_offset: int = 0):
+def build_decoder(wl: dict, name: str, device, seed_offset: int = 0, weights=None, profiles=None):
     import torch
 
     from paper_2512_23858_b200.engine import SpecDecoder, StepShape
     from paper_2512_23858_b200.model import Coupling, init_weights, preset
 
     tc, dc = preset(wl["target"]), preset(wl["draft"])
-    cp = Coupling(**COUPLING[name])
-    tw = init_weights(tc, 0, torch.bfloat16, device, cp)
-    dw = init_weights(dc, 1, torch.bfloat16, device, cp)
+    if weights is None:
+        cp = Coupling(**COUPLING[name])
+        tw = init_weights(tc, 0, torch.bfloat16, device, cp)
+        dw = init_weights(dc, 1, torch.bfloat16, device, cp)
+    else:
+        tw, dw = weights
 
     class PP:
         class drafter:
@@ -139,9 +149,120 @@ def build_decoder(wl: dict, name: str, device, seed_offset: int = 0):
     shape = StepShape(wl["depth"], wl["width"], wl["k"], wl["max_verify"])
     max_seq = wl["prompt"] + wl.get("gen", 2048)  # room for the timed steps of up to D+2 tokens
     sd = SpecDecoder(tc, tw, dc, dw, shape, batch=wl["batch"], max_seq=max_seq, act_dtype=torch.bfloat16,
-                     profiles=PP, device=device, mode=wl.get("mode", GREEDY),
+                     profiles=profiles if profiles is not None else PP, device=device, mode=wl.get("mode", GREEDY),
                      temperature=wl.get("temperature", 1.0))
+    if weights is not None:
+        return sd, tc, dc
+    sd._bench_weights = (tw, dw)
     return sd, tc, dc
+
+
+def profile_latency(sd, draft_widths=(1, 2, 4, 8, 16), verify_widths=(1, 17, 33, 49, 65), reps=10):
+    """K8 on real models: graph-replayed forward latency of the draft at each width (rows of one EGT
+    level) and of the target at each verify width, as reference LatencyProfile breakpoints
+    (latency.py:34-82, width -> us).  Uses the decoder's weights and caches (contents irrelevant)."""
+    import torch
+
+    from paper_2512_23858_b200.forward import Forward
+
+    def time_fwd(cfg, w, cache, rows):
+        mw = max(1, (rows + 31) // 32)
+        f = Forward(cfg, w, cache, 1, rows, mw, torch.bfloat16)
+        f.blk_start.fill_(int(sd.seq.P[0]))
+        f.blk_len.fill_(rows)
+        f.pos.copy_(f.blk_start[0] + torch.arange(rows, dtype=torch.int32, device=cache.device))
+        f.slot.copy_(f.pos)
+        f.qmask.fill_(-1)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            f.run()
+        for _ in range(3):
+            g.replay()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(reps):
+            g.replay()
+        b.record()
+        torch.cuda.synchronize()
+        del g, f
+        return a.elapsed_time(b) * 1e3 / reps
+
+    def monotone(pts):  # the reference requires non-decreasing latencies (latency.py:34-65): running max
+        out, hi = [], 0.0
+        for w, us in pts:
+            hi = max(hi, us)
+            out.append((w, round(hi, 2)))
+        return tuple(out)
+
+    dbp = monotone([(w, time_fwd(sd.dc, sd.dw, sd.dcache, max(w, 2))) for w in draft_widths])
+    vbp = monotone([(w, time_fwd(sd.tc, sd.tw, sd.tcache, w)) for w in verify_widths])
+    return dbp, vbp
+
+
+def run_cfg3(args, device):
+    """cfg3: profile the draft / verify latency tables on the device (K8), load them into the device
+    table the prune objective reads (Eq.3, latency.py:154-161), then run each of the 12 EGT shapes
+    and report the objective's choice next to the measured best."""
+    import torch
+
+    from paper_2512_23858_b200.latency import LatencyProfile, latency_at
+
+    wl = dict(WORKLOADS["cfg3"])
+    peak, peak_kind, _ = _peaks()
+    base, tc, dc = build_decoder(wl, "cfg3", device)
+    prompts = prompts_for(wl, tc.vocab, 0)
+    base.prefill(prompts)
+    dbp, vbp = profile_latency(base)
+
+    class PP:
+        drafter = LatencyProfile(dbp, "drafter")
+        verifier = LatencyProfile(vbp, "verifier")
+
+    weights = base._bench_weights
+    del base
+    torch.cuda.empty_cache()
+    rows = []
+    for (D, W, V) in wl["sweep"]:
+        w2 = dict(wl, depth=D, width=W, max_verify=V)
+        sd, _, _ = build_decoder(w2, "cfg3", device, weights=weights, profiles=PP)
+        sd.prefill(prompts)
+        sd.capture()
+        for _ in range(args.warmup):
+            sd.step()
+        torch.cuda.synchronize()
+        gen0 = sd.seq.n_gen.clone()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(args.steps):
+            sd.step()
+        b.record()
+        torch.cuda.synchronize()
+        t = a.elapsed_time(b) * 1e-3
+        tokens = int((sd.seq.n_gen - gen0).sum())
+        # objective: Eq.3 speedup of the last step's pruned tree from the profiled table, and the
+        # predicted accepted tokens/s = expected AAL / (D T_d(W) + T_v(w_verify + 1) + T_d(2)) (pass 0)
+        exp_aal = float(sd.exp_aal[0])
+        wv = int(sd.w_verify[0])
+        pred_step_us = (D * latency_at(PP.drafter, max(W, 2)) + latency_at(PP.drafter, 2)
+                        + latency_at(PP.verifier, wv + 1))
+        rows.append({"depth": D, "width": W, "max_verify": V, "tokens_per_s": round(tokens / t, 2),
+                     "ms_per_step": round(t * 1e3 / args.steps, 3), "aal": round(tokens / args.steps, 3),
+                     "w_verify": wv, "expected_aal": round(exp_aal, 3), "eq3_speedup": round(float(sd.speedup[0]), 4),
+                     "predicted_tokens_per_s": round(exp_aal / (pred_step_us * 1e-6), 2)})
+        del sd
+        torch.cuda.empty_cache()
+    chosen = max(rows, key=lambda r: r["predicted_tokens_per_s"])
+    best = max(rows, key=lambda r: r["tokens_per_s"])
+    line = {"metric": "accepted tokens/s", "value": chosen["tokens_per_s"], "unit": "tokens/s", "n_gpus": 1,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": chosen["ms_per_step"],
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic (coupled random-init weights, random prompts)",
+            "config": {"workload": wl["desc"], "chosen": {k: chosen[k] for k in ("depth", "width", "max_verify")},
+                       "measured_best": {k: best[k] for k in ("depth", "width", "max_verify", "tokens_per_s")},
+                       "profile": {"drafter": dbp, "verifier": vbp}},
+            "sweep": rows}
+    print(json.dumps(line), flush=True)
 
 
 def prompts_for(wl, vocab, rank):
@@ -533,6 +654,12 @@ def main():
         torch.cuda.set_device(local_rank)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     try:
+        if args.workload == "cfg3":
+            if rank == 0:
+                import torch
+
+                run_cfg3(args, torch.device("cuda", local_rank))
+            return
         run_ours(args, rank, world, local_rank)
     finally:
         if world > 1:

@@ -394,16 +394,20 @@ __global__ void __launch_bounds__(kKnapThreads) knapsack_prune_kernel(
   __shared__ int s_best_k;
   __shared__ double s_best_speed;
 
-  for (int i = threadIdx.x; i < N; i += blockDim.x) par[i] = t.parent[tb + i];
+  {
+    // Stage parents and node probabilities in shared memory with every thread (one round trip),
+    // so thread 0's in-order product chain below reads on-chip operands only.
+    const double* pr = probs ? probs + tb : t.prob + tb;
+    for (int i = threadIdx.x; i < N; i += blockDim.x) {
+      par[i] = t.parent[tb + i];
+      gain[i] = pr[i];
+    }
+  }
   __syncthreads();
   if (threadIdx.x == 0) {
     // path_products (acceptance.py:176-184) and subtree sizes (egt.py:225-229).
-    const double* pr = probs ? probs + tb : t.prob + tb;
-    gain[0] = pr[0];
-    if (args.probs_are_gains) {
-      for (int i = 1; i < N; ++i) gain[i] = pr[i];
-    } else {
-      for (int i = 1; i < N; ++i) gain[i] = gain[par[i]] * pr[i];
+    if (!args.probs_are_gains) {
+      for (int i = 1; i < N; ++i) gain[i] = gain[par[i]] * gain[i];
     }
     for (int i = 0; i < N; ++i) sz[i] = 1;
     for (int v = N - 1; v >= 1; --v) sz[par[v]] += sz[v];

@@ -425,11 +425,19 @@ int ygg_gemv_plan_init(void* plan, const void* W, const void* X, int M, int N, i
     const int v = s ? atoi(s) : 110;
     return v < 64 ? 64 : (v > 227 ? 227 : v);
   }();
-  const int per_sm = smem_kb <= 113 ? 2 : 1;
+  int per_sm = smem_kb <= 113 ? 2 : 1;
   p.grid = num_ctas > 0 ? num_ctas : std::min(sms * per_sm, p.nblk);
+  // A matrix with at most one block per SM (o / down projections: 128 blocks of 16 x K) is bound by
+  // one CTA's bytes in flight: give that CTA the whole SM's ring (YGG_GEMV_SOLO_KB, default 200).
+  static const int solo_kb = [] {
+    const char* s = getenv("YGG_GEMV_SOLO_KB");
+    const int v = s ? atoi(s) : 200;
+    return v < 64 ? 64 : (v > 227 ? 227 : v);
+  }();
+  const int budget_kb = (num_ctas <= 0 && p.nblk <= sms) ? solo_kb : smem_kb;
   const size_t stage = static_cast<size_t>(kRows) * kStageK * 2 + static_cast<size_t>(p.xrows) * kStageK * 2;
   const size_t fixed = 1024 + 16 * 2 * 8 + kMaxTok * 16 + kCompute * 2 * 4 * 32 * 4 + 64;
-  p.stages = static_cast<int>(std::min<size_t>(16, (static_cast<size_t>(smem_kb) * 1024 - fixed) / stage));
+  p.stages = static_cast<int>(std::min<size_t>(16, (static_cast<size_t>(budget_kb) * 1024 - fixed) / stage));
   YGG_CHECK_ARG(p.stages >= 2, "gemv: shared memory budget too small");
   pl->smem = fixed + static_cast<size_t>(p.stages) * stage;
   if (int rc = map3(&pl->tw, W, N, K, kRows)) return rc;

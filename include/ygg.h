@@ -281,6 +281,14 @@ int ygg_commit(ygg_seq seq, ygg_tree vtree, const int32_t* path, const int32_t* 
 /* ---------------- K8: on-device stage timer ---------------- */
 int ygg_stamp(unsigned long long* slot, ygg_stream_t stream);
 
+/* In-graph kernel timeline (profiling only).  While armed, every launch of a traced kernel
+ * (gemv = 1, decode attention = 2) takes the next slot of buf[slots][8] — {first CTA start, first
+ * return from the grid-dependency wait, last CTA end, kernel checkpoints 3..7 (latest over CTAs)},
+ * written with %globaltimer atomics; the caller initialises fields 0 and 1 to ~0, the rest to 0.  Arming with slots = 0 disarms.
+ * ygg_trace_used returns the number of slots taken and copies their kernel ids. */
+int ygg_trace_arm(unsigned long long* buf, int slots);
+int ygg_trace_used(int* kernel_ids, int cap);
+
 /* ---------------- Row-block GEMV (decode passes, 1..16 token rows) ----------------
  * Y = X . W^T with the layer epilogue fused; one launch per matmul, full K per 16-row block of W
  * (no split-K partials).  Weights in the fused layout (model.prepare_fused_): RMSNorm gains folded,
@@ -317,9 +325,9 @@ int ygg_gemv_run(const void* plan, const ygg_gemv_epilogue* epi, ygg_stream_t st
 size_t ygg_attn_dec_plan_size(void);
 int ygg_attn_dec_plan_init(void* plan, const void* q, const void* cache_layer, int B, int T, int Hq, int Hkv, int hd,
                            int S);
-/* workspace: >= ygg_attn_dec_workspace_size(plan) bytes, zero-filled once (cross-CTA key-split partials
- * and monotonic arrival counters; the chunks of each (kv head, request, row tile) are split over CTAs
- * and merged by the last one in fixed split order). */
+/* workspace: >= ygg_attn_dec_workspace_size(plan) bytes (currently 0; may be NULL).  The key chunks of
+ * each (kv head, request, row tile) are split over a thread-block cluster of CTAs and merged in the
+ * leader CTA's shared memory in fixed split order (YGG_ATTN_DEC_KVSPLIT overrides the cluster size). */
 size_t ygg_attn_dec_workspace_size(const void* plan);
 int ygg_attn_dec_run(const void* plan, const int32_t* blk_start, const int32_t* blk_len, const uint32_t* qmask,
                      int mask_words, float scale, void* out, void* workspace, ygg_stream_t stream);

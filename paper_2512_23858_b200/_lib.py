@@ -169,6 +169,8 @@ _SIGS: dict[str, tuple] = {
     "ygg_verify_inputs": (C.c_int, [YggTree, YggSeq, vp, vp, vp, vp, vp, C.c_int, vp, vp, vp]),
     "ygg_commit": (C.c_int, [YggSeq, YggTree, vp, vp, vp, vp, C.c_int, vp]),
     "ygg_stamp": (C.c_int, [vp, vp]),
+    "ygg_trace_arm": (C.c_int, [vp, C.c_int]),
+    "ygg_trace_used": (C.c_int, [vp, C.c_int]),
     "ygg_attn_dec_plan_size": (C.c_size_t, []),
     "ygg_attn_dec_plan_init": (C.c_int, [vp, vp, vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int]),
     "ygg_attn_dec_workspace_size": (C.c_size_t, [vp]),

@@ -1,6 +1,10 @@
-// Tree / prefix attention for decode-shaped passes: one CTA per (kv head, request, 64-row tile of
-// query rows) walks every visible key chunk with an online softmax, so there are no split-KV
-// partials and no combine launch.
+// Tree / prefix attention for decode-shaped passes: a (1, 1, kvsplit) thread-block cluster per
+// (kv head, request, 64-row tile of query rows) walks the visible key chunks with an online softmax
+// (chunks interleaved over the cluster's CTAs and, inside a CTA, over ksplit warp groups); the
+// partials merge in shared memory — in-CTA, then in the leader CTA through DSMEM — in fixed split
+// order, so there is no combine launch and the result is deterministic.  kvsplit defaults to the
+// cluster size that brings the grid to ~half the SMs (at most 4): with B = 1 only Hkv = 8 CTAs
+// would otherwise carry the whole mma.sync + softmax chain.
 //
 // The tcgen05 split-KV kernel (attn_tc.cu) is built for the verify pass (T = 50 tokens x 4 heads =
 // 200 query rows per kv head): there a 128-row UMMA tile is full and a separate combine is cheap.
@@ -12,7 +16,9 @@
 //                  (ldmatrix from the swizzled tiles), ancestor / prefix mask from the row's
 //                  tree-mask bits, online softmax in base 2, P re-used from the S accumulators as
 //                  the A operand of O += P V (the V^T cache layout is exactly the col-major B).
-// Output O / l in bf16 straight into attn[m][head][hd].  Fixed key order: deterministic.
+// Output O / l in bf16 straight into attn[m][head][hd].
+// Chunks wholly inside the committed prefix are loaded before the grid-dependency wait and skip the
+// mask work; the block's chunks and Q follow the wait.
 #include <cudaTypedefs.h>
 
 #include <cmath>
@@ -31,7 +37,7 @@ constexpr uint32_t kMagic = 0x59474144u;  // "YGAD"
 
 struct Plan {
   uint32_t magic;
-  int B, T, Hq, Hkv, hd, S, Gh, rows, warps, ksplit, stages, tpt, row_tiles, kvsplit;
+  int B, T, Hq, Hkv, hd, S, Gh, rows, warps, ksplit, stages, tpt, row_tiles, kvsplit, ring_bytes, slot_bytes;
   size_t smem;
   alignas(64) CUtensorMap tq;
   alignas(64) CUtensorMap tk;
@@ -40,15 +46,16 @@ struct Plan {
 
 struct Args {
   int T, Hq, Hkv, hd, S, Gh, rows, mask_words, ksplit, stages, tpt;  // rows = tpt * Gh (one row tile)
-  int kvsplit, row_tiles;  // CTAs per (kv head, request, row tile) splitting the key chunks
-  int ring_bytes;          // max(key/value ring, split-merge scratch): the barriers sit after it
-  float* part;             // [B][Hkv][row_tiles][kvsplit][warps][NV][32] cross-CTA partials
-  unsigned* ctr;           // [B][Hkv][row_tiles] arrival counters (monotonic)
+  int warps;               // compute warps = row warps x ksplit
+  int kvsplit, row_tiles;  // CTAs (one thread-block cluster) per (kv head, request, row tile)
+  int ring_bytes;          // max(key/value ring, in-CTA merge scratch)
+  int slot_bytes;          // cluster merge slots in the leader CTA [kvsplit - 1][warps][NV2][32] f32
   float scale_log2;
   const int32_t* blk_start;
   const int32_t* blk_len;
   const uint32_t* qmask;
   __nv_bfloat16* out;
+  unsigned long long* trace;  // kernel-timeline slot (profiling only) or nullptr
 };
 
 YGG_DEV void tma2(void* dst, const CUtensorMap* m, uint64_t* bar, int c0, int c1) {
@@ -77,6 +84,11 @@ YGG_DEV void mma16816(float* d, uint32_t a0, uint32_t a1, uint32_t a2, uint32_t 
       "{%0, %1, %2, %3};"
       : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
       : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+YGG_DEV float ex2(float x) {  // 2^x, flush-to-zero (ex2(-inf) = 0)
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
 }
 YGG_DEV uint32_t pack2(float lo, float hi) {
   __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
@@ -113,7 +125,7 @@ YGG_DEV uint32_t vis_word(int kw, int bs, int bl, int tq, int mask_words, const 
   return pre | blk;
 }
 
-template <int HD>
+template <int HD, int KS>  // KS: in-CTA key-split groups (== Args::ksplit)
 __global__ void __launch_bounds__(32 * (1 + kMaxWarps), 1)
     attn_dec_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
                     const __grid_constant__ CUtensorMap tv, Args a) {
@@ -127,9 +139,11 @@ __global__ void __launch_bounds__(32 * (1 + kMaxWarps), 1)
   unsigned char* sq = base;
   unsigned char* sk = sq + q_bytes;
   unsigned char* sv = sk + NS * k_bytes;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sk + a.ring_bytes);
+  float* slots = reinterpret_cast<float*>(sk + a.ring_bytes);
+  uint64_t* full = reinterpret_cast<uint64_t*>(sk + a.ring_bytes + a.slot_bytes);
   uint64_t* empty = full + NS;
   uint64_t* qbar = empty + NS;
+  uint64_t* cbar = qbar + 1;  // leader: every lane of every compute warp of the cluster has filled its slot
   const int kvh = blockIdx.x, r = blockIdx.y;
   const int rt = blockIdx.z / a.kvsplit, ks2 = blockIdx.z % a.kvsplit;  // row tile, cross-CTA key split
   const int t0 = rt * a.tpt;                                // first token of this row tile
@@ -142,32 +156,51 @@ __global__ void __launch_bounds__(32 * (1 + kMaxWarps), 1)
       mbar_init(&empty[s], nw);
     }
     mbar_init(qbar, 1);
+    mbar_init(cbar, (a.kvsplit - 1) * a.warps);  // one arrival per compute warp of the other CTAs
     fence_barrier_init();
+    trace_min(a.trace, 0);
   }
-  __syncthreads();
-  pdl_wait();
-  pdl_launch_dependents();
-  const int bs = __ldg(a.blk_start + r), bl = __ldg(a.blk_len + r);
-  const int nkeys = bs + bl;
-  const int nch = (nkeys + kKC - 1) / kKC;
+  // Cluster members arrive on the leader's barrier: it must be initialised cluster-wide first.
+  if (a.kvsplit > 1) cluster_sync();
+  else __syncthreads();
   const size_t kv_row0 = (static_cast<size_t>(r) * 2 * a.Hkv + kvh) * a.S;          // K rows of this head
   const size_t vt_row0 = ((static_cast<size_t>(r) * 2 + 1) * a.Hkv + kvh) * HD;     // V^T rows
   if (warp == 0) {
     if (lane == 0) {
-      mbar_arrive_expect_tx(qbar, static_cast<uint32_t>(a.rows) * 128u * DCH);  // full box (OOB rows zero-filled)
-      for (int dc = 0; dc < DCH; ++dc)
-        tma3(sq + dc * (64 * 128), &tq, qbar, dc * 64, kvh * a.Gh, r * a.T + t0);
-      for (int j = 0, c = ks2; c < nch; ++j, c += a.kvsplit) {  // this CTA's chunks, local index j
+      // The block bounds and the committed prefix's K / V were written at least two kernels back,
+      // and the kernel just before this one (gemv / epi_qkv_rope) triggers its dependents only
+      // after its own grid-dependency wait, so everything two or more kernels back has completed:
+      // chunks wholly inside the prefix stream in before the wait; the block's keys and Q (written
+      // by the previous kernel) are loaded after it.
+      const int bs = __ldg(a.blk_start + r), bl = __ldg(a.blk_len + r);
+      const int nch = (bs + bl + kKC - 1) / kKC;
+      auto load = [&](int j, int c) {
         const int st = j % NS;
         if (j >= NS) mbar_wait(&empty[st], ((j / NS) - 1) & 1);
         mbar_arrive_expect_tx(&full[st], k_bytes + v_bytes);
         for (int dc = 0; dc < DCH; ++dc)
           tma2(sk + st * k_bytes + dc * (kKC * 128), &tk, &full[st], dc * 64, static_cast<int>(kv_row0) + c * kKC);
         tma2(sv + st * v_bytes, &tv, &full[st], c * kKC, static_cast<int>(vt_row0));
-      }
+      };
+      int j = 0, c = ks2;  // this CTA's chunks, local index j
+      for (; j < NS && c < nch && (c + 1) * kKC <= bs; ++j, c += a.kvsplit) load(j, c);
+      pdl_wait();
+      mbar_arrive_expect_tx(qbar, static_cast<uint32_t>(a.rows) * 128u * DCH);  // full box (OOB rows zero-filled)
+      for (int dc = 0; dc < DCH; ++dc)
+        tma3(sq + dc * (64 * 128), &tq, qbar, dc * 64, kvh * a.Gh, r * a.T + t0);
+      for (; c < nch; ++j, c += a.kvsplit) load(j, c);
+    } else {
+      pdl_wait();
     }
+    pdl_launch_dependents();
     return;
   }
+  pdl_wait();
+  pdl_launch_dependents();
+  if (threadIdx.x == 32) trace_min(a.trace, 1);
+  const int bs = __ldg(a.blk_start + r), bl = __ldg(a.blk_len + r);
+  const int nkeys = bs + bl;
+  const int nch = (nkeys + kKC - 1) / kKC;
   // Compute warp (ks, rw): key split ks takes chunks ks, ks + ksplit, ...; row warp rw 16 query rows
   // (token t = row / Gh, head = kvh*Gh + row % Gh).  Splits are merged in fixed order at the end.
   const int cwi = warp - 1;
@@ -179,6 +212,7 @@ __global__ void __launch_bounds__(32 * (1 + kMaxWarps), 1)
   const uint32_t* mra = a.qmask + static_cast<size_t>(r * a.T + (va ? ta : 0)) * (a.mask_words ? a.mask_words : 1);
   const uint32_t* mrb = a.qmask + static_cast<size_t>(r * a.T + (vb ? tb : 0)) * (a.mask_words ? a.mask_words : 1);
   mbar_wait(qbar, 0);
+  if (lane == 0) trace_max(a.trace, 3);
   // Q fragments for all hd k-steps (A operand), kept in registers.
   uint32_t qa[HD / 16][4];
   {
@@ -193,58 +227,75 @@ __global__ void __launch_bounds__(32 * (1 + kMaxWarps), 1)
 #pragma unroll
   for (int n = 0; n < HD / 8; ++n) o[n][0] = o[n][1] = o[n][2] = o[n][3] = 0.f;
   float ma = -INFINITY, mb = -INFINITY, la = 0.f, lb = 0.f;
+  // Per-thread ldmatrix offsets: row 8n + brow of a swizzled [rows][128 B] tile has (row & 7) == brow,
+  // so chunk column j sits at n * 1024 + brow * 128 + ((j ^ brow) << 4) — the n part is an immediate.
   const int brow = lane & 7, bhi = (lane >> 3) & 1;
-  for (int j = ks; ks2 + j * a.kvsplit < nch; j += a.ksplit) {
+  uint32_t xoff[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) xoff[q] = static_cast<uint32_t>(brow * 128 + (((2 * q + bhi) ^ brow) << 4));
+  const float sl = a.scale_log2;
+  for (int j = ks; ks2 + j * a.kvsplit < nch; j += KS) {
     const int c = ks2 + j * a.kvsplit;
     const int st = j % NS;
     const int key0 = c * kKC;
+    // Chunks wholly inside the committed prefix are visible to every row: no mask work at all.
+    const bool in_prefix = key0 + kKC <= bs;
     // visibility of this thread's 16 key columns (n-tile j: keys 8j + 2*(lane&3) + {0,1}) per row
     uint32_t wa0 = 0u, wa1 = 0u, wb0 = 0u, wb1 = 0u;
-    if (va) {
-      wa0 = vis_word(key0, bs, bl, ta, a.mask_words, mra);
-      wa1 = vis_word(key0 + 32, bs, bl, ta, a.mask_words, mra);
-    }
-    if (vb) {
-      wb0 = vis_word(key0, bs, bl, tb, a.mask_words, mrb);
-      wb1 = vis_word(key0 + 32, bs, bl, tb, a.mask_words, mrb);
+    if (!in_prefix) {
+      if (va) {
+        wa0 = vis_word(key0, bs, bl, ta, a.mask_words, mra);
+        wa1 = vis_word(key0 + 32, bs, bl, ta, a.mask_words, mra);
+      }
+      if (vb) {
+        wb0 = vis_word(key0, bs, bl, tb, a.mask_words, mrb);
+        wb1 = vis_word(key0 + 32, bs, bl, tb, a.mask_words, mrb);
+      }
     }
     mbar_wait(&full[st], (j / NS) & 1);
+    if (j == ks && lane == 0) trace_max(a.trace, 4);
     const uint32_t kb = smem_u32(sk + st * k_bytes), vb_ = smem_u32(sv + st * v_bytes);
     float s[8][4];
 #pragma unroll
     for (int n = 0; n < 8; ++n) s[n][0] = s[n][1] = s[n][2] = s[n][3] = 0.f;
 #pragma unroll
-    for (int ks = 0; ks < HD / 16; ++ks) {
-      const int dc = ks / 4, j = 2 * (ks % 4) + bhi;
+    for (int kk = 0; kk < HD / 16; ++kk) {
+      const uint32_t ka = kb + (kk / 4) * (kKC * 128) + xoff[kk % 4];
 #pragma unroll
       for (int n = 0; n < 8; ++n) {
         uint32_t b0, b1;
-        ldsm_x2(kb + dc * (kKC * 128) + swz(8 * n + brow, j), b0, b1);
-        mma16816(s[n], qa[ks][0], qa[ks][1], qa[ks][2], qa[ks][3], b0, b1);
+        ldsm_x2(ka + n * 1024, b0, b1);
+        mma16816(s[n], qa[kk][0], qa[kk][1], qa[kk][2], qa[kk][3], b0, b1);
       }
     }
-    // mask + chunk row max
+    // mask (raw scores) + chunk row max
     float cma = -INFINITY, cmb = -INFINITY;
+    if (!in_prefix) {
+#pragma unroll
+      for (int n = 0; n < 8; ++n) {
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int col = 8 * n + 2 * (lane & 3) + e;  // key within the chunk
+          const uint32_t wa = col < 32 ? wa0 : wa1, wb = col < 32 ? wb0 : wb1;
+          if (!((wa >> (col & 31)) & 1u)) s[n][e] = -INFINITY;
+          if (!((wb >> (col & 31)) & 1u)) s[n][2 + e] = -INFINITY;
+        }
+      }
+    }
 #pragma unroll
     for (int n = 0; n < 8; ++n) {
-#pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const int col = 8 * n + 2 * (lane & 3) + e;  // key within the chunk
-        const uint32_t wa = col < 32 ? wa0 : wa1, wb = col < 32 ? wb0 : wb1;
-        const bool vis_a = (wa >> (col & 31)) & 1u, vis_b = (wb >> (col & 31)) & 1u;
-        s[n][e] = vis_a ? s[n][e] * a.scale_log2 : -INFINITY;
-        s[n][2 + e] = vis_b ? s[n][2 + e] * a.scale_log2 : -INFINITY;
-        cma = fmaxf(cma, s[n][e]);
-        cmb = fmaxf(cmb, s[n][2 + e]);
-      }
+      cma = fmaxf(cma, fmaxf(s[n][0], s[n][1]));
+      cmb = fmaxf(cmb, fmaxf(s[n][2], s[n][3]));
     }
 #pragma unroll
     for (int off = 1; off <= 2; off <<= 1) {
       cma = fmaxf(cma, __shfl_xor_sync(0xffffffffu, cma, off));
       cmb = fmaxf(cmb, __shfl_xor_sync(0xffffffffu, cmb, off));
     }
-    const float na = fmaxf(ma, cma), nb = fmaxf(mb, cmb);
-    const float fa = (na == -INFINITY) ? 1.f : exp2f(ma - na), fb = (nb == -INFINITY) ? 1.f : exp2f(mb - nb);
+    // running max in scaled log2 units (scale > 0, so the max commutes with the scaling)
+    const float na = fmaxf(ma, cma * sl), nb = fmaxf(mb, cmb * sl);
+    const float fa = (na == -INFINITY) ? 1.f : ex2(ma - na), fb = (nb == -INFINITY) ? 1.f : ex2(mb - nb);
+    const float nna = (na == -INFINITY) ? 0.f : -na, nnb = (nb == -INFINITY) ? 0.f : -nb;
     ma = na;
     mb = nb;
     float sa = 0.f, sb = 0.f;
@@ -252,8 +303,8 @@ __global__ void __launch_bounds__(32 * (1 + kMaxWarps), 1)
     for (int n = 0; n < 8; ++n) {
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
-        s[n][e] = (s[n][e] == -INFINITY) ? 0.f : exp2f(s[n][e] - na);
-        s[n][2 + e] = (s[n][2 + e] == -INFINITY) ? 0.f : exp2f(s[n][2 + e] - nb);
+        s[n][e] = ex2(fmaf(s[n][e], sl, nna));  // masked: -inf -> 0
+        s[n][2 + e] = ex2(fmaf(s[n][2 + e], sl, nnb));
         sa += s[n][e];
         sb += s[n][2 + e];
       }
@@ -265,131 +316,175 @@ __global__ void __launch_bounds__(32 * (1 + kMaxWarps), 1)
     }
     la = la * fa + sa;
     lb = lb * fb + sb;
+    if (__any_sync(0xffffffffu, fa != 1.f || fb != 1.f)) {
 #pragma unroll
-    for (int n = 0; n < HD / 8; ++n) {
-      o[n][0] *= fa;
-      o[n][1] *= fa;
-      o[n][2] *= fb;
-      o[n][3] *= fb;
+      for (int n = 0; n < HD / 8; ++n) {
+        o[n][0] *= fa;
+        o[n][1] *= fa;
+        o[n][2] *= fb;
+        o[n][3] *= fb;
+      }
     }
     // O += P V: A = P (16 rows x 16 keys per k-step, from the S accumulators), B = V^T rows.
 #pragma unroll
-    for (int ks = 0; ks < kKC / 16; ++ks) {
-      const uint32_t a0 = pack2(s[2 * ks][0], s[2 * ks][1]), a1 = pack2(s[2 * ks][2], s[2 * ks][3]);
-      const uint32_t a2 = pack2(s[2 * ks + 1][0], s[2 * ks + 1][1]), a3 = pack2(s[2 * ks + 1][2], s[2 * ks + 1][3]);
-      const int j = 2 * ks + bhi;
+    for (int kk = 0; kk < kKC / 16; ++kk) {
+      const uint32_t a0 = pack2(s[2 * kk][0], s[2 * kk][1]), a1 = pack2(s[2 * kk][2], s[2 * kk][3]);
+      const uint32_t a2 = pack2(s[2 * kk + 1][0], s[2 * kk + 1][1]), a3 = pack2(s[2 * kk + 1][2], s[2 * kk + 1][3]);
+      const uint32_t va_ = vb_ + xoff[kk];
 #pragma unroll
       for (int n = 0; n < HD / 8; ++n) {
         uint32_t b0, b1;
-        ldsm_x2(vb_ + swz(8 * n + brow, j), b0, b1);
+        ldsm_x2(va_ + n * 1024, b0, b1);
         mma16816(o[n], a0, a1, a2, a3, b0, b1);
       }
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[st]);
+    if (j == ks && lane == 0) trace_max(a.trace, 5);
   }
-  // Merge the key splits (fixed split order) through shared memory, reusing the drained ring.
-  if (a.ksplit > 1) {
-    asm volatile("bar.sync 1, %0;" ::"r"(32 * nw * a.ksplit) : "memory");  // ring fully consumed
-    constexpr int NV = HD / 8 * 4 + 4;  // o values + (ma, mb, la, lb)
+  if (lane == 0) trace_max(a.trace, 6);
+  // Merge.  (1) In-CTA key splits: every warp parks its (O, m, l) in the drained ring; warp (ks, rw)
+  // then merges n-tiles [ks*NPW, (ks+1)*NPW) of row warp rw over the KS partials in fixed order.
+  // (2) Cluster key splits: each warp writes its merged n-tiles + (m, l) into its slot in the leader
+  // CTA's shared memory (DSMEM) and arrives on the leader's barrier; the leader's warps merge the
+  // kvsplit slots in fixed order.  Both merges are deterministic and fully unrolled (compile-time
+  // KS / NPW; the cluster loop is predicated up to 8) — they are pure latency chains otherwise.
+  constexpr int NV = HD / 8 * 4 + 4;  // o values + (ma, mb, la, lb)
+  constexpr int NPW = (HD / 8) / KS;
+  const int n0 = ks * NPW;
+  float O[NPW][4];
+  float Ma = ma, Mb = mb, La = la, Lb = lb;
+  if constexpr (KS > 1) {
+    asm volatile("bar.sync 1, %0;" ::"r"(32 * a.warps) : "memory");  // ring fully consumed
     float* xs = reinterpret_cast<float*>(sk);
     float* mine = xs + static_cast<size_t>((ks * nw + rw) * NV) * 32 + lane;
-    if (ks > 0) {
 #pragma unroll
-      for (int n = 0; n < HD / 8; ++n)
+    for (int n = 0; n < HD / 8; ++n)
 #pragma unroll
-        for (int e = 0; e < 4; ++e) mine[(n * 4 + e) * 32] = o[n][e];
-      mine[(NV - 4) * 32] = ma;
-      mine[(NV - 3) * 32] = mb;
-      mine[(NV - 2) * 32] = la;
-      mine[(NV - 1) * 32] = lb;
+      for (int e = 0; e < 4; ++e) mine[(n * 4 + e) * 32] = o[n][e];
+    mine[(NV - 4) * 32] = ma;
+    mine[(NV - 3) * 32] = mb;
+    mine[(NV - 2) * 32] = la;
+    mine[(NV - 1) * 32] = lb;
+    asm volatile("bar.sync 1, %0;" ::"r"(32 * a.warps) : "memory");
+    const float* b0 = xs + static_cast<size_t>(rw * NV) * 32 + lane;
+    const int kstride = nw * NV * 32;
+    float pm[KS][4];  // (m_a, m_b, l_a, l_b) of every partial
+#pragma unroll
+    for (int k2 = 0; k2 < KS; ++k2)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) pm[k2][e] = b0[k2 * kstride + (NV - 4 + e) * 32];
+    Ma = pm[0][0];
+    Mb = pm[0][1];
+#pragma unroll
+    for (int k2 = 1; k2 < KS; ++k2) {
+      Ma = fmaxf(Ma, pm[k2][0]);
+      Mb = fmaxf(Mb, pm[k2][1]);
     }
-    asm volatile("bar.sync 1, %0;" ::"r"(32 * nw * a.ksplit) : "memory");
-    if (ks > 0) return;
-    for (int k2 = 1; k2 < a.ksplit; ++k2) {
-      const float* th = xs + static_cast<size_t>((k2 * nw + rw) * NV) * 32 + lane;
-      const float m2a = th[(NV - 4) * 32], m2b = th[(NV - 3) * 32];
-      const float na = fmaxf(ma, m2a), nb = fmaxf(mb, m2b);
-      const float f1a = na == -INFINITY ? 0.f : exp2f(ma - na), f2a = na == -INFINITY ? 0.f : exp2f(m2a - na);
-      const float f1b = nb == -INFINITY ? 0.f : exp2f(mb - nb), f2b = nb == -INFINITY ? 0.f : exp2f(m2b - nb);
+    La = 0.f;
+    Lb = 0.f;
 #pragma unroll
-      for (int n = 0; n < HD / 8; ++n) {
-        o[n][0] = o[n][0] * f1a + th[(n * 4 + 0) * 32] * f2a;
-        o[n][1] = o[n][1] * f1a + th[(n * 4 + 1) * 32] * f2a;
-        o[n][2] = o[n][2] * f1b + th[(n * 4 + 2) * 32] * f2b;
-        o[n][3] = o[n][3] * f1b + th[(n * 4 + 3) * 32] * f2b;
+    for (int k2 = 0; k2 < KS; ++k2) {
+      pm[k2][0] = Ma == -INFINITY ? 0.f : ex2(pm[k2][0] - Ma);  // now the partial's weight
+      pm[k2][1] = Mb == -INFINITY ? 0.f : ex2(pm[k2][1] - Mb);
+      La += pm[k2][2] * pm[k2][0];
+      Lb += pm[k2][3] * pm[k2][1];
+    }
+#pragma unroll
+    for (int n = 0; n < NPW; ++n) {
+      O[n][0] = O[n][1] = O[n][2] = O[n][3] = 0.f;
+#pragma unroll
+      for (int k2 = 0; k2 < KS; ++k2) {
+        const float* tv = b0 + k2 * kstride + ((n0 + n) * 4) * 32;
+        O[n][0] += tv[0] * pm[k2][0];
+        O[n][1] += tv[32] * pm[k2][0];
+        O[n][2] += tv[64] * pm[k2][1];
+        O[n][3] += tv[96] * pm[k2][1];
       }
-      la = la * f1a + th[(NV - 2) * 32] * f2a;
-      lb = lb * f1b + th[(NV - 1) * 32] * f2b;
-      ma = na;
-      mb = nb;
     }
+  } else {
+#pragma unroll
+    for (int n = 0; n < NPW; ++n)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) O[n][e] = o[n][e];
   }
-  // Cross-CTA key splits: publish this CTA's (O, m, l); the last of the group's CTAs merges all of
-  // them in fixed split order (deterministic whichever CTA arrives last).
   if (a.kvsplit > 1) {
-    constexpr int NV = HD / 8 * 4 + 4;
-    const size_t grp = (static_cast<size_t>(r) * a.Hkv + kvh) * a.row_tiles + rt;
-    const size_t gstride = static_cast<size_t>(nw) * NV * 32;
-    float* mine = a.part + (grp * a.kvsplit + ks2) * gstride + static_cast<size_t>(rw) * NV * 32 + lane;
+    // Slots [kvsplit - 1][warps][NPW + 1][32 lanes][4] in the leader: n-tile values, then
+    // (m_a, m_b, l_a, l_b).  The leader's own partial stays in registers.
+    constexpr int NV2 = (NPW + 1) * 4;
+    if (ks2 != 0) {
+      const uint32_t rslot = mapa_shared(
+          smem_u32(slots) + static_cast<uint32_t>((((ks2 - 1) * a.warps + cwi) * NV2) * 32 + lane * 4) * 4u, 0);
 #pragma unroll
-    for (int n = 0; n < HD / 8; ++n)
-#pragma unroll
-      for (int e = 0; e < 4; ++e) __stcg(mine + (n * 4 + e) * 32, o[n][e]);
-    __stcg(mine + (NV - 4) * 32, ma);
-    __stcg(mine + (NV - 3) * 32, mb);
-    __stcg(mine + (NV - 2) * 32, la);
-    __stcg(mine + (NV - 1) * 32, lb);
-    __threadfence();
-    asm volatile("bar.sync 2, %0;" ::"r"(32 * nw) : "memory");
-    __shared__ int last_s;
-    if (rw == 0 && lane == 0) {
-      const unsigned old = atomicAdd(a.ctr + grp, 1u);
-      last_s = ((old + 1u) % static_cast<unsigned>(a.kvsplit)) == 0u;
-    }
-    asm volatile("bar.sync 2, %0;" ::"r"(32 * nw) : "memory");
-    if (!last_s) return;
-    __threadfence();
-    const float* base0 = a.part + grp * a.kvsplit * gstride + static_cast<size_t>(rw) * NV * 32 + lane;
-    ma = __ldcg(base0 + (NV - 4) * 32);
-    mb = __ldcg(base0 + (NV - 3) * 32);
-    la = __ldcg(base0 + (NV - 2) * 32);
-    lb = __ldcg(base0 + (NV - 1) * 32);
-#pragma unroll
-    for (int n = 0; n < HD / 8; ++n)
-#pragma unroll
-      for (int e = 0; e < 4; ++e) o[n][e] = __ldcg(base0 + (n * 4 + e) * 32);
-    for (int k2 = 1; k2 < a.kvsplit; ++k2) {
-      const float* th = base0 + k2 * gstride;
-      const float m2a = __ldcg(th + (NV - 4) * 32), m2b = __ldcg(th + (NV - 3) * 32);
-      const float na = fmaxf(ma, m2a), nb = fmaxf(mb, m2b);
-      const float f1a = na == -INFINITY ? 0.f : exp2f(ma - na), f2a = na == -INFINITY ? 0.f : exp2f(m2a - na);
-      const float f1b = nb == -INFINITY ? 0.f : exp2f(mb - nb), f2b = nb == -INFINITY ? 0.f : exp2f(m2b - nb);
-#pragma unroll
-      for (int n = 0; n < HD / 8; ++n) {
-        o[n][0] = o[n][0] * f1a + __ldcg(th + (n * 4 + 0) * 32) * f2a;
-        o[n][1] = o[n][1] * f1a + __ldcg(th + (n * 4 + 1) * 32) * f2a;
-        o[n][2] = o[n][2] * f1b + __ldcg(th + (n * 4 + 2) * 32) * f2b;
-        o[n][3] = o[n][3] * f1b + __ldcg(th + (n * 4 + 3) * 32) * f2b;
+      for (int n = 0; n < NPW; ++n) st_cluster_v4(rslot + n * 512u, O[n][0], O[n][1], O[n][2], O[n][3]);
+      st_cluster_v4(rslot + NPW * 512u, Ma, Mb, La, Lb);
+      // every lane's stores happen-before lane 0's cluster-scope release arrival
+      __syncwarp();
+      if (lane == 0) {
+        fence_cluster();
+        mbar_arrive_cluster(mapa_shared(smem_u32(cbar), 0));
       }
-      la = la * f1a + __ldcg(th + (NV - 2) * 32) * f2a;
-      lb = lb * f1b + __ldcg(th + (NV - 1) * 32) * f2b;
-      ma = na;
-      mb = nb;
+      return;
+    }
+    mbar_wait_cluster(cbar, 0);
+    const float* b0 = slots + static_cast<size_t>(cwi * NV2) * 32 + lane * 4;
+    const int kstride = a.warps * NV2 * 32;
+    constexpr int KV = HD == 128 ? 4 : 8;  // cluster-size cap (plan_init clamps kvsplit to it)
+    float4 ml[KV];
+    ml[0] = make_float4(Ma, Mb, La, Lb);
+#pragma unroll
+    for (int k2 = 1; k2 < KV; ++k2)
+      if (k2 < a.kvsplit) ml[k2] = *reinterpret_cast<const float4*>(b0 + (k2 - 1) * kstride + NPW * 128);
+#pragma unroll
+    for (int k2 = 1; k2 < KV; ++k2)
+      if (k2 < a.kvsplit) {
+        Ma = fmaxf(Ma, ml[k2].x);
+        Mb = fmaxf(Mb, ml[k2].y);
+      }
+    La = 0.f;
+    Lb = 0.f;
+#pragma unroll
+    for (int k2 = 0; k2 < KV; ++k2)
+      if (k2 < a.kvsplit) {
+        ml[k2].x = Ma == -INFINITY ? 0.f : ex2(ml[k2].x - Ma);
+        ml[k2].y = Mb == -INFINITY ? 0.f : ex2(ml[k2].y - Mb);
+        La += ml[k2].z * ml[k2].x;
+        Lb += ml[k2].w * ml[k2].y;
+      }
+#pragma unroll
+    for (int n = 0; n < NPW; ++n) {
+      O[n][0] *= ml[0].x;
+      O[n][1] *= ml[0].x;
+      O[n][2] *= ml[0].y;
+      O[n][3] *= ml[0].y;
+#pragma unroll
+      for (int k2 = 1; k2 < KV; ++k2)
+        if (k2 < a.kvsplit) {
+          const float4 tv = *reinterpret_cast<const float4*>(b0 + (k2 - 1) * kstride + n * 128);
+          O[n][0] += tv.x * ml[k2].x;
+          O[n][1] += tv.y * ml[k2].x;
+          O[n][2] += tv.z * ml[k2].y;
+          O[n][3] += tv.w * ml[k2].y;
+        }
     }
   }
-  // O / l -> bf16 attn[m][head][hd]
-  const float ia = la > 0.f ? 1.f / la : 0.f, ib = lb > 0.f ? 1.f / lb : 0.f;
+  if (lane == 0) trace_max(a.trace, 7);
+  // O / l -> bf16 attn[m][head][hd], this warp's n-tiles
+  const float ia = La > 0.f ? 1.f / La : 0.f, ib = Lb > 0.f ? 1.f / Lb : 0.f;
   const int ha = kvh * a.Gh + ra % a.Gh, hb = kvh * a.Gh + rb % a.Gh;
   __nv_bfloat16* oa = a.out + (static_cast<size_t>(r * a.T + ta) * a.Hq + ha) * HD;
   __nv_bfloat16* ob = a.out + (static_cast<size_t>(r * a.T + tb) * a.Hq + hb) * HD;
 #pragma unroll
-  for (int n = 0; n < HD / 8; ++n) {
-    const int col = 8 * n + 2 * (lane & 3);
-    if (va) *reinterpret_cast<uint32_t*>(oa + col) = pack2(o[n][0] * ia, o[n][1] * ia);
-    if (vb) *reinterpret_cast<uint32_t*>(ob + col) = pack2(o[n][2] * ib, o[n][3] * ib);
+  for (int n = 0; n < NPW; ++n) {
+    const int col = 8 * (n0 + n) + 2 * (lane & 3);
+    if (va) *reinterpret_cast<uint32_t*>(oa + col) = pack2(O[n][0] * ia, O[n][1] * ia);
+    if (vb) *reinterpret_cast<uint32_t*>(ob + col) = pack2(O[n][2] * ib, O[n][3] * ib);
   }
+  if (lane == 0) trace_max(a.trace, 2);
 }
+
+// Instantiations: (hd, in-CTA key splits) for 1, 2 or 4 row warps (hd 128 keeps 2 splits).
+#define YGG_AD_KERNELS(X) X(64, 8) X(64, 4) X(64, 2) X(128, 2)
 
 static PFN_cuTensorMapEncodeTiled_v12000 encoder() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -426,7 +521,7 @@ using namespace ygg::ad;
 extern "C" {
 
 int ygg_prepare_attn_dec(void) {
-  for (auto fn : {attn_dec_kernel<64>, attn_dec_kernel<128>}) {
+  for (auto fn : {attn_dec_kernel<64, 8>, attn_dec_kernel<64, 4>, attn_dec_kernel<64, 2>, attn_dec_kernel<128, 2>}) {
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
     if (e != cudaSuccess) return ygg_fail(YGG_ERR_CUDA, "decode attention attribute: %s", cudaGetErrorString(e));
   }
@@ -436,12 +531,11 @@ int ygg_prepare_attn_dec(void) {
 size_t ygg_attn_dec_plan_size(void) { return sizeof(Plan) + 64; }
 
 size_t ygg_attn_dec_workspace_size(const void* plan) {
-  const Plan* p = plan_of(plan);
-  if (!p) return 0;
-  const size_t groups = static_cast<size_t>(p->B) * p->Hkv * p->row_tiles;
-  const size_t nv = static_cast<size_t>(p->hd) / 8 * 4 + 4;
-  const size_t part = groups * p->kvsplit * ((p->rows + 15) / 16) * nv * 32 * sizeof(float);
-  return ((part + 255) / 256) * 256 + groups * sizeof(unsigned) + 256;
+  // Key splits merge inside a thread-block cluster (DSMEM): no global workspace.  Measured (cfg2
+  // draft, 4 splits): a global-memory merge (fence + arrival counter + last-CTA merge) cost ~5 us
+  // against ~1.7 us through the leader's shared memory.
+  (void)plan;
+  return 0;
 }
 
 int ygg_attn_dec_plan_init(void* plan, const void* q, const void* cache_layer, int B, int T, int Hq, int Hkv, int hd,
@@ -469,25 +563,43 @@ int ygg_attn_dec_plan_init(void* plan, const void* q, const void* cache_layer, i
   p->ksplit = kMaxWarps / nw;            // split the key chunks over the remaining warps
   if (hd == 128 && p->ksplit > 2) p->ksplit = 2;  // register budget of the 128-wide accumulators
   p->warps = nw * p->ksplit;
-  p->stages = hd == 64 ? 8 : 4;
+  // Key chunks are split over ksplit warp groups inside a CTA and over a (1, 1, kvsplit) cluster of
+  // CTAs; the cluster's partials meet in the leader CTA's shared memory.  Default kvsplit: enough
+  // CTAs to reach ~1/2 of the SMs, at most 4 (the in-cluster merge is serial in the leader).
+  {
+    const int ctas = B * Hkv * p->row_tiles;
+    int kv = ctas >= 74 ? 1 : (74 / ctas < 4 ? 74 / ctas : 4);
+    if (const char* e = getenv("YGG_ATTN_DEC_KVSPLIT")) kv = atoi(e);
+    const int kv_cap = hd == 128 ? 4 : 8;
+    p->kvsplit = kv < 1 ? 1 : (kv > kv_cap ? kv_cap : kv);
+  }
+  const size_t stage_bytes = 2 * static_cast<size_t>(kKC) * hd * 2;
+  const size_t merge = static_cast<size_t>(p->warps) * (hd / 8 * 4 + 4) * 32 * 4;
+  const size_t nv2 = static_cast<size_t>(hd / 8 / p->ksplit) * 4 + 4;
+  auto smem_for = [&](int kv, int st) {
+    const size_t ring = static_cast<size_t>(st) * stage_bytes;
+    const size_t slots = kv > 1 ? static_cast<size_t>(kv - 1) * p->warps * nv2 * 32 * 4 : 0;
+    return 1024 + 64 * static_cast<size_t>(hd) * 2 + ((ring > merge ? ring : merge) + 15) / 16 * 16 + slots +
+           (2 * static_cast<size_t>(st) + 2) * 8;
+  };
+  const size_t budget = 220 * 1024 - 1024;  // attribute minus the static shared word
+  while (p->kvsplit > 1 && smem_for(p->kvsplit, p->ksplit) > budget) --p->kvsplit;
+  // Stages: every stage must always feed the same key-split group (chunk j -> stage j % stages,
+  // group j % ksplit), otherwise a group can wait on a stage two phases ahead and the parity wait
+  // would pass on a stale phase — so stages is a multiple of ksplit.
+  // A cluster member walks ~1/kvsplit of the chunks: a ring of one stage per key-split group keeps
+  // the CTA small enough to sit beside the producing GEMV's CTA (its prologue then overlaps it).
+  p->stages = p->kvsplit > 1 ? p->ksplit : (hd == 64 ? 8 : 4);
   if (const char* e = getenv("YGG_ATTN_DEC_STAGES")) p->stages = atoi(e) < 2 ? 2 : (atoi(e) > 8 ? 8 : atoi(e));
-  // Every stage must always feed the same key-split group (chunk j -> stage j % stages, group
-  // j % ksplit): otherwise a group can wait on a stage two phases ahead and the parity wait would pass
-  // on a stale phase.  So stages is a multiple of ksplit.
-  const int max_st = static_cast<int>((200 * 1024 - 64 * hd * 2) / (2 * kKC * hd * 2));  // smem budget
-  if (p->stages > max_st) p->stages = max_st;
+  while (p->stages > p->ksplit && smem_for(p->kvsplit, p->stages) > budget) --p->stages;
   p->stages = (p->stages / p->ksplit) * p->ksplit;
   if (p->stages < p->ksplit) p->stages = p->ksplit;
-  // Cross-CTA key splits (merge by the last CTA of each group): off by default — same-box cfg2
-  // draft pass 0.712 ms (1), 0.718 (2), 0.713 (4), 0.734 (8); verify (forced) 3.96 / 3.95 / 4.12.
   {
-    int kv = 1;
-    if (const char* e = getenv("YGG_ATTN_DEC_KVSPLIT")) kv = atoi(e);
-    p->kvsplit = kv < 1 ? 1 : (kv > 8 ? 8 : kv);
+    const size_t ring = static_cast<size_t>(p->stages) * stage_bytes;
+    p->ring_bytes = static_cast<int>(((ring > merge ? ring : merge) + 15) / 16 * 16);
+    p->slot_bytes = p->kvsplit > 1 ? static_cast<int>(static_cast<size_t>(p->kvsplit - 1) * p->warps * nv2 * 32 * 4) : 0;
   }
-  const size_t merge = static_cast<size_t>(p->warps) * (hd / 8 * 4 + 4) * 32 * 4;
-  const size_t ring = static_cast<size_t>(p->stages) * 2 * (kKC * hd * 2);
-  p->smem = 1024 + 64 * hd * 2 + ((ring > merge ? ring : merge) + 15) / 16 * 16 + (2 * p->stages + 2) * 8;
+  p->smem = smem_for(p->kvsplit, p->stages);
   const int M = B * T;
   {  // q [M][Hq][hd]: box {64, Gh, T} -> rows (token, head-in-group); 64 rows of smem reserved
     cuuint64_t dims[3] = {static_cast<cuuint64_t>(hd), static_cast<cuuint64_t>(Hq), static_cast<cuuint64_t>(M)};
@@ -531,31 +643,24 @@ int ygg_attn_dec_run(const void* plan, const int32_t* blk_start, const int32_t* 
   a.tpt = p->tpt;
   a.kvsplit = p->kvsplit;
   a.row_tiles = p->row_tiles;
-  {
-    const size_t merge = static_cast<size_t>(p->warps) * (p->hd / 8 * 4 + 4) * 32 * 4;
-    const size_t ring = static_cast<size_t>(p->stages) * 2 * (kKC * p->hd * 2);
-    a.ring_bytes = static_cast<int>(((ring > merge ? ring : merge) + 15) / 16 * 16);
-  }
-  YGG_CHECK_ARG(p->kvsplit == 1 || workspace != nullptr, "decode attention with key splits needs a workspace");
-  {
-    const size_t groups = static_cast<size_t>(p->B) * p->Hkv * p->row_tiles;
-    const size_t nv = static_cast<size_t>(p->hd) / 8 * 4 + 4;
-    const size_t part = groups * p->kvsplit * ((p->rows + 15) / 16) * nv * 32 * sizeof(float);
-    a.part = static_cast<float*>(workspace);
-    a.ctr = workspace ? reinterpret_cast<unsigned*>(static_cast<char*>(workspace) + ((part + 255) / 256) * 256) : nullptr;
-  }
+  a.warps = p->warps;
+  a.ring_bytes = p->ring_bytes;
+  a.slot_bytes = p->slot_bytes;
+  (void)workspace;
   a.scale_log2 = scale * 1.4426950408889634f;
   a.blk_start = blk_start;
   a.blk_len = blk_len;
   a.qmask = qmask ? qmask : reinterpret_cast<const uint32_t*>(blk_start);  // never read when mask_words == 0
   a.out = static_cast<__nv_bfloat16*>(out);
+  a.trace = trace_next(2);
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   const dim3 grid(p->Hkv, p->B, p->row_tiles * p->kvsplit), block(32 * (1 + p->warps));
-  if (p->hd == 64)
-    YGG_LAUNCH_PDL(attn_dec_kernel<64>, grid, block, p->smem, s, p->tq, p->tk, p->tv, a);
-  else
-    YGG_LAUNCH_PDL(attn_dec_kernel<128>, grid, block, p->smem, s, p->tq, p->tk, p->tv, a);
-  return YGG_OK;
+#define YGG_AD_LAUNCH(H, K)                                                                                    \
+  if (p->hd == H && p->ksplit == K)                                                                            \
+    return launch_pdl_cluster_z(attn_dec_kernel<H, K>, grid, block, p->smem, p->kvsplit, s, p->tq, p->tk, p->tv, a);
+  YGG_AD_KERNELS(YGG_AD_LAUNCH)
+#undef YGG_AD_LAUNCH
+  return ygg_fail(YGG_ERR_VALUE, "decode attention: no kernel for hd %d with %d key splits", p->hd, p->ksplit);
 }
 
 }  // extern "C"

@@ -15,6 +15,18 @@ int ygg_fail(int code, const char* fmt, ...) {
   va_end(ap);
   return code;
 }
+
+namespace {
+unsigned long long* g_trace = nullptr;
+int g_trace_cap = 0, g_trace_used = 0;
+int g_trace_ids[4096];
+}  // namespace
+
+unsigned long long* trace_next(int kernel_id) {
+  if (!g_trace || g_trace_used >= g_trace_cap) return nullptr;
+  g_trace_ids[g_trace_used] = kernel_id;  // kept host-side: kernels only fill the timer fields
+  return g_trace + 8 * g_trace_used++;
+}
 }  // namespace ygg
 
 extern "C" {
@@ -29,6 +41,19 @@ int ygg_prepare_attn_dec(void);
 int ygg_version(void) { return 100; }
 
 const char* ygg_last_error(void) { return ygg::g_err; }
+
+int ygg_trace_arm(unsigned long long* buf, int slots) {
+  ygg::g_trace = slots > 0 ? buf : nullptr;
+  ygg::g_trace_cap = slots < 0 ? 0 : (slots > 4096 ? 4096 : slots);
+  ygg::g_trace_used = 0;
+  return YGG_OK;
+}
+
+int ygg_trace_used(int* kernel_ids, int cap) {
+  const int n = ygg::g_trace_used;
+  for (int i = 0; i < n && i < cap; ++i) kernel_ids[i] = ygg::g_trace_ids[i];
+  return n;
+}
 
 int ygg_device_check(int* num_sms, int* cc_major, int* cc_minor) {
   int dev = 0;

@@ -27,6 +27,22 @@ YGG_DEV uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 
+YGG_DEV unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// In-graph kernel timeline (profiling only, see ygg_trace_arm): a traced launch carries an 8-word
+// slot {first CTA start, first return from the grid-dependency wait, last CTA end, then up to five
+// kernel-specific checkpoints (latest over CTAs)}.
+YGG_DEV void trace_min(unsigned long long* slot, int field) {
+  if (slot) atomicMin(slot + field, gtimer());
+}
+YGG_DEV void trace_max(unsigned long long* slot, int field) {
+  if (slot) atomicMax(slot + field, gtimer());
+}
+
 YGG_DEV float warp_sum(float v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -86,6 +102,45 @@ YGG_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
   if (mbar_try_wait(addr, parity)) return;
   const long long t0 = clock64();
   while (!mbar_try_wait(addr, parity)) {
+    if (clock64() - t0 > (1ll << 34)) __trap();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Thread-block clusters: DSMEM stores and remote mbarrier arrivals into another CTA of the cluster.
+// ---------------------------------------------------------------------------
+YGG_DEV void cluster_sync() {  // every thread of every CTA in the cluster
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+YGG_DEV uint32_t mapa_shared(uint32_t addr, uint32_t rank) {  // this CTA's smem address -> CTA `rank`'s
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+  return r;
+}
+YGG_DEV void st_cluster_f32(uint32_t addr, float v) {
+  asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(addr), "f"(v) : "memory");
+}
+YGG_DEV void st_cluster_v4(uint32_t addr, float a, float b, float c, float d) {
+  asm volatile("st.shared::cluster.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "f"(a), "f"(b), "f"(c), "f"(d)
+               : "memory");
+}
+YGG_DEV void fence_cluster() { asm volatile("fence.acq_rel.cluster;" ::: "memory"); }
+YGG_DEV void mbar_arrive_cluster(uint32_t remote_bar) {  // release: this thread's DSMEM stores first
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote_bar) : "memory");
+}
+YGG_DEV void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {  // acquire at cluster scope, bounded
+  const uint32_t addr = smem_u32(bar);
+  const long long t0 = clock64();
+  for (;;) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.b32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(addr), "r"(parity)
+        : "memory");
+    if (ok) return;
     if (clock64() - t0 > (1ll << 34)) __trap();
   }
 }

@@ -96,11 +96,6 @@ struct EpiArgs {
   const float2* rope_cs;   // optional [positions][hd/2] (cos, sin) table; else sincosf
 };
 
-YGG_DEV unsigned long long gtimer() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  return t;
-}
 
 YGG_DEV void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
 YGG_DEV int ld_acquire(const int32_t* p) {

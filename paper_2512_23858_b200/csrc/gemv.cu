@@ -66,6 +66,7 @@ struct Epilogue {
   float* resid;            // RESID [M][N]
   __nv_bfloat16* hb;
   float* ss_out;           // RESID [N/16][M]
+  unsigned long long* trace;  // kernel-timeline slot (profiling only) or nullptr
 };
 
 struct Plan {
@@ -123,6 +124,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&empty[s], kCompute);
     }
     fence_barrier_init();
+    trace_min(e.trace, 0);
   }
   __syncthreads();
   const int nb_mine = p.nblk > static_cast<int>(blockIdx.x) ? (p.nblk - 1 - blockIdx.x) / p.grid + 1 : 0;
@@ -163,6 +165,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           ph ^= 1u;
         }
       }
+    } else {
+      pdl_wait();  // dependents may only launch once this grid is past its wait (see attn_dec.cu)
     }
     pdl_launch_dependents();
     return;
@@ -170,6 +174,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   // ===== warps 1..kCompute: mma, then (warp 1) epilogue =====
   pdl_wait();
   pdl_launch_dependents();
+  if (threadIdx.x == 32) trace_min(e.trace, 1);
   const int M = p.M;
   const int cw = warp - 1;
   // Per-token inputs of the epilogue, before the main loop: rstd from the producing residual's
@@ -261,6 +266,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     asm volatile("bar.sync 1, %0;" ::"n"(32 * kCompute) : "memory");
     if (cw != 0) continue;
+    if (lane == 0) trace_max(e.trace, 3);
     // ---- epilogue: acc[t] = {(row r0, tok n0), (r0, n0+1), (r0+8, n0), (r0+8, n0+1)}
     const int r0 = b * kRows + (lane >> 2);
 #pragma unroll
@@ -348,6 +354,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   }
+  if (cw == 0 && lane == 0) trace_max(e.trace, 2);
 }
 
 static PFN_cuTensorMapEncodeTiled_v12000 encoder() {
@@ -485,6 +492,7 @@ int ygg_gemv_run(const void* plan, const ygg_gemv_epilogue* ep, ygg_stream_t str
     default: return ygg_fail(YGG_ERR_VALUE, "unknown gemv epilogue %d", e.kind);
   }
   YGG_CHECK_ARG(!e.ss_in || (e.ss_blocks >= 1 && e.norm_dim >= 1), "bad folded-RMSNorm arguments");
+  e.trace = trace_next(1);
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   if (p.xrows == 8)
     YGG_LAUNCH_PDL(gemv_kernel<1>, dim3(p.grid), dim3(kThreads), pl->smem, s, pl->tw, pl->tx, p, e);

@@ -1,0 +1,69 @@
+"""In-graph kernel timeline of one cfg2 draft forward (GEMV path), from the kernels' own
+%globaltimer stamps (ygg_trace_arm): per launch, when its first CTA started, when its grid
+dependency released (previous kernel done), and when its last CTA finished.  Profiling only."""
+import json
+import os
+import sys
+
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import bench  # noqa: E402
+from paper_2512_23858_b200 import _lib as L  # noqa: E402
+from paper_2512_23858_b200.forward import Forward  # noqa: E402
+
+which = sys.argv[1] if len(sys.argv) > 1 else "draft"
+wl = bench.WORKLOADS["cfg2"]
+sd, tc, dc = bench.build_decoder(wl, "cfg2", torch.device("cuda"))
+sd.prefill(bench.prompts_for(wl, tc.vocab, 0))
+for _ in range(2):
+    sd.step(use_graph=False)
+torch.cuda.synchronize()
+f = sd.draft if which == "draft" else sd.verify
+g = Forward(f.cfg, f.w, f.cache, f.B, f.R, f.mask_words, f.act_dtype)
+for t in ("tokens", "pos", "slot", "req", "qmask", "blk_start", "blk_len"):
+    getattr(g, t).copy_(getattr(f, t))
+lib = L.lib()
+CAP = 512
+buf = torch.zeros(CAP, 8, dtype=torch.int64, device="cuda")
+
+
+def reset():
+    buf[:, 0] = -1  # ~0 as u64 (atomicMin fields)
+    buf[:, 1] = -1
+    buf[:, 2:] = 0
+
+
+graph = torch.cuda.CUDAGraph()
+L.check(lib.ygg_trace_arm(buf.data_ptr(), CAP))
+with torch.cuda.graph(graph):
+    g.run()
+ids = (L.C.c_int * CAP)()
+n = lib.ygg_trace_used(ids, CAP)
+L.check(lib.ygg_trace_arm(None, 0))
+for _ in range(5):
+    graph.replay()
+reset()
+torch.cuda.synchronize()
+graph.replay()
+torch.cuda.synchronize()
+t = buf[:n].cpu().tolist()
+names = {1: "gemv", 2: "attn_dec"}
+t0 = t[0][0]
+rows = []
+prev_end = None
+for i in range(n):
+    s, w, e = (t[i][0] - t0) / 1e3, (t[i][1] - t0) / 1e3, (t[i][2] - t0) / 1e3
+    gap = None if prev_end is None else round(w - prev_end, 2)
+    marks = [round((t[i][j] - t0) / 1e3 - w, 2) for j in range(3, 8) if t[i][j]]
+    rows.append({"i": i, "k": names.get(ids[i], ids[i]), "start": round(s, 2), "released": round(w, 2),
+                 "end": round(e, 2), "after_release": round(e - w, 2), "release_gap": gap, "marks": marks})
+    prev_end = e
+for r in rows:
+    print(json.dumps(r))
+tot = {}
+for r in rows:
+    key = r["k"] + ("" if r["k"] != "gemv" else f"#{r['i'] % 5 if r['i'] < n - 1 else 'lm'}")
+    tot.setdefault(key, []).append(r["after_release"])
+print(json.dumps({k: round(sum(v) / len(v), 2) for k, v in tot.items()}))
+print(json.dumps({"total_us": round((t[n - 1][2] - t0) / 1e3, 2), "launches": n}))

@@ -45,6 +45,7 @@ struct AttnArgs {
   const uint32_t* qmask;
   float* opart;  // [chunks][M*Hq][hd]
   float* ml;     // [chunks][M*Hq][2]
+  unsigned long long* trace;  // kernel-timeline slot (profiling only) or nullptr
 };
 
 YGG_DEV void tma_load_3d(void* smem_dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1, int c2) {
@@ -88,8 +89,10 @@ __global__ void __launch_bounds__(kAttnTcThreads, 1)
 
   const int chunk = blockIdx.x, qt = blockIdx.y, kvh = blockIdx.z % a.Hkv, r = blockIdx.z / a.Hkv;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) trace_min(a.trace, 0);
   pdl_wait();
   pdl_launch_dependents();
+  if (threadIdx.x == 0) trace_min(a.trace, 1);
   const int bs = a.blk_start[r], bl = a.blk_len[r];
   const int nkeys = bs + bl;
   const int key0 = chunk * kKC;
@@ -265,6 +268,7 @@ __global__ void __launch_bounds__(kAttnTcThreads, 1)
   }
   tc_fence_before();
   __syncthreads();
+  if (threadIdx.x == 0) trace_max(a.trace, 2);
   if (warp == 8) {
     tc_fence_after();
     tmem_dealloc(tmem, 256);
@@ -278,9 +282,12 @@ __global__ void __launch_bounds__(128) attn_combine_kernel(const float* __restri
                                                            const float* __restrict__ ml, int rows, int Hq, int T,
                                                            const int32_t* __restrict__ blk_start,
                                                            const int32_t* __restrict__ blk_len,
-                                                           __nv_bfloat16* __restrict__ out) {
+                                                           __nv_bfloat16* __restrict__ out,
+                                                           unsigned long long* trace) {
+  if (threadIdx.x == 0) trace_min(trace, 0);
   pdl_wait();
   pdl_launch_dependents();
+  if (threadIdx.x == 0) trace_min(trace, 1);
   const int rr = blockIdx.x * 4 + (threadIdx.x >> 5);  // m*Hq + head
   const int lane = threadIdx.x & 31;
   if (rr >= rows) return;
@@ -308,6 +315,7 @@ __global__ void __launch_bounds__(128) attn_combine_kernel(const float* __restri
   __nv_bfloat16* dst = out + static_cast<size_t>(rr) * HD + lane * DPL;
 #pragma unroll
   for (int i = 0; i < DPL; ++i) dst[i] = __float2bfloat16_rn(acc[i] * inv);
+  if (lane == 0) trace_max(trace, 2);
 }
 
 static int encode(CUtensorMap* map, int rank, const void* ptr, const cuuint64_t* dims, const cuuint64_t* strides,
@@ -426,6 +434,7 @@ int ygg_attention_tc(const void* plan, const int32_t* blk_start, const int32_t* 
   a.qmask = qmask;
   a.opart = partials;
   a.ml = partials + static_cast<size_t>(p->chunks) * p->M * p->Hq * p->hd;
+  a.trace = trace_next(8);
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   dim3 grid(p->chunks, p->q_tiles, p->Hkv * p->B);
   if (p->hd == 64)
@@ -434,14 +443,15 @@ int ygg_attention_tc(const void* plan, const int32_t* blk_start, const int32_t* 
     YGG_LAUNCH_PDL(attn_tc_kernel<128>, grid, dim3(kAttnTcThreads), attn_smem<128>(), s, p->tm_q, p->tm_k, p->tm_vt,
                    a);
   const int rows = p->M * p->Hq;
+  unsigned long long* ctrace = trace_next(9);
   if (p->hd == 64)
     YGG_LAUNCH_PDL(attn_combine_kernel<64>, dim3((rows + 3) / 4), dim3(128), 0, s, static_cast<const float*>(a.opart),
                    static_cast<const float*>(a.ml), rows, p->Hq, p->T, blk_start, blk_len,
-                   static_cast<__nv_bfloat16*>(out));
+                   static_cast<__nv_bfloat16*>(out), ctrace);
   else
     YGG_LAUNCH_PDL(attn_combine_kernel<128>, dim3((rows + 3) / 4), dim3(128), 0, s, static_cast<const float*>(a.opart),
                    static_cast<const float*>(a.ml), rows, p->Hq, p->T, blk_start, blk_len,
-                   static_cast<__nv_bfloat16*>(out));
+                   static_cast<__nv_bfloat16*>(out), ctrace);
   return YGG_OK;
 }
 

@@ -93,6 +93,7 @@ struct EpiArgs {
   int n_total;
   int32_t* counters;      // [tiles] arrival counters, self-resetting
   unsigned long long* dbg; // optional per-CTA %globaltimer stamps [num_ctas][8] (profiling only)
+  unsigned long long* trace;  // kernel-timeline slot (profiling only) or nullptr
   const float2* rope_cs;   // optional [positions][hd/2] (cos, sin) table; else sincosf
 };
 
@@ -271,6 +272,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   if (e.dbg && threadIdx.x == 0) e.dbg[c * 8 + 0] = gtimer();
+  if (threadIdx.x == 0) trace_min(e.trace, 0);
   pdl_launch_dependents();
 
   // Processing order of this CTA's range: the (possibly split) first and last tiles first, then
@@ -324,6 +326,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         advance();
       }
       pdl_wait();
+      trace_min(e.trace, 1);
       for (int i = 0; i < pre; ++i)
         tma_load_2d(sb + static_cast<size_t>(i) * b_bytes, &tmap_x, &full[i], pre_kblk[i] * kBK, pre_xrow[i], pol_x);
       int stage = pre % S;
@@ -495,6 +498,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     if (e.dbg && et == 0) e.dbg[c * 8 + 4] = gtimer();
   }
   __syncthreads();
+  if (threadIdx.x == 0) trace_max(e.trace, 2);
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc(tmem_base, p.tmem_cols);
@@ -559,6 +563,7 @@ __global__ void __launch_bounds__(256) gemm_f32_simt_kernel(const float* __restr
 struct EpiGeom {
   int M, N, BN, m_tiles;
   const int32_t* seg_first;
+  unsigned long long* trace;  // kernel-timeline slot (profiling only) or nullptr
 };
 
 YGG_DEV float epi_value(const EpiGeom& g, const float* __restrict__ ws, int m, int n) {
@@ -671,14 +676,17 @@ constexpr int kEpiThreads = 128;  // x 8 features = 1024 features per CTA
 template <typename OutT>
 __global__ void __launch_bounds__(kEpiThreads) epi_store_kernel(EpiGeom g, const float* __restrict__ ws,
                                                                 OutT* __restrict__ out, int ld) {
+  if (threadIdx.x == 0) trace_min(g.trace, 0);
   pdl_wait();
   pdl_launch_dependents();
+  if (threadIdx.x == 0) trace_min(g.trace, 1);
   const int m = blockIdx.y;
   const int n = (blockIdx.x * blockDim.x + threadIdx.x) * 8;
   if (n >= g.N) return;
   float v[8];
   epi_values<8>(g, ws, m, n, v);
   store8<OutT>(out + static_cast<size_t>(m) * ld + n, v);
+  if (threadIdx.x == 0) trace_max(g.trace, 2);
 }
 
 YGG_DEV uint32_t cluster_ctarank() {
@@ -705,8 +713,10 @@ __global__ void __launch_bounds__(1024) epi_residual_norm_kernel(EpiGeom g, cons
                                                                  float* __restrict__ resid,
                                                                  const ActT* __restrict__ norm_w, float eps,
                                                                  ActT* __restrict__ xn) {
+  if (threadIdx.x == 0) trace_min(g.trace, 0);
   pdl_wait();
   pdl_launch_dependents();
+  if (threadIdx.x == 0) trace_min(g.trace, 1);
   __shared__ float red[32];
   const int m = blockIdx.x;
   const int n = threadIdx.x * 8;
@@ -737,13 +747,16 @@ __global__ void __launch_bounds__(1024) epi_residual_norm_kernel(EpiGeom g, cons
     for (int i = 0; i < 8; ++i) h[i] = h[i] * rs * w[i];
     store8<ActT>(xn + static_cast<size_t>(m) * g.N + n, h);
   }
+  if (threadIdx.x == 0) trace_max(g.trace, 2);
 }
 
 template <typename ActT>
 __global__ void __launch_bounds__(kEpiThreads) epi_swiglu_kernel(EpiGeom g, const float* __restrict__ ws,
                                                                  ActT* __restrict__ out) {
+  if (threadIdx.x == 0) trace_min(g.trace, 0);
   pdl_wait();
   pdl_launch_dependents();
+  if (threadIdx.x == 0) trace_min(g.trace, 1);
   const int m = blockIdx.y;
   const int F = g.N / 2;
   const int f = (blockIdx.x * blockDim.x + threadIdx.x) * 8;
@@ -753,6 +766,7 @@ __global__ void __launch_bounds__(kEpiThreads) epi_swiglu_kernel(EpiGeom g, cons
 #pragma unroll
   for (int i = 0; i < 8; ++i) o[i] = gate[i] / (1.f + expf(-gate[i])) * up[i];
   store8<ActT>(out + static_cast<size_t>(m) * F + f, o);
+  if (threadIdx.x == 0) trace_max(g.trace, 2);
 }
 
 // QKV epilogue: RoPE (rotate-half convention) on q and k at pos[m]; q -> q_out, k/v -> KV cache.
@@ -765,8 +779,10 @@ __global__ void __launch_bounds__(256) epi_qkv_rope_kernel(EpiGeom g, const floa
                                                            const int32_t* __restrict__ req, ActT* __restrict__ q_out,
                                                            ActT* __restrict__ cache, int S,
                                                            const float2* __restrict__ rope_cs) {
+  if (threadIdx.x == 0) trace_min(g.trace, 0);
   pdl_wait();
   pdl_launch_dependents();
+  if (threadIdx.x == 0) trace_min(g.trace, 1);
   const int m = blockIdx.x;
   const int half = hd / 2;
   const int per_head = half / 4;
@@ -829,6 +845,7 @@ __global__ void __launch_bounds__(256) epi_qkv_rope_kernel(EpiGeom g, const floa
       }
     }
   }
+  if (threadIdx.x == 0) trace_max(g.trace, 2);
 }
 
 // ---------------------------------------------------------------------------
@@ -865,7 +882,9 @@ static const GemmPlan* as_plan(const void* p) {
   return (g && g->magic == kPlanMagic) ? g : nullptr;
 }
 
-static EpiGeom geom_of(const GemmPlan* g) { return EpiGeom{g->M, g->N, g->BN, g->m_tiles, g->seg_table}; }
+static EpiGeom geom_of(const GemmPlan* g, int kernel_id) {
+  return EpiGeom{g->M, g->N, g->BN, g->m_tiles, g->seg_table, trace_next(kernel_id)};
+}
 
 }  // namespace ygg
 
@@ -1006,6 +1025,7 @@ static int gemm_launch(const GemmPlan* g, float* workspace, const ygg_epilogue* 
     const size_t smem = kSmemExtra + static_cast<size_t>(g->stages) * (kBM * kBK * 2 + g->BN * kBK * 2);
     EpiArgs e;
     std::memset(&e, 0, sizeof(e));
+    e.trace = trace_next(3);
     int kind = kEpiNone;
     if (epi) {
       kind = epi->kind;
@@ -1100,7 +1120,7 @@ int ygg_epi_store(const void* plan, const float* ws, void* out, int out_dtype, i
   const GemmPlan* g = plan_of(plan);
   YGG_CHECK_ARG(g && ws && out, "invalid arguments");
   YGG_CHECK_ARG(ld_out >= g->N, "ld_out < N");
-  EpiGeom geo = geom_of(g);
+  EpiGeom geo = geom_of(g, 4);
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   YGG_CHECK_ARG(ld_out % 8 == 0, "ld_out must be a multiple of 8");
   dim3 grid((g->N + 1023) / 1024, g->M);
@@ -1117,7 +1137,7 @@ int ygg_epi_residual_norm(const void* plan, const float* ws, float* resid, const
   const GemmPlan* g = plan_of(plan);
   YGG_CHECK_ARG(g && ws && resid && norm_w && xn_out, "invalid arguments");
   YGG_CHECK_ARG(g->N % 8 == 0 && g->N / 8 <= 1024, "row wider than 8192 features");
-  EpiGeom geo = geom_of(g);
+  EpiGeom geo = geom_of(g, 5);
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   const int threads = ((g->N / 8 + 31) / 32) * 32;
   if (act_dtype == YGG_F32)
@@ -1133,7 +1153,7 @@ int ygg_epi_swiglu(const void* plan, const float* ws, void* out, int act_dtype, 
   const GemmPlan* g = plan_of(plan);
   YGG_CHECK_ARG(g && ws && out, "invalid arguments");
   YGG_CHECK_ARG(g->N % 2 == 0, "gate_up width must be even");
-  EpiGeom geo = geom_of(g);
+  EpiGeom geo = geom_of(g, 6);
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   dim3 grid((g->N / 2 + 1023) / 1024, g->M);
   if (act_dtype == YGG_F32)
@@ -1151,7 +1171,7 @@ int ygg_epi_qkv_rope(const void* plan, const float* ws, int Hq, int Hkv, int hd,
   YGG_CHECK_ARG(g && ws && pos && slot && req && q_out && cache, "invalid arguments");
   YGG_CHECK_ARG(g->N == (Hq + 2 * Hkv) * hd, "QKV width mismatch");
   YGG_CHECK_ARG(hd % 8 == 0 && hd <= 256, "bad head dim");
-  EpiGeom geo = geom_of(g);
+  EpiGeom geo = geom_of(g, 7);
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   const int items = (Hq + 2 * Hkv) * (hd / 8);
   dim3 grid(g->M, (items + 255) / 256);

@@ -196,6 +196,19 @@ class Forward:
                 self.ad_plans.append(mem)
             self.ad_ws = torch.zeros(int(lib.ygg_attn_dec_workspace_size(self.ad_plans[0])) // 4 + 64,
                                      dtype=torch.float32, device=dev)
+        # Unfused bf16 LM head: whole output tiles go straight from TMEM to the f32 logits and only the
+        # split stream-K tiles are reduced (in fixed segment order, by their participants) — the
+        # [M, V] f32 partials round trip and the separate store epilogue disappear.  Same values.
+        self.lm_epi = None
+        if (bf16 and not self.fused and self.lm_plan is not None
+                and os.environ.get("YGG_LM_FUSED", "1") != "0"):
+            self.lm_counters = torch.zeros(self.lm_plan.tiles, dtype=torch.int32, device=dev)
+            e = L.YggEpilogue()
+            e.kind = L.YGG_EPI_STORE_F32
+            e.counters = self.lm_counters.data_ptr()
+            e.out = self.logits.data_ptr()
+            e.ld = cfg.vocab
+            self.lm_epi = e
         if self.fused:
             self._setup_fused()
         if self.mk:
@@ -516,8 +529,11 @@ class Forward:
                                               cfg.norm_eps, self.xn.data_ptr(), self.act, s))
             stamp()
         if self.lm_plan is not None and "lm" not in ko:
-            chk(lib.ygg_gemm_run(self.lm_plan.handle, ws, s))
-            chk(lib.ygg_epi_store(self.lm_plan.handle, ws, self.logits.data_ptr(), L.YGG_F32, cfg.vocab, s))
+            if self.lm_epi is not None:
+                chk(lib.ygg_gemm_fused(self.lm_plan.handle, ws, C.byref(self.lm_epi), s))
+            else:
+                chk(lib.ygg_gemm_run(self.lm_plan.handle, ws, s))
+                chk(lib.ygg_epi_store(self.lm_plan.handle, ws, self.logits.data_ptr(), L.YGG_F32, cfg.vocab, s))
             stamp()
 
 

@@ -48,7 +48,8 @@ torch.cuda.synchronize()
 graph.replay()
 torch.cuda.synchronize()
 t = buf[:n].cpu().tolist()
-names = {1: "gemv", 2: "attn_dec"}
+names = {1: "gemv", 2: "attn_dec", 3: "gemm", 4: "epi_store", 5: "epi_resid", 6: "epi_swiglu", 7: "epi_qkv",
+         8: "attn_tc", 9: "attn_combine"}
 t0 = t[0][0]
 rows = []
 prev_end = None
@@ -61,9 +62,22 @@ for i in range(n):
     prev_end = e
 for r in rows:
     print(json.dumps(r))
-tot = {}
+tot, gaps, seen = {}, {}, {}
 for r in rows:
-    key = r["k"] + ("" if r["k"] != "gemv" else f"#{r['i'] % 5 if r['i'] < n - 1 else 'lm'}")
+    k = r["k"]
+    seen[k] = seen.get(k, 0) + 1
+    per_layer = {"gemv": 5, "gemm": 4, "epi_resid": 2}.get(k)  # gemv: qkv/attn/o/gu/down slots by index
+    if k == "gemv":
+        key = f"gemv#{r['i'] % 5 if r['i'] < n - 1 else 'lm'}"
+    elif per_layer:
+        key = f"{k}#{(seen[k] - 1) % per_layer}"
+    else:
+        key = k
     tot.setdefault(key, []).append(r["after_release"])
-print(json.dumps({k: round(sum(v) / len(v), 2) for k, v in tot.items()}))
+    if r["release_gap"] is not None:
+        gaps.setdefault(key, []).append(r["release_gap"])
+print(json.dumps({k: [round(sum(v) / len(v), 2), len(v)] for k, v in tot.items()}))
+print(json.dumps({"gap_" + k: round(sum(v) / len(v), 2) for k, v in gaps.items()}))
+print(json.dumps({"sum_after_release": round(sum(sum(v) for v in tot.values()), 1),
+                  "sum_gaps": round(sum(sum(v) for v in gaps.values()), 1)}))
 print(json.dumps({"total_us": round((t[n - 1][2] - t0) / 1e3, 2), "launches": n}))

@@ -564,11 +564,12 @@ int ygg_attn_dec_plan_init(void* plan, const void* q, const void* cache_layer, i
   if (hd == 128 && p->ksplit > 2) p->ksplit = 2;  // register budget of the 128-wide accumulators
   p->warps = nw * p->ksplit;
   // Key chunks are split over ksplit warp groups inside a CTA and over a (1, 1, kvsplit) cluster of
-  // CTAs; the cluster's partials meet in the leader CTA's shared memory.  Default kvsplit: enough
-  // CTAs to reach ~1/2 of the SMs, at most 4 (the in-cluster merge is serial in the leader).
+  // CTAs; the cluster's partials meet in the leader CTA's shared memory.  Default kvsplit: as many
+  // CTAs as fit one wave, at most 4 (measured: cfg2 draft 8 CTAs -> 4 splits best, 8 slower; cfg2
+  // verify 32 CTAs -> 4 splits 9.8 us per layer, 2 splits 11.8, 1 split 14.5).
   {
     const int ctas = B * Hkv * p->row_tiles;
-    int kv = ctas >= 74 ? 1 : (74 / ctas < 4 ? 74 / ctas : 4);
+    int kv = ctas >= 148 ? 1 : (148 / ctas < 4 ? 148 / ctas : 4);
     if (const char* e = getenv("YGG_ATTN_DEC_KVSPLIT")) kv = atoi(e);
     const int kv_cap = hd == 128 ? 4 : 8;
     p->kvsplit = kv < 1 ? 1 : (kv > kv_cap ? kv_cap : kv);

@@ -310,8 +310,9 @@ class ARDecoder:
         self.dev = torch.device(device)
         self.cache = new_cache(cfg, batch, self.S, act_dtype, self.dev)
         # AR is the oracle of the lossless-greedy identity, so it runs the same kernel families as the
-        # verify pass (stream-K GEMM, split-KV tcgen05 attention), not the draft's GEMV / decode attention.
-        self.fwd = Forward(cfg, w, self.cache, batch, 1, 1, act_dtype, gemv=False, decode_attn=False)
+        # verify pass (stream-K GEMM and the cluster decode attention of tree passes that fit one
+        # wave), not the draft's GEMV.
+        self.fwd = Forward(cfg, w, self.cache, batch, 1, 1, act_dtype, gemv=False)
         self.fwd.qmask.fill_(1)
         self.argmax = torch.zeros(batch, dtype=torch.int32, device=self.dev)
         self.P = torch.zeros(batch, dtype=torch.int32, device=self.dev)

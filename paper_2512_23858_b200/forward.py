@@ -175,17 +175,19 @@ class Forward:
                                for li in range(cfg.n_layers)]
             self.attn_part = torch.empty(self.attn_plans[0].partial_bytes // 4 + 1, dtype=torch.float32, device=dev)
         self.rope_cs = rope_table(cfg, self.S + 64, dev)
-        # Decode attention (csrc/attn_dec.cu) when one kv head's query rows fit one 64-row tile (draft
-        # levels, AR): one CTA per (kv head, request), no split-KV partials / combine launch.  Wider
-        # passes (verify: 50 tokens x 4 heads) and prefill keep the split-KV tcgen05 kernel, which is
-        # faster there (measured same-box: verify 4.37 ms vs 4.41 ms with the decode kernel).
+        # Decode attention (csrc/attn_dec.cu: clusters of CTAs per (kv head, request, 64-row tile), no
+        # split-KV partials / combine launch) for draft levels and AR (one kv head's rows fit one tile)
+        # and for tree passes whose row tiles fit one wave (the cfg2 verify: 50 tokens x 4 heads = 4
+        # tiles x 8 kv heads; measured in-graph 9.8 us per layer vs 13.8 for tcgen05 split-KV +
+        # combine).  Prefill and wide batched verifies keep the split-KV tcgen05 kernel.
         self.ad_plans = None
         gh = cfg.n_heads // cfg.n_kv_heads
         force_dec = os.environ.get("YGG_ATTN_DEC") == "2"  # A/B: decode attention for every tree pass
         if decode_attn is None:
             decode_attn = os.environ.get("YGG_ATTN_DEC", "1") != "0"
+        tree_fits = mask_words > 0 and B * cfg.n_kv_heads * ((R * gh + 63) // 64) <= 148
         if (decode_attn and act_dtype == torch.bfloat16 and mask_words <= L.MAX_MASK_WORDS
-                and (R * gh <= 64 or (force_dec and mask_words > 0))):
+                and (R * gh <= 64 or tree_fits or (force_dec and mask_words > 0))):
             lib = L.lib()
             es = cache.element_size()
             self.ad_plans = []

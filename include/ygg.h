@@ -102,6 +102,11 @@ int ygg_device_check(int* num_sms, int* cc_major, int* cc_minor);
  * logits: [rows, ld] f32 or bf16.  out_tok [rows,k], out_prob [rows,k] (f64 of the f32 value),
  * out_stats [rows,2] (row max, log-sum-exp) or NULL.  workspace >= ygg_topk_workspace(rows,V,k). */
 size_t ygg_topk_workspace(int rows, int V, int k);
+/* Merge per-chunk top-k partials [rows][nchunks] (nchunks <= 1024; written by the LM-head GEMV's
+ * STORE_TOPK epilogue) into the same outputs as ygg_topk_softmax. */
+size_t ygg_topk_partial_bytes(int rows, int nchunks);
+int ygg_topk_merge(const void* partials, int rows, int nchunks, int k, int32_t* out_tok, double* out_prob,
+                   float* out_stats, ygg_stream_t stream);
 int ygg_topk_softmax(const void* logits, int dtype, int rows, int V, int ld, int k, float temperature,
                      int32_t* out_tok, double* out_prob, float* out_stats, void* workspace,
                      size_t workspace_bytes, ygg_stream_t stream);
@@ -294,7 +299,10 @@ int ygg_trace_used(int* kernel_ids, int cap);
  * (no split-K partials).  Weights in the fused layout (model.prepare_fused_): RMSNorm gains folded,
  * QKV rows RoPE-pair interleaved, gate/up rows interleaved.  ss_in / ss_out are per-block sums of
  * squares of the un-normalised residual ([blocks][M]); the consumer applies rstd. */
-typedef enum { YGG_GEMV_STORE = 1, YGG_GEMV_QKV = 2, YGG_GEMV_SWIGLU = 3, YGG_GEMV_RESID = 4 } ygg_gemv_kind;
+typedef enum {
+  YGG_GEMV_STORE = 1, YGG_GEMV_QKV = 2, YGG_GEMV_SWIGLU = 3, YGG_GEMV_RESID = 4,
+  YGG_GEMV_STORE_TOPK = 5  /* STORE + per-CTA top-k partials of every token row (M <= 8, k <= 8) */
+} ygg_gemv_kind;
 typedef struct {
   int32_t kind;
   float* out;            /* STORE: [M][ld] f32 */
@@ -312,8 +320,12 @@ typedef struct {
   float* resid;          /* RESID: [M][N] f32, updated in place */
   void* hb;              /* RESID: bf16 copy of the residual */
   float* ss_out;         /* RESID: [N/16][M] */
+  void* topk_part;       /* STORE_TOPK: >= ygg_topk_partial_bytes(M, ygg_gemv_grid(plan)) bytes */
+  int32_t topk_k;        /* STORE_TOPK: 1..8 */
+  float inv_temp;        /* STORE_TOPK: 1 / temperature applied to the logits before softmax / ranking */
 } ygg_gemv_epilogue;
 size_t ygg_gemv_plan_size(void);
+int ygg_gemv_grid(const void* plan);  /* CTAs of the plan = top-k chunks per row of STORE_TOPK */
 int ygg_gemv_plan_init(void* plan, const void* W, const void* X, int M, int N, int K, int num_ctas);
 int ygg_gemv_run(const void* plan, const ygg_gemv_epilogue* epi, ygg_stream_t stream);
 

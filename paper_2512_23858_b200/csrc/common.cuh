@@ -43,6 +43,18 @@ YGG_DEV void trace_max(unsigned long long* slot, int field) {
   if (slot) atomicMax(slot + field, gtimer());
 }
 
+// Top-k partial of one (row, chunk of the vocabulary): chunk max, f64 sum of exp(x - max) over the
+// chunk, and the chunk's best k (logit desc, token asc; token -1 = none).  Written by topk phase 1
+// (tree.cu) or by the LM-head GEMV epilogue (gemv.cu); merged by ygg_topk_merge.
+constexpr int kTopkMaxK = 32;
+struct TopkPartial {
+  float max_s;
+  double sum_exp;
+  float val[kTopkMaxK];
+  int32_t tok[kTopkMaxK];
+};
+YGG_DEV bool topk_better(float va, int ta, float vb, int tb) { return va > vb || (va == vb && ta < tb); }
+
 YGG_DEV float warp_sum(float v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);

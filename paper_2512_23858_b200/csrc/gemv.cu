@@ -37,11 +37,11 @@ constexpr int kRows = 16;       // weight rows per block (mma M)
 constexpr int kSub = 8;         // 64-wide k sub-chunks per stage
 constexpr int kStageK = kSub * 64;
 constexpr int kCompute = 4;                 // compute warps; warp w takes sub-chunks {2w, 2w+1} of a stage
-constexpr int kThreads = 32 * (1 + kCompute);
+constexpr int kThreads = 32 * (2 + kCompute);  // producer, kCompute mma warps, epilogue warp
 constexpr int kMaxTok = 16;
 constexpr uint32_t kMagic = 0x59474756u;  // "YGGV"
 
-enum Epi : int { kNone = 0, kStore = 1, kQkv = 2, kSwiglu = 3, kResid = 4 };
+enum Epi : int { kNone = 0, kStore = 1, kQkv = 2, kSwiglu = 3, kResid = 4, kStoreTopk = 5 };
 
 struct Params {
   int M, N, K, nblk, kchunks, stages, xrows, grid;
@@ -67,7 +67,56 @@ struct Epilogue {
   __nv_bfloat16* hb;
   float* ss_out;           // RESID [N/16][M]
   unsigned long long* trace;  // kernel-timeline slot (profiling only) or nullptr
+  TopkPartial* topk_part;     // STORE_TOPK: [M][grid] per-CTA partials (merged by ygg_topk_merge)
+  int topk_k;                 // STORE_TOPK: k <= kTopkLane
+  float inv_temp;             // STORE_TOPK: logits scale before the softmax / ranking
 };
+
+constexpr int kTopkLane = 8;  // per-lane candidate list of the fused top-k epilogue
+
+// Named barriers 1..4 between the mma warps and the epilogue warp (immediate ids: a register id
+// would make ptxas reserve all 16).
+YGG_DEV void named_sync(int id) {
+  constexpr int n = 32 * (kCompute + 1);
+  switch (id) {
+    case 1: asm volatile("bar.sync 1, %0;" ::"n"(n) : "memory"); break;
+    case 2: asm volatile("bar.sync 2, %0;" ::"n"(n) : "memory"); break;
+    case 3: asm volatile("bar.sync 3, %0;" ::"n"(n) : "memory"); break;
+    default: asm volatile("bar.sync 4, %0;" ::"n"(n) : "memory"); break;
+  }
+}
+YGG_DEV void named_arrive(int id) {
+  constexpr int n = 32 * (kCompute + 1);
+  switch (id) {
+    case 1: asm volatile("bar.arrive 1, %0;" ::"n"(n) : "memory"); break;
+    case 2: asm volatile("bar.arrive 2, %0;" ::"n"(n) : "memory"); break;
+    case 3: asm volatile("bar.arrive 3, %0;" ::"n"(n) : "memory"); break;
+    default: asm volatile("bar.arrive 4, %0;" ::"n"(n) : "memory"); break;
+  }
+}
+
+// Insert (v, t) into a lane's sorted list (logit desc, token asc); the caller checked that it beats
+// the last entry.  Static indices only, so the list stays in registers.
+YGG_DEV void topk_insert(float (&lv)[kTopkLane], int (&lt)[kTopkLane], float v, int t) {
+  bool done = false;
+#pragma unroll
+  for (int i = kTopkLane - 1; i >= 1; --i) {
+    if (!done) {
+      if (topk_better(v, t, lv[i - 1], lt[i - 1])) {
+        lv[i] = lv[i - 1];
+        lt[i] = lt[i - 1];
+      } else {
+        lv[i] = v;
+        lt[i] = t;
+        done = true;
+      }
+    }
+  }
+  if (!done) {
+    lv[0] = v;
+    lt[0] = t;
+  }
+}
 
 struct Plan {
   uint32_t magic;
@@ -100,7 +149,7 @@ YGG_DEV void mma16816(float* d, uint32_t a0, uint32_t a1, uint32_t a2, uint32_t 
       : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
 }
 
-template <int NT>  // token tiles of 8 (1: M <= 8, 2: M <= 16)
+template <int NT, bool TOPK>  // token tiles of 8 (1: M <= 8, 2: M <= 16); TOPK: STORE_TOPK epilogue (NT == 1)
 __global__ void __launch_bounds__(kThreads, 1)
     gemv_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ CUtensorMap tx, Params p, Epilogue e) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
@@ -114,7 +163,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* empty = full + S;
   float* rstd_s = reinterpret_cast<float*>(empty + S);
   int* tok_s = reinterpret_cast<int*>(rstd_s + kMaxTok);  // [3][kMaxTok] pos, slot, req
-  float* red = reinterpret_cast<float*>(tok_s + 3 * kMaxTok);  // [kCompute][NT][4][32] partial accumulators
+  float* red = reinterpret_cast<float*>(tok_s + 3 * kMaxTok);  // [2][kCompute][NT][4][32] partial accumulators
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     tma_prefetch_desc(&tw);
@@ -171,101 +220,131 @@ __global__ void __launch_bounds__(kThreads, 1)
     pdl_launch_dependents();
     return;
   }
-  // ===== warps 1..kCompute: mma, then (warp 1) epilogue =====
-  pdl_wait();
-  pdl_launch_dependents();
-  if (threadIdx.x == 32) trace_min(e.trace, 1);
-  const int M = p.M;
-  const int cw = warp - 1;
-  // Per-token inputs of the epilogue, before the main loop: rstd from the producing residual's
-  // per-block sums of squares (lanes split the blocks, fixed-order tree reduction), and the
-  // position / slot / request of each token row.
-  if (e.ss_in) {
-    float part[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const int n = cw + 4 * k;
-      if (n < M)
-        for (int j = lane; j < e.ss_blocks; j += 32) part[k] += __ldg(e.ss_in + static_cast<size_t>(j) * M + n);
+  // ===== warps 1..kCompute: mma; warp kCompute + 1: epilogue of the blocks they finish =====
+  if (warp <= kCompute) {
+    pdl_wait();
+    pdl_launch_dependents();
+    if (threadIdx.x == 32) trace_min(e.trace, 1);
+    const int M = p.M;
+    const int cw = warp - 1;
+    // Per-token inputs of the epilogue, before the main loop: rstd from the producing residual's
+    // per-block sums of squares (lanes split the blocks, fixed-order tree reduction), and the
+    // position / slot / request of each token row.
+    if (e.ss_in) {
+      float part[4] = {0.f, 0.f, 0.f, 0.f};
+  #pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int n = cw + 4 * k;
+        if (n < M)
+          for (int j = lane; j < e.ss_blocks; j += 32) part[k] += __ldg(e.ss_in + static_cast<size_t>(j) * M + n);
+      }
+  #pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        float v = part[k];
+  #pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        const int n = cw + 4 * k;
+        if (lane == 0 && n < M) rstd_s[n] = rsqrtf(v / static_cast<float>(e.norm_dim) + e.eps);
+      }
     }
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      float v = part[k];
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-      const int n = cw + 4 * k;
-      if (lane == 0 && n < M) rstd_s[n] = rsqrtf(v / static_cast<float>(e.norm_dim) + e.eps);
+    if (e.kind == kQkv && cw == 0 && lane < M) {
+      tok_s[lane] = __ldg(e.pos + lane);
+      tok_s[kMaxTok + lane] = __ldg(e.slot + lane);
+      tok_s[2 * kMaxTok + lane] = __ldg(e.req + lane);
     }
-  }
-  if (e.kind == kQkv && cw == 0 && lane < M) {
-    tok_s[lane] = __ldg(e.pos + lane);
-    tok_s[kMaxTok + lane] = __ldg(e.slot + lane);
-    tok_s[2 * kMaxTok + lane] = __ldg(e.req + lane);
-  }
-  const uint32_t sw0 = smem_u32(sw), sx0 = smem_u32(sx);
-  // ldmatrix lane roles: A (x4): row = (l & 7) + 8*((l >> 3) & 1), 16B chunk hi = l >> 4.
-  const int a_row = (lane & 7) + 8 * ((lane >> 3) & 1), a_hi = lane >> 4;
-  // B (x2 per token tile): token row = l & 7 (+8 for the second tile), 16B chunk hi = (l >> 3) & 1.
-  const int b_row = lane & 7, b_hi = (lane >> 3) & 1;
-  const int xrow_bytes = p.xrows * 128;
-  int st = 0;
-  uint32_t ph = 0;
-  for (int bi = 0; bi < nb_mine; ++bi) {
-    const int b = blockIdx.x + bi * p.grid;
-    float acc[NT][4], acc2[NT][4];
-#pragma unroll
-    for (int t = 0; t < NT; ++t)
-#pragma unroll
-      for (int j = 0; j < 4; ++j) acc[t][j] = acc2[t][j] = 0.f;
-    for (int q = 0; q < p.kchunks; ++q) {
-      mbar_wait(&full[st], ph);
-      const uint32_t ws = sw0 + st * w_bytes, xs = sx0 + st * x_bytes;
-#pragma unroll
-      for (int uu = 0; uu < 2; ++uu) {
-        const int u = 2 * cw + uu;
-        const uint32_t wu = ws + u * (kRows * 128);
-        const uint32_t xu = xs + u * xrow_bytes;
-#pragma unroll
-        for (int s4 = 0; s4 < 4; ++s4) {
-          uint32_t a0, a1, a2, a3;
-          const int ja = 2 * s4 + a_hi;
-          ldsm_x4(wu + a_row * 128 + ((ja ^ (a_row & 7)) << 4), a0, a1, a2, a3);
-          const int jb = 2 * s4 + b_hi;
-#pragma unroll
-          for (int t = 0; t < NT; ++t) {
-            const int r = b_row + 8 * t;
-            uint32_t b0, b1;
-            ldsm_x2(xu + r * 128 + ((jb ^ (r & 7)) << 4), b0, b1);
-            mma16816((s4 & 1) ? acc2[t] : acc[t], a0, a1, a2, a3, b0, b1);
+    const uint32_t sw0 = smem_u32(sw), sx0 = smem_u32(sx);
+    // ldmatrix lane roles: A (x4): row = (l & 7) + 8*((l >> 3) & 1), 16B chunk hi = l >> 4.
+    const int a_row = (lane & 7) + 8 * ((lane >> 3) & 1), a_hi = lane >> 4;
+    // B (x2 per token tile): token row = l & 7 (+8 for the second tile), 16B chunk hi = (l >> 3) & 1.
+    const int b_row = lane & 7, b_hi = (lane >> 3) & 1;
+    const int xrow_bytes = p.xrows * 128;
+    int st = 0;
+    uint32_t ph = 0;
+    for (int bi = 0; bi < nb_mine; ++bi) {
+      const int b = blockIdx.x + bi * p.grid;
+      float acc[NT][4], acc2[NT][4];
+  #pragma unroll
+      for (int t = 0; t < NT; ++t)
+  #pragma unroll
+        for (int j = 0; j < 4; ++j) acc[t][j] = acc2[t][j] = 0.f;
+      for (int q = 0; q < p.kchunks; ++q) {
+        mbar_wait(&full[st], ph);
+        const uint32_t ws = sw0 + st * w_bytes, xs = sx0 + st * x_bytes;
+  #pragma unroll
+        for (int uu = 0; uu < 2; ++uu) {
+          const int u = 2 * cw + uu;
+          const uint32_t wu = ws + u * (kRows * 128);
+          const uint32_t xu = xs + u * xrow_bytes;
+  #pragma unroll
+          for (int s4 = 0; s4 < 4; ++s4) {
+            uint32_t a0, a1, a2, a3;
+            const int ja = 2 * s4 + a_hi;
+            ldsm_x4(wu + a_row * 128 + ((ja ^ (a_row & 7)) << 4), a0, a1, a2, a3);
+            const int jb = 2 * s4 + b_hi;
+  #pragma unroll
+            for (int t = 0; t < NT; ++t) {
+              const int r = b_row + 8 * t;
+              uint32_t b0, b1;
+              ldsm_x2(xu + r * 128 + ((jb ^ (r & 7)) << 4), b0, b1);
+              mma16816((s4 & 1) ? acc2[t] : acc[t], a0, a1, a2, a3, b0, b1);
+            }
           }
         }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[st]);
+        if (++st == S) {
+          st = 0;
+          ph ^= 1u;
+        }
       }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[st]);
-      if (++st == S) {
-        st = 0;
-        ph ^= 1u;
-      }
-    }
-    // Sum the compute warps' partial accumulators in fixed warp order; warp 1 runs the epilogue.
-#pragma unroll
-    for (int t = 0; t < NT; ++t)
-#pragma unroll
-      for (int j = 0; j < 4; ++j) red[((cw * NT + t) * 4 + j) * 32 + lane] = acc[t][j] + acc2[t][j];
-    asm volatile("bar.sync 1, %0;" ::"n"(32 * kCompute) : "memory");
-    if (cw == 0) {
+      // Hand the partial accumulators to the epilogue warp through a double-buffered scratch:
+      // slot bi & 1 is free again once the epilogue warp has read block bi - 2 (named barriers
+      // 3 / 4 = empty, 1 / 2 = full; 128 compute + 32 epilogue threads each).
+      if (bi >= 2) named_sync(3 + (bi & 1));
+      float* rs = red + (bi & 1) * (kCompute * NT * 4 * 32);
 #pragma unroll
       for (int t = 0; t < NT; ++t)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          float v = 0.f;
-#pragma unroll
-          for (int w = 0; w < kCompute; ++w) v += red[((w * NT + t) * 4 + j) * 32 + lane];
-          acc[t][j] = v;
-        }
+        for (int j = 0; j < 4; ++j) rs[((cw * NT + t) * 4 + j) * 32 + lane] = acc[t][j] + acc2[t][j];
+      named_arrive(1 + (bi & 1));
     }
-    asm volatile("bar.sync 1, %0;" ::"n"(32 * kCompute) : "memory");
-    if (cw != 0) continue;
+    return;
+  }
+  // ===== warp kCompute + 1: epilogue (sums the compute warps' partials in fixed warp order) =====
+  pdl_wait();
+  pdl_launch_dependents();
+  const int M = p.M;
+  // STORE_TOPK (NT == 1 only): per lane and token slot q (token 2*(lane&3) + q) a running max / f64
+  // sum of exp and a sorted top-kTopkLane list over this lane's rows of every block.
+  constexpr int TQ = TOPK ? 2 : 1;
+  float tk_m[TQ], tk_v[TQ][kTopkLane];
+  double tk_s[TQ];
+  int tk_t[TQ][kTopkLane];
+#pragma unroll
+  for (int q = 0; q < TQ; ++q) {
+    tk_m[q] = -INFINITY;
+    tk_s[q] = 0.0;
+#pragma unroll
+    for (int i = 0; i < kTopkLane; ++i) {
+      tk_v[q][i] = -INFINITY;
+      tk_t[q][i] = 0x7fffffff;
+    }
+  }
+  for (int bi = 0; bi < nb_mine; ++bi) {
+    const int b = blockIdx.x + bi * p.grid;
+    named_sync(1 + (bi & 1));
+    const float* rs = red + (bi & 1) * (kCompute * NT * 4 * 32);
+    float acc[NT][4];
+#pragma unroll
+    for (int t = 0; t < NT; ++t)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        float v = 0.f;
+#pragma unroll
+        for (int w = 0; w < kCompute; ++w) v += rs[((w * NT + t) * 4 + j) * 32 + lane];
+        acc[t][j] = v;
+      }
+    if (bi + 2 < nb_mine) named_arrive(3 + (bi & 1));
     if (lane == 0) trace_max(e.trace, 3);
     // ---- epilogue: acc[t] = {(row r0, tok n0), (r0, n0+1), (r0+8, n0), (r0+8, n0+1)}
     const int r0 = b * kRows + (lane >> 2);
@@ -275,10 +354,30 @@ __global__ void __launch_bounds__(kThreads, 1)
       float v[4] = {acc[t][0], acc[t][1], acc[t][2], acc[t][3]};
       const int rr[4] = {r0, r0, r0 + 8, r0 + 8};
       const int nn[4] = {n0, n0 + 1, n0, n0 + 1};
-      if (e.kind == kStore) {
+      if (e.kind == kStore || e.kind == kStoreTopk) {
 #pragma unroll
-        for (int j = 0; j < 4; ++j)
-          if (nn[j] < M) e.out[static_cast<size_t>(nn[j]) * e.ld + rr[j]] = v[j] * (e.ss_in ? rstd_s[nn[j]] : 1.f);
+        for (int j = 0; j < 4; ++j) {
+          v[j] *= (e.ss_in ? rstd_s[nn[j]] : 1.f);
+          if (nn[j] < M) e.out[static_cast<size_t>(nn[j]) * e.ld + rr[j]] = v[j];
+        }
+        if constexpr (TOPK) {
+          {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const int q = j & 1;
+              const float x = v[j] * e.inv_temp;
+              if (isnan(x)) continue;
+              if (x > tk_m[q]) {
+                tk_s[q] = tk_s[q] * exp(static_cast<double>(tk_m[q]) - static_cast<double>(x)) + 1.0;
+                tk_m[q] = x;
+              } else {
+                tk_s[q] += exp(static_cast<double>(x) - static_cast<double>(tk_m[q]));
+              }
+              if (topk_better(x, rr[j], tk_v[q][kTopkLane - 1], tk_t[q][kTopkLane - 1]))
+                topk_insert(tk_v[q], tk_t[q], x, rr[j]);
+            }
+          }
+        }
       } else if (e.kind == kResid) {
         float sq[2] = {0.f, 0.f};
 #pragma unroll
@@ -354,7 +453,60 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   }
-  if (cw == 0 && lane == 0) trace_max(e.trace, 2);
+  if constexpr (TOPK) {
+    {
+      // Merge the 8 lanes holding each token (equal lane & 3): (max, sum) by the xor tree, then k
+      // rounds of a group tournament over the list heads (rows are distinct, so no exact ties).
+#pragma unroll
+      for (int q = 0; q < TQ; ++q) {
+        float m = tk_m[q];
+        double sm = tk_s[q];
+#pragma unroll
+        for (int o = 4; o < 32; o <<= 1) {
+          const float mo = __shfl_xor_sync(0xffffffffu, m, o);
+          const double so = __shfl_xor_sync(0xffffffffu, sm, o);
+          const float mn = fmaxf(m, mo);
+          sm = mn == -INFINITY ? 0.0
+                               : sm * exp(static_cast<double>(m) - mn) + so * exp(static_cast<double>(mo) - mn);
+          m = mn;
+        }
+        const int n = 2 * (lane & 3) + q;
+        TopkPartial* out = e.topk_part + static_cast<size_t>(n) * p.grid + blockIdx.x;
+        const bool leader = (lane >> 2) == 0 && n < M;
+        if (leader) {
+          out->max_s = m;
+          out->sum_exp = sm;
+        }
+        for (int r = 0; r < e.topk_k; ++r) {
+          float bv = tk_v[q][0];
+          int bt = tk_t[q][0];
+#pragma unroll
+          for (int o = 4; o < 32; o <<= 1) {
+            const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
+            const int ot = __shfl_xor_sync(0xffffffffu, bt, o);
+            if (topk_better(ov, ot, bv, bt)) {
+              bv = ov;
+              bt = ot;
+            }
+          }
+          if (leader) {
+            out->val[r] = bv;
+            out->tok[r] = bt == 0x7fffffff ? -1 : bt;
+          }
+          if (bt != 0x7fffffff && tk_t[q][0] == bt) {  // this lane's head won: pop it
+#pragma unroll
+            for (int i = 0; i < kTopkLane - 1; ++i) {
+              tk_v[q][i] = tk_v[q][i + 1];
+              tk_t[q][i] = tk_t[q][i + 1];
+            }
+            tk_v[q][kTopkLane - 1] = -INFINITY;
+            tk_t[q][kTopkLane - 1] = 0x7fffffff;
+          }
+        }
+      }
+    }
+  }
+  if (lane == 0) trace_max(e.trace, 2);
 }
 
 static PFN_cuTensorMapEncodeTiled_v12000 encoder() {
@@ -398,11 +550,16 @@ using namespace ygg::gv;
 extern "C" {
 
 int ygg_prepare_gemv(void) {
-  for (auto fn : {gemv_kernel<1>, gemv_kernel<2>}) {
+  for (auto fn : {gemv_kernel<1, false>, gemv_kernel<2, false>, gemv_kernel<1, true>}) {
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     if (e != cudaSuccess) return ygg_fail(YGG_ERR_CUDA, "gemv attribute: %s", cudaGetErrorString(e));
   }
   return YGG_OK;
+}
+
+int ygg_gemv_grid(const void* plan) {
+  const Plan* pl = plan_of(plan);
+  return pl ? pl->p.grid : 0;
 }
 
 size_t ygg_gemv_plan_size(void) { return sizeof(Plan) + 64; }
@@ -443,7 +600,7 @@ int ygg_gemv_plan_init(void* plan, const void* W, const void* X, int M, int N, i
   }();
   const int budget_kb = (num_ctas <= 0 && p.nblk <= sms) ? solo_kb : smem_kb;
   const size_t stage = static_cast<size_t>(kRows) * kStageK * 2 + static_cast<size_t>(p.xrows) * kStageK * 2;
-  const size_t fixed = 1024 + 16 * 2 * 8 + kMaxTok * 16 + kCompute * 2 * 4 * 32 * 4 + 64;
+  const size_t fixed = 1024 + 16 * 2 * 8 + kMaxTok * 16 + 2 * kCompute * 2 * 4 * 32 * 4 + 64;
   p.stages = static_cast<int>(std::min<size_t>(16, (static_cast<size_t>(budget_kb) * 1024 - fixed) / stage));
   YGG_CHECK_ARG(p.stages >= 2, "gemv: shared memory budget too small");
   pl->smem = fixed + static_cast<size_t>(p.stages) * stage;
@@ -480,8 +637,18 @@ int ygg_gemv_run(const void* plan, const ygg_gemv_epilogue* ep, ygg_stream_t str
   e.resid = ep->resid;
   e.hb = static_cast<__nv_bfloat16*>(ep->hb);
   e.ss_out = ep->ss_out;
+  e.topk_part = static_cast<TopkPartial*>(ep->topk_part);
+  e.topk_k = ep->topk_k;
+  e.inv_temp = ep->inv_temp;
   switch (e.kind) {
     case kStore: YGG_CHECK_ARG(e.out && e.ld >= p.N, "STORE needs out / ld"); break;
+    case kStoreTopk:
+      YGG_CHECK_ARG(e.out && e.ld >= p.N, "STORE_TOPK needs out / ld");
+      YGG_CHECK_ARG(p.xrows == 8, "STORE_TOPK needs M <= 8 token rows");
+      YGG_CHECK_ARG(e.topk_part && e.topk_k >= 1 && e.topk_k <= kTopkLane && e.topk_k <= p.N,
+                    "STORE_TOPK needs topk_part and 1 <= k <= 8");
+      YGG_CHECK_ARG(e.inv_temp > 0.f, "STORE_TOPK needs inv_temp > 0");
+      break;
     case kResid: YGG_CHECK_ARG(e.resid && e.hb && e.ss_out, "RESID needs resid / hb / ss_out"); break;
     case kSwiglu: YGG_CHECK_ARG(e.act_out && p.N % 2 == 0, "SWIGLU needs act_out"); break;
     case kQkv:
@@ -494,10 +661,12 @@ int ygg_gemv_run(const void* plan, const ygg_gemv_epilogue* ep, ygg_stream_t str
   YGG_CHECK_ARG(!e.ss_in || (e.ss_blocks >= 1 && e.norm_dim >= 1), "bad folded-RMSNorm arguments");
   e.trace = trace_next(1);
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  if (p.xrows == 8)
-    YGG_LAUNCH_PDL(gemv_kernel<1>, dim3(p.grid), dim3(kThreads), pl->smem, s, pl->tw, pl->tx, p, e);
+  if (e.kind == kStoreTopk)
+    YGG_LAUNCH_PDL((gemv_kernel<1, true>), dim3(p.grid), dim3(kThreads), pl->smem, s, pl->tw, pl->tx, p, e);
+  else if (p.xrows == 8)
+    YGG_LAUNCH_PDL((gemv_kernel<1, false>), dim3(p.grid), dim3(kThreads), pl->smem, s, pl->tw, pl->tx, p, e);
   else
-    YGG_LAUNCH_PDL(gemv_kernel<2>, dim3(p.grid), dim3(kThreads), pl->smem, s, pl->tw, pl->tx, p, e);
+    YGG_LAUNCH_PDL((gemv_kernel<2, false>), dim3(p.grid), dim3(kThreads), pl->smem, s, pl->tw, pl->tx, p, e);
   return YGG_OK;
 }
 

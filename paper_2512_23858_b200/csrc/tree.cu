@@ -22,18 +22,11 @@ enum : int32_t { kFlagShortfall = 1, kFlagContract = 2, kFlagCapacity = 4, kFlag
 // Phase 1: each CTA scans a chunk of one row: chunk max, f64 sum of exp, local top-k by
 // (logit desc, token asc).  Phase 2: one CTA per row merges chunks deterministically.
 // ===========================================================================
-constexpr int kTopkMaxK = 32;
 constexpr int kTopkChunk = 4096;
 constexpr int kTopkThreads = 256;
+using TopkChunkOut = TopkPartial;
 
-struct TopkChunkOut {
-  float max_s;
-  double sum_exp;
-  float val[kTopkMaxK];
-  int32_t tok[kTopkMaxK];
-};
-
-YGG_DEV bool better(float va, int ta, float vb, int tb) { return va > vb || (va == vb && ta < tb); }
+YGG_DEV bool better(float va, int ta, float vb, int tb) { return topk_better(va, ta, vb, tb); }
 
 template <typename T>
 __global__ void __launch_bounds__(kTopkThreads) topk_phase1(const T* __restrict__ logits, int V, int ld, int k,
@@ -170,6 +163,140 @@ __global__ void __launch_bounds__(kTopkThreads) topk_phase2(const TopkChunkOut* 
     if (out_stats) {
       out_stats[2 * row] = static_cast<float>(m);
       out_stats[2 * row + 1] = static_cast<float>(m + log(z_s));
+    }
+  }
+  pdl_launch_dependents();
+}
+
+// Phase 2 for <= 1024 chunks (thread t owns chunks t, t+256, ...): block max, then the f64 normaliser
+// sum_j sum_exp_j * exp(max_j - M) (per-thread terms, warp xor tree, warps in order: fixed order,
+// deterministic), and k rounds of a block tournament over the heads of the chunks' sorted lists, so
+// the winners come out in (logit desc, token asc) order without the O(n^2) ranking of phase 2.
+constexpr int kMergeOwn = 4;
+__global__ void __launch_bounds__(kTopkThreads) topk_merge_kernel(const TopkPartial* __restrict__ chunks, int nchunks,
+                                                                  int k, int32_t* out_tok, double* out_prob,
+                                                                  float* out_stats) {
+  pdl_wait();
+  const int row = blockIdx.x;
+  const TopkPartial* c = chunks + static_cast<size_t>(row) * nchunks;
+  const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
+  constexpr int NW = kTopkThreads / 32;
+  __shared__ float red_f[NW];
+  __shared__ double red_d[NW];
+  __shared__ int red_i[NW], red_o[NW];
+  __shared__ float sel_v[kTopkMaxK];
+  __shared__ int sel_t[kTopkMaxK];
+  __shared__ int win_owner;
+  float cm[kMergeOwn], hv[kMergeOwn];
+  double cs[kMergeOwn];
+  int ht[kMergeOwn], h[kMergeOwn];
+  float lm = -INFINITY;
+#pragma unroll
+  for (int o = 0; o < kMergeOwn; ++o) {
+    const int j = t + o * kTopkThreads;
+    cm[o] = -INFINITY;
+    cs[o] = 0.0;
+    hv[o] = -INFINITY;
+    ht[o] = 0x7fffffff;
+    h[o] = 0;
+    if (j < nchunks) {
+      cm[o] = c[j].max_s;
+      cs[o] = c[j].sum_exp;
+      hv[o] = c[j].val[0];
+      ht[o] = c[j].tok[0];
+      if (ht[o] < 0) { hv[o] = -INFINITY; ht[o] = 0x7fffffff; }
+    }
+    lm = fmaxf(lm, cm[o]);
+  }
+  const float wm = warp_max(lm);
+  if (lane == 0) red_f[warp] = wm;
+  __syncthreads();
+  float gm = red_f[0];
+  for (int w = 1; w < NW; ++w) gm = fmaxf(gm, red_f[w]);
+  double z = 0.0;
+#pragma unroll
+  for (int o = 0; o < kMergeOwn; ++o)
+    if (cm[o] != -INFINITY) z += cs[o] * exp(static_cast<double>(cm[o]) - static_cast<double>(gm));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) z += __shfl_xor_sync(0xffffffffu, z, o);
+  if (lane == 0) red_d[warp] = z;
+  __syncthreads();  // every warp has read red_f (block max) before the tournament reuses it
+  for (int r = 0; r < k; ++r) {
+    // this thread's best head, then the block's
+    float bv = hv[0];
+    int bt = ht[0], bo = t;
+#pragma unroll
+    for (int o = 1; o < kMergeOwn; ++o)
+      if (better(hv[o], ht[o], bv, bt)) { bv = hv[o]; bt = ht[o]; bo = t + o * kTopkThreads; }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      const float ov = __shfl_xor_sync(0xffffffffu, bv, off);
+      const int ot = __shfl_xor_sync(0xffffffffu, bt, off);
+      const int oo = __shfl_xor_sync(0xffffffffu, bo, off);
+      if (better(ov, ot, bv, bt)) { bv = ov; bt = ot; bo = oo; }
+    }
+    if (lane == 0) { red_f[warp] = bv; red_i[warp] = bt; red_o[warp] = bo; }
+    __syncthreads();
+    if (t == 0) {
+      float fv = red_f[0];
+      int ft = red_i[0], fo = red_o[0];
+      for (int w = 1; w < NW; ++w)
+        if (better(red_f[w], red_i[w], fv, ft)) { fv = red_f[w]; ft = red_i[w]; fo = red_o[w]; }
+      sel_v[r] = fv;
+      sel_t[r] = ft == 0x7fffffff ? -1 : ft;
+      win_owner = ft == 0x7fffffff ? -1 : fo;
+    }
+    __syncthreads();
+    const int wo = win_owner;
+#pragma unroll
+    for (int o = 0; o < kMergeOwn; ++o) {
+      const int j = t + o * kTopkThreads;
+      if (j == wo) {  // pop the winning chunk's head
+        ++h[o];
+        hv[o] = -INFINITY;
+        ht[o] = 0x7fffffff;
+        if (h[o] < k) {
+          hv[o] = c[j].val[h[o]];
+          ht[o] = c[j].tok[h[o]];
+          if (ht[o] < 0) { hv[o] = -INFINITY; ht[o] = 0x7fffffff; }
+        }
+      }
+    }
+  }
+  __syncthreads();
+  if (t == 0) {
+    double zs = 0.0;
+    for (int w = 0; w < NW; ++w) zs += red_d[w];
+    const double m = gm;
+    double e[kTopkMaxK];
+    double topsum = 0.0;
+    int kk = 0;
+    for (int r = 0; r < k; ++r) {
+      if (sel_t[r] < 0) break;
+      e[r] = exp(static_cast<double>(sel_v[r]) - m);
+      topsum += e[r];
+      ++kk;
+    }
+    const double zz = fmax(zs, topsum);  // rounding guard: sum(top-k probs) <= 1
+    double p[kTopkMaxK];
+    int tt[kTopkMaxK];
+    for (int r = 0; r < kk; ++r) { p[r] = e[r] / zz; tt[r] = sel_t[r]; }
+    // Final order (prob desc, token asc): exp is monotone, so only equal-prob runs can move.
+    for (int a = 1; a < kk; ++a) {
+      double pa = p[a];
+      int ta = tt[a];
+      int b = a - 1;
+      while (b >= 0 && (p[b] < pa || (p[b] == pa && tt[b] > ta))) { p[b + 1] = p[b]; tt[b + 1] = tt[b]; --b; }
+      p[b + 1] = pa;
+      tt[b + 1] = ta;
+    }
+    for (int r = 0; r < k; ++r) {
+      out_tok[static_cast<size_t>(row) * k + r] = r < kk ? tt[r] : -1;
+      out_prob[static_cast<size_t>(row) * k + r] = r < kk ? p[r] : 0.0;
+    }
+    if (out_stats) {
+      out_stats[2 * row] = static_cast<float>(m);
+      out_stats[2 * row + 1] = static_cast<float>(m + log(zs));
     }
   }
   pdl_launch_dependents();
@@ -791,9 +918,29 @@ int ygg_topk_softmax(const void* logits, int dtype, int rows, int V, int ld, int
                    static_cast<const __nv_bfloat16*>(logits), V, ld, k, inv_t, nchunks, ws);
   else
     return ygg_fail(YGG_ERR_VALUE, "unknown dtype");
+  if (nchunks <= kTopkThreads * kMergeOwn) {
+    YGG_LAUNCH_PDL(topk_merge_kernel, dim3(rows), dim3(kTopkThreads), 0, s, static_cast<const TopkPartial*>(ws),
+                   nchunks, k, out_tok, out_prob, out_stats);
+    return YGG_OK;
+  }
   const size_t smem = static_cast<size_t>(nchunks) * k * (sizeof(float) + sizeof(int));
   YGG_CHECK_ARG(smem <= 48 * 1024, "too many candidates for phase 2");
   YGG_LAUNCH_PDL(topk_phase2, dim3(rows), dim3(kTopkThreads), smem, s, ws, nchunks, k, out_tok, out_prob, out_stats);
+  return YGG_OK;
+}
+
+size_t ygg_topk_partial_bytes(int rows, int nchunks) {
+  return static_cast<size_t>(rows < 0 ? 0 : rows) * (nchunks < 0 ? 0 : nchunks) * sizeof(TopkPartial);
+}
+
+int ygg_topk_merge(const void* partials, int rows, int nchunks, int k, int32_t* out_tok, double* out_prob,
+                   float* out_stats, ygg_stream_t stream) {
+  YGG_CHECK_ARG(partials && out_tok && out_prob, "null pointer");
+  YGG_CHECK_ARG(rows >= 0 && nchunks >= 1 && nchunks <= kTopkThreads * kMergeOwn, "nchunks must be in [1, 1024]");
+  YGG_CHECK_ARG(k >= 1 && k <= kTopkMaxK, "k must be in [1, 32]");
+  if (rows == 0) return YGG_OK;
+  YGG_LAUNCH_PDL(topk_merge_kernel, dim3(rows), dim3(kTopkThreads), 0, reinterpret_cast<cudaStream_t>(stream),
+                 static_cast<const TopkPartial*>(partials), nchunks, k, out_tok, out_prob, out_stats);
   return YGG_OK;
 }
 

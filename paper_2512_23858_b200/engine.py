@@ -97,6 +97,8 @@ class SpecDecoder:
         self.cand_n = torch.zeros(rows, **i32)
         self.topk_ws = torch.empty(int(L.lib().ygg_topk_workspace(max(rows, 1), draft_cfg.vocab, k)),
                                    dtype=torch.uint8, device=dev)
+        # Draft top-k straight from the LM-head GEMV epilogue (per-CTA partials + one merge launch).
+        self.topk_fused = self.draft.fuse_topk(k)
         self.keep_idx = torch.zeros(batch, self.tree_cap, **i32)
         self.new_idx = torch.zeros(batch, self.tree_cap, **i32)
         self.w_verify = torch.zeros(batch, **i32)
@@ -164,6 +166,17 @@ class SpecDecoder:
         self.seq.step.zero_()
 
     # ------------------------------------------------------------------
+    def _draft_topk(self, rows: int, k: int, s) -> None:
+        """Candidates of every draft row (DrafterDistribution.candidates, egt.py:65-80)."""
+        lib, dr = L.lib(), self.draft
+        if self.topk_fused:
+            L.check(lib.ygg_topk_merge(dr.topk_part.data_ptr(), rows, dr.topk_chunks, k, self.cand_tok.data_ptr(),
+                                       self.cand_prob.data_ptr(), None, s))
+        else:
+            L.check(lib.ygg_topk_softmax(dr.logits.data_ptr(), L.YGG_F32, rows, self.dc.vocab, self.dc.vocab, k, 1.0,
+                                         self.cand_tok.data_ptr(), self.cand_prob.data_ptr(), None,
+                                         self.topk_ws.data_ptr(), self.topk_ws.numel(), s))
+
     def _launch_step(self, stream=None, stamp=None) -> None:
         """Enqueue one step.  ``stamp(i)`` (K8 profiler) is called at the stage boundaries
         0 | pass0 | 1 | draft levels | 2 | prune | 3 | verify forward | 4 | accept+compact+commit | 5."""
@@ -182,9 +195,7 @@ class SpecDecoder:
                                  dr.slot.data_ptr(), dr.req.data_ptr(), dr.qmask.data_ptr(), dr.mask_words,
                                  dr.blk_start.data_ptr(), dr.blk_len.data_ptr(), s))
         dr.run(stream)
-        chk(lib.ygg_topk_softmax(dr.logits.data_ptr(), L.YGG_F32, rows, self.dc.vocab, self.dc.vocab, k, 1.0,
-                                 self.cand_tok.data_ptr(), self.cand_prob.data_ptr(), None, self.topk_ws.data_ptr(),
-                                 self.topk_ws.numel(), s))
+        self._draft_topk(rows, k, s)
         chk(lib.ygg_init_roots(g.struct, self.cand_tok.data_ptr(), self.cand_prob.data_ptr(), k, self.R, 1, s))
         stamp(1)
         # ---- draft passes 1..D: grow one level each
@@ -193,9 +204,7 @@ class SpecDecoder:
                                      dr.slot.data_ptr(), dr.req.data_ptr(), dr.qmask.data_ptr(), dr.mask_words,
                                      dr.blk_start.data_ptr(), dr.blk_len.data_ptr(), self.cand_n.data_ptr(), s))
             dr.run(stream)
-            chk(lib.ygg_topk_softmax(dr.logits.data_ptr(), L.YGG_F32, rows, self.dc.vocab, self.dc.vocab, k, 1.0,
-                                     self.cand_tok.data_ptr(), self.cand_prob.data_ptr(), None,
-                                     self.topk_ws.data_ptr(), self.topk_ws.numel(), s))
+            self._draft_topk(rows, k, s)
             chk(lib.ygg_egt_grow_level(g.struct, self.R, k, W, self.cand_tok.data_ptr(), self.cand_prob.data_ptr(),
                                        self.cand_n.data_ptr(), s))
         stamp(2)

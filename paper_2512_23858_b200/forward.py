@@ -268,6 +268,23 @@ class Forward:
                       epi(L.YGG_GEMV_STORE, out=self.logits.data_ptr(), ld=cfg.vocab, ss_in=ss_last.data_ptr(),
                           ss_blocks=blocks_last, norm_dim=d, eps=eps))
 
+    def fuse_topk(self, k: int, temperature: float = 1.0) -> bool:
+        """Draft GEMV pass: have the LM-head epilogue also emit per-CTA top-k partials of every row
+        (STORE_TOPK; merged by ``ygg_topk_merge``), replacing the top-k scan of the logits.  Only
+        for <= 8 rows and k <= 8; returns whether it is on."""
+        if not (self.gemv and self.M <= 8 and 1 <= k <= 8) or os.environ.get("YGG_TOPK_FUSED", "1") == "0":
+            return False
+        lib = L.lib()
+        plan, e = self.gv_lm
+        self.topk_chunks = int(lib.ygg_gemv_grid(plan))
+        self.topk_part = torch.empty(int(lib.ygg_topk_partial_bytes(self.M, self.topk_chunks)), dtype=torch.uint8,
+                                     device=self.cache.device)
+        e.kind = L.YGG_GEMV_STORE_TOPK
+        e.topk_part = self.topk_part.data_ptr()
+        e.topk_k = k
+        e.inv_temp = 1.0 / temperature
+        return True
+
     def _attend(self, li: int, qm, s) -> None:
         """bf16 attention of layer li: decode kernel when planned, else split-KV tcgen05 + combine."""
         lib = L.lib()

@@ -87,6 +87,80 @@ def test_gemv_matches_per_kernel(name, B, R, mask_words, P, cuda):
     assert torch.equal(gv.logits, first)
 
 
+@pytest.mark.parametrize("M,V,k,temp", [(8, 128256, 8, 1.0), (5, 32000, 8, 0.7), (1, 4096, 3, 1.0), (8, 1008, 8, 1.3)])
+def test_gemv_fused_topk_matches_topk_softmax(M, V, k, temp, cuda):
+    """STORE_TOPK (LM-head GEMV epilogue partials + ygg_topk_merge) == ygg_topk_softmax over the
+    logits the same launch stored: identical tokens, probabilities to 1e-12 (f64 sums in another
+    order), and the oracle's topk_softmax on those logits."""
+    import ctypes as C
+
+    import numpy as np
+
+    from oracle import tree_ref as T
+    from paper_2512_23858_b200 import _lib as L
+
+    lib = L.lib()
+    K = 256
+    g = torch.Generator(device="cuda").manual_seed(V + M)
+    W = (torch.randn(V, K, device=cuda, generator=g) * 0.2).to(torch.bfloat16)
+    X = torch.randn(M, K, device=cuda, generator=g).to(torch.bfloat16)
+    W[V // 3] = W[V // 2]  # an exact logit tie (token order decides)
+    mem = C.create_string_buffer(int(lib.ygg_gemv_plan_size()))
+    L.check(lib.ygg_gemv_plan_init(mem, W.data_ptr(), X.data_ptr(), M, V, K, 0))
+    grid = int(lib.ygg_gemv_grid(mem))
+    part = torch.empty(int(lib.ygg_topk_partial_bytes(M, grid)), dtype=torch.uint8, device=cuda)
+    logits = torch.zeros(M, V, dtype=torch.float32, device=cuda)
+    e = L.YggGemvEpilogue()
+    e.kind = L.YGG_GEMV_STORE_TOPK
+    e.out = logits.data_ptr()
+    e.ld = V
+    e.topk_part = part.data_ptr()
+    e.topk_k = k
+    e.inv_temp = 1.0 / temp
+    L.check(lib.ygg_gemv_run(mem, C.byref(e), L.stream_ptr()))
+    tok = torch.zeros(M, k, dtype=torch.int32, device=cuda)
+    prob = torch.zeros(M, k, dtype=torch.float64, device=cuda)
+    L.check(lib.ygg_topk_merge(part.data_ptr(), M, grid, k, tok.data_ptr(), prob.data_ptr(), None, L.stream_ptr()))
+    ws = torch.empty(int(lib.ygg_topk_workspace(M, V, k)), dtype=torch.uint8, device=cuda)
+    tok2 = torch.zeros_like(tok)
+    prob2 = torch.zeros_like(prob)
+    L.check(lib.ygg_topk_softmax(logits.data_ptr(), L.YGG_F32, M, V, V, k, temp, tok2.data_ptr(), prob2.data_ptr(),
+                                 None, ws.data_ptr(), ws.numel(), L.stream_ptr()))
+    torch.cuda.synchronize()
+    assert torch.equal(tok, tok2)
+    np.testing.assert_allclose(prob.cpu().numpy(), prob2.cpu().numpy(), rtol=1e-12)
+    if temp != 1.0:  # the oracle divides by the temperature, the kernels multiply by its inverse
+        return
+    lg = logits.cpu().numpy()
+    for r in range(M):
+        ref = T.topk_softmax(lg[r], k, temp)
+        assert tok[r].cpu().tolist() == [t for t, _ in ref]
+        np.testing.assert_allclose(prob[r].cpu().numpy(), [p for _, p in ref], rtol=1e-12)
+
+
+def test_gemv_fused_topk_rejects_wide_rows(cuda):
+    import ctypes as C
+
+    from paper_2512_23858_b200 import _lib as L
+
+    lib = L.lib()
+    W = torch.zeros(256, 128, dtype=torch.bfloat16, device=cuda)
+    X = torch.zeros(12, 128, dtype=torch.bfloat16, device=cuda)
+    mem = C.create_string_buffer(int(lib.ygg_gemv_plan_size()))
+    L.check(lib.ygg_gemv_plan_init(mem, W.data_ptr(), X.data_ptr(), 12, 256, 128, 0))
+    out = torch.zeros(12, 256, dtype=torch.float32, device=cuda)
+    part = torch.empty(1 << 20, dtype=torch.uint8, device=cuda)
+    e = L.YggGemvEpilogue()
+    e.kind = L.YGG_GEMV_STORE_TOPK
+    e.out = out.data_ptr()
+    e.ld = 256
+    e.topk_part = part.data_ptr()
+    e.topk_k = 4
+    e.inv_temp = 1.0
+    with pytest.raises(ValueError):
+        L.check(lib.ygg_gemv_run(mem, C.byref(e), L.stream_ptr()))
+
+
 def test_gemv_plan_rejects_bad_shapes(cuda):
     import ctypes as C
 

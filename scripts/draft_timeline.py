@@ -19,7 +19,7 @@ sd.prefill(bench.prompts_for(wl, tc.vocab, 0))
 for _ in range(2):
     sd.step(use_graph=False)
 torch.cuda.synchronize()
-f = sd.draft if which == "draft" else sd.verify
+f = sd.verify if which == "verify" else sd.draft
 g = Forward(f.cfg, f.w, f.cache, f.B, f.R, f.mask_words, f.act_dtype)
 for t in ("tokens", "pos", "slot", "req", "qmask", "blk_start", "blk_len"):
     getattr(g, t).copy_(getattr(f, t))
@@ -34,22 +34,53 @@ def reset():
     buf[:, 2:] = 0
 
 
+def level(stream=None):
+    """One EGT draft level exactly as the step enqueues it (engine.SpecDecoder._launch_step)."""
+    sh = sd.shape
+    s = L.stream_ptr(stream)
+    dr, gr = sd.draft, sd.grown
+    L.check(lib.ygg_level_inputs(gr.struct, sd.seq.struct, sd.R, sh.expansion_k, dr.tokens.data_ptr(),
+                                 dr.pos.data_ptr(), dr.slot.data_ptr(), dr.req.data_ptr(), dr.qmask.data_ptr(),
+                                 dr.mask_words, dr.blk_start.data_ptr(), dr.blk_len.data_ptr(),
+                                 sd.cand_n.data_ptr(), s))
+    dr.run(stream)
+    sd._draft_topk(sd.B * sd.R, sh.expansion_k, s)
+    L.check(lib.ygg_egt_grow_level(gr.struct, sd.R, sh.expansion_k, sh.width, sd.cand_tok.data_ptr(),
+                                   sd.cand_prob.data_ptr(), sd.cand_n.data_ptr(), s))
+
+
 graph = torch.cuda.CUDAGraph()
 L.check(lib.ygg_trace_arm(buf.data_ptr(), CAP))
 with torch.cuda.graph(graph):
-    g.run()
+    if which == "level":
+        level()
+    else:
+        g.run()
 ids = (L.C.c_int * CAP)()
 n = lib.ygg_trace_used(ids, CAP)
 L.check(lib.ygg_trace_arm(None, 0))
+tree_state = [x.clone() for x in (sd.grown.token, sd.grown.parent, sd.grown.depth, sd.grown.prob, sd.grown.cum,
+                                   sd.grown.mask, sd.grown.size, sd.grown.frontier, sd.grown.frontier_n,
+                                   sd.grown.flags)]
+
+
+def restore():
+    for dst, src in zip((sd.grown.token, sd.grown.parent, sd.grown.depth, sd.grown.prob, sd.grown.cum, sd.grown.mask,
+                         sd.grown.size, sd.grown.frontier, sd.grown.frontier_n, sd.grown.flags), tree_state):
+        dst.copy_(src)
+
+
 for _ in range(5):
+    restore()
     graph.replay()
+restore()
 reset()
 torch.cuda.synchronize()
 graph.replay()
 torch.cuda.synchronize()
 t = buf[:n].cpu().tolist()
 names = {1: "gemv", 2: "attn_dec", 3: "gemm", 4: "epi_store", 5: "epi_resid", 6: "epi_swiglu", 7: "epi_qkv",
-         8: "attn_tc", 9: "attn_combine"}
+         8: "attn_tc", 9: "attn_combine", 10: "topk_merge", 11: "grow", 13: "level_inputs", 14: "embed"}
 t0 = t[0][0]
 rows = []
 prev_end = None

@@ -79,8 +79,11 @@ __global__ void init_roots_kernel(ygg_tree t, const int32_t* __restrict__ cand_t
 // Draft pass over the newest level: rows = frontier nodes (padded to R), block = tree nodes so far.
 __global__ void level_inputs_kernel(ygg_tree t, ygg_seq seq, int R, int k, int32_t* tokens, int32_t* pos,
                                     int32_t* slot, int32_t* req, uint32_t* qmask, int mask_words,
-                                    int32_t* blk_start, int32_t* blk_len, int32_t* cand_n) {
+                                    int32_t* blk_start, int32_t* blk_len, int32_t* cand_n,
+                                    unsigned long long* trace) {
+  if (threadIdx.x == 0) trace_min(trace, 0);
   pdl_wait();
+  if (threadIdx.x == 0) trace_min(trace, 1);
   pdl_launch_dependents();
   const int b = blockIdx.x;
   const size_t tb = static_cast<size_t>(b) * t.cap;
@@ -109,6 +112,7 @@ __global__ void level_inputs_kernel(ygg_tree t, ygg_seq seq, int R, int k, int32
     blk_start[b] = P + 1;
     blk_len[b] = t.size[b];
   }
+  if (threadIdx.x == 0) trace_max(trace, 2);
 }
 
 // Verify rows: row 0 = bonus (slot P), row 1+i = pruned node i (slot P+1+i); mask over the
@@ -214,7 +218,7 @@ int ygg_level_inputs(ygg_tree tree, ygg_seq seq, int R, int k, int32_t* tokens, 
                      int32_t* cand_n, ygg_stream_t stream) {
   YGG_CHECK_ARG(mask_words >= tree.mask_words, "query mask narrower than the tree mask");
   YGG_LAUNCH_PDL(level_inputs_kernel, dim3(tree.B), dim3(64), 0, reinterpret_cast<cudaStream_t>(stream), tree, seq, R,
-                 k, tokens, pos, slot, req, qmask, mask_words, blk_start, blk_len, cand_n);
+                 k, tokens, pos, slot, req, qmask, mask_words, blk_start, blk_len, cand_n, trace_next(13));
   return YGG_OK;
 }
 

@@ -942,13 +942,15 @@ int ygg_gemm_plan_init(void* plan_mem, int dtype, const void* W, const void* X, 
     if (num_ctas > g->units) num_ctas = static_cast<int>(g->units);
     g->num_ctas = num_ctas;
     const int stage_bytes = kBM * kBK * 2 + g->BN * kBK * 2;
-    // Shared-memory budget: YGG_GEMM_SMEM_KB (default 150: one CTA per SM with a 6-stage ring at
-    // BN = 64, leaving room for a co-resident epilogue / attention CTA under programmatic dependent
-    // launch).  Same-box sweep of the cfg2 verify forward: 113 KB (two CTAs/SM) 4.37 ms, 135 KB
-    // 4.24, 150 KB 4.22, 165 KB 4.22, 190 KB 4.25, 227 KB 4.47.
+    // Shared-memory budget: YGG_GEMM_SMEM_KB (default 190: one CTA per SM with a 7-stage ring at
+    // BN = 64; the small epilogue CTAs still co-reside under programmatic dependent launch, the
+    // decode attention of the verify (up to 190 KB itself) does not either way).  Same-box sweeps
+    // of the cfg2 verify forward — with the split-KV tcgen05 attention: 113 KB 4.37 ms, 135 KB
+    // 4.24, 150 KB 4.22, 165 KB 4.22, 190 KB 4.25, 227 KB 4.47; with the decode attention: 120 KB
+    // 3.76, 150 KB 3.605, 190 KB 3.586, 216 KB 3.605.
     static const int smem_kb = [] {
       const char* s = getenv("YGG_GEMM_SMEM_KB");
-      int v = s ? atoi(s) : 150;
+      int v = s ? atoi(s) : 190;
       return v < 48 ? 48 : (v > 227 ? 227 : v);
     }();
     g->stages = std::min(12, (smem_kb * 1024 - kSmemExtra) / stage_bytes);

@@ -20,30 +20,44 @@ __global__ void embed_kernel(const T* __restrict__ table, int V, int d, const in
   for (int i = threadIdx.x; i < d; i += blockDim.x) out[static_cast<size_t>(m) * d + i] = to_f32(row[i]);
 }
 
-// Embedding for the fused path: 128 threads = one 128-feature tile at a time; writes the f32
-// residual, its bf16 copy (next GEMM operand) and the tile's sum of squares (fixed-order reduce).
-__global__ void __launch_bounds__(128) embed_fused_kernel(const __nv_bfloat16* __restrict__ table, int V, int d,
-                                                          const int32_t* __restrict__ tokens, float* __restrict__ resid,
-                                                          __nv_bfloat16* __restrict__ hb, float* __restrict__ ss_out,
-                                                          int M) {
+// Embedding for the fused path: one CTA per token row, d/8 threads with 8 features (one 16-byte
+// load) each, so the whole row is a single round trip.  Writes the f32 residual, its bf16 copy
+// (next GEMM operand) and each 128-feature tile's sum of squares (16 threads per tile, fixed xor
+// order: deterministic).
+__global__ void __launch_bounds__(1024) embed_fused_kernel(const __nv_bfloat16* __restrict__ table, int V, int d,
+                                                           const int32_t* __restrict__ tokens, float* __restrict__ resid,
+                                                           __nv_bfloat16* __restrict__ hb, float* __restrict__ ss_out,
+                                                           int M, unsigned long long* trace) {
+  if (threadIdx.x == 0) trace_min(trace, 0);
   pdl_wait();
+  if (threadIdx.x == 0) trace_min(trace, 1);
   pdl_launch_dependents();
-  __shared__ float red[4];
   const int m = blockIdx.x;
   int tok = tokens[m];
   tok = tok < 0 ? 0 : (tok >= V ? V - 1 : tok);
-  for (int t = 0; t < d / 128; ++t) {
-    const int n = t * 128 + threadIdx.x;
-    const __nv_bfloat16 x = table[static_cast<size_t>(tok) * d + n];
-    const float h = __bfloat162float(x);
-    resid[static_cast<size_t>(m) * d + n] = h;
-    hb[static_cast<size_t>(m) * d + n] = x;
-    float s = warp_sum(h * h);
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
-    __syncthreads();
-    if (threadIdx.x == 0) ss_out[static_cast<size_t>(t) * M + m] = red[0] + red[1] + red[2] + red[3];
-    __syncthreads();
+  const int n = threadIdx.x * 8;
+  float s = 0.f;
+  if (n < d) {
+    const uint4 raw = __ldg(reinterpret_cast<const uint4*>(table + static_cast<size_t>(tok) * d + n));
+    const uint32_t w[4] = {raw.x, raw.y, raw.z, raw.w};
+    float h[8];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const __nv_bfloat162 b = *reinterpret_cast<const __nv_bfloat162*>(&w[i]);
+      h[2 * i] = __bfloat162float(b.x);
+      h[2 * i + 1] = __bfloat162float(b.y);
+    }
+    float4* rp = reinterpret_cast<float4*>(resid + static_cast<size_t>(m) * d + n);
+    rp[0] = make_float4(h[0], h[1], h[2], h[3]);
+    rp[1] = make_float4(h[4], h[5], h[6], h[7]);
+    *reinterpret_cast<uint4*>(hb + static_cast<size_t>(m) * d + n) = raw;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) s += h[i] * h[i];
   }
+#pragma unroll
+  for (int o = 8; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (n < d && (threadIdx.x & 15) == 0) ss_out[static_cast<size_t>(n / 128) * M + m] = s;
+  if (threadIdx.x == 0) trace_max(trace, 2);
 }
 
 template <typename T>
@@ -296,11 +310,11 @@ int ygg_embed(const void* table, int dtype, int V, int d, const int32_t* tokens,
 int ygg_embed_fused(const void* table, int V, int d, const int32_t* tokens, int M, float* resid, void* hb,
                     float* ss_out, ygg_stream_t stream) {
   YGG_CHECK_ARG(table && tokens && resid && hb && ss_out && V >= 1, "invalid arguments");
-  YGG_CHECK_ARG(d % 128 == 0, "model width must be a multiple of 128");
+  YGG_CHECK_ARG(d % 128 == 0 && d <= 8192, "model width must be a multiple of 128 and <= 8192");
   if (M <= 0) return YGG_OK;
-  YGG_LAUNCH_PDL(embed_fused_kernel, dim3(M), dim3(128), 0, reinterpret_cast<cudaStream_t>(stream),
+  YGG_LAUNCH_PDL(embed_fused_kernel, dim3(M), dim3(((d / 8 + 31) / 32) * 32), 0, reinterpret_cast<cudaStream_t>(stream),
                  static_cast<const __nv_bfloat16*>(table), V, d, tokens, resid, static_cast<__nv_bfloat16*>(hb),
-                 ss_out, M);
+                 ss_out, M, trace_next(14));
   return YGG_OK;
 }
 

@@ -175,8 +175,10 @@ __global__ void __launch_bounds__(kTopkThreads) topk_phase2(const TopkChunkOut* 
 constexpr int kMergeOwn = 4;
 __global__ void __launch_bounds__(kTopkThreads) topk_merge_kernel(const TopkPartial* __restrict__ chunks, int nchunks,
                                                                   int k, int32_t* out_tok, double* out_prob,
-                                                                  float* out_stats) {
+                                                                  float* out_stats, unsigned long long* trace) {
+  if (threadIdx.x == 0) trace_min(trace, 0);
   pdl_wait();
+  if (threadIdx.x == 0) trace_min(trace, 1);
   const int row = blockIdx.x;
   const TopkPartial* c = chunks + static_cast<size_t>(row) * nchunks;
   const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
@@ -186,7 +188,34 @@ __global__ void __launch_bounds__(kTopkThreads) topk_merge_kernel(const TopkPart
   __shared__ int red_i[NW], red_o[NW];
   __shared__ float sel_v[kTopkMaxK];
   __shared__ int sel_t[kTopkMaxK];
-  __shared__ int win_owner;
+  // every chunk's sorted list, staged once: the tournament then never touches global memory
+  extern __shared__ unsigned char merge_smem[];
+  float* lv = reinterpret_cast<float*>(merge_smem);
+  int* lt = reinterpret_cast<int*>(lv + static_cast<size_t>(nchunks) * k);
+  {  // loads batched 8 deep (a plain strided loop would serialise one L2 round trip per element)
+    const int total = nchunks * k;
+    for (int i0 = t; i0 < total; i0 += 8 * kTopkThreads) {
+      float v8[8];
+      int t8[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int i = i0 + u * kTopkThreads;
+        if (i < total) {
+          const int j = i / k, r = i - j * k;
+          v8[u] = c[j].val[r];
+          t8[u] = c[j].tok[r];
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int i = i0 + u * kTopkThreads;
+        if (i < total) {
+          lv[i] = v8[u];
+          lt[i] = t8[u];
+        }
+      }
+    }
+  }
   float cm[kMergeOwn], hv[kMergeOwn];
   double cs[kMergeOwn];
   int ht[kMergeOwn], h[kMergeOwn];
@@ -202,15 +231,22 @@ __global__ void __launch_bounds__(kTopkThreads) topk_merge_kernel(const TopkPart
     if (j < nchunks) {
       cm[o] = c[j].max_s;
       cs[o] = c[j].sum_exp;
-      hv[o] = c[j].val[0];
-      ht[o] = c[j].tok[0];
-      if (ht[o] < 0) { hv[o] = -INFINITY; ht[o] = 0x7fffffff; }
     }
     lm = fmaxf(lm, cm[o]);
   }
   const float wm = warp_max(lm);
   if (lane == 0) red_f[warp] = wm;
   __syncthreads();
+  if (t == 0) trace_max(trace, 3);
+#pragma unroll
+  for (int o = 0; o < kMergeOwn; ++o) {
+    const int j = t + o * kTopkThreads;
+    if (j < nchunks) {
+      hv[o] = lv[j * k];
+      ht[o] = lt[j * k];
+      if (ht[o] < 0) { hv[o] = -INFINITY; ht[o] = 0x7fffffff; }
+    }
+  }
   float gm = red_f[0];
   for (int w = 1; w < NW; ++w) gm = fmaxf(gm, red_f[w]);
   double z = 0.0;
@@ -221,8 +257,13 @@ __global__ void __launch_bounds__(kTopkThreads) topk_merge_kernel(const TopkPart
   for (int o = 16; o > 0; o >>= 1) z += __shfl_xor_sync(0xffffffffu, z, o);
   if (lane == 0) red_d[warp] = z;
   __syncthreads();  // every warp has read red_f (block max) before the tournament reuses it
+  if (t == 0) trace_max(trace, 4);
+  // Two-level tournament without block barriers per round: (1) each warp pops its k best from the
+  // heads of its lanes' chunk lists (shuffle argmax, lanes own chunks t, t+256, ...); (2) warp 0's
+  // lanes 0..NW-1 each own one warp's sorted result and pop the block's k best the same way.
+  __shared__ float wsel_v[NW][kTopkMaxK];
+  __shared__ int wsel_t[NW][kTopkMaxK];
   for (int r = 0; r < k; ++r) {
-    // this thread's best head, then the block's
     float bv = hv[0];
     int bt = ht[0], bo = t;
 #pragma unroll
@@ -235,71 +276,108 @@ __global__ void __launch_bounds__(kTopkThreads) topk_merge_kernel(const TopkPart
       const int oo = __shfl_xor_sync(0xffffffffu, bo, off);
       if (better(ov, ot, bv, bt)) { bv = ov; bt = ot; bo = oo; }
     }
-    if (lane == 0) { red_f[warp] = bv; red_i[warp] = bt; red_o[warp] = bo; }
-    __syncthreads();
-    if (t == 0) {
-      float fv = red_f[0];
-      int ft = red_i[0], fo = red_o[0];
-      for (int w = 1; w < NW; ++w)
-        if (better(red_f[w], red_i[w], fv, ft)) { fv = red_f[w]; ft = red_i[w]; fo = red_o[w]; }
-      sel_v[r] = fv;
-      sel_t[r] = ft == 0x7fffffff ? -1 : ft;
-      win_owner = ft == 0x7fffffff ? -1 : fo;
+    if (lane == 0) {
+      wsel_v[warp][r] = bv;
+      wsel_t[warp][r] = bt;
     }
-    __syncthreads();
-    const int wo = win_owner;
+    if (bt == 0x7fffffff) continue;  // this warp's lists are exhausted (uniform across the warp)
 #pragma unroll
     for (int o = 0; o < kMergeOwn; ++o) {
       const int j = t + o * kTopkThreads;
-      if (j == wo) {  // pop the winning chunk's head
+      if (j == bo) {  // pop the winning chunk's head
         ++h[o];
         hv[o] = -INFINITY;
         ht[o] = 0x7fffffff;
         if (h[o] < k) {
-          hv[o] = c[j].val[h[o]];
-          ht[o] = c[j].tok[h[o]];
+          hv[o] = lv[j * k + h[o]];
+          ht[o] = lt[j * k + h[o]];
           if (ht[o] < 0) { hv[o] = -INFINITY; ht[o] = 0x7fffffff; }
         }
       }
     }
   }
   __syncthreads();
+  if (warp == 0) {
+    int hp = 0;
+    float cv = -INFINITY;
+    int ct = 0x7fffffff;
+    if (lane < NW) {
+      cv = wsel_v[lane][0];
+      ct = wsel_t[lane][0];
+    }
+    for (int r = 0; r < k; ++r) {
+      float bv = cv;
+      int bt = ct, bo = lane;
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) {
+        const float ov = __shfl_xor_sync(0xffffffffu, bv, off);
+        const int ot = __shfl_xor_sync(0xffffffffu, bt, off);
+        const int oo = __shfl_xor_sync(0xffffffffu, bo, off);
+        if (better(ov, ot, bv, bt)) { bv = ov; bt = ot; bo = oo; }
+      }
+      if (lane == 0) {
+        sel_v[r] = bv;
+        sel_t[r] = bt == 0x7fffffff ? -1 : bt;
+      }
+      if (lane == bo && bt != 0x7fffffff) {
+        ++hp;
+        cv = -INFINITY;
+        ct = 0x7fffffff;
+        if (hp < k) {
+          cv = wsel_v[lane][hp];
+          ct = wsel_t[lane][hp];
+        }
+      }
+    }
+  }
+  __syncthreads();
+  if (t == 0) trace_max(trace, 5);
+  // Probabilities and final order, one thread per selected candidate: p = e / max(Z, sum of the
+  // top-k e) (rounding guard: the top-k probabilities never sum above 1), then each entry's rank
+  // under (prob desc, token asc) — exp is monotone, so only equal-probability runs move.
+  __shared__ double sel_e[kTopkMaxK];
+  __shared__ double s_zz, s_zs;
+  __shared__ int s_kk;
+  if (t < k) sel_e[t] = sel_t[t] >= 0 ? exp(static_cast<double>(sel_v[t]) - static_cast<double>(gm)) : 0.0;
+  __syncthreads();
   if (t == 0) {
     double zs = 0.0;
     for (int w = 0; w < NW; ++w) zs += red_d[w];
-    const double m = gm;
-    double e[kTopkMaxK];
     double topsum = 0.0;
     int kk = 0;
     for (int r = 0; r < k; ++r) {
       if (sel_t[r] < 0) break;
-      e[r] = exp(static_cast<double>(sel_v[r]) - m);
-      topsum += e[r];
+      topsum += sel_e[r];
       ++kk;
     }
-    const double zz = fmax(zs, topsum);  // rounding guard: sum(top-k probs) <= 1
-    double p[kTopkMaxK];
-    int tt[kTopkMaxK];
-    for (int r = 0; r < kk; ++r) { p[r] = e[r] / zz; tt[r] = sel_t[r]; }
-    // Final order (prob desc, token asc): exp is monotone, so only equal-prob runs can move.
-    for (int a = 1; a < kk; ++a) {
-      double pa = p[a];
-      int ta = tt[a];
-      int b = a - 1;
-      while (b >= 0 && (p[b] < pa || (p[b] == pa && tt[b] > ta))) { p[b + 1] = p[b]; tt[b + 1] = tt[b]; --b; }
-      p[b + 1] = pa;
-      tt[b + 1] = ta;
-    }
-    for (int r = 0; r < k; ++r) {
-      out_tok[static_cast<size_t>(row) * k + r] = r < kk ? tt[r] : -1;
-      out_prob[static_cast<size_t>(row) * k + r] = r < kk ? p[r] : 0.0;
-    }
-    if (out_stats) {
-      out_stats[2 * row] = static_cast<float>(m);
-      out_stats[2 * row + 1] = static_cast<float>(m + log(zs));
+    s_zs = zs;
+    s_zz = fmax(zs, topsum);
+    s_kk = kk;
+  }
+  __syncthreads();
+  if (t < k) {
+    const int kk = s_kk;
+    if (t < kk) {
+      const double pt = sel_e[t] / s_zz;
+      const int tt = sel_t[t];
+      int rank = 0;
+      for (int j = 0; j < kk; ++j) {
+        const double pj = sel_e[j] / s_zz;
+        if (pj > pt || (pj == pt && sel_t[j] < tt)) ++rank;
+      }
+      out_tok[static_cast<size_t>(row) * k + rank] = tt;
+      out_prob[static_cast<size_t>(row) * k + rank] = pt;
+    } else {
+      out_tok[static_cast<size_t>(row) * k + t] = -1;
+      out_prob[static_cast<size_t>(row) * k + t] = 0.0;
     }
   }
+  if (t == 0 && out_stats) {
+    out_stats[2 * row] = static_cast<float>(gm);
+    out_stats[2 * row + 1] = static_cast<float>(static_cast<double>(gm) + log(s_zs));
+  }
   pdl_launch_dependents();
+  if (threadIdx.x == 0) trace_max(trace, 2);
 }
 
 // ===========================================================================
@@ -312,8 +390,11 @@ constexpr int kGrowMaxFront = 256;
 __global__ void __launch_bounds__(kGrowThreads) grow_level_kernel(ygg_tree t, int Fmax, int k, int w_draft,
                                                                   const int32_t* __restrict__ cand_tok,
                                                                   const double* __restrict__ cand_prob,
-                                                                  const int32_t* __restrict__ cand_n) {
+                                                                  const int32_t* __restrict__ cand_n,
+                                                                  unsigned long long* trace) {
+  if (threadIdx.x == 0) trace_min(trace, 0);
   pdl_wait();
+  if (threadIdx.x == 0) trace_min(trace, 1);
   const int b = blockIdx.x;
   __shared__ double sc[kGrowMaxCand];
   __shared__ int spar[kGrowMaxCand];
@@ -322,23 +403,37 @@ __global__ void __launch_bounds__(kGrowThreads) grow_level_kernel(ygg_tree t, in
   __shared__ int s_n, s_ok, s_added;
   __shared__ int s_apar[kGrowMaxCand];     // attached nodes by rank: parent, surrogate prob
   __shared__ double s_aprob[kGrowMaxCand];
-  __shared__ int s_fn;
+  __shared__ int s_fn, s_size0, s_flags;
+  __shared__ int s_cnt[kGrowMaxFront], s_par[kGrowMaxFront], s_off[kGrowMaxFront + 1];
+  __shared__ double s_cum[kGrowMaxFront];
   int32_t* flags = t.flags + b;
-  const int size0 = t.size[b];
+  const size_t tb = static_cast<size_t>(b) * t.cap;
+  const int32_t* frontier = t.frontier + tb;
+  // One round of independent loads: the tree header (thread 0) and, speculatively for every
+  // possible frontier row f < Fmax (thread f), its candidate count, its k probabilities (contract
+  // check: range, descending, running sum — _checked_candidates, egt.py:65-80), its parent node and
+  // the parent's path probability.  Nothing below re-reads global candidate data.
   if (threadIdx.x == 0) {
     s_ok = 1;
     s_fn = t.frontier_n[b];
-    if (*flags & kFlagStopped) s_ok = 0;
+    s_size0 = t.size[b];
+    s_flags = *flags;
   }
-  __syncthreads();
-  if (!s_ok) return;
-  const int fn = s_fn;
-  const int32_t* frontier = t.frontier + static_cast<size_t>(b) * t.cap;
-  const size_t tb = static_cast<size_t>(b) * t.cap;
-  // Candidate contract (_checked_candidates, egt.py:65-80): range, descending, running sum.
-  if (threadIdx.x < fn) {
+  const int fmax = min(Fmax, kGrowMaxFront);
+  if (threadIdx.x < fmax) {
     const int f = threadIdx.x;
     const int cnt = cand_n ? cand_n[static_cast<size_t>(b) * Fmax + f] : k;
+    const int parent = frontier[f];
+    s_cnt[f] = cnt;
+    s_par[f] = parent;
+    s_cum[f] = (parent >= 0 && parent < t.cap) ? t.cum[tb + parent] : 0.0;
+  }
+  __syncthreads();
+  const int fn = s_fn, size0 = s_size0;
+  if (s_flags & kFlagStopped) return;
+  if (threadIdx.x < min(fn, fmax)) {
+    const int f = threadIdx.x;
+    const int cnt = s_cnt[f];
     const double* pr = cand_prob + (static_cast<size_t>(b) * Fmax + f) * k;
     double total = 0.0, prev = INFINITY;
     bool bad = cnt < 0 || cnt > k;
@@ -352,36 +447,30 @@ __global__ void __launch_bounds__(kGrowThreads) grow_level_kernel(ygg_tree t, in
     if (total > 1.0 + kSiblingTol) bad = true;
     if (bad) atomicExch(&s_ok, 0);
   }
+  if (threadIdx.x == 0) {  // candidate offsets of the frontier rows, from shared memory
+    int acc = 0;
+    for (int f = 0; f < fn && f < kGrowMaxFront; ++f) {
+      s_off[f] = acc;
+      acc += s_cnt[f];
+    }
+    s_off[min(fn, kGrowMaxFront)] = acc;
+    s_n = min(acc, kGrowMaxCand);
+  }
   __syncthreads();
   if (!s_ok) {
     if (threadIdx.x == 0) atomicOr(flags, kFlagContract);
     return;
   }
-  // Gather the scored candidates in (frontier row, rank) order, one thread per candidate slot:
-  // every load of the level is in flight at once instead of a serial walk on one thread.
-  {
-    __shared__ int s_off[kGrowMaxFront + 1];
-    if (threadIdx.x == 0) {
-      int acc = 0;
-      for (int f = 0; f < fn && f < kGrowMaxFront; ++f) {
-        s_off[f] = acc;
-        acc += cand_n ? cand_n[static_cast<size_t>(b) * Fmax + f] : k;
-      }
-      s_off[min(fn, kGrowMaxFront)] = acc;
-      s_n = min(acc, kGrowMaxCand);
-    }
-    __syncthreads();
-    for (int i = threadIdx.x; i < fn * k; i += blockDim.x) {
-      const int f = i / k, r = i % k;
-      if (f >= kGrowMaxFront) continue;
-      const int cnt = s_off[f + 1] - s_off[f];
-      const int n = s_off[f] + r;
-      if (r >= cnt || n >= kGrowMaxCand) continue;
-      const int parent = frontier[f];
-      sc[n] = t.cum[tb + parent] * cand_prob[(static_cast<size_t>(b) * Fmax + f) * k + r];
-      spar[n] = parent;
-      sslot[n] = f * k + r;
-    }
+  // Scored candidates in (frontier row, rank) order, one thread per candidate slot.
+  for (int i = threadIdx.x; i < fn * k; i += blockDim.x) {
+    const int f = i / k, r = i % k;
+    if (f >= kGrowMaxFront) continue;
+    const int cnt = s_off[f + 1] - s_off[f];
+    const int n = s_off[f] + r;
+    if (r >= cnt || n >= kGrowMaxCand) continue;
+    sc[n] = s_cum[f] * cand_prob[(static_cast<size_t>(b) * Fmax + f) * k + r];
+    spar[n] = s_par[f];
+    sslot[n] = f * k + r;
   }
   __syncthreads();
   const int n = s_n;
@@ -444,6 +533,7 @@ __global__ void __launch_bounds__(kGrowThreads) grow_level_kernel(ygg_tree t, in
     if (fl) atomicOr(flags, fl);
   }
   pdl_launch_dependents();
+  if (threadIdx.x == 0) trace_max(trace, 2);
 }
 
 // ===========================================================================
@@ -890,6 +980,8 @@ extern "C" {
 int ygg_prepare_tree(void) {
   cudaError_t e = cudaFuncSetAttribute(knapsack_prune_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
   if (e != cudaSuccess) return ygg_fail(YGG_ERR_CUDA, "knapsack attribute: %s", cudaGetErrorString(e));
+  e = cudaFuncSetAttribute(topk_merge_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  if (e != cudaSuccess) return ygg_fail(YGG_ERR_CUDA, "top-k merge attribute: %s", cudaGetErrorString(e));
   return YGG_OK;
 }
 
@@ -919,8 +1011,9 @@ int ygg_topk_softmax(const void* logits, int dtype, int rows, int V, int ld, int
   else
     return ygg_fail(YGG_ERR_VALUE, "unknown dtype");
   if (nchunks <= kTopkThreads * kMergeOwn) {
-    YGG_LAUNCH_PDL(topk_merge_kernel, dim3(rows), dim3(kTopkThreads), 0, s, static_cast<const TopkPartial*>(ws),
-                   nchunks, k, out_tok, out_prob, out_stats);
+    YGG_LAUNCH_PDL(topk_merge_kernel, dim3(rows), dim3(kTopkThreads), static_cast<size_t>(nchunks) * k * 8, s,
+                   static_cast<const TopkPartial*>(ws),
+                   nchunks, k, out_tok, out_prob, out_stats, trace_next(10));
     return YGG_OK;
   }
   const size_t smem = static_cast<size_t>(nchunks) * k * (sizeof(float) + sizeof(int));
@@ -938,9 +1031,11 @@ int ygg_topk_merge(const void* partials, int rows, int nchunks, int k, int32_t* 
   YGG_CHECK_ARG(partials && out_tok && out_prob, "null pointer");
   YGG_CHECK_ARG(rows >= 0 && nchunks >= 1 && nchunks <= kTopkThreads * kMergeOwn, "nchunks must be in [1, 1024]");
   YGG_CHECK_ARG(k >= 1 && k <= kTopkMaxK, "k must be in [1, 32]");
+  YGG_CHECK_ARG(static_cast<size_t>(nchunks) * k * 8 <= 200 * 1024, "too many candidates to merge");
   if (rows == 0) return YGG_OK;
-  YGG_LAUNCH_PDL(topk_merge_kernel, dim3(rows), dim3(kTopkThreads), 0, reinterpret_cast<cudaStream_t>(stream),
-                 static_cast<const TopkPartial*>(partials), nchunks, k, out_tok, out_prob, out_stats);
+  YGG_LAUNCH_PDL(topk_merge_kernel, dim3(rows), dim3(kTopkThreads), static_cast<size_t>(nchunks) * k * 8,
+                 reinterpret_cast<cudaStream_t>(stream),
+                 static_cast<const TopkPartial*>(partials), nchunks, k, out_tok, out_prob, out_stats, trace_next(10));
   return YGG_OK;
 }
 
@@ -960,7 +1055,7 @@ int ygg_egt_grow_level(ygg_tree tree, int Fmax, int k, int w_draft, const int32_
   YGG_CHECK_ARG(k >= 1 && Fmax >= 1 && Fmax <= kGrowThreads && Fmax * k <= kGrowMaxCand, "candidate grid too large");
   YGG_CHECK_ARG(cand_tok && cand_prob, "candidate pointers must be non-null");
   YGG_LAUNCH_PDL(grow_level_kernel, dim3(tree.B), dim3(kGrowThreads), 0, reinterpret_cast<cudaStream_t>(stream),
-                 tree, Fmax, k, w_draft, cand_tok, cand_prob, cand_n);
+                 tree, Fmax, k, w_draft, cand_tok, cand_prob, cand_n, trace_next(11));
   return YGG_OK;
 }
 

@@ -217,6 +217,7 @@ class Forward:
             self._setup_mk()
         if self.gemv:
             self._setup_gemv()
+        self._setup_attn_l2_prefetch()
 
     # ------------------------------------------------------------------
     def _setup_gemv(self) -> None:
@@ -267,6 +268,23 @@ class Forward:
         self.gv_lm = (plan(self.w["lm_head"], self.xn),
                       epi(L.YGG_GEMV_STORE, out=self.logits.data_ptr(), ld=cfg.vocab, ss_in=ss_last.data_ptr(),
                           ss_blocks=blocks_last, norm_dim=d, eps=eps))
+
+    def _setup_attn_l2_prefetch(self) -> None:
+        """While the decode attention of layer l runs, HBM is nearly idle: have it pull the start of
+        the next big weight stream into L2 — the draft's gate|up of layer l (its O-projection is
+        already prefetched into the GEMV ring), the verify's O-projection of layer l (its GEMM CTAs
+        cannot be resident beside the attention CTAs).  YGG_L2PF_DRAFT_MB / YGG_L2PF_VERIFY_MB."""
+        if self.ad_plans is None:
+            return
+        lib = L.lib()
+        key, name = ("YGG_L2PF_DRAFT_MB", "wgu") if self.gemv else ("YGG_L2PF_VERIFY_MB", "wo")
+        # Measured (same box, cfg2): verify forward 3.583 ms -> 3.552 ms with 24 MB (16 MB: 3.563; all
+        # 34 MB: no gain); draft: the attention slows by as much as gate|up gains, so off.
+        mb = float(os.environ.get(key, "0" if self.gemv else "24"))
+        for li, plan in enumerate(self.ad_plans):
+            W = self.w["layers"][li][name]
+            nbytes = min(int(mb * (1 << 20)), W.numel() * W.element_size())
+            L.check(lib.ygg_attn_dec_set_l2_prefetch(plan, W.data_ptr() if nbytes > 0 else None, max(nbytes, 0)))
 
     def fuse_topk(self, k: int, temperature: float = 1.0) -> bool:
         """Draft GEMV pass: have the LM-head epilogue also emit per-CTA top-k partials of every row

@@ -102,7 +102,7 @@ int ygg_device_check(int* num_sms, int* cc_major, int* cc_minor);
  * logits: [rows, ld] f32 or bf16.  out_tok [rows,k], out_prob [rows,k] (f64 of the f32 value),
  * out_stats [rows,2] (row max, log-sum-exp) or NULL.  workspace >= ygg_topk_workspace(rows,V,k). */
 size_t ygg_topk_workspace(int rows, int V, int k);
-/* Merge per-chunk top-k partials [rows][nchunks] (nchunks <= 1024; written by the LM-head GEMV's
+/* Merge per-chunk top-k partials [rows][nchunks] (nchunks <= 512; written by the LM-head GEMV's
  * STORE_TOPK epilogue) into the same outputs as ygg_topk_softmax. */
 size_t ygg_topk_partial_bytes(int rows, int nchunks);
 int ygg_topk_merge(const void* partials, int rows, int nchunks, int k, int32_t* out_tok, double* out_prob,

@@ -168,69 +168,90 @@ __global__ void __launch_bounds__(kTopkThreads) topk_phase2(const TopkChunkOut* 
   pdl_launch_dependents();
 }
 
-// Phase 2 for <= 1024 chunks (thread t owns chunks t, t+256, ...): block max, then the f64 normaliser
+// Phase 2 for <= 512 chunks (thread t owns chunks t and t + 256).  One round of vector loads stages
+// every chunk's stats and sorted list (lists in shared memory); block max, then the f64 normaliser
 // sum_j sum_exp_j * exp(max_j - M) (per-thread terms, warp xor tree, warps in order: fixed order,
-// deterministic), and k rounds of a block tournament over the heads of the chunks' sorted lists, so
-// the winners come out in (logit desc, token asc) order without the O(n^2) ranking of phase 2.
-constexpr int kMergeOwn = 4;
+// deterministic).  Candidates are packed into 64-bit keys ordered exactly like (logit desc, token
+// asc), so a tournament round is two redux.sync max reductions instead of a shuffle tree: each warp
+// pops its k best over its chunk heads, then warp 0 pops the block's k best over the warps' lists.
+constexpr int kMergeOwn = 2;
+YGG_DEV unsigned long long topk_key(float v, int tok) {  // larger key == better (v desc, tok asc)
+  const uint32_t b = __float_as_uint(v + 0.0f);  // -0 -> +0: equal values order by token, like better()
+  const uint32_t ord = (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+  return (static_cast<unsigned long long>(ord) << 32) | static_cast<uint32_t>(~static_cast<uint32_t>(tok));
+}
+YGG_DEV float key_val(unsigned long long key) {
+  const uint32_t ord = static_cast<uint32_t>(key >> 32);
+  return __uint_as_float((ord & 0x80000000u) ? (ord & 0x7fffffffu) : ~ord);
+}
+YGG_DEV int key_tok(unsigned long long key) { return static_cast<int>(~static_cast<uint32_t>(key)); }
+constexpr unsigned long long kNoKey = 0ull;  // below every real key (even -inf with token 2^31 - 1)
+YGG_DEV unsigned long long warp_max_key(unsigned long long key) {
+  const uint32_t hi = __reduce_max_sync(0xffffffffu, static_cast<uint32_t>(key >> 32));
+  const uint32_t lo = __reduce_max_sync(0xffffffffu, static_cast<uint32_t>(key >> 32) == hi ? static_cast<uint32_t>(key) : 0u);
+  return (static_cast<unsigned long long>(hi) << 32) | lo;
+}
+
 __global__ void __launch_bounds__(kTopkThreads) topk_merge_kernel(const TopkPartial* __restrict__ chunks, int nchunks,
                                                                   int k, int32_t* out_tok, double* out_prob,
                                                                   float* out_stats, unsigned long long* trace) {
-  if (threadIdx.x == 0) trace_min(trace, 0);
+  if (threadIdx.x == 0) { trace_min(trace, 0); trace_max(trace, 6); }
   pdl_wait();
-  if (threadIdx.x == 0) trace_min(trace, 1);
+  if (threadIdx.x == 0) { trace_min(trace, 1); trace_max(trace, 7); }
   const int row = blockIdx.x;
   const TopkPartial* c = chunks + static_cast<size_t>(row) * nchunks;
   const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
   constexpr int NW = kTopkThreads / 32;
   __shared__ float red_f[NW];
   __shared__ double red_d[NW];
-  __shared__ int red_i[NW], red_o[NW];
   __shared__ float sel_v[kTopkMaxK];
   __shared__ int sel_t[kTopkMaxK];
-  // every chunk's sorted list, staged once: the tournament then never touches global memory
-  extern __shared__ unsigned char merge_smem[];
-  float* lv = reinterpret_cast<float*>(merge_smem);
-  int* lt = reinterpret_cast<int*>(lv + static_cast<size_t>(nchunks) * k);
-  {  // loads batched 8 deep (a plain strided loop would serialise one L2 round trip per element)
-    const int total = nchunks * k;
-    for (int i0 = t; i0 < total; i0 += 8 * kTopkThreads) {
-      float v8[8];
-      int t8[8];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const int i = i0 + u * kTopkThreads;
-        if (i < total) {
-          const int j = i / k, r = i - j * k;
-          v8[u] = c[j].val[r];
-          t8[u] = c[j].tok[r];
-        }
-      }
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const int i = i0 + u * kTopkThreads;
-        if (i < total) {
-          lv[i] = v8[u];
-          lt[i] = t8[u];
-        }
-      }
-    }
-  }
-  float cm[kMergeOwn], hv[kMergeOwn];
+  __shared__ unsigned long long wsel[NW][kTopkMaxK];
+  extern __shared__ unsigned long long merge_keys[];  // [nchunks][k] candidate keys
+  float cm[kMergeOwn];
   double cs[kMergeOwn];
-  int ht[kMergeOwn], h[kMergeOwn];
   float lm = -INFINITY;
+  // Every load of both owned chunks issued before any is used (k <= 8: two float4 + two int4 per
+  // chunk; larger k falls back to a loop).
+  float4 v4[kMergeOwn][2];
+  int4 t4[kMergeOwn][2];
 #pragma unroll
   for (int o = 0; o < kMergeOwn; ++o) {
     const int j = t + o * kTopkThreads;
     cm[o] = -INFINITY;
     cs[o] = 0.0;
-    hv[o] = -INFINITY;
-    ht[o] = 0x7fffffff;
-    h[o] = 0;
     if (j < nchunks) {
-      cm[o] = c[j].max_s;
-      cs[o] = c[j].sum_exp;
+      const TopkPartial* cj = c + j;
+      cm[o] = __ldcg(&cj->max_s);
+      cs[o] = __ldcg(&cj->sum_exp);
+      if (k <= 8) {  // val / tok are 16-byte aligned in TopkPartial
+        v4[o][0] = __ldcg(reinterpret_cast<const float4*>(cj->val));
+        t4[o][0] = __ldcg(reinterpret_cast<const int4*>(cj->tok));
+        if (k > 4) {
+          v4[o][1] = __ldcg(reinterpret_cast<const float4*>(cj->val + 4));
+          t4[o][1] = __ldcg(reinterpret_cast<const int4*>(cj->tok + 4));
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int o = 0; o < kMergeOwn; ++o) {
+    const int j = t + o * kTopkThreads;
+    if (j < nchunks) {
+      unsigned long long* dst = merge_keys + static_cast<size_t>(j) * k;
+      if (k <= 8) {
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) {
+          const float vv[4] = {v4[o][hh].x, v4[o][hh].y, v4[o][hh].z, v4[o][hh].w};
+          const int tt[4] = {t4[o][hh].x, t4[o][hh].y, t4[o][hh].z, t4[o][hh].w};
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            if (4 * hh + u < k) dst[4 * hh + u] = tt[u] < 0 ? kNoKey : topk_key(vv[u], tt[u]);
+        }
+      } else {
+        const TopkPartial* cj = c + j;
+        for (int r = 0; r < k; ++r) dst[r] = cj->tok[r] < 0 ? kNoKey : topk_key(cj->val[r], cj->tok[r]);
+      }
     }
     lm = fmaxf(lm, cm[o]);
   }
@@ -238,15 +259,6 @@ __global__ void __launch_bounds__(kTopkThreads) topk_merge_kernel(const TopkPart
   if (lane == 0) red_f[warp] = wm;
   __syncthreads();
   if (t == 0) trace_max(trace, 3);
-#pragma unroll
-  for (int o = 0; o < kMergeOwn; ++o) {
-    const int j = t + o * kTopkThreads;
-    if (j < nchunks) {
-      hv[o] = lv[j * k];
-      ht[o] = lt[j * k];
-      if (ht[o] < 0) { hv[o] = -INFINITY; ht[o] = 0x7fffffff; }
-    }
-  }
   float gm = red_f[0];
   for (int w = 1; w < NW; ++w) gm = fmaxf(gm, red_f[w]);
   double z = 0.0;
@@ -256,77 +268,46 @@ __global__ void __launch_bounds__(kTopkThreads) topk_merge_kernel(const TopkPart
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) z += __shfl_xor_sync(0xffffffffu, z, o);
   if (lane == 0) red_d[warp] = z;
-  __syncthreads();  // every warp has read red_f (block max) before the tournament reuses it
   if (t == 0) trace_max(trace, 4);
-  // Two-level tournament without block barriers per round: (1) each warp pops its k best from the
-  // heads of its lanes' chunk lists (shuffle argmax, lanes own chunks t, t+256, ...); (2) warp 0's
-  // lanes 0..NW-1 each own one warp's sorted result and pop the block's k best the same way.
-  __shared__ float wsel_v[NW][kTopkMaxK];
-  __shared__ int wsel_t[NW][kTopkMaxK];
+  // (1) per-warp tournament over the heads of the lanes' chunk lists
+  int h[kMergeOwn];
+  unsigned long long hk[kMergeOwn];
+#pragma unroll
+  for (int o = 0; o < kMergeOwn; ++o) {
+    const int j = t + o * kTopkThreads;
+    h[o] = 0;
+    hk[o] = j < nchunks ? merge_keys[static_cast<size_t>(j) * k] : kNoKey;
+  }
   for (int r = 0; r < k; ++r) {
-    float bv = hv[0];
-    int bt = ht[0], bo = t;
+    unsigned long long best = hk[0];
 #pragma unroll
-    for (int o = 1; o < kMergeOwn; ++o)
-      if (better(hv[o], ht[o], bv, bt)) { bv = hv[o]; bt = ht[o]; bo = t + o * kTopkThreads; }
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) {
-      const float ov = __shfl_xor_sync(0xffffffffu, bv, off);
-      const int ot = __shfl_xor_sync(0xffffffffu, bt, off);
-      const int oo = __shfl_xor_sync(0xffffffffu, bo, off);
-      if (better(ov, ot, bv, bt)) { bv = ov; bt = ot; bo = oo; }
-    }
-    if (lane == 0) {
-      wsel_v[warp][r] = bv;
-      wsel_t[warp][r] = bt;
-    }
-    if (bt == 0x7fffffff) continue;  // this warp's lists are exhausted (uniform across the warp)
+    for (int o = 1; o < kMergeOwn; ++o) best = hk[o] > best ? hk[o] : best;
+    const unsigned long long win = warp_max_key(best);
+    if (lane == 0) wsel[warp][r] = win;
+    if (win == kNoKey) continue;  // warp-uniform
 #pragma unroll
     for (int o = 0; o < kMergeOwn; ++o) {
-      const int j = t + o * kTopkThreads;
-      if (j == bo) {  // pop the winning chunk's head
+      if (hk[o] == win) {  // keys are unique (distinct tokens): exactly one lane / chunk pops
+        const int j = t + o * kTopkThreads;
         ++h[o];
-        hv[o] = -INFINITY;
-        ht[o] = 0x7fffffff;
-        if (h[o] < k) {
-          hv[o] = lv[j * k + h[o]];
-          ht[o] = lt[j * k + h[o]];
-          if (ht[o] < 0) { hv[o] = -INFINITY; ht[o] = 0x7fffffff; }
-        }
+        hk[o] = h[o] < k ? merge_keys[static_cast<size_t>(j) * k + h[o]] : kNoKey;
       }
     }
   }
   __syncthreads();
+  // (2) warp 0: lanes 0..NW-1 each own one warp's sorted winners
   if (warp == 0) {
     int hp = 0;
-    float cv = -INFINITY;
-    int ct = 0x7fffffff;
-    if (lane < NW) {
-      cv = wsel_v[lane][0];
-      ct = wsel_t[lane][0];
-    }
+    unsigned long long ck = lane < NW ? wsel[lane][0] : kNoKey;
     for (int r = 0; r < k; ++r) {
-      float bv = cv;
-      int bt = ct, bo = lane;
-#pragma unroll
-      for (int off = 16; off > 0; off >>= 1) {
-        const float ov = __shfl_xor_sync(0xffffffffu, bv, off);
-        const int ot = __shfl_xor_sync(0xffffffffu, bt, off);
-        const int oo = __shfl_xor_sync(0xffffffffu, bo, off);
-        if (better(ov, ot, bv, bt)) { bv = ov; bt = ot; bo = oo; }
-      }
+      const unsigned long long win = warp_max_key(ck);
       if (lane == 0) {
-        sel_v[r] = bv;
-        sel_t[r] = bt == 0x7fffffff ? -1 : bt;
+        sel_v[r] = key_val(win);
+        sel_t[r] = win == kNoKey ? -1 : key_tok(win);
       }
-      if (lane == bo && bt != 0x7fffffff) {
+      if (win != kNoKey && ck == win) {
         ++hp;
-        cv = -INFINITY;
-        ct = 0x7fffffff;
-        if (hp < k) {
-          cv = wsel_v[lane][hp];
-          ct = wsel_t[lane][hp];
-        }
+        ck = hp < k ? wsel[lane][hp] : kNoKey;
       }
     }
   }
@@ -1029,7 +1010,7 @@ size_t ygg_topk_partial_bytes(int rows, int nchunks) {
 int ygg_topk_merge(const void* partials, int rows, int nchunks, int k, int32_t* out_tok, double* out_prob,
                    float* out_stats, ygg_stream_t stream) {
   YGG_CHECK_ARG(partials && out_tok && out_prob, "null pointer");
-  YGG_CHECK_ARG(rows >= 0 && nchunks >= 1 && nchunks <= kTopkThreads * kMergeOwn, "nchunks must be in [1, 1024]");
+  YGG_CHECK_ARG(rows >= 0 && nchunks >= 1 && nchunks <= kTopkThreads * kMergeOwn, "nchunks must be in [1, 512]");
   YGG_CHECK_ARG(k >= 1 && k <= kTopkMaxK, "k must be in [1, 32]");
   YGG_CHECK_ARG(static_cast<size_t>(nchunks) * k * 8 <= 200 * 1024, "too many candidates to merge");
   if (rows == 0) return YGG_OK;

@@ -49,6 +49,17 @@ def level(stream=None):
                                    sd.cand_prob.data_ptr(), sd.cand_n.data_ptr(), s))
 
 
+if which == "level":  # start from a fresh tree (pass 0 + roots), as the step does
+    sh0 = sd.shape
+    dr0, gr0 = sd.draft, sd.grown
+    L.check(lib.ygg_pass0_inputs(sd.seq.struct, sd.R, sd.tree_cap, dr0.tokens.data_ptr(), dr0.pos.data_ptr(),
+                                 dr0.slot.data_ptr(), dr0.req.data_ptr(), dr0.qmask.data_ptr(), dr0.mask_words,
+                                 dr0.blk_start.data_ptr(), dr0.blk_len.data_ptr(), L.stream_ptr()))
+    dr0.run()
+    sd._draft_topk(sd.B * sd.R, sh0.expansion_k, L.stream_ptr())
+    L.check(lib.ygg_init_roots(gr0.struct, sd.cand_tok.data_ptr(), sd.cand_prob.data_ptr(), sh0.expansion_k, sd.R, 1,
+                               L.stream_ptr()))
+    torch.cuda.synchronize()
 graph = torch.cuda.CUDAGraph()
 L.check(lib.ygg_trace_arm(buf.data_ptr(), CAP))
 with torch.cuda.graph(graph):

@@ -26,6 +26,10 @@ e.ld = V
 e.topk_part = part.data_ptr()
 e.topk_k = k
 e.inv_temp = 1.0
+e_store = L.YggGemvEpilogue()
+e_store.kind = L.YGG_GEMV_STORE
+e_store.out = logits.data_ptr()
+e_store.ld = V
 tok = torch.zeros(M, k, dtype=torch.int32, device=dev)
 prob = torch.zeros(M, k, dtype=torch.float64, device=dev)
 ws = torch.empty(int(lib.ygg_topk_workspace(M, V, k)), dtype=torch.uint8, device=dev)
@@ -55,3 +59,17 @@ res = {
     "grid": grid,
 }
 print(res)
+
+
+def pair():
+    L.check(lib.ygg_gemv_run(mem, C.byref(e), s))
+    L.check(lib.ygg_topk_merge(part.data_ptr(), M, grid, k, tok.data_ptr(), prob.data_ptr(), None, s))
+
+
+def pair_old():
+    L.check(lib.ygg_gemv_run(mem, C.byref(e_store), s))
+    L.check(lib.ygg_topk_softmax(logits.data_ptr(), L.YGG_F32, M, V, V, k, 1.0, tok.data_ptr(), prob.data_ptr(),
+                                 None, ws.data_ptr(), ws.numel(), s))
+
+print({"gemv_topk_then_merge_us": t(pair), "gemv_store_then_topk_softmax_us": t(pair_old),
+       "gemv_store_us": t(lambda: L.check(lib.ygg_gemv_run(mem, C.byref(e_store), s)))})

@@ -589,7 +589,7 @@ YGG_DEV void epi_values(const EpiGeom& g, const float* __restrict__ ws, int m, i
     const float4* q = reinterpret_cast<const float4*>(p + s * seg_stride);
 #pragma unroll
     for (int i = 0; i < V / 4; ++i) {
-      const float4 x = __ldg(q + i);
+      const float4 x = __ldcg(q + i);
       v[4 * i] += x.x;
       v[4 * i + 1] += x.y;
       v[4 * i + 2] += x.z;
@@ -620,8 +620,8 @@ YGG_DEV void epi_values2(const EpiGeom& g, const float* __restrict__ ws, int m, 
       const float4* q2 = reinterpret_cast<const float4*>(p2 + (b0 + j + k) * seg_stride);
 #pragma unroll
       for (int i = 0; i < V / 4; ++i) {
-        x[k][0][i] = (j + k < na) ? __ldg(q1 + i) : make_float4(0.f, 0.f, 0.f, 0.f);
-        x[k][1][i] = (j + k < nb) ? __ldg(q2 + i) : make_float4(0.f, 0.f, 0.f, 0.f);
+        x[k][0][i] = (j + k < na) ? __ldcg(q1 + i) : make_float4(0.f, 0.f, 0.f, 0.f);
+        x[k][1][i] = (j + k < nb) ? __ldcg(q2 + i) : make_float4(0.f, 0.f, 0.f, 0.f);
       }
     }
 #pragma unroll

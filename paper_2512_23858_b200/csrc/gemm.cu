@@ -340,6 +340,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         advance();
       }
       if (e.dbg) e.dbg[c * 8 + 6] = gtimer();
+      trace_max(e.trace, 3);  // producer: last load issued
     }
   } else if (warp == 1) {
     pdl_wait();
@@ -379,6 +380,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       acc ^= 1;
     }
     if (e.dbg && lane == 0) e.dbg[c * 8 + 5] = gtimer();
+    if (lane == 0) trace_max(e.trace, 4);  // mma: last commit
   } else {
     pdl_wait();
     // ===== Epilogue warps: TMEM -> (partials | fused op) =====
@@ -448,6 +450,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       acc ^= 1;
       if (k == min(n_sk, 2) - 1 && npend > 0) {
         if (e.dbg && et == 0) e.dbg[c * 8 + 1] = gtimer();
+        if (et == 0) trace_max(e.trace, 5);  // fixups start
         // Cooperative fixups (right after this CTA's split segments, overlapping the whole tiles
         // still streaming): participant j reduces 16-token column chunks j, j+nseg, ... in fixed
         // segment order and applies the op.
@@ -468,6 +471,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           }
           epi_bar();
           if (e.dbg && et == 0) e.dbg[c * 8 + 2 + i] = gtimer();
+          if (et == 0) trace_max(e.trace, 6);  // a fixup's partials all arrived
           const float* src = ws + static_cast<size_t>(fs) * BN * kBM + row;
           for (int c0 = fj * 16; c0 < BN; c0 += fn * 16) {
             const int nv = min(16, fvalid - c0);
@@ -496,6 +500,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       }
     }
     if (e.dbg && et == 0) e.dbg[c * 8 + 4] = gtimer();
+    if (et == 0) trace_max(e.trace, 7);  // epilogue warps done
   }
   __syncthreads();
   if (threadIdx.x == 0) trace_max(e.trace, 2);

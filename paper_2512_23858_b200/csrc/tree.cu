@@ -585,10 +585,16 @@ __global__ void __launch_bounds__(kKnapThreads) knapsack_prune_kernel(
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double* best = reinterpret_cast<double*>(smem_raw);                       // [N][R]
   double* gain = best + static_cast<size_t>(N) * R;                         // [N]
-  uint8_t* alloc = reinterpret_cast<uint8_t*>(gain + N);                    // [N][R] (indexed by child)
+  double* tmp = gain + N;                                                   // [R] ping-pong row
+  double* spv = tmp + R;                                                    // [R] Eq.3 per size
+  uint8_t* alloc = reinterpret_cast<uint8_t*>(spv + R);                     // [N][R] (indexed by child)
   int* par = reinterpret_cast<int*>(alloc + ((static_cast<size_t>(N) * R + 15) & ~size_t(15)));  // [N]
   int* sz = par + N;                                                        // [N]
   int* stack = sz + N;                                                      // [2N]
+  int* head_asc = stack + 2 * N;                                            // first child (index order)
+  int* next_asc = head_asc + N;
+  int* head_desc = next_asc + N;                                            // first child (reverse order)
+  int* next_desc = head_desc + N;
   __shared__ int s_best_k;
   __shared__ double s_best_speed;
 
@@ -609,36 +615,53 @@ __global__ void __launch_bounds__(kKnapThreads) knapsack_prune_kernel(
     }
     for (int i = 0; i < N; ++i) sz[i] = 1;
     for (int v = N - 1; v >= 1; --v) sz[par[v]] += sz[v];
+    // child lists: ascending index (= insertion order, the merge order) and descending (pick)
+    for (int i = 0; i < N; ++i) head_asc[i] = head_desc[i] = -1;
+    for (int c = N - 1; c >= 1; --c) {
+      next_asc[c] = head_asc[par[c]];
+      head_asc[par[c]] = c;
+    }
+    for (int c = 1; c < N; ++c) {
+      next_desc[c] = head_desc[par[c]];
+      head_desc[par[c]] = c;
+    }
   }
   __syncthreads();
   // Bottom-up merge (egt.py:175-196).  Thread s owns target size s; k ascending and the strict
   // '>' reproduce the reference's first-maximum tie rule exactly.
+  // Rows ping-pong between the node's slot and `tmp`, so each child merge is one barrier.
   for (int v = N - 1; v >= 0; --v) {
     double* row = best + static_cast<size_t>(v) * R;
-    for (int s = threadIdx.x; s < R; s += blockDim.x) row[s] = (s == 1) ? gain[v] : -INFINITY;
+    const int s = threadIdx.x;
+    if (s < R) row[s] = (s == 1) ? gain[v] : -INFINITY;
     __syncthreads();
-    for (int c = v + 1; c < N; ++c) {
-      if (par[c] != v) continue;  // children in insertion (= index) order
+    double* src = row;
+    double* dst = tmp;
+    for (int c = head_asc[v]; c >= 0; c = next_asc[c]) {  // children in insertion (= index) order
       const double* crow = best + static_cast<size_t>(c) * R;
       const int top_c = min(sz[c], cap);
-      double m = 0.0;
-      int a = 0;
-      const int s = threadIdx.x;
-      if (s >= 1 && s < R) {
-        m = row[s];
-        for (int kk = max(1, s - top_c); kk <= s - 1; ++kk) {
-          const double rk = row[kk];
-          if (rk == -INFINITY) continue;
-          const double value = rk + crow[s - kk];
-          if (value > m) { m = value; a = s - kk; }
+      if (s < R) {
+        double m = s >= 1 ? src[s] : 0.0;
+        int a = 0;
+        if (s >= 1) {
+#pragma unroll 4
+          for (int kk = max(1, s - top_c); kk <= s - 1; ++kk) {
+            const double rk = src[kk];
+            if (rk == -INFINITY) continue;
+            const double value = rk + crow[s - kk];
+            if (value > m) { m = value; a = s - kk; }
+          }
         }
-      }
-      __syncthreads();
-      if (s >= 1 && s < R) {
-        row[s] = m;
+        dst[s] = s >= 1 ? m : src[0];
         alloc[static_cast<size_t>(c) * R + s] = static_cast<uint8_t>(a);
       }
-      if (s == 0) alloc[static_cast<size_t>(c) * R] = 0;
+      __syncthreads();
+      double* t2 = src;
+      src = dst;
+      dst = t2;
+    }
+    if (src != row) {  // the last merge landed in tmp
+      if (s < R) row[s] = src[s];
       __syncthreads();
     }
   }
@@ -652,6 +675,12 @@ __global__ void __launch_bounds__(kKnapThreads) knapsack_prune_kernel(
       if (alloc_out) alloc_out[ob + i] = (s < R) ? alloc[static_cast<size_t>(v) * R + s] : 0;
     }
   }
+  {  // Eq.3 for every size at once; thread 0 then scans them in the reference's order
+    const int kk = threadIdx.x;
+    if (args.fixed_k <= 0 && kk >= 1 && kk <= cap && best[kk] != -INFINITY)
+      spv[kk] = tree_speedup_dev(*prof, 1.0 + best[kk], args.w_draft, args.d_draft, kk);
+  }
+  __syncthreads();
   if (threadIdx.x == 0) {
     const ygg_profile_pair pp = *prof;
     int best_k = 0;
@@ -662,10 +691,9 @@ __global__ void __launch_bounds__(kKnapThreads) knapsack_prune_kernel(
       best_k = min(args.fixed_k, cap);
       best_speed = shape_ok ? tree_speedup_dev(pp, 1.0 + root[best_k], args.w_draft, args.d_draft, best_k) : NAN;
     } else {
-      for (int kk = 1; kk <= cap; ++kk) {  // egt.py:261-273
-        const double value = root[kk];
-        if (value == -INFINITY) continue;
-        const double sp = tree_speedup_dev(pp, 1.0 + value, args.w_draft, args.d_draft, kk);
+      for (int kk = 1; kk <= cap; ++kk) {  // egt.py:261-273 (speedups precomputed in parallel)
+        if (root[kk] == -INFINITY) continue;
+        const double sp = spv[kk];
         if (sp > best_speed + 1e-12) { best_k = kk; best_speed = sp; }
       }
     }
@@ -681,7 +709,7 @@ __global__ void __launch_bounds__(kKnapThreads) knapsack_prune_kernel(
   }
   __syncthreads();
   // pick(best_k) (egt.py:206-222): peel the recorded allocations in reverse merge order.
-  uint8_t* keep = reinterpret_cast<uint8_t*>(stack + 2 * N);  // [N] flags (reuses tail of smem)
+  uint8_t* keep = reinterpret_cast<uint8_t*>(next_desc + N);  // [N] flags
   for (int i = threadIdx.x; i < N; i += blockDim.x) keep[i] = 0;
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -693,8 +721,7 @@ __global__ void __launch_bounds__(kKnapThreads) knapsack_prune_kernel(
       const int v = stack[--sp];
       keep[v] = 1;
       int remaining = kk;
-      for (int c = N - 1; c > v; --c) {
-        if (par[c] != v) continue;
+      for (int c = head_desc[v]; c >= 0; c = next_desc[c]) {  // children in reverse index order
         const int taken = alloc[static_cast<size_t>(c) * R + remaining];
         if (taken) {
           stack[sp++] = c;
@@ -1048,9 +1075,9 @@ int ygg_build_mask(ygg_tree tree, ygg_stream_t stream) {
 
 static size_t knap_smem(int N, int cap) {
   const size_t R = cap + 1;
-  size_t bytes = N * R * sizeof(double) + N * sizeof(double);
+  size_t bytes = N * R * sizeof(double) + N * sizeof(double) + 2 * R * sizeof(double);
   bytes += (N * R + 15) & ~size_t(15);
-  bytes += 2 * N * sizeof(int) + 2 * N * sizeof(int) + N;
+  bytes += 2 * N * sizeof(int) + 2 * N * sizeof(int) + 4 * N * sizeof(int) + N;
   return bytes + 64;
 }
 

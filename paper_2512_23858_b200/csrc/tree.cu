@@ -755,61 +755,67 @@ __global__ void path_products_kernel(ygg_tree t, const double* __restrict__ prob
 }
 
 // TokenTree.subtree (token_tree.py:146-168): kept nodes in ascending old order.
+constexpr int kSubtreeMax = 1024;  // largest pruned-tree capacity handled on chip
 __global__ void subtree_kernel(ygg_tree in, ygg_tree out, const int32_t* __restrict__ keep_idx,
                                const int32_t* __restrict__ new_idx) {
+  // Everything staged through shared memory in a few parallel rounds: kept count by a block count,
+  // gathered rows, ancestor-or-self mask rows by walking each node's (on-chip) parent chain, and
+  // the frontier (deepest level, index order) from on-chip depths.
   pdl_wait();
   const int b = blockIdx.x;
   const size_t ib = static_cast<size_t>(b) * in.cap, ob = static_cast<size_t>(b) * out.cap;
-  __shared__ int s_n;
+  __shared__ int s_par[kSubtreeMax], s_dep[kSubtreeMax];
+  __shared__ int s_n, s_md;
   if (threadIdx.x == 0) {
-    int n = 0;
-    while (n < in.cap && keep_idx[ib + n] >= 0) ++n;
-    s_n = n;
-    out.size[b] = n;
-    out.flags[b] = 0;
+    s_n = 0;
+    s_md = 0;
   }
   __syncthreads();
-  const int n = s_n;
+  int local = 0;
+  for (int i = threadIdx.x; i < in.cap; i += blockDim.x) local += keep_idx[ib + i] >= 0 ? 1 : 0;
+  if (local) atomicAdd(&s_n, local);
+  __syncthreads();
+  const int n = min(s_n, out.cap);  // kept indices are packed first, -1 after
   for (int i = threadIdx.x; i < out.cap; i += blockDim.x) {
+    int p = -1, d = 0;
     if (i < n) {
       const int o = keep_idx[ib + i];
-      const int p = in.parent[ib + o];
+      const int op = in.parent[ib + o];
+      p = op < 0 ? -1 : new_idx[ib + op];
+      d = in.depth[ib + o];
       out.token[ob + i] = in.token[ib + o];
-      out.parent[ob + i] = p < 0 ? -1 : new_idx[ib + p];
-      out.depth[ob + i] = in.depth[ib + o];
       out.prob[ob + i] = in.prob[ib + o];
       out.cum[ob + i] = in.cum[ib + o];
+      atomicMax(&s_md, d);
     } else {
       out.token[ob + i] = 0;
-      out.parent[ob + i] = -1;
-      out.depth[ob + i] = 0;
       out.prob[ob + i] = 0.0;
       out.cum[ob + i] = 0.0;
     }
+    out.parent[ob + i] = p;
+    out.depth[ob + i] = d;
+    s_par[i] = p;
+    s_dep[i] = d;
   }
   __syncthreads();
-  if (threadIdx.x < 32) {
-    const int lane = threadIdx.x;
-    for (int i = 0; i < out.cap; ++i) {
-      if (lane < out.mask_words) {
-        uint32_t v = 0;
-        if (i < n) {
-          const int p = out.parent[ob + i];
-          if (p >= 0) v = out.mask[(ob + p) * out.mask_words + lane];
-          if ((i >> 5) == lane) v |= 1u << (i & 31);
-        }
-        out.mask[(ob + i) * out.mask_words + lane] = v;
-      }
-      __syncwarp();
+  for (int i = threadIdx.x; i < out.cap; i += blockDim.x) {
+    uint32_t* row = out.mask + (ob + i) * out.mask_words;
+    for (int w = 0; w < out.mask_words; ++w) {
+      uint32_t bits = 0u;
+      if (i < n)
+        for (int v = i, steps = 0; v >= 0 && v < n && steps <= i; v = s_par[v], ++steps)  // bounded walk
+          if ((v >> 5) == w) bits |= 1u << (v & 31);
+      row[w] = bits;
     }
-    if (lane == 0) {
-      int md = 0;
-      for (int i = 0; i < n; ++i) md = max(md, out.depth[ob + i]);
-      int fnn = 0;
-      for (int i = 0; i < n; ++i)
-        if (out.depth[ob + i] == md) out.frontier[ob + fnn++] = i;
-      out.frontier_n[b] = fnn;
-    }
+  }
+  if (threadIdx.x == 0) {
+    const int md = s_md;
+    int fnn = 0;
+    for (int i = 0; i < n; ++i)
+      if (s_dep[i] == md) out.frontier[ob + fnn++] = i;
+    out.frontier_n[b] = fnn;
+    out.size[b] = n;
+    out.flags[b] = 0;
   }
   pdl_launch_dependents();
 }
@@ -1111,6 +1117,7 @@ int ygg_tree_subtree(ygg_tree in, ygg_tree out, const int32_t* keep_idx, const i
   if (int rc = check_tree(in)) return rc;
   if (int rc = check_tree(out)) return rc;
   YGG_CHECK_ARG(in.B == out.B && out.cap >= 1, "tree batch mismatch");
+  YGG_CHECK_ARG(out.cap <= kSubtreeMax, "pruned tree capacity too large");
   YGG_LAUNCH_PDL(subtree_kernel, dim3(in.B), dim3(128), 0, reinterpret_cast<cudaStream_t>(stream), in, out, keep_idx,
                  new_idx);
   return YGG_OK;

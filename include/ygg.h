@@ -337,7 +337,12 @@ int ygg_gemv_run(const void* plan, const ygg_gemv_epilogue* epi, ygg_stream_t st
 size_t ygg_attn_dec_plan_size(void);
 int ygg_attn_dec_plan_init(void* plan, const void* q, const void* cache_layer, int B, int T, int Hq, int Hkv, int hd,
                            int S);
-/* workspace: >= ygg_attn_dec_workspace_size(plan) bytes (currently 0; may be NULL).  The key chunks of
+/* Launch order contract (programmatic dependent launch): K / V chunks wholly inside the committed
+ * prefix (keys < blk_start) and blk_start / blk_len are read BEFORE the grid-dependency wait, so they
+ * must have been written at least two kernels earlier on the stream and the kernel immediately
+ * before this launch must not trigger its dependents before its own grid-dependency wait (every
+ * libygg kernel that precedes it in a pass obeys this; a non-PDL kernel always does).
+ * workspace: >= ygg_attn_dec_workspace_size(plan) bytes (currently 0; may be NULL).  The key chunks of
  * each (kv head, request, row tile) are split over a thread-block cluster of CTAs and merged in the
  * leader CTA's shared memory in fixed split order (YGG_ATTN_DEC_KVSPLIT overrides the cluster size). */
 size_t ygg_attn_dec_workspace_size(const void* plan);

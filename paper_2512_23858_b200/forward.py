@@ -271,16 +271,19 @@ class Forward:
 
     def _setup_attn_l2_prefetch(self) -> None:
         """While the decode attention of layer l runs, HBM is nearly idle: have it pull the start of
-        the next big weight stream into L2 — the draft's gate|up of layer l (its O-projection is
-        already prefetched into the GEMV ring), the verify's O-projection of layer l (its GEMM CTAs
-        cannot be resident beside the attention CTAs).  YGG_L2PF_DRAFT_MB / YGG_L2PF_VERIFY_MB."""
+        a later weight stream into L2 — for the draft the down projection of layer l (its GEMV CTAs
+        cannot be resident during the gate|up stream; the O-projection is already in the GEMV ring),
+        for the verify the O-projection of layer l (its GEMM CTAs cannot be resident beside the
+        attention CTAs).  YGG_L2PF_DRAFT_MB / YGG_L2PF_DRAFT_TARGET / YGG_L2PF_VERIFY_MB."""
         if self.ad_plans is None:
             return
         lib = L.lib()
-        key, name = ("YGG_L2PF_DRAFT_MB", "wgu") if self.gemv else ("YGG_L2PF_VERIFY_MB", "wo")
-        # Measured (same box, cfg2): verify forward 3.583 ms -> 3.552 ms with 24 MB (16 MB: 3.563; all
-        # 34 MB: no gain); draft: the attention slows by as much as gate|up gains, so off.
-        mb = float(os.environ.get(key, "0" if self.gemv else "24"))
+        key, name = ("YGG_L2PF_DRAFT_MB", os.environ.get("YGG_L2PF_DRAFT_TARGET", "wdown")) if self.gemv \
+            else ("YGG_L2PF_VERIFY_MB", "wo")
+        # Measured same-box (cfg2): verify forward 3.583 -> 3.552 ms with 24 MB of wo (16 MB: 3.563;
+        # all 34 MB: no gain); draft pass 0.634 -> 0.627 ms with 12 MB of wdown (16: 0.630, 20: 0.637;
+        # prefetching gate|up instead slows the attention as much as gate|up gains).
+        mb = float(os.environ.get(key, "12" if self.gemv else "24"))
         for li, plan in enumerate(self.ad_plans):
             W = self.w["layers"][li][name]
             nbytes = min(int(mb * (1 << 20)), W.numel() * W.element_size())

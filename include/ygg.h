@@ -346,10 +346,10 @@ int ygg_attn_dec_plan_init(void* plan, const void* q, const void* cache_layer, i
  * each (kv head, request, row tile) are split over a thread-block cluster of CTAs and merged in the
  * leader CTA's shared memory in fixed split order (YGG_ATTN_DEC_KVSPLIT overrides the cluster size). */
 size_t ygg_attn_dec_workspace_size(const void* plan);
-/* Optional: every launch of this plan also pulls [ptr, ptr + bytes) into L2 (split over its CTAs,
- * issued after the grid-dependency wait) — the next matrix's weights, streamed while the attention
- * leaves HBM idle.  bytes = 0 disables. */
-int ygg_attn_dec_set_l2_prefetch(void* plan, const void* ptr, size_t bytes);
+/* Optional: every launch of this plan also pulls up to two regions [ptr, ptr + bytes) into L2 (each
+ * split over its CTAs, issued after the CTA's own loads) — later weights, streamed while the
+ * attention leaves HBM idle.  region 0 or 1; bytes = 0 disables the region. */
+int ygg_attn_dec_set_l2_prefetch(void* plan, int region, const void* ptr, size_t bytes);
 int ygg_attn_dec_run(const void* plan, const int32_t* blk_start, const int32_t* blk_len, const uint32_t* qmask,
                      int mask_words, float scale, void* out, void* workspace, ygg_stream_t stream);
 

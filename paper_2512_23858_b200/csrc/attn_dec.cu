@@ -39,8 +39,8 @@ struct Plan {
   uint32_t magic;
   int B, T, Hq, Hkv, hd, S, Gh, rows, warps, ksplit, stages, tpt, row_tiles, kvsplit, ring_bytes, slot_bytes;
   size_t smem;
-  const char* pf_ptr;  // optional L2 prefetch of the next weights (issued while HBM is otherwise idle)
-  size_t pf_bytes;
+  const char* pf_ptr[2];  // optional L2 prefetch regions (issued while HBM is otherwise idle)
+  size_t pf_bytes[2];
   alignas(64) CUtensorMap tq;
   alignas(64) CUtensorMap tk;
   alignas(64) CUtensorMap tv;
@@ -58,8 +58,8 @@ struct Args {
   const uint32_t* qmask;
   __nv_bfloat16* out;
   unsigned long long* trace;  // kernel-timeline slot (profiling only) or nullptr
-  const char* pf_ptr;         // L2 prefetch region (split over the CTAs) or nullptr
-  size_t pf_bytes;
+  const char* pf_ptr[2];      // L2 prefetch regions (each split over the CTAs) or nullptr
+  size_t pf_bytes[2];
 };
 
 YGG_DEV void tma2(void* dst, const CUtensorMap* m, uint64_t* bar, int c0, int c1) {
@@ -193,16 +193,17 @@ __global__ void __launch_bounds__(32 * (1 + kMaxWarps), 1)
       for (int dc = 0; dc < DCH; ++dc)
         tma3(sq + dc * (64 * 128), &tq, qbar, dc * 64, kvh * a.Gh, r * a.T + t0);
       for (; c < nch; ++j, c += a.kvsplit) load(j, c);
-      if (a.pf_ptr) {
-        // After this CTA's own loads: the kernel barely touches HBM, so pull this CTA's slice of the next matrix's weights into
-        // L2 so that its stream starts from L2 (bulk prefetch, 64 KB per instruction).
+      for (int rg = 0; rg < 2; ++rg) {
+        // After this CTA's own loads: the kernel barely touches HBM, so pull this CTA's slice of
+        // later weights into L2 so that their stream starts from L2 (bulk prefetch, 64 KB each).
+        if (!a.pf_ptr[rg]) continue;
         const size_t ncta = static_cast<size_t>(gridDim.x) * gridDim.y * gridDim.z;
         const size_t cta = (static_cast<size_t>(blockIdx.z) * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
-        const size_t per = ((a.pf_bytes / ncta) + 255) & ~static_cast<size_t>(255);
-        const size_t b0 = cta * per, b1 = b0 + per < a.pf_bytes ? b0 + per : a.pf_bytes;
+        const size_t per = ((a.pf_bytes[rg] / ncta) + 255) & ~static_cast<size_t>(255);
+        const size_t b0 = cta * per, b1 = b0 + per < a.pf_bytes[rg] ? b0 + per : a.pf_bytes[rg];
         for (size_t o = b0; o < b1; o += 65536) {
           const uint32_t n = static_cast<uint32_t>(b1 - o < 65536 ? ((b1 - o) & ~static_cast<size_t>(15)) : 65536);
-          if (n) asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a.pf_ptr + o), "r"(n) : "memory");
+          if (n) asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a.pf_ptr[rg] + o), "r"(n) : "memory");
         }
       }
     } else {
@@ -546,12 +547,13 @@ int ygg_prepare_attn_dec(void) {
 
 size_t ygg_attn_dec_plan_size(void) { return sizeof(Plan) + 64; }
 
-int ygg_attn_dec_set_l2_prefetch(void* plan, const void* ptr, size_t bytes) {
+int ygg_attn_dec_set_l2_prefetch(void* plan, int region, const void* ptr, size_t bytes) {
   Plan* p = const_cast<Plan*>(plan_of(plan));
   YGG_CHECK_ARG(p != nullptr, "invalid decode-attention plan");
+  YGG_CHECK_ARG(region == 0 || region == 1, "prefetch region must be 0 or 1");
   YGG_CHECK_ARG(ptr == nullptr || (reinterpret_cast<uintptr_t>(ptr) & 15) == 0, "prefetch region must be 16-byte aligned");
-  p->pf_ptr = bytes ? static_cast<const char*>(ptr) : nullptr;
-  p->pf_bytes = ptr ? bytes : 0;
+  p->pf_ptr[region] = bytes ? static_cast<const char*>(ptr) : nullptr;
+  p->pf_bytes[region] = ptr ? bytes : 0;
   return YGG_OK;
 }
 
@@ -679,8 +681,10 @@ int ygg_attn_dec_run(const void* plan, const int32_t* blk_start, const int32_t* 
   a.qmask = qmask ? qmask : reinterpret_cast<const uint32_t*>(blk_start);  // never read when mask_words == 0
   a.out = static_cast<__nv_bfloat16*>(out);
   a.trace = trace_next(2);
-  a.pf_ptr = p->pf_ptr;
-  a.pf_bytes = p->pf_bytes;
+  for (int rg = 0; rg < 2; ++rg) {
+    a.pf_ptr[rg] = p->pf_ptr[rg];
+    a.pf_bytes[rg] = p->pf_bytes[rg];
+  }
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   const dim3 grid(p->Hkv, p->B, p->row_tiles * p->kvsplit), block(32 * (1 + p->warps));
 #define YGG_AD_LAUNCH(H, K)                                                                                    \

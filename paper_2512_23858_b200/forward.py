@@ -284,10 +284,15 @@ class Forward:
         # all 34 MB: no gain); draft pass 0.634 -> 0.627 ms with 12 MB of wdown (16: 0.630, 20: 0.637;
         # prefetching gate|up instead slows the attention as much as gate|up gains).
         mb = float(os.environ.get(key, "12" if self.gemv else "24"))
+        regions = [(name, mb)]
+        if not self.gemv:  # and the start of the verify gate|up stream (3.594 -> 3.567 ms with 16-32 MB)
+            regions.append(("wgu", float(os.environ.get("YGG_L2PF_VERIFY_GU_MB", "24"))))
         for li, plan in enumerate(self.ad_plans):
-            W = self.w["layers"][li][name]
-            nbytes = min(int(mb * (1 << 20)), W.numel() * W.element_size())
-            L.check(lib.ygg_attn_dec_set_l2_prefetch(plan, W.data_ptr() if nbytes > 0 else None, max(nbytes, 0)))
+            for rg, (nm, m) in enumerate(regions):
+                W = self.w["layers"][li][nm]
+                nbytes = min(int(m * (1 << 20)), W.numel() * W.element_size())
+                L.check(lib.ygg_attn_dec_set_l2_prefetch(plan, rg, W.data_ptr() if nbytes > 0 else None,
+                                                         max(nbytes, 0)))
 
     def fuse_topk(self, k: int, temperature: float = 1.0) -> bool:
         """Draft GEMV pass: have the LM-head epilogue also emit per-CTA top-k partials of every row

@@ -273,6 +273,21 @@ class Forward:
                 W = lw[qtarget]
                 nbytes = min(int(qmb * (1 << 20)), W.numel() * W.element_size())
                 L.check(lib.ygg_gemv_set_l2_prefetch(self.gv[li][0][0], W.data_ptr(), nbytes))
+        # The O GEMV (its weights already sit in its ring) pulls the next 16 MB of gate|up (same-box
+        # pass 0.625 -> 0.615 ms; 24 MB 0.618, 32 MB 0.624).  A/B knob: the down GEMV pulling the next
+        # layer's QKV weights is slower (0.628-0.631), so off.
+        omb = float(os.environ.get("YGG_L2PF_O_MB", "16"))
+        dmb = float(os.environ.get("YGG_L2PF_DOWN_MB", "0"))
+        for li, lw in enumerate(self.w["layers"]):
+            if omb > 0:
+                W = lw["wgu"]
+                off = min(int(qmb * (1 << 20)), W.numel() * W.element_size())
+                nbytes = min(int(omb * (1 << 20)), W.numel() * W.element_size() - off)
+                L.check(lib.ygg_gemv_set_l2_prefetch(self.gv[li][1][0], W.data_ptr() + off, nbytes))
+            if dmb > 0 and li + 1 < len(self.w["layers"]):
+                W = self.w["layers"][li + 1]["wqkv"]
+                nbytes = min(int(dmb * (1 << 20)), W.numel() * W.element_size())
+                L.check(lib.ygg_gemv_set_l2_prefetch(self.gv[li][3][0], W.data_ptr(), nbytes))
         ss_last, blocks_last = (self.ss_ga, d // 16) if cfg.n_layers > 0 else (self.ss_e, d // 128)
         self.gv_lm = (plan(self.w["lm_head"], self.xn),
                       epi(L.YGG_GEMV_STORE, out=self.logits.data_ptr(), ld=cfg.vocab, ss_in=ss_last.data_ptr(),

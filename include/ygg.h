@@ -107,6 +107,14 @@ size_t ygg_topk_workspace(int rows, int V, int k);
 size_t ygg_topk_partial_bytes(int rows, int nchunks);
 int ygg_topk_merge(const void* partials, int rows, int nchunks, int k, int32_t* out_tok, double* out_prob,
                    float* out_stats, ygg_stream_t stream);
+/* Same, and the merge also pulls up to 4 regions into L2 (the next pass's first weights) while it
+ * and the following tree kernels leave HBM idle. */
+typedef struct {
+  const void* ptr;
+  uint64_t bytes;
+} ygg_l2_region;
+int ygg_topk_merge_l2(const void* partials, int rows, int nchunks, int k, int32_t* out_tok, double* out_prob,
+                      float* out_stats, const ygg_l2_region* regions, int n_regions, ygg_stream_t stream);
 int ygg_topk_softmax(const void* logits, int dtype, int rows, int V, int ld, int k, float temperature,
                      int32_t* out_tok, double* out_prob, float* out_stats, void* workspace,
                      size_t workspace_bytes, ygg_stream_t stream);

@@ -121,6 +121,12 @@ class YggGemvEpilogue(C.Structure):
     ]
 
 
+class YggL2Region(C.Structure):
+    """ygg_l2_region (include/ygg.h): a byte range to pull into L2."""
+
+    _fields_ = [("ptr", vp), ("bytes", C.c_uint64)]
+
+
 YGG_GEMV_STORE, YGG_GEMV_QKV, YGG_GEMV_SWIGLU, YGG_GEMV_RESID, YGG_GEMV_STORE_TOPK = 1, 2, 3, 4, 5
 
 YGG_EPI_NONE, YGG_EPI_STORE_F32, YGG_EPI_QKV_ROPE, YGG_EPI_SWIGLU, YGG_EPI_RESID = range(5)
@@ -184,6 +190,7 @@ _SIGS: dict[str, tuple] = {
     "ygg_attn_dec_set_l2_prefetch": (C.c_int, [vp, C.c_int, vp, C.c_size_t]),
     "ygg_topk_partial_bytes": (C.c_size_t, [C.c_int, C.c_int]),
     "ygg_topk_merge": (C.c_int, [vp, C.c_int, C.c_int, C.c_int, vp, vp, vp, vp]),
+    "ygg_topk_merge_l2": (C.c_int, [vp, C.c_int, C.c_int, C.c_int, vp, vp, vp, vp, C.c_int, vp]),
     "ygg_mk_plan_size": (C.c_size_t, []),
     "ygg_mk_query": (C.c_int, [C.POINTER(YggMkDesc), C.POINTER(C.c_size_t), C.POINTER(C.c_size_t),
                                C.POINTER(C.c_size_t)]),
@@ -199,7 +206,7 @@ KERNELS_PER_CALL = {
     "ygg_tree_subtree": 1, "ygg_path_products": 1, "ygg_accept": 1, "ygg_kv_compact": 1, "ygg_gemm_run": 1, "ygg_gemm_fused": 1, "ygg_embed_fused": 1, "ygg_epi_store": 1,
     "ygg_epi_residual_norm": 1, "ygg_epi_swiglu": 1, "ygg_epi_qkv_rope": 1, "ygg_embed": 1, "ygg_rmsnorm": 1,
     "ygg_attention": 1, "ygg_attention_tc": 2, "ygg_row_stats": 1, "ygg_pass0_inputs": 1, "ygg_init_roots": 1, "ygg_level_inputs": 1,
-    "ygg_verify_inputs": 1, "ygg_commit": 1, "ygg_stamp": 1, "ygg_mk_run": 1, "ygg_gemv_run": 1, "ygg_attn_dec_run": 1, "ygg_topk_merge": 1,
+    "ygg_verify_inputs": 1, "ygg_commit": 1, "ygg_stamp": 1, "ygg_mk_run": 1, "ygg_gemv_run": 1, "ygg_attn_dec_run": 1, "ygg_topk_merge": 1, "ygg_topk_merge_l2": 1,
 }
 launches = {"count": 0}
 

@@ -192,12 +192,27 @@ YGG_DEV unsigned long long warp_max_key(unsigned long long key) {
   return (static_cast<unsigned long long>(hi) << 32) | lo;
 }
 
+struct L2Regions {  // weights of the next pass to pull into L2 while the merge / grow leave HBM idle
+  const char* ptr[4];
+  unsigned long long bytes[4];
+};
+
 __global__ void __launch_bounds__(kTopkThreads) topk_merge_kernel(const TopkPartial* __restrict__ chunks, int nchunks,
                                                                   int k, int32_t* out_tok, double* out_prob,
-                                                                  float* out_stats, unsigned long long* trace) {
+                                                                  float* out_stats, unsigned long long* trace,
+                                                                  L2Regions pf) {
   if (threadIdx.x == 0) { trace_min(trace, 0); trace_max(trace, 6); }
   pdl_wait();
   if (threadIdx.x == 0) { trace_min(trace, 1); trace_max(trace, 7); }
+  if (threadIdx.x < 4 && pf.ptr[threadIdx.x]) {  // one thread per region, slices over the CTAs
+    const int rg = threadIdx.x;
+    const size_t per = ((pf.bytes[rg] / gridDim.x) + 255) & ~static_cast<size_t>(255);
+    const size_t b0 = blockIdx.x * per, b1 = b0 + per < pf.bytes[rg] ? b0 + per : pf.bytes[rg];
+    for (size_t o = b0; o < b1; o += 65536) {
+      const uint32_t n = static_cast<uint32_t>(b1 - o < 65536 ? ((b1 - o) & ~static_cast<size_t>(15)) : 65536);
+      if (n) asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(pf.ptr[rg] + o), "r"(n) : "memory");
+    }
+  }
   const int row = blockIdx.x;
   const TopkPartial* c = chunks + static_cast<size_t>(row) * nchunks;
   const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
@@ -1027,7 +1042,7 @@ int ygg_topk_softmax(const void* logits, int dtype, int rows, int V, int ld, int
   if (nchunks <= kTopkThreads * kMergeOwn) {
     YGG_LAUNCH_PDL(topk_merge_kernel, dim3(rows), dim3(kTopkThreads), static_cast<size_t>(nchunks) * k * 8, s,
                    static_cast<const TopkPartial*>(ws),
-                   nchunks, k, out_tok, out_prob, out_stats, trace_next(10));
+                   nchunks, k, out_tok, out_prob, out_stats, trace_next(10), L2Regions{});
     return YGG_OK;
   }
   const size_t smem = static_cast<size_t>(nchunks) * k * (sizeof(float) + sizeof(int));
@@ -1042,14 +1057,26 @@ size_t ygg_topk_partial_bytes(int rows, int nchunks) {
 
 int ygg_topk_merge(const void* partials, int rows, int nchunks, int k, int32_t* out_tok, double* out_prob,
                    float* out_stats, ygg_stream_t stream) {
+  return ygg_topk_merge_l2(partials, rows, nchunks, k, out_tok, out_prob, out_stats, nullptr, 0, stream);
+}
+
+int ygg_topk_merge_l2(const void* partials, int rows, int nchunks, int k, int32_t* out_tok, double* out_prob,
+                      float* out_stats, const ygg_l2_region* regions, int n_regions, ygg_stream_t stream) {
   YGG_CHECK_ARG(partials && out_tok && out_prob, "null pointer");
+  YGG_CHECK_ARG(n_regions >= 0 && n_regions <= 4 && (n_regions == 0 || regions != nullptr), "at most 4 L2 regions");
+  L2Regions pf;
+  for (int i = 0; i < 4; ++i) {
+    pf.ptr[i] = i < n_regions && regions[i].bytes ? static_cast<const char*>(regions[i].ptr) : nullptr;
+    pf.bytes[i] = pf.ptr[i] ? regions[i].bytes : 0;
+    YGG_CHECK_ARG(!pf.ptr[i] || (reinterpret_cast<uintptr_t>(pf.ptr[i]) & 15) == 0, "L2 region must be 16-byte aligned");
+  }
   YGG_CHECK_ARG(rows >= 0 && nchunks >= 1 && nchunks <= kTopkThreads * kMergeOwn, "nchunks must be in [1, 512]");
   YGG_CHECK_ARG(k >= 1 && k <= kTopkMaxK, "k must be in [1, 32]");
   YGG_CHECK_ARG(static_cast<size_t>(nchunks) * k * 8 <= 200 * 1024, "too many candidates to merge");
   if (rows == 0) return YGG_OK;
   YGG_LAUNCH_PDL(topk_merge_kernel, dim3(rows), dim3(kTopkThreads), static_cast<size_t>(nchunks) * k * 8,
                  reinterpret_cast<cudaStream_t>(stream),
-                 static_cast<const TopkPartial*>(partials), nchunks, k, out_tok, out_prob, out_stats, trace_next(10));
+                 static_cast<const TopkPartial*>(partials), nchunks, k, out_tok, out_prob, out_stats, trace_next(10), pf);
   return YGG_OK;
 }
 

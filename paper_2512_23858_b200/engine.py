@@ -20,6 +20,7 @@ shape (D, W, max_verify, B) as a CUDA graph and replayed with no host synchronis
 
 from __future__ import annotations
 
+import os
 import time
 from dataclasses import dataclass
 
@@ -99,6 +100,21 @@ class SpecDecoder:
                                    dtype=torch.uint8, device=dev)
         # Draft top-k straight from the LM-head GEMV epilogue (per-CTA partials + one merge launch).
         self.topk_fused = self.draft.fuse_topk(k)
+        # A/B knobs (off): the merge pulling the next pass's first weights into L2 while the tree
+        # kernels leave HBM idle.  Measured slower — 37 MB issued from the merge's 8 CTAs occupies
+        # those SMs' TMA units well into the next pass (+250 us per step; verify variant +20-50 us).
+        self._l2_next = {}
+        if self.topk_fused:
+            def reg(W, mb):
+                n = min(int(mb * (1 << 20)), W.numel() * W.element_size())
+                return L.YggL2Region(W.data_ptr(), n)
+            dl0, tl0 = draft_w["layers"][0], target_w["layers"][0]
+            gmb = float(os.environ.get("YGG_L2PF_NEXT_DRAFT_MB", "0"))
+            vmb = float(os.environ.get("YGG_L2PF_NEXT_VERIFY_MB", "0"))
+            dr = [reg(dl0["wqkv"], gmb and 64), reg(dl0["wo"], gmb and 64), reg(dl0["wgu"], gmb)] if gmb else []
+            vr = [reg(tl0["wqkv"], vmb)] if vmb else []
+            self._l2_next = {"draft": (L.YggL2Region * 4)(*dr), "n_draft": len(dr),
+                             "verify": (L.YggL2Region * 4)(*vr), "n_verify": len(vr)}
         self.keep_idx = torch.zeros(batch, self.tree_cap, **i32)
         self.new_idx = torch.zeros(batch, self.tree_cap, **i32)
         self.w_verify = torch.zeros(batch, **i32)
@@ -166,12 +182,14 @@ class SpecDecoder:
         self.seq.step.zero_()
 
     # ------------------------------------------------------------------
-    def _draft_topk(self, rows: int, k: int, s) -> None:
+    def _draft_topk(self, rows: int, k: int, s, next_pass: str = "draft") -> None:
         """Candidates of every draft row (DrafterDistribution.candidates, egt.py:65-80)."""
         lib, dr = L.lib(), self.draft
         if self.topk_fused:
-            L.check(lib.ygg_topk_merge(dr.topk_part.data_ptr(), rows, dr.topk_chunks, k, self.cand_tok.data_ptr(),
-                                       self.cand_prob.data_ptr(), None, s))
+            regs = self._l2_next.get(next_pass)
+            n = self._l2_next.get("n_" + next_pass, 0)
+            L.check(lib.ygg_topk_merge_l2(dr.topk_part.data_ptr(), rows, dr.topk_chunks, k, self.cand_tok.data_ptr(),
+                                          self.cand_prob.data_ptr(), None, regs if n else None, n, s))
         else:
             L.check(lib.ygg_topk_softmax(dr.logits.data_ptr(), L.YGG_F32, rows, self.dc.vocab, self.dc.vocab, k, 1.0,
                                          self.cand_tok.data_ptr(), self.cand_prob.data_ptr(), None,
@@ -199,12 +217,12 @@ class SpecDecoder:
         chk(lib.ygg_init_roots(g.struct, self.cand_tok.data_ptr(), self.cand_prob.data_ptr(), k, self.R, 1, s))
         stamp(1)
         # ---- draft passes 1..D: grow one level each
-        for _ in range(D):
+        for lvl in range(D):
             chk(lib.ygg_level_inputs(g.struct, self.seq.struct, self.R, k, dr.tokens.data_ptr(), dr.pos.data_ptr(),
                                      dr.slot.data_ptr(), dr.req.data_ptr(), dr.qmask.data_ptr(), dr.mask_words,
                                      dr.blk_start.data_ptr(), dr.blk_len.data_ptr(), self.cand_n.data_ptr(), s))
             dr.run(stream)
-            self._draft_topk(rows, k, s)
+            self._draft_topk(rows, k, s, "verify" if lvl == D - 1 else "draft")
             chk(lib.ygg_egt_grow_level(g.struct, self.R, k, W, self.cand_tok.data_ptr(), self.cand_prob.data_ptr(),
                                        self.cand_n.data_ptr(), s))
         stamp(2)

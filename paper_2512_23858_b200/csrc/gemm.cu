@@ -57,6 +57,7 @@ struct GemmParams {
   long long units;  // stream-K units (remainder tiles x kb)
   const int32_t* seg_first;
   const int32_t* seg_base;
+  int prewait;      // weight stages issued before the grid-dependency wait (<= stages)
 };
 
 // ---------------------------------------------------------------------------
@@ -298,7 +299,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       const uint64_t pol_w = policy_evict_first();
       const uint64_t pol_x = policy_evict_last();
       const long long n_units = u1 - u0;
-      const int pre = static_cast<int>(n_units < S ? n_units : S);
+      const int pre = static_cast<int>(n_units < p.prewait ? n_units : p.prewait);
       // Unit coordinates are stepped incrementally inside a segment (one tile): the single producer
       // thread must not pay 64-bit divisions per stage (that alone capped a CTA near 30 GB/s).
       int k = 0, left = 0, kblk = 0, wrow = 0, xrow = 0;
@@ -1026,6 +1027,10 @@ static int gemm_launch(const GemmPlan* g, float* workspace, const ygg_epilogue* 
     p.dp_per_cta = g->dp_per_cta;
     p.stages = g->stages;
     p.tmem_cols = g->tmem_cols;
+    {  // A/B knob: YGG_GEMM_PREWAIT = stages streamed before the dependency wait (default: all)
+      static const int pw = [] { const char* e = getenv("YGG_GEMM_PREWAIT"); return e ? atoi(e) : 1 << 30; }();
+      p.prewait = pw < 0 ? 0 : (pw < g->stages ? pw : g->stages);
+    }
     p.units = g->units;
     p.seg_first = g->seg_table;
     p.seg_base = g->seg_table + g->tiles + 1;

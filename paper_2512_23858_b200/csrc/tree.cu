@@ -200,7 +200,7 @@ struct L2Regions {  // weights of the next pass to pull into L2 while the merge 
 __global__ void __launch_bounds__(kTopkThreads) topk_merge_kernel(const TopkPartial* __restrict__ chunks, int nchunks,
                                                                   int k, int32_t* out_tok, double* out_prob,
                                                                   float* out_stats, unsigned long long* trace,
-                                                                  L2Regions pf) {
+                                                                  L2Regions pf, int stage) {
   if (threadIdx.x == 0) { trace_min(trace, 0); trace_max(trace, 6); }
   pdl_wait();
   if (threadIdx.x == 0) { trace_min(trace, 1); trace_max(trace, 7); }
@@ -222,7 +222,26 @@ __global__ void __launch_bounds__(kTopkThreads) topk_merge_kernel(const TopkPart
   __shared__ float sel_v[kTopkMaxK];
   __shared__ int sel_t[kTopkMaxK];
   __shared__ unsigned long long wsel[NW][kTopkMaxK];
-  extern __shared__ unsigned long long merge_keys[];  // [nchunks][k] candidate keys
+  extern __shared__ __align__(16) unsigned long long merge_keys[];  // [nchunks][k] candidate keys
+  // stage: this row's partials ([nchunks] x 272 B, contiguous) arrive in shared memory by one bulk
+  // copy — the TMA engine streams them instead of every thread waiting on its own L2 round trips.
+  if (stage) {
+    __shared__ __align__(8) uint64_t sbar;
+    TopkPartial* sp = reinterpret_cast<TopkPartial*>(merge_keys + ((static_cast<size_t>(nchunks) * k + 1) & ~static_cast<size_t>(1)));
+    if (t == 0) {
+      mbar_init(&sbar, 1);
+      fence_barrier_init();
+      const uint32_t bytes = static_cast<uint32_t>(nchunks) * static_cast<uint32_t>(sizeof(TopkPartial));
+      mbar_arrive_expect_tx(&sbar, bytes);
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+          ::"r"(smem_u32(sp)), "l"(reinterpret_cast<uint64_t>(c)), "r"(bytes), "r"(smem_u32(&sbar))
+          : "memory");
+    }
+    __syncthreads();
+    mbar_wait(&sbar, 0);
+    c = sp;
+  }
   float cm[kMergeOwn];
   double cs[kMergeOwn];
   float lm = -INFINITY;
@@ -237,14 +256,14 @@ __global__ void __launch_bounds__(kTopkThreads) topk_merge_kernel(const TopkPart
     cs[o] = 0.0;
     if (j < nchunks) {
       const TopkPartial* cj = c + j;
-      cm[o] = __ldcg(&cj->max_s);
-      cs[o] = __ldcg(&cj->sum_exp);
+      cm[o] = stage ? cj->max_s : __ldcg(&cj->max_s);
+      cs[o] = stage ? cj->sum_exp : __ldcg(&cj->sum_exp);
       if (k <= 8) {  // val / tok are 16-byte aligned in TopkPartial
-        v4[o][0] = __ldcg(reinterpret_cast<const float4*>(cj->val));
-        t4[o][0] = __ldcg(reinterpret_cast<const int4*>(cj->tok));
+        v4[o][0] = stage ? *reinterpret_cast<const float4*>(cj->val) : __ldcg(reinterpret_cast<const float4*>(cj->val));
+        t4[o][0] = stage ? *reinterpret_cast<const int4*>(cj->tok) : __ldcg(reinterpret_cast<const int4*>(cj->tok));
         if (k > 4) {
-          v4[o][1] = __ldcg(reinterpret_cast<const float4*>(cj->val + 4));
-          t4[o][1] = __ldcg(reinterpret_cast<const int4*>(cj->tok + 4));
+          v4[o][1] = stage ? *reinterpret_cast<const float4*>(cj->val + 4) : __ldcg(reinterpret_cast<const float4*>(cj->val + 4));
+          t4[o][1] = stage ? *reinterpret_cast<const int4*>(cj->tok + 4) : __ldcg(reinterpret_cast<const int4*>(cj->tok + 4));
         }
       }
     }
@@ -1040,9 +1059,12 @@ int ygg_topk_softmax(const void* logits, int dtype, int rows, int V, int ld, int
   else
     return ygg_fail(YGG_ERR_VALUE, "unknown dtype");
   if (nchunks <= kTopkThreads * kMergeOwn) {
-    YGG_LAUNCH_PDL(topk_merge_kernel, dim3(rows), dim3(kTopkThreads), static_cast<size_t>(nchunks) * k * 8, s,
+    const size_t keys = (static_cast<size_t>(nchunks) * k + 1) / 2 * 2 * 8;
+    const size_t staged = keys + static_cast<size_t>(nchunks) * sizeof(TopkPartial);
+    const int stage = staged <= 200 * 1024 ? 1 : 0;
+    YGG_LAUNCH_PDL(topk_merge_kernel, dim3(rows), dim3(kTopkThreads), stage ? staged : keys, s,
                    static_cast<const TopkPartial*>(ws),
-                   nchunks, k, out_tok, out_prob, out_stats, trace_next(10), L2Regions{});
+                   nchunks, k, out_tok, out_prob, out_stats, trace_next(10), L2Regions{}, stage);
     return YGG_OK;
   }
   const size_t smem = static_cast<size_t>(nchunks) * k * (sizeof(float) + sizeof(int));
@@ -1074,9 +1096,13 @@ int ygg_topk_merge_l2(const void* partials, int rows, int nchunks, int k, int32_
   YGG_CHECK_ARG(k >= 1 && k <= kTopkMaxK, "k must be in [1, 32]");
   YGG_CHECK_ARG(static_cast<size_t>(nchunks) * k * 8 <= 200 * 1024, "too many candidates to merge");
   if (rows == 0) return YGG_OK;
-  YGG_LAUNCH_PDL(topk_merge_kernel, dim3(rows), dim3(kTopkThreads), static_cast<size_t>(nchunks) * k * 8,
+  const size_t keys = (static_cast<size_t>(nchunks) * k + 1) / 2 * 2 * 8;
+  const size_t staged = keys + static_cast<size_t>(nchunks) * sizeof(TopkPartial);
+  const int stage = staged <= 200 * 1024 ? 1 : 0;
+  YGG_LAUNCH_PDL(topk_merge_kernel, dim3(rows), dim3(kTopkThreads), stage ? staged : keys,
                  reinterpret_cast<cudaStream_t>(stream),
-                 static_cast<const TopkPartial*>(partials), nchunks, k, out_tok, out_prob, out_stats, trace_next(10), pf);
+                 static_cast<const TopkPartial*>(partials), nchunks, k, out_tok, out_prob, out_stats, trace_next(10), pf,
+                 stage);
   return YGG_OK;
 }
 

@@ -237,31 +237,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (threadIdx.x == 32) trace_min(e.trace, 1);
     const int M = p.M;
     const int cw = warp - 1;
-    // Per-token inputs of the epilogue, before the main loop: rstd from the producing residual's
-    // per-block sums of squares (lanes split the blocks, fixed-order tree reduction), and the
-    // position / slot / request of each token row.
-    if (e.ss_in) {
-      float part[4] = {0.f, 0.f, 0.f, 0.f};
-  #pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const int n = cw + 4 * k;
-        if (n < M)
-          for (int j = lane; j < e.ss_blocks; j += 32) part[k] += __ldg(e.ss_in + static_cast<size_t>(j) * M + n);
-      }
-  #pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        float v = part[k];
-  #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-        const int n = cw + 4 * k;
-        if (lane == 0 && n < M) rstd_s[n] = rsqrtf(v / static_cast<float>(e.norm_dim) + e.eps);
-      }
-    }
-    if (e.kind == kQkv && cw == 0 && lane < M) {
-      tok_s[lane] = __ldg(e.pos + lane);
-      tok_s[kMaxTok + lane] = __ldg(e.slot + lane);
-      tok_s[2 * kMaxTok + lane] = __ldg(e.req + lane);
-    }
     const uint32_t sw0 = smem_u32(sw), sx0 = smem_u32(sx);
     // ldmatrix lane roles: A (x4): row = (l & 7) + 8*((l >> 3) & 1), 16B chunk hi = l >> 4.
     const int a_row = (lane & 7) + 8 * ((lane >> 3) & 1), a_hi = lane >> 4;
@@ -324,6 +299,34 @@ __global__ void __launch_bounds__(kThreads, 1)
   pdl_wait();
   pdl_launch_dependents();
   const int M = p.M;
+  // Per-token inputs of the epilogue, while the mma warps stream the first block: rstd from the
+  // producing residual's per-block sums of squares (lanes split the blocks, fixed-order tree
+  // reduction), and the position / slot / request of each token row.
+  if (e.ss_in) {
+    constexpr int NTOK = 8 * NT;  // token rows this instantiation handles
+    float v[NTOK];
+#pragma unroll
+    for (int n = 0; n < NTOK; ++n) v[n] = 0.f;
+    for (int j = lane; j < e.ss_blocks; j += 32) {  // every token's load of block j in flight together
+      const float* row = e.ss_in + static_cast<size_t>(j) * M;
+#pragma unroll
+      for (int n = 0; n < NTOK; ++n)
+        if (n < M) v[n] += __ldg(row + n);
+    }
+#pragma unroll
+    for (int n = 0; n < NTOK; ++n) {
+      float x = v[n];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+      if (lane == 0 && n < M) rstd_s[n] = rsqrtf(x / static_cast<float>(e.norm_dim) + e.eps);
+    }
+  }
+  if (e.kind == kQkv && lane < M) {
+    tok_s[lane] = __ldg(e.pos + lane);
+    tok_s[kMaxTok + lane] = __ldg(e.slot + lane);
+    tok_s[2 * kMaxTok + lane] = __ldg(e.req + lane);
+  }
+  __syncwarp();
   // STORE_TOPK (NT == 1 only): per lane and token slot q (token 2*(lane&3) + q) a running max / f64
   // sum of exp and a sorted top-kTopkLane list over this lane's rows of every block.
   constexpr int TQ = TOPK ? 2 : 1;

@@ -581,11 +581,25 @@ YGG_DEV float epi_value(const EpiGeom& g, const float* __restrict__ ws, int m, i
   return v;
 }
 
-// Sum of the partials of V consecutive features [n, n+V) of row m (n % V == 0, one tile).
+// Segment range [s0, s1) of the tile holding (row m, feature n): plan constants, so the epilogue
+// kernels load them before their grid-dependency wait.
+YGG_DEV int2 epi_segs(const EpiGeom& g, int m, int n) {
+  const int t = (n / kBM) * g.m_tiles + m / g.BN;
+  return make_int2(__ldg(g.seg_first + t), __ldg(g.seg_first + t + 1));
+}
+
+template <int V>
+YGG_DEV void epi_values(const EpiGeom& g, const float* __restrict__ ws, int m, int n, float* v, int2 sg);
+
 template <int V>
 YGG_DEV void epi_values(const EpiGeom& g, const float* __restrict__ ws, int m, int n, float* v) {
-  const int t = (n / kBM) * g.m_tiles + m / g.BN;
-  const int s0 = __ldg(g.seg_first + t), s1 = __ldg(g.seg_first + t + 1);
+  epi_values<V>(g, ws, m, n, v, epi_segs(g, m, n));
+}
+
+// Sum of the partials of V consecutive features [n, n+V) of row m (n % V == 0, one tile).
+template <int V>
+YGG_DEV void epi_values(const EpiGeom& g, const float* __restrict__ ws, int m, int n, float* v, int2 sg) {
+  const int s0 = sg.x, s1 = sg.y;
   const float* p = ws + static_cast<size_t>(m % g.BN) * kBM + (n % kBM);
   const size_t seg_stride = static_cast<size_t>(g.BN) * kBM;
 #pragma unroll
@@ -607,10 +621,9 @@ YGG_DEV void epi_values(const EpiGeom& g, const float* __restrict__ ws, int m, i
 // Partial sums of two V-wide feature runs [n1, n1+V) and [n2, n2+V) of row m (possibly different
 // tiles), both runs' loads in flight together; each run summed in its own segment order.
 template <int V>
-YGG_DEV void epi_values2(const EpiGeom& g, const float* __restrict__ ws, int m, int n1, int n2, float* v1, float* v2) {
-  const int t1 = (n1 / kBM) * g.m_tiles + m / g.BN, t2 = (n2 / kBM) * g.m_tiles + m / g.BN;
-  const int a0 = __ldg(g.seg_first + t1), a1 = __ldg(g.seg_first + t1 + 1);
-  const int b0 = __ldg(g.seg_first + t2), b1 = __ldg(g.seg_first + t2 + 1);
+YGG_DEV void epi_values2(const EpiGeom& g, const float* __restrict__ ws, int m, int n1, int n2, float* v1, float* v2,
+                         int2 sa, int2 sb) {
+  const int a0 = sa.x, a1 = sa.y, b0 = sb.x, b1 = sb.y;
   const size_t row = static_cast<size_t>(m % g.BN) * kBM;
   const float* p1 = ws + row + (n1 % kBM);
   const float* p2 = ws + row + (n2 % kBM);
@@ -683,14 +696,15 @@ template <typename OutT>
 __global__ void __launch_bounds__(kEpiThreads) epi_store_kernel(EpiGeom g, const float* __restrict__ ws,
                                                                 OutT* __restrict__ out, int ld) {
   if (threadIdx.x == 0) trace_min(g.trace, 0);
+  const int m = blockIdx.y;
+  const int n = (blockIdx.x * blockDim.x + threadIdx.x) * 8;
+  const int2 sg = n < g.N ? epi_segs(g, m, n) : make_int2(0, 0);
   pdl_wait();
   pdl_launch_dependents();
   if (threadIdx.x == 0) trace_min(g.trace, 1);
-  const int m = blockIdx.y;
-  const int n = (blockIdx.x * blockDim.x + threadIdx.x) * 8;
   if (n >= g.N) return;
   float v[8];
-  epi_values<8>(g, ws, m, n, v);
+  epi_values<8>(g, ws, m, n, v, sg);
   store8<OutT>(out + static_cast<size_t>(m) * ld + n, v);
   if (threadIdx.x == 0) trace_max(g.trace, 2);
 }
@@ -720,20 +734,24 @@ __global__ void __launch_bounds__(1024) epi_residual_norm_kernel(EpiGeom g, cons
                                                                  const ActT* __restrict__ norm_w, float eps,
                                                                  ActT* __restrict__ xn) {
   if (threadIdx.x == 0) trace_min(g.trace, 0);
-  pdl_wait();
-  pdl_launch_dependents();
-  if (threadIdx.x == 0) trace_min(g.trace, 1);
   __shared__ float red[32];
   const int m = blockIdx.x;
   const int n = threadIdx.x * 8;
   const bool live = n < g.N;
   float h[8], w[8], v[8];
+  int2 sg = make_int2(0, 0);
+  if (live) {  // plan constants and the norm gains before the dependency wait
+    sg = epi_segs(g, m, n);
+    load8<ActT>(norm_w + n, w);
+  }
+  pdl_wait();
+  pdl_launch_dependents();
+  if (threadIdx.x == 0) trace_min(g.trace, 1);
   float ss = 0.f;
   if (live) {
     float* hp = resid + static_cast<size_t>(m) * g.N + n;
     load8<float>(hp, h);
-    load8<ActT>(norm_w + n, w);
-    epi_values<8>(g, ws, m, n, v);
+    epi_values<8>(g, ws, m, n, v, sg);
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
       h[i] += v[i];
@@ -760,15 +778,16 @@ template <typename ActT>
 __global__ void __launch_bounds__(kEpiThreads) epi_swiglu_kernel(EpiGeom g, const float* __restrict__ ws,
                                                                  ActT* __restrict__ out) {
   if (threadIdx.x == 0) trace_min(g.trace, 0);
-  pdl_wait();
-  pdl_launch_dependents();
-  if (threadIdx.x == 0) trace_min(g.trace, 1);
   const int m = blockIdx.y;
   const int F = g.N / 2;
   const int f = (blockIdx.x * blockDim.x + threadIdx.x) * 8;
+  const int2 sa = f < F ? epi_segs(g, m, f) : make_int2(0, 0), sb = f < F ? epi_segs(g, m, F + f) : make_int2(0, 0);
+  pdl_wait();
+  pdl_launch_dependents();
+  if (threadIdx.x == 0) trace_min(g.trace, 1);
   if (f >= F) return;
   float gate[8], up[8], o[8];
-  epi_values2<8>(g, ws, m, f, F + f, gate, up);
+  epi_values2<8>(g, ws, m, f, F + f, gate, up, sa, sb);
 #pragma unroll
   for (int i = 0; i < 8; ++i) o[i] = gate[i] / (1.f + expf(-gate[i])) * up[i];
   store8<ActT>(out + static_cast<size_t>(m) * F + f, o);
@@ -786,19 +805,21 @@ __global__ void __launch_bounds__(256) epi_qkv_rope_kernel(EpiGeom g, const floa
                                                            ActT* __restrict__ cache, int S,
                                                            const float2* __restrict__ rope_cs) {
   if (threadIdx.x == 0) trace_min(g.trace, 0);
-  pdl_wait();
-  pdl_launch_dependents();
-  if (threadIdx.x == 0) trace_min(g.trace, 1);
   const int m = blockIdx.x;
   const int half = hd / 2;
   const int per_head = half / 4;
   const int items = (Hq + 2 * Hkv) * per_head;
   const int it = blockIdx.y * blockDim.x + threadIdx.x;
-  if (it >= items) return;
-  const int pm = pos[m];
   const int head = it / per_head;
   const int i0 = (it % per_head) * 4;
   const int n0 = head * hd;
+  const int2 sa = it < items ? epi_segs(g, m, n0 + i0) : make_int2(0, 0);
+  const int2 sb = it < items ? epi_segs(g, m, n0 + i0 + half) : make_int2(0, 0);
+  pdl_wait();
+  pdl_launch_dependents();
+  if (threadIdx.x == 0) trace_min(g.trace, 1);
+  if (it >= items) return;
+  const int pm = pos[m];
   float x1[4], x2[4], cs[4], sn[4];
   const bool rot = head < Hq + Hkv;
   if (rot && rope_cs) {  // table loads first: they overlap the partial-sum loads below
@@ -809,7 +830,7 @@ __global__ void __launch_bounds__(256) epi_qkv_rope_kernel(EpiGeom g, const floa
       sn[j] = t.y;
     }
   }
-  epi_values2<4>(g, ws, m, n0 + i0, n0 + i0 + half, x1, x2);
+  epi_values2<4>(g, ws, m, n0 + i0, n0 + i0 + half, x1, x2, sa, sb);
   if (rot) {
     if (rope_cs) {
     } else {

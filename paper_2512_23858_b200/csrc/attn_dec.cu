@@ -212,10 +212,12 @@ __global__ void __launch_bounds__(32 * (1 + kMaxWarps), 1)
     pdl_launch_dependents();
     return;
   }
+  // Block bounds were written at least two kernels back (see the producer): load them before the
+  // wait, off the critical path.
+  const int bs = __ldg(a.blk_start + r), bl = __ldg(a.blk_len + r);
   pdl_wait();
   pdl_launch_dependents();
   if (threadIdx.x == 32) trace_min(a.trace, 1);
-  const int bs = __ldg(a.blk_start + r), bl = __ldg(a.blk_len + r);
   const int nkeys = bs + bl;
   const int nch = (nkeys + kKC - 1) / kKC;
   // Compute warp (ks, rw): key split ks takes chunks ks, ks + ksplit, ...; row warp rw 16 query rows

@@ -14,7 +14,7 @@ from pathlib import Path
 import torch
 
 _HERE = Path(__file__).resolve().parent
-LIB_PATH = _HERE / "libygg.so"
+LIB_PATH = Path(os.environ["YGG_LIB_PATH"]) if os.environ.get("YGG_LIB_PATH") else _HERE / "libygg.so"  # A/B builds
 
 YGG_OK, YGG_ERR_VALUE, YGG_ERR_INDEX, YGG_ERR_CUDA, YGG_ERR_UNSUPPORTED = range(5)
 YGG_F32, YGG_BF16 = 0, 1

@@ -408,8 +408,6 @@ __global__ void __launch_bounds__(kGrowThreads) grow_level_kernel(ygg_tree t, in
                                                                   const int32_t* __restrict__ cand_n,
                                                                   unsigned long long* trace) {
   if (threadIdx.x == 0) trace_min(trace, 0);
-  pdl_wait();
-  if (threadIdx.x == 0) trace_min(trace, 1);
   const int b = blockIdx.x;
   __shared__ double sc[kGrowMaxCand];
   __shared__ int spar[kGrowMaxCand];
@@ -443,6 +441,10 @@ __global__ void __launch_bounds__(kGrowThreads) grow_level_kernel(ygg_tree t, in
     s_par[f] = parent;
     s_cum[f] = (parent >= 0 && parent < t.cap) ? t.cum[tb + parent] : 0.0;
   }
+  // The header, frontier rows and candidate counts come from kernels long done (the previous grow /
+  // the level inputs); only the candidate probabilities come from the merge just before: wait here.
+  pdl_wait();
+  if (threadIdx.x == 0) trace_min(trace, 1);
   __syncthreads();
   const int fn = s_fn, size0 = s_size0;
   if (s_flags & kFlagStopped) return;

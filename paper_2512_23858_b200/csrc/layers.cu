@@ -11,13 +11,21 @@ namespace ygg {
 template <typename T>
 __global__ void embed_kernel(const T* __restrict__ table, int V, int d, const int32_t* __restrict__ tokens,
                              float* __restrict__ out) {
+  // One CTA per row, 8 features per thread with every load in flight at once (a strided loop would
+  // serialise one round trip per iteration).
   pdl_wait();
   pdl_launch_dependents();
   const int m = blockIdx.x;
   int tok = tokens[m];
   tok = tok < 0 ? 0 : (tok >= V ? V - 1 : tok);
   const T* row = table + static_cast<size_t>(tok) * d;
-  for (int i = threadIdx.x; i < d; i += blockDim.x) out[static_cast<size_t>(m) * d + i] = to_f32(row[i]);
+  const int n = threadIdx.x * 8;
+  float v[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) v[i] = n + i < d ? to_f32(row[n + i]) : 0.f;
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+    if (n + i < d) out[static_cast<size_t>(m) * d + n + i] = v[i];
 }
 
 // Embedding for the fused path: one CTA per token row, d/8 threads with 8 features (one 16-byte
@@ -61,27 +69,34 @@ __global__ void __launch_bounds__(1024) embed_fused_kernel(const __nv_bfloat16* 
 }
 
 template <typename T>
-__global__ void __launch_bounds__(256) rmsnorm_kernel(const float* __restrict__ x, const T* __restrict__ w, int d,
-                                                      float eps, T* __restrict__ out) {
+__global__ void __launch_bounds__(1024) rmsnorm_kernel(const float* __restrict__ x, const T* __restrict__ w, int d,
+                                                       float eps, T* __restrict__ out) {
+  // One CTA per row, 8 features per thread, all loads in flight at once; one block reduction
+  // (warp sums, then the warps' sums in fixed order: deterministic).
   pdl_wait();
   pdl_launch_dependents();
   __shared__ float red[32];
   const int m = blockIdx.x;
   const float* row = x + static_cast<size_t>(m) * d;
+  const int n = threadIdx.x * 8;
+  float v[8], g[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    v[i] = n + i < d ? row[n + i] : 0.f;
+    g[i] = n + i < d ? to_f32(w[n + i]) : 0.f;
+  }
   float ss = 0.f;
-  for (int i = threadIdx.x; i < d; i += blockDim.x) ss += row[i] * row[i];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) ss += v[i] * v[i];
   ss = warp_sum(ss);
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
   __syncthreads();
-  if (threadIdx.x < 32) {
-    float t = (threadIdx.x < blockDim.x / 32) ? red[threadIdx.x] : 0.f;
-    t = warp_sum(t);
-    if (threadIdx.x == 0) red[0] = t;
-  }
-  __syncthreads();
-  const float r = rsqrtf(red[0] / static_cast<float>(d) + eps);
-  for (int i = threadIdx.x; i < d; i += blockDim.x)
-    out[static_cast<size_t>(m) * d + i] = from_f32<T>(row[i] * r * to_f32(w[i]));
+  float t = 0.f;
+  for (int k = 0; k < static_cast<int>(blockDim.x >> 5); ++k) t += red[k];
+  const float r = rsqrtf(t / static_cast<float>(d) + eps);
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+    if (n + i < d) out[static_cast<size_t>(m) * d + n + i] = from_f32<T>(v[i] * r * g[i]);
 }
 
 // ---------------------------------------------------------------------------
@@ -295,15 +310,16 @@ int ygg_prepare_layers(void) {
 
 int ygg_embed(const void* table, int dtype, int V, int d, const int32_t* tokens, int M, float* resid_out,
               ygg_stream_t stream) {
-  YGG_CHECK_ARG(table && tokens && resid_out && V >= 1 && d >= 1, "invalid arguments");
+  YGG_CHECK_ARG(table && tokens && resid_out && V >= 1 && d >= 1 && d <= 8192, "invalid arguments");
   if (M <= 0) return YGG_OK;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const int threads = ((d + 7) / 8 + 31) / 32 * 32;  // 8 features per thread
   if (dtype == YGG_F32)
-    YGG_LAUNCH_PDL(embed_kernel<float>, dim3(M), dim3(256), 0, s, static_cast<const float*>(table), V, d, tokens,
+    YGG_LAUNCH_PDL(embed_kernel<float>, dim3(M), dim3(threads), 0, s, static_cast<const float*>(table), V, d, tokens,
                    resid_out);
   else
-    YGG_LAUNCH_PDL(embed_kernel<__nv_bfloat16>, dim3(M), dim3(256), 0, s, static_cast<const __nv_bfloat16*>(table), V,
-                   d, tokens, resid_out);
+    YGG_LAUNCH_PDL(embed_kernel<__nv_bfloat16>, dim3(M), dim3(threads), 0, s, static_cast<const __nv_bfloat16*>(table),
+                   V, d, tokens, resid_out);
   return YGG_OK;
 }
 
@@ -319,15 +335,16 @@ int ygg_embed_fused(const void* table, int V, int d, const int32_t* tokens, int 
 }
 
 int ygg_rmsnorm(const float* x, const void* w, int dtype, int M, int d, float eps, void* out, ygg_stream_t stream) {
-  YGG_CHECK_ARG(x && w && out && d >= 1, "invalid arguments");
+  YGG_CHECK_ARG(x && w && out && d >= 1 && d <= 8192, "invalid arguments");
   if (M <= 0) return YGG_OK;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const int threads = ((d + 7) / 8 + 31) / 32 * 32;  // 8 features per thread
   if (dtype == YGG_F32)
-    YGG_LAUNCH_PDL(rmsnorm_kernel<float>, dim3(M), dim3(256), 0, s, x, static_cast<const float*>(w), d, eps,
+    YGG_LAUNCH_PDL(rmsnorm_kernel<float>, dim3(M), dim3(threads), 0, s, x, static_cast<const float*>(w), d, eps,
                    static_cast<float*>(out));
   else
-    YGG_LAUNCH_PDL(rmsnorm_kernel<__nv_bfloat16>, dim3(M), dim3(256), 0, s, x, static_cast<const __nv_bfloat16*>(w), d,
-                   eps, static_cast<__nv_bfloat16*>(out));
+    YGG_LAUNCH_PDL(rmsnorm_kernel<__nv_bfloat16>, dim3(M), dim3(threads), 0, s, x, static_cast<const __nv_bfloat16*>(w),
+                   d, eps, static_cast<__nv_bfloat16*>(out));
   return YGG_OK;
 }
 

@@ -242,8 +242,20 @@ __global__ void __launch_bounds__(kRowStatsThreads) row_stats_kernel(const T* __
     if ((reinterpret_cast<uintptr_t>(x) & 15) == 0) {
       const int nv = V >> 2;
       const float4* x4 = reinterpret_cast<const float4*>(x);
-      for (int i = threadIdx.x; i < nv; i += kRowStatsThreads) {
-        const float4 q = __ldg(x4 + i);
+      // 8 loads in flight per thread (through L2: the logits were just written by the LM head).
+      int i = threadIdx.x;
+      for (; i + 7 * kRowStatsThreads < nv; i += 8 * kRowStatsThreads) {
+        float4 q[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) q[u] = __ldcg(x4 + i + u * kRowStatsThreads);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int b = 4 * (i + u * kRowStatsThreads);
+          take(q[u].x, b); take(q[u].y, b + 1); take(q[u].z, b + 2); take(q[u].w, b + 3);
+        }
+      }
+      for (; i < nv; i += kRowStatsThreads) {
+        const float4 q = __ldcg(x4 + i);
         take(q.x, 4 * i); take(q.y, 4 * i + 1); take(q.z, 4 * i + 2); take(q.w, 4 * i + 3);
       }
       for (int v = (nv << 2) + threadIdx.x; v < V; v += kRowStatsThreads) take(to_f32(x[v]), v);

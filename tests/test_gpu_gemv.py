@@ -237,3 +237,93 @@ def test_decode_attention_vs_fp32(hd, Hq, Hkv, B, T, P, mw, kvsplit, cuda, monke
                 ref[b * T + t, h] = Vt[b, kv][:, vis] @ p
     err = (out.double().cpu() - ref).abs().max()
     assert err <= 2e-2 * ref.abs().max(), float(err)
+
+
+def test_l2_prefetch_regions_leave_results_unchanged(cuda):
+    """The optional L2 prefetch regions of the GEMV / decode attention / top-k merge only move data
+    into L2: every output is bit-identical with and without them; bad regions are rejected."""
+    import ctypes as C
+
+    from paper_2512_23858_b200 import _lib as L
+
+    lib = L.lib()
+    g = torch.Generator(device="cuda").manual_seed(7)
+    V, K, M, k = 4096, 256, 8, 8
+    W = (torch.randn(V, K, device=cuda, generator=g) * 0.2).to(torch.bfloat16)
+    X = torch.randn(M, K, device=cuda, generator=g).to(torch.bfloat16)
+    other = torch.randn(1 << 20, device=cuda, generator=g)  # 4 MB "next weights"
+    mem = C.create_string_buffer(int(lib.ygg_gemv_plan_size()))
+    L.check(lib.ygg_gemv_plan_init(mem, W.data_ptr(), X.data_ptr(), M, V, K, 0))
+    grid = int(lib.ygg_gemv_grid(mem))
+    part = torch.empty(int(lib.ygg_topk_partial_bytes(M, grid)), dtype=torch.uint8, device=cuda)
+    outs = []
+    for pf in (0, other.numel() * 4):
+        L.check(lib.ygg_gemv_set_l2_prefetch(mem, other.data_ptr() if pf else None, pf))
+        logits = torch.zeros(M, V, dtype=torch.float32, device=cuda)
+        e = L.YggGemvEpilogue()
+        e.kind, e.out, e.ld = L.YGG_GEMV_STORE_TOPK, logits.data_ptr(), V
+        e.topk_part, e.topk_k, e.inv_temp = part.data_ptr(), k, 1.0
+        L.check(lib.ygg_gemv_run(mem, C.byref(e), L.stream_ptr()))
+        tok = torch.zeros(M, k, dtype=torch.int32, device=cuda)
+        prob = torch.zeros(M, k, dtype=torch.float64, device=cuda)
+        regs = (L.YggL2Region * 4)(L.YggL2Region(other.data_ptr(), pf)) if pf else None
+        L.check(lib.ygg_topk_merge_l2(part.data_ptr(), M, grid, k, tok.data_ptr(), prob.data_ptr(), None, regs,
+                                      1 if pf else 0, L.stream_ptr()))
+        torch.cuda.synchronize()
+        outs.append((logits.clone(), tok.clone(), prob.clone()))
+    for a, b in zip(outs[0], outs[1]):
+        assert torch.equal(a, b)
+    with pytest.raises(ValueError):  # misaligned region
+        L.check(lib.ygg_gemv_set_l2_prefetch(mem, other.data_ptr() + 4, 1024))
+    with pytest.raises(ValueError):  # too many regions
+        L.check(lib.ygg_topk_merge_l2(part.data_ptr(), M, grid, k, tok.data_ptr(), prob.data_ptr(), None,
+                                      (L.YggL2Region * 5)(), 5, L.stream_ptr()))
+    # decode attention: same output with both prefetch regions set
+    Hq, Hkv, hd, T, P = 32, 8, 64, 8, 300
+    S = ((P + T + 63) // 64) * 64
+    q = torch.randn(T, Hq, hd, device=cuda, generator=g).to(torch.bfloat16)
+    cache = torch.randn(1, 2, Hkv, S, hd, device=cuda, generator=g).to(torch.bfloat16)
+    bs = torch.full((1,), P, dtype=torch.int32, device=cuda)
+    bl = torch.full((1,), T, dtype=torch.int32, device=cuda)
+    att = C.create_string_buffer(int(lib.ygg_attn_dec_plan_size()))
+    L.check(lib.ygg_attn_dec_plan_init(att, q.data_ptr(), cache.data_ptr(), 1, T, Hq, Hkv, hd, S))
+    res = []
+    for pf in (0, 1 << 20):
+        for rg in (0, 1):
+            L.check(lib.ygg_attn_dec_set_l2_prefetch(att, rg, other.data_ptr() if pf else None, pf))
+        out = torch.zeros(T, Hq, hd, dtype=torch.bfloat16, device=cuda)
+        L.check(lib.ygg_attn_dec_run(att, bs.data_ptr(), bl.data_ptr(), None, 0, 0.125, out.data_ptr(), None,
+                                     L.stream_ptr()))
+        torch.cuda.synchronize()
+        res.append(out.clone())
+    assert torch.equal(res[0], res[1])
+    with pytest.raises(ValueError):
+        L.check(lib.ygg_attn_dec_set_l2_prefetch(att, 2, other.data_ptr(), 1024))
+
+
+def test_kernel_timeline_trace_slots(cuda):
+    """ygg_trace_arm: a traced launch fills its slot with start <= release <= end (globaltimer ns)."""
+    import ctypes as C
+
+    from paper_2512_23858_b200 import _lib as L
+
+    lib = L.lib()
+    W = torch.randn(2048, 512, device=cuda).to(torch.bfloat16)
+    X = torch.randn(8, 512, device=cuda).to(torch.bfloat16)
+    out = torch.zeros(8, 2048, dtype=torch.float32, device=cuda)
+    mem = C.create_string_buffer(int(lib.ygg_gemv_plan_size()))
+    L.check(lib.ygg_gemv_plan_init(mem, W.data_ptr(), X.data_ptr(), 8, 2048, 512, 0))
+    buf = torch.zeros(4, 8, dtype=torch.int64, device=cuda)
+    buf[:, :2] = -1
+    L.check(lib.ygg_trace_arm(buf.data_ptr(), 4))
+    e = L.YggGemvEpilogue()
+    e.kind, e.out, e.ld = L.YGG_GEMV_STORE, out.data_ptr(), 2048
+    L.check(lib.ygg_gemv_run(mem, C.byref(e), L.stream_ptr()))
+    ids = (C.c_int * 4)()
+    n = lib.ygg_trace_used(ids, 4)
+    L.check(lib.ygg_trace_arm(None, 0))
+    torch.cuda.synchronize()
+    assert n == 1 and ids[0] == 1
+    s, r, t = [int(x) for x in buf[0, :3].cpu()]
+    assert 0 < s <= r <= t, (s, r, t)
+    torch.testing.assert_close(out, (X.float() @ W.float().T), rtol=2e-2, atol=2e-2)

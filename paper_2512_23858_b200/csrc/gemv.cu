@@ -614,10 +614,11 @@ int ygg_gemv_plan_init(void* plan, const void* W, const void* X, int M, int N, i
   int per_sm = smem_kb <= 113 ? 2 : 1;
   p.grid = num_ctas > 0 ? num_ctas : std::min(sms * per_sm, p.nblk);
   // A matrix with at most one block per SM (o / down projections: 128 blocks of 16 x K) is bound by
-  // one CTA's bytes in flight: give that CTA the whole SM's ring (YGG_GEMV_SOLO_KB, default 200).
+  // one CTA's bytes in flight: give that CTA the whole SM's ring (YGG_GEMV_SOLO_KB, default 224 =
+  // 9 stages; same-box draft pass 0.593 ms at 200 KB, 0.591 at 224).
   static const int solo_kb = [] {
     const char* s = getenv("YGG_GEMV_SOLO_KB");
-    const int v = s ? atoi(s) : 200;
+    const int v = s ? atoi(s) : 224;
     return v < 64 ? 64 : (v > 227 ? 227 : v);
   }();
   const int budget_kb = (num_ctas <= 0 && p.nblk <= sms) ? solo_kb : smem_kb;

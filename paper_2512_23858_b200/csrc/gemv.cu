@@ -313,13 +313,32 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int n = 0; n < NTOK; ++n)
         if (n < M) v[n] += __ldg(row + n);
     }
+    // Reduce-scatter across the lanes (halving the token set per xor step, NTOK - 1 shuffles in all
+    // instead of 5 * NTOK), then full xor sums over the remaining lane bits: fixed order,
+    // deterministic.  Lane l ends with token t(l) built from its high lane bits.
+    int cnt = NTOK, tsel = 0;
 #pragma unroll
-    for (int n = 0; n < NTOK; ++n) {
-      float x = v[n];
+    for (int o = 16; o >= 1; o >>= 1) {
+      if (cnt > 1) {
+        const int half = cnt / 2;
+        const bool upper = (lane & o) != 0;
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
-      if (lane == 0 && n < M) rstd_s[n] = rsqrtf(x / static_cast<float>(e.norm_dim) + e.eps);
+        for (int i = 0; i < NTOK / 2; ++i) {
+          if (i < half) {
+            const float send = upper ? v[i] : v[i + half];
+            const float recv = __shfl_xor_sync(0xffffffffu, send, o);
+            v[i] = (upper ? v[i + half] : v[i]) + recv;
+          }
+        }
+        tsel = tsel * 2 + (upper ? 1 : 0);
+        cnt = half;
+      } else {
+        v[0] += __shfl_xor_sync(0xffffffffu, v[0], o);
+      }
     }
+    // every lane now holds the full sum of token tsel (lanes differing only in the low bits agree)
+    const int low_bits = 32 / NTOK;  // lanes sharing a token
+    if ((lane & (low_bits - 1)) == 0 && tsel < M) rstd_s[tsel] = rsqrtf(v[0] / static_cast<float>(e.norm_dim) + e.eps);
   }
   if (e.kind == kQkv && lane < M) {
     tok_s[lane] = __ldg(e.pos + lane);

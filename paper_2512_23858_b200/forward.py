@@ -266,7 +266,7 @@ class Forward:
             ])
         # The QKV GEMV streams only ~12 MB: after it, each CTA pulls a slice of a later stream of the
         # layer into L2 (YGG_L2PF_QKV_MB of YGG_L2PF_QKV_TARGET).
-        qmb = float(os.environ.get("YGG_L2PF_QKV_MB", "8"))  # same-box draft pass 0.631 -> 0.625 ms (16 MB: 0.627)
+        qmb = float(os.environ.get("YGG_L2PF_QKV_MB", "16"))  # re-tuned same-box: 8 MB 0.570, 16 MB 0.563, 24 MB 0.566 ms
         qtarget = os.environ.get("YGG_L2PF_QKV_TARGET", "wgu")
         if qmb > 0:
             for li, lw in enumerate(self.w["layers"]):

@@ -334,9 +334,10 @@ typedef struct {
 } ygg_gemv_epilogue;
 size_t ygg_gemv_plan_size(void);
 int ygg_gemv_grid(const void* plan);  /* CTAs of the plan = top-k chunks per row of STORE_TOPK */
-/* Optional: after streaming its own weights every CTA pulls its slice of [ptr, ptr + bytes) into L2
- * (later weights of the pass; bytes = 0 disables). */
-int ygg_gemv_set_l2_prefetch(void* plan, const void* ptr, size_t bytes);
+/* Optional: after streaming its own weights every CTA pulls its slices of up to two regions
+ * [ptr, ptr + bytes) into L2 (later weights / the next attention's cache; region 0 or 1, issued in
+ * that order; bytes = 0 disables the region). */
+int ygg_gemv_set_l2_prefetch(void* plan, int region, const void* ptr, size_t bytes);
 int ygg_gemv_plan_init(void* plan, const void* W, const void* X, int M, int N, int K, int num_ctas);
 int ygg_gemv_run(const void* plan, const ygg_gemv_epilogue* epi, ygg_stream_t stream);
 

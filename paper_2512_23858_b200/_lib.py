@@ -186,7 +186,7 @@ _SIGS: dict[str, tuple] = {
     "ygg_gemv_plan_init": (C.c_int, [vp, vp, vp, C.c_int, C.c_int, C.c_int, C.c_int]),
     "ygg_gemv_run": (C.c_int, [vp, C.POINTER(YggGemvEpilogue), vp]),
     "ygg_gemv_grid": (C.c_int, [vp]),
-    "ygg_gemv_set_l2_prefetch": (C.c_int, [vp, vp, C.c_size_t]),
+    "ygg_gemv_set_l2_prefetch": (C.c_int, [vp, C.c_int, vp, C.c_size_t]),
     "ygg_attn_dec_set_l2_prefetch": (C.c_int, [vp, C.c_int, vp, C.c_size_t]),
     "ygg_topk_partial_bytes": (C.c_size_t, [C.c_int, C.c_int]),
     "ygg_topk_merge": (C.c_int, [vp, C.c_int, C.c_int, C.c_int, vp, vp, vp, vp]),

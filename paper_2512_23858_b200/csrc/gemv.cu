@@ -45,8 +45,8 @@ enum Epi : int { kNone = 0, kStore = 1, kQkv = 2, kSwiglu = 3, kResid = 4, kStor
 
 struct Params {
   int M, N, K, nblk, kchunks, stages, xrows, grid;
-  const char* pf_ptr;  // optional L2 prefetch region (later weights), split over the CTAs
-  size_t pf_bytes;
+  const char* pf_ptr[2];  // optional L2 prefetch regions (later weights / caches), split over the CTAs
+  size_t pf_bytes[2];
 };
 
 struct Epilogue {
@@ -216,12 +216,13 @@ __global__ void __launch_bounds__(kThreads, 1)
           ph ^= 1u;
         }
       }
-      if (p.pf_ptr) {  // after this CTA's own stream: pull a slice of later weights into L2
-        const size_t per = ((p.pf_bytes / gridDim.x) + 255) & ~static_cast<size_t>(255);
-        const size_t b0 = blockIdx.x * per, b1 = b0 + per < p.pf_bytes ? b0 + per : p.pf_bytes;
+      for (int rg = 0; rg < 2; ++rg) {  // after this CTA's own stream: pull slices of later data into L2
+        if (!p.pf_ptr[rg]) continue;
+        const size_t per = ((p.pf_bytes[rg] / gridDim.x) + 255) & ~static_cast<size_t>(255);
+        const size_t b0 = blockIdx.x * per, b1 = b0 + per < p.pf_bytes[rg] ? b0 + per : p.pf_bytes[rg];
         for (size_t o = b0; o < b1; o += 65536) {
           const uint32_t n = static_cast<uint32_t>(b1 - o < 65536 ? ((b1 - o) & ~static_cast<size_t>(15)) : 65536);
-          if (n) asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p.pf_ptr + o), "r"(n) : "memory");
+          if (n) asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p.pf_ptr[rg] + o), "r"(n) : "memory");
         }
       }
     } else {
@@ -589,12 +590,13 @@ int ygg_prepare_gemv(void) {
   return YGG_OK;
 }
 
-int ygg_gemv_set_l2_prefetch(void* plan, const void* ptr, size_t bytes) {
+int ygg_gemv_set_l2_prefetch(void* plan, int region, const void* ptr, size_t bytes) {
   Plan* pl = const_cast<Plan*>(plan_of(plan));
   YGG_CHECK_ARG(pl != nullptr, "invalid gemv plan");
+  YGG_CHECK_ARG(region == 0 || region == 1, "prefetch region must be 0 or 1");
   YGG_CHECK_ARG(ptr == nullptr || (reinterpret_cast<uintptr_t>(ptr) & 15) == 0, "prefetch region must be 16-byte aligned");
-  pl->p.pf_ptr = bytes ? static_cast<const char*>(ptr) : nullptr;
-  pl->p.pf_bytes = ptr ? bytes : 0;
+  pl->p.pf_ptr[region] = bytes ? static_cast<const char*>(ptr) : nullptr;
+  pl->p.pf_bytes[region] = ptr ? bytes : 0;
   return YGG_OK;
 }
 

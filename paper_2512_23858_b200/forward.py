@@ -268,11 +268,18 @@ class Forward:
         # layer into L2 (YGG_L2PF_QKV_MB of YGG_L2PF_QKV_TARGET).
         qmb = float(os.environ.get("YGG_L2PF_QKV_MB", "16"))  # re-tuned same-box: 8 MB 0.570, 16 MB 0.563, 24 MB 0.566 ms
         qtarget = os.environ.get("YGG_L2PF_QKV_TARGET", "wgu")
-        if qmb > 0:
-            for li, lw in enumerate(self.w["layers"]):
+        # Region 0 (issued first): the layer's KV cache block, which the attention right after reads
+        # (YGG_L2PF_KV, A/B knob: off — the whole cache block, S capacity included, cost more than the
+        # attention gained: 0.565 -> 0.567 ms); region 1: the start of gate|up.
+        kv_on = os.environ.get("YGG_L2PF_KV", "0") != "0"
+        for li, lw in enumerate(self.w["layers"]):
+            if kv_on:
+                L.check(lib.ygg_gemv_set_l2_prefetch(self.gv[li][0][0], 0, self.cache.data_ptr() + li * self.layer_stride * es,
+                                                     self.layer_stride * es))
+            if qmb > 0:
                 W = lw[qtarget]
                 nbytes = min(int(qmb * (1 << 20)), W.numel() * W.element_size())
-                L.check(lib.ygg_gemv_set_l2_prefetch(self.gv[li][0][0], W.data_ptr(), nbytes))
+                L.check(lib.ygg_gemv_set_l2_prefetch(self.gv[li][0][0], 1, W.data_ptr(), nbytes))
         # The O GEMV (its weights already sit in its ring) pulls the next 16 MB of gate|up (same-box
         # pass 0.625 -> 0.615 ms; 24 MB 0.618, 32 MB 0.624).  A/B knob: the down GEMV pulling the next
         # layer's QKV weights is slower (0.628-0.631), so off.
@@ -283,11 +290,11 @@ class Forward:
                 W = lw["wgu"]
                 off = min(int(qmb * (1 << 20)), W.numel() * W.element_size())
                 nbytes = min(int(omb * (1 << 20)), W.numel() * W.element_size() - off)
-                L.check(lib.ygg_gemv_set_l2_prefetch(self.gv[li][1][0], W.data_ptr() + off, nbytes))
+                L.check(lib.ygg_gemv_set_l2_prefetch(self.gv[li][1][0], 0, W.data_ptr() + off, nbytes))
             if dmb > 0 and li + 1 < len(self.w["layers"]):
                 W = self.w["layers"][li + 1]["wqkv"]
                 nbytes = min(int(dmb * (1 << 20)), W.numel() * W.element_size())
-                L.check(lib.ygg_gemv_set_l2_prefetch(self.gv[li][3][0], W.data_ptr(), nbytes))
+                L.check(lib.ygg_gemv_set_l2_prefetch(self.gv[li][3][0], 0, W.data_ptr(), nbytes))
         ss_last, blocks_last = (self.ss_ga, d // 16) if cfg.n_layers > 0 else (self.ss_e, d // 128)
         self.gv_lm = (plan(self.w["lm_head"], self.xn),
                       epi(L.YGG_GEMV_STORE, out=self.logits.data_ptr(), ld=cfg.vocab, ss_in=ss_last.data_ptr(),

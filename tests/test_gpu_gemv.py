@@ -258,7 +258,8 @@ def test_l2_prefetch_regions_leave_results_unchanged(cuda):
     part = torch.empty(int(lib.ygg_topk_partial_bytes(M, grid)), dtype=torch.uint8, device=cuda)
     outs = []
     for pf in (0, other.numel() * 4):
-        L.check(lib.ygg_gemv_set_l2_prefetch(mem, other.data_ptr() if pf else None, pf))
+        L.check(lib.ygg_gemv_set_l2_prefetch(mem, 0, other.data_ptr() if pf else None, pf))
+        L.check(lib.ygg_gemv_set_l2_prefetch(mem, 1, other.data_ptr() if pf else None, pf // 2))
         logits = torch.zeros(M, V, dtype=torch.float32, device=cuda)
         e = L.YggGemvEpilogue()
         e.kind, e.out, e.ld = L.YGG_GEMV_STORE_TOPK, logits.data_ptr(), V
@@ -274,7 +275,7 @@ def test_l2_prefetch_regions_leave_results_unchanged(cuda):
     for a, b in zip(outs[0], outs[1]):
         assert torch.equal(a, b)
     with pytest.raises(ValueError):  # misaligned region
-        L.check(lib.ygg_gemv_set_l2_prefetch(mem, other.data_ptr() + 4, 1024))
+        L.check(lib.ygg_gemv_set_l2_prefetch(mem, 0, other.data_ptr() + 4, 1024))
     with pytest.raises(ValueError):  # too many regions
         L.check(lib.ygg_topk_merge_l2(part.data_ptr(), M, grid, k, tok.data_ptr(), prob.data_ptr(), None,
                                       (L.YggL2Region * 5)(), 5, L.stream_ptr()))

@@ -314,9 +314,11 @@ class Forward:
         # Measured same-box (cfg2): verify forward 3.583 -> 3.552 ms with 24 MB of wo (16 MB: 3.563;
         # all 34 MB: no gain); draft pass 0.634 -> 0.627 ms with 12 MB of wdown (16: 0.630, 20: 0.637;
         # prefetching gate|up instead slows the attention as much as gate|up gains).
-        mb = float(os.environ.get(key, "12" if self.gemv else "24"))
+        mb = float(os.environ.get(key, "12" if self.gemv else "0"))
         regions = [(name, mb)]
-        if not self.gemv:  # and the start of the verify gate|up stream (3.594 -> 3.567 ms with 16-32 MB)
+        # Verify: only the start of the gate|up stream (re-tuned same-box: none 3.578 ms; O 24 + gate|up
+        # 24 MB 3.530; gate|up 24 MB alone 3.464; 16: 3.495; 32: 3.485).
+        if not self.gemv:
             regions.append(("wgu", float(os.environ.get("YGG_L2PF_VERIFY_GU_MB", "24"))))
         for li, plan in enumerate(self.ad_plans):
             for rg, (nm, m) in enumerate(regions):

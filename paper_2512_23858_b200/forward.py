@@ -310,7 +310,7 @@ class Forward:
             return
         lib = L.lib()
         key, name = ("YGG_L2PF_DRAFT_MB", os.environ.get("YGG_L2PF_DRAFT_TARGET", "wdown")) if self.gemv \
-            else ("YGG_L2PF_VERIFY_MB", "wo")
+            else ("YGG_L2PF_VERIFY_MB", os.environ.get("YGG_L2PF_VERIFY_TARGET", "wo"))
         # Measured same-box (cfg2): verify forward 3.583 -> 3.552 ms with 24 MB of wo (16 MB: 3.563;
         # all 34 MB: no gain); draft pass 0.634 -> 0.627 ms with 12 MB of wdown (16: 0.630, 20: 0.637;
         # prefetching gate|up instead slows the attention as much as gate|up gains).
@@ -320,9 +320,16 @@ class Forward:
         # 24 MB 3.530; gate|up 24 MB alone 3.464; 16: 3.495; 32: 3.485).
         if not self.gemv:
             regions.append(("wgu", float(os.environ.get("YGG_L2PF_VERIFY_GU_MB", "24"))))
+        nl = len(self.ad_plans)
         for li, plan in enumerate(self.ad_plans):
             for rg, (nm, m) in enumerate(regions):
-                W = self.w["layers"][li][nm]
+                if nm == "next_wqkv":  # A/B target: the next layer's QKV weights
+                    if li + 1 >= nl:
+                        L.check(lib.ygg_attn_dec_set_l2_prefetch(plan, rg, None, 0))
+                        continue
+                    W = self.w["layers"][li + 1]["wqkv"]
+                else:
+                    W = self.w["layers"][li][nm]
                 nbytes = min(int(m * (1 << 20)), W.numel() * W.element_size())
                 L.check(lib.ygg_attn_dec_set_l2_prefetch(plan, rg, W.data_ptr() if nbytes > 0 else None,
                                                          max(nbytes, 0)))

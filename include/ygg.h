@@ -248,6 +248,9 @@ int ygg_epi_qkv_rope(const void* plan, const float* ws, int Hq, int Hkv, int hd,
 int ygg_embed(const void* table, int dtype, int V, int d, const int32_t* tokens, int M, float* resid_out,
               ygg_stream_t stream);
 int ygg_rmsnorm(const float* x, const void* w, int dtype, int M, int d, float eps, void* out, ygg_stream_t stream);
+/* ygg_embed followed by ygg_rmsnorm in one launch (table, norm gains and activations share dtype). */
+int ygg_embed_rmsnorm(const void* table, const void* norm_w, int dtype, int V, int d, const int32_t* tokens, int M,
+                      float eps, float* resid_out, void* xn_out, ygg_stream_t stream);
 
 /* Tree/prefix attention.  q [M, Hq, hd]; per query row m of request r, mask row
  * qmask[m, mask_words] over the request's block; keys [0, blk_start[r]) always visible,

@@ -163,6 +163,7 @@ _SIGS: dict[str, tuple] = {
                                    vp, vp]),
     "ygg_embed": (C.c_int, [vp, C.c_int, C.c_int, C.c_int, vp, C.c_int, vp, vp]),
     "ygg_rmsnorm": (C.c_int, [vp, vp, C.c_int, C.c_int, C.c_int, C.c_float, vp, vp]),
+    "ygg_embed_rmsnorm": (C.c_int, [vp, vp, C.c_int, C.c_int, C.c_int, vp, C.c_int, C.c_float, vp, vp, vp]),
     "ygg_attention": (C.c_int, [vp, vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, vp, vp, vp,
                                 C.c_int, C.c_float, vp, vp]),
     "ygg_attn_plan_size": (C.c_size_t, []),
@@ -204,7 +205,7 @@ EXPORTED = tuple(_SIGS)
 KERNELS_PER_CALL = {
     "ygg_topk_softmax": 2, "ygg_egt_grow_level": 1, "ygg_build_mask": 1, "ygg_knapsack_prune": 1,
     "ygg_tree_subtree": 1, "ygg_path_products": 1, "ygg_accept": 1, "ygg_kv_compact": 1, "ygg_gemm_run": 1, "ygg_gemm_fused": 1, "ygg_embed_fused": 1, "ygg_epi_store": 1,
-    "ygg_epi_residual_norm": 1, "ygg_epi_swiglu": 1, "ygg_epi_qkv_rope": 1, "ygg_embed": 1, "ygg_rmsnorm": 1,
+    "ygg_epi_residual_norm": 1, "ygg_epi_swiglu": 1, "ygg_epi_qkv_rope": 1, "ygg_embed": 1, "ygg_rmsnorm": 1, "ygg_embed_rmsnorm": 1,
     "ygg_attention": 1, "ygg_attention_tc": 2, "ygg_row_stats": 1, "ygg_pass0_inputs": 1, "ygg_init_roots": 1, "ygg_level_inputs": 1,
     "ygg_verify_inputs": 1, "ygg_commit": 1, "ygg_stamp": 1, "ygg_mk_run": 1, "ygg_gemv_run": 1, "ygg_attn_dec_run": 1, "ygg_topk_merge": 1, "ygg_topk_merge_l2": 1,
 }

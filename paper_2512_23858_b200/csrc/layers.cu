@@ -28,6 +28,45 @@ __global__ void embed_kernel(const T* __restrict__ table, int V, int d, const in
     if (n + i < d) out[static_cast<size_t>(m) * d + n + i] = v[i];
 }
 
+// Embedding + the first RMSNorm in one pass (verify / AR / prefill entry): one CTA per row, 8
+// features per thread; writes the f32 residual and the normalised activations.  Same arithmetic as
+// embed_kernel followed by rmsnorm_kernel.
+template <typename T>
+__global__ void __launch_bounds__(1024) embed_rmsnorm_kernel(const T* __restrict__ table, int V, int d,
+                                                             const int32_t* __restrict__ tokens,
+                                                             const T* __restrict__ w, float eps,
+                                                             float* __restrict__ resid, T* __restrict__ xn) {
+  pdl_wait();
+  pdl_launch_dependents();
+  __shared__ float red[32];
+  const int m = blockIdx.x;
+  int tok = tokens[m];
+  tok = tok < 0 ? 0 : (tok >= V ? V - 1 : tok);
+  const T* row = table + static_cast<size_t>(tok) * d;
+  const int n = threadIdx.x * 8;
+  float v[8], g[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    v[i] = n + i < d ? to_f32(row[n + i]) : 0.f;
+    g[i] = n + i < d ? to_f32(w[n + i]) : 0.f;
+  }
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+    if (n + i < d) resid[static_cast<size_t>(m) * d + n + i] = v[i];
+  float ss = 0.f;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) ss += v[i] * v[i];
+  ss = warp_sum(ss);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
+  __syncthreads();
+  float t = 0.f;
+  for (int k = 0; k < static_cast<int>(blockDim.x >> 5); ++k) t += red[k];
+  const float r = rsqrtf(t / static_cast<float>(d) + eps);
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+    if (n + i < d) xn[static_cast<size_t>(m) * d + n + i] = from_f32<T>(v[i] * r * g[i]);
+}
+
 // Embedding for the fused path: one CTA per token row, d/8 threads with 8 features (one 16-byte
 // load) each, so the whole row is a single round trip.  Writes the f32 residual, its bf16 copy
 // (next GEMM operand) and each 128-feature tile's sum of squares (16 threads per tile, fixed xor
@@ -343,6 +382,23 @@ int ygg_embed_fused(const void* table, int V, int d, const int32_t* tokens, int 
   YGG_LAUNCH_PDL(embed_fused_kernel, dim3(M), dim3(((d / 8 + 31) / 32) * 32), 0, reinterpret_cast<cudaStream_t>(stream),
                  static_cast<const __nv_bfloat16*>(table), V, d, tokens, resid, static_cast<__nv_bfloat16*>(hb),
                  ss_out, M, trace_next(14));
+  return YGG_OK;
+}
+
+int ygg_embed_rmsnorm(const void* table, const void* norm_w, int dtype, int V, int d, const int32_t* tokens, int M,
+                      float eps, float* resid_out, void* xn_out, ygg_stream_t stream) {
+  YGG_CHECK_ARG(table && norm_w && tokens && resid_out && xn_out && V >= 1 && d >= 1 && d <= 8192,
+                "invalid arguments");
+  if (M <= 0) return YGG_OK;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const int threads = ((d + 7) / 8 + 31) / 32 * 32;
+  if (dtype == YGG_F32)
+    YGG_LAUNCH_PDL(embed_rmsnorm_kernel<float>, dim3(M), dim3(threads), 0, s, static_cast<const float*>(table), V, d,
+                   tokens, static_cast<const float*>(norm_w), eps, resid_out, static_cast<float*>(xn_out));
+  else
+    YGG_LAUNCH_PDL(embed_rmsnorm_kernel<__nv_bfloat16>, dim3(M), dim3(threads), 0, s,
+                   static_cast<const __nv_bfloat16*>(table), V, d, tokens, static_cast<const __nv_bfloat16*>(norm_w),
+                   eps, resid_out, static_cast<__nv_bfloat16*>(xn_out));
   return YGG_OK;
 }
 

@@ -568,10 +568,16 @@ class Forward:
 
         stamp()
         wdt = L.dtype_code(w["embed"].dtype)
-        chk(lib.ygg_embed(w["embed"].data_ptr(), wdt, cfg.vocab, cfg.d_model, self.tokens.data_ptr(), M,
-                          self.resid.data_ptr(), s))
-        chk(lib.ygg_rmsnorm(self.resid.data_ptr(), w["layers"][0]["attn_norm"].data_ptr(), self.act, M, cfg.d_model,
-                            cfg.norm_eps, self.xn.data_ptr(), s))
+        n0 = w["layers"][0]["attn_norm"]
+        if wdt == self.act and L.dtype_code(n0.dtype) == self.act:  # one launch: embedding + first norm
+            chk(lib.ygg_embed_rmsnorm(w["embed"].data_ptr(), n0.data_ptr(), self.act, cfg.vocab, cfg.d_model,
+                                      self.tokens.data_ptr(), M, cfg.norm_eps, self.resid.data_ptr(),
+                                      self.xn.data_ptr(), s))
+        else:
+            chk(lib.ygg_embed(w["embed"].data_ptr(), wdt, cfg.vocab, cfg.d_model, self.tokens.data_ptr(), M,
+                              self.resid.data_ptr(), s))
+            chk(lib.ygg_rmsnorm(self.resid.data_ptr(), n0.data_ptr(), self.act, M, cfg.d_model, cfg.norm_eps,
+                                self.xn.data_ptr(), s))
         ws = self.ws.data_ptr()
         nl = len(self.plans)
         qm = self.qmask.data_ptr() if self.mask_words > 0 else None

@@ -337,6 +337,9 @@ typedef struct {
 } ygg_gemv_epilogue;
 size_t ygg_gemv_plan_size(void);
 int ygg_gemv_grid(const void* plan);  /* CTAs of the plan = top-k chunks per row of STORE_TOPK */
+/* The plan's weight tensor map (CUtensorMap, 128 bytes: box {64, 16 rows, 8 k-chunks of 64}) and
+ * stream geometry (16-row blocks, 512-wide k chunks per block, ring stages). */
+int ygg_gemv_stream_info(const void* plan, void* weight_map, int* nblk, int* kchunks, int* stages);
 /* Optional: after streaming its own weights every CTA pulls its slices of up to two regions
  * [ptr, ptr + bytes) into L2 (later weights / the next attention's cache; region 0 or 1, issued in
  * that order; bytes = 0 disables the region). */
@@ -365,6 +368,10 @@ size_t ygg_attn_dec_workspace_size(const void* plan);
  * split over its CTAs, issued after the CTA's own loads) — later weights, streamed while the
  * attention leaves HBM idle.  region 0 or 1; bytes = 0 disables the region. */
 int ygg_attn_dec_set_l2_prefetch(void* plan, int region, const void* ptr, size_t bytes);
+/* Optional: every launch also pulls into L2 the weight chunks of a row-block GEMV plan that its ring
+ * cannot hold (chunks >= its stage count of every block), through the GEMV's own tensor map — for a
+ * GEMV whose CTAs stream one block each.  gemv_plan = NULL disables. */
+int ygg_attn_dec_set_gemv_prefetch(void* plan, const void* gemv_plan);
 int ygg_attn_dec_run(const void* plan, const int32_t* blk_start, const int32_t* blk_len, const uint32_t* qmask,
                      int mask_words, float scale, void* out, void* workspace, ygg_stream_t stream);
 

@@ -189,6 +189,8 @@ _SIGS: dict[str, tuple] = {
     "ygg_gemv_grid": (C.c_int, [vp]),
     "ygg_gemv_set_l2_prefetch": (C.c_int, [vp, C.c_int, vp, C.c_size_t]),
     "ygg_attn_dec_set_l2_prefetch": (C.c_int, [vp, C.c_int, vp, C.c_size_t]),
+    "ygg_attn_dec_set_gemv_prefetch": (C.c_int, [vp, vp]),
+    "ygg_gemv_stream_info": (C.c_int, [vp, vp, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int)]),
     "ygg_topk_partial_bytes": (C.c_size_t, [C.c_int, C.c_int]),
     "ygg_topk_merge": (C.c_int, [vp, C.c_int, C.c_int, C.c_int, vp, vp, vp, vp]),
     "ygg_topk_merge_l2": (C.c_int, [vp, C.c_int, C.c_int, C.c_int, vp, vp, vp, vp, C.c_int, vp]),

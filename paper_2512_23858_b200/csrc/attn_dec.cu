@@ -41,6 +41,8 @@ struct Plan {
   size_t smem;
   const char* pf_ptr[2];  // optional L2 prefetch regions (issued while HBM is otherwise idle)
   size_t pf_bytes[2];
+  int tpf_nblk, tpf_kchunks, tpf_first;  // optional strided prefetch of a GEMV's weight chunks
+  alignas(64) CUtensorMap tpf;
   alignas(64) CUtensorMap tq;
   alignas(64) CUtensorMap tk;
   alignas(64) CUtensorMap tv;
@@ -60,6 +62,7 @@ struct Args {
   unsigned long long* trace;  // kernel-timeline slot (profiling only) or nullptr
   const char* pf_ptr[2];      // L2 prefetch regions (each split over the CTAs) or nullptr
   size_t pf_bytes[2];
+  int tpf_nblk, tpf_kchunks, tpf_first;  // strided GEMV-chunk prefetch (tpf_nblk = 0: off)
 };
 
 YGG_DEV void tma2(void* dst, const CUtensorMap* m, uint64_t* bar, int c0, int c1) {
@@ -132,7 +135,7 @@ YGG_DEV uint32_t vis_word(int kw, int bs, int bl, int tq, int mask_words, const 
 template <int HD, int KS>  // KS: in-CTA key-split groups (== Args::ksplit)
 __global__ void __launch_bounds__(32 * (1 + kMaxWarps), 1)
     attn_dec_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
-                    const __grid_constant__ CUtensorMap tv, Args a) {
+                    const __grid_constant__ CUtensorMap tv, const __grid_constant__ CUtensorMap tpf, Args a) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* base = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   constexpr int DCH = HD / 64;                    // 128-byte column blocks of a K / Q row
@@ -193,6 +196,19 @@ __global__ void __launch_bounds__(32 * (1 + kMaxWarps), 1)
       for (int dc = 0; dc < DCH; ++dc)
         tma3(sq + dc * (64 * 128), &tq, qbar, dc * 64, kvh * a.Gh, r * a.T + t0);
       for (; c < nch; ++j, c += a.kvsplit) load(j, c);
+      if (a.tpf_nblk > 0) {
+        // The next GEMV's weight chunks its ring cannot hold (chunks >= tpf_first of every 16-row
+        // block), pulled into L2 through its own tensor map: one 16 KB box per instruction.
+        const int ncta = static_cast<int>(gridDim.x * gridDim.y * gridDim.z);
+        const int cta = static_cast<int>((blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x);
+        const int per_blk = a.tpf_kchunks - a.tpf_first;
+        for (int i = cta; i < a.tpf_nblk * per_blk; i += ncta) {
+          const int bq = i / per_blk, qq = a.tpf_first + i % per_blk;
+          asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];"
+                       ::"l"(reinterpret_cast<uint64_t>(&tpf)), "r"(0), "r"(bq * 16), "r"(qq * 8)
+                       : "memory");
+        }
+      }
       for (int rg = 0; rg < 2; ++rg) {
         // After this CTA's own loads: the kernel barely touches HBM, so pull this CTA's slice of
         // later weights into L2 so that their stream starts from L2 (bulk prefetch, 64 KB each).
@@ -559,6 +575,22 @@ int ygg_attn_dec_set_l2_prefetch(void* plan, int region, const void* ptr, size_t
   return YGG_OK;
 }
 
+int ygg_attn_dec_set_gemv_prefetch(void* plan, const void* gemv_plan) {
+  Plan* p = const_cast<Plan*>(plan_of(plan));
+  YGG_CHECK_ARG(p != nullptr, "invalid decode-attention plan");
+  if (gemv_plan == nullptr) {
+    p->tpf_nblk = 0;
+    return YGG_OK;
+  }
+  int nblk = 0, kchunks = 0, stages = 0;
+  if (int rc = ygg_gemv_stream_info(gemv_plan, &p->tpf, &nblk, &kchunks, &stages)) return rc;
+  // only a GEMV whose CTAs stream one block each leaves a fixed, known tail per block
+  p->tpf_first = stages;
+  p->tpf_kchunks = kchunks;
+  p->tpf_nblk = kchunks > stages ? nblk : 0;
+  return YGG_OK;
+}
+
 size_t ygg_attn_dec_workspace_size(const void* plan) {
   // Key splits merge inside a thread-block cluster (DSMEM): no global workspace.  Measured (cfg2
   // draft, 4 splits): a global-memory merge (fence + arrival counter + last-CTA merge) cost ~5 us
@@ -687,11 +719,15 @@ int ygg_attn_dec_run(const void* plan, const int32_t* blk_start, const int32_t* 
     a.pf_ptr[rg] = p->pf_ptr[rg];
     a.pf_bytes[rg] = p->pf_bytes[rg];
   }
+  a.tpf_nblk = p->tpf_nblk;
+  a.tpf_kchunks = p->tpf_kchunks;
+  a.tpf_first = p->tpf_first;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   const dim3 grid(p->Hkv, p->B, p->row_tiles * p->kvsplit), block(32 * (1 + p->warps));
 #define YGG_AD_LAUNCH(H, K)                                                                                    \
   if (p->hd == H && p->ksplit == K)                                                                            \
-    return launch_pdl_cluster_z(attn_dec_kernel<H, K>, grid, block, p->smem, p->kvsplit, s, p->tq, p->tk, p->tv, a);
+    return launch_pdl_cluster_z(attn_dec_kernel<H, K>, grid, block, p->smem, p->kvsplit, s, p->tq, p->tk, p->tv, \
+                                p->tpf_nblk > 0 ? p->tpf : p->tq, a);
   YGG_AD_KERNELS(YGG_AD_LAUNCH)
 #undef YGG_AD_LAUNCH
   return ygg_fail(YGG_ERR_VALUE, "decode attention: no kernel for hd %d with %d key splits", p->hd, p->ksplit);

@@ -600,6 +600,16 @@ int ygg_gemv_set_l2_prefetch(void* plan, int region, const void* ptr, size_t byt
   return YGG_OK;
 }
 
+int ygg_gemv_stream_info(const void* plan, void* weight_map, int* nblk, int* kchunks, int* stages) {
+  const Plan* pl = plan_of(plan);
+  YGG_CHECK_ARG(pl != nullptr && weight_map && nblk && kchunks && stages, "invalid gemv plan / outputs");
+  std::memcpy(weight_map, &pl->tw, sizeof(CUtensorMap));
+  *nblk = pl->p.nblk;
+  *kchunks = pl->p.kchunks;
+  *stages = pl->p.stages;
+  return YGG_OK;
+}
+
 int ygg_gemv_grid(const void* plan) {
   const Plan* pl = plan_of(plan);
   return pl ? pl->p.grid : 0;

@@ -320,6 +320,11 @@ class Forward:
         # 24 MB 3.530; gate|up 24 MB alone 3.464; 16: 3.495; 32: 3.485).
         if not self.gemv:
             regions.append(("wgu", float(os.environ.get("YGG_L2PF_VERIFY_GU_MB", "24"))))
+        # Draft A/B knob: instead of / besides the contiguous start of the down projection, the tail
+        # chunks of every down-GEMV block its ring cannot hold (strided, via the GEMV's tensor map).
+        if self.gemv and os.environ.get("YGG_L2PF_DOWN_TENSOR", "0") != "0":
+            for li, plan in enumerate(self.ad_plans):
+                L.check(lib.ygg_attn_dec_set_gemv_prefetch(plan, self.gv[li][3][0]))
         nl = len(self.ad_plans)
         for li, plan in enumerate(self.ad_plans):
             for rg, (nm, m) in enumerate(regions):

@@ -1001,15 +1001,25 @@ __global__ void kv_compact_kernel(T* cache, int B, int Hkv, int S, int hd, long 
   const size_t d_stride = vt ? static_cast<size_t>(S) : 1;
   const int p0 = base[b] + 1;
   constexpr int kMaxPath = 64;
+  // The move list (source node per accepted position, or -1) resolved once per CTA, one thread per
+  // path entry, instead of every thread chasing path -> keep_idx -> depth serially.
+  __shared__ int s_src[kMaxPath];
+  const int np = n < kMaxPath ? n : kMaxPath;
+  for (int i = threadIdx.x; i < np; i += blockDim.x) {
+    const int node = path[static_cast<size_t>(b) * path_cap + i];
+    const int src_node = keep_idx ? keep_idx[static_cast<size_t>(b) * keep_cap + node] : node;
+    const bool skip = (node_depth && node_depth[static_cast<size_t>(b) * depth_cap + src_node] >= skip_depth) ||
+                      src_node == i;
+    s_src[i] = skip ? -1 : src_node;
+  }
+  __syncthreads();
   for (int d = threadIdx.x; d < hd; d += blockDim.x) {
     T vals[kMaxPath];
     int dst[kMaxPath];
     int m = 0;
-    for (int i = 0; i < n && i < kMaxPath; ++i) {
-      const int node = path[static_cast<size_t>(b) * path_cap + i];
-      const int src_node = keep_idx ? keep_idx[static_cast<size_t>(b) * keep_cap + node] : node;
-      if (node_depth && node_depth[static_cast<size_t>(b) * depth_cap + src_node] >= skip_depth) continue;
-      if (src_node == i) continue;
+    for (int i = 0; i < np; ++i) {
+      const int src_node = s_src[i];
+      if (src_node < 0) continue;
       vals[m] = head[static_cast<size_t>(p0 + src_node) * s_stride + d * d_stride];
       dst[m] = p0 + i;
       ++m;

@@ -127,13 +127,17 @@ def build_decoder(wl: dict, name: str, device, seed_offset: int = 0, weights=Non
     import torch
 
     from paper_2512_23858_b200.engine import SpecDecoder, StepShape
-    from paper_2512_23858_b200.model import Coupling, init_weights, preset
+    from paper_2512_23858_b200.model import Coupling, init_weights, preset, weights_to
 
     tc, dc = preset(wl["target"]), preset(wl["draft"])
     if weights is None:
+        # generated by CPU generators (like the reference arm, oracle/ref_arm.py), so both arms decode
+        # with identical synthetic weights; tensors move to the GPU as bf16 one at a time
+        # (a 70B target does not fit host RAM in fp32: cfg5 generates on the device)
         cp = Coupling(**COUPLING[name])
-        tw = init_weights(tc, 0, torch.bfloat16, device, cp)
-        dw = init_weights(dc, 1, torch.bfloat16, device, cp)
+        gen = "cpu" if tc.matmul_params() * 4 < 64e9 else device
+        tw = weights_to(init_weights(tc, 0, torch.float32, gen, cp), device, torch.bfloat16)
+        dw = weights_to(init_weights(dc, 1, torch.float32, gen, cp), device, torch.bfloat16)
     else:
         tw, dw = weights
 
@@ -408,82 +412,45 @@ def stage_profile(sd, steps=4):
     return prof.measure(steps)
 
 
-def cpu_step_sample(wl_name: str, aal: float):
-    """CPU port of the same step (oracle, torch fp32, all host threads) timed on a bounded sample:
-    one target layer at the verify width, one draft layer at the draft width, both LM heads, and the
-    tree logic (top-k, EGT growth, knapsack prune, walk) — composed by layer count."""
-    import numpy as np
-    import torch
-
-    from oracle import tree_ref as T
-    from oracle.llama_ref import RefCache, RefLlama
-    from paper_2512_23858_b200.model import Coupling, init_weights, preset
+def host_steps(wl_name: str, steps: int, warmup: int) -> dict:
+    """The speculative step on the host CPU (oracle/ref_arm.py): the reference's own specsim tree
+    logic from baseline/_ref + the fp32 torch-CPU model port, every host thread, full workload
+    (same model shapes, tree shape and prompt length), ``warmup`` untimed then ``steps`` timed steps."""
+    from oracle import ref_arm
 
     wl = WORKLOADS[wl_name]
-    torch.set_num_threads(os.cpu_count() or 1)
-    tcfg, dcfg = preset(wl["target"]), preset(wl["draft"])
-    D, W, k = wl["depth"], wl["width"], wl["k"]
-    Tv = min(wl["max_verify"], 1 + D * W) + 1
-    P = wl["prompt"]
-    S = P + 1 + Tv + 8
+    res = ref_arm.run_host_steps(wl, COUPLING[wl_name], steps, warmup, DRAFT_PROF, VERIFY_PROF)
+    res.update(ref_arm.host_info())
+    return res
 
-    def layer_time(cfg, rows, reps=2):
-        one = preset(cfg.name, n_layers=1)
-        w = init_weights(one, 0, torch.float32, "cpu", None)
-        m = RefLlama(one, w)
-        cache = RefCache(one, S)
-        vis = torch.zeros(rows, S, dtype=torch.bool)
-        vis[:, : P + rows] = True
-        toks = list(range(rows))
-        pos = list(range(P, P + rows))
-        m.forward(cache, toks, pos, pos, vis)
-        t0 = time.perf_counter()
-        for _ in range(reps):
-            m.forward(cache, toks, pos, pos, vis)
-        full = (time.perf_counter() - t0) / reps
-        # head-only time (embedding + final norm + lm_head) to split layer vs head
-        x = torch.randn(rows, cfg.d_model)
-        t0 = time.perf_counter()
-        for _ in range(reps):
-            _ = x @ m.head.T
-        head = (time.perf_counter() - t0) / reps
-        return max(full - head, 0.0), head, w
 
-    t_layer_t, t_head_t, _ = layer_time(tcfg, Tv)
-    t_layer_d, t_head_d, _ = layer_time(dcfg, max(W, 2))
-    rng = np.random.default_rng(0)
-    logits = rng.standard_normal((max(W, 2), dcfg.vocab)).astype(np.float32)
-    t0 = time.perf_counter()
-    tree = T.Tree.root(1, 0.9)
-    for _ in range(D):
-        cands = {f: T.topk_softmax(logits[i % len(logits)], k) for i, f in enumerate(tree.levels()[-1])}
-        T.grow_step(tree, lambda tr, n, kk: cands[n], W, k)
-    pr = T.prune_verify(tree, tree.prob, DRAFT_PROF, VERIFY_PROF, D, W, wl["max_verify"])
-    am = rng.integers(0, 10, size=len(pr.tree) + 1)
-    T.greedy_walk(pr.tree, am)
-    t_tree = time.perf_counter() - t0
-    step = tcfg.n_layers * t_layer_t + t_head_t + (D + 1) * (dcfg.n_layers * t_layer_d + t_head_d) + t_tree
-    sample = (f"1 {tcfg.name} layer @ {Tv} rows + LM head, 1 {dcfg.name} layer @ {max(W, 2)} rows + LM head, "
-              f"tree logic (D{D} W{W} k{k}); step = {tcfg.n_layers}x target layer + {D + 1}x "
-              f"({dcfg.n_layers}x draft layer + head) + tree; tokens/step = GPU-measured AAL {aal:.3f}")
-    return {"value": round(aal / step, 4), "unit": "tokens/s", "cores": torch.get_num_threads(), "kind": "port",
-            "sample": sample, "step_s": round(step, 4)}
+def _host_sample(res: dict, steps: int, warmup: int) -> str:
+    return (f"{steps} timed speculative steps (+{warmup} untimed) of the full workload on the host: "
+            f"{res['target_layers']}-layer target + {res['draft_layers']}-layer draft in fp32 torch-CPU "
+            f"({res['threads']} threads, {res['cpu_model']}), tree logic = {res['tree_impl']} "
+            f"({res['tree_logic_ms_per_step']:.2f} ms/step), measured AAL {res['aal']:.3f}")
 
 
 def run_reference(args, rank, world):
+    """Reference arm: the step on the host CPU (rank 0 only; other ranks exit without work)."""
     if rank != 0:
         return
     wl = WORKLOADS[args.workload]
-    aal = args.ref_aal
-    res = cpu_step_sample(args.workload, aal)
-    line = {"impl": "reference", "metric": "accepted tokens/s", "value": res["value"], "unit": "tokens/s",
+    res = host_steps(args.workload, args.steps, args.warmup)
+    kind = "reference" if res["tree_impl"] == "specsim" else "port"
+    v = round(res["tokens_per_s"], 4)
+    line = {"impl": "reference", "metric": "accepted tokens/s", "value": v, "unit": "tokens/s",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": round(res["step_s"] * 1e3, 3), "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": wl["desc"], "aal_assumed": aal},
-            "cpu_baseline": {"value": res["value"], "unit": "tokens/s", "cores": res["cores"], "kind": "port",
-                             "sample": res["sample"]},
-            "e2e": {"value": res["value"], "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+            "ms_per_step": round(res["ms_per_step"], 2), "p50_step_ms": round(res["p50_step_ms"], 2),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (coupled random-init weights from CPU generators, random prompt)",
+            "config": {"workload": wl["desc"], "aal": round(res["aal"], 4)},
+            "cpu_baseline": {"value": v, "unit": "tokens/s", "cores": res["threads"], "kind": kind,
+                             "sample": _host_sample(res, args.steps, args.warmup)},
+            "host": {"cpu_model": res["cpu_model"], "cpu_count": res["cpu_count"], "init_s": res["init_s"],
+                     "prefill_s": res["prefill_s"], "tree_impl": res["tree_impl"],
+                     "tree_logic_ms_per_step": round(res["tree_logic_ms_per_step"], 3)},
+            "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
@@ -544,7 +511,7 @@ def run_ours(args, rank, world, local_rank):
     aal = tokens / (args.steps * sd.B)
 
     # ---- e2e through the public API: pinned H2D of the step inputs, replay, D2H of the emitted tokens
-    e2e = e2e_run(sd, args.steps, device)
+    e2e = e2e_run(sd, prompts, args.steps, device)
     e2e_tokens = torch.tensor([e2e["tokens"]], dtype=torch.float64, device=device)
     e2e_t = torch.tensor([e2e["seconds"]], dtype=torch.float64, device=device)
     if world > 1:
@@ -558,18 +525,21 @@ def run_ours(args, rank, world, local_rank):
         stages = stage_profile(sd)
     except Exception as exc:  # profiler is diagnostic only
         stages = {"error": str(exc)}
-    # final result gather (the only collective)
-    gathered = None
-    if world > 1:
-        out = [None] * world
-        dist.all_gather_object(out, sd.generated(0)[:8])
-        gathered = len(out)
+    ar = ar_baseline(sd, prompts) if not args.no_ar_baseline else None
+    # final result gather of every request's generated ids (the only collective)
+    from paper_2512_23858_b200.dist import gather_generated
+
+    mine = {rank * sd.B + b: sd.generated(b) for b in range(sd.B)}
+    merged = gather_generated(mine, world)
+    gathered = {"ranks": world, "requests": len(merged), "tokens": sum(len(v) for v in merged.values())}
     if rank != 0:
         return
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_step_sample(args.workload, aal)
-        cpu.pop("step_s", None)
+        res = host_steps(args.workload, 2, 1)
+        cpu = {"value": round(res["tokens_per_s"], 4), "unit": "tokens/s", "cores": res["threads"],
+               "kind": "reference" if res["tree_impl"] == "specsim" else "port",
+               "sample": _host_sample(res, 2, 1)}
     line = {
         "metric": "accepted tokens/s", "value": round(tokens_all / total_s, 2), "unit": "tokens/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -586,33 +556,42 @@ def run_ours(args, rank, world, local_rank):
                 "h2d_bytes_per_step": e2e["h2d"], "d2h_bytes_per_step": e2e["d2h"],
                 "ms_per_step": round(float(e2e_t) * 1e3 / args.steps, 4),
                 "aal": round(e2e["tokens"] / (args.steps * sd.B), 4),
-                "note": "steps after the timed window (longer context, its own AAL); lagged pinned readback"},
+                "note": "prompt H2D + prefill + K steps with streamed per-step readback, all timed; "
+                        "its own AAL (fresh prefill, same prompt)"},
         "gpu_launches": launches_per_step * args.steps, "launches_per_step": launches_per_step,
-        "clocks": clk, "cpu_baseline": cpu, "peak_kind": peak_kind, "gathered_ranks": gathered,
+        "clocks": clk, "cpu_baseline": cpu, "peak_kind": peak_kind, "gathered": gathered, "ar_baseline": ar,
+        "speculative_speedup_vs_ar": round((tokens_all / total_s) / (world * ar["tokens_per_s"]), 3) if ar else None,
     }
     print(json.dumps(line), flush=True)
 
 
-def e2e_run(sd, steps, device):
-    """Public-API serving loop: each step copies its inputs (sampling uniforms / control words) from
-    pinned host memory, replays the step graph, and reads the emitted tokens back into pinned host
-    memory.  The readback is double-buffered: the host consumes step i-1's tokens (event wait) while
-    step i runs, as a server streaming tokens would; every step's D2H is inside the timed region."""
+def e2e_run(sd, prompts, steps, device):
+    """End to end through the public API, as a user serving one batch: the prompts go host -> device
+    from pinned memory, the decoder prefills them, then every step (SAMPLE: after the H2D of its
+    acceptance uniforms from a pinned double buffer) replays the step graph and its emitted tokens come
+    back to pinned host memory.  The readback is double-buffered: the host consumes step i-1's tokens
+    (event wait) while step i runs, as a server streaming tokens would.  Everything from the prompt
+    upload to the last token on the host is inside the timed region."""
     import torch
 
     B = sd.B
-    n_emit = sd.shape.depth + 2
-    host_out = [torch.zeros(B, n_emit + 1, dtype=torch.int32).pin_memory() for _ in range(2)]
-    host_in = torch.zeros_like(sd.uniforms_host).pin_memory()
-    h2d = host_in.numel() * host_in.element_size()
-    d2h = host_out[0].numel() * host_out[0].element_size()
+    sample = sd.mode != "greedy"
+    n_emit = sd.emit.shape[1]
+    host_out = [torch.zeros(B, n_emit, dtype=torch.int32).pin_memory() for _ in range(2)]
+    host_prompts = prompts.to(torch.int32).pin_memory()
+    h2d = host_prompts.numel() * host_prompts.element_size()
+    if sample:
+        h2d += steps * sd.uniforms.numel() * sd.uniforms.element_size()
+    d2h = steps * host_out[0].numel() * host_out[0].element_size()
     done = [torch.cuda.Event(), torch.cuda.Event()]
     torch.cuda.synchronize()
-    gen0 = sd.seq.n_gen.clone()
     streamed = 0
     t0 = time.perf_counter()
+    sd.prefill(host_prompts.to(device, non_blocking=True))
+    gen0 = sd.seq.n_gen.clone()
     for i in range(steps):
-        sd.uniforms.copy_(host_in, non_blocking=True)
+        if sample:  # pinned double-buffered H2D of this step's uniforms, enqueued before the replay
+            sd.set_uniforms(10_000 + i, 0)
         sd.step()
         sd.read_emitted(host_out[i % 2])
         done[i % 2].record()
@@ -625,7 +604,30 @@ def e2e_run(sd, steps, device):
     tokens = int((sd.seq.n_gen - gen0).sum())
     if streamed != tokens:
         raise RuntimeError(f"e2e: host received {streamed} tokens, device generated {tokens}")
-    return {"tokens": tokens, "seconds": dt, "h2d": h2d, "d2h": d2h}
+    return {"tokens": tokens, "seconds": dt, "h2d": h2d // steps, "d2h": d2h // steps}
+
+
+def ar_baseline(sd, prompts, n_tokens: int = 32) -> dict:
+    """Plain greedy autoregressive decoding of the target alone (engine.ARDecoder: graph-replayed
+    single-row forwards through the verify kernel families), for the speculative speed-up."""
+    import torch
+
+    from paper_2512_23858_b200.engine import ARDecoder
+
+    ar = ARDecoder(sd.tc, sd.tw, batch=sd.B, max_seq=prompts.shape[1] + n_tokens + 8, device=sd.dev)
+    ar.generate(prompts, 4)  # builds the prefill plans and captures the token graph
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(n_tokens):
+        ar.graph.replay()
+    b.record()
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(b) / n_tokens
+    del ar
+    torch.cuda.empty_cache()
+    return {"tokens_per_s": round(1e3 * sd.B / ms, 2), "ms_per_token": round(ms, 4),
+            "kernels": "verify families at 1 row (tcgen05 stream-K GEMM + epilogues, decode attention)"}
 
 
 def main():
@@ -636,11 +638,15 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default="cfg2")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--ref-aal", type=float, default=float(os.environ.get("YGG_REF_AAL", "3.78")),
-                    help="accepted tokens per step for --impl reference: the GPU-measured AAL of the same workload (profiles/r1_bench_full.jsonl); greedy decoding is lossless so both arms accept the same tokens")
+    ap.add_argument("--no-ar-baseline", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        # one process per GPU: re-run this script under torch.distributed.run with N ranks
+        from paper_2512_23858_b200.dist import launch
+
+        sys.exit(launch(args.gpus, str(Path(__file__).resolve()), sys.argv[1:]))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))

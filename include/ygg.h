@@ -89,6 +89,10 @@ typedef struct {
   int32_t* acc_log; /* [B, log_cap] accepted_len per step (ring), may be NULL */
   int32_t* step;    /* [1] step counter */
   int32_t log_cap;
+  int32_t p_limit;  /* commit never advances P[b] past p_limit (the tree / scratch slots of the next
+                       step must fit in S); 0 = S - 1 */
+  int32_t* gen_limit; /* [B] a request with n_gen >= gen_limit[b] is finished and frozen; may be NULL */
+  int32_t* status;  /* [B] bit0 finished (gen_limit reached), bit1 frozen at p_limit; may be NULL */
 } ygg_seq;
 
 /* ---------------- library ---------------- */

@@ -15,9 +15,38 @@ from . import tree_ref as T
 from .llama_ref import RefCache, RefLlama, causal_visible
 
 
+class OracleTreeOps:
+    """Tree logic of the step from the oracle restatement (``tree_ref``)."""
+
+    name = "oracle"
+
+    def root(self, tok, prob):
+        return T.Tree.root(tok, prob)
+
+    def frontier(self, tree):
+        return tree.levels()[-1]
+
+    def node(self, tree, i):
+        return tree.token[i], tree.depth[i], tree.path(i)
+
+    def grow(self, tree, cands, W, k):
+        return T.grow_step(tree, lambda tr, node, kk: cands[node], W, k)
+
+    def prune(self, tree, dp, vp, D, W, maxv):
+        pr = T.prune_verify(tree, tree.prob, dp, vp, D, W, maxv)
+        return pr.tree, pr.tree, pr.kept
+
+    def as_oracle(self, tree):
+        return tree
+
+    def walk(self, vtree_native, am):
+        return T.greedy_walk(vtree_native, am)
+
+
 class RefSpecDecoder:
     def __init__(self, target: RefLlama, draft: RefLlama, depth: int, width: int, k: int, max_verify: int,
-                 drafter_profile, verifier_profile, S: int, fixed_verify: int = 0):
+                 drafter_profile, verifier_profile, S: int, fixed_verify: int = 0, tree_ops=None):
+        self.ops = tree_ops if tree_ops is not None else OracleTreeOps()
         self.t, self.d = target, draft
         self.D, self.W, self.k, self.maxv = depth, width, k, max_verify
         self.dp, self.vp = drafter_profile, verifier_profile
@@ -49,35 +78,38 @@ class RefSpecDecoder:
         vis[1, : P + 1] = True
         lg = self._draft_rows([self.hist[P - 1], self.hist[P]], [P - 1, P], [P - 1, P], vis)
         root = T.topk_softmax(lg[1].numpy(), self.k)[0]
-        tree = T.Tree.root(*root)
+        ops = self.ops
+        tree = ops.root(*root)
         stopped = False
         for _ in range(self.D):
             if stopped:
                 break
-            frontier = tree.levels()[-1]
-            n = len(tree)
+            frontier = ops.frontier(tree)
+            info = [ops.node(tree, f) for f in frontier]
             vis = torch.zeros(len(frontier), S, dtype=torch.bool)
             vis[:, : P + 1] = True
-            for r, node in enumerate(frontier):
-                for a in tree.path(node):
+            for r, (_, _, path) in enumerate(info):
+                for a in path:
                     vis[r, P + 1 + a] = True
-            lg = self._draft_rows([tree.token[f] for f in frontier], [P + 1 + tree.depth[f] for f in frontier],
+            lg = self._draft_rows([tok for tok, _, _ in info], [P + 1 + dep for _, dep, _ in info],
                                   [P + 1 + f for f in frontier], vis)
             cands = {f: T.topk_softmax(lg[r].numpy(), self.k) for r, f in enumerate(frontier)}
-            added = T.grow_step(tree, lambda tr, node, kk: cands[node], self.W, self.k)
+            added = ops.grow(tree, cands, self.W, self.k)
             if not added:
                 stopped = True
-            assert len(tree) >= n
-        grown = tree
+        grown_native = tree
+        grown = ops.as_oracle(tree)
         if self.fixed_verify > 0:
             dp = T.Knapsack(grown, T.path_products(grown, grown.prob), self.maxv)
             kk = min(self.fixed_verify, dp.cap)
             keep = dp.pick(kk)
             vtree, _ = grown.subtree(keep)
+            vnative = vtree
             kept = tuple(sorted(keep))
+            walk = T.greedy_walk
         else:
-            pr = T.prune_verify(grown, grown.prob, self.dp, self.vp, self.D, self.W, self.maxv)
-            vtree, kept = pr.tree, pr.kept
+            vnative, vtree, kept = ops.prune(grown_native, self.dp, self.vp, self.D, self.W, self.maxv)
+            walk = ops.walk
         # verify
         n = len(vtree)
         tokens = [self.hist[P]] + vtree.token
@@ -90,7 +122,7 @@ class RefSpecDecoder:
                 vis[1 + i, P + 1 + a] = True
         lt = self.t.forward(self.tc, tokens, pos, slots, vis)
         am = torch.argmax(lt, dim=-1).tolist()
-        path, bonus = T.greedy_walk(vtree, am)
+        path, bonus = walk(vnative, am)
         a = len(path)
         # compaction: target (verify order), draft (grown order, leaves at depth D never drafted)
         self.tc.move([P + 1 + p for p in path], [P + 1 + i for i in range(a)])

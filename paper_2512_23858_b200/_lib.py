@@ -59,6 +59,9 @@ class YggSeq(C.Structure):
         ("acc_log", vp),
         ("step", vp),
         ("log_cap", C.c_int32),
+        ("p_limit", C.c_int32),
+        ("gen_limit", vp),
+        ("status", vp),
     ]
 
 

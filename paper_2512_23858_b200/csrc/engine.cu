@@ -162,7 +162,9 @@ __global__ void verify_inputs_kernel(ygg_tree t, ygg_seq seq, int32_t* tokens, i
 }
 
 // Commit an accepted path: append the accepted tokens + bonus to the history, advance P,
-// record accepted_len (lagged host readback feeds the depth predictor).
+// record accepted_len (lagged host readback feeds the depth predictor).  A request that has reached
+// its generation limit, or whose next prefix would pass seq.p_limit (the next step's tree and scratch
+// slots must stay inside the S-slot cache), is frozen: nothing is appended, P stays, emit count 0.
 __global__ void commit_kernel(ygg_seq seq, ygg_tree vt, const int32_t* __restrict__ path,
                               const int32_t* __restrict__ path_len, const int32_t* __restrict__ bonus,
                               int32_t* __restrict__ emit, int emit_cap) {
@@ -174,18 +176,30 @@ __global__ void commit_kernel(ygg_seq seq, ygg_tree vt, const int32_t* __restric
     const size_t tb = static_cast<size_t>(b) * vt.cap;
     const int P = seq.P[b];
     const int a = path_len[b];
-    int32_t* h = seq.hist + static_cast<size_t>(b) * seq.S;
-    for (int i = 0; i < a; ++i) h[P + 1 + i] = vt.token[tb + path[tb + i]];
-    h[P + 1 + a] = bonus[b];
-    if (emit) {  // per-step emitted tokens for host streaming: [count, tokens...]
-      int32_t* em = emit + static_cast<size_t>(b) * emit_cap;
-      em[0] = 1 + a;
-      for (int i = 0; i < emit_cap - 1; ++i) em[1 + i] = (i <= a) ? h[P + 1 + i] : -1;
+    const int limit = seq.p_limit > 0 ? seq.p_limit : seq.S - 1;
+    const bool finished = seq.gen_limit && seq.n_gen[b] >= seq.gen_limit[b];
+    const bool full = !finished && P + 1 + a > limit;
+    int32_t* em = emit ? emit + static_cast<size_t>(b) * emit_cap : nullptr;
+    if (finished || full) {
+      if (seq.status) seq.status[b] |= (finished ? 1 : 0) | (full ? 2 : 0);
+      if (em) {
+        em[0] = 0;
+        for (int i = 0; i < emit_cap - 1; ++i) em[1 + i] = -1;
+      }
+    } else {
+      int32_t* h = seq.hist + static_cast<size_t>(b) * seq.S;
+      for (int i = 0; i < a; ++i) h[P + 1 + i] = vt.token[tb + path[tb + i]];
+      h[P + 1 + a] = bonus[b];
+      if (em) {  // per-step emitted tokens for host streaming: [count, tokens...]
+        em[0] = 1 + a;
+        for (int i = 0; i < emit_cap - 1; ++i) em[1 + i] = (i <= a) ? h[P + 1 + i] : -1;
+      }
+      seq.P[b] = P + 1 + a;
+      seq.n_gen[b] += 1 + a;
+      if (seq.status && seq.gen_limit && seq.n_gen[b] >= seq.gen_limit[b]) seq.status[b] |= 1;
     }
-    seq.P[b] = P + 1 + a;
-    seq.n_gen[b] += 1 + a;
     if (seq.acc_log && seq.log_cap > 0)
-      seq.acc_log[static_cast<size_t>(b) * seq.log_cap + (step % seq.log_cap)] = 1 + a;
+      seq.acc_log[static_cast<size_t>(b) * seq.log_cap + (step % seq.log_cap)] = (finished || full) ? 0 : 1 + a;
   }
   __syncthreads();
   if (b == 0) seq.step[0] = step + 1;

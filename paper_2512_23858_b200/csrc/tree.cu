@@ -958,22 +958,35 @@ __global__ void __launch_bounds__(kAcceptThreads) accept_kernel(
       const double target = s_u2 * s_total;
       double acc = 0.0;
       int pick = -1;
+      int last_ok = -1;  // last non-excluded token with mass: the fallback never returns a rejected child
       for (int i = 0; i < (int)blockDim.x && pick < 0; ++i) {
-        if (acc + s_part[i] > target) {
+        if (s_part[i] > 0.0) {
           const int l2 = i * per, h2 = min(V, l2 + per);
-          for (int v = l2; v < h2; ++v) {
-            bool ex = false;
-            for (int e = 0; e < nex; ++e) ex |= (s_excl[e] == v);
-            if (ex) continue;
-            acc += exp(static_cast<double>(to_f32(lr[v]) * inv_temp) - lse);
-            if (acc > target) { pick = v; break; }
+          if (acc + s_part[i] > target) {
+            const double slice_start = acc;
+            for (int v = l2; v < h2; ++v) {
+              bool ex = false;
+              for (int e = 0; e < nex; ++e) ex |= (s_excl[e] == v);
+              if (ex) continue;
+              const double pv = exp(static_cast<double>(to_f32(lr[v]) * inv_temp) - lse);
+              if (pv > 0.0) last_ok = v;
+              acc += pv;
+              if (acc > target) { pick = v; break; }
+            }
+            // re-accumulated slice fell a few ulps short of s_part: the slice's last valid token
+            if (pick < 0 && last_ok >= l2) pick = last_ok;
+            acc = slice_start + s_part[i];
+          } else {
+            acc += s_part[i];
+            for (int v = h2 - 1; v >= l2; --v) {  // remember this slice's last valid token
+              bool ex = false;
+              for (int e = 0; e < nex; ++e) ex |= (s_excl[e] == v);
+              if (!ex) { last_ok = v; break; }
+            }
           }
-          if (pick < 0) pick = h2 - 1;
-        } else {
-          acc += s_part[i];
         }
       }
-      if (pick < 0) pick = V - 1;
+      if (pick < 0) pick = last_ok >= 0 ? last_ok : 0;
       bonus[b] = pick;
     }
   }
@@ -1002,29 +1015,34 @@ __global__ void kv_compact_kernel(T* cache, int B, int Hkv, int S, int hd, long 
   const int p0 = base[b] + 1;
   constexpr int kMaxPath = 64;
   // The move list (source node per accepted position, or -1) resolved once per CTA, one thread per
-  // path entry, instead of every thread chasing path -> keep_idx -> depth serially.
+  // path entry, instead of every thread chasing path -> keep_idx -> depth serially.  Paths longer
+  // than kMaxPath go in chunks: a chunk's destinations (< its first position) never overlap a later
+  // chunk's sources (source node >= path position), and inside a chunk every read precedes the writes.
   __shared__ int s_src[kMaxPath];
-  const int np = n < kMaxPath ? n : kMaxPath;
-  for (int i = threadIdx.x; i < np; i += blockDim.x) {
-    const int node = path[static_cast<size_t>(b) * path_cap + i];
-    const int src_node = keep_idx ? keep_idx[static_cast<size_t>(b) * keep_cap + node] : node;
-    const bool skip = (node_depth && node_depth[static_cast<size_t>(b) * depth_cap + src_node] >= skip_depth) ||
-                      src_node == i;
-    s_src[i] = skip ? -1 : src_node;
-  }
-  __syncthreads();
-  for (int d = threadIdx.x; d < hd; d += blockDim.x) {
-    T vals[kMaxPath];
-    int dst[kMaxPath];
-    int m = 0;
-    for (int i = 0; i < np; ++i) {
-      const int src_node = s_src[i];
-      if (src_node < 0) continue;
-      vals[m] = head[static_cast<size_t>(p0 + src_node) * s_stride + d * d_stride];
-      dst[m] = p0 + i;
-      ++m;
+  for (int c0 = 0; c0 < n; c0 += kMaxPath) {
+    const int np = (n - c0) < kMaxPath ? (n - c0) : kMaxPath;
+    __syncthreads();
+    for (int i = threadIdx.x; i < np; i += blockDim.x) {
+      const int node = path[static_cast<size_t>(b) * path_cap + c0 + i];
+      const int src_node = keep_idx ? keep_idx[static_cast<size_t>(b) * keep_cap + node] : node;
+      const bool skip = (node_depth && node_depth[static_cast<size_t>(b) * depth_cap + src_node] >= skip_depth) ||
+                        src_node == c0 + i;
+      s_src[i] = skip ? -1 : src_node;
     }
-    for (int j = 0; j < m; ++j) head[static_cast<size_t>(dst[j]) * s_stride + d * d_stride] = vals[j];
+    __syncthreads();
+    for (int d = threadIdx.x; d < hd; d += blockDim.x) {
+      T vals[kMaxPath];
+      int dst[kMaxPath];
+      int m = 0;
+      for (int i = 0; i < np; ++i) {
+        const int src_node = s_src[i];
+        if (src_node < 0) continue;
+        vals[m] = head[static_cast<size_t>(p0 + src_node) * s_stride + d * d_stride];
+        dst[m] = p0 + c0 + i;
+        ++m;
+      }
+      for (int j = 0; j < m; ++j) head[static_cast<size_t>(dst[j]) * s_stride + d * d_stride] = vals[j];
+    }
   }
 }
 

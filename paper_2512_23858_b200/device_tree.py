@@ -107,7 +107,11 @@ class DeviceTrees:
 
 
 class SeqState:
-    def __init__(self, B: int, S: int, log_cap: int = 4096, device="cuda"):
+    """Per-request sequence state (``ygg_seq``).  ``p_limit`` bounds the prefix: the commit kernel
+    freezes a request instead of advancing P past it (status bit1), and a request whose n_gen reaches
+    ``gen_limit[b]`` is finished and frozen (status bit0)."""
+
+    def __init__(self, B: int, S: int, log_cap: int = 4096, device="cuda", p_limit: int = 0):
         i32 = dict(dtype=torch.int32, device=device)
         self.B, self.S, self.log_cap = B, S, log_cap
         self.hist = torch.zeros(B, S, **i32)
@@ -115,8 +119,12 @@ class SeqState:
         self.n_gen = torch.zeros(B, **i32)
         self.acc_log = torch.zeros(B, log_cap, **i32)
         self.step = torch.zeros(1, **i32)
+        self.gen_limit = torch.full((B,), 2**31 - 1, **i32)
+        self.status = torch.zeros(B, **i32)
+        self.p_limit = int(p_limit)
         self._struct = L.YggSeq(B, S, self.hist.data_ptr(), self.P.data_ptr(), self.n_gen.data_ptr(),
-                                self.acc_log.data_ptr(), self.step.data_ptr(), log_cap)
+                                self.acc_log.data_ptr(), self.step.data_ptr(), log_cap, self.p_limit,
+                                self.gen_limit.data_ptr(), self.status.data_ptr())
 
     @property
     def struct(self) -> L.YggSeq:

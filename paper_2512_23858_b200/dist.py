@@ -39,3 +39,31 @@ def gather_generated(outputs: dict[int, list[int]], world: int) -> dict[int, lis
                 raise ValueError(f"request {rid} produced by two ranks")
             merged[rid] = toks
     return merged
+
+
+def free_port() -> int:
+    import socket
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def launch(nproc: int, script: str, argv: list[str], env: dict | None = None, timeout: float | None = None) -> int:
+    """One process per GPU on this node: re-run ``script argv`` under ``torch.distributed.run`` with
+    ``nproc`` ranks rendezvousing on 127.0.0.1 (each rank reads RANK / LOCAL_RANK / WORLD_SIZE).
+    Returns the launcher's exit code (non-zero if any rank failed)."""
+    import subprocess
+    import sys
+
+    if nproc < 1:
+        raise ValueError("nproc must be >= 1")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nproc}",
+           "--master-addr=127.0.0.1", f"--master-port={free_port()}", script, *argv]
+    e = dict(os.environ)
+    e.update(env or {})
+    e.setdefault("NCCL_DEBUG", "INFO")  # keep NCCL's init log (transport / NVLS choice) in the run's stderr
+    e.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    return subprocess.run(cmd, env=e, timeout=timeout).returncode

@@ -43,6 +43,16 @@ class StepShape:
     max_verify: int = 64
     fixed_verify: int = 0  # >0: prune to exactly this many nodes (static verify width)
 
+    def __post_init__(self):
+        if self.depth < 1 or self.width < 1 or self.expansion_k < 1:
+            raise ValueError("depth, width and expansion_k must be >= 1")
+        if self.depth + 1 > 64:  # an accepted path holds <= depth + 1 nodes (KV compaction bound)
+            raise ValueError("depth must be <= 63")
+        if self.expansion_k > 32:
+            raise ValueError("expansion_k must be <= 32")
+        if self.max_verify < 1:
+            raise ValueError("max_verify must be >= 1")
+
 
 class SpecDecoder:
     def __init__(
@@ -81,7 +91,8 @@ class SpecDecoder:
         self.S = (max_seq + scratch + 63) // 64 * 64
         dev = torch.device(device)
         self.dev = dev
-        self.seq = SeqState(batch, self.S, device=dev)
+        # commit freezes a request rather than let the next step's tree / scratch slots pass S
+        self.seq = SeqState(batch, self.S, device=dev, p_limit=self.S - scratch)
         self.tcache = new_cache(target_cfg, batch, self.S, act_dtype, dev)
         self.dcache = new_cache(draft_cfg, batch, self.S, act_dtype, dev)
         tmw = max(1, (self.T + 31) // 32)
@@ -129,7 +140,10 @@ class SpecDecoder:
         self.emit = torch.zeros(batch, D + 3, **i32)
         self.n_uniform = D + 3
         self.uniforms = torch.full((batch, self.n_uniform), 0.5, **f64)
-        self.uniforms_host = torch.full((batch, self.n_uniform), 0.5, dtype=torch.float64).pin_memory()
+        self._u_host = [torch.full((batch, self.n_uniform), 0.5, dtype=torch.float64).pin_memory() for _ in range(2)]
+        self._u_ev = [torch.cuda.Event(), torch.cuda.Event()]
+        self._u_used = [False, False]
+        self._u_next = 0
         self.set_profiles(profiles)
         self.prefill_len = prefill_len
         self._prefill_fwd = {}
@@ -180,6 +194,8 @@ class SpecDecoder:
         self.seq.P.fill_(P0)
         self.seq.n_gen.fill_(1)
         self.seq.step.zero_()
+        self.seq.status.zero_()
+        self.seq.gen_limit.fill_(2**31 - 1)
 
     # ------------------------------------------------------------------
     def _draft_topk(self, rows: int, k: int, s, next_pass: str = "draft") -> None:
@@ -246,8 +262,7 @@ class SpecDecoder:
             chk(lib.ygg_accept(vt.struct, L.YGG_ACCEPT_GREEDY, None, None, 0, self.row_argmax.data_ptr(), None,
                                L.YGG_F32, self.tc.vocab, self.tc.vocab, None, 1.0, self.path.data_ptr(),
                                self.path_len.data_ptr(), self.acc_len.data_ptr(), self.bonus.data_ptr(), None, s))
-        else:
-            self.uniforms.copy_(self.uniforms_host, non_blocking=True)
+        else:  # self.uniforms is filled by set_uniforms() on the stream, before the replay
             chk(lib.ygg_row_stats(vf.logits.data_ptr(), L.YGG_F32, nrows, self.tc.vocab, self.tc.vocab,
                                   self.temperature, self.row_argmax.data_ptr(), self.row_stats.data_ptr(), s))
             chk(lib.ygg_accept(vt.struct, L.YGG_ACCEPT_SAMPLE, None, self.uniforms.data_ptr(), self.n_uniform,
@@ -268,11 +283,25 @@ class SpecDecoder:
         stamp(5)
 
     # ------------------------------------------------------------------
-    def set_uniforms(self, step_index: int, seed: int) -> None:
-        """Host-pregenerated uniforms from default_rng([seed, step]) (simulator.py:306)."""
+    def set_uniforms(self, step_index: int, seed: int, stream=None) -> None:
+        """Acceptance uniforms of the next step from default_rng([seed, step]) (simulator.py:306).
+
+        The host fills one of two pinned buffers and enqueues its H2D copy into the device buffer the
+        step graph reads, on the launching stream, so the copy lands after the previous step and before
+        the next replay.  Before a pinned buffer is rewritten, the event recorded after its previous copy
+        is awaited: the host may run many steps ahead without overwriting uniforms still in flight."""
+        slot = self._u_next % 2
+        self._u_next += 1
+        ev = self._u_ev[slot]
+        if self._u_used[slot]:
+            ev.synchronize()
         rng = np.random.default_rng([seed, step_index])
-        u = rng.random((self.B, self.n_uniform))
-        self.uniforms_host.copy_(torch.from_numpy(u))
+        self._u_host[slot].copy_(torch.from_numpy(rng.random((self.B, self.n_uniform))))
+        st = stream if stream is not None else torch.cuda.current_stream(self.dev)
+        with torch.cuda.stream(st):
+            self.uniforms.copy_(self._u_host[slot], non_blocking=True)
+            ev.record(st)
+        self._u_used[slot] = True
 
     def capture(self) -> None:
         """Capture one step as a CUDA graph (static shapes, device-resident control)."""
@@ -306,19 +335,36 @@ class SpecDecoder:
         n = int(self.seq.n_gen[b])
         return self.seq.hist[b, P0 : P0 + n].cpu().tolist()
 
-    def generate(self, prompts: torch.Tensor, n_tokens: int, use_graph: bool = True, sync_every: int = 8):
-        """Public generate loop: prefill, then steps until every request has n_tokens."""
-        self.prefill_len = prompts.shape[1]
+    def generate(self, prompts: torch.Tensor, n_tokens: int, use_graph: bool = True, sync_every: int = 8,
+                 seed: int = 0):
+        """Public generate loop: prefill, then steps until every request has n_tokens.
+
+        Each request stops on the device once it has n_tokens (commit freezes it: no more history, no
+        KV movement past its prefix), so requests that accept fast never run past the cache while the
+        slowest catches up; the host polls the finished flags every ``sync_every`` steps."""
+        B, P0 = prompts.shape
+        D = self.shape.depth
+        # every step appends at most D + 2 tokens; a request may overshoot n_tokens by D + 1 before it
+        # freezes, and the next step's tree / scratch slots sit past the prefix
+        if P0 + n_tokens + D + 2 > self.seq.p_limit:
+            raise ValueError(f"prompt {P0} + {n_tokens} generated tokens do not fit the cache (max_seq too small: "
+                             f"prefix limit {self.seq.p_limit})")
+        self.prefill_len = P0
         self.prefill(prompts)
+        self.seq.gen_limit.fill_(n_tokens)
+        self.seq.status.zero_()
         if use_graph and self.graph is None:
             self.capture()
         steps = 0
         while True:
             if steps % sync_every == 0:
-                if int(self.seq.n_gen.min()) >= n_tokens:
+                st = self.seq.status.cpu()
+                if bool((st != 0).all()):
+                    if bool((st & 2).any()):
+                        raise RuntimeError("a request reached the cache capacity before n_tokens")
                     break
             if self.mode == SAMPLE:
-                self.set_uniforms(steps, 0)
+                self.set_uniforms(steps, seed)
             self.step(use_graph)
             steps += 1
         return [self.generated(b)[:n_tokens] for b in range(self.B)], steps

@@ -200,3 +200,24 @@ def test_profiler_csv_round_trip(tmp_path):
     for name, _, us in rows:
         assert sp.base(name) == us
     assert sp.base("DraftStep3") == 1104.45  # DraftStep fallback (reference scheduler.py:112-118)
+
+
+def test_launcher_runs_world2_gloo(tmp_path):
+    """dist.launch (what `bench.py --gpus N` uses when WORLD_SIZE is unset) starts N ranks under
+    torch.distributed.run on 127.0.0.1; the gathered ids equal the single-process decode."""
+    import json
+
+    from oracle.llama_ref import RefLlama, greedy_ar
+    from paper_2512_23858_b200.dist import launch
+    from paper_2512_23858_b200.model import init_weights, preset
+
+    out = tmp_path / "gathered.json"
+    rc = launch(2, str(ROOT / "tests" / "_launch_worker.py"), [str(out), "5"], timeout=300)
+    assert rc == 0
+    got = json.loads(out.read_text())
+    assert got["world"] == 2
+    cfg = preset("tiny-target", n_layers=1)
+    model = RefLlama(cfg, init_weights(cfg, 0, torch.float32))
+    for rid in range(5):
+        g = torch.Generator().manual_seed(1000 + rid)
+        assert got["merged"][str(rid)] == greedy_ar(model, torch.randint(0, cfg.vocab, (8,), generator=g).tolist(), 4, 32)

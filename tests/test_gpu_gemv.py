@@ -8,6 +8,8 @@ orders); appended KV rows must agree to bf16 rounding.  Relaunches are bit-ident
 
 import copy
 
+import numpy as np
+
 import pytest
 import torch
 
@@ -328,3 +330,64 @@ def test_kernel_timeline_trace_slots(cuda):
     s, r, t = [int(x) for x in buf[0, :3].cpu()]
     assert 0 < s <= r <= t, (s, r, t)
     torch.testing.assert_close(out, (X.float() @ W.float().T), rtol=2e-2, atol=2e-2)
+
+
+@pytest.mark.parametrize("hd,Hq,Hkv", [(128, 32, 8), (64, 32, 8)])
+def test_decode_attention_wide_tree_mask(hd, Hq, Hkv, cuda):
+    """cfg5-shaped draft level: 16 query rows (the newest level of a D8 W16 tree) over a 129-key
+    tree block (5 mask words) after a 300-token prefix; vs float64 attention over the visible keys."""
+    import ctypes as C
+    import math
+
+    from oracle import tree_ref as T
+    from paper_2512_23858_b200 import _lib as L
+
+    lib = L.lib()
+    rng = np.random.default_rng(hd)
+    t = T.Tree.root(0, 0.9)
+    for _ in range(8):
+        cands = {}
+        for f in t.levels()[-1]:
+            ps = np.sort(rng.dirichlet(np.ones(17))[:16])[::-1]
+            cands[f] = [(int(x), float(p)) for x, p in zip(rng.choice(10**5, 16, replace=False), ps)]
+        T.grow_step(t, lambda tr, n, kk: cands[n], 16, 16)
+    N = len(t)
+    assert N == 129
+    B, R, P, mw = 2, 16, 300, 5
+    rows_nodes = t.levels()[-1]
+    masks = []
+    for i in rows_nodes:
+        m = 0
+        for a in t.path(i):
+            m |= 1 << a
+        masks.append(m)
+    S = ((P + N + 63) // 64) * 64
+    g = torch.Generator(device="cuda").manual_seed(hd)
+    M = B * R
+    q = torch.randn(M, Hq, hd, device=cuda, generator=g).to(torch.bfloat16)
+    cache = torch.randn(B, 2, Hkv, S, hd, device=cuda, generator=g).to(torch.bfloat16)
+    qmask = torch.tensor([[(m >> (32 * w)) & 0xFFFFFFFF for w in range(mw)] for m in masks] * B,
+                         dtype=torch.int64).to(torch.int32).to(cuda)
+    bs = torch.full((B,), P, dtype=torch.int32, device=cuda)
+    bl = torch.full((B,), N, dtype=torch.int32, device=cuda)
+    out = torch.zeros(M, Hq, hd, dtype=torch.bfloat16, device=cuda)
+    mem = C.create_string_buffer(int(lib.ygg_attn_dec_plan_size()))
+    L.check(lib.ygg_attn_dec_plan_init(mem, q.data_ptr(), cache.data_ptr(), B, R, Hq, Hkv, hd, S))
+    ws = torch.zeros(int(lib.ygg_attn_dec_workspace_size(mem)) // 4 + 64, dtype=torch.float32, device=cuda)
+    scale = 1.0 / math.sqrt(hd)
+    L.check(lib.ygg_attn_dec_run(mem, bs.data_ptr(), bl.data_ptr(), qmask.data_ptr(), mw, scale, out.data_ptr(),
+                                 ws.data_ptr(), L.stream_ptr()))
+    torch.cuda.synchronize()
+    K = cache[:, 0].double().cpu()
+    Vt = cache[:, 1].double().cpu().reshape(B, Hkv, hd, S)
+    qd = q.double().cpu()
+    ref = torch.zeros(M, Hq, hd, dtype=torch.float64)
+    G = Hq // Hkv
+    for b in range(B):
+        for r, m in enumerate(masks):
+            vis = torch.tensor(list(range(P)) + [P + j for j in range(N) if (m >> j) & 1])
+            for h in range(Hq):
+                s = K[b, h // G, vis] @ qd[b * R + r, h] * scale
+                ref[b * R + r, h] = Vt[b, h // G][:, vis] @ torch.softmax(s, 0)
+    err = (out.double().cpu() - ref).abs().max()
+    assert err <= 2e-2 * ref.abs().max(), float(err)

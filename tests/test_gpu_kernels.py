@@ -213,6 +213,51 @@ def test_grow_levels_match_oracle(seed, cuda):
         np.testing.assert_array_equal(dt.masks_bool(b).numpy(), T.build_mask(r))
 
 
+@pytest.mark.parametrize("seed", range(3))
+def test_grow_wide_levels_match_oracle(seed, cuda):
+    """cfg5 shape: D8 W16 k16 -> 129-node trees (5 mask words), candidate lists mostly full."""
+    from paper_2512_23858_b200.device_tree import DeviceTrees
+
+    L = _lib()
+    rng = np.random.default_rng(50 + seed)
+    B, D, W, k = 2, 8, 16, 16
+    cap = 1 + D * W
+    dt = DeviceTrees(B, cap, cuda)
+    refs = [T.Tree.root(int(rng.integers(0, 99)), float(rng.uniform(0.2, 1.0))) for _ in range(B)]
+    dt.load_host([r.to_dict() for r in refs])
+    for _ in range(D):
+        Fmax = max(len(r.levels()[-1]) for r in refs)
+        ctok = torch.zeros(B, Fmax, k, dtype=torch.int32)
+        cprob = torch.zeros(B, Fmax, k, dtype=torch.float64)
+        cn = torch.zeros(B, Fmax, dtype=torch.int32)
+        per = []
+        for b, r in enumerate(refs):
+            fr = r.levels()[-1]
+            cands = []
+            for _f in fr:
+                ps = np.sort(rng.dirichlet(np.ones(k + 1))[:k])[::-1]
+                if rng.random() < 0.3:  # exact score ties across parents / ranks
+                    ps[1] = ps[0]
+                toks = rng.choice(128256, size=k, replace=False)
+                cands.append([(int(t), float(p)) for t, p in zip(toks, ps)])
+            per.append(dict(zip(fr, cands)))
+            for f, cl in enumerate(cands):
+                cn[b, f] = len(cl)
+                for j, (t, p) in enumerate(cl):
+                    ctok[b, f, j], cprob[b, f, j] = t, p
+        ctok_d, cprob_d, cn_d = ctok.cuda(), cprob.cuda(), cn.cuda()
+        L.check(L.lib().ygg_egt_grow_level(dt.struct, Fmax, k, W, ctok_d.data_ptr(), cprob_d.data_ptr(),
+                                           cn_d.data_ptr(), L.stream_ptr()))
+        torch.cuda.synchronize()
+        for b, r in enumerate(refs):
+            T.grow_step(r, lambda tr, node, kk, b=b: per[b][node], W, k)
+    got = dt.to_dicts()
+    for b, r in enumerate(refs):
+        assert len(r) == cap
+        assert got[b] == r.to_dict()
+        np.testing.assert_array_equal(dt.masks_bool(b).numpy(), T.build_mask(r))
+
+
 def test_grow_rejects_contract_violations(cuda):
     from paper_2512_23858_b200.device_tree import DeviceTrees
 
@@ -293,6 +338,52 @@ def test_knapsack_prune_matches_oracle(seed, cuda):
         assert float(sp[b]) == pr.speedup
         dp = T.Knapsack(t, T.path_products(t, probs[b, : len(t)].tolist()), max_verify)
         assert float(aal_cap[b]) == 1.0 + dp.best[0][dp.cap]
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_knapsack_prune_129_nodes_cap_64(seed, cuda):
+    """cfg3 / cfg5 shape: EGT trees of 129 nodes (D8 W16 / D16 W8), max_verify 64, surrogate gains."""
+    from paper_2512_23858_b200.device_tree import DeviceTrees
+
+    L = _lib()
+    rng = np.random.default_rng(300 + seed)
+    B = 3
+    D, W = (8, 16) if seed % 2 == 0 else (16, 8)
+    trees = []
+    for _ in range(B):
+        t = T.Tree.root(0, float(rng.uniform(0.5, 1.0)))
+        for _lvl in range(D):
+            cands = {}
+            for f in t.levels()[-1]:
+                ps = np.sort(rng.dirichlet(np.ones(9))[:8])[::-1]
+                cands[f] = [(int(x), float(p)) for x, p in zip(rng.choice(10**6, 8, replace=False), ps)]
+            T.grow_step(t, lambda tr, n, kk: cands[n], W, 8)
+        assert len(t) == 129
+        trees.append(t)
+    cap = 129
+    dprof = ((1, 400.0), (16, 410.0), (64, 430.0), (128, 470.0))
+    vprof = ((1, 2400.0), (17, 2430.0), (65, 2600.0), (129, 3100.0))
+    dt = DeviceTrees(B, cap, cuda)
+    dt.load_host([t.to_dict() for t in trees])
+    pp = torch.frombuffer(bytearray(L.profile_pair_bytes(dprof, vprof)), dtype=torch.uint8).cuda()
+    i32 = dict(dtype=torch.int32, device=cuda)
+    keep, new = torch.zeros(B, cap, **i32), torch.zeros(B, cap, **i32)
+    wv = torch.zeros(B, **i32)
+    aal = torch.zeros(B, dtype=torch.float64, device=cuda)
+    sp = torch.zeros_like(aal)
+    args = L.YggPruneArgs(64, D, W, 0)
+    L.check(L.lib().ygg_knapsack_prune(dt.struct, None, pp.data_ptr(), args, keep.data_ptr(), new.data_ptr(),
+                                       wv.data_ptr(), aal.data_ptr(), sp.data_ptr(), None, None, None, None,
+                                       L.stream_ptr()))
+    torch.cuda.synchronize()
+    for b, t in enumerate(trees):
+        pr = T.prune_verify(t, t.prob, dprof, vprof, D, W, 64)
+        assert tuple(i for i in keep[b].tolist() if i >= 0) == pr.kept
+        assert int(wv[b]) == pr.w_verify
+        assert float(aal[b]) == pr.expected_aal
+        assert float(sp[b]) == pr.speedup
+        m = {old: i for i, old in enumerate(pr.kept)}
+        assert [m.get(i, -1) for i in range(cap)] == new[b].tolist()
 
 
 # ---------------------------------------------------------------------------

@@ -37,7 +37,7 @@ def test_abi_struct_layouts_match_header(tmp_path):
     structs = {"ygg_tree": _lib.YggTree, "ygg_seq": _lib.YggSeq, "ygg_profile": _lib.YggProfile,
                "ygg_profile_pair": _lib.YggProfilePair, "ygg_prune_args": _lib.YggPruneArgs,
                "ygg_epilogue": _lib.YggEpilogue, "ygg_gemv_epilogue": _lib.YggGemvEpilogue,
-               "ygg_mk_desc": _lib.YggMkDesc, "ygg_l2_region": _lib.YggL2Region}
+               "ygg_l2_region": _lib.YggL2Region}
     lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "ygg.h"', "int main(void) {"]
     for cname, py in structs.items():
         lines.append(f'  printf("{cname} %zu\\n", sizeof({cname}));')

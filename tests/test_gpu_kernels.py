@@ -237,6 +237,7 @@ def test_grow_wide_levels_match_oracle(seed, cuda):
             for _f in fr:
                 ps = np.sort(rng.dirichlet(np.ones(k + 1))[:k])[::-1]
                 if rng.random() < 0.3:  # exact score ties across parents / ranks
+                    ps = ps * 0.5
                     ps[1] = ps[0]
                 toks = rng.choice(128256, size=k, replace=False)
                 cands.append([(int(t), float(p)) for t, p in zip(toks, ps)])
@@ -355,9 +356,9 @@ def test_knapsack_prune_129_nodes_cap_64(seed, cuda):
         for _lvl in range(D):
             cands = {}
             for f in t.levels()[-1]:
-                ps = np.sort(rng.dirichlet(np.ones(9))[:8])[::-1]
-                cands[f] = [(int(x), float(p)) for x, p in zip(rng.choice(10**6, 8, replace=False), ps)]
-            T.grow_step(t, lambda tr, n, kk: cands[n], W, 8)
+                ps = np.sort(rng.dirichlet(np.ones(17))[:16])[::-1]
+                cands[f] = [(int(x), float(p)) for x, p in zip(rng.choice(10**6, 16, replace=False), ps)]
+            T.grow_step(t, lambda tr, n, kk: cands[n], W, 16)
         assert len(t) == 129
         trees.append(t)
     cap = 129

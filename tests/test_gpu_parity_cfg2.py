@@ -14,7 +14,8 @@ bf16 and the oracle gets the same rounded values in fp32, so only the kernels' a
 (b) the bf16 verify pass at T = 50 rows with a real EGT (D6 W8 k8) ancestor mask on the tcgen05
     GEMM + epilogues + decode-attention path: logits within 2e-2, argmax equal where the margin allows;
 (c) the fp32 speculative step over 5 steps vs RefSpecDecoder: grown trees, kept sets, accepted paths
-    and bonus tokens bit-exact (probabilities within 1e-4 relative: f32 logits summed in another order).
+    and bonus tokens bit-exact; drafted probabilities within 5e-3 relative (f32 logits of magnitude
+    ~50 summed over K = 4096 in another order differ by ~1e-5 relative, i.e. ~5e-4 in the logit).
 """
 
 import numpy as np
@@ -144,23 +145,30 @@ def test_cfg2_draft_gemv_pass_vs_oracle(pair, cuda):
     # appended KV of the tree slots (K rows and V^T columns) vs the oracle cache
     for li in range(dc.n_layers):
         kg = cache[li, 0, 0].float().cpu()[:, P0 + 1 : P0 + 1 + n, :]
-        vg = cache[li, 0, 1].float().cpu()[:, :, P0 + 1 : P0 + 1 + n].transpose(1, 2)
+        vt = cache[li, 0, 1].float().cpu().reshape(dc.n_kv_heads, dc.head_dim, S)  # V^T rows [hd][S]
+        vg = vt[:, :, P0 + 1 : P0 + 1 + n].transpose(1, 2)
         assert _rel_err(kg, rc.k[li][:, P0 + 1 : P0 + 1 + n]) <= 2e-2
         assert _rel_err(vg, rc.v[li][:, P0 + 1 : P0 + 1 + n]) <= 2e-2
-    # fused top-k: exactly the oracle's softmax top-k of the GPU logits, and the oracle's top-k of its
-    # own logits wherever the top-(k+1) gaps exceed twice this row's logit error
+    # fused top-k: exactly the oracle's softmax top-k of the GPU logits; against the oracle's own
+    # logits, every rank whose separation from its neighbours exceeds twice this row's logit error
+    # must hold the same token, and every token clearly inside the oracle's top-k must be drafted
     checked = 0
     for r in range(len(rows_b)):
         mine = T.topk_softmax(lb[r].numpy(), k)
         assert ctok[r].tolist() == [t for t, _ in mine]
         np.testing.assert_allclose(cprob[r].cpu().numpy(), [p for _, p in mine], rtol=1e-9, atol=1e-12)
         err = float((lb[r] - rb[r]).abs().max())
-        top = np.sort(rb[r].numpy())[::-1][: k + 1]
-        if np.all(np.diff(-top) > 2 * err):
-            theirs = T.topk_softmax(rb[r].numpy(), k)
-            assert [t for t, _ in theirs] == ctok[r].tolist()
-            checked += 1
-    assert checked >= 1
+        ref_vals, ref_idx = torch.sort(rb[r], descending=True)
+        vals, idx = ref_vals[: k + 1].numpy(), ref_idx[: k + 1].tolist()
+        for j in range(k):
+            below = vals[j] - vals[j + 1]
+            above = vals[j - 1] - vals[j] if j > 0 else np.inf
+            if min(below, above) > 2 * err:
+                assert ctok[r, j].item() == idx[j], (r, j)
+                checked += 1
+            if vals[j] - vals[k] > 2 * err:
+                assert idx[j] in ctok[r].tolist(), (r, j)
+    assert checked >= len(rows_b)  # at least one separated rank per row on average (top-1 is)
 
 
 def test_cfg2_verify_pass_vs_oracle(pair, cuda):
@@ -248,7 +256,7 @@ def test_cfg2_fp32_step_trace_vs_oracle(pair, cuda):
         assert [x["token"] for x in grown["nodes"]] == [x["token"] for x in rec["tree"]["nodes"]], f"step {i}"
         assert [x["parent"] for x in grown["nodes"]] == [x["parent"] for x in rec["tree"]["nodes"]], f"step {i}"
         for a, b in zip(grown["nodes"], rec["tree"]["nodes"]):
-            assert abs(a["prob"] - b["prob"]) <= 1e-4 * max(b["prob"], 1e-6), f"step {i}"
+            assert abs(a["prob"] - b["prob"]) <= 5e-3 * max(b["prob"], 1e-6), f"step {i}"
         assert [x for x in sd.keep_idx[0].tolist() if x >= 0] == rec["kept"], f"step {i}"
         assert sd.path[0, : int(sd.path_len[0])].tolist() == rec["path"], f"step {i}"
         assert int(sd.bonus[0]) == rec["bonus"], f"step {i}"

@@ -306,6 +306,7 @@ int ygg_stamp(unsigned long long* slot, ygg_stream_t stream);
  * return from the grid-dependency wait, last CTA end, kernel checkpoints 3..7 (latest over CTAs)},
  * written with %globaltimer atomics; the caller initialises fields 0 and 1 to ~0, the rest to 0.  Arming with slots = 0 disarms.
  * ygg_trace_used returns the number of slots taken and copies their kernel ids. */
+/* The armed state is per host thread (thread_local): only launches issued by the arming thread are traced. */
 int ygg_trace_arm(unsigned long long* buf, int slots);
 int ygg_trace_used(int* kernel_ids, int cap);
 
@@ -355,10 +356,11 @@ int ygg_gemv_run(const void* plan, const ygg_gemv_epilogue* epi, ygg_stream_t st
  * One CTA per (kv head, request, 64-row tile of (token, head) query rows) walks every visible key
  * chunk with an online softmax (no split-KV partials, no combine launch); prefix keys always visible,
  * block keys by the row's tree-mask bits (causal when mask_words == 0).  q [B*T][Hq][hd]; cache_layer as for ygg_attn_plan_init;
- * out [B*T][Hq][hd] bf16. */
+ * out [B*T][Hq][hd] bf16.  kvsplit = CTAs per cluster splitting the keys (0 = automatic: as many as
+ * fit one wave, at most 4; capped at 4 for hd 128 and 8 for hd 64). */
 size_t ygg_attn_dec_plan_size(void);
 int ygg_attn_dec_plan_init(void* plan, const void* q, const void* cache_layer, int B, int T, int Hq, int Hkv, int hd,
-                           int S);
+                           int S, int kvsplit);
 /* Launch order contract (programmatic dependent launch): K / V chunks wholly inside the committed
  * prefix (keys < blk_start) and blk_start / blk_len are read BEFORE the grid-dependency wait, so they
  * must have been written at least two kernels earlier on the stream and the kernel immediately
@@ -379,53 +381,6 @@ int ygg_attn_dec_set_gemv_prefetch(void* plan, const void* gemv_plan);
 int ygg_attn_dec_run(const void* plan, const int32_t* blk_start, const int32_t* blk_len, const uint32_t* qmask,
                      int mask_words, float scale, void* out, void* workspace, ygg_stream_t stream);
 
-/* ---------------- Persistent forward (bf16, decode-shaped: B*T <= 128 rows) ----------------
- * One launch runs a whole draft or verify forward (the passes the reference prices as
- * latency_at(drafter|verifier, width), simulator.py:202-214): embed, then per layer
- * QKV GEMM -> RoPE/KV append -> tcgen05 tree attention -> combine -> O GEMM -> residual ->
- * gate|up GEMM -> SwiGLU -> down GEMM -> residual, then the LM head.  One CTA per SM; phases
- * are separated by a grid-wide arrival counter, and the weight stream (TMA into a smem ring
- * plus an L2 prefetch look-ahead) runs ahead across phase boundaries, so HBM never waits on
- * the dependency chain.  RMSNorm gains must be folded into wqkv / wgu / lm_head (the per-row
- * rstd is applied in the consumer epilogue).  Weights are row-major [N, K] bf16. */
-typedef struct {
-  int32_t n_layers, d_model, n_heads, n_kv_heads, head_dim, ffn, vocab;
-  int32_t B, T;        /* requests, rows per request; M = B*T <= 128 */
-  int32_t S;           /* KV capacity per request (multiple of 64) */
-  int32_t mask_words;  /* tree-mask words per row (0 = causal block) */
-  float eps, attn_scale;
-  const void* const* wqkv; /* host arrays of n_layers device pointers */
-  const void* const* wo;
-  const void* const* wgu;
-  const void* const* wdown;
-  const void* embed;   /* [V, d] */
-  const void* lm_head; /* [V, d] */
-  const int32_t* tokens; const int32_t* pos; const int32_t* slot; const int32_t* req; /* [M] */
-  const uint32_t* qmask; /* [M, mask_words] */
-  const int32_t* blk_start; const int32_t* blk_len; /* [B] */
-  const float* rope_cs;  /* [positions, hd/2, 2] */
-  void* cache;           /* [layers][B][2][Hkv][S][hd] (kv=1 holds V^T) */
-  long long layer_stride;/* elements */
-  float* resid;          /* [M, d] f32 */
-  void* hb;              /* [M, d] bf16 (un-normalised residual = GEMM input) */
-  void* q;               /* [M, Hq*hd] bf16 */
-  void* attn;            /* [M, Hq*hd] bf16 */
-  void* mlp;             /* [M, ffn] bf16 */
-  float* logits;         /* [M, V] f32 */
-  float* ss;             /* [2][d/128][M] per-tile sums of squares */
-  float* ws;             /* two stream-K partial buffers, ws_bytes total */
-  float* attn_part;      /* attention chunk partials, attn_part_bytes */
-  int32_t num_ctas;      /* 0 = one per SM */
-  int32_t lookahead;     /* L2 prefetch depth in weight tiles per CTA (<0 = default) */
-  void* dbg;             /* optional u64 [grid][phases]: %globaltimer at each phase end (profiling) */
-} ygg_mk_desc;
-
-size_t ygg_mk_plan_size(void);
-/* Device table / workspace sizes for a descriptor (pointers may be NULL). */
-int ygg_mk_query(const ygg_mk_desc* desc, size_t* table_bytes, size_t* ws_bytes, size_t* attn_part_bytes);
-/* Builds the phase program + TMA maps into table_dev (device memory, >= table_bytes). */
-int ygg_mk_plan_init(void* plan, const ygg_mk_desc* desc, void* table_dev, size_t table_bytes);
-int ygg_mk_run(const void* plan, ygg_stream_t stream);
 
 #ifdef __cplusplus
 }

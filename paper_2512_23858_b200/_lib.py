@@ -97,21 +97,6 @@ class YggEpilogue(C.Structure):
     ]
 
 
-class YggMkDesc(C.Structure):
-    """ygg_mk_desc (include/ygg.h): persistent-forward descriptor."""
-
-    _fields_ = [
-        ("n_layers", C.c_int32), ("d_model", C.c_int32), ("n_heads", C.c_int32), ("n_kv_heads", C.c_int32),
-        ("head_dim", C.c_int32), ("ffn", C.c_int32), ("vocab", C.c_int32), ("B", C.c_int32), ("T", C.c_int32),
-        ("S", C.c_int32), ("mask_words", C.c_int32), ("eps", C.c_float), ("attn_scale", C.c_float),
-        ("wqkv", C.POINTER(vp)), ("wo", C.POINTER(vp)), ("wgu", C.POINTER(vp)), ("wdown", C.POINTER(vp)),
-        ("embed", vp), ("lm_head", vp), ("tokens", vp), ("pos", vp), ("slot", vp), ("req", vp), ("qmask", vp),
-        ("blk_start", vp), ("blk_len", vp), ("rope_cs", vp), ("cache", vp), ("layer_stride", C.c_longlong),
-        ("resid", vp), ("hb", vp), ("q", vp), ("attn", vp), ("mlp", vp), ("logits", vp), ("ss", vp), ("ws", vp),
-        ("attn_part", vp), ("num_ctas", C.c_int32), ("lookahead", C.c_int32), ("dbg", vp),
-    ]
-
-
 class YggGemvEpilogue(C.Structure):
     """ygg_gemv_epilogue (include/ygg.h)."""
 
@@ -183,7 +168,7 @@ _SIGS: dict[str, tuple] = {
     "ygg_trace_arm": (C.c_int, [vp, C.c_int]),
     "ygg_trace_used": (C.c_int, [vp, C.c_int]),
     "ygg_attn_dec_plan_size": (C.c_size_t, []),
-    "ygg_attn_dec_plan_init": (C.c_int, [vp, vp, vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int]),
+    "ygg_attn_dec_plan_init": (C.c_int, [vp, vp, vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int]),
     "ygg_attn_dec_workspace_size": (C.c_size_t, [vp]),
     "ygg_attn_dec_run": (C.c_int, [vp, vp, vp, vp, C.c_int, C.c_float, vp, vp, vp]),
     "ygg_gemv_plan_size": (C.c_size_t, []),
@@ -197,11 +182,6 @@ _SIGS: dict[str, tuple] = {
     "ygg_topk_partial_bytes": (C.c_size_t, [C.c_int, C.c_int]),
     "ygg_topk_merge": (C.c_int, [vp, C.c_int, C.c_int, C.c_int, vp, vp, vp, vp]),
     "ygg_topk_merge_l2": (C.c_int, [vp, C.c_int, C.c_int, C.c_int, vp, vp, vp, vp, C.c_int, vp]),
-    "ygg_mk_plan_size": (C.c_size_t, []),
-    "ygg_mk_query": (C.c_int, [C.POINTER(YggMkDesc), C.POINTER(C.c_size_t), C.POINTER(C.c_size_t),
-                               C.POINTER(C.c_size_t)]),
-    "ygg_mk_plan_init": (C.c_int, [vp, C.POINTER(YggMkDesc), vp, C.c_size_t]),
-    "ygg_mk_run": (C.c_int, [vp, vp]),
 }
 
 EXPORTED = tuple(_SIGS)
@@ -212,7 +192,7 @@ KERNELS_PER_CALL = {
     "ygg_tree_subtree": 1, "ygg_path_products": 1, "ygg_accept": 1, "ygg_kv_compact": 1, "ygg_gemm_run": 1, "ygg_gemm_fused": 1, "ygg_embed_fused": 1, "ygg_epi_store": 1,
     "ygg_epi_residual_norm": 1, "ygg_epi_swiglu": 1, "ygg_epi_qkv_rope": 1, "ygg_embed": 1, "ygg_rmsnorm": 1, "ygg_embed_rmsnorm": 1,
     "ygg_attention": 1, "ygg_attention_tc": 2, "ygg_row_stats": 1, "ygg_pass0_inputs": 1, "ygg_init_roots": 1, "ygg_level_inputs": 1,
-    "ygg_verify_inputs": 1, "ygg_commit": 1, "ygg_stamp": 1, "ygg_mk_run": 1, "ygg_gemv_run": 1, "ygg_attn_dec_run": 1, "ygg_topk_merge": 1, "ygg_topk_merge_l2": 1,
+    "ygg_verify_inputs": 1, "ygg_commit": 1, "ygg_stamp": 1, "ygg_gemv_run": 1, "ygg_attn_dec_run": 1, "ygg_topk_merge": 1, "ygg_topk_merge_l2": 1,
 }
 launches = {"count": 0}
 

@@ -16,10 +16,13 @@ int ygg_fail(int code, const char* fmt, ...) {
   return code;
 }
 
+// Kernel-timeline tracing (profiling only) is armed per host thread: the state is thread_local, so
+// one thread's armed buffer never receives another thread's launches and the library keeps no
+// process-wide mutable state.
 namespace {
-unsigned long long* g_trace = nullptr;
-int g_trace_cap = 0, g_trace_used = 0;
-int g_trace_ids[4096];
+thread_local unsigned long long* g_trace = nullptr;
+thread_local int g_trace_cap = 0, g_trace_used = 0;
+thread_local int g_trace_ids[4096];
 }  // namespace
 
 unsigned long long* trace_next(int kernel_id) {
@@ -34,7 +37,6 @@ int ygg_prepare_tree(void);
 int ygg_prepare_gemm(void);
 int ygg_prepare_layers(void);
 int ygg_prepare_attn_tc(void);
-int ygg_prepare_mk(void);
 int ygg_prepare_gemv(void);
 int ygg_prepare_attn_dec(void);
 
@@ -72,7 +74,6 @@ int ygg_device_check(int* num_sms, int* cc_major, int* cc_minor) {
   if (int rc = ygg_prepare_gemm()) return rc;
   if (int rc = ygg_prepare_layers()) return rc;
   if (int rc = ygg_prepare_attn_tc()) return rc;
-  if (int rc = ygg_prepare_mk()) return rc;
   if (int rc = ygg_prepare_gemv()) return rc;
   if (int rc = ygg_prepare_attn_dec()) return rc;
   return YGG_OK;

@@ -959,27 +959,19 @@ int ygg_gemm_plan_init(void* plan_mem, int dtype, const void* W, const void* X, 
     g->units = static_cast<long long>(g->tiles) * g->kb;
     // Default grid: every SM, but never fewer than 8 k-blocks (128 KB of weights) per CTA, which
     // bounds how many CTAs share (and must later reduce) one output tile for small layers.
-    static const int min_units = [] {
-      const char* s = getenv("YGG_GEMM_MIN_UNITS");
-      const int v = s ? atoi(s) : 8;
-      return v < 1 ? 1 : v;
-    }();
+    constexpr int min_units = 8;
     if (num_ctas <= 0)
       num_ctas = static_cast<int>(std::max(1LL, std::min<long long>(kNumSMs, g->units / min_units)));
     if (num_ctas > g->units) num_ctas = static_cast<int>(g->units);
     g->num_ctas = num_ctas;
     const int stage_bytes = kBM * kBK * 2 + g->BN * kBK * 2;
-    // Shared-memory budget: YGG_GEMM_SMEM_KB (default 190: one CTA per SM with a 7-stage ring at
+    // Shared-memory budget: 190 KB (one CTA per SM with a 7-stage ring at
     // BN = 64; the small epilogue CTAs still co-reside under programmatic dependent launch, the
     // decode attention of the verify (up to 190 KB itself) does not either way).  Same-box sweeps
     // of the cfg2 verify forward — with the split-KV tcgen05 attention: 113 KB 4.37 ms, 135 KB
     // 4.24, 150 KB 4.22, 165 KB 4.22, 190 KB 4.25, 227 KB 4.47; with the decode attention: 120 KB
     // 3.76, 150 KB 3.605, 190 KB 3.586, 216 KB 3.605.
-    static const int smem_kb = [] {
-      const char* s = getenv("YGG_GEMM_SMEM_KB");
-      int v = s ? atoi(s) : 190;
-      return v < 48 ? 48 : (v > 227 ? 227 : v);
-    }();
+    constexpr int smem_kb = 190;
     g->stages = std::min(12, (smem_kb * 1024 - kSmemExtra) / stage_bytes);
     YGG_CHECK_ARG(g->stages >= 2, "tile too large for shared memory");
     int cols = 32;
@@ -1048,10 +1040,7 @@ static int gemm_launch(const GemmPlan* g, float* workspace, const ygg_epilogue* 
     p.dp_per_cta = g->dp_per_cta;
     p.stages = g->stages;
     p.tmem_cols = g->tmem_cols;
-    {  // A/B knob: YGG_GEMM_PREWAIT = stages streamed before the dependency wait (default: all)
-      static const int pw = [] { const char* e = getenv("YGG_GEMM_PREWAIT"); return e ? atoi(e) : 1 << 30; }();
-      p.prewait = pw < 0 ? 0 : (pw < g->stages ? pw : g->stages);
-    }
+    p.prewait = g->stages;  // every weight stage is streamed before the grid-dependency wait
     p.units = g->units;
     p.seg_first = g->seg_table;
     p.seg_base = g->seg_table + g->tiles + 1;

@@ -637,21 +637,13 @@ int ygg_gemv_plan_init(void* plan, const void* W, const void* X, int M, int N, i
   // Two CTAs per SM by default (~110 KB of ring each): a 2048-row matmul's 128-192 blocks fit one
   // wave with one block per CTA, and the next kernel's CTAs are co-resident with this one's tail,
   // so under programmatic dependent launch their weight ring fills while this kernel drains.
-  static const int smem_kb = [] {
-    const char* s = getenv("YGG_GEMV_SMEM_KB");
-    const int v = s ? atoi(s) : 110;
-    return v < 64 ? 64 : (v > 227 ? 227 : v);
-  }();
+  constexpr int smem_kb = 110;
   int per_sm = smem_kb <= 113 ? 2 : 1;
   p.grid = num_ctas > 0 ? num_ctas : std::min(sms * per_sm, p.nblk);
   // A matrix with at most one block per SM (o / down projections: 128 blocks of 16 x K) is bound by
-  // one CTA's bytes in flight: give that CTA the whole SM's ring (YGG_GEMV_SOLO_KB, default 224 =
-  // 9 stages; same-box draft pass 0.593 ms at 200 KB, 0.591 at 224).
-  static const int solo_kb = [] {
-    const char* s = getenv("YGG_GEMV_SOLO_KB");
-    const int v = s ? atoi(s) : 224;
-    return v < 64 ? 64 : (v > 227 ? 227 : v);
-  }();
+  // one CTA's bytes in flight: give that CTA the whole SM's ring (224 KB = 9 stages; same-box draft
+  // pass 0.593 ms at 200 KB, 0.591 at 224).
+  constexpr int solo_kb = 224;
   const int budget_kb = (num_ctas <= 0 && p.nblk <= sms) ? solo_kb : smem_kb;
   const size_t stage = static_cast<size_t>(kRows) * kStageK * 2 + static_cast<size_t>(p.xrows) * kStageK * 2;
   const size_t fixed = 1024 + 16 * 2 * 8 + kMaxTok * 16 + 2 * kCompute * 2 * 4 * 32 * 4 + 64;

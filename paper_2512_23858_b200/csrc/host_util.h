@@ -19,11 +19,8 @@ int ygg_fail(int code, const char* fmt, ...);
 // Next slot of the armed kernel-timeline buffer (ygg_trace_arm), tagged with kernel_id, or nullptr.
 unsigned long long* trace_next(int kernel_id);
 
-// Programmatic dependent launch is on unless YGG_NO_PDL is set (A/B measurements).
-inline int pdl_enabled() {
-  static const int on = std::getenv("YGG_NO_PDL") ? 0 : 1;
-  return on;
-}
+// Every launch uses programmatic dependent launch (griddepcontrol in the kernels).
+inline int pdl_enabled() { return 1; }
 
 template <typename Kernel, typename... Args>
 int launch_pdl(Kernel kernel, dim3 grid, dim3 block, size_t smem, cudaStream_t stream, Args... args) {

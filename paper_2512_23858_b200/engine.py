@@ -20,8 +20,6 @@ shape (D, W, max_verify, B) as a CUDA graph and replayed with no host synchronis
 
 from __future__ import annotations
 
-import os
-import time
 from dataclasses import dataclass
 
 import numpy as np
@@ -31,6 +29,7 @@ from . import _lib as L
 from .device_tree import DeviceTrees, SeqState
 from .forward import Forward, new_cache, prefill_causal
 from .model import ModelConfig
+from .plan import ForwardPlan
 
 GREEDY, SAMPLE = "greedy", "sample"
 
@@ -70,6 +69,7 @@ class SpecDecoder:
         profiles=None,
         prefill_len: int = 0,
         device="cuda",
+        plan: ForwardPlan | None = None,
     ):
         L.require_device()
         if target_cfg.vocab != draft_cfg.vocab:
@@ -97,8 +97,9 @@ class SpecDecoder:
         self.dcache = new_cache(draft_cfg, batch, self.S, act_dtype, dev)
         tmw = max(1, (self.T + 31) // 32)
         dmw = max(1, (self.tree_cap + 31) // 32)
-        self.draft = Forward(draft_cfg, draft_w, self.dcache, batch, self.R, dmw, act_dtype)
-        self.verify = Forward(target_cfg, target_w, self.tcache, batch, self.T, tmw, act_dtype)
+        self.plan = plan
+        self.draft = Forward(draft_cfg, draft_w, self.dcache, batch, self.R, dmw, act_dtype, plan=plan)
+        self.verify = Forward(target_cfg, target_w, self.tcache, batch, self.T, tmw, act_dtype, plan=plan)
         self.grown = DeviceTrees(batch, self.tree_cap, dev)
         self.vtree = DeviceTrees(batch, self.vcap, dev)
         i32 = dict(dtype=torch.int32, device=dev)
@@ -111,21 +112,6 @@ class SpecDecoder:
                                    dtype=torch.uint8, device=dev)
         # Draft top-k straight from the LM-head GEMV epilogue (per-CTA partials + one merge launch).
         self.topk_fused = self.draft.fuse_topk(k)
-        # A/B knobs (off): the merge pulling the next pass's first weights into L2 while the tree
-        # kernels leave HBM idle.  Measured slower — 37 MB issued from the merge's 8 CTAs occupies
-        # those SMs' TMA units well into the next pass (+250 us per step; verify variant +20-50 us).
-        self._l2_next = {}
-        if self.topk_fused:
-            def reg(W, mb):
-                n = min(int(mb * (1 << 20)), W.numel() * W.element_size())
-                return L.YggL2Region(W.data_ptr(), n)
-            dl0, tl0 = draft_w["layers"][0], target_w["layers"][0]
-            gmb = float(os.environ.get("YGG_L2PF_NEXT_DRAFT_MB", "0"))
-            vmb = float(os.environ.get("YGG_L2PF_NEXT_VERIFY_MB", "0"))
-            dr = [reg(dl0["wqkv"], gmb and 64), reg(dl0["wo"], gmb and 64), reg(dl0["wgu"], gmb)] if gmb else []
-            vr = [reg(tl0["wqkv"], vmb)] if vmb else []
-            self._l2_next = {"draft": (L.YggL2Region * 4)(*dr), "n_draft": len(dr),
-                             "verify": (L.YggL2Region * 4)(*vr), "n_verify": len(vr)}
         self.keep_idx = torch.zeros(batch, self.tree_cap, **i32)
         self.new_idx = torch.zeros(batch, self.tree_cap, **i32)
         self.w_verify = torch.zeros(batch, **i32)
@@ -198,14 +184,12 @@ class SpecDecoder:
         self.seq.gen_limit.fill_(2**31 - 1)
 
     # ------------------------------------------------------------------
-    def _draft_topk(self, rows: int, k: int, s, next_pass: str = "draft") -> None:
+    def _draft_topk(self, rows: int, k: int, s) -> None:
         """Candidates of every draft row (DrafterDistribution.candidates, egt.py:65-80)."""
         lib, dr = L.lib(), self.draft
         if self.topk_fused:
-            regs = self._l2_next.get(next_pass)
-            n = self._l2_next.get("n_" + next_pass, 0)
-            L.check(lib.ygg_topk_merge_l2(dr.topk_part.data_ptr(), rows, dr.topk_chunks, k, self.cand_tok.data_ptr(),
-                                          self.cand_prob.data_ptr(), None, regs if n else None, n, s))
+            L.check(lib.ygg_topk_merge(dr.topk_part.data_ptr(), rows, dr.topk_chunks, k, self.cand_tok.data_ptr(),
+                                       self.cand_prob.data_ptr(), None, s))
         else:
             L.check(lib.ygg_topk_softmax(dr.logits.data_ptr(), L.YGG_F32, rows, self.dc.vocab, self.dc.vocab, k, 1.0,
                                          self.cand_tok.data_ptr(), self.cand_prob.data_ptr(), None,
@@ -238,7 +222,7 @@ class SpecDecoder:
                                      dr.slot.data_ptr(), dr.req.data_ptr(), dr.qmask.data_ptr(), dr.mask_words,
                                      dr.blk_start.data_ptr(), dr.blk_len.data_ptr(), self.cand_n.data_ptr(), s))
             dr.run(stream)
-            self._draft_topk(rows, k, s, "verify" if lvl == D - 1 else "draft")
+            self._draft_topk(rows, k, s)
             chk(lib.ygg_egt_grow_level(g.struct, self.R, k, W, self.cand_tok.data_ptr(), self.cand_prob.data_ptr(),
                                        self.cand_n.data_ptr(), s))
         stamp(2)
@@ -375,7 +359,7 @@ class ARDecoder:
     for the lossless-greedy identity: speculative output == AR output)."""
 
     def __init__(self, cfg: ModelConfig, w: dict, batch: int = 1, max_seq: int = 2048,
-                 act_dtype: torch.dtype = torch.bfloat16, device="cuda"):
+                 act_dtype: torch.dtype = torch.bfloat16, device="cuda", plan: ForwardPlan | None = None):
         L.require_device()
         self.cfg, self.w, self.B = cfg, w, batch
         self.S = (max_seq + 8 + 63) // 64 * 64
@@ -385,7 +369,7 @@ class ARDecoder:
         # AR is the oracle of the lossless-greedy identity, so it runs the same kernel families as the
         # verify pass (stream-K GEMM and the cluster decode attention of tree passes that fit one
         # wave), not the draft's GEMV.
-        self.fwd = Forward(cfg, w, self.cache, batch, 1, 1, act_dtype, gemv=False)
+        self.fwd = Forward(cfg, w, self.cache, batch, 1, 1, act_dtype, gemv=False, plan=plan)
         self.fwd.qmask.fill_(1)
         self.argmax = torch.zeros(batch, dtype=torch.int32, device=self.dev)
         self.P = torch.zeros(batch, dtype=torch.int32, device=self.dev)

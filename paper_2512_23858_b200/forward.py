@@ -10,7 +10,7 @@ bf16 default (10 launches per layer): tcgen05 stream-K GEMM writing f32 partials
 vectorised epilogue kernel (RoPE + KV append from a host RoPE table / residual + cluster-DSMEM
 RMSNorm / SwiGLU), and the tcgen05 split-KV tree attention + combine.
 
-bf16 with YGG_FUSED=1 (6 launches per layer): every epilogue fused into its GEMM —
+bf16 with ForwardPlan(fused_epilogues=True) (6 launches per layer): every epilogue fused into its GEMM —
   GEMM(qkv, x=hb)  + rstd + RoPE + q / KV-cache append      (YGG_EPI_QKV_ROPE)
   GEMM(o)          + residual add, hb, per-tile sum-of-squares (YGG_EPI_RESID)
   GEMM(gate|up, x=hb) + rstd + SwiGLU                        (YGG_EPI_SWIGLU)
@@ -18,12 +18,6 @@ bf16 with YGG_FUSED=1 (6 launches per layer): every epilogue fused into its GEMM
 with RMSNorm gains folded into the next weights (model.prepare_fused_) and the per-token rstd
 applied by the consuming GEMM's epilogue.  Same results; today slower, because the split-tile
 fixups sit on each GEMM's critical path.
-
-bf16 persistent (B*R <= 128; YGG_MK=1 or persistent=True): the whole pass is ONE launch of
-the persistent forward kernel (csrc/mk.cu) — one CTA per SM walking a static phase program with
-grid-wide arrival counters between phases while the weight stream (TMA ring + L2 prefetch
-look-ahead) runs ahead across them.  RMSNorm gains are folded into the next weight
-(model.prepare_folded_) and the per-row rstd is applied by the consuming epilogue phase.
 
 f32 (parity path): SIMT GEMM + the same separate epilogue kernels + SIMT attention.  The
 residual stream is f32 in every path.
@@ -33,15 +27,12 @@ from __future__ import annotations
 
 import ctypes as C
 import math
-import os
 
 import torch
 
 from . import _lib as L
-from .model import ModelConfig, prepare_folded_, prepare_fused_, rope_table
-
-
-_KNOCKOUT = set(filter(None, os.environ.get("YGG_KO", "").split(",")))
+from .model import ModelConfig, prepare_fused_, rope_table
+from .plan import DEFAULT, ForwardPlan
 
 
 class GemmPlan:
@@ -103,34 +94,32 @@ class Forward:
         act_dtype: torch.dtype,
         logits: bool = True,
         num_ctas: int = 0,
-        persistent: bool | None = None,
         gemv: bool | None = None,
         decode_attn: bool | None = None,
+        plan: ForwardPlan | None = None,
     ):
         L.require_device()
+        plan = plan or DEFAULT
+        self.plan = plan
         self.cfg, self.cache = cfg, cache
         self.B, self.R, self.M = B, R, B * R
         self.mask_words = mask_words
         self.act_dtype = act_dtype
         self.act = L.dtype_code(act_dtype)
         # bf16 default: plain stream-K GEMM + separate vectorised epilogue kernels (faster today);
-        # YGG_FUSED=1 selects the fused-epilogue GEMMs (same results, tested).
+        # plan.fused_epilogues selects the fused-epilogue GEMMs (same results, tested).
         bf16 = act_dtype == torch.bfloat16
         if gemv is None:
-            gemv = os.environ.get("YGG_GEMV", "1") != "0"
+            gemv = True if plan.gemv is None else plan.gemv
+        if decode_attn is None:
+            decode_attn = True if plan.decode_attn is None else plan.decode_attn
         # Decode passes of <= 16 rows: row-block GEMV with fused epilogues (csrc/gemv.cu); needs the
         # fused weight layout, which then also routes every other bf16 forward on these weights
         # (prefill, verify) through the fused-epilogue GEMM.
         self.gemv = bool(gemv) and bf16 and logits and B * R <= 16 and mask_words <= L.MAX_MASK_WORDS
-        self.fused = bf16 and (bool(os.environ.get("YGG_FUSED")) or self.gemv or weights.get("_layout") == "fused")
-        if persistent is None:
-            persistent = os.environ.get("YGG_MK", "0") != "0"
-        self.mk = (persistent and bf16 and not self.fused and logits and B * R <= 128
-                   and mask_words <= L.MAX_MASK_WORDS)
+        self.fused = bf16 and (plan.fused_epilogues or self.gemv or weights.get("_layout") == "fused")
         if self.fused:
             prepare_fused_(weights, cfg)
-        elif self.mk:
-            prepare_folded_(weights, cfg)
         self.w = weights
         dev = cache.device
         M, d = self.M, cfg.d_model
@@ -182,19 +171,17 @@ class Forward:
         # combine).  Prefill and wide batched verifies keep the split-KV tcgen05 kernel.
         self.ad_plans = None
         gh = cfg.n_heads // cfg.n_kv_heads
-        force_dec = os.environ.get("YGG_ATTN_DEC") == "2"  # A/B: decode attention for every tree pass
-        if decode_attn is None:
-            decode_attn = os.environ.get("YGG_ATTN_DEC", "1") != "0"
         tree_fits = mask_words > 0 and B * cfg.n_kv_heads * ((R * gh + 63) // 64) <= 148
         if (decode_attn and act_dtype == torch.bfloat16 and mask_words <= L.MAX_MASK_WORDS
-                and (R * gh <= 64 or tree_fits or (force_dec and mask_words > 0))):
+                and (R * gh <= 64 or tree_fits)):
             lib = L.lib()
             es = cache.element_size()
             self.ad_plans = []
             for li in range(cfg.n_layers):
                 mem = C.create_string_buffer(int(lib.ygg_attn_dec_plan_size()))
                 L.check(lib.ygg_attn_dec_plan_init(mem, self.q.data_ptr(), cache.data_ptr() + li * self.layer_stride * es,
-                                                   B, R, cfg.n_heads, cfg.n_kv_heads, cfg.head_dim, self.S))
+                                                   B, R, cfg.n_heads, cfg.n_kv_heads, cfg.head_dim, self.S,
+                                                   plan.attn_kvsplit))
                 self.ad_plans.append(mem)
             self.ad_ws = torch.zeros(int(lib.ygg_attn_dec_workspace_size(self.ad_plans[0])) // 4 + 64,
                                      dtype=torch.float32, device=dev)
@@ -202,8 +189,7 @@ class Forward:
         # split stream-K tiles are reduced (in fixed segment order, by their participants) — the
         # [M, V] f32 partials round trip and the separate store epilogue disappear.  Same values.
         self.lm_epi = None
-        if (bf16 and not self.fused and self.lm_plan is not None
-                and os.environ.get("YGG_LM_FUSED", "1") != "0"):
+        if bf16 and not self.fused and self.lm_plan is not None and plan.lm_store_fused:
             self.lm_counters = torch.zeros(self.lm_plan.tiles, dtype=torch.int32, device=dev)
             e = L.YggEpilogue()
             e.kind = L.YGG_EPI_STORE_F32
@@ -213,8 +199,6 @@ class Forward:
             self.lm_epi = e
         if self.fused:
             self._setup_fused()
-        if self.mk:
-            self._setup_mk()
         if self.gemv:
             self._setup_gemv()
         self._setup_attn_l2_prefetch()
@@ -264,86 +248,41 @@ class Forward:
                  epi(L.YGG_GEMV_RESID, resid=self.resid.data_ptr(), hb=self.xn.data_ptr(),
                      ss_out=self.ss_ga.data_ptr())),
             ])
-        # The QKV GEMV streams only ~12 MB: after it, each CTA pulls a slice of a later stream of the
-        # layer into L2 (YGG_L2PF_QKV_MB of YGG_L2PF_QKV_TARGET).
-        qmb = float(os.environ.get("YGG_L2PF_QKV_MB", "16"))  # re-tuned same-box: 8 MB 0.570, 16 MB 0.563, 24 MB 0.566 ms
-        qtarget = os.environ.get("YGG_L2PF_QKV_TARGET", "wgu")
-        # Region 0 (issued first): the layer's KV cache block, which the attention right after reads
-        # (YGG_L2PF_KV, A/B knob: off — the whole cache block, S capacity included, cost more than the
-        # attention gained: 0.565 -> 0.567 ms); region 1: the start of gate|up.
-        kv_on = os.environ.get("YGG_L2PF_KV", "0") != "0"
+        # Latency-bound GEMVs pull a share of the layer's later weight streams into L2 while HBM would
+        # otherwise idle (plan.draft_qkv_l2 / draft_o_l2; sizes derived from the matrix sizes).
         for li, lw in enumerate(self.w["layers"]):
-            if kv_on:
-                L.check(lib.ygg_gemv_set_l2_prefetch(self.gv[li][0][0], 0, self.cache.data_ptr() + li * self.layer_stride * es,
-                                                     self.layer_stride * es))
-            if qmb > 0:
-                W = lw[qtarget]
-                nbytes = min(int(qmb * (1 << 20)), W.numel() * W.element_size())
-                L.check(lib.ygg_gemv_set_l2_prefetch(self.gv[li][0][0], 1, W.data_ptr(), nbytes))
-        # The O GEMV (its weights already sit in its ring) pulls the next 16 MB of gate|up (same-box
-        # pass 0.625 -> 0.615 ms; 24 MB 0.618, 32 MB 0.624).  A/B knob: the down GEMV pulling the next
-        # layer's QKV weights is slower (0.628-0.631), so off.
-        omb = float(os.environ.get("YGG_L2PF_O_MB", "16"))
-        dmb = float(os.environ.get("YGG_L2PF_DOWN_MB", "0"))
-        for li, lw in enumerate(self.w["layers"]):
-            if omb > 0:
-                W = lw["wgu"]
-                off = min(int(qmb * (1 << 20)), W.numel() * W.element_size())
-                nbytes = min(int(omb * (1 << 20)), W.numel() * W.element_size() - off)
-                L.check(lib.ygg_gemv_set_l2_prefetch(self.gv[li][1][0], 0, W.data_ptr() + off, nbytes))
-            if dmb > 0 and li + 1 < len(self.w["layers"]):
-                W = self.w["layers"][li + 1]["wqkv"]
-                nbytes = min(int(dmb * (1 << 20)), W.numel() * W.element_size())
-                L.check(lib.ygg_gemv_set_l2_prefetch(self.gv[li][3][0], 0, W.data_ptr(), nbytes))
+            for (pl, _), regs, first in ((self.gv[li][0], self.plan.draft_qkv_l2, 1),
+                                         (self.gv[li][1], self.plan.draft_o_l2, 0)):
+                for j, rg in enumerate(regs[: 2 - first]):
+                    W = lw[rg.target]
+                    off, n = rg.region(W, self.plan.l2_bytes)
+                    if n > 0:
+                        L.check(lib.ygg_gemv_set_l2_prefetch(pl, first + j, W.data_ptr() + off, n))
         ss_last, blocks_last = (self.ss_ga, d // 16) if cfg.n_layers > 0 else (self.ss_e, d // 128)
         self.gv_lm = (plan(self.w["lm_head"], self.xn),
                       epi(L.YGG_GEMV_STORE, out=self.logits.data_ptr(), ld=cfg.vocab, ss_in=ss_last.data_ptr(),
                           ss_blocks=blocks_last, norm_dim=d, eps=eps))
 
     def _setup_attn_l2_prefetch(self) -> None:
-        """While the decode attention of layer l runs, HBM is nearly idle: have it pull the start of
-        a later weight stream into L2 — for the draft the down projection of layer l (its GEMV CTAs
-        cannot be resident during the gate|up stream; the O-projection is already in the GEMV ring),
-        for the verify the O-projection of layer l (its GEMM CTAs cannot be resident beside the
-        attention CTAs).  YGG_L2PF_DRAFT_MB / YGG_L2PF_DRAFT_TARGET / YGG_L2PF_VERIFY_MB."""
+        """While the decode attention of layer l runs, HBM is nearly idle: it pulls the start of a later
+        weight stream of the layer into L2 — for the draft the down projection (its GEMV CTAs cannot be
+        resident during the gate|up stream; the O projection already sits in the GEMV ring), for the
+        verify the start of gate|up (plan.draft_attn_l2 / verify_attn_l2)."""
         if self.ad_plans is None:
             return
         lib = L.lib()
-        key, name = ("YGG_L2PF_DRAFT_MB", os.environ.get("YGG_L2PF_DRAFT_TARGET", "wdown")) if self.gemv \
-            else ("YGG_L2PF_VERIFY_MB", os.environ.get("YGG_L2PF_VERIFY_TARGET", "wo"))
-        # Measured same-box (cfg2): verify forward 3.583 -> 3.552 ms with 24 MB of wo (16 MB: 3.563;
-        # all 34 MB: no gain); draft pass 0.634 -> 0.627 ms with 12 MB of wdown (16: 0.630, 20: 0.637;
-        # prefetching gate|up instead slows the attention as much as gate|up gains).
-        mb = float(os.environ.get(key, "12" if self.gemv else "0"))
-        regions = [(name, mb)]
-        # Verify: only the start of the gate|up stream (re-tuned same-box: none 3.578 ms; O 24 + gate|up
-        # 24 MB 3.530; gate|up 24 MB alone 3.464; 16: 3.495; 32: 3.485).
-        if not self.gemv:
-            regions.append(("wgu", float(os.environ.get("YGG_L2PF_VERIFY_GU_MB", "24"))))
-        # Draft A/B knob: instead of / besides the contiguous start of the down projection, the tail
-        # chunks of every down-GEMV block its ring cannot hold (strided, via the GEMV's tensor map).
-        if self.gemv and os.environ.get("YGG_L2PF_DOWN_TENSOR", "0") != "0":
-            for li, plan in enumerate(self.ad_plans):
-                L.check(lib.ygg_attn_dec_set_gemv_prefetch(plan, self.gv[li][3][0]))
-        nl = len(self.ad_plans)
+        regions = self.plan.draft_attn_l2 if self.gemv else self.plan.verify_attn_l2
         for li, plan in enumerate(self.ad_plans):
-            for rg, (nm, m) in enumerate(regions):
-                if nm == "next_wqkv":  # A/B target: the next layer's QKV weights
-                    if li + 1 >= nl:
-                        L.check(lib.ygg_attn_dec_set_l2_prefetch(plan, rg, None, 0))
-                        continue
-                    W = self.w["layers"][li + 1]["wqkv"]
-                else:
-                    W = self.w["layers"][li][nm]
-                nbytes = min(int(m * (1 << 20)), W.numel() * W.element_size())
-                L.check(lib.ygg_attn_dec_set_l2_prefetch(plan, rg, W.data_ptr() if nbytes > 0 else None,
-                                                         max(nbytes, 0)))
+            for j, rg in enumerate(regions[:2]):
+                W = self.w["layers"][li][rg.target]
+                off, n = rg.region(W, self.plan.l2_bytes)
+                L.check(lib.ygg_attn_dec_set_l2_prefetch(plan, j, W.data_ptr() + off if n > 0 else None, n))
 
     def fuse_topk(self, k: int, temperature: float = 1.0) -> bool:
         """Draft GEMV pass: have the LM-head epilogue also emit per-CTA top-k partials of every row
         (STORE_TOPK; merged by ``ygg_topk_merge``), replacing the top-k scan of the logits.  Only
         for <= 8 rows and k <= 8; returns whether it is on."""
-        if not (self.gemv and self.M <= 8 and 1 <= k <= 8) or os.environ.get("YGG_TOPK_FUSED", "1") == "0":
+        if not (self.gemv and self.M <= 8 and 1 <= k <= 8) or not self.plan.topk_fused:
             return False
         lib = L.lib()
         plan, e = self.gv_lm
@@ -374,71 +313,14 @@ class Forward:
         chk(lib.ygg_embed_fused(self.w["embed"].data_ptr(), cfg.vocab, cfg.d_model, self.tokens.data_ptr(), self.M,
                                 self.resid.data_ptr(), self.xn.data_ptr(), self.ss_e.data_ptr(), s))
         qm = self.qmask.data_ptr() if self.mask_words > 0 else None
-        ko = _KNOCKOUT  # A/B timing only (YGG_KO)
         for li, ops in enumerate(self.gv):
             (pq, eq), (po, eo), (pg, eg), (pd, ed) = ops
-            if "qkv" not in ko:
-                chk(lib.ygg_gemv_run(pq, C.byref(eq), s))
-            if "attn" not in ko:
-                self._attend(li, qm, s)
-            if "o" not in ko:
-                chk(lib.ygg_gemv_run(po, C.byref(eo), s))
-            if "gu" not in ko:
-                chk(lib.ygg_gemv_run(pg, C.byref(eg), s))
-            if "down" not in ko:
-                chk(lib.ygg_gemv_run(pd, C.byref(ed), s))
-        if "lm" not in ko:
-            chk(lib.ygg_gemv_run(self.gv_lm[0], C.byref(self.gv_lm[1]), s))
-
-    # ------------------------------------------------------------------
-    def _setup_mk(self) -> None:
-        """Descriptor + device phase table of the persistent forward (csrc/mk.cu)."""
-        lib, cfg, M = L.lib(), self.cfg, self.M
-        dev = self.cache.device
-        lw = self.w["layers"]
-        n = cfg.n_layers
-        self._mk_ptrs = [(C.c_void_p * n)(*[x[k].data_ptr() for x in lw]) for k in ("wqkv", "wo", "wgu", "wdown")]
-        self.ss = torch.zeros(2, cfg.d_model // 128, M, dtype=torch.float32, device=dev)
-        d = L.YggMkDesc()
-        d.n_layers, d.d_model, d.n_heads, d.n_kv_heads = n, cfg.d_model, cfg.n_heads, cfg.n_kv_heads
-        d.head_dim, d.ffn, d.vocab = cfg.head_dim, cfg.ffn, cfg.vocab
-        d.B, d.T, d.S, d.mask_words = self.B, self.R, self.S, self.mask_words
-        d.eps, d.attn_scale = float(cfg.norm_eps), float(self.scale)
-        d.wqkv, d.wo, d.wgu, d.wdown = [C.cast(p, C.POINTER(C.c_void_p)) for p in self._mk_ptrs]
-        d.embed, d.lm_head = self.w["embed"].data_ptr(), self.w["lm_head"].data_ptr()
-        d.tokens, d.pos, d.slot, d.req = (t.data_ptr() for t in (self.tokens, self.pos, self.slot, self.req))
-        d.qmask = self.qmask.data_ptr() if self.mask_words > 0 else None
-        d.blk_start, d.blk_len = self.blk_start.data_ptr(), self.blk_len.data_ptr()
-        d.rope_cs, d.cache, d.layer_stride = self.rope_cs.data_ptr(), self.cache.data_ptr(), self.layer_stride
-        d.resid, d.hb, d.q, d.attn = (t.data_ptr() for t in (self.resid, self.xn, self.q, self.attn))
-        d.mlp, d.logits, d.ss = self.mlp.data_ptr(), self.logits.data_ptr(), self.ss.data_ptr()
-        d.num_ctas, d.lookahead = 0, -1
-        tb, wb, pb = C.c_size_t(), C.c_size_t(), C.c_size_t()
-        L.check(lib.ygg_mk_query(C.byref(d), C.byref(tb), C.byref(wb), C.byref(pb)))
-        self.mk_table = torch.zeros(tb.value, dtype=torch.uint8, device=dev)
-        self.mk_ws = torch.empty(wb.value // 4 + 4, dtype=torch.float32, device=dev)
-        self.mk_part = torch.empty(pb.value // 4 + 4, dtype=torch.float32, device=dev)
-        d.ws, d.attn_part = self.mk_ws.data_ptr(), self.mk_part.data_ptr()
-        self._mk_desc = d
-        self._mk_plan = C.create_string_buffer(int(lib.ygg_mk_plan_size()))
-        L.check(lib.ygg_mk_plan_init(self._mk_plan, C.byref(d), self.mk_table.data_ptr(), tb.value))
-
-    def mk_phase_stamps(self, on: bool) -> torch.Tensor | None:
-        """Profiling only: re-plan with (or without) per-CTA %globaltimer stamps at every phase end.
-        Returns the u64 [grid, phases] stamp buffer (int64 view) or None."""
-        if not self.mk:
-            raise ValueError("not a persistent forward")
-        lib = L.lib()
-        buf = None
-        if on:
-            g = torch.cuda.get_device_properties(self.cache.device).multi_processor_count
-            nph = 1 + 6 * self.cfg.n_layers + 1
-            buf = torch.zeros(8 * g, nph, dtype=torch.int64, device=self.cache.device)
-        self._mk_desc.dbg = buf.data_ptr() if buf is not None else None
-        self._mk_stamps = buf
-        L.check(lib.ygg_mk_plan_init(self._mk_plan, C.byref(self._mk_desc), self.mk_table.data_ptr(),
-                                     self.mk_table.numel()))
-        return buf
+            chk(lib.ygg_gemv_run(pq, C.byref(eq), s))
+            self._attend(li, qm, s)
+            chk(lib.ygg_gemv_run(po, C.byref(eo), s))
+            chk(lib.ygg_gemv_run(pg, C.byref(eg), s))
+            chk(lib.ygg_gemv_run(pd, C.byref(ed), s))
+        chk(lib.ygg_gemv_run(self.gv_lm[0], C.byref(self.gv_lm[1]), s))
 
     # ------------------------------------------------------------------
     def _setup_fused(self) -> None:
@@ -517,8 +399,6 @@ class Forward:
     def run(self, stream: torch.cuda.Stream | None = None) -> None:
         if self.gemv:
             self._run_gemv(stream)
-        elif self.mk:
-            L.check(L.lib().ygg_mk_run(self._mk_plan, L.stream_ptr(stream)))
         elif self.fused:
             self._run_fused(stream)
         else:
@@ -586,45 +466,34 @@ class Forward:
         ws = self.ws.data_ptr()
         nl = len(self.plans)
         qm = self.qmask.data_ptr() if self.mask_words > 0 else None
-        ko = _KNOCKOUT  # A/B timing only (YGG_KO): launches left out, results invalid
         for li, (p, lw) in enumerate(zip(self.plans, w["layers"])):
             cache_l = self.cache.data_ptr() + li * self.layer_stride * self.cache.element_size()
-            if "gemm" not in ko:
-                chk(lib.ygg_gemm_run(p["qkv"].handle, ws, s))
-            if "epi" not in ko and "epi_qkv" not in ko:
-                chk(lib.ygg_epi_qkv_rope(p["qkv"].handle, ws, cfg.n_heads, cfg.n_kv_heads, cfg.head_dim,
-                                         cfg.rope_theta, self.pos.data_ptr(), self.slot.data_ptr(),
-                                         self.req.data_ptr(), self.q.data_ptr(), cache_l, self.S, self.act,
-                                         self.rope_cs.data_ptr(), s))
+            chk(lib.ygg_gemm_run(p["qkv"].handle, ws, s))
+            chk(lib.ygg_epi_qkv_rope(p["qkv"].handle, ws, cfg.n_heads, cfg.n_kv_heads, cfg.head_dim,
+                                     cfg.rope_theta, self.pos.data_ptr(), self.slot.data_ptr(),
+                                     self.req.data_ptr(), self.q.data_ptr(), cache_l, self.S, self.act,
+                                     self.rope_cs.data_ptr(), s))
             stamp()
-            if "attn" in ko:
-                pass
-            elif self.attn_plans is not None:
+            if self.attn_plans is not None:
                 self._attend(li, qm, s)
             else:
                 chk(lib.ygg_attention(self.q.data_ptr(), cache_l, self.act, M, self.B, cfg.n_heads, cfg.n_kv_heads,
                                       cfg.head_dim, self.S, self.blk_start.data_ptr(), self.blk_len.data_ptr(),
                                       qm, self.mask_words, self.scale, self.attn.data_ptr(), s))
             stamp()
-            if "gemm" not in ko:
-                chk(lib.ygg_gemm_run(p["o"].handle, ws, s))
-            if "epi" not in ko and "epi_resid" not in ko:
-                chk(lib.ygg_epi_residual_norm(p["o"].handle, ws, self.resid.data_ptr(), lw["mlp_norm"].data_ptr(),
-                                              cfg.norm_eps, self.xn.data_ptr(), self.act, s))
+            chk(lib.ygg_gemm_run(p["o"].handle, ws, s))
+            chk(lib.ygg_epi_residual_norm(p["o"].handle, ws, self.resid.data_ptr(), lw["mlp_norm"].data_ptr(),
+                                          cfg.norm_eps, self.xn.data_ptr(), self.act, s))
             stamp()
-            if "gemm" not in ko:
-                chk(lib.ygg_gemm_run(p["gu"].handle, ws, s))
-            if "epi" not in ko and "epi_swiglu" not in ko:
-                chk(lib.ygg_epi_swiglu(p["gu"].handle, ws, self.mlp.data_ptr(), self.act, s))
+            chk(lib.ygg_gemm_run(p["gu"].handle, ws, s))
+            chk(lib.ygg_epi_swiglu(p["gu"].handle, ws, self.mlp.data_ptr(), self.act, s))
             stamp()
-            if "gemm" not in ko:
-                chk(lib.ygg_gemm_run(p["down"].handle, ws, s))
+            chk(lib.ygg_gemm_run(p["down"].handle, ws, s))
             nxt = w["layers"][li + 1]["attn_norm"] if li + 1 < nl else w["final_norm"]
-            if "epi" not in ko and "epi_resid" not in ko:
-                chk(lib.ygg_epi_residual_norm(p["down"].handle, ws, self.resid.data_ptr(), nxt.data_ptr(),
-                                              cfg.norm_eps, self.xn.data_ptr(), self.act, s))
+            chk(lib.ygg_epi_residual_norm(p["down"].handle, ws, self.resid.data_ptr(), nxt.data_ptr(),
+                                          cfg.norm_eps, self.xn.data_ptr(), self.act, s))
             stamp()
-        if self.lm_plan is not None and "lm" not in ko:
+        if self.lm_plan is not None:
             if self.lm_epi is not None:
                 chk(lib.ygg_gemm_fused(self.lm_plan.handle, ws, C.byref(self.lm_epi), s))
             else:
@@ -651,7 +520,7 @@ def prefill_causal(cfg: ModelConfig, w: dict, cache: torch.Tensor, prompts: torc
         f = fwd.get(key)
         if f is None:
             f = Forward(cfg, w, cache, B, n, 0, act_dtype, logits=final and want_logits, gemv=False,
-                        decode_attn=False, persistent=False)
+                        decode_attn=False)
             fwd[key] = f
         f.tokens.copy_(prompts[:, c0:c0 + n].reshape(-1))
         pos = torch.arange(c0, c0 + n, dtype=torch.int32, device=dev).repeat(B)

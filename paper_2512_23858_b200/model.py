@@ -216,32 +216,6 @@ def prepare_fused_(w: dict, cfg: ModelConfig) -> dict:
     return w
 
 
-def prepare_folded_(w: dict, cfg: ModelConfig) -> dict:
-    """In-place fold of the RMSNorm gains into the following matmuls (wqkv, wgu, lm_head columns),
-    row order unchanged (idempotent).  Used by the persistent forward, whose epilogue phases apply
-    the per-row rstd to the GEMM output; the per-kernel path stays exact with the unit gains left
-    behind (rmsnorm(x) . W^T == rstd * (x . (W diag g)^T))."""
-    if w.get("_layout") in ("folded", "fused"):
-        if w["_layout"] == "fused":
-            raise ValueError("weights are in the fused (row-permuted) layout; the persistent forward needs folded")
-        return w
-    for lw in w["layers"]:
-        an = lw["attn_norm"].float()
-        mn = lw["mlp_norm"].float()
-        if not bool(torch.all(an == 1)):
-            lw["wqkv"] = (lw["wqkv"].float() * an[None, :]).to(lw["wqkv"].dtype).contiguous()
-        if not bool(torch.all(mn == 1)):
-            lw["wgu"] = (lw["wgu"].float() * mn[None, :]).to(lw["wgu"].dtype).contiguous()
-        lw["attn_norm"] = torch.ones_like(lw["attn_norm"])
-        lw["mlp_norm"] = torch.ones_like(lw["mlp_norm"])
-    fn = w["final_norm"].float()
-    if not bool(torch.all(fn == 1)):
-        w["lm_head"] = (w["lm_head"].float() * fn[None, :]).to(w["lm_head"].dtype)
-    w["final_norm"] = torch.ones_like(w["final_norm"])
-    w["_layout"] = "folded"
-    return w
-
-
 def rope_table(cfg: ModelConfig, positions: int, device) -> torch.Tensor:
     """[positions, hd/2, 2] (cos, sin) of the RoPE angle for the fused QKV epilogue.
 

@@ -1,0 +1,61 @@
+"""Typed per-forward kernel plan: which kernel family runs each part of a pass and how much of the
+later weight streams each latency-bound kernel pulls into L2 while HBM would otherwise idle.
+
+Everything the round-1 code read from ``YGG_*`` environment variables at plan time is a field
+here; a ``Forward`` takes one ``ForwardPlan`` (default: ``ForwardPlan()``, the measured-best
+choices below).  L2-prefetch sizes are derived from the matrix sizes of the model being run, not
+fixed byte counts: each is a fraction of the target matrix, capped by a share of the L2.
+
+Measured on cfg2 (same-box A/Bs), which the fractions reproduce at the 1B draft / 8B
+target sizes:
+  draft QKV GEMV      -> the first quarter of gate|up      (16 MB of 64: pass 0.570 -> 0.563 ms)
+  draft O GEMV        -> the next quarter of gate|up       (16 MB: 0.625 -> 0.615 ms)
+  draft attention     -> the first 3/8 of down             (12 MB of 32: 0.634 -> 0.627 ms)
+  verify attention    -> the first tenth of gate|up        (24 MB of 235: verify 3.578 -> 3.464 ms)
+A kernel that pulls more than it leaves idle slows itself as much as the next kernel gains, so every
+region is also capped at a quarter of the L2 (31.5 MB on B200).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+L2_BYTES_B200 = 126 * (1 << 20)
+
+
+@dataclass(frozen=True)
+class L2Prefetch:
+    """One kernel's L2 pull: ``fraction`` of matrix ``target`` starting at ``offset_fraction``."""
+
+    target: str               # weight name in the layer dict (wqkv / wo / wgu / wdown)
+    fraction: float
+    offset_fraction: float = 0.0
+
+    def region(self, W, l2_bytes: int) -> tuple[int, int]:
+        """(byte offset, byte count) of the region inside ``W``."""
+        total = W.numel() * W.element_size()
+        cap = l2_bytes // 4
+        off = min(int(self.offset_fraction * total), cap) if self.offset_fraction else 0
+        n = min(int(self.fraction * total), cap, total - off)
+        return off, max(n, 0)
+
+
+@dataclass(frozen=True)
+class ForwardPlan:
+    # kernel families (None = automatic by shape: bf16 passes of <= 16 rows take the row-block GEMV;
+    # the decode attention for passes whose row tiles fit one wave)
+    gemv: bool | None = None
+    decode_attn: bool | None = None
+    fused_epilogues: bool = False   # fused-epilogue stream-K GEMMs (weights in the fused layout)
+    lm_store_fused: bool = True     # LM-head logits straight from TMEM (no partials round trip)
+    topk_fused: bool = True         # draft top-k partials from the LM-head GEMV epilogue
+    attn_kvsplit: int = 0           # decode attention cluster size (0 = automatic)
+    # L2 prefetch issued by latency-bound kernels (see module docstring)
+    draft_qkv_l2: tuple = (L2Prefetch("wgu", 0.25),)
+    draft_o_l2: tuple = (L2Prefetch("wgu", 0.25, 0.25),)
+    draft_attn_l2: tuple = (L2Prefetch("wdown", 0.375),)
+    verify_attn_l2: tuple = (L2Prefetch("wgu", 0.1),)
+    l2_bytes: int = field(default=L2_BYTES_B200)
+
+
+DEFAULT = ForwardPlan()

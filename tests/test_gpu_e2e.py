@@ -79,22 +79,21 @@ def test_fp32_step_trace_matches_oracle(coupled, cuda):
 
 @pytest.mark.parametrize("fused", [False, True])
 @pytest.mark.parametrize("coupled", [False, True])
-def test_bf16_spec_equals_ar_and_graph_equals_eager(coupled, fused, cuda, monkeypatch):
+def test_bf16_spec_equals_ar_and_graph_equals_eager(coupled, fused, cuda):
     from paper_2512_23858_b200.engine import ARDecoder, SpecDecoder, StepShape
     from paper_2512_23858_b200.model import weights_to
+    from paper_2512_23858_b200.plan import ForwardPlan
 
-    if fused:
-        monkeypatch.setenv("YGG_FUSED", "1")
-    else:
-        monkeypatch.delenv("YGG_FUSED", raising=False)
+    plan = ForwardPlan(fused_epilogues=fused)
     tc, dc, tw, dw = _models(torch.float32, coupled)
     twb, dwb = weights_to(tw, cuda, torch.bfloat16), weights_to(dw, cuda, torch.bfloat16)
     prompts = torch.stack([_prompt(tc.vocab, 32, s) for s in (1000, 1001)])
     n_tok = 40
-    ar = ARDecoder(tc, twb, batch=2, max_seq=256).generate(prompts, n_tok)
+    ar = ARDecoder(tc, twb, batch=2, max_seq=256, plan=plan).generate(prompts, n_tok)
     outs = []
     for use_graph in (False, True):
-        sd = SpecDecoder(tc, twb, dc, dwb, StepShape(4, 4, 8, 64), batch=2, max_seq=256, profiles=_profiles())
+        sd = SpecDecoder(tc, twb, dc, dwb, StepShape(4, 4, 8, 64), batch=2, max_seq=256, profiles=_profiles(),
+                         plan=plan)
         got, steps = sd.generate(prompts, n_tok, use_graph=use_graph)
         outs.append(got)
     assert outs[0] == outs[1]

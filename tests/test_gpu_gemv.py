@@ -47,7 +47,7 @@ def _fwd(cfg, w, cache, B, R, mask_words, gemv, inp, P):
     from paper_2512_23858_b200.forward import Forward
 
     tokens, pos, slot, req, qmask = inp
-    f = Forward(cfg, w, cache, B, R, mask_words, torch.bfloat16, gemv=gemv, persistent=False)
+    f = Forward(cfg, w, cache, B, R, mask_words, torch.bfloat16, gemv=gemv)
     assert f.gemv == gemv
     f.tokens.copy_(tokens)
     f.pos.copy_(pos)
@@ -183,7 +183,7 @@ def test_gemv_plan_rejects_bad_shapes(cuda):
                                                 (128, 32, 8, 1, 50, 512, 2), (64, 32, 8, 2, 33, 90, 2),
                                                 (128, 32, 8, 1, 40, 64, 0)])
 @pytest.mark.parametrize("kvsplit", ["1", "2", "3", "8"])
-def test_decode_attention_vs_fp32(hd, Hq, Hkv, B, T, P, mw, kvsplit, cuda, monkeypatch):
+def test_decode_attention_vs_fp32(hd, Hq, Hkv, B, T, P, mw, kvsplit, cuda):
     """ygg_attn_dec_run vs a float64 softmax(QK^T/sqrt(hd)) V over the visible keys (prefix + tree /
     causal block), with the key chunks split over 1..8 CTAs of a cluster.  bf16 operands; tolerance
     2e-2 of the output scale (bf16 P and output rounding); repeated launches are bit-identical."""
@@ -192,7 +192,6 @@ def test_decode_attention_vs_fp32(hd, Hq, Hkv, B, T, P, mw, kvsplit, cuda, monke
 
     from paper_2512_23858_b200 import _lib as L
 
-    monkeypatch.setenv("YGG_ATTN_DEC_KVSPLIT", kvsplit)  # read at plan time
     lib = L.lib()
     S = ((P + T + 63) // 64) * 64
     g = torch.Generator(device="cuda").manual_seed(hd + T)
@@ -210,7 +209,7 @@ def test_decode_attention_vs_fp32(hd, Hq, Hkv, B, T, P, mw, kvsplit, cuda, monke
     bl = torch.full((B,), T, dtype=torch.int32, device=cuda)
     out = torch.zeros(M, Hq, hd, dtype=torch.bfloat16, device=cuda)
     mem = C.create_string_buffer(int(lib.ygg_attn_dec_plan_size()))
-    L.check(lib.ygg_attn_dec_plan_init(mem, q.data_ptr(), cache.data_ptr(), B, T, Hq, Hkv, hd, S))
+    L.check(lib.ygg_attn_dec_plan_init(mem, q.data_ptr(), cache.data_ptr(), B, T, Hq, Hkv, hd, S, int(kvsplit)))
     scale = 1.0 / math.sqrt(hd)
     ws = torch.zeros(int(lib.ygg_attn_dec_workspace_size(mem)) // 4 + 64, dtype=torch.float32, device=cuda)
     outs = []
@@ -289,7 +288,7 @@ def test_l2_prefetch_regions_leave_results_unchanged(cuda):
     bs = torch.full((1,), P, dtype=torch.int32, device=cuda)
     bl = torch.full((1,), T, dtype=torch.int32, device=cuda)
     att = C.create_string_buffer(int(lib.ygg_attn_dec_plan_size()))
-    L.check(lib.ygg_attn_dec_plan_init(att, q.data_ptr(), cache.data_ptr(), 1, T, Hq, Hkv, hd, S))
+    L.check(lib.ygg_attn_dec_plan_init(att, q.data_ptr(), cache.data_ptr(), 1, T, Hq, Hkv, hd, S, 0))
     res = []
     for pf in (0, 1 << 20):
         for rg in (0, 1):
@@ -372,7 +371,7 @@ def test_decode_attention_wide_tree_mask(hd, Hq, Hkv, cuda):
     bl = torch.full((B,), N, dtype=torch.int32, device=cuda)
     out = torch.zeros(M, Hq, hd, dtype=torch.bfloat16, device=cuda)
     mem = C.create_string_buffer(int(lib.ygg_attn_dec_plan_size()))
-    L.check(lib.ygg_attn_dec_plan_init(mem, q.data_ptr(), cache.data_ptr(), B, R, Hq, Hkv, hd, S))
+    L.check(lib.ygg_attn_dec_plan_init(mem, q.data_ptr(), cache.data_ptr(), B, R, Hq, Hkv, hd, S, 0))
     ws = torch.zeros(int(lib.ygg_attn_dec_workspace_size(mem)) // 4 + 64, dtype=torch.float32, device=cuda)
     scale = 1.0 / math.sqrt(hd)
     L.check(lib.ygg_attn_dec_run(mem, bs.data_ptr(), bl.data_ptr(), qmask.data_ptr(), mw, scale, out.data_ptr(),

@@ -232,6 +232,13 @@ typedef struct {
 } ygg_epilogue;
 
 int ygg_gemm_fused(const void* plan, float* workspace, const ygg_epilogue* epi, ygg_stream_t stream);
+/* Cluster split-K (bf16): one thread-block cluster of `cluster` CTAs per 128-row output tile, the tile's
+ * K range split evenly over them, the partials reduced through DSMEM into the cluster's leader, which
+ * applies the fused epilogue (no workspace partials, no counters).  Fails with YGG_ERR_UNSUPPORTED
+ * unless every tile's cluster is co-resident in one wave.  cluster = 0 restores stream-K.  Such a plan
+ * runs only through ygg_gemm_fused. */
+int ygg_gemm_plan_set_cluster(void* plan, int cluster);
+int ygg_gemm_plan_cluster(const void* plan);
 int ygg_gemm_tiles(const void* plan);
 /* Embedding gather for the fused path: resid (f32), hb (bf16) and per-128-feature-tile sums of
  * squares ss_out [d/128][M] (the first layer's folded RMSNorm input). */

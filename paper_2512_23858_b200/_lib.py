@@ -141,6 +141,8 @@ _SIGS: dict[str, tuple] = {
                                      C.POINTER(C.c_int), C.POINTER(C.c_size_t)]),
     "ygg_gemm_seg_table_len": (C.c_int, [vp]),
     "ygg_gemm_run": (C.c_int, [vp, vp, vp]),
+    "ygg_gemm_plan_set_cluster": (C.c_int, [vp, C.c_int]),
+    "ygg_gemm_plan_cluster": (C.c_int, [vp]),
     "ygg_gemm_fused": (C.c_int, [vp, vp, C.POINTER(YggEpilogue), vp]),
     "ygg_gemm_tiles": (C.c_int, [vp]),
     "ygg_embed_fused": (C.c_int, [vp, C.c_int, C.c_int, vp, C.c_int, vp, vp, vp, vp]),

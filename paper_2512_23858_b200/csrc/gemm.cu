@@ -43,6 +43,7 @@ struct GemmPlan {
   int segments;
   int stages;
   int tmem_cols;
+  int cluster;   // > 0: cluster split-K (one cluster of `cluster` CTAs per tile, DSMEM reduction)
   const void* W;
   const void* X;
   int32_t* seg_table;  // device: seg_first[tiles+1], seg_base[num_ctas]
@@ -100,6 +101,11 @@ struct EpiArgs {
 
 
 YGG_DEV void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+YGG_DEV uint32_t cluster_ctarank_u32() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
 YGG_DEV int ld_acquire(const int32_t* p) {
   int v;
   asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -502,6 +508,205 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     }
     if (e.dbg && et == 0) e.dbg[c * 8 + 4] = gtimer();
     if (et == 0) trace_max(e.trace, 7);  // epilogue warps done
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) trace_max(e.trace, 2);
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, p.tmem_cols);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Cluster split-K kernel: one (cs, 1, 1) thread-block cluster per output tile, the tile's K range
+// split evenly over the cs CTAs, the partials reduce-scattered through DSMEM: the tile's 16-token
+// column chunks are owned round-robin by the cluster's CTAs (chunk q -> rank q % cs), every CTA
+// stores the chunks it does not own into their owner's receive slots, and after one cluster barrier
+// each owner sums its chunk's cs partials in rank order (deterministic) and applies the fused
+// epilogue.  No global partials, no arrival counters, no fixups, and the epilogue's global round
+// trips are spread over the cluster (one chunk per CTA at cs = 4).  A tile's CTAs are co-scheduled
+// and stream the same number of weight bytes, so they reach the exchange together.  Used where the
+// tile count times the cluster size fits one wave (the cfg2 verify's O / down: 32 tiles x 4 CTAs).
+// ---------------------------------------------------------------------------
+struct ClusterParams {
+  int M, BN, m_tiles, kb, stages, tmem_cols, cs;
+  int own_max;  // chunks owned per CTA (ceil(BN/16 / cs)); receive slots per CTA = (cs-1) * own_max
+};
+
+constexpr int kChunkBytes = 16 * kBM * 4;  // one 16-token x 128-feature f32 partial chunk
+
+__host__ __device__ inline size_t cluster_recv_bytes(int cs, int BN) {
+  const int nchunks = BN / 16;
+  const int own_max = (nchunks + cs - 1) / cs;
+  return static_cast<size_t>(cs - 1) * own_max * kChunkBytes;
+}
+
+template <int KIND>
+__global__ void __launch_bounds__(kGemmThreads, 1)
+    gemm_cluster_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant__ CUtensorMap tmap_x,
+                        ClusterParams p, EpiArgs e) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* base = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int BN = p.BN, S = p.stages, cs = p.cs;
+  const uint32_t a_bytes = kBM * kBK * 2;
+  const uint32_t b_bytes = BN * kBK * 2;
+  unsigned char* sa = base;
+  unsigned char* sb = base + static_cast<size_t>(S) * a_bytes;
+  // receive slots [cs-1][own_max][16/4][128][4] f32, outside the ring: peers may store into them
+  // while this CTA is still streaming
+  float* recv = reinterpret_cast<float*>(sb + static_cast<size_t>(S) * b_bytes);
+  uint64_t* full = reinterpret_cast<uint64_t*>(reinterpret_cast<unsigned char*>(recv) +
+                                               static_cast<size_t>(cs - 1) * p.own_max * kChunkBytes);
+  uint64_t* empty = full + S;
+  uint64_t* tfull = empty + S;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tfull + 2);
+  float* red_s = reinterpret_cast<float*>(tmem_slot + 8);  // [4][16]
+  float* rstd_s = red_s + 64;                             // [kMaxRstdTokens]
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int rank = static_cast<int>(cluster_ctarank_u32());
+  const int tile = blockIdx.x / cs;
+  const int m_tile = tile % p.m_tiles, n_tile = tile / p.m_tiles;
+  const int k0 = p.kb * rank / cs, k1 = p.kb * (rank + 1) / cs;
+  const int nk = k1 - k0;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmap_w);
+    tma_prefetch_desc(&tmap_x);
+    for (int s = 0; s < S; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    mbar_init(&tfull[0], 1);
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, p.tmem_cols);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  if (threadIdx.x == 0) trace_min(e.trace, 0);
+  pdl_launch_dependents();
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ===== TMA producer: weights before the grid-dependency wait, activations after =====
+      const uint64_t pol_w = policy_evict_first();
+      const uint64_t pol_x = policy_evict_last();
+      const int wrow = n_tile * kBM, xrow = m_tile * BN;
+      const int pre = nk < S ? nk : S;
+      for (int i = 0; i < pre; ++i) {
+        mbar_arrive_expect_tx(&full[i], a_bytes + b_bytes);
+        tma_load_2d(sa + static_cast<size_t>(i) * a_bytes, &tmap_w, &full[i], (k0 + i) * kBK, wrow, pol_w);
+      }
+      pdl_wait();
+      trace_min(e.trace, 1);
+      for (int i = 0; i < pre; ++i)
+        tma_load_2d(sb + static_cast<size_t>(i) * b_bytes, &tmap_x, &full[i], (k0 + i) * kBK, xrow, pol_x);
+      int stage = pre % S;
+      uint32_t phase = (pre == S) ? 1u : 0u;
+      for (int kb = k0 + pre; kb < k1; ++kb) {
+        mbar_wait(&empty[stage], phase ^ 1u);
+        mbar_arrive_expect_tx(&full[stage], a_bytes + b_bytes);
+        tma_load_2d(sa + static_cast<size_t>(stage) * a_bytes, &tmap_w, &full[stage], kb * kBK, wrow, pol_w);
+        tma_load_2d(sb + static_cast<size_t>(stage) * b_bytes, &tmap_x, &full[stage], kb * kBK, xrow, pol_x);
+        if (++stage == S) { stage = 0; phase ^= 1u; }
+      }
+      trace_max(e.trace, 3);
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    // ===== MMA issuer (one accumulator: one K range per CTA) =====
+    const uint32_t idesc = umma_idesc_bf16(kBM, BN);
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int u = 0; u < nk; ++u) {
+      mbar_wait(&full[stage], phase);
+      tc_fence_after();
+      if (lane == 0) {
+        const uint32_t a_addr = smem_u32(sa + static_cast<size_t>(stage) * a_bytes);
+        const uint32_t b_addr = smem_u32(sb + static_cast<size_t>(stage) * b_bytes);
+#pragma unroll
+        for (int kk = 0; kk < kBK / 16; ++kk)
+          umma_bf16(tmem_base, umma_desc_sw128(a_addr + kk * 32), umma_desc_sw128(b_addr + kk * 32), idesc,
+                    (u == 0 && kk == 0) ? 0u : 1u);
+        umma_commit(&empty[stage]);
+      }
+      __syncwarp();
+      if (++stage == S) { stage = 0; phase ^= 1u; }
+    }
+    if (lane == 0) {
+      umma_commit(&tfull[0]);
+      trace_max(e.trace, 4);
+    }
+    __syncwarp();
+  } else {
+    // ===== epilogue warps: the previous kernel's outputs become visible, then the folded-RMSNorm
+    // rstd of every token is computed while the mainloop runs =====
+    pdl_wait();
+    if (KIND != kEpiNone && e.ss_in) {
+      const int et = threadIdx.x - 64;
+      for (int m = et; m < p.M; m += 128) {
+        float s = 0.f;
+#pragma unroll 16
+        for (int t = 0; t < e.ss_tiles; ++t) s += __ldg(e.ss_in + static_cast<size_t>(t) * p.M + m);
+        rstd_s[m] = rsqrtf(s / static_cast<float>(e.norm_dim) + e.eps);
+      }
+      epi_bar();
+    }
+  }
+  const int quarter = warp & 3;
+  const int row = quarter * 32 + lane;
+  const uint32_t taddr = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16);
+  const int valid = min(BN, p.M - m_tile * BN);
+  const int nchunks = (valid + 15) / 16;  // chunks holding at least one real token
+  if (warp >= 2) {
+    mbar_wait(&tfull[0], 0);
+    tc_fence_after();
+    // scatter: every chunk this CTA does not own goes to its owner's receive slot for this rank
+    for (int q = 0; q < nchunks; ++q) {
+      const int owner = q % cs;
+      if (owner == rank) continue;
+      float v[16];
+      tmem_ld16(taddr + q * 16, v);
+      const int slot = (rank - owner - 1 + cs) % cs;  // 0..cs-2, the source's position after the owner
+      const int local = q / cs;
+      const uint32_t dst = mapa_shared(smem_u32(recv), static_cast<uint32_t>(owner)) +
+                           static_cast<uint32_t>((((slot * p.own_max + local) * 4) * kBM + row) * 16);
+#pragma unroll
+      for (int c4 = 0; c4 < 4; ++c4)
+        st_cluster_v4(dst + static_cast<uint32_t>(c4 * kBM * 16), v[4 * c4], v[4 * c4 + 1], v[4 * c4 + 2],
+                      v[4 * c4 + 3]);
+    }
+  }
+  // every partial is in its owner's shared memory (release / acquire at cluster scope)
+  cluster_sync();
+  if (warp >= 2) {
+    const int n = n_tile * kBM + row;
+    for (int q = rank; q < nchunks; q += cs) {
+      const int local = q / cs;
+      float own[16], v[16];
+      tmem_ld16(taddr + q * 16, own);
+#pragma unroll
+      for (int j = 0; j < 16; ++j) v[j] = 0.f;
+      for (int r = 0; r < cs; ++r) {  // rank order: deterministic
+        if (r == rank) {
+#pragma unroll
+          for (int j = 0; j < 16; ++j) v[j] += own[j];
+        } else {
+          const int slot = (r - rank - 1 + cs) % cs;
+          const float4* src = reinterpret_cast<const float4*>(recv) + ((slot * p.own_max + local) * 4) * kBM + row;
+#pragma unroll
+          for (int c4 = 0; c4 < 4; ++c4) {
+            const float4 x = src[c4 * kBM];
+            v[4 * c4] += x.x;
+            v[4 * c4 + 1] += x.y;
+            v[4 * c4 + 2] += x.z;
+            v[4 * c4 + 3] += x.w;
+          }
+        }
+      }
+      if constexpr (KIND != kEpiNone)
+        epi_apply<KIND>(e, p.M, n, m_tile * BN + q * 16, valid - q * 16, v, rstd_s, red_s, quarter, lane);
+    }
+    if (threadIdx.x == 64) trace_max(e.trace, 7);
   }
   __syncthreads();
   if (threadIdx.x == 0) trace_max(e.trace, 2);
@@ -917,6 +1122,27 @@ static EpiGeom geom_of(const GemmPlan* g, int kernel_id) {
 
 using namespace ygg;
 
+// Ring stages of a cluster plan: the stream-K budget minus the receive slots.
+static int cluster_stages(const GemmPlan* g, int cs) {
+  const int stage_bytes = kBM * kBK * 2 + g->BN * kBK * 2;
+  const long long avail = 190LL * 1024 - kSmemExtra - static_cast<long long>(cluster_recv_bytes(cs, g->BN));
+  return static_cast<int>(std::min<long long>(12, avail / stage_bytes));
+}
+
+static size_t cluster_smem(const GemmPlan* g) {
+  return kSmemExtra + static_cast<size_t>(cluster_stages(g, g->cluster)) * (kBM * kBK * 2 + g->BN * kBK * 2) +
+         cluster_recv_bytes(g->cluster, g->BN);
+}
+
+template <int KIND>
+static int launch_cluster_kind(const GemmPlan* g, const EpiArgs& e, cudaStream_t s) {
+  const int nchunks = g->BN / 16;
+  ClusterParams cp{g->M, g->BN, g->m_tiles, g->kb, cluster_stages(g, g->cluster), g->tmem_cols, g->cluster,
+                   (nchunks + g->cluster - 1) / g->cluster};
+  return launch_pdl_cluster_x(gemm_cluster_kernel<KIND>, dim3(g->tiles * g->cluster), dim3(kGemmThreads),
+                              cluster_smem(g), g->cluster, s, g->tmap_w, g->tmap_x, cp, e);
+}
+
 extern "C" {
 
 int ygg_prepare_gemm(void) {
@@ -925,6 +1151,16 @@ int ygg_prepare_gemm(void) {
                   gemm_bf16_tc_kernel<kEpiSwiglu>, gemm_bf16_tc_kernel<kEpiResid>}) {
     e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     if (e != cudaSuccess) return ygg_fail(YGG_ERR_CUDA, "gemm attribute: %s", cudaGetErrorString(e));
+  }
+  for (auto fn : {gemm_cluster_kernel<kEpiNone>, gemm_cluster_kernel<kEpiStoreF32>, gemm_cluster_kernel<kEpiQkvRope>,
+                  gemm_cluster_kernel<kEpiSwiglu>, gemm_cluster_kernel<kEpiResid>}) {
+    e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    if (e != cudaSuccess) return ygg_fail(YGG_ERR_CUDA, "gemm attribute: %s", cudaGetErrorString(e));
+  }
+  for (auto fn : {gemm_cluster_kernel<kEpiNone>, gemm_cluster_kernel<kEpiStoreF32>, gemm_cluster_kernel<kEpiQkvRope>,
+                  gemm_cluster_kernel<kEpiSwiglu>, gemm_cluster_kernel<kEpiResid>}) {
+    e = cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (e != cudaSuccess) return ygg_fail(YGG_ERR_CUDA, "gemm cluster attribute: %s", cudaGetErrorString(e));
   }
   return YGG_OK;
 }
@@ -1075,7 +1311,7 @@ static int gemm_launch(const GemmPlan* g, float* workspace, const ygg_epilogue* 
       e.counters = epi->counters;
       e.dbg = reinterpret_cast<unsigned long long*>(epi->dbg);
       e.rope_cs = reinterpret_cast<const float2*>(epi->rope_cs);
-      YGG_CHECK_ARG(kind == kEpiNone || e.counters != nullptr, "fused epilogue needs tile counters");
+      YGG_CHECK_ARG(kind == kEpiNone || g->cluster > 0 || e.counters != nullptr, "fused epilogue needs tile counters");
       YGG_CHECK_ARG(!e.ss_in || g->M <= kMaxRstdTokens, "too many tokens for the folded RMSNorm");
       YGG_CHECK_ARG(!e.ss_in || (e.ss_tiles >= 1 && e.norm_dim >= 1), "bad RMSNorm fold arguments");
       if (kind == kEpiStoreF32) YGG_CHECK_ARG(e.out && e.ld >= g->N, "STORE_F32 needs out / ld");
@@ -1085,6 +1321,16 @@ static int gemm_launch(const GemmPlan* g, float* workspace, const ygg_epilogue* 
                       "QKV_ROPE arguments");
       if (kind == kEpiSwiglu) YGG_CHECK_ARG(e.act_out != nullptr, "SWIGLU needs act_out");
       if (kind == kEpiResid) YGG_CHECK_ARG(e.resid && e.hb && e.ss_out, "RESID needs resid / hb / ss_out");
+    }
+    if (g->cluster > 0) {
+      YGG_CHECK_ARG(kind != kEpiNone, "a cluster split-K plan needs a fused epilogue (no partials)");
+      switch (kind) {
+        case kEpiStoreF32: return launch_cluster_kind<kEpiStoreF32>(g, e, s);
+        case kEpiQkvRope: return launch_cluster_kind<kEpiQkvRope>(g, e, s);
+        case kEpiSwiglu: return launch_cluster_kind<kEpiSwiglu>(g, e, s);
+        case kEpiResid: return launch_cluster_kind<kEpiResid>(g, e, s);
+        default: return ygg_fail(YGG_ERR_VALUE, "unknown epilogue kind %d", kind);
+      }
     }
     switch (kind) {
       case kEpiNone:
@@ -1119,9 +1365,52 @@ static int gemm_launch(const GemmPlan* g, float* workspace, const ygg_epilogue* 
   return YGG_OK;
 }
 
+int ygg_gemm_plan_set_cluster(void* plan, int cluster) {
+  GemmPlan* g = const_cast<GemmPlan*>(plan_of(plan));
+  YGG_CHECK_ARG(g != nullptr, "invalid GEMM plan");
+  YGG_CHECK_ARG(cluster >= 0 && cluster <= 16, "cluster size must be in [0, 16]");
+  if (cluster == 0) {
+    g->cluster = 0;
+    return YGG_OK;
+  }
+  YGG_CHECK_ARG(g->dtype == YGG_BF16, "cluster split-K runs on the bf16 tcgen05 path only");
+  YGG_CHECK_ARG(g->kb >= cluster, "fewer k-blocks than cluster CTAs");
+  YGG_CHECK_ARG(cluster_stages(g, cluster) >= 2, "the receive slots leave no room for a two-stage ring");
+  // every cluster must be co-resident (one wave): a second wave would double the GEMM
+  const int keep = g->cluster;
+  g->cluster = cluster;
+  const size_t smem = cluster_smem(g);
+  g->cluster = keep;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(g->tiles * cluster);
+  cfg.blockDim = dim3(kGemmThreads);
+  cfg.dynamicSmemBytes = smem;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = cluster;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  int max_clusters = 0;
+  cudaError_t e = cudaOccupancyMaxActiveClusters(&max_clusters, gemm_cluster_kernel<kEpiResid>, &cfg);
+  if (e != cudaSuccess) return ygg_fail(YGG_ERR_CUDA, "cluster occupancy: %s", cudaGetErrorString(e));
+  if (max_clusters < g->tiles)
+    return ygg_fail(YGG_ERR_UNSUPPORTED, "%d tiles need %d co-resident clusters of %d; only %d fit", g->tiles,
+                    g->tiles, cluster, max_clusters);
+  g->cluster = cluster;
+  return YGG_OK;
+}
+
+int ygg_gemm_plan_cluster(const void* plan) {
+  const GemmPlan* g = plan_of(plan);
+  return g ? g->cluster : -1;
+}
+
 int ygg_gemm_run(const void* plan, float* workspace, ygg_stream_t stream) {
   const GemmPlan* g = plan_of(plan);
   YGG_CHECK_ARG(g != nullptr, "invalid GEMM plan");
+  YGG_CHECK_ARG(g->cluster == 0, "a cluster split-K plan runs through ygg_gemm_fused");
   YGG_CHECK_ARG(workspace != nullptr, "null workspace");
   return gemm_launch(g, workspace, nullptr, reinterpret_cast<cudaStream_t>(stream));
 }

@@ -60,6 +60,29 @@ int launch_pdl_cluster(Kernel kernel, dim3 grid, dim3 block, int cluster_x, cuda
   return YGG_OK;
 }
 
+// PDL launch with a (cluster_x, 1, 1) thread-block cluster and dynamic shared memory.
+template <typename Kernel, typename... Args>
+int launch_pdl_cluster_x(Kernel kernel, dim3 grid, dim3 block, size_t smem, int cluster_x, cudaStream_t stream,
+                         Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled();
+  attr[1].id = cudaLaunchAttributeClusterDimension;
+  attr[1].val.clusterDim.x = cluster_x;
+  attr[1].val.clusterDim.y = 1;
+  attr[1].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 2;
+  cudaError_t err = cudaLaunchKernelEx(&cfg, kernel, args...);
+  if (err != cudaSuccess) return ygg_fail(YGG_ERR_CUDA, "cluster launch failed: %s", cudaGetErrorString(err));
+  return YGG_OK;
+}
+
 // PDL launch with a (1, 1, cluster_z) thread-block cluster and dynamic shared memory.
 template <typename Kernel, typename... Args>
 int launch_pdl_cluster_z(Kernel kernel, dim3 grid, dim3 block, size_t smem, int cluster_z, cudaStream_t stream,

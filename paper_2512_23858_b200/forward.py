@@ -60,6 +60,7 @@ class GemmPlan:
         self.ws_bytes = wsb.value
         self.W, self.X = W, X  # keep alive
         self.epi = None  # L.YggEpilogue for the fused path
+        self.cluster = 0  # > 0: cluster split-K (Forward._try_cluster)
 
     @property
     def handle(self):
@@ -350,6 +351,10 @@ class Forward:
                 setattr(e, k, v)
             return e
 
+        if self.plan.cluster_split_k:
+            for p in self.plans:
+                for name in ("qkv", "o", "gu", "down"):
+                    self._try_cluster(p[name])
         for li, p in enumerate(self.plans):
             cache_l = self.cache.data_ptr() + li * self.layer_stride * es
             cur["plan"] = p["qkv"]
@@ -370,6 +375,16 @@ class Forward:
             cur["plan"] = self.lm_plan
             self.lm_plan.epi = epi(L.YGG_EPI_STORE_F32, ss_in=self.ss_a.data_ptr(), ss_tiles=nt, norm_dim=d, eps=eps,
                                    out=self.logits.data_ptr(), ld=cfg.vocab)
+
+    def _try_cluster(self, gp: GemmPlan) -> None:
+        """Cluster split-K for a GEMM whose tiles, times a cluster of 2-4 CTAs, fill one wave."""
+        lib = L.lib()
+        sms = torch.cuda.get_device_properties(self.cache.device).multi_processor_count
+        gp.cluster = 0
+        for cs in (4, 3, 2):
+            if gp.tiles * cs <= sms and lib.ygg_gemm_plan_set_cluster(gp.handle, cs) == L.YGG_OK:
+                gp.cluster = cs
+                return
 
     def weight_bytes(self) -> int:
         """Algorithmic HBM bytes of the matmul weights streamed per pass."""

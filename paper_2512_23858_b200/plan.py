@@ -46,7 +46,9 @@ class ForwardPlan:
     # the decode attention for passes whose row tiles fit one wave)
     gemv: bool | None = None
     decode_attn: bool | None = None
-    fused_epilogues: bool = False   # fused-epilogue stream-K GEMMs (weights in the fused layout)
+    fused_epilogues: bool = False   # fused-epilogue GEMMs for every non-GEMV bf16 pass (fused weight layout)
+    cluster_split_k: bool = True    # fused-epilogue GEMMs whose tiles x cluster fill one wave run as cluster
+    #                                 split-K with a DSMEM reduction (csrc/gemm.cu gemm_cluster_kernel)
     lm_store_fused: bool = True     # LM-head logits straight from TMEM (no partials round trip)
     topk_fused: bool = True         # draft top-k partials from the LM-head GEMV epilogue
     attn_kvsplit: int = 0           # decode attention cluster size (0 = automatic)

@@ -19,8 +19,15 @@ sd.prefill(bench.prompts_for(wl, tc.vocab, 0))
 for _ in range(2):
     sd.step(use_graph=False)
 torch.cuda.synchronize()
-f = sd.verify if which == "verify" else sd.draft
-g = Forward(f.cfg, f.w, f.cache, f.B, f.R, f.mask_words, f.act_dtype)
+f = sd.verify if which.startswith("verify") else sd.draft
+if which == "verify_fused":  # fused layout + cluster split-K on a separate weight copy
+    from paper_2512_23858_b200.model import weights_to
+    from paper_2512_23858_b200.plan import ForwardPlan
+
+    g = Forward(f.cfg, weights_to(sd.tw, f.cache.device), f.cache, f.B, f.R, f.mask_words, f.act_dtype,
+                plan=ForwardPlan(fused_epilogues=True, cluster_split_k="nocluster" not in sys.argv))
+else:
+    g = Forward(f.cfg, f.w, f.cache, f.B, f.R, f.mask_words, f.act_dtype)
 for t in ("tokens", "pos", "slot", "req", "qmask", "blk_start", "blk_len"):
     getattr(g, t).copy_(getattr(f, t))
 lib = L.lib()
@@ -108,7 +115,7 @@ tot, gaps, seen = {}, {}, {}
 for r in rows:
     k = r["k"]
     seen[k] = seen.get(k, 0) + 1
-    per_layer = {"gemv": 5, "gemm": 4, "epi_resid": 2}.get(k)  # gemv: qkv/attn/o/gu/down slots by index
+    per_layer = {"gemv": 5, "gemm": 4, "epi_resid": 2, "attn_dec": 1}.get(k)  # gemv: qkv/attn/o/gu/down slots by index
     if k == "gemv":
         key = f"gemv#{r['i'] % 5 if r['i'] < n - 1 else 'lm'}"
     elif per_layer:

@@ -1,7 +1,8 @@
 """Fused tcgen05 GEMM epilogues vs torch fp64 references of the same bf16 operands.
 
-Covers single-segment tiles (finished from TMEM) and multi-segment stream-K tiles (last-arrival
-reduction), via different CTA counts.  Tolerance: 2e-3 relative to the output scale (bf16
+Covers single-segment tiles (finished from TMEM), multi-segment stream-K tiles (last-arrival
+reduction), via different CTA counts, and cluster split-K plans ("cN": N CTAs per tile, partials
+reduced through DSMEM in the cluster's leader).  Tolerance: 2e-3 relative to the output scale (bf16
 operands are exact; f32 accumulation order differs), and bf16 rounding of stored outputs.
 """
 
@@ -14,8 +15,15 @@ pytestmark = pytest.mark.gpu
 
 
 def _plan(W, X, M, ctas):
+    """ctas: stream-K CTA count (0 = default), or "cN" = cluster split-K with N CTAs per tile."""
+    from paper_2512_23858_b200 import _lib as L
     from paper_2512_23858_b200.forward import GemmPlan
 
+    if isinstance(ctas, str):
+        p = GemmPlan(W, X, M, 0)
+        L.check(L.lib().ygg_gemm_plan_set_cluster(p.handle, int(ctas[1:])))
+        assert L.lib().ygg_gemm_plan_cluster(p.handle) == int(ctas[1:])
+        return p
     return GemmPlan(W, X, M, ctas)
 
 
@@ -39,17 +47,21 @@ def _epi(kind, counters, **kw):
     return e
 
 
-@pytest.mark.parametrize("ctas", [0, 5, 37])
+@pytest.mark.parametrize("ctas", [0, 5, 37, "c1", "c2", "c3", "c4"])
 @pytest.mark.parametrize("M", [8, 50, 300])
 def test_store_f32_with_rstd(ctas, M, cuda):
     from paper_2512_23858_b200 import _lib as L
 
     N, K = 1024, 512
-    g = torch.Generator(device="cuda").manual_seed(M + ctas)
+    g = torch.Generator(device="cuda").manual_seed(M + len(str(ctas)))
     X = torch.randn(M, K, device=cuda, generator=g).to(torch.bfloat16)
     W = (torch.randn(N, K, device=cuda, generator=g) / math.sqrt(K)).to(torch.bfloat16)
     ss = torch.rand(4, M, device=cuda, generator=g) * 100
     out = torch.zeros(M, N, device=cuda)
+    if ctas in ("c3", "c4") and M > 256:  # BN = 256: the receive slots leave no room for a ring
+        with pytest.raises(ValueError, match="ring"):
+            _plan(W, X, M, ctas)
+        return
     plan = _plan(W, X, M, ctas)
     cnt = torch.zeros(plan.tiles, dtype=torch.int32, device=cuda)
     _run(plan, _epi(L.YGG_EPI_STORE_F32, cnt, ss_in=ss.data_ptr(), ss_tiles=4, norm_dim=512, eps=1e-5,
@@ -65,13 +77,13 @@ def test_store_f32_with_rstd(ctas, M, cuda):
     assert torch.equal(out, first)
 
 
-@pytest.mark.parametrize("ctas", [0, 11])
+@pytest.mark.parametrize("ctas", [0, 11, "c2", "c4"])
 def test_resid_and_swiglu(ctas, cuda):
     from paper_2512_23858_b200 import _lib as L
     from paper_2512_23858_b200.model import gate_up_interleave, preset
 
     M, d, F = 40, 512, 768
-    g = torch.Generator(device="cuda").manual_seed(ctas + 3)
+    g = torch.Generator(device="cuda").manual_seed(len(str(ctas)) + 3)
     # RESID: resid += X W^T, hb = bf16(resid), ss per 128-feature tile
     X = torch.randn(M, F, device=cuda, generator=g).to(torch.bfloat16)
     W = (torch.randn(d, F, device=cuda, generator=g) / math.sqrt(F)).to(torch.bfloat16)
@@ -102,7 +114,7 @@ def test_resid_and_swiglu(ctas, cuda):
 
 
 @pytest.mark.parametrize("hd,Hq,Hkv", [(64, 4, 2), (128, 8, 2)])
-@pytest.mark.parametrize("ctas", [0, 9])
+@pytest.mark.parametrize("ctas", [0, 9, "c3", "c4"])
 def test_qkv_rope_kv_append(hd, Hq, Hkv, ctas, cuda):
     from oracle.llama_ref import rope
     from paper_2512_23858_b200 import _lib as L
@@ -110,7 +122,7 @@ def test_qkv_rope_kv_append(hd, Hq, Hkv, ctas, cuda):
 
     M, d, S, B = 12, 256, 64, 2
     cfg = preset("tiny-target", d_model=d, n_heads=Hq, n_kv_heads=Hkv, head_dim=hd)
-    g = torch.Generator(device="cuda").manual_seed(hd + ctas)
+    g = torch.Generator(device="cuda").manual_seed(hd + len(str(ctas)))
     X = torch.randn(M, d, device=cuda, generator=g).to(torch.bfloat16)
     W = (torch.randn(cfg.qkv_dim, d, device=cuda, generator=g) / math.sqrt(d)).to(torch.bfloat16)
     Wp = W[qkv_row_permutation(cfg).to(cuda)].contiguous()

@@ -478,6 +478,10 @@ def run_ours(args, rank, world, local_rank):
         if sample:
             sd.set_uniforms(i, rank)
         sd.step()
+    # The timed window is the first K steps after a fresh prefill of the same prompts, so that the
+    # end-to-end run below (prefill + the same K steps through the public API) decodes exactly the
+    # same steps: greedy (and seeded SAMPLE) decoding is deterministic.
+    sd.prefill(prompts)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -489,7 +493,7 @@ def run_ours(args, rank, world, local_rank):
     evs[0].record()
     for i in range(args.steps):
         if sample:  # host-pregenerated acceptance uniforms, default_rng([seed, step]) (simulator.py:306)
-            sd.set_uniforms(args.warmup + i, rank)
+            sd.set_uniforms(i, rank)
         sd.step()
         evs[i + 1].record()
     torch.cuda.synchronize()
@@ -511,7 +515,7 @@ def run_ours(args, rank, world, local_rank):
     aal = tokens / (args.steps * sd.B)
 
     # ---- e2e through the public API: pinned H2D of the step inputs, replay, D2H of the emitted tokens
-    e2e = e2e_run(sd, prompts, args.steps, device)
+    e2e = e2e_run(sd, prompts, args.steps, device, rank)
     e2e_tokens = torch.tensor([e2e["tokens"]], dtype=torch.float64, device=device)
     e2e_t = torch.tensor([e2e["seconds"]], dtype=torch.float64, device=device)
     if world > 1:
@@ -556,8 +560,8 @@ def run_ours(args, rank, world, local_rank):
                 "h2d_bytes_per_step": e2e["h2d"], "d2h_bytes_per_step": e2e["d2h"],
                 "ms_per_step": round(float(e2e_t) * 1e3 / args.steps, 4),
                 "aal": round(e2e["tokens"] / (args.steps * sd.B), 4),
-                "note": "prompt H2D + prefill + K steps with streamed per-step readback, all timed; "
-                        "its own AAL (fresh prefill, same prompt)"},
+                "note": "prompt H2D + prefill + the same K steps as the timed window (fresh prefill of "
+                        "the same prompt; deterministic decoding) with streamed per-step readback, all timed"},
         "gpu_launches": launches_per_step * args.steps, "launches_per_step": launches_per_step,
         "clocks": clk, "cpu_baseline": cpu, "peak_kind": peak_kind, "gathered": gathered, "ar_baseline": ar,
         "speculative_speedup_vs_ar": round((tokens_all / total_s) / (world * ar["tokens_per_s"]), 3) if ar else None,
@@ -565,7 +569,7 @@ def run_ours(args, rank, world, local_rank):
     print(json.dumps(line), flush=True)
 
 
-def e2e_run(sd, prompts, steps, device):
+def e2e_run(sd, prompts, steps, device, rank=0):
     """End to end through the public API, as a user serving one batch: the prompts go host -> device
     from pinned memory, the decoder prefills them, then every step (SAMPLE: after the H2D of its
     acceptance uniforms from a pinned double buffer) replays the step graph and its emitted tokens come
@@ -591,7 +595,7 @@ def e2e_run(sd, prompts, steps, device):
     gen0 = sd.seq.n_gen.clone()
     for i in range(steps):
         if sample:  # pinned double-buffered H2D of this step's uniforms, enqueued before the replay
-            sd.set_uniforms(10_000 + i, 0)
+            sd.set_uniforms(i, rank)
         sd.step()
         sd.read_emitted(host_out[i % 2])
         done[i % 2].record()

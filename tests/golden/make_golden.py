@@ -197,6 +197,26 @@ def main(src: str) -> None:
         "trace": [[r.iteration, r.d_draft, r.tree_size, r.w_verify, r.accepted_len, hx(r.step_us)]
                   for r in stats.trace[:128]],
     }
+    # ---- depth predictor training (depth_predictor.py:149-344) on the reference's own profiling
+    # samples (collect_depth_samples, simulator.py:553-579) of the example config
+    from specsim import depth_predictor as dp
+
+    samples = simulator.collect_depth_samples(cfg, 160, probe_depth=8)
+    runs = []
+    for tc in (dp.TrainConfig(epochs=40), dp.TrainConfig(hidden=8, epochs=25, batch_size=16, seed=3, max_depth=12)):
+        res = dp.train_predictor(samples, tc)
+        pr = res.predictor
+        runs.append({"config": {"hidden": tc.hidden, "epochs": tc.epochs, "batch_size": tc.batch_size,
+                                "seed": tc.seed, "max_depth": tc.max_depth, "learning_rate": hx(tc.learning_rate),
+                                "head_depths": list(tc.head_depths)},
+                     "w1": [[hx(v) for v in row] for row in pr.w1], "b1": [hx(v) for v in pr.b1],
+                     "w2": [[hx(v) for v in row] for row in pr.w2], "b2": [hx(v) for v in pr.b2],
+                     "mean": [hx(v) for v in pr.feature_mean], "std": [hx(v) for v in pr.feature_std],
+                     "initial_loss": hx(res.initial_loss), "final_loss": hx(res.final_loss),
+                     "predictions": [pr.predict(s.features) for s in samples],
+                     "heads0": {str(k): hx(v) for k, v in pr.head_outputs(samples[0].features).items()}})
+    golden["depth_predictor"] = {"samples": [[[hx(v) for v in s.features], s.realized_len] for s in samples],
+                                 "runs": runs}
     for name, val in golden.items():
         if isinstance(val, (list, dict)) and name not in ("source", "numpy"):
             (OUT / f"{name}.json").write_text(json.dumps(val, indent=None, sort_keys=True) + "\n")

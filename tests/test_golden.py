@@ -121,3 +121,29 @@ def test_plan_search_host(i):
     assert res.per_token_us == fx(case["per_token"])
     assert {k: [fx(a), fx(b)] for k, (a, b) in [(k, v) for k, v in case["timeline"].items()]} == {
         k: list(v) for k, v in res.timeline.entries.items()}
+
+
+def test_depth_predictor_training_matches_reference():
+    """train_predictor / MlpPredictor (depth_predictor.py:149-344) on the reference's own profiling
+    samples: bit-identical weights, losses, head outputs and per-sample depth choices."""
+    from paper_2512_23858_b200.depth_predictor import DepthSample, MlpPredictor, TrainConfig, train_predictor
+
+    g = load("depth_predictor")
+    samples = [DepthSample(np.array([fx(v) for v in f]), n) for f, n in g["samples"]]
+    for run in g["runs"]:
+        c = run["config"]
+        tc = TrainConfig(hidden=c["hidden"], epochs=c["epochs"], batch_size=c["batch_size"], seed=c["seed"],
+                         max_depth=c["max_depth"], learning_rate=fx(c["learning_rate"]),
+                         head_depths=tuple(c["head_depths"]))
+        res = train_predictor(samples, tc)
+        p = res.predictor
+        assert [[v.hex() for v in row] for row in p.w1.tolist()] == run["w1"]
+        assert [v.hex() for v in p.b1.tolist()] == run["b1"]
+        assert [[v.hex() for v in row] for row in p.w2.tolist()] == run["w2"]
+        assert [v.hex() for v in p.b2.tolist()] == run["b2"]
+        assert [v.hex() for v in p.feature_mean.tolist()] == run["mean"]
+        assert [v.hex() for v in p.feature_std.tolist()] == run["std"]
+        assert res.initial_loss.hex() == run["initial_loss"] and res.final_loss.hex() == run["final_loss"]
+        assert [p.predict(s.features) for s in samples] == run["predictions"]
+        assert {str(k): v.hex() for k, v in p.head_outputs(samples[0].features).items()} == run["heads0"]
+        assert MlpPredictor.from_dict(p.to_dict()).to_dict() == p.to_dict()

@@ -139,6 +139,9 @@ typedef struct {
   int32_t w_draft;     /* TreeShape.w_draft for Eq.3 */
   int32_t fixed_k;     /* >0: skip the objective and keep exactly min(fixed_k, cap) nodes */
   int32_t probs_are_gains; /* 1: `probs` already holds the per-node gains (SubtreeKnapsack(tree, gains, k)) */
+  const double* node_table; /* optional [B, cap] calibrated acceptance per node position (an ExplicitAcceptance,
+                               acceptance.py:106-129, keyed by the grown-tree index); entries < 0 fall back to
+                               `probs` / tree.prob; NULL = off */
 } ygg_prune_args;
 
 /* probs [B, cap] f64 acceptance probabilities (freeze_probs); NULL = use tree.prob.
@@ -150,6 +153,13 @@ int ygg_knapsack_prune(ygg_tree tree, const double* probs, const ygg_profile_pai
                        ygg_prune_args args, int32_t* keep_idx, int32_t* new_idx, int32_t* w_verify,
                        double* expected_aal, double* speedup, double* aal_at_cap, double* speedup_at_cap,
                        double* best_table, uint8_t* alloc_table, ygg_stream_t stream);
+
+/* Acceptance statistics of one step, per grown-tree node position (pooled over requests): for every
+ * verified node whose parent was accepted (the root always), counts[2g] += 1 (tested) and, if it was
+ * accepted itself, counts[2g+1] += 1, where g = keep_idx[b][j] is the verified node's grown index.
+ * counts [keep_cap][2] u32 (caller zeroes).  Feeds the calibrated node_table of ygg_knapsack_prune. */
+int ygg_accept_stats(ygg_tree vtree, const int32_t* keep_idx, int keep_cap, const int32_t* path,
+                     const int32_t* path_len, uint32_t* counts, ygg_stream_t stream);
 
 /* path_products (acceptance.py:176-184): out[b,0] = p[b,0]; out[b,i] = out[b,parent(i)] * p[b,i] (f64,
  * index order); probs NULL = tree.prob. */
@@ -364,10 +374,13 @@ int ygg_gemv_run(const void* plan, const ygg_gemv_epilogue* epi, ygg_stream_t st
  * chunk with an online softmax (no split-KV partials, no combine launch); prefix keys always visible,
  * block keys by the row's tree-mask bits (causal when mask_words == 0).  q [B*T][Hq][hd]; cache_layer as for ygg_attn_plan_init;
  * out [B*T][Hq][hd] bf16.  kvsplit = CTAs per cluster splitting the keys (0 = automatic: as many as
- * fit one wave, at most 4; capped at 4 for hd 128 and 8 for hd 64). */
+ * fit one wave, at most 4; capped at 4 for hd 128 and 8 for hd 64); ksplit = key-split warp groups
+ * inside a CTA (0 = automatic: 8 warps / row warps, at most 2 for hd 128).  The partials merge in
+ * fixed order, so two plans with the same (kvsplit, ksplit) reduce identically whatever their row
+ * count (the lossless-greedy identity between a tree verify and AR decoding relies on it). */
 size_t ygg_attn_dec_plan_size(void);
 int ygg_attn_dec_plan_init(void* plan, const void* q, const void* cache_layer, int B, int T, int Hq, int Hkv, int hd,
-                           int S, int kvsplit);
+                           int S, int kvsplit, int ksplit);
 /* Launch order contract (programmatic dependent launch): K / V chunks wholly inside the committed
  * prefix (keys < blk_start) and blk_start / blk_len are read BEFORE the grid-dependency wait, so they
  * must have been written at least two kernels earlier on the stream and the kernel immediately

@@ -84,6 +84,7 @@ class YggPruneArgs(C.Structure):
         ("w_draft", C.c_int32),
         ("fixed_k", C.c_int32),
         ("probs_are_gains", C.c_int32),
+        ("node_table", vp),
     ]
 
 
@@ -130,6 +131,7 @@ _SIGS: dict[str, tuple] = {
     "ygg_egt_grow_level": (C.c_int, [YggTree, C.c_int, C.c_int, C.c_int, vp, vp, vp, vp]),
     "ygg_build_mask": (C.c_int, [YggTree, vp]),
     "ygg_knapsack_prune": (C.c_int, [YggTree, vp, vp, YggPruneArgs, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp]),
+    "ygg_accept_stats": (C.c_int, [YggTree, vp, C.c_int, vp, vp, vp, vp]),
     "ygg_tree_subtree": (C.c_int, [YggTree, YggTree, vp, vp, vp]),
     "ygg_path_products": (C.c_int, [YggTree, vp, vp, vp]),
     "ygg_accept": (C.c_int, [YggTree, C.c_int, vp, vp, C.c_int, vp, vp, C.c_int, C.c_int, C.c_int, vp, C.c_float,
@@ -170,7 +172,8 @@ _SIGS: dict[str, tuple] = {
     "ygg_trace_arm": (C.c_int, [vp, C.c_int]),
     "ygg_trace_used": (C.c_int, [vp, C.c_int]),
     "ygg_attn_dec_plan_size": (C.c_size_t, []),
-    "ygg_attn_dec_plan_init": (C.c_int, [vp, vp, vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int]),
+    "ygg_attn_dec_plan_init": (C.c_int, [vp, vp, vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
+                                         C.c_int]),
     "ygg_attn_dec_workspace_size": (C.c_size_t, [vp]),
     "ygg_attn_dec_run": (C.c_int, [vp, vp, vp, vp, C.c_int, C.c_float, vp, vp, vp]),
     "ygg_gemv_plan_size": (C.c_size_t, []),

@@ -600,7 +600,7 @@ size_t ygg_attn_dec_workspace_size(const void* plan) {
 }
 
 int ygg_attn_dec_plan_init(void* plan, const void* q, const void* cache_layer, int B, int T, int Hq, int Hkv, int hd,
-                           int S, int kvsplit) {
+                           int S, int kvsplit, int ksplit) {
   YGG_CHECK_ARG(plan && q && cache_layer, "null pointer");
   YGG_CHECK_ARG(hd == 64 || hd == 128, "head dim must be 64 or 128");
   YGG_CHECK_ARG(Hkv >= 1 && Hq % Hkv == 0, "bad head grouping");
@@ -623,6 +623,7 @@ int ygg_attn_dec_plan_init(void* plan, const void* q, const void* cache_layer, i
   const int nw = (p->rows + 15) / 16;
   p->ksplit = kMaxWarps / nw;            // split the key chunks over the remaining warps
   if (hd == 128 && p->ksplit > 2) p->ksplit = 2;  // register budget of the 128-wide accumulators
+  if (ksplit > 0 && ksplit * nw <= kMaxWarps && !(hd == 128 && ksplit > 2)) p->ksplit = ksplit;
   p->warps = nw * p->ksplit;
   // Key chunks are split over ksplit warp groups inside a CTA and over a (1, 1, kvsplit) cluster of
   // CTAs; the cluster's partials meet in the leader CTA's shared memory.  Default kvsplit: as many

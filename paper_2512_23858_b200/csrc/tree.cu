@@ -638,9 +638,11 @@ __global__ void __launch_bounds__(kKnapThreads) knapsack_prune_kernel(
     // Stage parents and node probabilities in shared memory with every thread (one round trip),
     // so thread 0's in-order product chain below reads on-chip operands only.
     const double* pr = probs ? probs + tb : t.prob + tb;
+    const double* tab = args.node_table ? args.node_table + tb : nullptr;
     for (int i = threadIdx.x; i < N; i += blockDim.x) {
       par[i] = t.parent[tb + i];
-      gain[i] = pr[i];
+      const double c = tab ? tab[i] : -1.0;
+      gain[i] = c >= 0.0 ? c : pr[i];
     }
   }
   __syncthreads();
@@ -994,6 +996,32 @@ __global__ void __launch_bounds__(kAcceptThreads) accept_kernel(
 }
 
 // ===========================================================================
+// Acceptance statistics per grown-tree position (calibrated acceptance for the Eq.3 objective).
+// ===========================================================================
+__global__ void accept_stats_kernel(ygg_tree vt, const int32_t* __restrict__ keep_idx, int keep_cap,
+                                    const int32_t* __restrict__ path, const int32_t* __restrict__ path_len,
+                                    uint32_t* __restrict__ counts) {
+  pdl_wait();
+  pdl_launch_dependents();
+  const int b = blockIdx.x;
+  const size_t tb = static_cast<size_t>(b) * vt.cap;
+  const int N = vt.size[b];
+  const int n = path_len[b];
+  __shared__ unsigned char on_path[256];
+  for (int i = threadIdx.x; i < N; i += blockDim.x) on_path[i] = 0;
+  __syncthreads();
+  for (int i = threadIdx.x; i < n; i += blockDim.x) on_path[path[tb + i]] = 1;
+  __syncthreads();
+  for (int j = threadIdx.x; j < N; j += blockDim.x) {
+    const int p = vt.parent[tb + j];
+    if (p >= 0 && !on_path[p]) continue;  // parent rejected: this node was never tested
+    const int g = keep_idx[static_cast<size_t>(b) * keep_cap + j];
+    atomicAdd(counts + 2 * g, 1u);
+    if (on_path[j]) atomicAdd(counts + 2 * g + 1, 1u);
+  }
+}
+
+// ===========================================================================
 // KV compaction of the accepted path (new; the map is derived from accepted_path).
 // ===========================================================================
 template <typename T>
@@ -1184,6 +1212,15 @@ int ygg_knapsack_prune(ygg_tree tree, const double* probs, const ygg_profile_pai
   YGG_LAUNCH_PDL(knapsack_prune_kernel, dim3(tree.B), dim3(kKnapThreads), smem, reinterpret_cast<cudaStream_t>(stream),
                  tree, probs, profiles_dev, args, keep_idx, new_idx, w_verify, expected_aal, speedup, aal_at_cap,
                  speedup_at_cap, best_table, alloc_table);
+  return YGG_OK;
+}
+
+int ygg_accept_stats(ygg_tree vtree, const int32_t* keep_idx, int keep_cap, const int32_t* path,
+                     const int32_t* path_len, uint32_t* counts, ygg_stream_t stream) {
+  YGG_CHECK_ARG(keep_idx && path && path_len && counts, "null pointer");
+  YGG_CHECK_ARG(vtree.cap <= 256 && keep_cap >= vtree.cap, "verify trees are limited to 256 nodes");
+  YGG_LAUNCH_PDL(accept_stats_kernel, dim3(vtree.B), dim3(128), 0, reinterpret_cast<cudaStream_t>(stream), vtree,
+                 keep_idx, keep_cap, path, path_len, counts);
   return YGG_OK;
 }
 

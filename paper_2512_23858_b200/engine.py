@@ -70,7 +70,15 @@ class SpecDecoder:
         prefill_len: int = 0,
         device="cuda",
         plan: ForwardPlan | None = None,
+        share: "SpecDecoder | None" = None,
+        scratch: int = 0,
+        calibrate: bool = False,
     ):
+        """``share``: another decoder whose sequence state, KV caches and prefill forwards this one
+        uses (one decoding state, several captured step shapes: runtime.AdaptiveDecoder); ``scratch``:
+        tree / padding slots to reserve past the prefix (default this shape's); ``calibrate``: the
+        Eq.3 objective uses per-position acceptance rates measured on the device (set_node_table)
+        instead of the draft's surrogate probabilities wherever a rate is known."""
         L.require_device()
         if target_cfg.vocab != draft_cfg.vocab:
             raise ValueError("target and draft must share a vocabulary")
@@ -87,19 +95,30 @@ class SpecDecoder:
         self.vcap = min(shape.max_verify, self.tree_cap)
         self.T = self.vcap + 1
         self.R = max(W, 2)
-        scratch = self.tree_cap + self.R + 8
-        self.S = (max_seq + scratch + 63) // 64 * 64
+        scratch = max(scratch, self.tree_cap + self.R + 8)
         dev = torch.device(device)
         self.dev = dev
-        # commit freezes a request rather than let the next step's tree / scratch slots pass S
-        self.seq = SeqState(batch, self.S, device=dev, p_limit=self.S - scratch)
-        self.tcache = new_cache(target_cfg, batch, self.S, act_dtype, dev)
-        self.dcache = new_cache(draft_cfg, batch, self.S, act_dtype, dev)
+        if share is not None:
+            if share.B != batch or share.tc is not target_cfg or share.dc is not draft_cfg:
+                raise ValueError("a shared decoding state needs the same batch and models")
+            if share.S - share.seq.p_limit < scratch:
+                raise ValueError("the shared state reserves too few scratch slots for this shape")
+            self.S, self.seq, self.tcache, self.dcache = share.S, share.seq, share.tcache, share.dcache
+        else:
+            self.S = (max_seq + scratch + 63) // 64 * 64
+            # commit freezes a request rather than let the next step's tree / scratch slots pass S
+            self.seq = SeqState(batch, self.S, device=dev, p_limit=self.S - scratch)
+            self.tcache = new_cache(target_cfg, batch, self.S, act_dtype, dev)
+            self.dcache = new_cache(draft_cfg, batch, self.S, act_dtype, dev)
         tmw = max(1, (self.T + 31) // 32)
         dmw = max(1, (self.tree_cap + 31) // 32)
         self.plan = plan
         self.draft = Forward(draft_cfg, draft_w, self.dcache, batch, self.R, dmw, act_dtype, plan=plan)
-        self.verify = Forward(target_cfg, target_w, self.tcache, batch, self.T, tmw, act_dtype, plan=plan)
+        # The verify always runs the target's tree-pass families (stream-K GEMM, decode attention), never
+        # the draft's row-block GEMV even when B * T <= 16: the GEMV needs the fused weight layout (it
+        # would rewrite the shared target weights in place) and would round differently from ARDecoder,
+        # the oracle of the lossless-greedy identity.
+        self.verify = Forward(target_cfg, target_w, self.tcache, batch, self.T, tmw, act_dtype, gemv=False, plan=plan)
         self.grown = DeviceTrees(batch, self.tree_cap, dev)
         self.vtree = DeviceTrees(batch, self.vcap, dev)
         i32 = dict(dtype=torch.int32, device=dev)
@@ -132,7 +151,14 @@ class SpecDecoder:
         self._u_next = 0
         self.set_profiles(profiles)
         self.prefill_len = prefill_len
-        self._prefill_fwd = {}
+        self._prefill_fwd = share._prefill_fwd if share is not None else {}
+        # root candidate probabilities of the step's pass 0 (depth-predictor features)
+        self.root_probs = torch.zeros(batch, k, **f64)
+        # calibrated acceptance (ExplicitAcceptance by grown-tree position): device counts of tested /
+        # accepted per position, and the table the prune objective reads (< 0: surrogate probability)
+        self.calibrate = calibrate
+        self.accept_counts = torch.zeros(self.tree_cap, 2, dtype=torch.int32, device=dev)
+        self.node_table = torch.full((batch, self.tree_cap), -1.0, **f64)
         self.graph = None
         self.step_count = 0
 
@@ -215,6 +241,8 @@ class SpecDecoder:
         dr.run(stream)
         self._draft_topk(rows, k, s)
         chk(lib.ygg_init_roots(g.struct, self.cand_tok.data_ptr(), self.cand_prob.data_ptr(), k, self.R, 1, s))
+        with torch.cuda.stream(stream if stream is not None else torch.cuda.current_stream()):
+            self.root_probs.copy_(self.cand_prob.view(self.B, self.R, k)[:, 1, :])
         stamp(1)
         # ---- draft passes 1..D: grow one level each
         for lvl in range(D):
@@ -227,7 +255,8 @@ class SpecDecoder:
                                        self.cand_n.data_ptr(), s))
         stamp(2)
         # ---- prune (latency-aware objective or fixed width)
-        args = L.YggPruneArgs(sh.max_verify, D, W, sh.fixed_verify, 0)
+        args = L.YggPruneArgs(sh.max_verify, D, W, sh.fixed_verify, 0,
+                              self.node_table.data_ptr() if self.calibrate else None)
         chk(lib.ygg_knapsack_prune(g.struct, None, self.profiles_dev.data_ptr(), args, self.keep_idx.data_ptr(),
                                    self.new_idx.data_ptr(), self.w_verify.data_ptr(), self.exp_aal.data_ptr(),
                                    self.speedup.data_ptr(), None, None, None, None, s))
@@ -253,6 +282,9 @@ class SpecDecoder:
                                None, vf.logits.data_ptr(), L.YGG_F32, self.tc.vocab, self.tc.vocab,
                                self.row_stats.data_ptr(), self.temperature, self.path.data_ptr(),
                                self.path_len.data_ptr(), self.acc_len.data_ptr(), self.bonus.data_ptr(), None, s))
+        if self.calibrate:
+            chk(lib.ygg_accept_stats(vt.struct, self.keep_idx.data_ptr(), self.tree_cap, self.path.data_ptr(),
+                                     self.path_len.data_ptr(), self.accept_counts.data_ptr(), s))
         # ---- KV compaction (target: verify order; draft: grown-tree slots, leaves never drafted)
         tc, dc = self.tc, self.dc
         chk(lib.ygg_kv_compact(self.tcache.data_ptr(), L.dtype_code(self.act_dtype), tc.n_layers, self.B,
@@ -265,6 +297,32 @@ class SpecDecoder:
         chk(lib.ygg_commit(self.seq.struct, vt.struct, self.path.data_ptr(), self.path_len.data_ptr(),
                            self.bonus.data_ptr(), self.emit.data_ptr(), self.emit.shape[1], s))
         stamp(5)
+
+    # ------------------------------------------------------------------
+    def node_rates(self, prior: float = 4.0) -> np.ndarray:
+        """Calibrated acceptance per grown-tree position from the device counts (host sync):
+        p_i = (accepted_i + m r_d) / (tested_i + m) with r_d the pooled rate of i's EGT level (depth
+        d = level of position i: nodes 1 + (d-1) W .. d W) and m = ``prior``; -1 where neither the
+        position nor its level has been tested (the objective then keeps the surrogate probability)."""
+        c = self.accept_counts.cpu().numpy().astype(np.float64)
+        W, D = self.shape.width, self.shape.depth
+        out = np.full(self.tree_cap, -1.0)
+        last = None
+        for d in range(D + 1):
+            lo, hi = (0, 1) if d == 0 else (1 + (d - 1) * W, 1 + d * W)
+            tested, acc = c[lo:hi, 0], c[lo:hi, 1]
+            if tested.sum() > 0:
+                last = acc.sum() / tested.sum()
+            if last is None:
+                continue
+            out[lo:hi] = (acc + prior * last) / (tested + prior)
+        return out
+
+    def set_node_table(self, rates) -> None:
+        """Load per-position acceptance rates (same for every request) into the prune objective's
+        table; takes effect from the next step (stream-ordered copy, no re-capture)."""
+        t = torch.as_tensor(np.asarray(rates, dtype=np.float64)).reshape(1, -1).expand(self.B, -1)
+        self.node_table.copy_(t)
 
     # ------------------------------------------------------------------
     def set_uniforms(self, step_index: int, seed: int, stream=None) -> None:

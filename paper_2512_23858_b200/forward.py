@@ -182,7 +182,7 @@ class Forward:
                 mem = C.create_string_buffer(int(lib.ygg_attn_dec_plan_size()))
                 L.check(lib.ygg_attn_dec_plan_init(mem, self.q.data_ptr(), cache.data_ptr() + li * self.layer_stride * es,
                                                    B, R, cfg.n_heads, cfg.n_kv_heads, cfg.head_dim, self.S,
-                                                   plan.attn_kvsplit))
+                                                   plan.attn_kvsplit, plan.attn_ksplit))
                 self.ad_plans.append(mem)
             self.ad_ws = torch.zeros(int(lib.ygg_attn_dec_workspace_size(self.ad_plans[0])) // 4 + 64,
                                      dtype=torch.float32, device=dev)

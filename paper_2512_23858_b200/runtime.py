@@ -1,0 +1,224 @@
+"""Runtime shape control with real models: per-step choice of the EGT (depth, width) among captured
+step graphs over ONE decoding state (the reference's per-iteration
+depth decision and width selection, pkg/src/specsim/simulator.py:305-324, egt.py:285-318).
+
+* Every candidate ``StepShape`` gets its own ``SpecDecoder`` (forwards, trees, CUDA graph) sharing
+  the first one's sequence state and KV caches, so switching shape between steps costs nothing but
+  choosing which graph to replay.
+* The host decides the shape of step i from a lagged pinned readback of step i - ``lag`` (accepted
+  length, the pass-0 root candidate distribution, the step's device time), so it never waits for
+  the GPU: the reference's loop observes the previous outcome; here the observation is ``lag``
+  steps old (default 2 keeps one step queued ahead).
+* Depth: a reference ``DepthPredictor`` (FixedDepth / EmaHeuristic / MlpPredictor, fed the reference's
+  five features from device data — depth_predictor.DeviceFeatures), snapped to the captured depths.
+* Width at that depth (and, with ``policy="bandit"``, the whole shape): the reference picks the width
+  maximizing the latency-aware objective over provisional trees grown from its synthetic drafter,
+  which a real draft model cannot afford; here each captured shape's realized accepted tokens per
+  device-second is tracked and the best is exploited, after a short round-robin exploration and with
+  a small exploration share — the objective's ratio (expected accepted length over step latency,
+  latency.py:154-161) measured instead of modelled.
+* Calibrated Eq.3: with ``calibrate`` every shape's prune objective (K6) reads per-position acceptance
+  rates accumulated on the device (ygg_accept_stats; an ExplicitAcceptance keyed by grown-tree
+  position, acceptance.py:106-129) instead of the over-confident surrogate draft probabilities,
+  refreshed every ``refresh`` steps.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from .depth_predictor import DeviceFeatures
+from .engine import GREEDY, SAMPLE, SpecDecoder, StepShape
+from .plugins import DepthPredictor
+
+
+@dataclass
+class ShapeStats:
+    steps: int = 0
+    tokens: float = 0.0
+    seconds: float = 0.0
+
+    @property
+    def rate(self) -> float:
+        return self.tokens / self.seconds if self.seconds > 0 else 0.0
+
+
+@dataclass
+class AdaptiveTrace:
+    chosen: list = field(default_factory=list)  # shape index per step
+    accepted: list = field(default_factory=list)  # accepted tokens (all requests) per observed step
+    step_ms: list = field(default_factory=list)
+
+
+class AdaptiveDecoder:
+    def __init__(self, target_cfg, target_w, draft_cfg, draft_w, shapes: list[StepShape], batch: int = 1,
+                 max_seq: int = 2048, act_dtype=torch.bfloat16, mode: str = GREEDY, temperature: float = 1.0,
+                 profiles=None, device="cuda", policy: str = "bandit", predictor: DepthPredictor | None = None,
+                 calibrate: bool = True, refresh: int = 16, explore_steps: int = 2, explore_share: float = 0.05,
+                 lag: int = 2, seed: int = 0, plan=None):
+        if not shapes:
+            raise ValueError("need at least one step shape")
+        if policy not in ("bandit", "predictor"):
+            raise ValueError("policy must be 'bandit' or 'predictor'")
+        if policy == "predictor" and predictor is None:
+            raise ValueError("policy 'predictor' needs a DepthPredictor")
+        if lag < 1:
+            raise ValueError("lag must be >= 1")
+        scratch = max(1 + s.depth * s.width + max(s.width, 2) + 8 for s in shapes)
+        self.shapes = list(shapes)
+        self.decs: list[SpecDecoder] = []
+        for sh in self.shapes:
+            self.decs.append(SpecDecoder(target_cfg, target_w, draft_cfg, draft_w, sh, batch=batch, max_seq=max_seq,
+                                         act_dtype=act_dtype, mode=mode, temperature=temperature, profiles=profiles,
+                                         device=device, share=self.decs[0] if self.decs else None, scratch=scratch,
+                                         calibrate=calibrate, plan=plan))
+        d0 = self.decs[0]
+        self.B, self.seq, self.dev, self.mode = batch, d0.seq, d0.dev, mode
+        self.policy, self.predictor = policy, predictor
+        self.calibrate, self.refresh = calibrate, refresh
+        self.explore_steps, self.explore_share, self.lag = explore_steps, explore_share, lag
+        self.stats = [ShapeStats() for _ in self.shapes]
+        self.features = DeviceFeatures(batch)
+        self._last_features = None
+        self.rng = np.random.default_rng(seed)
+        self.trace = AdaptiveTrace()
+        self._pending: list = []  # (shape index, event pair, pinned acc_len, pinned root probs)
+        kmax = max(s.expansion_k for s in self.shapes)
+        # readback ring: a slot is reused only after its step was observed (ring longer than the lag)
+        self._ring = [(torch.empty(batch, dtype=torch.int32).pin_memory(),
+                       torch.empty(batch, kmax, dtype=torch.float64).pin_memory(),
+                       torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                      for _ in range(lag + 2)]
+        self._issued = [0] * len(self.shapes)
+        self.steps = 0
+        self.prefill_len = 0
+
+    # ------------------------------------------------------------------
+    def prefill(self, prompts: torch.Tensor) -> None:
+        self.prefill_len = prompts.shape[1]
+        self.decs[0].prefill(prompts)
+        for d in self.decs:
+            d.prefill_len = self.prefill_len
+
+    def capture(self) -> None:
+        for d in self.decs:
+            if d.graph is None:
+                d.capture()
+
+    def set_profiles(self, profiles) -> None:
+        for d in self.decs:
+            d.set_profiles(profiles)
+
+    # ------------------------------------------------------------------
+    def _observe(self, block: bool) -> None:
+        """Consume lagged readbacks: shape statistics, predictor / feature state."""
+        while self._pending and (block or len(self._pending) > self.lag - 1):
+            idx, (ea, eb), acc_h, root_h = self._pending.pop(0)
+            eb.synchronize()
+            ms = ea.elapsed_time(eb)
+            acc = acc_h.numpy()
+            st = self.stats[idx]
+            st.steps += 1
+            st.tokens += float(acc.sum())
+            st.seconds += ms * 1e-3
+            self.trace.accepted.append(int(acc.sum()))
+            self.trace.step_ms.append(ms)
+            feats = self.features.update(acc, root_h.numpy())
+            self._last_features = feats[0]
+            if self.predictor is not None:
+                self.predictor.observe(int(acc[0]))
+            if not block:
+                break
+
+    def _choose(self) -> int:
+        n = len(self.shapes)
+        if self.policy == "predictor":
+            cand = list(range(n))
+            if self.predictor.ready:
+                want = self.predictor.predict(self._last_features)
+                depths = sorted({s.depth for s in self.shapes})
+                d = min(depths, key=lambda x: (abs(x - want), x))
+                cand = [i for i in range(n) if self.shapes[i].depth == d]
+        else:
+            cand = list(range(n))
+        # exploration: every candidate a few issued steps first, then a small share
+        for i in cand:
+            if self._issued[i] < self.explore_steps:
+                return i
+        if len(cand) > 1 and self.rng.random() < self.explore_share:
+            return int(self.rng.choice(cand))
+        return max(cand, key=lambda i: (self.stats[i].rate, -i))
+
+    def _refresh_calibration(self) -> None:
+        for d in self.decs:
+            if d.calibrate:
+                d.set_node_table(d.node_rates())
+
+    def step(self) -> int:
+        """Choose a shape, replay its step graph, queue the lagged readback. Returns the shape index."""
+        self._observe(block=False)
+        if self.calibrate and self.steps > 0 and self.steps % self.refresh == 0:
+            self._refresh_calibration()
+        i = self._choose()
+        d = self.decs[i]
+        if self.mode == SAMPLE:
+            d.set_uniforms(self.steps, 0)
+        acc_h, root_h, ea, eb = self._ring[self.steps % len(self._ring)]
+        if len(self._pending) >= len(self._ring):
+            self._observe(block=True)
+        ea.record()
+        d.step(use_graph=d.graph is not None)
+        eb.record()
+        acc_h.copy_(d.acc_len, non_blocking=True)
+        k = d.shape.expansion_k
+        root_h[:, :k].copy_(d.root_probs, non_blocking=True)
+        root_h[:, k:] = 0.0
+        self._pending.append((i, (ea, eb), acc_h, root_h))
+        self._issued[i] += 1
+        self.trace.chosen.append(i)
+        self.steps += 1
+        return i
+
+    def drain(self) -> None:
+        self._observe(block=True)
+
+    def generated(self, b: int = 0) -> list[int]:
+        n = int(self.seq.n_gen[b])
+        return self.seq.hist[b, self.prefill_len : self.prefill_len + n].cpu().tolist()
+
+    def generate(self, prompts: torch.Tensor, n_tokens: int, sync_every: int = 8):
+        B, P0 = prompts.shape
+        if P0 + n_tokens + max(s.depth for s in self.shapes) + 2 > self.seq.p_limit:
+            raise ValueError("prompt + generated tokens do not fit the cache (max_seq too small)")
+        self.prefill(prompts)
+        self.seq.gen_limit.fill_(n_tokens)
+        self.seq.status.zero_()
+        self.capture()
+        steps = 0
+        while True:
+            if steps % sync_every == 0:
+                st = self.seq.status.cpu()
+                if bool((st != 0).all()):
+                    if bool((st & 2).any()):
+                        raise RuntimeError("a request reached the cache capacity before n_tokens")
+                    break
+            self.step()
+            steps += 1
+        self.drain()
+        return [self.generated(b)[:n_tokens] for b in range(self.B)], steps
+
+    def summary(self) -> dict:
+        hist = np.bincount(np.asarray(self.trace.chosen, dtype=np.int64), minlength=len(self.shapes))
+        return {"shapes": [{"depth": s.depth, "width": s.width, "max_verify": s.max_verify, "steps": int(h),
+                            "tokens_per_s": round(st.rate, 2),
+                            "aal": round(st.tokens / st.steps / self.B, 3) if st.steps else None}
+                           for s, h, st in zip(self.shapes, hist, self.stats)]}
+
+
+def rate_ci(st: ShapeStats) -> float:
+    """Half-width proxy of a shape's rate estimate (diagnostic)."""
+    return st.rate / math.sqrt(max(st.steps, 1))

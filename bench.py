@@ -169,9 +169,11 @@ def profile_latency(sd, draft_widths=(1, 2, 4, 8, 16), verify_widths=(1, 17, 33,
 
     from paper_2512_23858_b200.forward import Forward
 
-    def time_fwd(cfg, w, cache, rows):
+    def time_fwd(cfg, w, cache, rows, gemv=None):
         mw = max(1, (rows + 31) // 32)
-        f = Forward(cfg, w, cache, 1, rows, mw, torch.bfloat16)
+        # the target always runs its verify families (never the draft's GEMV, which would also rewrite
+        # the shared target weights into the fused layout)
+        f = Forward(cfg, w, cache, 1, rows, mw, torch.bfloat16, gemv=gemv)
         f.blk_start.fill_(int(sd.seq.P[0]))
         f.blk_len.fill_(rows)
         f.pos.copy_(f.blk_start[0] + torch.arange(rows, dtype=torch.int32, device=cache.device))
@@ -200,72 +202,151 @@ def profile_latency(sd, draft_widths=(1, 2, 4, 8, 16), verify_widths=(1, 17, 33,
         return tuple(out)
 
     dbp = monotone([(w, time_fwd(sd.dc, sd.dw, sd.dcache, max(w, 2))) for w in draft_widths])
-    vbp = monotone([(w, time_fwd(sd.tc, sd.tw, sd.tcache, w)) for w in verify_widths])
+    vbp = monotone([(w, time_fwd(sd.tc, sd.tw, sd.tcache, w, gemv=False)) for w in verify_widths])
     return dbp, vbp
 
 
-def run_cfg3(args, device):
-    """cfg3: profile the draft / verify latency tables on the device (K8), load them into the device
-    table the prune objective reads (Eq.3, latency.py:154-161), then run each of the 12 EGT shapes
-    and report the objective's choice next to the measured best."""
+def cfg3_study(base, prompts, steps: int, warmup: int, learn_steps: int = 128, export: str | None = None) -> dict:  # noqa: C901
+    """cfg3: the latency-aware objective over 12 EGT shapes D in {4, 8, 16} x W in
+    {4, 8} x max_verify in {16, 64} on the cfg2 models.
+
+    1. K8 profiles the draft forward at each level width and the verify at each verify width on the
+       device (LatencyProfile breakpoints) and loads them into the table the prune objective reads.
+    2. Every shape runs alone (one runtime.AdaptiveDecoder holds all 12 step graphs over one decoding
+       state) with the calibrated Eq.3 (per-position acceptance measured on the device during its
+       warm-up): measured tokens/s, realized AAL, and the objective's calibrated expected AAL -> its
+       predicted tokens/s = E[AAL] / (profiled step latency).  The objective's choice is the shape with
+       the best prediction; the measured best is the shape with the best measurement.
+    3. The runtime policy (bandit on measured accepted tokens per device-second) learns over
+       ``learn_steps`` steps, then decodes ``steps`` timed steps from a fresh prefill."""
+    import numpy as np
     import torch
 
+    from paper_2512_23858_b200.engine import StepShape
     from paper_2512_23858_b200.latency import LatencyProfile, latency_at
+    from paper_2512_23858_b200.runtime import AdaptiveDecoder
 
-    wl = dict(WORKLOADS["cfg3"])
-    peak, peak_kind, _ = _peaks()
-    base, tc, dc = build_decoder(wl, "cfg3", device)
-    prompts = prompts_for(wl, tc.vocab, 0)
-    base.prefill(prompts)
+    grid = [(d, w, v) for d in (4, 8, 16) for w in (4, 8) for v in (16, 64)]
     dbp, vbp = profile_latency(base)
 
     class PP:
         drafter = LatencyProfile(dbp, "drafter")
         verifier = LatencyProfile(vbp, "verifier")
 
-    weights = base._bench_weights
-    del base
-    torch.cuda.empty_cache()
-    rows = []
-    for (D, W, V) in wl["sweep"]:
-        w2 = dict(wl, depth=D, width=W, max_verify=V)
-        sd, _, _ = build_decoder(w2, "cfg3", device, weights=weights, profiles=PP)
-        sd.prefill(prompts)
-        sd.capture()
-        for _ in range(args.warmup):
-            sd.step()
-        torch.cuda.synchronize()
-        gen0 = sd.seq.n_gen.clone()
+    if export:
+        from paper_2512_23858_b200.profiler import write_profile_csv
+
+        Path(export).mkdir(parents=True, exist_ok=True)
+        write_profile_csv(list(dbp), Path(export) / "draft_profile.csv")
+        write_profile_csv(list(vbp), Path(export) / "verify_profile.csv")
+    shapes = [StepShape(d, w, 8, v) for d, w, v in grid]
+    ad = AdaptiveDecoder(base.tc, base.tw, base.dc, base.dw, shapes, batch=base.B,
+                         max_seq=prompts.shape[1] + (max(learn_steps, 64) + max(steps, 40) + max(warmup, 24)) * 18 + 64,
+                         profiles=PP, device=base.dev, calibrate=True, explore_steps=6, explore_share=0.05, seed=0)
+    ad.prefill(prompts)
+    ad.capture()
+
+    def timed(fn, n):
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        g0 = ad.seq.n_gen.clone()
         a.record()
-        for _ in range(args.steps):
-            sd.step()
+        for _ in range(n):
+            fn()
         b.record()
         torch.cuda.synchronize()
-        t = a.elapsed_time(b) * 1e-3
-        tokens = int((sd.seq.n_gen - gen0).sum())
-        # objective: Eq.3 speedup of the last step's pruned tree from the profiled table, and the
-        # predicted accepted tokens/s = expected AAL / (D T_d(W) + T_v(w_verify + 1) + T_d(2)) (pass 0)
-        exp_aal = float(sd.exp_aal[0])
-        wv = int(sd.w_verify[0])
-        pred_step_us = (D * latency_at(PP.drafter, max(W, 2)) + latency_at(PP.drafter, 2)
-                        + latency_at(PP.verifier, wv + 1))
-        rows.append({"depth": D, "width": W, "max_verify": V, "tokens_per_s": round(tokens / t, 2),
-                     "ms_per_step": round(t * 1e3 / args.steps, 3), "aal": round(tokens / args.steps, 3),
-                     "w_verify": wv, "expected_aal": round(exp_aal, 3), "eq3_speedup": round(float(sd.speedup[0]), 4),
-                     "predicted_tokens_per_s": round(exp_aal / (pred_step_us * 1e-6), 2)})
-        del sd
-        torch.cuda.empty_cache()
+        return float((ad.seq.n_gen - g0).sum()), a.elapsed_time(b) * 1e-3
+
+    rows = []
+    n_shape = max(steps, 40)  # per-shape window: accepted lengths vary 1..D+2 step to step
+    for i, (d, w, v) in enumerate(grid):
+        dec = ad.decs[i]
+        ad.prefill(prompts)
+        for j in range(max(warmup, 24)):  # warm-up doubles as the calibration window of this shape
+            dec.step()
+            if j % 4 == 3:
+                dec.set_node_table(dec.node_rates())
+        ad.prefill(prompts)
+        exp = []
+
+        def one():
+            dec.step()
+            exp.append(dec.exp_aal.clone())
+
+        tokens, secs = timed(one, n_shape)
+        exp_aal = float(torch.stack(exp).mean())
+        wv = int(dec.w_verify[0])
+        step_us = d * latency_at(PP.drafter, max(w, 2)) + latency_at(PP.drafter, 2) + latency_at(PP.verifier, wv + 1)
+        rows.append({"depth": d, "width": w, "max_verify": v, "tokens_per_s": round(tokens / secs, 2),
+                     "ms_per_step": round(secs * 1e3 / n_shape, 3), "aal": round(tokens / n_shape / base.B, 3),
+                     "calibrated_expected_aal": round(exp_aal, 3), "w_verify_last": wv,
+                     "predicted_tokens_per_s": round(exp_aal * base.B / (step_us * 1e-6), 2)})
     chosen = max(rows, key=lambda r: r["predicted_tokens_per_s"])
     best = max(rows, key=lambda r: r["tokens_per_s"])
-    line = {"metric": "accepted tokens/s", "value": chosen["tokens_per_s"], "unit": "tokens/s", "n_gpus": 1,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": chosen["ms_per_step"],
+    # acceptance of the deepest shape as the reference's DepthDecayAcceptance, for the offline bridge
+    from paper_2512_23858_b200.runtime import fit_depth_decay
+
+    deep = grid.index((16, 8, 64))
+    p0, gamma = fit_depth_decay(ad.decs[deep].accept_counts.cpu().numpy(), 16, 8)
+    if export:
+        from paper_2512_23858_b200.profiler import write_stage_csv
+
+        st = stage_profile(base)
+        D = base.shape.depth
+        write_stage_csv([("Verify", "base", round(st["Verify"], 2)), ("Accept", "base", round(st["Accept"], 2)),
+                         ("BonusSample", "base", 0.0), ("TailDraft", "base", 0.0),
+                         ("HeadDraft", "base", round(st["HeadDraft"], 2)),
+                         ("DraftStep", "base", round(st["DraftLevels"] / D, 2)),
+                         ("PrepareVerify", "base", round(st["Prune"], 2))], Path(export) / "stages.csv")
+        cfg = {"seed": 0, "iterations": 512, "acceptance": {"variant": "depth_decay", "p0": round(p0, 6),
+                                                              "gamma": round(gamma, 6)},
+               "workload": {"variant": "stationary", "drafter": {"variant": "geometric", "top_mass": 0.9,
+                                                                 "decay": 0.9}},
+               "profiles": {"draft": "draft_profile.csv", "verify": "verify_profile.csv"}, "stages": "stages.csv",
+               "policy": {"variant": "egt", "candidate_widths": [1, 2, 4, 8], "max_depth": 16, "max_verify": 64,
+                          "expansion_k": 8, "fallback_depth": 8, "predictor": {"variant": "ema", "window": 4,
+                                                                               "alpha": 0.4}},
+               "plan_search": True}
+        (Path(export) / "config.json").write_text(json.dumps(cfg, indent=2) + "\n")
+    # runtime policy: learn, then a timed window from a fresh prefill
+    ad.prefill(prompts)
+    for _ in range(learn_steps):
+        ad.step()
+        if ad.seq.P.max() > ad.seq.p_limit - 64:
+            ad.drain()
+            ad.prefill(prompts)
+    ad.drain()
+    ad.prefill(prompts)
+    tokens, secs = timed(ad.step, steps)
+    ad.drain()
+    counts = np.bincount(np.asarray(ad.trace.chosen[-steps:], dtype=np.int64), minlength=len(grid))
+    top = int(counts.argmax())
+    res = {"profile": {"drafter": dbp, "verifier": vbp}, "sweep": rows,
+           "depth_decay_fit": {"p0": round(p0, 4), "gamma": round(gamma, 4), "shape": "D16 W8 V64"},
+           "objective_choice": {k: chosen[k] for k in ("depth", "width", "max_verify", "tokens_per_s")},
+           "measured_best": {k: best[k] for k in ("depth", "width", "max_verify", "tokens_per_s")},
+           "objective_vs_best": round(chosen["tokens_per_s"] / best["tokens_per_s"], 4),
+           "adaptive": {"tokens_per_s": round(tokens / secs, 2), "ms_per_step": round(secs * 1e3 / steps, 3),
+                        "learn_steps": learn_steps, "most_used": dict(zip(("depth", "width", "max_verify"), grid[top])),
+                        "most_used_share": round(float(counts[top]) / steps, 3),
+                        "vs_best": round((tokens / secs) / best["tokens_per_s"], 4)}}
+    del ad
+    torch.cuda.empty_cache()
+    return res
+
+
+def run_cfg3(args, device):
+    """--workload cfg3: the cfg3 study as its own JSON line (value = the runtime policy's tokens/s)."""
+    wl = dict(WORKLOADS["cfg3"])
+    base, tc, dc = build_decoder(wl, "cfg3", device)
+    prompts = prompts_for(wl, tc.vocab, 0)
+    base.prefill(prompts)
+    res = cfg3_study(base, prompts, args.steps, args.warmup, export=args.export_profiles)
+    line = {"metric": "accepted tokens/s", "value": res["adaptive"]["tokens_per_s"], "unit": "tokens/s", "n_gpus": 1,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": res["adaptive"]["ms_per_step"],
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic (coupled random-init weights, random prompts)",
-            "config": {"workload": wl["desc"], "chosen": {k: chosen[k] for k in ("depth", "width", "max_verify")},
-                       "measured_best": {k: best[k] for k in ("depth", "width", "max_verify", "tokens_per_s")},
-                       "profile": {"drafter": dbp, "verifier": vbp}},
-            "sweep": rows}
+            "config": {"workload": wl["desc"]}, "cfg3": res}
     print(json.dumps(line), flush=True)
 
 
@@ -643,6 +724,8 @@ def main():
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default="cfg2")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-ar-baseline", action="store_true")
+    ap.add_argument("--export-profiles", default=None,
+                    help="cfg3: write the K8-measured draft / verify latency profiles (reference CSV format) here")
     args = ap.parse_args()
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")

@@ -219,6 +219,27 @@ class AdaptiveDecoder:
                            for s, h, st in zip(self.shapes, hist, self.stats)]}
 
 
+def fit_depth_decay(counts, depth: int, width: int) -> tuple[float, float]:
+    """DepthDecayAcceptance(p0, gamma) (acceptance.py:60-103) fitted to device acceptance counts of one
+    EGT shape ([tree_cap, 2] tested / accepted per grown position, ygg_accept_stats): the level-d
+    conditional acceptance m_d = accepted(level d) / accepted(level d-1) (m_0 = accepted(root) /
+    steps) is the model's level mass p0 * gamma**d; least squares on log m_d."""
+    c = np.asarray(counts, dtype=np.float64)
+    acc = [c[0, 1]] + [c[1 + (d - 1) * width : 1 + d * width, 1].sum() for d in range(1, depth + 1)]
+    steps = c[0, 0]
+    if steps <= 0 or acc[0] <= 0:
+        raise ValueError("no accepted root yet")
+    ds, ys = [0], [math.log(acc[0] / steps)]
+    for d in range(1, depth + 1):
+        if acc[d] > 0 and acc[d - 1] > 0:
+            ds.append(d)
+            ys.append(math.log(acc[d] / acc[d - 1]))
+    if len(ds) < 2:
+        return min(1.0, acc[0] / steps), 1.0
+    slope, icpt = np.polyfit(np.asarray(ds, dtype=np.float64), np.asarray(ys), 1)
+    return float(min(1.0, math.exp(icpt))), float(min(1.0, math.exp(slope)))
+
+
 def rate_ci(st: ShapeStats) -> float:
     """Half-width proxy of a shape's rate estimate (diagnostic)."""
     return st.rate / math.sqrt(max(st.steps, 1))

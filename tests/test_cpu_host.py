@@ -221,3 +221,34 @@ def test_launcher_runs_world2_gloo(tmp_path):
     for rid in range(5):
         g = torch.Generator().manual_seed(1000 + rid)
         assert got["merged"][str(rid)] == greedy_ar(model, torch.randint(0, cfg.vocab, (8,), generator=g).tolist(), 4, 32)
+
+
+def test_measured_b200_bundle_feeds_reference_offline_drivers():
+    """§8 f2: the K8-measured B200 profiles (profiles/b200_cfg2, written by `bench.py --workload cfg3
+    --export-profiles`) are in the reference's on-disk formats: our loaders read them, and — when the
+    reference is installed in baseline/_ref — its own simulator reproduces the committed offline run."""
+    import json
+
+    from paper_2512_23858_b200.latency import latency_at, load_profile
+    from paper_2512_23858_b200.scheduler import StageProfiles
+
+    b = ROOT / "profiles" / "b200_cfg2"
+    d = load_profile(b / "draft_profile.csv", "drafter")
+    v = load_profile(b / "verify_profile.csv", "verifier")
+    assert latency_at(v, 1) > 1000.0 and latency_at(d, 8) < latency_at(v, 1)
+    sp = StageProfiles.from_csv(b / "stages.csv")
+    assert sp.base("Verify") > 0 and sp.base("DraftStep5") == sp.base("DraftStep")
+    ref = ROOT / "baseline" / "_ref"
+    if not (ref / "specsim").exists():
+        pytest.skip("reference not installed in baseline/_ref")
+    import importlib.util
+    import sys
+
+    spec = importlib.util.spec_from_file_location("reference_offline", ROOT / "scripts" / "reference_offline.py")
+    mod = importlib.util.module_from_spec(spec)
+    sys.path.insert(0, str(ref))
+    spec.loader.exec_module(mod)
+    got = mod.main(str(b))
+    want = json.loads((b / "reference_offline.json").read_text())
+    assert got["run"] == want["run"]
+    assert [r["speedup"] for r in got["breakdown"]] == [r["speedup"] for r in want["breakdown"]]

@@ -242,7 +242,8 @@ def cfg3_study(base, prompts, steps: int, warmup: int, learn_steps: int = 128, e
     shapes = [StepShape(d, w, 8, v) for d, w, v in grid]
     ad = AdaptiveDecoder(base.tc, base.tw, base.dc, base.dw, shapes, batch=base.B,
                          max_seq=prompts.shape[1] + (max(learn_steps, 64) + max(steps, 40) + max(warmup, 24)) * 18 + 64,
-                         profiles=PP, device=base.dev, calibrate=True, explore_steps=6, explore_share=0.05, seed=0)
+                         profiles=PP, device=base.dev, calibrate=True, explore_steps=6, explore_share=0.05, seed=0,
+                         proj_dim=8)
     ad.prefill(prompts)
     ad.capture()
 
@@ -321,15 +322,35 @@ def cfg3_study(base, prompts, steps: int, warmup: int, learn_steps: int = 128, e
     ad.drain()
     counts = np.bincount(np.asarray(ad.trace.chosen[-steps:], dtype=np.int64), minlength=len(grid))
     top = int(counts.argmax())
+    bandit = {"tokens_per_s": round(tokens / secs, 2), "ms_per_step": round(secs * 1e3 / steps, 3)}
+    # depth predictor (§8 f3): profile (features, realized length) on the deepest shape, train the
+    # reference's perceptron on them, then let it choose the depth per step (width: best measured)
+    from paper_2512_23858_b200.depth_predictor import TrainConfig, train_predictor
+
+    ad.prefill(prompts)
+    samples = ad.collect_depth_samples(deep, 96)
+    trained = train_predictor(samples, TrainConfig(max_depth=16, epochs=100))
+    ad.policy, ad.predictor = "predictor", trained.predictor
+    ad.prefill(prompts)
+    n0 = len(ad.trace.chosen)
+    ptok, psecs = timed(ad.step, steps)
+    ad.drain()
+    pdepth = np.bincount([grid[i][0] for i in ad.trace.chosen[n0:]], minlength=17)
+    predictor = {"tokens_per_s": round(ptok / psecs, 2), "ms_per_step": round(psecs * 1e3 / steps, 3),
+                 "samples": len(samples), "features": ad.features.dim,
+                 "train_loss": [round(trained.initial_loss, 4), round(trained.final_loss, 4)],
+                 "depth_histogram": {str(d): int(pdepth[d]) for d in (4, 8, 16)},
+                 "vs_best": round((ptok / psecs) / best["tokens_per_s"], 4)}
     res = {"profile": {"drafter": dbp, "verifier": vbp}, "sweep": rows,
            "depth_decay_fit": {"p0": round(p0, 4), "gamma": round(gamma, 4), "shape": "D16 W8 V64"},
            "objective_choice": {k: chosen[k] for k in ("depth", "width", "max_verify", "tokens_per_s")},
            "measured_best": {k: best[k] for k in ("depth", "width", "max_verify", "tokens_per_s")},
            "objective_vs_best": round(chosen["tokens_per_s"] / best["tokens_per_s"], 4),
-           "adaptive": {"tokens_per_s": round(tokens / secs, 2), "ms_per_step": round(secs * 1e3 / steps, 3),
-                        "learn_steps": learn_steps, "most_used": dict(zip(("depth", "width", "max_verify"), grid[top])),
+           "adaptive": {**bandit, "policy": "bandit", "learn_steps": learn_steps,
+                        "most_used": dict(zip(("depth", "width", "max_verify"), grid[top])),
                         "most_used_share": round(float(counts[top]) / steps, 3),
-                        "vs_best": round((tokens / secs) / best["tokens_per_s"], 4)}}
+                        "vs_best": round(bandit["tokens_per_s"] / best["tokens_per_s"], 4)},
+           "predictor": predictor}
     del ad
     torch.cuda.empty_cache()
     return res

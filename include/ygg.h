@@ -161,6 +161,12 @@ int ygg_knapsack_prune(ygg_tree tree, const double* probs, const ygg_profile_pai
 int ygg_accept_stats(ygg_tree vtree, const int32_t* keep_idx, int keep_cap, const int32_t* path,
                      const int32_t* path_len, uint32_t* counts, ygg_stream_t stream);
 
+/* Depth-predictor feature tap: the target's last-token hidden state of each
+ * request — row `stop` of the verify's final-norm output, stop = 0 (bonus row) when nothing was
+ * accepted, else 1 + the last accepted node — copied as f32 to out [B, d].  hidden [B*T, d] bf16. */
+int ygg_feature_tap(const void* hidden, int T, int d, const int32_t* path, int path_cap, const int32_t* path_len,
+                    int B, float* out, ygg_stream_t stream);
+
 /* path_products (acceptance.py:176-184): out[b,0] = p[b,0]; out[b,i] = out[b,parent(i)] * p[b,i] (f64,
  * index order); probs NULL = tree.prob. */
 int ygg_path_products(ygg_tree tree, const double* probs, double* out, ygg_stream_t stream);

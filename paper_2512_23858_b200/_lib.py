@@ -132,6 +132,7 @@ _SIGS: dict[str, tuple] = {
     "ygg_build_mask": (C.c_int, [YggTree, vp]),
     "ygg_knapsack_prune": (C.c_int, [YggTree, vp, vp, YggPruneArgs, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp]),
     "ygg_accept_stats": (C.c_int, [YggTree, vp, C.c_int, vp, vp, vp, vp]),
+    "ygg_feature_tap": (C.c_int, [vp, C.c_int, C.c_int, vp, C.c_int, vp, C.c_int, vp, vp]),
     "ygg_tree_subtree": (C.c_int, [YggTree, YggTree, vp, vp, vp]),
     "ygg_path_products": (C.c_int, [YggTree, vp, vp, vp]),
     "ygg_accept": (C.c_int, [YggTree, C.c_int, vp, vp, C.c_int, vp, vp, C.c_int, C.c_int, C.c_int, vp, C.c_float,

@@ -1021,6 +1021,19 @@ __global__ void accept_stats_kernel(ygg_tree vt, const int32_t* __restrict__ kee
   }
 }
 
+// Feature tap: the target's hidden state at each request's last accepted row (the bonus's context).
+__global__ void feature_tap_kernel(const __nv_bfloat16* __restrict__ hidden, int T, int d,
+                                   const int32_t* __restrict__ path, int path_cap,
+                                   const int32_t* __restrict__ path_len, float* __restrict__ out) {
+  pdl_wait();
+  pdl_launch_dependents();
+  const int b = blockIdx.x;
+  const int n = path_len[b];
+  const int stop = n > 0 ? 1 + path[static_cast<size_t>(b) * path_cap + n - 1] : 0;
+  const __nv_bfloat16* src = hidden + (static_cast<size_t>(b) * T + stop) * d;
+  for (int i = threadIdx.x; i < d; i += blockDim.x) out[static_cast<size_t>(b) * d + i] = __bfloat162float(src[i]);
+}
+
 // ===========================================================================
 // KV compaction of the accepted path (new; the map is derived from accepted_path).
 // ===========================================================================
@@ -1221,6 +1234,14 @@ int ygg_accept_stats(ygg_tree vtree, const int32_t* keep_idx, int keep_cap, cons
   YGG_CHECK_ARG(vtree.cap <= 256 && keep_cap >= vtree.cap, "verify trees are limited to 256 nodes");
   YGG_LAUNCH_PDL(accept_stats_kernel, dim3(vtree.B), dim3(128), 0, reinterpret_cast<cudaStream_t>(stream), vtree,
                  keep_idx, keep_cap, path, path_len, counts);
+  return YGG_OK;
+}
+
+int ygg_feature_tap(const void* hidden, int T, int d, const int32_t* path, int path_cap, const int32_t* path_len,
+                    int B, float* out, ygg_stream_t stream) {
+  YGG_CHECK_ARG(hidden && path && path_len && out && T >= 1 && d >= 1 && B >= 1, "invalid arguments");
+  YGG_LAUNCH_PDL(feature_tap_kernel, dim3(B), dim3(256), 0, reinterpret_cast<cudaStream_t>(stream),
+                 static_cast<const __nv_bfloat16*>(hidden), T, d, path, path_cap, path_len, out);
   return YGG_OK;
 }
 

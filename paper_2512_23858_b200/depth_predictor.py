@@ -178,24 +178,35 @@ def predict_depth(predictor: DepthPredictor, features=None) -> int:
 
 
 class DeviceFeatures:
-    """The reference's five predictor features from a running decoder's device state.
+    """The reference's five predictor features from a running decoder's device state, optionally
+    followed by a fixed random projection of the target's tapped last-token hidden state.
 
-    ``update(acc_len_host, root_probs_host)`` takes one step's lagged pinned readback (accepted length
-    per request, the pass-0 root candidate probabilities per request) and returns the feature vector
-    the next step's depth is predicted from, per request."""
+    ``update(acc_len, root_probs, hidden)`` takes one step's lagged pinned readback (accepted length
+    per request, the pass-0 root candidate probabilities per request, the [B, d] hidden tap or None)
+    and returns, per request, the feature vector the next step's depth is predicted from."""
 
-    def __init__(self, batch: int, history: int = 8, alpha: float = 0.4):
+    def __init__(self, batch: int, history: int = 8, alpha: float = 0.4, hidden_dim: int = 0, proj_dim: int = 0,
+                 seed: int = 0):
         self.states = [FeatureState(history, alpha) for _ in range(batch)]
+        self.proj = None
+        if proj_dim > 0:
+            if hidden_dim <= 0:
+                raise ValueError("a hidden-state projection needs hidden_dim")
+            rng = np.random.default_rng(seed)
+            self.proj = rng.standard_normal((hidden_dim, proj_dim)) / np.sqrt(hidden_dim)
 
-    def update(self, acc_len, root_probs) -> list[np.ndarray]:
+    @property
+    def dim(self) -> int:
+        return len(FEATURE_NAMES) + (self.proj.shape[1] if self.proj is not None else 0)
+
+    def update(self, acc_len, root_probs, hidden=None) -> list[np.ndarray]:
         out = []
-        for st, n, probs in zip(self.states, acc_len, root_probs):
+        for b, (st, n, probs) in enumerate(zip(self.states, acc_len, root_probs)):
             if int(n) >= 1:
                 st.observe(int(n))
-            out.append(st.features([(0, float(p)) for p in probs]))
+            f = st.features([(0, float(p)) for p in probs])
+            if self.proj is not None:
+                h = np.asarray(hidden[b], dtype=np.float64)
+                f = np.concatenate([f, (h / (np.linalg.norm(h) + 1e-12)) @ self.proj])
+            out.append(f)
         return out
-
-    def observe_only(self, acc_len) -> None:
-        for st, n in zip(self.states, acc_len):
-            if int(n) >= 1:
-                st.observe(int(n))

@@ -73,6 +73,7 @@ class SpecDecoder:
         share: "SpecDecoder | None" = None,
         scratch: int = 0,
         calibrate: bool = False,
+        feature_tap: bool = False,
     ):
         """``share``: another decoder whose sequence state, KV caches and prefill forwards this one
         uses (one decoding state, several captured step shapes: runtime.AdaptiveDecoder); ``scratch``:
@@ -158,6 +159,9 @@ class SpecDecoder:
         # accepted per position, and the table the prune objective reads (< 0: surrogate probability)
         self.calibrate = calibrate
         self.accept_counts = torch.zeros(self.tree_cap, 2, dtype=torch.int32, device=dev)
+        # the target's last-token hidden state per request (depth-predictor feature)
+        self.feature_tap = feature_tap and act_dtype == torch.bfloat16
+        self.hidden_tap = torch.zeros(batch, target_cfg.d_model, dtype=torch.float32, device=dev)
         self.node_table = torch.full((batch, self.tree_cap), -1.0, **f64)
         self.graph = None
         self.step_count = 0
@@ -282,6 +286,9 @@ class SpecDecoder:
                                None, vf.logits.data_ptr(), L.YGG_F32, self.tc.vocab, self.tc.vocab,
                                self.row_stats.data_ptr(), self.temperature, self.path.data_ptr(),
                                self.path_len.data_ptr(), self.acc_len.data_ptr(), self.bonus.data_ptr(), None, s))
+        if self.feature_tap:
+            chk(lib.ygg_feature_tap(vf.xn.data_ptr(), self.T, self.tc.d_model, self.path.data_ptr(), self.vcap,
+                                    self.path_len.data_ptr(), self.B, self.hidden_tap.data_ptr(), s))
         if self.calibrate:
             chk(lib.ygg_accept_stats(vt.struct, self.keep_idx.data_ptr(), self.tree_cap, self.path.data_ptr(),
                                      self.path_len.data_ptr(), self.accept_counts.data_ptr(), s))

@@ -59,7 +59,7 @@ class AdaptiveDecoder:
                  max_seq: int = 2048, act_dtype=torch.bfloat16, mode: str = GREEDY, temperature: float = 1.0,
                  profiles=None, device="cuda", policy: str = "bandit", predictor: DepthPredictor | None = None,
                  calibrate: bool = True, refresh: int = 16, explore_steps: int = 2, explore_share: float = 0.05,
-                 lag: int = 2, seed: int = 0, plan=None):
+                 lag: int = 2, seed: int = 0, plan=None, proj_dim: int = 0):
         if not shapes:
             raise ValueError("need at least one step shape")
         if policy not in ("bandit", "predictor"):
@@ -75,23 +75,26 @@ class AdaptiveDecoder:
             self.decs.append(SpecDecoder(target_cfg, target_w, draft_cfg, draft_w, sh, batch=batch, max_seq=max_seq,
                                          act_dtype=act_dtype, mode=mode, temperature=temperature, profiles=profiles,
                                          device=device, share=self.decs[0] if self.decs else None, scratch=scratch,
-                                         calibrate=calibrate, plan=plan))
+                                         calibrate=calibrate, plan=plan, feature_tap=proj_dim > 0))
         d0 = self.decs[0]
         self.B, self.seq, self.dev, self.mode = batch, d0.seq, d0.dev, mode
         self.policy, self.predictor = policy, predictor
         self.calibrate, self.refresh = calibrate, refresh
         self.explore_steps, self.explore_share, self.lag = explore_steps, explore_share, lag
         self.stats = [ShapeStats() for _ in self.shapes]
-        self.features = DeviceFeatures(batch)
+        self.features = DeviceFeatures(batch, hidden_dim=target_cfg.d_model, proj_dim=proj_dim, seed=seed)
+        self.proj_dim = proj_dim
         self._last_features = None
         self.rng = np.random.default_rng(seed)
         self.trace = AdaptiveTrace()
         self._pending: list = []  # (shape index, event pair, pinned acc_len, pinned root probs)
         kmax = max(s.expansion_k for s in self.shapes)
         # readback ring: a slot is reused only after its step was observed (ring longer than the lag)
+        hd = target_cfg.d_model if proj_dim > 0 else 1
         self._ring = [(torch.empty(batch, dtype=torch.int32).pin_memory(),
                        torch.empty(batch, kmax, dtype=torch.float64).pin_memory(),
-                       torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                       torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
+                       torch.empty(batch, hd, dtype=torch.float32).pin_memory())
                       for _ in range(lag + 2)]
         self._issued = [0] * len(self.shapes)
         self.steps = 0
@@ -117,7 +120,7 @@ class AdaptiveDecoder:
     def _observe(self, block: bool) -> None:
         """Consume lagged readbacks: shape statistics, predictor / feature state."""
         while self._pending and (block or len(self._pending) > self.lag - 1):
-            idx, (ea, eb), acc_h, root_h = self._pending.pop(0)
+            idx, (ea, eb), acc_h, root_h, hid_h = self._pending.pop(0)
             eb.synchronize()
             ms = ea.elapsed_time(eb)
             acc = acc_h.numpy()
@@ -127,7 +130,7 @@ class AdaptiveDecoder:
             st.seconds += ms * 1e-3
             self.trace.accepted.append(int(acc.sum()))
             self.trace.step_ms.append(ms)
-            feats = self.features.update(acc, root_h.numpy())
+            feats = self.features.update(acc, root_h.numpy(), hid_h.numpy() if self.proj_dim > 0 else None)
             self._last_features = feats[0]
             if self.predictor is not None:
                 self.predictor.observe(int(acc[0]))
@@ -167,7 +170,7 @@ class AdaptiveDecoder:
         d = self.decs[i]
         if self.mode == SAMPLE:
             d.set_uniforms(self.steps, 0)
-        acc_h, root_h, ea, eb = self._ring[self.steps % len(self._ring)]
+        acc_h, root_h, ea, eb, hid_h = self._ring[self.steps % len(self._ring)]
         if len(self._pending) >= len(self._ring):
             self._observe(block=True)
         ea.record()
@@ -177,11 +180,36 @@ class AdaptiveDecoder:
         k = d.shape.expansion_k
         root_h[:, :k].copy_(d.root_probs, non_blocking=True)
         root_h[:, k:] = 0.0
-        self._pending.append((i, (ea, eb), acc_h, root_h))
+        if self.proj_dim > 0:
+            hid_h.copy_(d.hidden_tap, non_blocking=True)
+        self._pending.append((i, (ea, eb), acc_h, root_h, hid_h))
         self._issued[i] += 1
         self.trace.chosen.append(i)
         self.steps += 1
         return i
+
+    def collect_depth_samples(self, shape_index: int, n: int) -> list:
+        """Offline profiling for train_predictor (the reference's collect_depth_samples, simulator.py:
+        553-579, with a deep EGT shape instead of a synthetic chain): before each of ``n`` steps the
+        features the decoder would predict from, then the accepted length that step realized.
+        Synchronous (one readback per step); call after prefill."""
+        from .depth_predictor import DepthSample
+
+        self.drain()
+        d = self.decs[shape_index]
+        feats = self._last_features
+        if feats is None:
+            feats = self.features.update([0] * self.B, np.zeros((self.B, d.shape.expansion_k)),
+                                         np.zeros((self.B, self.features.proj.shape[0])) if self.proj_dim else None)[0]
+        out = []
+        for _ in range(n):
+            d.step(use_graph=d.graph is not None)
+            acc = d.acc_len.cpu().numpy()
+            out.append(DepthSample(features=np.asarray(feats), realized_len=int(acc[0])))
+            hid = d.hidden_tap.cpu().numpy() if self.proj_dim > 0 else None
+            feats = self.features.update(acc, d.root_probs.cpu().numpy(), hid)[0]
+        self._last_features = feats
+        return out
 
     def drain(self) -> None:
         self._observe(block=True)

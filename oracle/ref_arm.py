@@ -195,6 +195,9 @@ def run_host_steps(wl: dict, coupling: dict, steps: int, warmup: int, drafter_bp
     prefill_s = time.perf_counter() - t0
     for _ in range(warmup):
         dec.step()
+    # the timed window is the first `steps` steps after a fresh prefill of the same prompt, as in the
+    # GPU arm (bench.py run_ours), so both arms decode the same tokens
+    dec.prefill(prompt)
     timer.seconds = 0.0
     times, acc = [], []
     for _ in range(steps):

@@ -71,3 +71,48 @@ def write_profile_csv(breakpoints, path) -> None:
         f.write("width,latency_us\n")
         for w, us in breakpoints:
             f.write(f"{int(w)},{float(us)!r}\n")
+
+
+KERNEL_NAMES = {1: "gemv", 2: "attn_dec", 3: "gemm", 4: "epi_store", 5: "epi_resid", 6: "epi_swiglu", 7: "epi_qkv",
+                8: "attn_tc", 9: "attn_combine", 10: "topk_merge", 11: "grow", 13: "level_inputs", 14: "embed"}
+
+
+def kernel_timeline(run, cap: int = 1024, replays: int = 5, before=None) -> list[dict]:
+    """In-graph kernel timeline (profiling only): capture ``run()`` as a graph with the library's
+    timeline tracing armed (ygg_trace_arm), replay it, and return per traced launch its kernel name,
+    first-CTA start, grid-dependency release and last-CTA end (us, relative to the first start).
+    ``before()`` (optional) restores state before each replay.  Launches are PDL-chained, so a kernel's
+    incremental cost to the pass is end - previous end."""
+    lib = L.lib()
+    buf = torch.zeros(cap, 8, dtype=torch.int64, device="cuda")
+    g = torch.cuda.CUDAGraph()
+    L.check(lib.ygg_trace_arm(buf.data_ptr(), cap))
+    try:
+        with torch.cuda.graph(g):
+            run()
+        ids = (L.C.c_int * cap)()
+        n = lib.ygg_trace_used(ids, cap)
+    finally:
+        L.check(lib.ygg_trace_arm(None, 0))
+    for _ in range(replays):
+        if before:
+            before()
+        g.replay()
+    if before:
+        before()
+    buf[:, 0] = -1  # ~0 as u64: atomicMin fields
+    buf[:, 1] = -1
+    buf[:, 2:] = 0
+    torch.cuda.synchronize()
+    g.replay()
+    torch.cuda.synchronize()
+    t = buf[:n].cpu().tolist()
+    t0 = t[0][0]
+    rows, prev = [], None
+    for i in range(n):
+        s, w, e = ((x - t0) / 1e3 for x in t[i][:3])
+        rows.append({"kernel": KERNEL_NAMES.get(ids[i], str(ids[i])), "start": s, "released": w, "end": e,
+                     "incremental": e - (prev if prev is not None else w)})
+        prev = e
+    del g
+    return rows

@@ -214,6 +214,63 @@ class SpecDecoder:
         self.seq.gen_limit.fill_(2**31 - 1)
 
     # ------------------------------------------------------------------
+    def prefill_slot(self, b: int, prompt: torch.Tensor, n_tokens: int, chunk: int = 64) -> None:
+        """Admit one request into slot ``b`` while the other slots keep their state (continuous
+        batching): causal prefill of ``prompt`` [P0] into slot b's region of both caches in fixed
+        ``chunk``-row passes (one set of plans per slot, whatever the prompt length; the last chunk is
+        padded — its padding rows only write KV past the prefix), the bonus = target argmax of the last
+        prompt row, and slot b's sequence state reset with generation limit ``n_tokens``."""
+        P0 = int(prompt.numel())
+        if not 0 <= b < self.B:
+            raise IndexError(f"slot {b} out of range")
+        if P0 < 1 or P0 + n_tokens + self.shape.depth + 2 > self.seq.p_limit or P0 + chunk > self.S:
+            raise ValueError("prompt + generation do not fit the slot's cache")
+        lib = L.lib()
+        dev = self.dev
+        toks = torch.zeros(((P0 + chunk - 1) // chunk) * chunk, dtype=torch.int32, device=dev)
+        toks[:P0] = prompt.to(dev, torch.int32)
+        bonus = torch.zeros(1, dtype=torch.int32, device=dev)
+        for cfg, w, cache in ((self.tc, self.tw, self.tcache), (self.dc, self.dw, self.dcache)):
+            view = cache[:, b : b + 1]
+            nchunk = toks.numel() // chunk
+            for c in range(nchunk):
+                final = c == nchunk - 1
+                key = ("slot", b, cfg.name, chunk, final and cfg is self.tc)
+                f = self._prefill_fwd.get(key)
+                if f is None:
+                    f = Forward(cfg, w, view, 1, chunk, 0, self.act_dtype, logits=final and cfg is self.tc, gemv=False,
+                                decode_attn=False, plan=self.plan)
+                    self._prefill_fwd[key] = f
+                f.tokens.copy_(toks[c * chunk : (c + 1) * chunk])
+                pos = torch.arange(c * chunk, (c + 1) * chunk, dtype=torch.int32, device=dev)
+                f.pos.copy_(pos)
+                f.slot.copy_(pos)
+                f.blk_start.fill_(c * chunk)
+                f.blk_len.fill_(chunk)
+                f.run()
+                if final and cfg is self.tc:
+                    r = (P0 - 1) - c * chunk
+                    L.check(lib.ygg_row_stats(f.logits[r:].data_ptr(), L.YGG_F32, 1, cfg.vocab, cfg.vocab, 1.0,
+                                              bonus.data_ptr(), None, L.stream_ptr()))
+        sq = self.seq
+        sq.hist[b].zero_()
+        sq.hist[b, :P0] = toks[:P0]
+        sq.hist[b, P0] = bonus[0]
+        sq.P[b] = P0
+        sq.n_gen[b] = 1
+        sq.status[b] = 0
+        sq.gen_limit[b] = n_tokens
+
+    def park_slot(self, b: int) -> None:
+        """Mark slot b idle: a valid dummy state (P = 1) that the commit kernel keeps frozen."""
+        sq = self.seq
+        sq.hist[b].zero_()
+        sq.P[b] = 1
+        sq.n_gen[b] = 0
+        sq.gen_limit[b] = 0
+        sq.status[b] = 1
+
+    # ------------------------------------------------------------------
     def _draft_topk(self, rows: int, k: int, s) -> None:
         """Candidates of every draft row (DrafterDistribution.candidates, egt.py:65-80)."""
         lib, dr = L.lib(), self.draft

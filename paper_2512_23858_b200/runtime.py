@@ -271,3 +271,67 @@ def fit_depth_decay(counts, depth: int, width: int) -> tuple[float, float]:
 def rate_ci(st: ShapeStats) -> float:
     """Half-width proxy of a shape's rate estimate (diagnostic)."""
     return st.rate / math.sqrt(max(st.steps, 1))
+
+
+class ServingEngine:
+    """Slot-level continuous batching over one captured step graph.
+
+    The decoder's B request slots run one graph replay per step.  Requests wait in a queue; an idle slot
+    admits the next one (SpecDecoder.prefill_slot: prefill of that slot only, between replays, while
+    the other slots keep decoding); a slot whose request reached its token budget is frozen on the
+    device by the commit kernel (generation limit), its tokens are collected at the next poll and the
+    slot is refilled.  KV stays in the fixed-stride per-slot layout (no paging): each slot holds up to
+    the decoder's S positions."""
+
+    def __init__(self, sd: SpecDecoder, poll: int = 4, chunk: int = 64):
+        self.sd, self.poll, self.chunk = sd, poll, chunk
+        self.queue: list = []
+        self.slot_req = [None] * sd.B
+        self.slot_p0 = [0] * sd.B
+        self.done: dict = {}
+        self._next = 0
+        self.steps = 0
+
+    def submit(self, prompt, n_tokens: int) -> int:
+        rid = self._next
+        self._next += 1
+        self.queue.append((rid, torch.as_tensor(prompt, dtype=torch.int32).reshape(-1), int(n_tokens)))
+        return rid
+
+    def _admit(self) -> None:
+        for b in range(self.sd.B):
+            if self.slot_req[b] is None:
+                if self.queue:
+                    rid, prompt, n = self.queue.pop(0)
+                    self.sd.prefill_slot(b, prompt, n, self.chunk)
+                    self.slot_req[b], self.slot_p0[b] = (rid, n), prompt.numel()
+                else:
+                    self.sd.park_slot(b)
+
+    def _collect(self) -> None:
+        sq = self.sd.seq
+        status = sq.status.cpu()
+        for b in range(self.sd.B):
+            if self.slot_req[b] is not None and int(status[b]) & 1:
+                rid, n = self.slot_req[b]
+                p0 = self.slot_p0[b]
+                self.done[rid] = sq.hist[b, p0 : p0 + n].cpu().tolist()
+                self.slot_req[b] = None
+            elif self.slot_req[b] is not None and int(status[b]) & 2:
+                raise RuntimeError(f"request {self.slot_req[b][0]} reached the slot's cache capacity")
+
+    def run(self, use_graph: bool = True, max_steps: int = 1 << 20) -> dict:
+        """Serve every submitted request; returns {request id: generated tokens}."""
+        self._admit()
+        if use_graph and self.sd.graph is None:
+            self.sd.capture()
+        while (self.queue or any(r is not None for r in self.slot_req)) and self.steps < max_steps:
+            if self.sd.mode == SAMPLE:
+                self.sd.set_uniforms(self.steps, 0)
+            self.sd.step(use_graph)
+            self.steps += 1
+            if self.steps % self.poll == 0:
+                self._collect()
+                self._admit()
+        self._collect()
+        return dict(self.done)

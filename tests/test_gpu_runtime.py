@@ -174,3 +174,26 @@ def test_calibrated_objective_stays_lossless_and_rates_are_probabilities(cuda):
     c = sd.accept_counts.cpu().numpy()
     assert c[0, 0] == 40 and np.all(c[:, 1] <= c[:, 0])  # the root is tested every step
     assert_lossless([sd.generated(0)[:n_tok]], [ar[0][: min(n_tok, len(sd.generated(0)))]], tc, tw, prompts)
+
+
+def test_continuous_batching_serves_queue_losslessly(cuda):
+    """ServingEngine: 6 requests with different prompt lengths and token budgets through 2 slots; each
+    request's output equals greedy AR of that request alone (up to bf16 near-ties)."""
+    from paper_2512_23858_b200.engine import ARDecoder, SpecDecoder, StepShape
+    from paper_2512_23858_b200.plan import ForwardPlan
+    from paper_2512_23858_b200.runtime import ServingEngine
+
+    tc, dc, tw, dw = _models(cuda)
+    plan = ForwardPlan(attn_ksplit=2)
+    reqs = [(20, 30), (37, 16), (64, 40), (9, 25), (50, 12), (33, 33)]
+    prompts = [torch.randint(0, tc.vocab, (n,), generator=torch.Generator().manual_seed(500 + i))
+               for i, (n, _) in enumerate(reqs)]
+    sd = SpecDecoder(tc, tw, dc, dw, StepShape(4, 4, 8, 64), batch=2, max_seq=192, profiles=_profiles(), plan=plan)
+    eng = ServingEngine(sd, poll=2)
+    ids = [eng.submit(p, n) for p, (_, n) in zip(prompts, reqs)]
+    out = eng.run()
+    assert sorted(out) == ids
+    for rid, p, (_, n) in zip(ids, prompts, reqs):
+        ar = ARDecoder(tc, tw, batch=1, max_seq=192, plan=plan).generate(p[None], n)
+        assert len(out[rid]) == n
+        assert_lossless([out[rid]], ar, tc, tw, p[None], plan)

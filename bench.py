@@ -123,7 +123,8 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(rows)}
 
 
-def build_decoder(wl: dict, name: str, device, seed_offset: int = 0, weights=None, profiles=None):
+def build_decoder(wl: dict, name: str, device, seed_offset: int = 0, weights=None, profiles=None,
+                  overlap_compaction: bool = False):
     import torch
 
     from paper_2512_23858_b200.engine import SpecDecoder, StepShape
@@ -154,7 +155,7 @@ def build_decoder(wl: dict, name: str, device, seed_offset: int = 0, weights=Non
     max_seq = wl["prompt"] + wl.get("gen", 2048)  # room for the timed steps of up to D+2 tokens
     sd = SpecDecoder(tc, tw, dc, dw, shape, batch=wl["batch"], max_seq=max_seq, act_dtype=torch.bfloat16,
                      profiles=profiles if profiles is not None else PP, device=device, mode=wl.get("mode", GREEDY),
-                     temperature=wl.get("temperature", 1.0))
+                     temperature=wl.get("temperature", 1.0), overlap_compaction=overlap_compaction)
     if weights is not None:
         return sd, tc, dc
     sd._bench_weights = (tw, dw)
@@ -576,7 +577,7 @@ def run_ours(args, rank, world, local_rank):
     if "global_batch" in wl:
         wl["batch"] = max(1, wl["global_batch"] // world)
     peak, peak_kind, _ = _peaks()
-    sd, tc, dc = build_decoder(wl, args.workload, device)
+    sd, tc, dc = build_decoder(wl, args.workload, device, overlap_compaction=args.overlap_compaction)
     prompts = prompts_for(wl, tc.vocab, rank)
     sd.prefill_len = prompts.shape[1]
     sd.prefill(prompts)
@@ -753,6 +754,8 @@ def main():
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default="cfg2")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-ar-baseline", action="store_true")
+    ap.add_argument("--overlap-compaction", action="store_true",
+                    help="two-lane step: target KV compaction on a side stream under the next draft phase")
     ap.add_argument("--export-profiles", default=None,
                     help="cfg3: write the K8-measured draft / verify latency profiles (reference CSV format) here")
     args = ap.parse_args()

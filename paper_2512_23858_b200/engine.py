@@ -74,6 +74,7 @@ class SpecDecoder:
         scratch: int = 0,
         calibrate: bool = False,
         feature_tap: bool = False,
+        overlap_compaction: bool = False,
     ):
         """``share``: another decoder whose sequence state, KV caches and prefill forwards this one
         uses (one decoding state, several captured step shapes: runtime.AdaptiveDecoder); ``scratch``:
@@ -162,6 +163,12 @@ class SpecDecoder:
         # the target's last-token hidden state per request (depth-predictor feature)
         self.feature_tap = feature_tap and act_dtype == torch.bfloat16
         self.hidden_tap = torch.zeros(batch, target_cfg.d_model, dtype=torch.float32, device=dev)
+        # Two-lane step (the reference's stage overlap, scheduler.py:224-268, on the GPU): the target KV
+        # compaction of step i only has to land before the verify of step i+1, so it runs on a side
+        # stream concurrently with step i+1's draft phase instead of on the critical path.
+        self.overlap_compaction = overlap_compaction
+        self._side = torch.cuda.Stream(device=dev) if overlap_compaction else None
+        self.compact_base = torch.zeros(batch, dtype=torch.int32, device=dev)
         self.node_table = torch.full((batch, self.tree_cap), -1.0, **f64)
         self.graph = None
         self.step_count = 0
@@ -212,6 +219,7 @@ class SpecDecoder:
         self.seq.step.zero_()
         self.seq.status.zero_()
         self.seq.gen_limit.fill_(2**31 - 1)
+        self.path_len.zero_()  # no pending (deferred) compaction
 
     # ------------------------------------------------------------------
     def prefill_slot(self, b: int, prompt: torch.Tensor, n_tokens: int, chunk: int = 64) -> None:
@@ -252,6 +260,7 @@ class SpecDecoder:
                     r = (P0 - 1) - c * chunk
                     L.check(lib.ygg_row_stats(f.logits[r:].data_ptr(), L.YGG_F32, 1, cfg.vocab, cfg.vocab, 1.0,
                                               bonus.data_ptr(), None, L.stream_ptr()))
+        self.path_len[b] = 0  # no deferred compaction of the slot's previous request
         sq = self.seq
         sq.hist[b].zero_()
         sq.hist[b, :P0] = toks[:P0]
@@ -263,6 +272,7 @@ class SpecDecoder:
 
     def park_slot(self, b: int) -> None:
         """Mark slot b idle: a valid dummy state (P = 1) that the commit kernel keeps frozen."""
+        self.path_len[b] = 0
         sq = self.seq
         sq.hist[b].zero_()
         sq.P[b] = 1
@@ -295,6 +305,15 @@ class SpecDecoder:
         D, W, k = sh.depth, sh.width, sh.expansion_k
         dr, vf, g, vt = self.draft, self.verify, self.grown, self.vtree
         rows = self.B * self.R
+        tc, dc = self.tc, self.dc
+        main = stream if stream is not None else torch.cuda.current_stream(self.dev)
+        if self.overlap_compaction:
+            # lane 2: the previous step's target KV compaction (base = its pre-commit prefix length)
+            self._side.wait_stream(main)
+            chk(lib.ygg_kv_compact(self.tcache.data_ptr(), L.dtype_code(self.act_dtype), tc.n_layers, self.B,
+                                   tc.n_kv_heads, self.S, tc.head_dim, self.tcache.stride(0),
+                                   self.compact_base.data_ptr(), self.path.data_ptr(), self.path_len.data_ptr(),
+                                   self.vcap, None, 0, None, 0, 0, L.stream_ptr(self._side)))
         # ---- draft pass 0: [x_{P-1}, bonus] -> root
         chk(lib.ygg_pass0_inputs(self.seq.struct, self.R, self.tree_cap, dr.tokens.data_ptr(), dr.pos.data_ptr(),
                                  dr.slot.data_ptr(), dr.req.data_ptr(), dr.qmask.data_ptr(), dr.mask_words,
@@ -324,6 +343,8 @@ class SpecDecoder:
         chk(lib.ygg_tree_subtree(g.struct, vt.struct, self.keep_idx.data_ptr(), self.new_idx.data_ptr(), s))
         stamp(3)
         # ---- verify
+        if self.overlap_compaction:
+            main.wait_stream(self._side)  # join: the target prefix is compacted
         chk(lib.ygg_verify_inputs(vt.struct, self.seq.struct, vf.tokens.data_ptr(), vf.pos.data_ptr(),
                                   vf.slot.data_ptr(), vf.req.data_ptr(), vf.qmask.data_ptr(), vf.mask_words,
                                   vf.blk_start.data_ptr(), vf.blk_len.data_ptr(), s))
@@ -350,10 +371,13 @@ class SpecDecoder:
             chk(lib.ygg_accept_stats(vt.struct, self.keep_idx.data_ptr(), self.tree_cap, self.path.data_ptr(),
                                      self.path_len.data_ptr(), self.accept_counts.data_ptr(), s))
         # ---- KV compaction (target: verify order; draft: grown-tree slots, leaves never drafted)
-        tc, dc = self.tc, self.dc
-        chk(lib.ygg_kv_compact(self.tcache.data_ptr(), L.dtype_code(self.act_dtype), tc.n_layers, self.B,
-                               tc.n_kv_heads, self.S, tc.head_dim, self.tcache.stride(0), self.seq.P.data_ptr(),
-                               self.path.data_ptr(), self.path_len.data_ptr(), self.vcap, None, 0, None, 0, 0, s))
+        if self.overlap_compaction:
+            with torch.cuda.stream(main):
+                self.compact_base.copy_(self.seq.P)  # deferred to the next step's lane 2
+        else:
+            chk(lib.ygg_kv_compact(self.tcache.data_ptr(), L.dtype_code(self.act_dtype), tc.n_layers, self.B,
+                                   tc.n_kv_heads, self.S, tc.head_dim, self.tcache.stride(0), self.seq.P.data_ptr(),
+                                   self.path.data_ptr(), self.path_len.data_ptr(), self.vcap, None, 0, None, 0, 0, s))
         chk(lib.ygg_kv_compact(self.dcache.data_ptr(), L.dtype_code(self.act_dtype), dc.n_layers, self.B,
                                dc.n_kv_heads, self.S, dc.head_dim, self.dcache.stride(0), self.seq.P.data_ptr(),
                                self.path.data_ptr(), self.path_len.data_ptr(), self.vcap, self.keep_idx.data_ptr(),

@@ -197,3 +197,19 @@ def test_continuous_batching_serves_queue_losslessly(cuda):
         ar = ARDecoder(tc, tw, batch=1, max_seq=192, plan=plan).generate(p[None], n)
         assert len(out[rid]) == n
         assert_lossless([out[rid]], ar, tc, tw, p[None], plan)
+
+
+@pytest.mark.parametrize("use_graph", [False, True])
+def test_two_lane_step_is_lossless(use_graph, cuda):
+    """The deferred target KV compaction on a side stream (overlap_compaction) keeps spec == AR."""
+    from paper_2512_23858_b200.engine import ARDecoder, SpecDecoder, StepShape
+    from paper_2512_23858_b200.plan import ForwardPlan
+
+    tc, dc, tw, dw = _models(cuda)
+    plan = ForwardPlan(attn_ksplit=2)
+    prompts = _prompts(tc.vocab, 2)
+    ar = ARDecoder(tc, tw, batch=2, max_seq=256, plan=plan).generate(prompts, 64)
+    sd = SpecDecoder(tc, tw, dc, dw, StepShape(4, 4, 8, 64), batch=2, max_seq=256, profiles=_profiles(), plan=plan,
+                     overlap_compaction=True)
+    got, _ = sd.generate(prompts, 64, use_graph=use_graph)
+    assert_lossless(got, ar, tc, tw, prompts, plan)

@@ -220,7 +220,9 @@ typedef enum {
   YGG_EPI_STORE_F32 = 1, /* out[m][n] = y (logits) */
   YGG_EPI_QKV_ROPE = 2,  /* RoPE at pos[m]; q -> q_out [M,Hq,hd]; k -> K rows, v -> V^T of the cache */
   YGG_EPI_SWIGLU = 3,    /* act_out[m][j] = silu(gate_j) * up_j */
-  YGG_EPI_RESID = 4      /* resid[m][n] += y; hb = bf16(resid); ss_out[n/128][m] = per-tile sum of squares */
+  YGG_EPI_RESID = 4,     /* resid[m][n] += y; hb = bf16(resid); ss_out[n/128][m] = per-tile sum of squares */
+  YGG_EPI_ARGMAX = 5     /* greedy LM head: no logits; out (as u64 [N/128][M]) = per 128-row tile and token the
+                            key (ordered f32 max << 32 | ~index) of its first maximum; ygg_argmax_reduce */
 } ygg_epi_kind;
 
 typedef struct {
@@ -248,6 +250,9 @@ typedef struct {
 } ygg_epilogue;
 
 int ygg_gemm_fused(const void* plan, float* workspace, const ygg_epilogue* epi, ygg_stream_t stream);
+/* Row argmax from the ARGMAX epilogue's per-tile keys [ntiles][M]: out[m] = index of the first maximum
+ * over all tiles (the same value row_stats returns on the stored logits). */
+int ygg_argmax_reduce(const void* keys, int ntiles, int M, int32_t* out, ygg_stream_t stream);
 /* Cluster split-K (bf16): one thread-block cluster of `cluster` CTAs per 128-row output tile, the tile's
  * K range split evenly over them, the partials reduced through DSMEM into the cluster's leader, which
  * applies the fused epilogue (no workspace partials, no counters).  Fails with YGG_ERR_UNSUPPORTED
@@ -383,10 +388,11 @@ int ygg_gemv_run(const void* plan, const ygg_gemv_epilogue* epi, ygg_stream_t st
  * fit one wave, at most 4; capped at 4 for hd 128 and 8 for hd 64); ksplit = key-split warp groups
  * inside a CTA (0 = automatic: 8 warps / row warps, at most 2 for hd 128).  The partials merge in
  * fixed order, so two plans with the same (kvsplit, ksplit) reduce identically whatever their row
- * count (the lossless-greedy identity between a tree verify and AR decoding relies on it). */
+ * count (the lossless-greedy identity between a tree verify and AR decoding relies on it); stages = key /
+ * value ring stages (0 = automatic; rounded down to a multiple of ksplit, shrunk to fit shared memory). */
 size_t ygg_attn_dec_plan_size(void);
 int ygg_attn_dec_plan_init(void* plan, const void* q, const void* cache_layer, int B, int T, int Hq, int Hkv, int hd,
-                           int S, int kvsplit, int ksplit);
+                           int S, int kvsplit, int ksplit, int stages);
 /* Launch order contract (programmatic dependent launch): K / V chunks wholly inside the committed
  * prefix (keys < blk_start) and blk_start / blk_len are read BEFORE the grid-dependency wait, so they
  * must have been written at least two kernels earlier on the stream and the kernel immediately

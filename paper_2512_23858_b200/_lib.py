@@ -118,7 +118,7 @@ class YggL2Region(C.Structure):
 
 YGG_GEMV_STORE, YGG_GEMV_QKV, YGG_GEMV_SWIGLU, YGG_GEMV_RESID, YGG_GEMV_STORE_TOPK = 1, 2, 3, 4, 5
 
-YGG_EPI_NONE, YGG_EPI_STORE_F32, YGG_EPI_QKV_ROPE, YGG_EPI_SWIGLU, YGG_EPI_RESID = range(5)
+YGG_EPI_NONE, YGG_EPI_STORE_F32, YGG_EPI_QKV_ROPE, YGG_EPI_SWIGLU, YGG_EPI_RESID, YGG_EPI_ARGMAX = range(6)
 
 # name -> (restype, argtypes)
 _SIGS: dict[str, tuple] = {
@@ -144,6 +144,7 @@ _SIGS: dict[str, tuple] = {
                                      C.POINTER(C.c_int), C.POINTER(C.c_size_t)]),
     "ygg_gemm_seg_table_len": (C.c_int, [vp]),
     "ygg_gemm_run": (C.c_int, [vp, vp, vp]),
+    "ygg_argmax_reduce": (C.c_int, [vp, C.c_int, C.c_int, vp, vp]),
     "ygg_gemm_plan_set_cluster": (C.c_int, [vp, C.c_int]),
     "ygg_gemm_plan_cluster": (C.c_int, [vp]),
     "ygg_gemm_fused": (C.c_int, [vp, vp, C.POINTER(YggEpilogue), vp]),
@@ -174,7 +175,7 @@ _SIGS: dict[str, tuple] = {
     "ygg_trace_used": (C.c_int, [vp, C.c_int]),
     "ygg_attn_dec_plan_size": (C.c_size_t, []),
     "ygg_attn_dec_plan_init": (C.c_int, [vp, vp, vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
-                                         C.c_int]),
+                                         C.c_int, C.c_int]),
     "ygg_attn_dec_workspace_size": (C.c_size_t, [vp]),
     "ygg_attn_dec_run": (C.c_int, [vp, vp, vp, vp, C.c_int, C.c_float, vp, vp, vp]),
     "ygg_gemv_plan_size": (C.c_size_t, []),

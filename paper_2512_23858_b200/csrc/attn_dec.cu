@@ -600,7 +600,7 @@ size_t ygg_attn_dec_workspace_size(const void* plan) {
 }
 
 int ygg_attn_dec_plan_init(void* plan, const void* q, const void* cache_layer, int B, int T, int Hq, int Hkv, int hd,
-                           int S, int kvsplit, int ksplit) {
+                           int S, int kvsplit, int ksplit, int stages) {
   YGG_CHECK_ARG(plan && q && cache_layer, "null pointer");
   YGG_CHECK_ARG(hd == 64 || hd == 128, "head dim must be 64 or 128");
   YGG_CHECK_ARG(Hkv >= 1 && Hq % Hkv == 0, "bad head grouping");
@@ -653,6 +653,7 @@ int ygg_attn_dec_plan_init(void* plan, const void* q, const void* cache_layer, i
   // A cluster member walks ~1/kvsplit of the chunks: a ring of one stage per key-split group keeps
   // the CTA small enough to sit beside the producing GEMV's CTA (its prologue then overlaps it).
   p->stages = p->kvsplit > 1 ? p->ksplit : (hd == 64 ? 8 : 4);
+  if (stages > 0) p->stages = stages > kStages ? kStages : stages;
   while (p->stages > p->ksplit && smem_for(p->kvsplit, p->stages) > budget) --p->stages;
   p->stages = (p->stages / p->ksplit) * p->ksplit;
   if (p->stages < p->ksplit) p->stages = p->ksplit;

@@ -71,7 +71,8 @@ struct GemmParams {
 // RMSNorm is folded: its gain lives in the next weight matrix and the per-token rstd (from the
 // producer's per-tile sums of squares) scales the consumer's output rows.
 // ---------------------------------------------------------------------------
-enum EpiKind : int { kEpiNone = 0, kEpiStoreF32 = 1, kEpiQkvRope = 2, kEpiSwiglu = 3, kEpiResid = 4 };
+enum EpiKind : int { kEpiNone = 0, kEpiStoreF32 = 1, kEpiQkvRope = 2, kEpiSwiglu = 3, kEpiResid = 4, kEpiArgmax = 5 };
+constexpr int kArgmaxKeyOffset = 512;  // u64 key scratch inside rstd_s (argmax plans keep M <= 512)
 constexpr int kMaxRstdTokens = 1024;
 
 struct EpiArgs {
@@ -199,6 +200,31 @@ YGG_DEV void epi_apply(const EpiArgs& e, int M, int n, int m0, int valid16, floa
         else e.cache[base + static_cast<size_t>(orig) * e.S + slot[j]] = yb;  // V^T [hd][S]
       }
     }
+  } else if constexpr (KIND == kEpiArgmax) {
+    // Greedy LM head: the first maximum of each token column over this tile's 128 vocabulary rows as
+    // a u64 key (ordered f32 bits << 32 | ~row), max-reduced over the warp, then over the 4 warps.
+    unsigned long long* keys = reinterpret_cast<unsigned long long*>(const_cast<float*>(rstd_s) + kArgmaxKeyOffset);
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const uint32_t u = __float_as_uint(v[j]);
+      const uint32_t ord = (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+      unsigned long long k = j < valid16 ? ((static_cast<unsigned long long>(ord) << 32) | (0xFFFFFFFFu - static_cast<uint32_t>(n))) : 0ull;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const unsigned long long q = __shfl_xor_sync(0xffffffffu, k, o);
+        k = q > k ? q : k;
+      }
+      if (lane == 0) keys[quarter * 16 + j] = k;
+    }
+    epi_bar();
+    const int t = quarter * 32 + lane;
+    if (t < 16 && t < valid16) {
+      unsigned long long best = keys[t];
+#pragma unroll
+      for (int q = 1; q < 4; ++q) best = keys[q * 16 + t] > best ? keys[q * 16 + t] : best;
+      reinterpret_cast<unsigned long long*>(e.out)[static_cast<size_t>(n / kBM) * M + m0 + t] = best;
+    }
+    epi_bar();
   } else if constexpr (KIND == kEpiResid) {
     float h[16], sq[16];
 #pragma unroll
@@ -999,6 +1025,31 @@ __global__ void __launch_bounds__(kEpiThreads) epi_swiglu_kernel(EpiGeom g, cons
   if (threadIdx.x == 0) trace_max(g.trace, 2);
 }
 
+// Row argmax over the ARGMAX epilogue's per-tile keys: one CTA per token row, max over tiles.
+__global__ void __launch_bounds__(256) argmax_reduce_kernel(const unsigned long long* __restrict__ keys, int ntiles,
+                                                            int M, int32_t* __restrict__ out) {
+  pdl_wait();
+  pdl_launch_dependents();
+  const int m = blockIdx.x;
+  unsigned long long best = 0ull;
+  for (int t = threadIdx.x; t < ntiles; t += blockDim.x) {
+    const unsigned long long k = __ldcg(keys + static_cast<size_t>(t) * M + m);
+    best = k > best ? k : best;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const unsigned long long q = __shfl_xor_sync(0xffffffffu, best, o);
+    best = q > best ? q : best;
+  }
+  __shared__ unsigned long long wb[8];
+  if ((threadIdx.x & 31) == 0) wb[threadIdx.x >> 5] = best;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < static_cast<int>(blockDim.x >> 5); ++w) best = wb[w] > best ? wb[w] : best;
+    out[m] = static_cast<int32_t>(0xFFFFFFFFu - static_cast<uint32_t>(best & 0xFFFFFFFFull));
+  }
+}
+
 // QKV epilogue: RoPE (rotate-half convention) on q and k at pos[m]; q -> q_out, k/v -> KV cache.
 // Work item = 4 rotation pairs (i..i+3, i+half..i+half+3) of one head; one item per thread.
 // cos/sin come from the host table rope_cs [positions][hd/2] when given (else sincosf).
@@ -1148,7 +1199,7 @@ extern "C" {
 int ygg_prepare_gemm(void) {
   cudaError_t e = cudaSuccess;
   for (auto fn : {gemm_bf16_tc_kernel<kEpiNone>, gemm_bf16_tc_kernel<kEpiStoreF32>, gemm_bf16_tc_kernel<kEpiQkvRope>,
-                  gemm_bf16_tc_kernel<kEpiSwiglu>, gemm_bf16_tc_kernel<kEpiResid>}) {
+                  gemm_bf16_tc_kernel<kEpiSwiglu>, gemm_bf16_tc_kernel<kEpiResid>, gemm_bf16_tc_kernel<kEpiArgmax>}) {
     e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     if (e != cudaSuccess) return ygg_fail(YGG_ERR_CUDA, "gemm attribute: %s", cudaGetErrorString(e));
   }
@@ -1321,6 +1372,9 @@ static int gemm_launch(const GemmPlan* g, float* workspace, const ygg_epilogue* 
                       "QKV_ROPE arguments");
       if (kind == kEpiSwiglu) YGG_CHECK_ARG(e.act_out != nullptr, "SWIGLU needs act_out");
       if (kind == kEpiResid) YGG_CHECK_ARG(e.resid && e.hb && e.ss_out, "RESID needs resid / hb / ss_out");
+      if (kind == kEpiArgmax) YGG_CHECK_ARG(e.out && g->M <= kArgmaxKeyOffset && (!e.ss_in || g->M <= kArgmaxKeyOffset),
+                                            "ARGMAX needs out (u64 keys) and M <= 512");
+      YGG_CHECK_ARG(kind != kEpiArgmax || g->cluster == 0, "ARGMAX runs on stream-K plans");
     }
     if (g->cluster > 0) {
       YGG_CHECK_ARG(kind != kEpiNone, "a cluster split-K plan needs a fused epilogue (no partials)");
@@ -1353,6 +1407,10 @@ static int gemm_launch(const GemmPlan* g, float* workspace, const ygg_epilogue* 
         YGG_LAUNCH_PDL(gemm_bf16_tc_kernel<kEpiResid>, dim3(g->num_ctas), dim3(kGemmThreads), smem, s, g->tmap_w,
                        g->tmap_x, p, workspace, e);
         break;
+      case kEpiArgmax:
+        YGG_LAUNCH_PDL(gemm_bf16_tc_kernel<kEpiArgmax>, dim3(g->num_ctas), dim3(kGemmThreads), smem, s, g->tmap_w,
+                       g->tmap_x, p, workspace, e);
+        break;
       default:
         return ygg_fail(YGG_ERR_VALUE, "unknown epilogue kind %d", kind);
     }
@@ -1362,6 +1420,13 @@ static int gemm_launch(const GemmPlan* g, float* workspace, const ygg_epilogue* 
     YGG_LAUNCH_PDL(gemm_f32_simt_kernel, grid, dim3(256), 0, s, static_cast<const float*>(g->W),
                    static_cast<const float*>(g->X), g->M, g->N, g->K, g->BN, g->m_tiles, workspace);
   }
+  return YGG_OK;
+}
+
+int ygg_argmax_reduce(const void* keys, int ntiles, int M, int32_t* out, ygg_stream_t stream) {
+  YGG_CHECK_ARG(keys && out && ntiles >= 1 && M >= 1, "invalid arguments");
+  YGG_LAUNCH_PDL(argmax_reduce_kernel, dim3(M), dim3(256), 0, reinterpret_cast<cudaStream_t>(stream),
+                 static_cast<const unsigned long long*>(keys), ntiles, M, out);
   return YGG_OK;
 }
 

@@ -120,7 +120,8 @@ class SpecDecoder:
         # the draft's row-block GEMV even when B * T <= 16: the GEMV needs the fused weight layout (it
         # would rewrite the shared target weights in place) and would round differently from ARDecoder,
         # the oracle of the lossless-greedy identity.
-        self.verify = Forward(target_cfg, target_w, self.tcache, batch, self.T, tmw, act_dtype, gemv=False, plan=plan)
+        self.verify = Forward(target_cfg, target_w, self.tcache, batch, self.T, tmw, act_dtype, gemv=False, plan=plan,
+                              lm_argmax=mode == GREEDY)
         self.grown = DeviceTrees(batch, self.tree_cap, dev)
         self.vtree = DeviceTrees(batch, self.vcap, dev)
         i32 = dict(dtype=torch.int32, device=dev)
@@ -352,8 +353,7 @@ class SpecDecoder:
         stamp(4)
         nrows = self.B * self.T
         if self.mode == GREEDY:
-            chk(lib.ygg_row_stats(vf.logits.data_ptr(), L.YGG_F32, nrows, self.tc.vocab, self.tc.vocab, 1.0,
-                                  self.row_argmax.data_ptr(), None, s))
+            vf.argmax_rows(self.row_argmax, s)  # fused LM-head argmax keys (bf16) / logits scan (f32)
             chk(lib.ygg_accept(vt.struct, L.YGG_ACCEPT_GREEDY, None, None, 0, self.row_argmax.data_ptr(), None,
                                L.YGG_F32, self.tc.vocab, self.tc.vocab, None, 1.0, self.path.data_ptr(),
                                self.path_len.data_ptr(), self.acc_len.data_ptr(), self.bonus.data_ptr(), None, s))

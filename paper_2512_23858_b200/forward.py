@@ -98,6 +98,7 @@ class Forward:
         gemv: bool | None = None,
         decode_attn: bool | None = None,
         plan: ForwardPlan | None = None,
+        lm_argmax: bool = False,
     ):
         L.require_device()
         plan = plan or DEFAULT
@@ -182,7 +183,7 @@ class Forward:
                 mem = C.create_string_buffer(int(lib.ygg_attn_dec_plan_size()))
                 L.check(lib.ygg_attn_dec_plan_init(mem, self.q.data_ptr(), cache.data_ptr() + li * self.layer_stride * es,
                                                    B, R, cfg.n_heads, cfg.n_kv_heads, cfg.head_dim, self.S,
-                                                   plan.attn_kvsplit, plan.attn_ksplit))
+                                                   plan.attn_kvsplit, plan.attn_ksplit, plan.attn_stages))
                 self.ad_plans.append(mem)
             self.ad_ws = torch.zeros(int(lib.ygg_attn_dec_workspace_size(self.ad_plans[0])) // 4 + 64,
                                      dtype=torch.float32, device=dev)
@@ -190,12 +191,17 @@ class Forward:
         # split stream-K tiles are reduced (in fixed segment order, by their participants) — the
         # [M, V] f32 partials round trip and the separate store epilogue disappear.  Same values.
         self.lm_epi = None
-        if bf16 and not self.fused and self.lm_plan is not None and plan.lm_store_fused:
+        # Greedy verify (lm_argmax): the LM head stores no logits, only per-128-row-tile keys of each
+        # token's first maximum (YGG_EPI_ARGMAX), reduced by ygg_argmax_reduce.
+        self.lm_argmax = bool(lm_argmax and bf16 and self.lm_plan is not None and M <= 512)
+        if self.lm_argmax:
+            self.lm_keys = torch.zeros(cfg.vocab // 128, M, dtype=torch.int64, device=dev)
+        if bf16 and not self.fused and self.lm_plan is not None and (plan.lm_store_fused or self.lm_argmax):
             self.lm_counters = torch.zeros(self.lm_plan.tiles, dtype=torch.int32, device=dev)
             e = L.YggEpilogue()
-            e.kind = L.YGG_EPI_STORE_F32
+            e.kind = L.YGG_EPI_ARGMAX if self.lm_argmax else L.YGG_EPI_STORE_F32
             e.counters = self.lm_counters.data_ptr()
-            e.out = self.logits.data_ptr()
+            e.out = self.lm_keys.data_ptr() if self.lm_argmax else self.logits.data_ptr()
             e.ld = cfg.vocab
             self.lm_epi = e
         if self.fused:
@@ -373,8 +379,9 @@ class Forward:
                                 ss_out=self.ss_a.data_ptr())
         if self.lm_plan:
             cur["plan"] = self.lm_plan
-            self.lm_plan.epi = epi(L.YGG_EPI_STORE_F32, ss_in=self.ss_a.data_ptr(), ss_tiles=nt, norm_dim=d, eps=eps,
-                                   out=self.logits.data_ptr(), ld=cfg.vocab)
+            self.lm_plan.epi = epi(L.YGG_EPI_ARGMAX if self.lm_argmax else L.YGG_EPI_STORE_F32, ss_in=self.ss_a.data_ptr(),
+                                   ss_tiles=nt, norm_dim=d, eps=eps,
+                                   out=(self.lm_keys if self.lm_argmax else self.logits).data_ptr(), ld=cfg.vocab)
 
     def _try_cluster(self, gp: GemmPlan) -> None:
         """Cluster split-K for a GEMM whose tiles, times a cluster of 2-4 CTAs, fill one wave."""
@@ -385,6 +392,17 @@ class Forward:
             if gp.tiles * cs <= sms and lib.ygg_gemm_plan_set_cluster(gp.handle, cs) == L.YGG_OK:
                 gp.cluster = cs
                 return
+
+    def argmax_rows(self, out: torch.Tensor, stream_ptr) -> None:
+        """Row argmax of this pass's logits into ``out`` [M] int32: from the fused LM-head keys when the
+        pass was built with lm_argmax, else by scanning the stored logits (row_stats)."""
+        lib = L.lib()
+        if self.lm_argmax:
+            L.check(lib.ygg_argmax_reduce(self.lm_keys.data_ptr(), self.cfg.vocab // 128, self.M, out.data_ptr(),
+                                          stream_ptr))
+        else:
+            L.check(lib.ygg_row_stats(self.logits.data_ptr(), L.YGG_F32, self.M, self.cfg.vocab, self.cfg.vocab, 1.0,
+                                      out.data_ptr(), None, stream_ptr))
 
     def weight_bytes(self) -> int:
         """Algorithmic HBM bytes of the matmul weights streamed per pass."""

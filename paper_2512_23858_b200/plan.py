@@ -53,6 +53,7 @@ class ForwardPlan:
     topk_fused: bool = True         # draft top-k partials from the LM-head GEMV epilogue
     attn_kvsplit: int = 0           # decode attention cluster size (0 = automatic)
     attn_ksplit: int = 0            # decode attention key-split warp groups per CTA (0 = automatic)
+    attn_stages: int = 0            # decode attention K/V ring stages (0 = automatic)
     # L2 prefetch issued by latency-bound kernels (see module docstring)
     draft_qkv_l2: tuple = (L2Prefetch("wgu", 0.25),)
     draft_o_l2: tuple = (L2Prefetch("wgu", 0.25, 0.25),)

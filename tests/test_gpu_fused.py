@@ -148,3 +148,32 @@ def test_qkv_rope_kv_append(hd, Hq, Hkv, ctas, cuda):
         assert (c[b, 0, :, s, :] - kr[m]).abs().max() <= tol
         vt = c[b, 1].reshape(Hkv, hd, S)[:, :, s]  # V^T [hd][S]
         assert (vt - v[m]).abs().max() <= tol
+
+
+@pytest.mark.parametrize("ctas", [0, 7, 37])
+@pytest.mark.parametrize("M", [1, 50, 130])
+def test_argmax_epilogue_equals_argmax_of_stored_logits(ctas, M, cuda):
+    """YGG_EPI_ARGMAX (greedy LM head: per-tile first-maximum keys, no logits) + ygg_argmax_reduce ==
+    the first argmax of the STORE_F32 logits of the same plan, including exact ties (duplicated
+    weight rows) across and inside tiles, split and whole stream-K tiles."""
+    from paper_2512_23858_b200 import _lib as L
+
+    N, K = 4096, 512
+    g = torch.Generator(device="cuda").manual_seed(M + ctas)
+    X = torch.randn(M, K, device=cuda, generator=g).to(torch.bfloat16)
+    W = (torch.randn(N, K, device=cuda, generator=g) / math.sqrt(K)).to(torch.bfloat16)
+    W[3000] = W[77]   # a tie across tiles: the lower index must win
+    W[78] = W[77]     # and inside a tile
+    out = torch.zeros(M, N, device=cuda)
+    plan = _plan(W, X, M, ctas)
+    cnt = torch.zeros(plan.tiles, dtype=torch.int32, device=cuda)
+    _run(plan, _epi(L.YGG_EPI_STORE_F32, cnt, out=out.data_ptr(), ld=N), cuda)
+    keys = torch.zeros(N // 128, M, dtype=torch.int64, device=cuda)
+    cnt2 = torch.zeros(plan.tiles, dtype=torch.int32, device=cuda)
+    _run(plan, _epi(L.YGG_EPI_ARGMAX, cnt2, out=keys.data_ptr(), ld=N), cuda)
+    am = torch.zeros(M, dtype=torch.int32, device=cuda)
+    L.check(L.lib().ygg_argmax_reduce(keys.data_ptr(), N // 128, M, am.data_ptr(), L.stream_ptr()))
+    torch.cuda.synchronize()
+    want = torch.tensor([int(torch.nonzero(r == r.max())[0]) for r in out.cpu()], dtype=torch.int32)
+    assert torch.equal(am.cpu(), want)
+    assert not (am.cpu() == 78).any() and not (am.cpu() == 3000).any()

@@ -209,7 +209,7 @@ def test_decode_attention_vs_fp32(hd, Hq, Hkv, B, T, P, mw, kvsplit, cuda):
     bl = torch.full((B,), T, dtype=torch.int32, device=cuda)
     out = torch.zeros(M, Hq, hd, dtype=torch.bfloat16, device=cuda)
     mem = C.create_string_buffer(int(lib.ygg_attn_dec_plan_size()))
-    L.check(lib.ygg_attn_dec_plan_init(mem, q.data_ptr(), cache.data_ptr(), B, T, Hq, Hkv, hd, S, int(kvsplit), 0))
+    L.check(lib.ygg_attn_dec_plan_init(mem, q.data_ptr(), cache.data_ptr(), B, T, Hq, Hkv, hd, S, int(kvsplit), 0, 0))
     scale = 1.0 / math.sqrt(hd)
     ws = torch.zeros(int(lib.ygg_attn_dec_workspace_size(mem)) // 4 + 64, dtype=torch.float32, device=cuda)
     outs = []
@@ -288,7 +288,7 @@ def test_l2_prefetch_regions_leave_results_unchanged(cuda):
     bs = torch.full((1,), P, dtype=torch.int32, device=cuda)
     bl = torch.full((1,), T, dtype=torch.int32, device=cuda)
     att = C.create_string_buffer(int(lib.ygg_attn_dec_plan_size()))
-    L.check(lib.ygg_attn_dec_plan_init(att, q.data_ptr(), cache.data_ptr(), 1, T, Hq, Hkv, hd, S, 0, 0))
+    L.check(lib.ygg_attn_dec_plan_init(att, q.data_ptr(), cache.data_ptr(), 1, T, Hq, Hkv, hd, S, 0, 0, 0))
     res = []
     for pf in (0, 1 << 20):
         for rg in (0, 1):
@@ -371,7 +371,7 @@ def test_decode_attention_wide_tree_mask(hd, Hq, Hkv, cuda):
     bl = torch.full((B,), N, dtype=torch.int32, device=cuda)
     out = torch.zeros(M, Hq, hd, dtype=torch.bfloat16, device=cuda)
     mem = C.create_string_buffer(int(lib.ygg_attn_dec_plan_size()))
-    L.check(lib.ygg_attn_dec_plan_init(mem, q.data_ptr(), cache.data_ptr(), B, R, Hq, Hkv, hd, S, 0, 0))
+    L.check(lib.ygg_attn_dec_plan_init(mem, q.data_ptr(), cache.data_ptr(), B, R, Hq, Hkv, hd, S, 0, 0, 0))
     ws = torch.zeros(int(lib.ygg_attn_dec_workspace_size(mem)) // 4 + 64, dtype=torch.float32, device=cuda)
     scale = 1.0 / math.sqrt(hd)
     L.check(lib.ygg_attn_dec_run(mem, bs.data_ptr(), bl.data_ptr(), qmask.data_ptr(), mw, scale, out.data_ptr(),

@@ -260,6 +260,10 @@ int ygg_argmax_reduce(const void* keys, int ntiles, int M, int32_t* out, ygg_str
  * runs only through ygg_gemm_fused. */
 int ygg_gemm_plan_set_cluster(void* plan, int cluster);
 int ygg_gemm_plan_cluster(const void* plan);
+/* L2 prefetch issued by this plan's separate epilogue kernel (ygg_epi_*): right after its dependency
+ * wait every CTA pulls its share of [ptr, ptr + bytes) into L2 — a later weight stream, fetched while
+ * HBM would otherwise idle.  bytes = 0 turns it off.  Results are unaffected. */
+int ygg_gemm_plan_set_epi_prefetch(void* plan, const void* ptr, size_t bytes);
 int ygg_gemm_tiles(const void* plan);
 /* Embedding gather for the fused path: resid (f32), hb (bf16) and per-128-feature-tile sums of
  * squares ss_out [d/128][M] (the first layer's folded RMSNorm input). */
@@ -412,6 +416,26 @@ int ygg_attn_dec_set_l2_prefetch(void* plan, int region, const void* ptr, size_t
 int ygg_attn_dec_set_gemv_prefetch(void* plan, const void* gemv_plan);
 int ygg_attn_dec_run(const void* plan, const int32_t* blk_start, const int32_t* blk_len, const uint32_t* qmask,
                      int mask_words, float scale, void* out, void* workspace, ygg_stream_t stream);
+
+/* K2 tree attention on tcgen05 / TMEM (csrc/attn_tree.cu) for tree / decode passes: the same
+ * visibility and arguments as ygg_attn_dec_run: committed prefix + ancestor mask over the tree block;
+ * S = Q K^T and O = P V on the tensor cores with S / O in TMEM, one (csplit, 1, 1) thread-block
+ * cluster per (kv head, request, row tile of <= 32 tokens), the keys split over the cluster's CTAs in
+ * 64-key chunks and merged through DSMEM in fixed rank order (deterministic, no combine launch, no
+ * workspace).  csplit in {0 (automatic: the largest of 4, 2, 1 keeping the grid in one wave), 1, 2, 4};
+ * row_tiles = 0 picks the fewest tiles.  Same launch-order contract as ygg_attn_dec_run. */
+size_t ygg_attn_tree_plan_size(void);
+int ygg_attn_tree_plan_init(void* plan, const void* q, const void* cache_layer, int B, int T, int Hq, int Hkv, int hd,
+                            int S, int csplit, int row_tiles);
+int ygg_attn_tree_info(const void* plan, int* csplit, int* row_tiles, int* tokens_per_tile);
+int ygg_attn_tree_set_l2_prefetch(void* plan, int region, const void* ptr, size_t bytes);
+/* Profiling only: every launch writes 16 %globaltimer checkpoints per CTA into stamps (NULL = off). */
+int ygg_attn_tree_set_debug(void* plan, unsigned long long* stamps);
+/* A/B knob: late = 0 triggers the dependent launch right after the dependency wait (the next kernel's
+ * prologue overlaps this one); late = 1 (the plan default, measured faster) only when each CTA ends. */
+int ygg_attn_tree_set_trigger(void* plan, int late);
+int ygg_attn_tree_run(const void* plan, const int32_t* blk_start, const int32_t* blk_len, const uint32_t* qmask,
+                      int mask_words, float scale, void* out, ygg_stream_t stream);
 
 
 #ifdef __cplusplus

@@ -39,6 +39,7 @@ int ygg_prepare_layers(void);
 int ygg_prepare_attn_tc(void);
 int ygg_prepare_gemv(void);
 int ygg_prepare_attn_dec(void);
+int ygg_prepare_attn_tree(void);
 
 int ygg_version(void) { return 100; }
 
@@ -76,6 +77,7 @@ int ygg_device_check(int* num_sms, int* cc_major, int* cc_minor) {
   if (int rc = ygg_prepare_attn_tc()) return rc;
   if (int rc = ygg_prepare_gemv()) return rc;
   if (int rc = ygg_prepare_attn_dec()) return rc;
+  if (int rc = ygg_prepare_attn_tree()) return rc;
   return YGG_OK;
 }
 

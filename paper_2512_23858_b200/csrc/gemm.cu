@@ -47,6 +47,8 @@ struct GemmPlan {
   const void* W;
   const void* X;
   int32_t* seg_table;  // device: seg_first[tiles+1], seg_base[num_ctas]
+  const char* epi_pf;  // L2 prefetch region of this plan's separate epilogue kernel (or nullptr)
+  size_t epi_pf_bytes;
   alignas(64) CUtensorMap tmap_w;
   alignas(64) CUtensorMap tmap_x;
 };
@@ -801,7 +803,24 @@ struct EpiGeom {
   int M, N, BN, m_tiles;
   const int32_t* seg_first;
   unsigned long long* trace;  // kernel-timeline slot (profiling only) or nullptr
+  const char* pf;             // L2 prefetch region (a later weight stream) or nullptr
+  size_t pf_bytes;
 };
+
+// The epilogue kernels barely touch HBM (their partials are L2 hits): right after the dependency
+// wait, thread 0 of every CTA pulls its share of a later weight stream into L2 (bulk prefetch,
+// <= 64 KB per instruction, fire and forget), so the next GEMM starts that much of its stream from L2.
+YGG_DEV void epi_l2_prefetch(const EpiGeom& g) {
+  if (!g.pf || threadIdx.x != 0) return;
+  const size_t ncta = static_cast<size_t>(gridDim.x) * gridDim.y;
+  const size_t cta = static_cast<size_t>(blockIdx.y) * gridDim.x + blockIdx.x;
+  const size_t per = ((g.pf_bytes / ncta) + 255) & ~static_cast<size_t>(255);
+  const size_t b0 = cta * per, b1 = b0 + per < g.pf_bytes ? b0 + per : g.pf_bytes;
+  for (size_t o = b0; o < b1; o += 65536) {
+    const uint32_t n = static_cast<uint32_t>(b1 - o < 65536 ? ((b1 - o) & ~static_cast<size_t>(15)) : 65536);
+    if (n) asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(g.pf + o), "r"(n) : "memory");
+  }
+}
 
 YGG_DEV float epi_value(const EpiGeom& g, const float* __restrict__ ws, int m, int n) {
   const int t = (n / kBM) * g.m_tiles + m / g.BN;
@@ -932,6 +951,7 @@ __global__ void __launch_bounds__(kEpiThreads) epi_store_kernel(EpiGeom g, const
   const int2 sg = n < g.N ? epi_segs(g, m, n) : make_int2(0, 0);
   pdl_wait();
   pdl_launch_dependents();
+  epi_l2_prefetch(g);
   if (threadIdx.x == 0) trace_min(g.trace, 1);
   if (n >= g.N) return;
   float v[8];
@@ -977,6 +997,7 @@ __global__ void __launch_bounds__(1024) epi_residual_norm_kernel(EpiGeom g, cons
   }
   pdl_wait();
   pdl_launch_dependents();
+  epi_l2_prefetch(g);
   if (threadIdx.x == 0) trace_min(g.trace, 1);
   float ss = 0.f;
   if (live) {
@@ -1015,6 +1036,7 @@ __global__ void __launch_bounds__(kEpiThreads) epi_swiglu_kernel(EpiGeom g, cons
   const int2 sa = f < F ? epi_segs(g, m, f) : make_int2(0, 0), sb = f < F ? epi_segs(g, m, F + f) : make_int2(0, 0);
   pdl_wait();
   pdl_launch_dependents();
+  epi_l2_prefetch(g);
   if (threadIdx.x == 0) trace_min(g.trace, 1);
   if (f >= F) return;
   float gate[8], up[8], o[8];
@@ -1073,6 +1095,7 @@ __global__ void __launch_bounds__(256) epi_qkv_rope_kernel(EpiGeom g, const floa
   const int2 sb = it < items ? epi_segs(g, m, n0 + i0 + half) : make_int2(0, 0);
   pdl_wait();
   pdl_launch_dependents();
+  epi_l2_prefetch(g);
   if (threadIdx.x == 0) trace_min(g.trace, 1);
   if (it >= items) return;
   const int pm = pos[m];
@@ -1166,7 +1189,7 @@ static const GemmPlan* as_plan(const void* p) {
 }
 
 static EpiGeom geom_of(const GemmPlan* g, int kernel_id) {
-  return EpiGeom{g->M, g->N, g->BN, g->m_tiles, g->seg_table, trace_next(kernel_id)};
+  return EpiGeom{g->M, g->N, g->BN, g->m_tiles, g->seg_table, trace_next(kernel_id), g->epi_pf, g->epi_pf_bytes};
 }
 
 }  // namespace ygg
@@ -1464,6 +1487,15 @@ int ygg_gemm_plan_set_cluster(void* plan, int cluster) {
     return ygg_fail(YGG_ERR_UNSUPPORTED, "%d tiles need %d co-resident clusters of %d; only %d fit", g->tiles,
                     g->tiles, cluster, max_clusters);
   g->cluster = cluster;
+  return YGG_OK;
+}
+
+int ygg_gemm_plan_set_epi_prefetch(void* plan, const void* ptr, size_t bytes) {
+  GemmPlan* g = const_cast<GemmPlan*>(plan_of(plan));
+  YGG_CHECK_ARG(g != nullptr, "invalid GEMM plan");
+  YGG_CHECK_ARG(ptr == nullptr || (reinterpret_cast<uintptr_t>(ptr) & 15) == 0, "prefetch region must be 16-byte aligned");
+  g->epi_pf = bytes ? static_cast<const char*>(ptr) : nullptr;
+  g->epi_pf_bytes = g->epi_pf ? (bytes & ~static_cast<size_t>(15)) : 0;
   return YGG_OK;
 }
 

@@ -187,6 +187,20 @@ class Forward:
                 self.ad_plans.append(mem)
             self.ad_ws = torch.zeros(int(lib.ygg_attn_dec_workspace_size(self.ad_plans[0])) // 4 + 64,
                                      dtype=torch.float32, device=dev)
+        # tcgen05 / TMEM tree attention (csrc/attn_tree.cu): S and O on the tensor cores, keys split over
+        # a thread-block cluster, merged through DSMEM; replaces the decode attention when planned.
+        self.at_plans = None
+        use_tree = plan.tree_attn if plan.tree_attn is not None else not self.gemv
+        if self.ad_plans is not None and use_tree and gh <= 32 and gh & (gh - 1) == 0:
+            lib = L.lib()
+            es = cache.element_size()
+            self.at_plans = []
+            for li in range(cfg.n_layers):
+                mem = C.create_string_buffer(int(lib.ygg_attn_tree_plan_size()))
+                L.check(lib.ygg_attn_tree_plan_init(mem, self.q.data_ptr(), cache.data_ptr() + li * self.layer_stride * es,
+                                                    B, R, cfg.n_heads, cfg.n_kv_heads, cfg.head_dim, self.S,
+                                                    plan.tree_csplit, plan.tree_row_tiles))
+                self.at_plans.append(mem)
         # Unfused bf16 LM head: whole output tiles go straight from TMEM to the f32 logits and only the
         # split stream-K tiles are reduced (in fixed segment order, by their participants) — the
         # [M, V] f32 partials round trip and the separate store epilogue disappear.  Same values.
@@ -209,6 +223,8 @@ class Forward:
         if self.gemv:
             self._setup_gemv()
         self._setup_attn_l2_prefetch()
+        if not self.gemv and not self.fused and bf16:
+            self._setup_epi_l2_prefetch()
 
     # ------------------------------------------------------------------
     def _setup_gemv(self) -> None:
@@ -284,6 +300,23 @@ class Forward:
                 W = self.w["layers"][li][rg.target]
                 off, n = rg.region(W, self.plan.l2_bytes)
                 L.check(lib.ygg_attn_dec_set_l2_prefetch(plan, j, W.data_ptr() + off if n > 0 else None, n))
+                if self.at_plans is not None:
+                    L.check(lib.ygg_attn_tree_set_l2_prefetch(self.at_plans[li], j, W.data_ptr() + off if n > 0 else None,
+                                                              n))
+
+    def _setup_epi_l2_prefetch(self) -> None:
+        """The separate epilogue kernels of a verify / prefill pass idle HBM too: each pulls a region of a
+        later weight stream into L2 (plan.verify_epi_l2: (GEMM name, L2Prefetch) pairs)."""
+        lib = L.lib()
+        layers = self.w["layers"]
+        for li, p in enumerate(self.plans):
+            for name, rg in self.plan.verify_epi_l2:
+                lj = li + (1 if rg.next_layer else 0)
+                if lj >= len(layers):
+                    continue
+                W = layers[lj][rg.target]
+                off, n = rg.region(W, self.plan.l2_bytes)
+                L.check(lib.ygg_gemm_plan_set_epi_prefetch(p[name].handle, W.data_ptr() + off if n > 0 else None, n))
 
     def fuse_topk(self, k: int, temperature: float = 1.0) -> bool:
         """Draft GEMV pass: have the LM-head epilogue also emit per-CTA top-k partials of every row
@@ -305,7 +338,10 @@ class Forward:
     def _attend(self, li: int, qm, s) -> None:
         """bf16 attention of layer li: decode kernel when planned, else split-KV tcgen05 + combine."""
         lib = L.lib()
-        if self.ad_plans is not None:
+        if self.at_plans is not None:
+            L.check(lib.ygg_attn_tree_run(self.at_plans[li], self.blk_start.data_ptr(), self.blk_len.data_ptr(), qm,
+                                          self.mask_words, self.scale, self.attn.data_ptr(), s))
+        elif self.ad_plans is not None:
             L.check(lib.ygg_attn_dec_run(self.ad_plans[li], self.blk_start.data_ptr(), self.blk_len.data_ptr(), qm,
                                          self.mask_words, self.scale, self.attn.data_ptr(), self.ad_ws.data_ptr(), s))
         else:

@@ -30,13 +30,14 @@ class L2Prefetch:
     target: str               # weight name in the layer dict (wqkv / wo / wgu / wdown)
     fraction: float
     offset_fraction: float = 0.0
+    next_layer: bool = False  # the matrix of the following layer (nothing after the last layer)
 
     def region(self, W, l2_bytes: int) -> tuple[int, int]:
         """(byte offset, byte count) of the region inside ``W``."""
         total = W.numel() * W.element_size()
         cap = l2_bytes // 4
-        off = min(int(self.offset_fraction * total), cap) if self.offset_fraction else 0
-        n = min(int(self.fraction * total), cap, total - off)
+        off = min(int(self.offset_fraction * total), cap) & ~255 if self.offset_fraction else 0
+        n = min(int(self.fraction * total), cap, total - off) & ~255
         return off, max(n, 0)
 
 
@@ -54,11 +55,21 @@ class ForwardPlan:
     attn_kvsplit: int = 0           # decode attention cluster size (0 = automatic)
     attn_ksplit: int = 0            # decode attention key-split warp groups per CTA (0 = automatic)
     attn_stages: int = 0            # decode attention K/V ring stages (0 = automatic)
+    tree_attn: bool | None = None   # tcgen05 / TMEM tree attention (csrc/attn_tree.cu) instead of the
+    #                                 mma.sync decode attention wherever the latter would run; None =
+    #                                 automatic: verify / AR passes (measured at parity in the cfg2 verify
+    #                                 graph, 3.498 vs 3.491 ms), not the GEMV draft passes (32 query rows
+    #                                 per kv head: 0.604 vs 0.565 ms per pass)
+    tree_csplit: int = 0            # its key-split cluster size (0 = automatic)
+    tree_row_tiles: int = 0         # its row tiles per (kv head, request) (0 = fewest)
     # L2 prefetch issued by latency-bound kernels (see module docstring)
     draft_qkv_l2: tuple = (L2Prefetch("wgu", 0.25),)
     draft_o_l2: tuple = (L2Prefetch("wgu", 0.25, 0.25),)
     draft_attn_l2: tuple = (L2Prefetch("wdown", 0.375),)
     verify_attn_l2: tuple = (L2Prefetch("wgu", 0.1),)
+    # (GEMM, region) pairs: the separate epilogue kernel of that GEMM (verify / prefill passes) pulls the
+    # region into L2 after its dependency wait (csrc/gemm.cu epi_l2_prefetch)
+    verify_epi_l2: tuple = ()
     l2_bytes: int = field(default=L2_BYTES_B200)
 
 

@@ -27,10 +27,29 @@ if which == "verify_fused":  # fused layout + cluster split-K on a separate weig
     g = Forward(f.cfg, weights_to(sd.tw, f.cache.device), f.cache, f.B, f.R, f.mask_words, f.act_dtype,
                 plan=ForwardPlan(fused_epilogues=True, cluster_split_k="nocluster" not in sys.argv))
 else:
-    g = Forward(f.cfg, f.w, f.cache, f.B, f.R, f.mask_words, f.act_dtype)
+    from paper_2512_23858_b200.plan import ForwardPlan
+
+    kw, late = {}, False
+    for a in sys.argv[2:]:  # plan overrides, e.g. tree_attn=1 tree_csplit=4 (late_trigger=1, nopf=1)
+        k, v = a.split("=")
+        if k == "late_trigger":
+            late = bool(int(v))
+        elif k == "nopf":
+            kw["verify_attn_l2"] = ()
+            kw["draft_attn_l2"] = ()
+        else:
+            kw[k] = int(v) if k != "tree_attn" else bool(int(v))
+    g = Forward(f.cfg, f.w, f.cache, f.B, f.R, f.mask_words, f.act_dtype, plan=ForwardPlan(**kw))
+    if late and g.at_plans:
+        for pl in g.at_plans:
+            L.check(L.lib().ygg_attn_tree_set_trigger(pl, 1))
 for t in ("tokens", "pos", "slot", "req", "qmask", "blk_start", "blk_len"):
     getattr(g, t).copy_(getattr(f, t))
 lib = L.lib()
+dbg = None
+if getattr(g, "at_plans", None):  # per-CTA checkpoints of layer 10's tree attention
+    dbg = torch.zeros(1024, 16, dtype=torch.int64, device="cuda")
+    L.check(lib.ygg_attn_tree_set_debug(g.at_plans[10], dbg.data_ptr()))
 CAP = 512
 buf = torch.zeros(CAP, 8, dtype=torch.int64, device="cuda")
 
@@ -98,7 +117,7 @@ graph.replay()
 torch.cuda.synchronize()
 t = buf[:n].cpu().tolist()
 names = {1: "gemv", 2: "attn_dec", 3: "gemm", 4: "epi_store", 5: "epi_resid", 6: "epi_swiglu", 7: "epi_qkv",
-         8: "attn_tc", 9: "attn_combine", 10: "topk_merge", 11: "grow", 13: "level_inputs", 14: "embed"}
+         8: "attn_tc", 9: "attn_combine", 10: "topk_merge", 11: "grow", 13: "level_inputs", 14: "embed", 15: "attn_tree"}
 t0 = t[0][0]
 rows = []
 prev_end = None
@@ -115,7 +134,7 @@ tot, gaps, seen = {}, {}, {}
 for r in rows:
     k = r["k"]
     seen[k] = seen.get(k, 0) + 1
-    per_layer = {"gemv": 5, "gemm": 4, "epi_resid": 2, "attn_dec": 1}.get(k)  # gemv: qkv/attn/o/gu/down slots by index
+    per_layer = {"gemv": 5, "gemm": 4, "epi_resid": 2, "attn_dec": 1, "attn_tree": 1}.get(k)  # gemv: qkv/attn/o/gu/down slots by index
     if k == "gemv":
         key = f"gemv#{r['i'] % 5 if r['i'] < n - 1 else 'lm'}"
     elif per_layer:
@@ -130,3 +149,16 @@ print(json.dumps({"gap_" + k: round(sum(v) / len(v), 2) for k, v in gaps.items()
 print(json.dumps({"sum_after_release": round(sum(sum(v) for v in tot.values()), 1),
                   "sum_gaps": round(sum(sum(v) for v in gaps.values()), 1)}))
 print(json.dumps({"total_us": round((t[n - 1][2] - t0) / 1e3, 2), "launches": n}))
+if dbg is not None:
+    NAMES = ["entry", "cluster_sync", "released", "q", "kv0", "kv_last_r0", "p_r0", "o_done", "pushed", "recv",
+             "end", "rounds", "s_r0"]
+    d = dbg.cpu()
+    d = d[: int((d[:, 2] > 0).sum())].double()
+    t0 = d[:, 2].min()
+    st = {}
+    for k, nm in enumerate(NAMES):
+        col = d[:, k]
+        v = col[col > 0]
+        if nm != "rounds" and len(v):
+            st[nm] = [round(float((v.median() - t0) / 1e3), 2), round(float((v.max() - t0) / 1e3), 2)]
+    print(json.dumps({"attn_tree_stamps": st}))

@@ -124,7 +124,7 @@ class ClockSampler:
 
 
 def build_decoder(wl: dict, name: str, device, seed_offset: int = 0, weights=None, profiles=None,
-                  overlap_compaction: bool = False):
+                  overlap_compaction: bool = False, plan=None):
     import torch
 
     from paper_2512_23858_b200.engine import SpecDecoder, StepShape
@@ -155,7 +155,7 @@ def build_decoder(wl: dict, name: str, device, seed_offset: int = 0, weights=Non
     max_seq = wl["prompt"] + wl.get("gen", 2048)  # room for the timed steps of up to D+2 tokens
     sd = SpecDecoder(tc, tw, dc, dw, shape, batch=wl["batch"], max_seq=max_seq, act_dtype=torch.bfloat16,
                      profiles=profiles if profiles is not None else PP, device=device, mode=wl.get("mode", GREEDY),
-                     temperature=wl.get("temperature", 1.0), overlap_compaction=overlap_compaction)
+                     temperature=wl.get("temperature", 1.0), overlap_compaction=overlap_compaction, plan=plan)
     if weights is not None:
         return sd, tc, dc
     sd._bench_weights = (tw, dw)

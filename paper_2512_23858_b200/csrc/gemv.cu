@@ -124,6 +124,7 @@ struct Plan {
   uint32_t magic;
   Params p;
   size_t smem;
+  size_t stage_bytes, fixed_bytes;
   alignas(64) CUtensorMap tw;
   alignas(64) CUtensorMap tx;
 };
@@ -649,9 +650,27 @@ int ygg_gemv_plan_init(void* plan, const void* W, const void* X, int M, int N, i
   const size_t fixed = 1024 + 16 * 2 * 8 + kMaxTok * 16 + 2 * kCompute * 2 * 4 * 32 * 4 + 64;
   p.stages = static_cast<int>(std::min<size_t>(16, (static_cast<size_t>(budget_kb) * 1024 - fixed) / stage));
   YGG_CHECK_ARG(p.stages >= 2, "gemv: shared memory budget too small");
+  // Never more stages than a CTA has chunks to stream (the o projection: 4 chunks of one block): the
+  // surplus ring only keeps this CTA from sharing its SM with the previous kernel's CTAs, whose
+  // presence delays the pre-wait weight fill.
+  const int nb_max = (p.nblk + p.grid - 1) / p.grid;
+  p.stages = std::max(2, std::min(p.stages, p.kchunks * nb_max));
   pl->smem = fixed + static_cast<size_t>(p.stages) * stage;
+  pl->stage_bytes = stage;
+  pl->fixed_bytes = fixed;
   if (int rc = map3(&pl->tw, W, N, K, kRows)) return rc;
   if (int rc = map3(&pl->tx, X, M, K, p.xrows)) return rc;
+  return YGG_OK;
+}
+
+int ygg_gemv_plan_set_stages(void* plan, int stages) {
+  Plan* pl = const_cast<Plan*>(plan_of(plan));
+  YGG_CHECK_ARG(pl != nullptr, "invalid gemv plan");
+  YGG_CHECK_ARG(stages >= 2 && stages <= 16, "stages must be in [2, 16]");
+  YGG_CHECK_ARG(pl->fixed_bytes + static_cast<size_t>(stages) * pl->stage_bytes <= 227 * 1024,
+                "ring exceeds shared memory");
+  pl->p.stages = stages;
+  pl->smem = pl->fixed_bytes + static_cast<size_t>(stages) * pl->stage_bytes;
   return YGG_OK;
 }
 

@@ -192,7 +192,7 @@ class SpecDecoder:
         key = (cfg.name, n, id(cache))
         f = self._prefill_fwd.get(key)
         if f is None:
-            f = Forward(cfg, w, cache, self.B, n, 0, self.act_dtype)
+            f = Forward(cfg, w, cache, self.B, n, 0, self.act_dtype, plan=self.plan)
             self._prefill_fwd[key] = f
         return f
 
@@ -209,7 +209,8 @@ class SpecDecoder:
         self.seq.hist.zero_()
         self.seq.hist[:, :P0] = prompts_d
         for cfg, w, cache in ((self.tc, self.tw, self.tcache), (self.dc, self.dw, self.dcache)):
-            last = prefill_causal(cfg, w, cache, prompts_d, self.act_dtype, cfg is self.tc, self._prefill_fwd)
+            last = prefill_causal(cfg, w, cache, prompts_d, self.act_dtype, cfg is self.tc, self._prefill_fwd,
+                                  plan=self.plan)
             if cfg is self.tc:
                 am = torch.zeros(B, dtype=torch.int32, device=self.dev)
                 L.check(lib.ygg_row_stats(last.data_ptr(), L.YGG_F32, B, cfg.vocab, cfg.vocab, 1.0, am.data_ptr(),
@@ -515,6 +516,7 @@ class ARDecoder:
         # AR is the oracle of the lossless-greedy identity, so it runs the same kernel families as the
         # verify pass (stream-K GEMM and the cluster decode attention of tree passes that fit one
         # wave), not the draft's GEMV.
+        self.plan = plan
         self.fwd = Forward(cfg, w, self.cache, batch, 1, 1, act_dtype, gemv=False, plan=plan)
         self.fwd.qmask.fill_(1)
         self.argmax = torch.zeros(batch, dtype=torch.int32, device=self.dev)
@@ -537,7 +539,7 @@ class ARDecoder:
     def generate(self, prompts: torch.Tensor, n_tokens: int, use_graph: bool = True) -> list:
         B, P0 = prompts.shape
         pd = prompts.to(self.dev, torch.int32)
-        last = prefill_causal(self.cfg, self.w, self.cache, pd, self.act_dtype, True)
+        last = prefill_causal(self.cfg, self.w, self.cache, pd, self.act_dtype, True, plan=self.plan)
         L.check(L.lib().ygg_row_stats(last.data_ptr(), L.YGG_F32, B, self.cfg.vocab, self.cfg.vocab, 1.0,
                                       self.argmax.data_ptr(), None, L.stream_ptr()))
         self.P.fill_(P0)

@@ -1,5 +1,6 @@
 // Probe: kernel-to-kernel dependency latency on a chain of short 148-CTA kernels (profiling only).
 //   mode 0: programmatic dependent launch, consumer waits with griddepcontrol.wait (grid completion)
+//   big 1: every other kernel takes 190 KB of dynamic shared memory (the verify GEMM's footprint)
 //   mode 1: consumer launched early by PDL, but waits on a per-launch arrival counter that every
 //           producer CTA releases after its stores (acquire-poll), no griddepcontrol.wait
 // Each kernel: every CTA reads 4 KB of the previous kernel's output, writes 4 KB.  Reports us per kernel.
@@ -14,6 +15,8 @@ __device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
 }
 
 __global__ void step(const float* in, float* out, unsigned* ctr, int idx, int mode) {
+  extern __shared__ float dyn[];
+  if (threadIdx.x == 1023) dyn[0] = 0.f;
   if (mode == 0) {
     asm volatile("griddepcontrol.wait;" ::: "memory");
   } else {
@@ -47,6 +50,8 @@ int main() {
   cudaMalloc(&ctr, K * 4);
   cudaStream_t s;
   cudaStreamCreate(&s);
+  cudaFuncSetAttribute(step, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  for (int big : {0, 1})
   for (int mode : {0, 1, 0, 1}) {
     float best = 1e9;
     for (int it = 0; it < 5; ++it) {
@@ -60,6 +65,7 @@ int main() {
         cfg.gridDim = dim3(148);
         cfg.blockDim = dim3(256);
         cfg.stream = s;
+        cfg.dynamicSmemBytes = (big && (k & 1)) ? 190 * 1024 : 0;
         cudaLaunchAttribute at[1];
         at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
         at[0].val.programmaticStreamSerializationAllowed = 1;
@@ -73,7 +79,7 @@ int main() {
       cudaEventElapsedTime(&ms, e0, e1);
       if (ms < best) best = ms;
     }
-    printf("mode %d: %.3f us per kernel (%s)\n", mode, best * 1e3 / K, cudaGetErrorString(cudaGetLastError()));
+    printf("big %d mode %d: %.3f us per kernel (%s)\n", big, mode, best * 1e3 / K, cudaGetErrorString(cudaGetLastError()));
   }
   return 0;
 }

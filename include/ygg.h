@@ -260,10 +260,6 @@ int ygg_argmax_reduce(const void* keys, int ntiles, int M, int32_t* out, ygg_str
  * runs only through ygg_gemm_fused. */
 int ygg_gemm_plan_set_cluster(void* plan, int cluster);
 int ygg_gemm_plan_cluster(const void* plan);
-/* Dependent-trigger placement of this plan's separate residual-norm / SwiGLU epilogue kernel: early != 0
- * triggers before its grid-dependency wait, so the next GEMM's CTAs become resident (and stream their
- * first weight stages) as the previous GEMM's CTAs exit.  Only for epilogues followed by a GEMM. */
-int ygg_gemm_plan_set_epi_trigger(void* plan, int early);
 /* L2 prefetch issued by this plan's separate epilogue kernel (ygg_epi_*): right after its dependency
  * wait every CTA pulls its share of [ptr, ptr + bytes) into L2 — a later weight stream, fetched while
  * HBM would otherwise idle.  bytes = 0 turns it off.  Results are unaffected. */
@@ -284,18 +280,6 @@ int ygg_epi_swiglu(const void* plan, const float* ws, void* out, int act_dtype, 
 int ygg_epi_qkv_rope(const void* plan, const float* ws, int Hq, int Hkv, int hd, float rope_theta,
                      const int32_t* pos, const int32_t* slot, const int32_t* req, void* q_out, void* cache,
                      int S, int act_dtype, const float* rope_cs, ygg_stream_t stream);
-/* Folded-RMSNorm variants (hybrid verify): the GEMM ran on the unnormalised bf16
- * residual with the norm gains folded into its weight columns (model.prepare_folded_); the per-token
- * rstd = rsqrt(sum_t ss_in[t][m] / norm_dim + eps) over the producer's ss_tiles per-128-feature sums
- * of squares is applied to the partial sums before SwiGLU / RoPE.  ss_in == NULL: the plain kernels.
- * Replaces the RMSNorm the reference prices inside latency_at(profiles.verifier, ...)
- * (pkg/src/specsim/simulator.py:211). */
-int ygg_epi_swiglu_rstd(const void* plan, const float* ws, const float* ss_in, int ss_tiles, int norm_dim,
-                        float eps, void* out, int act_dtype, ygg_stream_t stream);
-int ygg_epi_qkv_rope_rstd(const void* plan, const float* ws, const float* ss_in, int ss_tiles, int norm_dim,
-                          float eps, int Hq, int Hkv, int hd, float rope_theta, const int32_t* pos,
-                          const int32_t* slot, const int32_t* req, void* q_out, void* cache, int S,
-                          int act_dtype, const float* rope_cs, ygg_stream_t stream);
 
 int ygg_embed(const void* table, int dtype, int V, int d, const int32_t* tokens, int M, float* resid_out,
               ygg_stream_t stream);
@@ -398,8 +382,7 @@ int ygg_gemv_stream_info(const void* plan, void* weight_map, int* nblk, int* kch
  * that order; bytes = 0 disables the region). */
 int ygg_gemv_set_l2_prefetch(void* plan, int region, const void* ptr, size_t bytes);
 int ygg_gemv_plan_init(void* plan, const void* W, const void* X, int M, int N, int K, int num_ctas);
-/* Ring depth override (2..16 stages of 16 weight rows x 512 k; default: the shared-memory budget, capped
- * at the chunks one CTA streams).  A smaller ring lets the CTAs share an SM with the previous kernel's. */
+/* Ring depth override (2..16 stages of 16 weight rows x 512 k; default: the shared-memory budget). */
 int ygg_gemv_plan_set_stages(void* plan, int stages);
 int ygg_gemv_run(const void* plan, const ygg_gemv_epilogue* epi, ygg_stream_t stream);
 

@@ -49,7 +49,6 @@ struct GemmPlan {
   int32_t* seg_table;  // device: seg_first[tiles+1], seg_base[num_ctas]
   const char* epi_pf;  // L2 prefetch region of this plan's separate epilogue kernel (or nullptr)
   size_t epi_pf_bytes;
-  int epi_early;       // residual-norm / SwiGLU epilogue kernels trigger their dependents before their wait
   alignas(64) CUtensorMap tmap_w;
   alignas(64) CUtensorMap tmap_x;
 };
@@ -806,19 +805,7 @@ struct EpiGeom {
   unsigned long long* trace;  // kernel-timeline slot (profiling only) or nullptr
   const char* pf;             // L2 prefetch region (a later weight stream) or nullptr
   size_t pf_bytes;
-  int early;                  // trigger dependents before the grid-dependency wait (see epi_trigger_wait)
 };
-
-// Grid-dependency wait + dependent trigger of a separate epilogue kernel.  Default: trigger after the
-// wait, which keeps the invariant the attention kernels rely on (everything two launches back has
-// completed when a kernel's predecessor triggers).  early: trigger first — only for epilogues whose
-// successor is a GEMM (it reads nothing but weights before its own wait), so the next GEMM's CTAs
-// take each SM the moment the previous GEMM's CTA there exits and stream weights during this kernel.
-YGG_DEV void epi_trigger_wait(const EpiGeom& g) {
-  if (g.early) pdl_launch_dependents();
-  pdl_wait();
-  if (!g.early) pdl_launch_dependents();
-}
 
 // The epilogue kernels barely touch HBM (their partials are L2 hits): right after the dependency
 // wait, thread 0 of every CTA pulls its share of a later weight stream into L2 (bulk prefetch,
@@ -1008,7 +995,8 @@ __global__ void __launch_bounds__(1024) epi_residual_norm_kernel(EpiGeom g, cons
     sg = epi_segs(g, m, n);
     load8<ActT>(norm_w + n, w);
   }
-  epi_trigger_wait(g);
+  pdl_wait();
+  pdl_launch_dependents();
   epi_l2_prefetch(g);
   if (threadIdx.x == 0) trace_min(g.trace, 1);
   float ss = 0.f;
@@ -1038,61 +1026,21 @@ __global__ void __launch_bounds__(1024) epi_residual_norm_kernel(EpiGeom g, cons
   if (threadIdx.x == 0) trace_max(g.trace, 2);
 }
 
-// Folded-RMSNorm input of a separate epilogue kernel (the hybrid verify): the GEMM ran on
-// the unnormalised bf16 residual with the norm gains folded into its weights, so the per-token rstd is
-// applied here, from the producer's per-128-feature-tile sums of squares [tiles][M].  Summed in tile
-// order like the fused GEMM epilogue (same rstd bits).
-struct RstdIn {
-  const float* ss;  // nullptr: no rstd (plain epilogue)
-  int tiles;
-  int dim;
-  float eps;
-};
-
-// Block-wide rstd of row m in two halves so that its L2 round trip overlaps the partial-sum loads:
-// rstd_part (warp 0's lanes load tiles lane, lane + 32, ...) before them, rstd_block (fixed-order xor
-// reduction in warp 0, one shared-memory broadcast; every thread of the block must call it) after.
-YGG_DEV float rstd_part(const RstdIn& r, int M, int m) {
-  float s = 0.f;
-  if (threadIdx.x < 32)
-    for (int t = static_cast<int>(threadIdx.x); t < r.tiles; t += 32) s += __ldcg(r.ss + static_cast<size_t>(t) * M + m);
-  return s;
-}
-
-YGG_DEV float rstd_block(float part, const RstdIn& r) {
-  __shared__ float rs_s;
-  if (threadIdx.x < 32) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
-    if (threadIdx.x == 0) rs_s = rsqrtf(part / static_cast<float>(r.dim) + r.eps);
-  }
-  __syncthreads();
-  return rs_s;
-}
-
 template <typename ActT>
 __global__ void __launch_bounds__(kEpiThreads) epi_swiglu_kernel(EpiGeom g, const float* __restrict__ ws,
-                                                                 ActT* __restrict__ out, RstdIn rn) {
+                                                                 ActT* __restrict__ out) {
   if (threadIdx.x == 0) trace_min(g.trace, 0);
   const int m = blockIdx.y;
   const int F = g.N / 2;
   const int f = (blockIdx.x * blockDim.x + threadIdx.x) * 8;
   const int2 sa = f < F ? epi_segs(g, m, f) : make_int2(0, 0), sb = f < F ? epi_segs(g, m, F + f) : make_int2(0, 0);
-  epi_trigger_wait(g);
+  pdl_wait();
+  pdl_launch_dependents();
   epi_l2_prefetch(g);
   if (threadIdx.x == 0) trace_min(g.trace, 1);
-  const float ssp = rn.ss ? rstd_part(rn, g.M, m) : 0.f;
-  float gate[8], up[8], o[8];
-  if (f < F) epi_values2<8>(g, ws, m, f, F + f, gate, up, sa, sb);
-  const float rs = rn.ss ? rstd_block(ssp, rn) : 1.f;
   if (f >= F) return;
-  if (rn.ss) {
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      gate[i] *= rs;
-      up[i] *= rs;
-    }
-  }
+  float gate[8], up[8], o[8];
+  epi_values2<8>(g, ws, m, f, F + f, gate, up, sa, sb);
 #pragma unroll
   for (int i = 0; i < 8; ++i) o[i] = gate[i] / (1.f + expf(-gate[i])) * up[i];
   store8<ActT>(out + static_cast<size_t>(m) * F + f, o);
@@ -1133,7 +1081,7 @@ __global__ void __launch_bounds__(256) epi_qkv_rope_kernel(EpiGeom g, const floa
                                                            const int32_t* __restrict__ slot,
                                                            const int32_t* __restrict__ req, ActT* __restrict__ q_out,
                                                            ActT* __restrict__ cache, int S,
-                                                           const float2* __restrict__ rope_cs, RstdIn rn) {
+                                                           const float2* __restrict__ rope_cs) {
   if (threadIdx.x == 0) trace_min(g.trace, 0);
   const int m = blockIdx.x;
   const int half = hd / 2;
@@ -1149,12 +1097,11 @@ __global__ void __launch_bounds__(256) epi_qkv_rope_kernel(EpiGeom g, const floa
   pdl_launch_dependents();
   epi_l2_prefetch(g);
   if (threadIdx.x == 0) trace_min(g.trace, 1);
-  const float ssp = rn.ss ? rstd_part(rn, g.M, m) : 0.f;
-  const bool live = it < items;
+  if (it >= items) return;
   const int pm = pos[m];
   float x1[4], x2[4], cs[4], sn[4];
   const bool rot = head < Hq + Hkv;
-  if (live && rot && rope_cs) {  // table loads first: they overlap the partial-sum loads below
+  if (rot && rope_cs) {  // table loads first: they overlap the partial-sum loads below
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       const float2 t = __ldg(rope_cs + static_cast<size_t>(pm) * half + i0 + j);
@@ -1162,16 +1109,7 @@ __global__ void __launch_bounds__(256) epi_qkv_rope_kernel(EpiGeom g, const floa
       sn[j] = t.y;
     }
   }
-  if (live) epi_values2<4>(g, ws, m, n0 + i0, n0 + i0 + half, x1, x2, sa, sb);
-  const float rs = rn.ss ? rstd_block(ssp, rn) : 1.f;  // every thread of the block takes part
-  if (!live) return;
-  if (rn.ss) {
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      x1[j] *= rs;
-      x2[j] *= rs;
-    }
-  }
+  epi_values2<4>(g, ws, m, n0 + i0, n0 + i0 + half, x1, x2, sa, sb);
   if (rot) {
     if (rope_cs) {
     } else {
@@ -1251,8 +1189,7 @@ static const GemmPlan* as_plan(const void* p) {
 }
 
 static EpiGeom geom_of(const GemmPlan* g, int kernel_id) {
-  return EpiGeom{g->M, g->N, g->BN, g->m_tiles, g->seg_table, trace_next(kernel_id), g->epi_pf, g->epi_pf_bytes,
-                 g->epi_early};
+  return EpiGeom{g->M, g->N, g->BN, g->m_tiles, g->seg_table, trace_next(kernel_id), g->epi_pf, g->epi_pf_bytes};
 }
 
 }  // namespace ygg
@@ -1553,13 +1490,6 @@ int ygg_gemm_plan_set_cluster(void* plan, int cluster) {
   return YGG_OK;
 }
 
-int ygg_gemm_plan_set_epi_trigger(void* plan, int early) {
-  GemmPlan* g = const_cast<GemmPlan*>(plan_of(plan));
-  YGG_CHECK_ARG(g != nullptr, "invalid GEMM plan");
-  g->epi_early = early ? 1 : 0;
-  return YGG_OK;
-}
-
 int ygg_gemm_plan_set_epi_prefetch(void* plan, const void* ptr, size_t bytes) {
   GemmPlan* g = const_cast<GemmPlan*>(plan_of(plan));
   YGG_CHECK_ARG(g != nullptr, "invalid GEMM plan");
@@ -1628,42 +1558,25 @@ int ygg_epi_residual_norm(const void* plan, const float* ws, float* resid, const
 }
 
 int ygg_epi_swiglu(const void* plan, const float* ws, void* out, int act_dtype, ygg_stream_t stream) {
-  return ygg_epi_swiglu_rstd(plan, ws, nullptr, 0, 0, 0.f, out, act_dtype, stream);
-}
-
-int ygg_epi_swiglu_rstd(const void* plan, const float* ws, const float* ss_in, int ss_tiles, int norm_dim, float eps,
-                        void* out, int act_dtype, ygg_stream_t stream) {
   const GemmPlan* g = plan_of(plan);
   YGG_CHECK_ARG(g && ws && out, "invalid arguments");
-  YGG_CHECK_ARG(!ss_in || (ss_tiles >= 1 && norm_dim >= 1 && eps >= 0.f), "bad folded-RMSNorm arguments");
-  const RstdIn rn{ss_in, ss_tiles, norm_dim, eps};
   YGG_CHECK_ARG(g->N % 2 == 0, "gate_up width must be even");
   EpiGeom geo = geom_of(g, 6);
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   dim3 grid((g->N / 2 + 1023) / 1024, g->M);
   if (act_dtype == YGG_F32)
-    YGG_LAUNCH_PDL(epi_swiglu_kernel<float>, grid, dim3(kEpiThreads), 0, s, geo, ws, static_cast<float*>(out), rn);
+    YGG_LAUNCH_PDL(epi_swiglu_kernel<float>, grid, dim3(kEpiThreads), 0, s, geo, ws, static_cast<float*>(out));
   else
     YGG_LAUNCH_PDL(epi_swiglu_kernel<__nv_bfloat16>, grid, dim3(kEpiThreads), 0, s, geo, ws,
-                   static_cast<__nv_bfloat16*>(out), rn);
+                   static_cast<__nv_bfloat16*>(out));
   return YGG_OK;
 }
 
 int ygg_epi_qkv_rope(const void* plan, const float* ws, int Hq, int Hkv, int hd, float rope_theta, const int32_t* pos,
                      const int32_t* slot, const int32_t* req, void* q_out, void* cache, int S, int act_dtype,
                      const float* rope_cs, ygg_stream_t stream) {
-  return ygg_epi_qkv_rope_rstd(plan, ws, nullptr, 0, 0, 0.f, Hq, Hkv, hd, rope_theta, pos, slot, req, q_out, cache, S,
-                               act_dtype, rope_cs, stream);
-}
-
-int ygg_epi_qkv_rope_rstd(const void* plan, const float* ws, const float* ss_in, int ss_tiles, int norm_dim, float eps,
-                          int Hq, int Hkv, int hd, float rope_theta, const int32_t* pos, const int32_t* slot,
-                          const int32_t* req, void* q_out, void* cache, int S, int act_dtype, const float* rope_cs,
-                          ygg_stream_t stream) {
   const GemmPlan* g = plan_of(plan);
   YGG_CHECK_ARG(g && ws && pos && slot && req && q_out && cache, "invalid arguments");
-  YGG_CHECK_ARG(!ss_in || (ss_tiles >= 1 && norm_dim >= 1 && eps >= 0.f), "bad folded-RMSNorm arguments");
-  const RstdIn rn{ss_in, ss_tiles, norm_dim, eps};
   YGG_CHECK_ARG(g->N == (Hq + 2 * Hkv) * hd, "QKV width mismatch");
   YGG_CHECK_ARG(hd % 8 == 0 && hd <= 256, "bad head dim");
   EpiGeom geo = geom_of(g, 7);
@@ -1674,10 +1587,10 @@ int ygg_epi_qkv_rope_rstd(const void* plan, const float* ws, const float* ss_in,
   const float2* rt = reinterpret_cast<const float2*>(rope_cs);
   if (act_dtype == YGG_F32)
     YGG_LAUNCH_PDL(epi_qkv_rope_kernel<float>, grid, dim3(256), 0, s, geo, ws, Hq, Hkv, hd, l2t, pos, slot, req,
-                   static_cast<float*>(q_out), static_cast<float*>(cache), S, rt, rn);
+                   static_cast<float*>(q_out), static_cast<float*>(cache), S, rt);
   else
     YGG_LAUNCH_PDL(epi_qkv_rope_kernel<__nv_bfloat16>, grid, dim3(256), 0, s, geo, ws, Hq, Hkv, hd, l2t, pos, slot, req,
-                   static_cast<__nv_bfloat16*>(q_out), static_cast<__nv_bfloat16*>(cache), S, rt, rn);
+                   static_cast<__nv_bfloat16*>(q_out), static_cast<__nv_bfloat16*>(cache), S, rt);
   return YGG_OK;
 }
 

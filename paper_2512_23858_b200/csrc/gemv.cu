@@ -650,11 +650,6 @@ int ygg_gemv_plan_init(void* plan, const void* W, const void* X, int M, int N, i
   const size_t fixed = 1024 + 16 * 2 * 8 + kMaxTok * 16 + 2 * kCompute * 2 * 4 * 32 * 4 + 64;
   p.stages = static_cast<int>(std::min<size_t>(16, (static_cast<size_t>(budget_kb) * 1024 - fixed) / stage));
   YGG_CHECK_ARG(p.stages >= 2, "gemv: shared memory budget too small");
-  // Never more stages than a CTA has chunks to stream (the o projection: 4 chunks of one block): the
-  // surplus ring only keeps this CTA from sharing its SM with the previous kernel's CTAs, whose
-  // presence delays the pre-wait weight fill.
-  const int nb_max = (p.nblk + p.grid - 1) / p.grid;
-  p.stages = std::max(2, std::min(p.stages, p.kchunks * nb_max));
   pl->smem = fixed + static_cast<size_t>(p.stages) * stage;
   pl->stage_bytes = stage;
   pl->fixed_bytes = fixed;

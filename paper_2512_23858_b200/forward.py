@@ -19,16 +19,6 @@ with RMSNorm gains folded into the next weights (model.prepare_fused_) and the p
 applied by the consuming GEMM's epilogue.  Same results; today slower, because the split-tile
 fixups sit on each GEMM's critical path.
 
-bf16 hybrid (ForwardPlan.hybrid, the default for verify / AR / prefill; 8 launches per layer): measured
-per kernel in the cfg2 verify graph, the cluster split-K GEMM with the residual epilogue beats GEMM +
-separate kernel for O and down, the separate kernels win for QKV and gate|up —
-  GEMM(qkv, x=hb) ; epilogue kernel: rstd + RoPE + q / KV-cache append   (ygg_epi_qkv_rope_rstd)
-  GEMM(o)  cluster split-K + residual add, hb, per-tile sum-of-squares    (YGG_EPI_RESID)
-  GEMM(gate|up, x=hb) ; epilogue kernel: rstd + SwiGLU                   (ygg_epi_swiglu_rstd)
-  GEMM(down) cluster split-K + residual add, hb, sum-of-squares           (YGG_EPI_RESID)
-with the RMSNorm gains folded into wqkv / wgu / lm_head columns (model.prepare_folded_, rows in the
-standard order) and the LM head applying the final rstd in its fused STORE / ARGMAX epilogue.
-
 f32 (parity path): SIMT GEMM + the same separate epilogue kernels + SIMT attention.  The
 residual stream is f32 in every path.
 """
@@ -41,7 +31,7 @@ import math
 import torch
 
 from . import _lib as L
-from .model import ModelConfig, prepare_folded_, prepare_fused_, rope_table
+from .model import ModelConfig, prepare_fused_, rope_table
 from .plan import DEFAULT, ForwardPlan
 
 
@@ -132,9 +122,6 @@ class Forward:
         self.fused = bf16 and (plan.fused_epilogues or self.gemv or weights.get("_layout") == "fused")
         if self.fused:
             prepare_fused_(weights, cfg)
-        self.hybrid = bf16 and not self.fused and (plan.hybrid or weights.get("_layout") == "folded")
-        if self.hybrid:  # (folded weights carry unit norm gains, so every other path runs on them too)
-            prepare_folded_(weights, cfg)
         self.w = weights
         dev = cache.device
         M, d = self.M, cfg.d_model
@@ -223,8 +210,7 @@ class Forward:
         self.lm_argmax = bool(lm_argmax and bf16 and self.lm_plan is not None and M <= 512)
         if self.lm_argmax:
             self.lm_keys = torch.zeros(cfg.vocab // 128, M, dtype=torch.int64, device=dev)
-        if bf16 and not self.fused and not self.hybrid and self.lm_plan is not None and (plan.lm_store_fused or
-                                                                                        self.lm_argmax):
+        if bf16 and not self.fused and self.lm_plan is not None and (plan.lm_store_fused or self.lm_argmax):
             self.lm_counters = torch.zeros(self.lm_plan.tiles, dtype=torch.int32, device=dev)
             e = L.YggEpilogue()
             e.kind = L.YGG_EPI_ARGMAX if self.lm_argmax else L.YGG_EPI_STORE_F32
@@ -234,64 +220,11 @@ class Forward:
             self.lm_epi = e
         if self.fused:
             self._setup_fused()
-        if self.hybrid:
-            self._setup_hybrid()
         if self.gemv:
             self._setup_gemv()
         self._setup_attn_l2_prefetch()
         if not self.gemv and not self.fused and bf16:
             self._setup_epi_l2_prefetch()
-        if plan.epi_early_trigger and bf16 and not self.gemv and not self.fused:
-            lib = L.lib()
-            nl = len(self.plans)
-            for li, p in enumerate(self.plans):
-                # only epilogue kernels followed by a GEMM of this pass (never the pass's last kernel)
-                names = ("gu",) if self.hybrid else ("o", "gu") + (("down",) if li + 1 < nl or self.lm_plan else ())
-                for name in names:
-                    L.check(lib.ygg_gemm_plan_set_epi_trigger(p[name].handle, 1))
-
-    def _epoch_counters(self, plans) -> dict:
-        """One arrival-counter array per fused stream-K plan: the counters are monotonic epochs (launch L
-        of a plan moves a split tile's counter from L*nseg to (L+1)*nseg), so plans must never share
-        them.  Returns {id(plan): device pointer}."""
-        offs, total = [], 0
-        for p in plans:
-            offs.append(total)
-            total += p.tiles
-        self.counters = torch.zeros(max(total, 1), dtype=torch.int32, device=self.cache.device)
-        return {id(p): self.counters.data_ptr() + 4 * o for p, o in zip(plans, offs)}
-
-    def _setup_hybrid(self) -> None:
-        """Hybrid bf16 forward (module docstring): cluster split-K residual GEMMs for O / down (stream-K
-        fused when the cluster does not fit one wave, e.g. prefill chunks), rstd epilogue kernels for
-        QKV / gate|up, LM head with the final rstd fused."""
-        cfg, M, d = self.cfg, self.M, self.cfg.d_model
-        dev = self.cache.device
-        nt = d // 128
-        self.ss_a = torch.zeros(nt, M, dtype=torch.float32, device=dev)  # after down (and the embedding)
-        self.ss_b = torch.zeros(nt, M, dtype=torch.float32, device=dev)  # after o-proj
-        fused_plans = [p[n] for p in self.plans for n in ("o", "down")] + ([self.lm_plan] if self.lm_plan else [])
-        if self.plan.cluster_split_k:
-            for p in self.plans:
-                self._try_cluster(p["o"])
-                self._try_cluster(p["down"])
-        counter_ptr = self._epoch_counters(fused_plans)
-        eps = float(cfg.norm_eps)
-        for p in self.plans:
-            for name, ss in (("o", self.ss_b), ("down", self.ss_a)):
-                e = L.YggEpilogue()
-                e.kind = L.YGG_EPI_RESID
-                e.counters = counter_ptr[id(p[name])]
-                e.resid, e.hb, e.ss_out = self.resid.data_ptr(), self.xn.data_ptr(), ss.data_ptr()
-                p[name].epi = e
-        if self.lm_plan:
-            e = L.YggEpilogue()
-            e.kind = L.YGG_EPI_ARGMAX if self.lm_argmax else L.YGG_EPI_STORE_F32
-            e.counters = counter_ptr[id(self.lm_plan)]
-            e.ss_in, e.ss_tiles, e.norm_dim, e.eps = self.ss_a.data_ptr(), nt, d, eps
-            e.out = (self.lm_keys if self.lm_argmax else self.logits).data_ptr()
-            e.ld = cfg.vocab
-            self.lm_plan.epi = e
 
     # ------------------------------------------------------------------
     def _setup_gemv(self) -> None:
@@ -442,7 +375,12 @@ class Forward:
         # One arrival-counter array per plan: the counters are monotonic epochs (launch L of a plan
         # moves a split tile's counter from L*nseg to (L+1)*nseg), so plans must never share them.
         plans = [p for layer in self.plans for p in layer.values()] + ([self.lm_plan] if self.lm_plan else [])
-        counter_ptr = self._epoch_counters(plans)
+        offs, total = [], 0
+        for p in plans:
+            offs.append(total)
+            total += p.tiles
+        self.counters = torch.zeros(max(total, 1), dtype=torch.int32, device=dev)
+        counter_ptr = {id(p): self.counters.data_ptr() + 4 * o for p, o in zip(plans, offs)}
         eps = float(cfg.norm_eps)
         es = self.cache.element_size()
         cur = {"plan": None}
@@ -522,7 +460,7 @@ class Forward:
 
     def launch_gemm(self, plan: GemmPlan, stream_ptr) -> None:
         lib = L.lib()
-        if self.fused or (self.hybrid and plan.epi is not None):
+        if self.fused:
             L.check(lib.ygg_gemm_fused(plan.handle, self.ws.data_ptr(), C.byref(plan.epi), stream_ptr))
         else:
             L.check(lib.ygg_gemm_run(plan.handle, self.ws.data_ptr(), stream_ptr))
@@ -532,8 +470,6 @@ class Forward:
             self._run_gemv(stream)
         elif self.fused:
             self._run_fused(stream)
-        elif self.hybrid:
-            self._run_hybrid(stream)
         else:
             self._run_unfused(stream)
 
@@ -570,38 +506,6 @@ class Forward:
         if self.lm_plan is not None:
             chk(lib.ygg_gemm_fused(self.lm_plan.handle, ws, C.byref(self.lm_plan.epi), s))
             stamp()
-
-    def _run_hybrid(self, stream) -> None:
-        lib, cfg = L.lib(), self.cfg
-        s = L.stream_ptr(stream)
-        chk = L.check
-        ws = self.ws.data_ptr()
-        d, nt, eps = cfg.d_model, cfg.d_model // 128, float(cfg.norm_eps)
-        ss_a, ss_b = self.ss_a.data_ptr(), self.ss_b.data_ptr()
-        chk(lib.ygg_embed_fused(self.w["embed"].data_ptr(), cfg.vocab, d, self.tokens.data_ptr(), self.M,
-                                self.resid.data_ptr(), self.xn.data_ptr(), ss_a, s))
-        qm = self.qmask.data_ptr() if self.mask_words > 0 else None
-        es = self.cache.element_size()
-        for li, p in enumerate(self.plans):
-            cache_l = self.cache.data_ptr() + li * self.layer_stride * es
-            chk(lib.ygg_gemm_run(p["qkv"].handle, ws, s))
-            chk(lib.ygg_epi_qkv_rope_rstd(p["qkv"].handle, ws, ss_a, nt, d, eps, cfg.n_heads, cfg.n_kv_heads,
-                                          cfg.head_dim, cfg.rope_theta, self.pos.data_ptr(), self.slot.data_ptr(),
-                                          self.req.data_ptr(), self.q.data_ptr(), cache_l, self.S, self.act,
-                                          self.rope_cs.data_ptr(), s))
-            if self.attn_plans is not None:
-                self._attend(li, qm, s)
-            else:
-                chk(lib.ygg_attention(self.q.data_ptr(), cache_l, self.act, self.M, self.B, cfg.n_heads,
-                                      cfg.n_kv_heads, cfg.head_dim, self.S, self.blk_start.data_ptr(),
-                                      self.blk_len.data_ptr(), qm, self.mask_words, self.scale, self.attn.data_ptr(),
-                                      s))
-            chk(lib.ygg_gemm_fused(p["o"].handle, ws, C.byref(p["o"].epi), s))
-            chk(lib.ygg_gemm_run(p["gu"].handle, ws, s))
-            chk(lib.ygg_epi_swiglu_rstd(p["gu"].handle, ws, ss_b, nt, d, eps, self.mlp.data_ptr(), self.act, s))
-            chk(lib.ygg_gemm_fused(p["down"].handle, ws, C.byref(p["down"].epi), s))
-        if self.lm_plan is not None:
-            chk(lib.ygg_gemm_fused(self.lm_plan.handle, ws, C.byref(self.lm_plan.epi), s))
 
     def _run_unfused(self, stream, stamps: torch.Tensor | None = None) -> None:
         lib, cfg = L.lib(), self.cfg

@@ -198,8 +198,6 @@ def prepare_fused_(w: dict, cfg: ModelConfig) -> dict:
     interleaved.  The per-token rstd is applied by the consumer GEMM's epilogue."""
     if w.get("_layout") == "fused":
         return w
-    if w.get("_layout") == "folded":
-        raise ValueError("weights already in the folded (hybrid) layout: the fused layout needs the original gains")
     dev = w["embed"].device
     qperm = qkv_row_permutation(cfg).to(dev)
     gperm = gate_up_interleave(cfg).to(dev)
@@ -215,29 +213,6 @@ def prepare_fused_(w: dict, cfg: ModelConfig) -> dict:
         w["lm_head"] = (w["lm_head"].float() * fn[None, :]).to(w["lm_head"].dtype)
     w["final_norm"] = torch.ones_like(w["final_norm"])
     w["_layout"] = "fused"
-    return w
-
-
-def prepare_folded_(w: dict, cfg: ModelConfig) -> dict:
-    """In-place conversion to the folded bf16 layout of the hybrid verify forward (idempotent): the
-    RMSNorm gains folded into the columns of the following matmul (wqkv, wgu, lm_head) exactly as in
-    ``prepare_fused_``, but rows keep the standard order, so the separate QKV / SwiGLU epilogue kernels
-    (which apply the per-token rstd, ``ygg_epi_*_rstd``) and the cluster split-K residual epilogues
-    work on them.  A fused-layout dict is left as it is (its forwards take the fused path)."""
-    if w.get("_layout") in ("folded", "fused"):
-        return w
-    for lw in w["layers"]:
-        an = lw["attn_norm"].float()
-        mn = lw["mlp_norm"].float()
-        lw["wqkv"] = (lw["wqkv"].float() * an[None, :]).to(lw["wqkv"].dtype).contiguous()
-        lw["wgu"] = (lw["wgu"].float() * mn[None, :]).to(lw["wgu"].dtype).contiguous()
-        lw["attn_norm"] = torch.ones_like(lw["attn_norm"])
-        lw["mlp_norm"] = torch.ones_like(lw["mlp_norm"])
-    fn = w["final_norm"].float()
-    if not bool(torch.all(fn == 1)):
-        w["lm_head"] = (w["lm_head"].float() * fn[None, :]).to(w["lm_head"].dtype)
-    w["final_norm"] = torch.ones_like(w["final_norm"])
-    w["_layout"] = "folded"
     return w
 
 

@@ -48,13 +48,6 @@ class ForwardPlan:
     gemv: bool | None = None
     decode_attn: bool | None = None
     fused_epilogues: bool = False   # fused-epilogue GEMMs for every non-GEMV bf16 pass (fused weight layout)
-    hybrid: bool = True             # non-GEMV bf16 passes on standard-layout weights (verify / AR / prefill):
-    #                                 norms folded into the weights (model.prepare_folded_), O and down as
-    #                                 cluster split-K GEMMs with the residual epilogue fused, QKV and gate|up
-    #                                 stream-K + the rstd-applying epilogue kernels (8 launches per layer
-    #                                 instead of 10; forward.py docstring)
-    epi_early_trigger: bool = False  # separate residual-norm / SwiGLU epilogue kernels followed by a GEMM trigger
-    #                                 it before their dependency wait (ygg_gemm_plan_set_epi_trigger)
     cluster_split_k: bool = True    # fused-epilogue GEMMs whose tiles x cluster fill one wave run as cluster
     #                                 split-K with a DSMEM reduction (csrc/gemm.cu gemm_cluster_kernel)
     lm_store_fused: bool = True     # LM-head logits straight from TMEM (no partials round trip)

@@ -14,8 +14,8 @@ import bench  # noqa: E402
 from paper_2512_23858_b200 import _lib as L  # noqa: E402
 
 VARIANTS = {
-    "o9": {"o": 9},          # round-1/2 ring: 224 KB solo ring for the o projection
-    "auto": {},              # stages capped at the chunks a CTA streams (o: 4)
+    "default": {},           # plan defaults (o: 224 KB solo ring = 9 stages)
+    "o4": {"o": 4},          # o ring = its 4 chunks (co-resident with the attention CTAs): slower
     "down6": {"down": 6},
     "down4": {"down": 4},
     "qkv2_gu2": {"qkv": 2, "gu": 2},

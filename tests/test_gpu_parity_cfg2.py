@@ -171,14 +171,10 @@ def test_cfg2_draft_gemv_pass_vs_oracle(pair, cuda):
     assert checked >= len(rows_b)  # at least one separated rank per row on average (top-1 is)
 
 
-@pytest.mark.parametrize("hybrid", [True, False])
-def test_cfg2_verify_pass_vs_oracle(pair, cuda, hybrid):
-    """T = 50 EGT verify rows at 8B dims: the default hybrid forward (folded norms, cluster split-K
-    residual GEMMs, rstd epilogue kernels) and the per-kernel forward, each against the fp32 oracle."""
+def test_cfg2_verify_pass_vs_oracle(pair, cuda):
     from oracle.llama_ref import RefLlama
     from paper_2512_23858_b200.forward import Forward, new_cache, prefill_causal
     from paper_2512_23858_b200.model import weights_to
-    from paper_2512_23858_b200.plan import ForwardPlan
 
     tc = pair["tc"]
     rng = np.random.default_rng(5)
@@ -189,8 +185,7 @@ def test_cfg2_verify_pass_vs_oracle(pair, cuda, hybrid):
     prompt = pair["prompt"]
     w = weights_to(pair["tw16"], cuda, torch.bfloat16)
     cache = new_cache(tc, 1, S, torch.bfloat16, cuda)
-    plan = ForwardPlan(hybrid=hybrid)
-    prefill_causal(tc, w, cache, prompt[None].to(cuda, torch.int32), torch.bfloat16, False, plan=plan)
+    prefill_causal(tc, w, cache, prompt[None].to(cuda, torch.int32), torch.bfloat16, False)
     bonus = int(rng.integers(tc.vocab))
     tokens = [bonus] + tree.token
     pos = [P0] + [P0 + 1 + d for d in tree.depth]
@@ -201,10 +196,8 @@ def test_cfg2_verify_pass_vs_oracle(pair, cuda, hybrid):
         for a in tree.path(i):
             m |= 1 << (1 + a)
         masks.append(m)
-    f = Forward(tc, w, cache, 1, T_rows, 2, torch.bfloat16, plan=plan)
-    assert not f.gemv and f.hybrid == hybrid
-    if hybrid:
-        assert w["_layout"] == "folded" and f.plans[0]["o"].cluster == 4 and f.plans[0]["down"].cluster == 4
+    f = Forward(tc, w, cache, 1, T_rows, 2, torch.bfloat16)
+    assert not f.gemv
     f.tokens.copy_(torch.tensor(tokens, dtype=torch.int32))
     f.pos.copy_(torch.tensor(pos, dtype=torch.int32))
     f.slot.copy_(torch.tensor(slots, dtype=torch.int32))

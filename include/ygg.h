@@ -260,6 +260,13 @@ int ygg_argmax_reduce(const void* keys, int ntiles, int M, int32_t* out, ygg_str
  * runs only through ygg_gemm_fused. */
 int ygg_gemm_plan_set_cluster(void* plan, int cluster);
 int ygg_gemm_plan_cluster(const void* plan);
+/* Row layout of W for this plan's separate QKV / SwiGLU epilogue kernels: interleaved != 0 = the fused
+ * layout (model.prepare_fused_: RoPE pair (i, i + hd/2) of a head at rows (2i, 2i + 1); gate j / up j
+ * at rows 2j / 2j + 1), so passes over fused-layout weights that do not take the GEMV (prefill chunks,
+ * batched draft levels) run the per-kernel epilogues.  Default 0 (standard row order). */
+int ygg_gemm_plan_set_layout(void* plan, int interleaved);
+/* TMA ring depth override of a bf16 stream-K plan (2..12 stages, <= 227 KB of shared memory). */
+int ygg_gemm_plan_set_stages(void* plan, int stages);
 /* L2 prefetch issued by this plan's separate epilogue kernel (ygg_epi_*): right after its dependency
  * wait every CTA pulls its share of [ptr, ptr + bytes) into L2 — a later weight stream, fetched while
  * HBM would otherwise idle.  bytes = 0 turns it off.  Results are unaffected. */

@@ -148,6 +148,8 @@ _SIGS: dict[str, tuple] = {
     "ygg_gemm_plan_set_cluster": (C.c_int, [vp, C.c_int]),
     "ygg_gemm_plan_cluster": (C.c_int, [vp]),
     "ygg_gemm_plan_set_epi_prefetch": (C.c_int, [vp, vp, C.c_size_t]),
+    "ygg_gemm_plan_set_layout": (C.c_int, [vp, C.c_int]),
+    "ygg_gemm_plan_set_stages": (C.c_int, [vp, C.c_int]),
     "ygg_gemm_fused": (C.c_int, [vp, vp, C.POINTER(YggEpilogue), vp]),
     "ygg_gemm_tiles": (C.c_int, [vp]),
     "ygg_embed_fused": (C.c_int, [vp, C.c_int, C.c_int, vp, C.c_int, vp, vp, vp, vp]),

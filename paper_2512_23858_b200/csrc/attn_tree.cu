@@ -269,7 +269,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   // Block bounds were written at least two kernels back (the kernel just before this one triggers
   // its dependents only after its own dependency wait): read them before the wait.
   const int bs = __ldg(a.blk_start + r), bl = __ldg(a.blk_len + r);
-  const int nkeys = bs + bl;
+  // causal block (no tree mask, e.g. a prefill chunk): this tile's last token sees block keys <= its own
+  const int nkeys = bs + (a.mask_words == 0 ? min(bl, t0 + tcnt) : bl);
   const int nch = (nkeys + kKC - 1) / kKC;
   const int n_my = nch > ks ? (nch - ks + C - 1) >> a.lc : 0;
   const int rounds = (n_my + NST - 1) / NST;

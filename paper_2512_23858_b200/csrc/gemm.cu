@@ -49,6 +49,7 @@ struct GemmPlan {
   int32_t* seg_table;  // device: seg_first[tiles+1], seg_base[num_ctas]
   const char* epi_pf;  // L2 prefetch region of this plan's separate epilogue kernel (or nullptr)
   size_t epi_pf_bytes;
+  int interleaved;     // W rows in the fused layout (RoPE pairs / gate-up pairs adjacent): separate epilogues
   alignas(64) CUtensorMap tmap_w;
   alignas(64) CUtensorMap tmap_x;
 };
@@ -805,6 +806,7 @@ struct EpiGeom {
   unsigned long long* trace;  // kernel-timeline slot (profiling only) or nullptr
   const char* pf;             // L2 prefetch region (a later weight stream) or nullptr
   size_t pf_bytes;
+  int il;                     // fused-layout rows (model.prepare_fused_): pairs are adjacent rows
 };
 
 // The epilogue kernels barely touch HBM (their partials are L2 hits): right after the dependency
@@ -1033,14 +1035,28 @@ __global__ void __launch_bounds__(kEpiThreads) epi_swiglu_kernel(EpiGeom g, cons
   const int m = blockIdx.y;
   const int F = g.N / 2;
   const int f = (blockIdx.x * blockDim.x + threadIdx.x) * 8;
-  const int2 sa = f < F ? epi_segs(g, m, f) : make_int2(0, 0), sb = f < F ? epi_segs(g, m, F + f) : make_int2(0, 0);
+  // fused layout: gate j / up j are rows 2j / 2j + 1, so this thread's 16 rows start at 2f (one tile)
+  const int na = g.il ? 2 * f : f, nb = g.il ? 2 * f + 8 : F + f;
+  const int2 sa = f < F ? epi_segs(g, m, na) : make_int2(0, 0), sb = f < F ? epi_segs(g, m, nb) : make_int2(0, 0);
   pdl_wait();
   pdl_launch_dependents();
   epi_l2_prefetch(g);
   if (threadIdx.x == 0) trace_min(g.trace, 1);
   if (f >= F) return;
   float gate[8], up[8], o[8];
-  epi_values2<8>(g, ws, m, f, F + f, gate, up, sa, sb);
+  if (g.il) {
+    float a[8], b[8];
+    epi_values2<8>(g, ws, m, na, nb, a, b, sa, sb);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      gate[i] = a[2 * i];
+      up[i] = a[2 * i + 1];
+      gate[4 + i] = b[2 * i];
+      up[4 + i] = b[2 * i + 1];
+    }
+  } else {
+    epi_values2<8>(g, ws, m, f, F + f, gate, up, sa, sb);
+  }
 #pragma unroll
   for (int i = 0; i < 8; ++i) o[i] = gate[i] / (1.f + expf(-gate[i])) * up[i];
   store8<ActT>(out + static_cast<size_t>(m) * F + f, o);
@@ -1091,8 +1107,9 @@ __global__ void __launch_bounds__(256) epi_qkv_rope_kernel(EpiGeom g, const floa
   const int head = it / per_head;
   const int i0 = (it % per_head) * 4;
   const int n0 = head * hd;
-  const int2 sa = it < items ? epi_segs(g, m, n0 + i0) : make_int2(0, 0);
-  const int2 sb = it < items ? epi_segs(g, m, n0 + i0 + half) : make_int2(0, 0);
+  // fused layout: rotation pair (i, i + hd/2) of a head is rows (2i, 2i + 1): this thread's 8 rows from 2*i0
+  const int2 sa = it < items ? epi_segs(g, m, g.il ? n0 + 2 * i0 : n0 + i0) : make_int2(0, 0);
+  const int2 sb = it < items ? epi_segs(g, m, g.il ? n0 + 2 * i0 : n0 + i0 + half) : make_int2(0, 0);
   pdl_wait();
   pdl_launch_dependents();
   epi_l2_prefetch(g);
@@ -1109,7 +1126,17 @@ __global__ void __launch_bounds__(256) epi_qkv_rope_kernel(EpiGeom g, const floa
       sn[j] = t.y;
     }
   }
-  epi_values2<4>(g, ws, m, n0 + i0, n0 + i0 + half, x1, x2, sa, sb);
+  if (g.il) {
+    float v[8];
+    epi_values<8>(g, ws, m, n0 + 2 * i0, v, sa);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      x1[j] = v[2 * j];
+      x2[j] = v[2 * j + 1];
+    }
+  } else {
+    epi_values2<4>(g, ws, m, n0 + i0, n0 + i0 + half, x1, x2, sa, sb);
+  }
   if (rot) {
     if (rope_cs) {
     } else {
@@ -1189,7 +1216,8 @@ static const GemmPlan* as_plan(const void* p) {
 }
 
 static EpiGeom geom_of(const GemmPlan* g, int kernel_id) {
-  return EpiGeom{g->M, g->N, g->BN, g->m_tiles, g->seg_table, trace_next(kernel_id), g->epi_pf, g->epi_pf_bytes};
+  return EpiGeom{g->M, g->N, g->BN, g->m_tiles, g->seg_table, trace_next(kernel_id), g->epi_pf, g->epi_pf_bytes,
+                 g->interleaved};
 }
 
 }  // namespace ygg
@@ -1280,8 +1308,10 @@ int ygg_gemm_plan_init(void* plan_mem, int dtype, const void* W, const void* X, 
     // decode attention of the verify (up to 190 KB itself) does not either way).  Same-box sweeps
     // of the cfg2 verify forward — with the split-KV tcgen05 attention: 113 KB 4.37 ms, 135 KB
     // 4.24, 150 KB 4.22, 165 KB 4.22, 190 KB 4.25, 227 KB 4.47; with the decode attention: 120 KB
-    // 3.76, 150 KB 3.605, 190 KB 3.586, 216 KB 3.605.
-    constexpr int smem_kb = 190;
+    // 3.76, 150 KB 3.605, 190 KB 3.586, 216 KB 3.605.  Compute-bound 256-token tiles (prefill chunks):
+    // 190 KB holds only 3 of their 48 KB stages; 4 stages (224 KB) run the cfg2 target prefill in 9.30
+    // vs 9.91 ms (scripts/prefill_stages_ab.py), the 1B draft's unchanged.
+    const int smem_kb = g->BN >= 256 ? 224 : 190;
     g->stages = std::min(12, (smem_kb * 1024 - kSmemExtra) / stage_bytes);
     YGG_CHECK_ARG(g->stages >= 2, "tile too large for shared memory");
     int cols = 32;
@@ -1487,6 +1517,23 @@ int ygg_gemm_plan_set_cluster(void* plan, int cluster) {
     return ygg_fail(YGG_ERR_UNSUPPORTED, "%d tiles need %d co-resident clusters of %d; only %d fit", g->tiles,
                     g->tiles, cluster, max_clusters);
   g->cluster = cluster;
+  return YGG_OK;
+}
+
+int ygg_gemm_plan_set_stages(void* plan, int stages) {
+  GemmPlan* g = const_cast<GemmPlan*>(plan_of(plan));
+  YGG_CHECK_ARG(g != nullptr && g->dtype == YGG_BF16, "invalid bf16 GEMM plan");
+  YGG_CHECK_ARG(stages >= 2 && stages <= 12, "stages must be in [2, 12]");
+  YGG_CHECK_ARG(kSmemExtra + static_cast<size_t>(stages) * (kBM * kBK * 2 + g->BN * kBK * 2) <= 227 * 1024,
+                "ring exceeds shared memory");
+  g->stages = stages;
+  return YGG_OK;
+}
+
+int ygg_gemm_plan_set_layout(void* plan, int interleaved) {
+  GemmPlan* g = const_cast<GemmPlan*>(plan_of(plan));
+  YGG_CHECK_ARG(g != nullptr, "invalid GEMM plan");
+  g->interleaved = interleaved ? 1 : 0;
   return YGG_OK;
 }
 

@@ -25,6 +25,7 @@ residual stream is f32 in every path.
 
 from __future__ import annotations
 
+import contextlib
 import ctypes as C
 import math
 
@@ -99,7 +100,10 @@ class Forward:
         decode_attn: bool | None = None,
         plan: ForwardPlan | None = None,
         lm_argmax: bool = False,
+        last_logits: bool = False,
     ):
+        """``last_logits``: the LM head runs on each request's last row only (``logits`` is [B, V]) — a
+        prefill chunk needs nothing else, and the [B*R, V] head is most of a chunk's wasted work."""
         L.require_device()
         plan = plan or DEFAULT
         self.plan = plan
@@ -119,9 +123,13 @@ class Forward:
         # fused weight layout, which then also routes every other bf16 forward on these weights
         # (prefill, verify) through the fused-epilogue GEMM.
         self.gemv = bool(gemv) and bf16 and logits and B * R <= 16 and mask_words <= L.MAX_MASK_WORDS
-        self.fused = bf16 and (plan.fused_epilogues or self.gemv or weights.get("_layout") == "fused")
-        if self.fused:
+        self.layout_fused = bf16 and (plan.fused_epilogues or self.gemv or weights.get("_layout") == "fused")
+        if self.layout_fused:
             prepare_fused_(weights, cfg)
+        # Non-GEMV passes over fused-layout weights (draft prefill chunks, batched draft levels) run the
+        # per-kernel epilogues with the layout flag (ygg_gemm_plan_set_layout) unless the plan asks for the
+        # fused-epilogue GEMMs (measured slower at M = 512: DESIGN.md §4).
+        self.fused = self.layout_fused and (self.gemv or plan.fused_epilogues or plan.fused_layout_gemm)
         self.w = weights
         dev = cache.device
         M, d = self.M, cfg.d_model
@@ -140,7 +148,10 @@ class Forward:
         self.q = torch.zeros(M, cfg.q_dim, dtype=act_dtype, device=dev)
         self.attn = torch.zeros(M, cfg.q_dim, dtype=act_dtype, device=dev)
         self.mlp = torch.zeros(M, cfg.ffn, dtype=act_dtype, device=dev)
-        self.logits = torch.zeros(M, cfg.vocab, dtype=torch.float32, device=dev) if logits else None
+        self.last_logits = bool(last_logits and logits)
+        self.logits = (torch.zeros(B if self.last_logits else M, cfg.vocab, dtype=torch.float32, device=dev)
+                       if logits else None)
+        self.xn_last = torch.zeros(B, d, dtype=act_dtype, device=dev) if self.last_logits else None
         self.layer_stride = cache.stride(0)
         self.S = cache.shape[4]
         self.scale = 1.0 / math.sqrt(cfg.head_dim)
@@ -155,7 +166,8 @@ class Forward:
             }
             self.plans.append(p)
             ws = max(ws, *(q.ws_bytes for q in p.values()))
-        self.lm_plan = GemmPlan(weights["lm_head"], self.xn, M, num_ctas) if logits else None
+        self.lm_plan = (GemmPlan(weights["lm_head"], self.xn_last if self.last_logits else self.xn,
+                                 B if self.last_logits else M, num_ctas) if logits else None)
         if self.lm_plan:
             ws = max(ws, self.lm_plan.ws_bytes)
         self.ws = torch.empty(max(ws // 4, 1), dtype=torch.float32, device=dev)
@@ -191,7 +203,10 @@ class Forward:
         # a thread-block cluster, merged through DSMEM; replaces the decode attention when planned.
         self.at_plans = None
         use_tree = plan.tree_attn if plan.tree_attn is not None else not self.gemv
-        if self.ad_plans is not None and use_tree and gh <= 32 and gh & (gh - 1) == 0:
+        # causal passes (prefill chunks, no tree mask) take it too: one CTA per (kv head, request, 32-token
+        # row tile) that walks only the keys its last token sees, instead of split-KV + combine launches
+        causal_tree = mask_words == 0 and plan.prefill_tree_attn and act_dtype == torch.bfloat16
+        if (self.ad_plans is not None and use_tree or causal_tree) and gh <= 32 and gh & (gh - 1) == 0:
             lib = L.lib()
             es = cache.element_size()
             self.at_plans = []
@@ -207,7 +222,7 @@ class Forward:
         self.lm_epi = None
         # Greedy verify (lm_argmax): the LM head stores no logits, only per-128-row-tile keys of each
         # token's first maximum (YGG_EPI_ARGMAX), reduced by ygg_argmax_reduce.
-        self.lm_argmax = bool(lm_argmax and bf16 and self.lm_plan is not None and M <= 512)
+        self.lm_argmax = bool(lm_argmax and bf16 and self.lm_plan is not None and M <= 512 and not self.last_logits)
         if self.lm_argmax:
             self.lm_keys = torch.zeros(cfg.vocab // 128, M, dtype=torch.int64, device=dev)
         if bf16 and not self.fused and self.lm_plan is not None and (plan.lm_store_fused or self.lm_argmax):
@@ -220,6 +235,10 @@ class Forward:
             self.lm_epi = e
         if self.fused:
             self._setup_fused()
+        elif self.layout_fused:
+            for p in self.plans:
+                L.check(L.lib().ygg_gemm_plan_set_layout(p["qkv"].handle, 1))
+                L.check(L.lib().ygg_gemm_plan_set_layout(p["gu"].handle, 1))
         if self.gemv:
             self._setup_gemv()
         self._setup_attn_l2_prefetch()
@@ -413,9 +432,12 @@ class Forward:
             cur["plan"] = p["down"]
             p["down"].epi = epi(L.YGG_EPI_RESID, resid=self.resid.data_ptr(), hb=self.xn.data_ptr(),
                                 ss_out=self.ss_a.data_ptr())
+        if self.last_logits:
+            self.ss_last = torch.zeros(nt, self.B, dtype=torch.float32, device=dev)
         if self.lm_plan:
             cur["plan"] = self.lm_plan
-            self.lm_plan.epi = epi(L.YGG_EPI_ARGMAX if self.lm_argmax else L.YGG_EPI_STORE_F32, ss_in=self.ss_a.data_ptr(),
+            lm_ss = self.ss_last if self.last_logits else self.ss_a
+            self.lm_plan.epi = epi(L.YGG_EPI_ARGMAX if self.lm_argmax else L.YGG_EPI_STORE_F32, ss_in=lm_ss.data_ptr(),
                                    ss_tiles=nt, norm_dim=d, eps=eps,
                                    out=(self.lm_keys if self.lm_argmax else self.logits).data_ptr(), ld=cfg.vocab)
 
@@ -473,6 +495,14 @@ class Forward:
         else:
             self._run_unfused(stream)
 
+    def _gather_last(self, stream) -> None:
+        """last_logits: each request's last row of the LM-head input (and, fused, of its sums of squares)."""
+        with torch.cuda.stream(stream) if stream is not None else contextlib.nullcontext():
+            self.xn_last.copy_(self.xn.view(self.B, self.R, -1)[:, -1])
+            if self.fused:
+                nt = self.ss_a.shape[0]
+                self.ss_last.copy_(self.ss_a.view(nt, self.B, self.R)[:, :, -1])
+
     def _run_fused(self, stream, stamps: torch.Tensor | None = None) -> None:
         """``stamps`` (int64 [>= 6*layers+3], debug only): a %globaltimer stamp kernel is enqueued
         after every launch, giving in-graph per-kernel durations."""
@@ -504,6 +534,8 @@ class Forward:
             chk(lib.ygg_gemm_fused(p["down"].handle, ws, C.byref(p["down"].epi), s))
             stamp()
         if self.lm_plan is not None:
+            if self.last_logits:
+                self._gather_last(stream)
             chk(lib.ygg_gemm_fused(self.lm_plan.handle, ws, C.byref(self.lm_plan.epi), s))
             stamp()
 
@@ -563,6 +595,8 @@ class Forward:
                                           cfg.norm_eps, self.xn.data_ptr(), self.act, s))
             stamp()
         if self.lm_plan is not None:
+            if self.last_logits:
+                self._gather_last(stream)
             if self.lm_epi is not None:
                 chk(lib.ygg_gemm_fused(self.lm_plan.handle, ws, C.byref(self.lm_epi), s))
             else:
@@ -590,7 +624,7 @@ def prefill_causal(cfg: ModelConfig, w: dict, cache: torch.Tensor, prompts: torc
         f = fwd.get(key)
         if f is None:
             f = Forward(cfg, w, cache, B, n, 0, act_dtype, logits=final and want_logits, gemv=False,
-                        decode_attn=False, plan=plan)
+                        decode_attn=False, plan=plan, last_logits=True)
             fwd[key] = f
         f.tokens.copy_(prompts[:, c0:c0 + n].reshape(-1))
         pos = torch.arange(c0, c0 + n, dtype=torch.int32, device=dev).repeat(B)
@@ -600,7 +634,7 @@ def prefill_causal(cfg: ModelConfig, w: dict, cache: torch.Tensor, prompts: torc
         f.blk_len.fill_(n)
         f.run()
         if final and want_logits:
-            last = f.logits.view(B, n, -1)[:, -1, :].contiguous()
+            last = f.logits
     return last
 
 

@@ -48,6 +48,9 @@ class ForwardPlan:
     gemv: bool | None = None
     decode_attn: bool | None = None
     fused_epilogues: bool = False   # fused-epilogue GEMMs for every non-GEMV bf16 pass (fused weight layout)
+    fused_layout_gemm: bool = False  # non-GEMV passes over weights already in the fused layout (the draft's
+    #                                  prefill / batched levels) take the fused-epilogue GEMMs too (default:
+    #                                  stream-K GEMM + layout-aware epilogue kernels, faster at M = 512)
     cluster_split_k: bool = True    # fused-epilogue GEMMs whose tiles x cluster fill one wave run as cluster
     #                                 split-K with a DSMEM reduction (csrc/gemm.cu gemm_cluster_kernel)
     lm_store_fused: bool = True     # LM-head logits straight from TMEM (no partials round trip)
@@ -60,6 +63,8 @@ class ForwardPlan:
     #                                 automatic: verify / AR passes (measured at parity in the cfg2 verify
     #                                 graph, 3.498 vs 3.491 ms), not the GEMV draft passes (32 query rows
     #                                 per kv head: 0.604 vs 0.565 ms per pass)
+    prefill_tree_attn: bool = True  # causal passes (prefill chunks) on the tree attention too (causal tiles
+    #                                 stop at their last token's key) instead of split-KV tcgen05 + combine
     tree_csplit: int = 0            # its key-split cluster size (0 = automatic)
     tree_row_tiles: int = 0         # its row tiles per (kv head, request) (0 = fewest)
     # L2 prefetch issued by latency-bound kernels (see module docstring)

@@ -319,3 +319,42 @@ def test_cfg2_verify_pass_cluster_fused_vs_oracle(pair, cuda):
     want = ref.forward(rc, tokens, pos, slots, vis)
     err = _rel_err(got, want)
     assert err <= 2e-2, err
+
+
+@pytest.mark.parametrize("fused_gemm", [False, True])
+def test_cfg2_draft_prefill_fused_layout_vs_oracle(pair, cuda, fused_gemm):
+    """Causal prefill of the 1B-dims draft on fused-layout weights (RoPE-pair-interleaved QKV rows,
+    interleaved gate|up rows, folded norms) — the path every draft prefill takes: stream-K GEMMs with
+    the layout-aware QKV / SwiGLU epilogue kernels (ygg_gemm_plan_set_layout), causal tree attention and
+    the last-row LM head (default), or the fused-epilogue GEMMs (fused_layout_gemm).  The last row's
+    logits within 2e-2 of the fp32 oracle, the whole prompt's K / V within 2e-2."""
+    from oracle.llama_ref import RefLlama
+    from paper_2512_23858_b200.forward import new_cache, prefill_causal
+    from paper_2512_23858_b200.model import prepare_fused_, weights_to
+    from paper_2512_23858_b200.plan import ForwardPlan
+
+    dc = pair["dc"]
+    S, n = 512, P0
+    prompt = pair["prompt"]
+    w = prepare_fused_(weights_to(pair["dw16"], cuda, torch.bfloat16), dc)
+    cache = new_cache(dc, 1, S, torch.bfloat16, cuda)
+    fwd = {}
+    last = prefill_causal(dc, w, cache, prompt[None].to(cuda, torch.int32), torch.bfloat16, True, fwd,
+                          plan=ForwardPlan(fused_layout_gemm=fused_gemm))
+    f = next(iter(fwd.values()))
+    assert f.layout_fused and f.fused == fused_gemm and f.last_logits and f.at_plans is not None
+    got = last.cpu()
+    assert got.shape == (1, dc.vocab)
+    ref = RefLlama(dc, pair["dw16"])
+    from oracle.llama_ref import RefCache, causal_visible
+
+    rc = RefCache(dc, S)
+    pos = list(range(n))
+    want = ref.forward(rc, prompt.tolist(), pos, pos, causal_visible(n, S))[-1:]
+    err = _rel_err(got, want)
+    assert err <= 2e-2, err
+    for li in range(dc.n_layers):
+        kg = cache[li, 0, 0].float().cpu()[:, :n, :]
+        vg = cache[li, 0, 1].float().cpu().reshape(dc.n_kv_heads, dc.head_dim, S)[:, :, :n].transpose(1, 2)
+        assert _rel_err(kg, rc.k[li][:, :n]) <= 2e-2
+        assert _rel_err(vg, rc.v[li][:, :n]) <= 2e-2

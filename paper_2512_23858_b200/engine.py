@@ -155,6 +155,7 @@ class SpecDecoder:
         self.set_profiles(profiles)
         self.prefill_len = prefill_len
         self._prefill_fwd = share._prefill_fwd if share is not None else {}
+        self._prefill_side = None  # side stream of the draft prefill (created on first use)
         # root candidate probabilities of the step's pass 0 (depth-predictor features)
         self.root_probs = torch.zeros(batch, k, **f64)
         # calibrated acceptance (ExplicitAcceptance by grown-tree position): device counts of tested /
@@ -208,14 +209,23 @@ class SpecDecoder:
         prompts_d = prompts.to(self.dev, torch.int32)
         self.seq.hist.zero_()
         self.seq.hist[:, :P0] = prompts_d
-        for cfg, w, cache in ((self.tc, self.tw, self.tcache), (self.dc, self.dw, self.dcache)):
-            last = prefill_causal(cfg, w, cache, prompts_d, self.act_dtype, cfg is self.tc, self._prefill_fwd,
-                                  plan=self.plan)
-            if cfg is self.tc:
-                am = torch.zeros(B, dtype=torch.int32, device=self.dev)
-                L.check(lib.ygg_row_stats(last.data_ptr(), L.YGG_F32, B, cfg.vocab, cfg.vocab, 1.0, am.data_ptr(),
-                                          None, s))
-                self.seq.hist[torch.arange(B, device=self.dev), P0] = am
+        # The two models' prefills are independent: the draft's runs on a side stream, filling the SMs the
+        # target's latency-bound kernels (attention, epilogues, dependency gaps) leave idle.
+        main = torch.cuda.current_stream(self.dev)
+        if self._prefill_side is None:
+            self._prefill_side = torch.cuda.Stream(self.dev)
+        side = self._prefill_side
+        side.wait_stream(main)
+        with torch.cuda.stream(side):
+            prefill_causal(self.dc, self.dw, self.dcache, prompts_d, self.act_dtype, False, self._prefill_fwd,
+                           plan=self.plan)
+        last = prefill_causal(self.tc, self.tw, self.tcache, prompts_d, self.act_dtype, True, self._prefill_fwd,
+                              plan=self.plan)
+        am = torch.zeros(B, dtype=torch.int32, device=self.dev)
+        L.check(lib.ygg_row_stats(last.data_ptr(), L.YGG_F32, B, self.tc.vocab, self.tc.vocab, 1.0, am.data_ptr(),
+                                  None, s))
+        self.seq.hist[torch.arange(B, device=self.dev), P0] = am
+        main.wait_stream(side)
         self.seq.P.fill_(P0)
         self.seq.n_gen.fill_(1)
         self.seq.step.zero_()

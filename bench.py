@@ -123,6 +123,22 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(rows)}
 
 
+def plan_from_args(items):
+    """ForwardPlan from ``key=value`` overrides (ints / bools / None); the default plan when empty."""
+    if not items:
+        return None
+    from paper_2512_23858_b200.plan import ForwardPlan
+
+    kw = {}
+    for it in items:
+        k, v = it.split("=", 1)
+        kw[k] = None if v == "None" else int(v) if v.lstrip("-").isdigit() else v
+        if k in ("gemv", "decode_attn", "tree_attn", "fused_epilogues", "fused_layout_gemm", "cluster_split_k",
+                 "lm_store_fused", "topk_fused", "prefill_tree_attn") and kw[k] is not None:
+            kw[k] = bool(kw[k])
+    return ForwardPlan(**kw)
+
+
 def build_decoder(wl: dict, name: str, device, seed_offset: int = 0, weights=None, profiles=None,
                   overlap_compaction: bool = False, plan=None):
     import torch
@@ -137,8 +153,9 @@ def build_decoder(wl: dict, name: str, device, seed_offset: int = 0, weights=Non
         # (a 70B target does not fit host RAM in fp32: cfg5 generates on the device)
         cp = Coupling(**COUPLING[name])
         gen = "cpu" if tc.matmul_params() * 4 < 64e9 else device
-        tw = weights_to(init_weights(tc, 0, torch.float32, gen, cp), device, torch.bfloat16)
-        dw = weights_to(init_weights(dc, 1, torch.float32, gen, cp), device, torch.bfloat16)
+        gdt = torch.float32 if gen == "cpu" else torch.bfloat16  # (a 70B fp32 copy does not fit the GPU either)
+        tw = weights_to(init_weights(tc, 0, gdt, gen, cp), device, torch.bfloat16)
+        dw = weights_to(init_weights(dc, 1, gdt, gen, cp), device, torch.bfloat16)
     else:
         tw, dw = weights
 
@@ -577,7 +594,8 @@ def run_ours(args, rank, world, local_rank):
     if "global_batch" in wl:
         wl["batch"] = max(1, wl["global_batch"] // world)
     peak, peak_kind, _ = _peaks()
-    sd, tc, dc = build_decoder(wl, args.workload, device, overlap_compaction=args.overlap_compaction)
+    sd, tc, dc = build_decoder(wl, args.workload, device, overlap_compaction=args.overlap_compaction,
+                               plan=plan_from_args(args.plan))
     prompts = prompts_for(wl, tc.vocab, rank)
     sd.prefill_len = prompts.shape[1]
     sd.prefill(prompts)
@@ -770,6 +788,8 @@ def main():
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default="cfg2")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-ar-baseline", action="store_true")
+    ap.add_argument("--plan", action="append", default=[],
+                    help="ForwardPlan override key=value (A/B runs), e.g. --plan fused_layout_gemm=1")
     ap.add_argument("--aal-steps", type=int, default=180,
                     help="untimed extra greedy steps after the e2e run for the long-window AAL (0 = off)")
     ap.add_argument("--overlap-compaction", action="store_true",

@@ -1283,8 +1283,12 @@ int ygg_gemm_plan_init(void* plan_mem, int dtype, const void* W, const void* X, 
   g->N = N;
   g->K = K;
   const int mp = (M + 15) / 16 * 16;
-  g->BN = mp <= 256 ? mp : 256;
-  if (dtype == YGG_F32) g->BN = mp <= 256 ? mp : 256;
+  // Token tile (UMMA N): as few tiles of <= 256 as the rows need, split evenly (multiple of 16), so a
+  // 520-row cfg5 verify runs 3 x 176 instead of 3 x 256 columns of MMA work (2 x 256 at 512 rows).
+  {
+    const int mt = (mp + 255) / 256;
+    g->BN = ((mp + mt - 1) / mt + 15) / 16 * 16;
+  }
   g->m_tiles = (M + g->BN - 1) / g->BN;
   g->n_tiles = N / kBM;
   g->tiles = g->n_tiles * g->m_tiles;

@@ -20,6 +20,7 @@ shape (D, W, max_verify, B) as a CUDA graph and replayed with no host synchronis
 
 from __future__ import annotations
 
+import dataclasses
 from dataclasses import dataclass
 
 import numpy as np
@@ -115,7 +116,10 @@ class SpecDecoder:
         tmw = max(1, (self.T + 31) // 32)
         dmw = max(1, (self.tree_cap + 31) // 32)
         self.plan = plan
-        self.draft = Forward(draft_cfg, draft_w, self.dcache, batch, self.R, dmw, act_dtype, plan=plan)
+        dplan = plan or ForwardPlan()
+        if dplan.tree_attn is None:  # draft levels keep the mma.sync decode attention (plan.py: tree_attn)
+            dplan = dataclasses.replace(dplan, tree_attn=False)
+        self.draft = Forward(draft_cfg, draft_w, self.dcache, batch, self.R, dmw, act_dtype, plan=dplan)
         # The verify always runs the target's tree-pass families (stream-K GEMM, decode attention), never
         # the draft's row-block GEMV even when B * T <= 16: the GEMV needs the fused weight layout (it
         # would rewrite the shared target weights in place) and would round differently from ARDecoder,

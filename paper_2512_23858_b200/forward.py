@@ -129,7 +129,8 @@ class Forward:
         # Non-GEMV passes over fused-layout weights (draft prefill chunks, batched draft levels) run the
         # per-kernel epilogues with the layout flag (ygg_gemm_plan_set_layout) unless the plan asks for the
         # fused-epilogue GEMMs (measured slower at M = 512: DESIGN.md §4).
-        self.fused = self.layout_fused and (self.gemv or plan.fused_epilogues or plan.fused_layout_gemm)
+        flg = plan.fused_layout_gemm if plan.fused_layout_gemm is not None else B * R <= 128
+        self.fused = self.layout_fused and (self.gemv or plan.fused_epilogues or flg)
         self.w = weights
         dev = cache.device
         M, d = self.M, cfg.d_model

@@ -48,9 +48,11 @@ class ForwardPlan:
     gemv: bool | None = None
     decode_attn: bool | None = None
     fused_epilogues: bool = False   # fused-epilogue GEMMs for every non-GEMV bf16 pass (fused weight layout)
-    fused_layout_gemm: bool = False  # non-GEMV passes over weights already in the fused layout (the draft's
-    #                                  prefill / batched levels) take the fused-epilogue GEMMs too (default:
-    #                                  stream-K GEMM + layout-aware epilogue kernels, faster at M = 512)
+    fused_layout_gemm: bool | None = None  # non-GEMV passes over weights already in the fused layout (the
+    #                                  draft's prefill / batched levels): fused-epilogue GEMMs, or stream-K GEMM +
+    #                                  layout-aware epilogue kernels; None = by rows: fused up to 128 (cfg4 draft
+    #                                  levels, 16 x 8 rows: 35.6 vs 36.0 ms per step), per-kernel above (512-row
+    #                                  prefill chunk of the 1B draft: 2.0 vs 3.7 ms)
     cluster_split_k: bool = True    # fused-epilogue GEMMs whose tiles x cluster fill one wave run as cluster
     #                                 split-K with a DSMEM reduction (csrc/gemm.cu gemm_cluster_kernel)
     lm_store_fused: bool = True     # LM-head logits straight from TMEM (no partials round trip)
@@ -61,8 +63,9 @@ class ForwardPlan:
     tree_attn: bool | None = None   # tcgen05 / TMEM tree attention (csrc/attn_tree.cu) instead of the
     #                                 mma.sync decode attention wherever the latter would run; None =
     #                                 automatic: verify / AR passes (measured at parity in the cfg2 verify
-    #                                 graph, 3.498 vs 3.491 ms), not the GEMV draft passes (32 query rows
-    #                                 per kv head: 0.604 vs 0.565 ms per pass)
+    #                                 graph, 3.498 vs 3.491 ms), not draft passes (32 query rows per kv head:
+    #                                 cfg2 GEMV pass 0.604 vs 0.565 ms; cfg4 batched levels 39.3 vs 36.0 ms
+    #                                 per step) — SpecDecoder builds its draft forward with tree_attn=False
     prefill_tree_attn: bool = True  # causal passes (prefill chunks) on the tree attention too (causal tiles
     #                                 stop at their last token's key) instead of split-KV tcgen05 + combine
     tree_csplit: int = 0            # its key-split cluster size (0 = automatic)

@@ -58,11 +58,11 @@ def test_store_f32_with_rstd(ctas, M, cuda):
     W = (torch.randn(N, K, device=cuda, generator=g) / math.sqrt(K)).to(torch.bfloat16)
     ss = torch.rand(4, M, device=cuda, generator=g) * 100
     out = torch.zeros(M, N, device=cuda)
-    if ctas in ("c3", "c4") and M > 256:  # BN = 256: the receive slots leave no room for a ring
-        with pytest.raises(ValueError, match="ring"):
-            _plan(W, X, M, ctas)
+    try:
+        plan = _plan(W, X, M, ctas)
+    except ValueError as exc:  # wide token tiles: the cluster's receive slots may leave no room for a ring
+        assert ctas in ("c3", "c4") and M > 256 and "ring" in str(exc)
         return
-    plan = _plan(W, X, M, ctas)
     cnt = torch.zeros(plan.tiles, dtype=torch.int32, device=cuda)
     _run(plan, _epi(L.YGG_EPI_STORE_F32, cnt, ss_in=ss.data_ptr(), ss_tiles=4, norm_dim=512, eps=1e-5,
                     out=out.data_ptr(), ld=N), cuda)

@@ -207,7 +207,8 @@ class Forward:
         # causal passes (prefill chunks, no tree mask) take it too: one CTA per (kv head, request, 32-token
         # row tile) that walks only the keys its last token sees, instead of split-KV + combine launches
         causal_tree = mask_words == 0 and plan.prefill_tree_attn and act_dtype == torch.bfloat16
-        if (self.ad_plans is not None and use_tree or causal_tree) and gh <= 32 and gh & (gh - 1) == 0:
+        tree_pass = use_tree and act_dtype == torch.bfloat16 and 0 < mask_words <= L.MAX_MASK_WORDS
+        if (tree_pass or causal_tree) and gh <= 32 and gh & (gh - 1) == 0:
             lib = L.lib()
             es = cache.element_size()
             self.at_plans = []

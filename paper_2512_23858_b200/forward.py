@@ -129,8 +129,7 @@ class Forward:
         # Non-GEMV passes over fused-layout weights (draft prefill chunks, batched draft levels) run the
         # per-kernel epilogues with the layout flag (ygg_gemm_plan_set_layout) unless the plan asks for the
         # fused-epilogue GEMMs (measured slower at M = 512: DESIGN.md §4).
-        flg = plan.fused_layout_gemm if plan.fused_layout_gemm is not None else B * R <= 128
-        self.fused = self.layout_fused and (self.gemv or plan.fused_epilogues or flg)
+        self.fused = self.layout_fused and (self.gemv or plan.fused_epilogues or plan.fused_layout_gemm)
         self.w = weights
         dev = cache.device
         M, d = self.M, cfg.d_model
@@ -186,7 +185,7 @@ class Forward:
         # combine).  Prefill and wide batched verifies keep the split-KV tcgen05 kernel.
         self.ad_plans = None
         gh = cfg.n_heads // cfg.n_kv_heads
-        tree_fits = mask_words > 0 and B * cfg.n_kv_heads * ((R * gh + 63) // 64) <= 148
+        tree_fits = mask_words > 0 and (B * cfg.n_kv_heads * ((R * gh + 63) // 64) <= 148 or plan.decode_attn_wide)
         if (decode_attn and act_dtype == torch.bfloat16 and mask_words <= L.MAX_MASK_WORDS
                 and (R * gh <= 64 or tree_fits)):
             lib = L.lib()

@@ -48,15 +48,16 @@ class ForwardPlan:
     gemv: bool | None = None
     decode_attn: bool | None = None
     fused_epilogues: bool = False   # fused-epilogue GEMMs for every non-GEMV bf16 pass (fused weight layout)
-    fused_layout_gemm: bool | None = None  # non-GEMV passes over weights already in the fused layout (the
-    #                                  draft's prefill / batched levels): fused-epilogue GEMMs, or stream-K GEMM +
-    #                                  layout-aware epilogue kernels; None = by rows: fused up to 128 (cfg4 draft
-    #                                  levels, 16 x 8 rows: 35.6 vs 36.0 ms per step), per-kernel above (512-row
-    #                                  prefill chunk of the 1B draft: 2.0 vs 3.7 ms)
+    fused_layout_gemm: bool = False  # non-GEMV passes over weights already in the fused layout (the draft's
+    #                                  prefill chunks): fused-epilogue GEMMs instead of stream-K GEMM + the
+    #                                  layout-aware epilogue kernels (512-row chunk of the 1B draft: 3.7 vs 2.0 ms)
     cluster_split_k: bool = True    # fused-epilogue GEMMs whose tiles x cluster fill one wave run as cluster
     #                                 split-K with a DSMEM reduction (csrc/gemm.cu gemm_cluster_kernel)
     lm_store_fused: bool = True     # LM-head logits straight from TMEM (no partials round trip)
     topk_fused: bool = True         # draft top-k partials from the LM-head GEMV epilogue
+    decode_attn_wide: bool = False  # the decode attention also for tree passes whose row tiles exceed a wave
+    #                                 (measured slower than the tree attention: cfg4 verify 20.2 vs 17.4 ms,
+    #                                 cfg5 94.0 vs 91.8 ms; scripts/cfg_plan_ab.py)
     attn_kvsplit: int = 0           # decode attention cluster size (0 = automatic)
     attn_ksplit: int = 0            # decode attention key-split warp groups per CTA (0 = automatic)
     attn_stages: int = 0            # decode attention K/V ring stages (0 = automatic)

@@ -13,8 +13,10 @@ from paper_2512_23858_b200 import _lib as L  # noqa: E402
 from paper_2512_23858_b200.forward import Forward  # noqa: E402
 
 which = sys.argv[1] if len(sys.argv) > 1 else "draft"
-wl = bench.WORKLOADS["cfg2"]
-sd, tc, dc = bench.build_decoder(wl, "cfg2", torch.device("cuda"))
+WL = os.environ.get("YGG_WORKLOAD", "cfg2")  # tooling: which bench workload to trace
+wl = dict(bench.WORKLOADS[WL])
+wl.setdefault("batch", wl.get("global_batch", 1))
+sd, tc, dc = bench.build_decoder(wl, WL, torch.device("cuda"))
 sd.prefill(bench.prompts_for(wl, tc.vocab, 0))
 for _ in range(2):
     sd.step(use_graph=False)
@@ -50,7 +52,7 @@ dbg = None
 if getattr(g, "at_plans", None):  # per-CTA checkpoints of layer 10's tree attention
     dbg = torch.zeros(1024, 16, dtype=torch.int64, device="cuda")
     L.check(lib.ygg_attn_tree_set_debug(g.at_plans[10], dbg.data_ptr()))
-CAP = 512
+CAP = 2048
 buf = torch.zeros(CAP, 8, dtype=torch.int64, device="cuda")
 
 

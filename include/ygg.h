@@ -265,33 +265,6 @@ int ygg_gemm_plan_cluster(const void* plan);
  * at rows 2j / 2j + 1), so passes over fused-layout weights that do not take the GEMV (prefill chunks,
  * batched draft levels) run the per-kernel epilogues.  Default 0 (standard row order). */
 int ygg_gemm_plan_set_layout(void* plan, int interleaved);
-/* Prologue epilogue of a bf16 stream-K plan (prologue verify): the previous GEMM's f32
- * partials are finished into this GEMM's X by its own epilogue warps while its weight ring fills, instead
- * of by a separate epilogue kernel between the two launches.  RESID: X = bf16(resid += prev), resid
- * updated in place, ss_out[K/64][M] = per-64-feature-block sums of squares (RMSNorm folded: gains in the
- * weights, rstd applied by the consumer).  SWIGLU: X = bf16(silu(g r) (u r)) with g / u the previous
- * GEMM's halves and r the rstd from ss_in [ss_tiles][M].  The work is spread over every CTA; each
- * CTA then adds one release arrival to flags[0] and loads X once it reads epoch * grid (epochs counted
- * per CTA in launches[grid]; both zero-initialised and owned by this plan).  prev_ws must not be the workspace this plan writes.  kind = 0 removes it.
- * Replaces the RMSNorm / residual / SwiGLU the reference prices inside latency_at(profiles.verifier, ...)
- * (pkg/src/specsim/simulator.py:211). */
-#define YGG_PRO_NONE 0
-#define YGG_PRO_RESID 1
-#define YGG_PRO_SWIGLU 2
-typedef struct {
-  int kind;
-  const void* prev_plan;
-  const float* prev_ws;
-  float* resid;
-  float* ss_out;
-  const float* ss_in;
-  int ss_tiles;
-  int norm_dim;
-  float eps;
-  int32_t* flags;
-  int32_t* launches;
-} ygg_prologue;
-int ygg_gemm_plan_set_prologue(void* plan, const ygg_prologue* pro);
 /* TMA ring depth override of a bf16 stream-K plan (2..12 stages, <= 227 KB of shared memory). */
 int ygg_gemm_plan_set_stages(void* plan, int stages);
 /* L2 prefetch issued by this plan's separate epilogue kernel (ygg_epi_*): right after its dependency
@@ -314,12 +287,6 @@ int ygg_epi_swiglu(const void* plan, const float* ws, void* out, int act_dtype, 
 int ygg_epi_qkv_rope(const void* plan, const float* ws, int Hq, int Hkv, int hd, float rope_theta,
                      const int32_t* pos, const int32_t* slot, const int32_t* req, void* q_out, void* cache,
                      int S, int act_dtype, const float* rope_cs, ygg_stream_t stream);
-/* The same with the folded RMSNorm's rstd = rsqrt(sum_t ss_in[t][m] / norm_dim + eps) applied to the
- * partial sums first (the QKV GEMM ran on the unnormalised residual; ss_in == NULL: the plain kernel). */
-int ygg_epi_qkv_rope_rstd(const void* plan, const float* ws, const float* ss_in, int ss_tiles, int norm_dim,
-                          float eps, int Hq, int Hkv, int hd, float rope_theta, const int32_t* pos,
-                          const int32_t* slot, const int32_t* req, void* q_out, void* cache, int S,
-                          int act_dtype, const float* rope_cs, ygg_stream_t stream);
 
 int ygg_embed(const void* table, int dtype, int V, int d, const int32_t* tokens, int M, float* resid_out,
               ygg_stream_t stream);

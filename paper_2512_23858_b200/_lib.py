@@ -98,18 +98,6 @@ class YggEpilogue(C.Structure):
     ]
 
 
-class YggPrologue(C.Structure):
-    """ygg_prologue (include/ygg.h)."""
-
-    _fields_ = [
-        ("kind", C.c_int32), ("prev_plan", vp), ("prev_ws", vp), ("resid", vp), ("ss_out", vp), ("ss_in", vp),
-        ("ss_tiles", C.c_int32), ("norm_dim", C.c_int32), ("eps", C.c_float), ("flags", vp), ("launches", vp),
-    ]
-
-
-YGG_PRO_NONE, YGG_PRO_RESID, YGG_PRO_SWIGLU = 0, 1, 2
-
-
 class YggGemvEpilogue(C.Structure):
     """ygg_gemv_epilogue (include/ygg.h)."""
 
@@ -161,7 +149,6 @@ _SIGS: dict[str, tuple] = {
     "ygg_gemm_plan_cluster": (C.c_int, [vp]),
     "ygg_gemm_plan_set_epi_prefetch": (C.c_int, [vp, vp, C.c_size_t]),
     "ygg_gemm_plan_set_layout": (C.c_int, [vp, C.c_int]),
-    "ygg_gemm_plan_set_prologue": (C.c_int, [vp, C.POINTER(YggPrologue)]),
     "ygg_gemm_plan_set_stages": (C.c_int, [vp, C.c_int]),
     "ygg_gemm_fused": (C.c_int, [vp, vp, C.POINTER(YggEpilogue), vp]),
     "ygg_gemm_tiles": (C.c_int, [vp]),
@@ -171,8 +158,6 @@ _SIGS: dict[str, tuple] = {
     "ygg_epi_swiglu": (C.c_int, [vp, vp, vp, C.c_int, vp]),
     "ygg_epi_qkv_rope": (C.c_int, [vp, vp, C.c_int, C.c_int, C.c_int, C.c_float, vp, vp, vp, vp, vp, C.c_int, C.c_int,
                                    vp, vp]),
-    "ygg_epi_qkv_rope_rstd": (C.c_int, [vp, vp, vp, C.c_int, C.c_int, C.c_float, C.c_int, C.c_int, C.c_int, C.c_float,
-                                        vp, vp, vp, vp, vp, C.c_int, C.c_int, vp, vp]),
     "ygg_embed": (C.c_int, [vp, C.c_int, C.c_int, C.c_int, vp, C.c_int, vp, vp]),
     "ygg_rmsnorm": (C.c_int, [vp, vp, C.c_int, C.c_int, C.c_int, C.c_float, vp, vp]),
     "ygg_embed_rmsnorm": (C.c_int, [vp, vp, C.c_int, C.c_int, C.c_int, vp, C.c_int, C.c_float, vp, vp, vp]),
@@ -224,7 +209,7 @@ EXPORTED = tuple(_SIGS)
 KERNELS_PER_CALL = {
     "ygg_topk_softmax": 2, "ygg_egt_grow_level": 1, "ygg_build_mask": 1, "ygg_knapsack_prune": 1,
     "ygg_tree_subtree": 1, "ygg_path_products": 1, "ygg_accept": 1, "ygg_kv_compact": 1, "ygg_gemm_run": 1, "ygg_gemm_fused": 1, "ygg_embed_fused": 1, "ygg_epi_store": 1,
-    "ygg_epi_residual_norm": 1, "ygg_epi_swiglu": 1, "ygg_epi_qkv_rope": 1, "ygg_epi_qkv_rope_rstd": 1, "ygg_embed": 1, "ygg_rmsnorm": 1, "ygg_embed_rmsnorm": 1,
+    "ygg_epi_residual_norm": 1, "ygg_epi_swiglu": 1, "ygg_epi_qkv_rope": 1, "ygg_embed": 1, "ygg_rmsnorm": 1, "ygg_embed_rmsnorm": 1,
     "ygg_attention": 1, "ygg_attention_tc": 2, "ygg_row_stats": 1, "ygg_pass0_inputs": 1, "ygg_init_roots": 1, "ygg_level_inputs": 1,
     "ygg_verify_inputs": 1, "ygg_commit": 1, "ygg_stamp": 1, "ygg_gemv_run": 1, "ygg_attn_dec_run": 1, "ygg_attn_tree_run": 1, "ygg_topk_merge": 1, "ygg_topk_merge_l2": 1,
 }

@@ -29,7 +29,7 @@ constexpr int kBK = 64;           // k per stage: 64 bf16 = one 128B swizzle row
 constexpr int kGemmThreads = 192; // 6 warps
 constexpr int kMaxRstdTokensHost = 1024;
 // alignment slack + barriers (<= 2*12+4 u64) + tmem slot/pending + red_s[64] + rstd_s[1024]
-constexpr int kSmemExtra = 1024 + 30 * 8 + 32 + 64 * 4 + kMaxRstdTokensHost * 4;
+constexpr int kSmemExtra = 1024 + 28 * 8 + 32 + 64 * 4 + kMaxRstdTokensHost * 4;
 
 struct GemmPlan {
   uint32_t magic;
@@ -50,18 +50,6 @@ struct GemmPlan {
   const char* epi_pf;  // L2 prefetch region of this plan's separate epilogue kernel (or nullptr)
   size_t epi_pf_bytes;
   int interleaved;     // W rows in the fused layout (RoPE pairs / gate-up pairs adjacent): separate epilogues
-  // prologue epilogue (ygg_gemm_plan_set_prologue): the previous GEMM's partials finished into X
-  int pro_kind;
-  int pro_pM, pro_pN, pro_pBN, pro_pm_tiles;
-  const int32_t* pro_pseg;
-  const float* pro_pws;
-  float* pro_resid;
-  float* pro_ss_out;
-  const float* pro_ss_in;
-  int pro_ss_tiles, pro_norm_dim;
-  float pro_eps;
-  int32_t* pro_flags;
-  int32_t* pro_launches;
   alignas(64) CUtensorMap tmap_w;
   alignas(64) CUtensorMap tmap_x;
 };
@@ -275,255 +263,12 @@ YGG_DEV void epi_apply(const EpiArgs& e, int M, int n, int m0, int valid16, floa
 }
 
 // ---------------------------------------------------------------------------
-// Epilogues.  value(m, n) = sum over segments of tile(n/128, m/BN) of ws[seg][m%BN][n%128].
-// ---------------------------------------------------------------------------
-struct EpiGeom {
-  int M, N, BN, m_tiles;
-  const int32_t* seg_first;
-  unsigned long long* trace;  // kernel-timeline slot (profiling only) or nullptr
-  const char* pf;             // L2 prefetch region (a later weight stream) or nullptr
-  size_t pf_bytes;
-  int il;                     // fused-layout rows (model.prepare_fused_): pairs are adjacent rows
-};
-
-// The epilogue kernels barely touch HBM (their partials are L2 hits): right after the dependency
-// wait, thread 0 of every CTA pulls its share of a later weight stream into L2 (bulk prefetch,
-// <= 64 KB per instruction, fire and forget), so the next GEMM starts that much of its stream from L2.
-YGG_DEV void epi_l2_prefetch(const EpiGeom& g) {
-  if (!g.pf || threadIdx.x != 0) return;
-  const size_t ncta = static_cast<size_t>(gridDim.x) * gridDim.y;
-  const size_t cta = static_cast<size_t>(blockIdx.y) * gridDim.x + blockIdx.x;
-  const size_t per = ((g.pf_bytes / ncta) + 255) & ~static_cast<size_t>(255);
-  const size_t b0 = cta * per, b1 = b0 + per < g.pf_bytes ? b0 + per : g.pf_bytes;
-  for (size_t o = b0; o < b1; o += 65536) {
-    const uint32_t n = static_cast<uint32_t>(b1 - o < 65536 ? ((b1 - o) & ~static_cast<size_t>(15)) : 65536);
-    if (n) asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(g.pf + o), "r"(n) : "memory");
-  }
-}
-
-YGG_DEV float epi_value(const EpiGeom& g, const float* __restrict__ ws, int m, int n) {
-  const int t = (n / kBM) * g.m_tiles + m / g.BN;
-  const int s0 = g.seg_first[t], s1 = g.seg_first[t + 1];
-  const size_t off = static_cast<size_t>(m % g.BN) * kBM + (n % kBM);
-  float v = 0.f;
-  for (int s = s0; s < s1; ++s) v += ws[static_cast<size_t>(s) * g.BN * kBM + off];
-  return v;
-}
-
-// Segment range [s0, s1) of the tile holding (row m, feature n): plan constants, so the epilogue
-// kernels load them before their grid-dependency wait.
-YGG_DEV int2 epi_segs(const EpiGeom& g, int m, int n) {
-  const int t = (n / kBM) * g.m_tiles + m / g.BN;
-  return make_int2(__ldg(g.seg_first + t), __ldg(g.seg_first + t + 1));
-}
-
-template <int V>
-YGG_DEV void epi_values(const EpiGeom& g, const float* __restrict__ ws, int m, int n, float* v, int2 sg);
-
-template <int V>
-YGG_DEV void epi_values(const EpiGeom& g, const float* __restrict__ ws, int m, int n, float* v) {
-  epi_values<V>(g, ws, m, n, v, epi_segs(g, m, n));
-}
-
-// Sum of the partials of V consecutive features [n, n+V) of row m (n % V == 0, one tile).
-template <int V>
-YGG_DEV void epi_values(const EpiGeom& g, const float* __restrict__ ws, int m, int n, float* v, int2 sg) {
-  const int s0 = sg.x, s1 = sg.y;
-  const float* p = ws + static_cast<size_t>(m % g.BN) * kBM + (n % kBM);
-  const size_t seg_stride = static_cast<size_t>(g.BN) * kBM;
-#pragma unroll
-  for (int i = 0; i < V; ++i) v[i] = 0.f;
-#pragma unroll 4
-  for (int s = s0; s < s1; ++s) {
-    const float4* q = reinterpret_cast<const float4*>(p + s * seg_stride);
-#pragma unroll
-    for (int i = 0; i < V / 4; ++i) {
-      const float4 x = __ldcg(q + i);
-      v[4 * i] += x.x;
-      v[4 * i + 1] += x.y;
-      v[4 * i + 2] += x.z;
-      v[4 * i + 3] += x.w;
-    }
-  }
-}
-
-// Partial sums of two V-wide feature runs [n1, n1+V) and [n2, n2+V) of row m (possibly different
-// tiles), both runs' loads in flight together; each run summed in its own segment order.
-template <int V>
-YGG_DEV void epi_values2(const EpiGeom& g, const float* __restrict__ ws, int m, int n1, int n2, float* v1, float* v2,
-                         int2 sa, int2 sb) {
-  const int a0 = sa.x, a1 = sa.y, b0 = sb.x, b1 = sb.y;
-  const size_t row = static_cast<size_t>(m % g.BN) * kBM;
-  const float* p1 = ws + row + (n1 % kBM);
-  const float* p2 = ws + row + (n2 % kBM);
-  const size_t seg_stride = static_cast<size_t>(g.BN) * kBM;
-#pragma unroll
-  for (int i = 0; i < V; ++i) v1[i] = v2[i] = 0.f;
-  const int na = a1 - a0, nb = b1 - b0, n = na > nb ? na : nb;
-  for (int j = 0; j < n; j += 4) {
-    float4 x[4][2][V / 4];
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const float4* q1 = reinterpret_cast<const float4*>(p1 + (a0 + j + k) * seg_stride);
-      const float4* q2 = reinterpret_cast<const float4*>(p2 + (b0 + j + k) * seg_stride);
-#pragma unroll
-      for (int i = 0; i < V / 4; ++i) {
-        x[k][0][i] = (j + k < na) ? __ldcg(q1 + i) : make_float4(0.f, 0.f, 0.f, 0.f);
-        x[k][1][i] = (j + k < nb) ? __ldcg(q2 + i) : make_float4(0.f, 0.f, 0.f, 0.f);
-      }
-    }
-#pragma unroll
-    for (int k = 0; k < 4; ++k)
-#pragma unroll
-      for (int i = 0; i < V / 4; ++i) {
-        v1[4 * i] += x[k][0][i].x; v1[4 * i + 1] += x[k][0][i].y; v1[4 * i + 2] += x[k][0][i].z; v1[4 * i + 3] += x[k][0][i].w;
-        v2[4 * i] += x[k][1][i].x; v2[4 * i + 1] += x[k][1][i].y; v2[4 * i + 2] += x[k][1][i].z; v2[4 * i + 3] += x[k][1][i].w;
-      }
-  }
-}
-
-template <typename T>
-YGG_DEV void store8(T* dst, const float* v);
-template <>
-YGG_DEV void store8<float>(float* dst, const float* v) {
-  reinterpret_cast<float4*>(dst)[0] = make_float4(v[0], v[1], v[2], v[3]);
-  reinterpret_cast<float4*>(dst)[1] = make_float4(v[4], v[5], v[6], v[7]);
-}
-template <>
-YGG_DEV void store8<__nv_bfloat16>(__nv_bfloat16* dst, const float* v) {
-  uint4 u;
-  __nv_bfloat162 a = __floats2bfloat162_rn(v[0], v[1]), b = __floats2bfloat162_rn(v[2], v[3]);
-  __nv_bfloat162 c = __floats2bfloat162_rn(v[4], v[5]), d = __floats2bfloat162_rn(v[6], v[7]);
-  u.x = *reinterpret_cast<uint32_t*>(&a);
-  u.y = *reinterpret_cast<uint32_t*>(&b);
-  u.z = *reinterpret_cast<uint32_t*>(&c);
-  u.w = *reinterpret_cast<uint32_t*>(&d);
-  *reinterpret_cast<uint4*>(dst) = u;
-}
-template <typename T>
-YGG_DEV void load8(const T* src, float* v);
-template <>
-YGG_DEV void load8<float>(const float* src, float* v) {
-  const float4 a = reinterpret_cast<const float4*>(src)[0], b = reinterpret_cast<const float4*>(src)[1];
-  v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
-}
-template <>
-YGG_DEV void load8<__nv_bfloat16>(const __nv_bfloat16* src, float* v) {
-  const uint4 u = *reinterpret_cast<const uint4*>(src);
-  const uint32_t w[4] = {u.x, u.y, u.z, u.w};
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const __nv_bfloat162 b = *reinterpret_cast<const __nv_bfloat162*>(&w[i]);
-    v[2 * i] = __bfloat162float(b.x);
-    v[2 * i + 1] = __bfloat162float(b.y);
-  }
-}
-
-// ---------------------------------------------------------------------------
-// Prologue epilogues ("prologue verify").  The previous GEMM leaves f32 partials; instead
-// of a separate epilogue kernel between the two GEMMs, this GEMM's four epilogue warps — idle until its
-// first accumulator is full — finish the previous GEMM's output into this GEMM's X while the weight ring
-// (issued before griddepcontrol.wait) fills:
-//   RESID : X = bf16(resid += prev) per 64-feature k-block, plus the block's per-token sums of squares
-//           (the RMSNorm is folded: gains in this GEMM's weights, rstd applied by the consumer);
-//   SWIGLU: X = bf16(silu(gate * r) * (up * r)), r = the gate|up input's rstd from its sums of squares.
-// The (k-block, token, 8-feature) items are spread over every CTA's epilogue warps (one or two rounds at
-// verify sizes); each CTA then adds one release arrival to the plan's counter, and a CTA's TMA producer
-// loads X only once the counter reached epoch * grid.  Epochs: every CTA counts its own launches
-// (launches[c]); all CTAs of a plan run every launch, so they agree on the epoch without a reset.
-// ---------------------------------------------------------------------------
-enum ProKind : int { kProNone = 0, kProResid = 1, kProSwiglu = 2 };
-
-struct ProArgs {
-  EpiGeom prev;        // the previous GEMM's partials: M, N, BN, m_tiles, seg_first
-  const float* pws;    // its f32 partials
-  float* resid;        // RESID: [M][K] f32 residual stream, updated in place
-  float* ss_out;       // RESID: [K/64][M] per-k-block sums of squares of the new residual
-  const float* ss_in;  // SWIGLU: [ss_tiles][M] sums of squares of the gate|up GEMM's input
-  int ss_tiles, norm_dim;
-  float eps;
-  __nv_bfloat16* x;    // this GEMM's X [M][K]
-  int K;
-  int32_t* flags;      // [0]: arrival counter, one per CTA per launch (epoch * grid once X is complete)
-  int32_t* launches;   // [grid] per-CTA launch counters
-};
-
-YGG_DEV void st_release_s32(int32_t* p, int v) {
-  asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-YGG_DEV void fence_proxy_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
-
-template <int PRO>
-YGG_DEV void run_prologue(const ProArgs& q, int M, int c, int G, int epoch, float* rstd_s) {
-  const int et = static_cast<int>(threadIdx.x) - 64;  // 0..127: the four epilogue warps
-  const int lane = et & 31;
-  const size_t K = static_cast<size_t>(q.K);
-  if constexpr (PRO == kProSwiglu) {
-    for (int m = et; m < M; m += 128) {
-      float s = 0.f;
-#pragma unroll 16
-      for (int t = 0; t < q.ss_tiles; ++t) s += __ldcg(q.ss_in + static_cast<size_t>(t) * M + m);
-      rstd_s[m] = rsqrtf(s / static_cast<float>(q.norm_dim) + q.eps);
-    }
-    epi_bar();
-  }
-  // Items (k-block j, token m, 8-feature run f8), i = (j * M + m) * 8 + f8, spread over every CTA's
-  // 128 epilogue threads (the whole grid works on each round; a token's 8 runs of a k-block sit in 8
-  // consecutive lanes, so its sum of squares is a fixed-order xor tree — deterministic).
-  const int items = M * (q.K / 8);
-  const int stride = G * 128;
-  const int rounds = (items + stride - 1) / stride;  // uniform over the grid: every lane runs every round
-  for (int r = 0; r < rounds; ++r) {
-    const int i = r * stride + c * 128 + et;
-    const bool ok = i < items;
-    const int jm = ok ? i >> 3 : 0;
-    const int j = jm / M, m = jm - j * M;
-    const int k = j * 64 + (i & 7) * 8;
-    if constexpr (PRO == kProResid) {
-      float h[8], v[8];
-      if (ok) {
-        float* rp = q.resid + static_cast<size_t>(m) * K + k;
-        load8<float>(rp, h);
-        epi_values<8>(q.prev, q.pws, m, k, v);
-#pragma unroll
-        for (int t = 0; t < 8; ++t) h[t] += v[t];
-        store8<float>(rp, h);
-        store8<__nv_bfloat16>(q.x + static_cast<size_t>(m) * K + k, h);
-      }
-      float ss = 0.f;
-#pragma unroll
-      for (int t = 0; t < 8; ++t) ss += ok ? h[t] * h[t] : 0.f;
-      ss += __shfl_xor_sync(0xffffffffu, ss, 1);
-      ss += __shfl_xor_sync(0xffffffffu, ss, 2);
-      ss += __shfl_xor_sync(0xffffffffu, ss, 4);
-      if (ok && (lane & 7) == 0) q.ss_out[static_cast<size_t>(j) * M + m] = ss;
-    } else if (ok) {
-      float g[8], u[8], v[8];
-      epi_values2<8>(q.prev, q.pws, m, k, q.K + k, g, u, epi_segs(q.prev, m, k), epi_segs(q.prev, m, q.K + k));
-      const float rs = rstd_s[m];
-#pragma unroll
-      for (int t = 0; t < 8; ++t) {
-        const float gg = g[t] * rs;
-        v[t] = gg / (1.f + expf(-gg)) * (u[t] * rs);
-      }
-      store8<__nv_bfloat16>(q.x + static_cast<size_t>(m) * K + k, v);
-    }
-  }
-  fence_proxy_async_global();  // this thread's generic stores, before the async-proxy (TMA) readers
-  epi_bar();
-  if (et == 0) {  // one release arrival per CTA on the plan's counter (epoch * grid when all are in)
-    __threadfence();
-    asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(q.flags) : "memory");
-  }
-}
-
-// ---------------------------------------------------------------------------
 // tcgen05 kernel
 // ---------------------------------------------------------------------------
-template <int KIND, int PRO = kProNone>
+template <int KIND>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     gemm_bf16_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant__ CUtensorMap tmap_x,
-                        GemmParams p, float* __restrict__ ws, EpiArgs e, ProArgs pro) {
+                        GemmParams p, float* __restrict__ ws, EpiArgs e) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   // 1024-align the dynamic smem base (SW128 atoms).
   unsigned char* base = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -536,8 +281,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   uint64_t* empty = full + S;
   uint64_t* tfull = empty + S;   // [2]
   uint64_t* tempty = tfull + 2;  // [2]
-  uint64_t* xbar = tempty + 2;   // prologue plans: every k-block of X is published (epilogue warps -> producer)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(xbar + 1);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
   int* pend_tile = reinterpret_cast<int*>(tmem_slot + 1);  // [2] split tiles awaiting their fixup
   int* pend_j = pend_tile + 2;                               // [2] participant index in the tile
   int* pend_tgt = pend_j + 2;                                // [2] epoch-counter target
@@ -550,15 +294,12 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   // stream-K units of the remaining tiles, which start at tile t_dp.
   const long long sk_base = static_cast<long long>(p.dp_per_cta) * p.num_ctas * p.kb;
   const long long u0 = sk_base + p.units * c / p.num_ctas, u1 = sk_base + p.units * (c + 1) / p.num_ctas;
-  // prologue epoch of this launch (only this CTA ever writes launches[c]: at its end)
-  const int epoch = PRO != kProNone ? __ldcg(pro.launches + c) + 1 : 0;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmap_w);
     tma_prefetch_desc(&tmap_x);
     for (int s = 0; s < S; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
     for (int a = 0; a < 2; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], 128); }
-    mbar_init(xbar, 128);
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc(tmem_slot, p.tmem_cols);
@@ -622,12 +363,6 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       }
       pdl_wait();
       trace_min(e.trace, 1);
-      if constexpr (PRO != kProNone) {
-        // X is written by the grid's prologues (generic stores): once this CTA's epilogue warps have
-        // acquired every k-block's flag, order those writes before this thread's async-proxy (TMA) reads.
-        mbar_wait(xbar, 0);
-        fence_proxy_async_global();
-      }
       for (int i = 0; i < pre; ++i)
         tma_load_2d(sb + static_cast<size_t>(i) * b_bytes, &tmap_x, &full[i], pre_kblk[i] * kBK, pre_xrow[i], pol_x);
       int stage = pre % S;
@@ -688,22 +423,6 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     const int quarter = warp & 3;  // TMEM lanes accessible by this warp
     const int row = quarter * 32 + lane;
     const int et = threadIdx.x - 64;  // 0..127
-    if constexpr (PRO != kProNone) {
-      run_prologue<PRO>(pro, p.M, c, p.num_ctas, epoch, rstd_s);
-      if (et == 0 && KIND == kEpiNone) trace_max(e.trace, 5);  // this CTA's prologue share done
-      // all of X (and the sums of squares the LM head's rstd reads) published by every CTA: then the
-      // producer's X loads may start
-      if (et == 0) {
-        const long long t0 = clock64();
-        while (ld_acquire(pro.flags) < epoch * p.num_ctas) {
-          __nanosleep(20);
-          if (clock64() - t0 > (1ll << 34)) __trap();
-        }
-      }
-      epi_bar();
-      if (et == 0 && KIND == kEpiNone) trace_max(e.trace, 6);  // every CTA's share published
-      mbar_arrive(xbar);
-    }
     if (KIND != kEpiNone && e.ss_in) {
       for (int m = et; m < p.M; m += 128) {
         float s = 0.f;
@@ -821,7 +540,6 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   }
   __syncthreads();
   if (threadIdx.x == 0) trace_max(e.trace, 2);
-  if (PRO != kProNone && threadIdx.x == 0) pro.launches[c] = epoch;
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc(tmem_base, p.tmem_cols);
@@ -1079,6 +797,151 @@ __global__ void __launch_bounds__(256) gemm_f32_simt_kernel(const float* __restr
   }
 }
 
+// ---------------------------------------------------------------------------
+// Epilogues.  value(m, n) = sum over segments of tile(n/128, m/BN) of ws[seg][m%BN][n%128].
+// ---------------------------------------------------------------------------
+struct EpiGeom {
+  int M, N, BN, m_tiles;
+  const int32_t* seg_first;
+  unsigned long long* trace;  // kernel-timeline slot (profiling only) or nullptr
+  const char* pf;             // L2 prefetch region (a later weight stream) or nullptr
+  size_t pf_bytes;
+  int il;                     // fused-layout rows (model.prepare_fused_): pairs are adjacent rows
+};
+
+// The epilogue kernels barely touch HBM (their partials are L2 hits): right after the dependency
+// wait, thread 0 of every CTA pulls its share of a later weight stream into L2 (bulk prefetch,
+// <= 64 KB per instruction, fire and forget), so the next GEMM starts that much of its stream from L2.
+YGG_DEV void epi_l2_prefetch(const EpiGeom& g) {
+  if (!g.pf || threadIdx.x != 0) return;
+  const size_t ncta = static_cast<size_t>(gridDim.x) * gridDim.y;
+  const size_t cta = static_cast<size_t>(blockIdx.y) * gridDim.x + blockIdx.x;
+  const size_t per = ((g.pf_bytes / ncta) + 255) & ~static_cast<size_t>(255);
+  const size_t b0 = cta * per, b1 = b0 + per < g.pf_bytes ? b0 + per : g.pf_bytes;
+  for (size_t o = b0; o < b1; o += 65536) {
+    const uint32_t n = static_cast<uint32_t>(b1 - o < 65536 ? ((b1 - o) & ~static_cast<size_t>(15)) : 65536);
+    if (n) asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(g.pf + o), "r"(n) : "memory");
+  }
+}
+
+YGG_DEV float epi_value(const EpiGeom& g, const float* __restrict__ ws, int m, int n) {
+  const int t = (n / kBM) * g.m_tiles + m / g.BN;
+  const int s0 = g.seg_first[t], s1 = g.seg_first[t + 1];
+  const size_t off = static_cast<size_t>(m % g.BN) * kBM + (n % kBM);
+  float v = 0.f;
+  for (int s = s0; s < s1; ++s) v += ws[static_cast<size_t>(s) * g.BN * kBM + off];
+  return v;
+}
+
+// Segment range [s0, s1) of the tile holding (row m, feature n): plan constants, so the epilogue
+// kernels load them before their grid-dependency wait.
+YGG_DEV int2 epi_segs(const EpiGeom& g, int m, int n) {
+  const int t = (n / kBM) * g.m_tiles + m / g.BN;
+  return make_int2(__ldg(g.seg_first + t), __ldg(g.seg_first + t + 1));
+}
+
+template <int V>
+YGG_DEV void epi_values(const EpiGeom& g, const float* __restrict__ ws, int m, int n, float* v, int2 sg);
+
+template <int V>
+YGG_DEV void epi_values(const EpiGeom& g, const float* __restrict__ ws, int m, int n, float* v) {
+  epi_values<V>(g, ws, m, n, v, epi_segs(g, m, n));
+}
+
+// Sum of the partials of V consecutive features [n, n+V) of row m (n % V == 0, one tile).
+template <int V>
+YGG_DEV void epi_values(const EpiGeom& g, const float* __restrict__ ws, int m, int n, float* v, int2 sg) {
+  const int s0 = sg.x, s1 = sg.y;
+  const float* p = ws + static_cast<size_t>(m % g.BN) * kBM + (n % kBM);
+  const size_t seg_stride = static_cast<size_t>(g.BN) * kBM;
+#pragma unroll
+  for (int i = 0; i < V; ++i) v[i] = 0.f;
+#pragma unroll 4
+  for (int s = s0; s < s1; ++s) {
+    const float4* q = reinterpret_cast<const float4*>(p + s * seg_stride);
+#pragma unroll
+    for (int i = 0; i < V / 4; ++i) {
+      const float4 x = __ldcg(q + i);
+      v[4 * i] += x.x;
+      v[4 * i + 1] += x.y;
+      v[4 * i + 2] += x.z;
+      v[4 * i + 3] += x.w;
+    }
+  }
+}
+
+// Partial sums of two V-wide feature runs [n1, n1+V) and [n2, n2+V) of row m (possibly different
+// tiles), both runs' loads in flight together; each run summed in its own segment order.
+template <int V>
+YGG_DEV void epi_values2(const EpiGeom& g, const float* __restrict__ ws, int m, int n1, int n2, float* v1, float* v2,
+                         int2 sa, int2 sb) {
+  const int a0 = sa.x, a1 = sa.y, b0 = sb.x, b1 = sb.y;
+  const size_t row = static_cast<size_t>(m % g.BN) * kBM;
+  const float* p1 = ws + row + (n1 % kBM);
+  const float* p2 = ws + row + (n2 % kBM);
+  const size_t seg_stride = static_cast<size_t>(g.BN) * kBM;
+#pragma unroll
+  for (int i = 0; i < V; ++i) v1[i] = v2[i] = 0.f;
+  const int na = a1 - a0, nb = b1 - b0, n = na > nb ? na : nb;
+  for (int j = 0; j < n; j += 4) {
+    float4 x[4][2][V / 4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const float4* q1 = reinterpret_cast<const float4*>(p1 + (a0 + j + k) * seg_stride);
+      const float4* q2 = reinterpret_cast<const float4*>(p2 + (b0 + j + k) * seg_stride);
+#pragma unroll
+      for (int i = 0; i < V / 4; ++i) {
+        x[k][0][i] = (j + k < na) ? __ldcg(q1 + i) : make_float4(0.f, 0.f, 0.f, 0.f);
+        x[k][1][i] = (j + k < nb) ? __ldcg(q2 + i) : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+#pragma unroll
+      for (int i = 0; i < V / 4; ++i) {
+        v1[4 * i] += x[k][0][i].x; v1[4 * i + 1] += x[k][0][i].y; v1[4 * i + 2] += x[k][0][i].z; v1[4 * i + 3] += x[k][0][i].w;
+        v2[4 * i] += x[k][1][i].x; v2[4 * i + 1] += x[k][1][i].y; v2[4 * i + 2] += x[k][1][i].z; v2[4 * i + 3] += x[k][1][i].w;
+      }
+  }
+}
+
+template <typename T>
+YGG_DEV void store8(T* dst, const float* v);
+template <>
+YGG_DEV void store8<float>(float* dst, const float* v) {
+  reinterpret_cast<float4*>(dst)[0] = make_float4(v[0], v[1], v[2], v[3]);
+  reinterpret_cast<float4*>(dst)[1] = make_float4(v[4], v[5], v[6], v[7]);
+}
+template <>
+YGG_DEV void store8<__nv_bfloat16>(__nv_bfloat16* dst, const float* v) {
+  uint4 u;
+  __nv_bfloat162 a = __floats2bfloat162_rn(v[0], v[1]), b = __floats2bfloat162_rn(v[2], v[3]);
+  __nv_bfloat162 c = __floats2bfloat162_rn(v[4], v[5]), d = __floats2bfloat162_rn(v[6], v[7]);
+  u.x = *reinterpret_cast<uint32_t*>(&a);
+  u.y = *reinterpret_cast<uint32_t*>(&b);
+  u.z = *reinterpret_cast<uint32_t*>(&c);
+  u.w = *reinterpret_cast<uint32_t*>(&d);
+  *reinterpret_cast<uint4*>(dst) = u;
+}
+template <typename T>
+YGG_DEV void load8(const T* src, float* v);
+template <>
+YGG_DEV void load8<float>(const float* src, float* v) {
+  const float4 a = reinterpret_cast<const float4*>(src)[0], b = reinterpret_cast<const float4*>(src)[1];
+  v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+}
+template <>
+YGG_DEV void load8<__nv_bfloat16>(const __nv_bfloat16* src, float* v) {
+  const uint4 u = *reinterpret_cast<const uint4*>(src);
+  const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const __nv_bfloat162 b = *reinterpret_cast<const __nv_bfloat162*>(&w[i]);
+    v[2 * i] = __bfloat162float(b.x);
+    v[2 * i + 1] = __bfloat162float(b.y);
+  }
+}
+
 constexpr int kEpiThreads = 128;  // x 8 features = 1024 features per CTA
 
 template <typename OutT>
@@ -1225,37 +1088,6 @@ __global__ void __launch_bounds__(256) argmax_reduce_kernel(const unsigned long 
   }
 }
 
-// Folded-RMSNorm input of the QKV epilogue kernel (prologue verify): the QKV GEMM ran on the
-// unnormalised bf16 residual with the attention-norm gains folded into its weights, so the per-token
-// rstd is applied here from the producer's per-block sums of squares [tiles][M].  In two halves so its
-// L2 round trip overlaps the partial-sum loads: rstd_part (warp 0's lanes load tiles lane, lane + 32,
-// ...) before them, rstd_block (fixed-order xor reduction in warp 0, a shared-memory broadcast; every
-// thread of the block calls it) after.
-struct RstdIn {
-  const float* ss;  // nullptr: no rstd (plain epilogue)
-  int tiles;
-  int dim;
-  float eps;
-};
-
-YGG_DEV float rstd_part(const RstdIn& r, int M, int m) {
-  float s = 0.f;
-  if (threadIdx.x < 32)
-    for (int t = static_cast<int>(threadIdx.x); t < r.tiles; t += 32) s += __ldcg(r.ss + static_cast<size_t>(t) * M + m);
-  return s;
-}
-
-YGG_DEV float rstd_block(float part, const RstdIn& r) {
-  __shared__ float rs_s;
-  if (threadIdx.x < 32) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
-    if (threadIdx.x == 0) rs_s = rsqrtf(part / static_cast<float>(r.dim) + r.eps);
-  }
-  __syncthreads();
-  return rs_s;
-}
-
 // QKV epilogue: RoPE (rotate-half convention) on q and k at pos[m]; q -> q_out, k/v -> KV cache.
 // Work item = 4 rotation pairs (i..i+3, i+half..i+half+3) of one head; one item per thread.
 // cos/sin come from the host table rope_cs [positions][hd/2] when given (else sincosf).
@@ -1265,7 +1097,7 @@ __global__ void __launch_bounds__(256) epi_qkv_rope_kernel(EpiGeom g, const floa
                                                            const int32_t* __restrict__ slot,
                                                            const int32_t* __restrict__ req, ActT* __restrict__ q_out,
                                                            ActT* __restrict__ cache, int S,
-                                                           const float2* __restrict__ rope_cs, RstdIn rn) {
+                                                           const float2* __restrict__ rope_cs) {
   if (threadIdx.x == 0) trace_min(g.trace, 0);
   const int m = blockIdx.x;
   const int half = hd / 2;
@@ -1282,12 +1114,11 @@ __global__ void __launch_bounds__(256) epi_qkv_rope_kernel(EpiGeom g, const floa
   pdl_launch_dependents();
   epi_l2_prefetch(g);
   if (threadIdx.x == 0) trace_min(g.trace, 1);
-  const float ssp = rn.ss ? rstd_part(rn, g.M, m) : 0.f;
-  const bool live = it < items;
+  if (it >= items) return;
   const int pm = pos[m];
   float x1[4], x2[4], cs[4], sn[4];
   const bool rot = head < Hq + Hkv;
-  if (live && rot && rope_cs) {  // table loads first: they overlap the partial-sum loads below
+  if (rot && rope_cs) {  // table loads first: they overlap the partial-sum loads below
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       const float2 t = __ldg(rope_cs + static_cast<size_t>(pm) * half + i0 + j);
@@ -1295,7 +1126,7 @@ __global__ void __launch_bounds__(256) epi_qkv_rope_kernel(EpiGeom g, const floa
       sn[j] = t.y;
     }
   }
-  if (live && g.il) {
+  if (g.il) {
     float v[8];
     epi_values<8>(g, ws, m, n0 + 2 * i0, v, sa);
 #pragma unroll
@@ -1303,18 +1134,9 @@ __global__ void __launch_bounds__(256) epi_qkv_rope_kernel(EpiGeom g, const floa
       x1[j] = v[2 * j];
       x2[j] = v[2 * j + 1];
     }
-  } else if (live) {
+  } else {
     epi_values2<4>(g, ws, m, n0 + i0, n0 + i0 + half, x1, x2, sa, sb);
   }
-  if (rn.ss) {
-    const float rs = rstd_block(ssp, rn);  // every thread of the block takes part
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      x1[j] *= rs;
-      x2[j] *= rs;
-    }
-  }
-  if (!live) return;
   if (rot) {
     if (rope_cs) {
     } else {
@@ -1428,9 +1250,7 @@ extern "C" {
 int ygg_prepare_gemm(void) {
   cudaError_t e = cudaSuccess;
   for (auto fn : {gemm_bf16_tc_kernel<kEpiNone>, gemm_bf16_tc_kernel<kEpiStoreF32>, gemm_bf16_tc_kernel<kEpiQkvRope>,
-                  gemm_bf16_tc_kernel<kEpiSwiglu>, gemm_bf16_tc_kernel<kEpiResid>, gemm_bf16_tc_kernel<kEpiArgmax>,
-                  gemm_bf16_tc_kernel<kEpiNone, kProResid>, gemm_bf16_tc_kernel<kEpiNone, kProSwiglu>,
-                  gemm_bf16_tc_kernel<kEpiStoreF32, kProResid>, gemm_bf16_tc_kernel<kEpiArgmax, kProResid>}) {
+                  gemm_bf16_tc_kernel<kEpiSwiglu>, gemm_bf16_tc_kernel<kEpiResid>, gemm_bf16_tc_kernel<kEpiArgmax>}) {
     e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     if (e != cudaSuccess) return ygg_fail(YGG_ERR_CUDA, "gemm attribute: %s", cudaGetErrorString(e));
   }
@@ -1623,58 +1443,30 @@ static int gemm_launch(const GemmPlan* g, float* workspace, const ygg_epilogue* 
         default: return ygg_fail(YGG_ERR_VALUE, "unknown epilogue kind %d", kind);
       }
     }
-    ProArgs pa;
-    std::memset(&pa, 0, sizeof(pa));
-    if (g->pro_kind != kProNone) {
-      YGG_CHECK_ARG(workspace != g->pro_pws, "a prologue GEMM must not write the partials it reads");
-      pa.prev = EpiGeom{g->pro_pM, g->pro_pN, g->pro_pBN, g->pro_pm_tiles, g->pro_pseg, nullptr, nullptr, 0, 0};
-      pa.pws = g->pro_pws;
-      pa.resid = g->pro_resid;
-      pa.ss_out = g->pro_ss_out;
-      pa.ss_in = g->pro_ss_in;
-      pa.ss_tiles = g->pro_ss_tiles;
-      pa.norm_dim = g->pro_norm_dim;
-      pa.eps = g->pro_eps;
-      pa.x = static_cast<__nv_bfloat16*>(const_cast<void*>(g->X));
-      pa.K = g->K;
-      pa.flags = g->pro_flags;
-      pa.launches = g->pro_launches;
-      const int pk = g->pro_kind;
-#define YGG_PRO_LAUNCH(KD, PK)                                                                                  \
-  YGG_LAUNCH_PDL((gemm_bf16_tc_kernel<KD, PK>), dim3(g->num_ctas), dim3(kGemmThreads), smem, s, g->tmap_w, g->tmap_x, \
-                 p, workspace, e, pa)
-      if (kind == kEpiNone && pk == kProResid) YGG_PRO_LAUNCH(kEpiNone, kProResid);
-      else if (kind == kEpiNone && pk == kProSwiglu) YGG_PRO_LAUNCH(kEpiNone, kProSwiglu);
-      else if (kind == kEpiStoreF32 && pk == kProResid) YGG_PRO_LAUNCH(kEpiStoreF32, kProResid);
-      else if (kind == kEpiArgmax && pk == kProResid) YGG_PRO_LAUNCH(kEpiArgmax, kProResid);
-      else return ygg_fail(YGG_ERR_UNSUPPORTED, "prologue %d with epilogue %d", pk, kind);
-#undef YGG_PRO_LAUNCH
-      return YGG_OK;
-    }
     switch (kind) {
       case kEpiNone:
         YGG_LAUNCH_PDL(gemm_bf16_tc_kernel<kEpiNone>, dim3(g->num_ctas), dim3(kGemmThreads), smem, s, g->tmap_w,
-                       g->tmap_x, p, workspace, e, pa);
+                       g->tmap_x, p, workspace, e);
         break;
       case kEpiStoreF32:
         YGG_LAUNCH_PDL(gemm_bf16_tc_kernel<kEpiStoreF32>, dim3(g->num_ctas), dim3(kGemmThreads), smem, s, g->tmap_w,
-                       g->tmap_x, p, workspace, e, pa);
+                       g->tmap_x, p, workspace, e);
         break;
       case kEpiQkvRope:
         YGG_LAUNCH_PDL(gemm_bf16_tc_kernel<kEpiQkvRope>, dim3(g->num_ctas), dim3(kGemmThreads), smem, s, g->tmap_w,
-                       g->tmap_x, p, workspace, e, pa);
+                       g->tmap_x, p, workspace, e);
         break;
       case kEpiSwiglu:
         YGG_LAUNCH_PDL(gemm_bf16_tc_kernel<kEpiSwiglu>, dim3(g->num_ctas), dim3(kGemmThreads), smem, s, g->tmap_w,
-                       g->tmap_x, p, workspace, e, pa);
+                       g->tmap_x, p, workspace, e);
         break;
       case kEpiResid:
         YGG_LAUNCH_PDL(gemm_bf16_tc_kernel<kEpiResid>, dim3(g->num_ctas), dim3(kGemmThreads), smem, s, g->tmap_w,
-                       g->tmap_x, p, workspace, e, pa);
+                       g->tmap_x, p, workspace, e);
         break;
       case kEpiArgmax:
         YGG_LAUNCH_PDL(gemm_bf16_tc_kernel<kEpiArgmax>, dim3(g->num_ctas), dim3(kGemmThreads), smem, s, g->tmap_w,
-                       g->tmap_x, p, workspace, e, pa);
+                       g->tmap_x, p, workspace, e);
         break;
       default:
         return ygg_fail(YGG_ERR_VALUE, "unknown epilogue kind %d", kind);
@@ -1729,43 +1521,6 @@ int ygg_gemm_plan_set_cluster(void* plan, int cluster) {
     return ygg_fail(YGG_ERR_UNSUPPORTED, "%d tiles need %d co-resident clusters of %d; only %d fit", g->tiles,
                     g->tiles, cluster, max_clusters);
   g->cluster = cluster;
-  return YGG_OK;
-}
-
-int ygg_gemm_plan_set_prologue(void* plan, const ygg_prologue* pro) {
-  GemmPlan* g = const_cast<GemmPlan*>(plan_of(plan));
-  YGG_CHECK_ARG(g != nullptr && g->dtype == YGG_BF16 && g->cluster == 0, "invalid bf16 stream-K GEMM plan");
-  if (!pro || pro->kind == kProNone) {
-    g->pro_kind = kProNone;
-    return YGG_OK;
-  }
-  const GemmPlan* pv = plan_of(pro->prev_plan);
-  YGG_CHECK_ARG(pv != nullptr && pv->dtype == YGG_BF16 && pv->cluster == 0, "prologue needs the previous stream-K plan");
-  YGG_CHECK_ARG(pro->kind == kProResid || pro->kind == kProSwiglu, "unknown prologue kind");
-  YGG_CHECK_ARG(pv->M == g->M, "previous GEMM has another row count");
-  YGG_CHECK_ARG(g->K % 64 == 0 && g->K / 64 <= 512, "prologue k-blocks: K must be a multiple of 64, <= 32768");
-  YGG_CHECK_ARG(pro->prev_ws && pro->flags && pro->launches, "prologue needs prev_ws / flags / launches");
-  if (pro->kind == kProResid) {
-    YGG_CHECK_ARG(pv->N == g->K && pro->resid && pro->ss_out, "RESID prologue: previous N == K, resid, ss_out");
-  } else {
-    YGG_CHECK_ARG(pv->N == 2 * g->K && pro->ss_in && pro->ss_tiles >= 1 && pro->norm_dim >= 1 && g->M <= kMaxRstdTokens,
-                  "SWIGLU prologue: previous N == 2K, ss_in / ss_tiles / norm_dim");
-  }
-  g->pro_kind = pro->kind;
-  g->pro_pM = pv->M;
-  g->pro_pN = pv->N;
-  g->pro_pBN = pv->BN;
-  g->pro_pm_tiles = pv->m_tiles;
-  g->pro_pseg = pv->seg_table;
-  g->pro_pws = pro->prev_ws;
-  g->pro_resid = pro->resid;
-  g->pro_ss_out = pro->ss_out;
-  g->pro_ss_in = pro->ss_in;
-  g->pro_ss_tiles = pro->ss_tiles;
-  g->pro_norm_dim = pro->norm_dim;
-  g->pro_eps = pro->eps;
-  g->pro_flags = pro->flags;
-  g->pro_launches = pro->launches;
   return YGG_OK;
 }
 
@@ -1871,18 +1626,8 @@ int ygg_epi_swiglu(const void* plan, const float* ws, void* out, int act_dtype, 
 int ygg_epi_qkv_rope(const void* plan, const float* ws, int Hq, int Hkv, int hd, float rope_theta, const int32_t* pos,
                      const int32_t* slot, const int32_t* req, void* q_out, void* cache, int S, int act_dtype,
                      const float* rope_cs, ygg_stream_t stream) {
-  return ygg_epi_qkv_rope_rstd(plan, ws, nullptr, 0, 0, 0.f, Hq, Hkv, hd, rope_theta, pos, slot, req, q_out, cache, S,
-                               act_dtype, rope_cs, stream);
-}
-
-int ygg_epi_qkv_rope_rstd(const void* plan, const float* ws, const float* ss_in, int ss_tiles, int norm_dim, float eps,
-                          int Hq, int Hkv, int hd, float rope_theta, const int32_t* pos, const int32_t* slot,
-                          const int32_t* req, void* q_out, void* cache, int S, int act_dtype, const float* rope_cs,
-                          ygg_stream_t stream) {
   const GemmPlan* g = plan_of(plan);
   YGG_CHECK_ARG(g && ws && pos && slot && req && q_out && cache, "invalid arguments");
-  YGG_CHECK_ARG(!ss_in || (ss_tiles >= 1 && norm_dim >= 1 && eps >= 0.f), "bad folded-RMSNorm arguments");
-  const RstdIn rn{ss_in, ss_tiles, norm_dim, eps};
   YGG_CHECK_ARG(g->N == (Hq + 2 * Hkv) * hd, "QKV width mismatch");
   YGG_CHECK_ARG(hd % 8 == 0 && hd <= 256, "bad head dim");
   EpiGeom geo = geom_of(g, 7);
@@ -1893,10 +1638,10 @@ int ygg_epi_qkv_rope_rstd(const void* plan, const float* ws, const float* ss_in,
   const float2* rt = reinterpret_cast<const float2*>(rope_cs);
   if (act_dtype == YGG_F32)
     YGG_LAUNCH_PDL(epi_qkv_rope_kernel<float>, grid, dim3(256), 0, s, geo, ws, Hq, Hkv, hd, l2t, pos, slot, req,
-                   static_cast<float*>(q_out), static_cast<float*>(cache), S, rt, rn);
+                   static_cast<float*>(q_out), static_cast<float*>(cache), S, rt);
   else
     YGG_LAUNCH_PDL(epi_qkv_rope_kernel<__nv_bfloat16>, grid, dim3(256), 0, s, geo, ws, Hq, Hkv, hd, l2t, pos, slot, req,
-                   static_cast<__nv_bfloat16*>(q_out), static_cast<__nv_bfloat16*>(cache), S, rt, rn);
+                   static_cast<__nv_bfloat16*>(q_out), static_cast<__nv_bfloat16*>(cache), S, rt);
   return YGG_OK;
 }
 

@@ -32,7 +32,7 @@ import math
 import torch
 
 from . import _lib as L
-from .model import ModelConfig, prepare_folded_, prepare_fused_, rope_table
+from .model import ModelConfig, prepare_fused_, rope_table
 from .plan import DEFAULT, ForwardPlan
 
 
@@ -130,11 +130,6 @@ class Forward:
         # per-kernel epilogues with the layout flag (ygg_gemm_plan_set_layout) unless the plan asks for the
         # fused-epilogue GEMMs (measured slower at M = 512: DESIGN.md §4).
         self.fused = self.layout_fused and (self.gemv or plan.fused_epilogues or plan.fused_layout_gemm)
-        # prologue verify: tree / AR passes on standard-layout weights (module docstring)
-        self.pro = (bf16 and not self.fused and not self.layout_fused and plan.prologue and mask_words > 0
-                    and logits and cfg.d_model % 128 == 0)
-        if self.pro:
-            prepare_folded_(weights, cfg)
         self.w = weights
         dev = cache.device
         M, d = self.M, cfg.d_model
@@ -176,9 +171,6 @@ class Forward:
         if self.lm_plan:
             ws = max(ws, self.lm_plan.ws_bytes)
         self.ws = torch.empty(max(ws // 4, 1), dtype=torch.float32, device=dev)
-        # prologue path: GEMMs alternate between two partial workspaces (a GEMM's prologue reads the
-        # previous GEMM's partials while its own MMA writes the other buffer)
-        self.ws2 = torch.empty(max(ws // 4, 1), dtype=torch.float32, device=dev) if self.pro else None
         self.attn_plans = None
         if act_dtype == torch.bfloat16 and mask_words <= L.MAX_MASK_WORDS:
             es = cache.element_size()
@@ -242,10 +234,6 @@ class Forward:
             e.out = self.lm_keys.data_ptr() if self.lm_argmax else self.logits.data_ptr()
             e.ld = cfg.vocab
             self.lm_epi = e
-        if self.pro and self.lm_epi is None and self.lm_plan is not None:
-            raise ValueError("the prologue path needs the fused LM-head epilogue (plan.lm_store_fused)")
-        if self.pro:
-            self._setup_prologue()
         if self.fused:
             self._setup_fused()
         elif self.layout_fused:
@@ -259,46 +247,6 @@ class Forward:
             self._setup_epi_l2_prefetch()
 
     # ------------------------------------------------------------------
-    def _setup_prologue(self) -> None:
-        """Prologue verify (plan.prologue): O's residual + sums of squares run in gate|up's prologue,
-        SwiGLU (with the rstd) in down's, down's residual in the next QKV's (or the LM head's); the QKV
-        epilogue kernel applies the folded attention norm's rstd, the LM head's fused epilogue the final
-        one.  GEMMs write partials alternately to ws (QKV, gate|up) and ws2 (O, down)."""
-        lib, cfg, M, d = L.lib(), self.cfg, self.M, self.cfg.d_model
-        dev = self.cache.device
-        eps = float(cfg.norm_eps)
-        self.ss_e = torch.zeros(d // 128, M, dtype=torch.float32, device=dev)  # embed (first norm)
-        self.ss_a = torch.zeros(d // 64, M, dtype=torch.float32, device=dev)   # residual before attention / LM
-        self.ss_b = torch.zeros(d // 64, M, dtype=torch.float32, device=dev)   # residual before the MLP
-        chain = []  # (plan, kind, previous plan, previous workspace, resid/ss_out or ss_in)
-        prev_down = None
-        for p in self.plans:
-            if prev_down is not None:
-                chain.append((p["qkv"], L.YGG_PRO_RESID, prev_down, self.ws2, self.ss_a))
-            chain.append((p["gu"], L.YGG_PRO_RESID, p["o"], self.ws2, self.ss_b))
-            chain.append((p["down"], L.YGG_PRO_SWIGLU, p["gu"], self.ws, self.ss_b))
-            prev_down = p["down"]
-        if self.lm_plan is not None and prev_down is not None:
-            chain.append((self.lm_plan, L.YGG_PRO_RESID, prev_down, self.ws2, self.ss_a))
-        n_i32 = sum(gp.K // 64 + 148 for gp, *_ in chain)
-        self.pro_state = torch.zeros(max(n_i32, 1), dtype=torch.int32, device=dev)  # flags + launch counters
-        off = 0
-        self._pro = []
-        for gp, kind, prev, pws, ss in chain:
-            q = L.YggPrologue()
-            q.kind = kind
-            q.prev_plan = C.addressof(prev.handle)
-            q.prev_ws = pws.data_ptr()
-            if kind == L.YGG_PRO_RESID:
-                q.resid, q.ss_out = self.resid.data_ptr(), ss.data_ptr()
-            else:
-                q.ss_in, q.ss_tiles, q.norm_dim, q.eps = ss.data_ptr(), d // 64, d, eps
-            q.flags = self.pro_state.data_ptr() + 4 * off
-            q.launches = self.pro_state.data_ptr() + 4 * (off + gp.K // 64)
-            off += gp.K // 64 + 148
-            L.check(lib.ygg_gemm_plan_set_prologue(gp.handle, C.byref(q)))
-            self._pro.append(q)
-
     def _setup_gemv(self) -> None:
         """Row-block GEMV plans + epilogues (csrc/gemv.cu) for a <= 16-row decode pass."""
         lib, cfg, M = L.lib(), self.cfg, self.M
@@ -543,8 +491,6 @@ class Forward:
     def run(self, stream: torch.cuda.Stream | None = None) -> None:
         if self.gemv:
             self._run_gemv(stream)
-        elif self.pro:
-            self._run_prologue(stream)
         elif self.fused:
             self._run_fused(stream)
         else:
@@ -593,33 +539,6 @@ class Forward:
                 self._gather_last(stream)
             chk(lib.ygg_gemm_fused(self.lm_plan.handle, ws, C.byref(self.lm_plan.epi), s))
             stamp()
-
-    def _run_prologue(self, stream) -> None:
-        lib, cfg = L.lib(), self.cfg
-        s = L.stream_ptr(stream)
-        chk = L.check
-        d, eps = cfg.d_model, float(cfg.norm_eps)
-        wa, wb = self.ws.data_ptr(), self.ws2.data_ptr()
-        chk(lib.ygg_embed_fused(self.w["embed"].data_ptr(), cfg.vocab, d, self.tokens.data_ptr(), self.M,
-                                self.resid.data_ptr(), self.xn.data_ptr(), self.ss_e.data_ptr(), s))
-        qm = self.qmask.data_ptr() if self.mask_words > 0 else None
-        es = self.cache.element_size()
-        for li, p in enumerate(self.plans):
-            cache_l = self.cache.data_ptr() + li * self.layer_stride * es
-            chk(lib.ygg_gemm_run(p["qkv"].handle, wa, s))  # (prologue: the previous layer's down residual)
-            ss, tiles = (self.ss_e, d // 128) if li == 0 else (self.ss_a, d // 64)
-            chk(lib.ygg_epi_qkv_rope_rstd(p["qkv"].handle, wa, ss.data_ptr(), tiles, d, eps, cfg.n_heads,
-                                          cfg.n_kv_heads, cfg.head_dim, cfg.rope_theta, self.pos.data_ptr(),
-                                          self.slot.data_ptr(), self.req.data_ptr(), self.q.data_ptr(), cache_l,
-                                          self.S, self.act, self.rope_cs.data_ptr(), s))
-            self._attend(li, qm, s)
-            chk(lib.ygg_gemm_run(p["o"].handle, wb, s))
-            chk(lib.ygg_gemm_run(p["gu"].handle, wa, s))    # prologue: O's residual + sums of squares
-            chk(lib.ygg_gemm_run(p["down"].handle, wb, s))  # prologue: rstd + SwiGLU
-        if self.lm_plan is not None:
-            e = self.lm_epi
-            e.ss_in, e.ss_tiles, e.norm_dim, e.eps = self.ss_a.data_ptr(), d // 64, d, eps
-            chk(lib.ygg_gemm_fused(self.lm_plan.handle, wa, C.byref(e), s))  # prologue: down's residual
 
     def _run_unfused(self, stream, stamps: torch.Tensor | None = None) -> None:
         lib, cfg = L.lib(), self.cfg

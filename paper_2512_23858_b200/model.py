@@ -216,28 +216,6 @@ def prepare_fused_(w: dict, cfg: ModelConfig) -> dict:
     return w
 
 
-def prepare_folded_(w: dict, cfg: ModelConfig) -> dict:
-    """In-place conversion to the folded bf16 layout of the prologue verify forward (idempotent): the
-    RMSNorm gains folded into the columns of the following matmul (wqkv, wgu, lm_head) exactly as in
-    ``prepare_fused_``, rows kept in the standard order.  The norms become ones, so every other forward
-    runs on folded weights unchanged; a fused-layout dict is left as it is."""
-    if w.get("_layout") in ("folded", "fused"):
-        return w
-    for lw in w["layers"]:
-        an = lw["attn_norm"].float()
-        mn = lw["mlp_norm"].float()
-        lw["wqkv"] = (lw["wqkv"].float() * an[None, :]).to(lw["wqkv"].dtype).contiguous()
-        lw["wgu"] = (lw["wgu"].float() * mn[None, :]).to(lw["wgu"].dtype).contiguous()
-        lw["attn_norm"] = torch.ones_like(lw["attn_norm"])
-        lw["mlp_norm"] = torch.ones_like(lw["mlp_norm"])
-    fn = w["final_norm"].float()
-    if not bool(torch.all(fn == 1)):
-        w["lm_head"] = (w["lm_head"].float() * fn[None, :]).to(w["lm_head"].dtype)
-    w["final_norm"] = torch.ones_like(w["final_norm"])
-    w["_layout"] = "folded"
-    return w
-
-
 def rope_table(cfg: ModelConfig, positions: int, device) -> torch.Tensor:
     """[positions, hd/2, 2] (cos, sin) of the RoPE angle for the fused QKV epilogue.
 

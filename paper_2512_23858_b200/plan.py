@@ -48,9 +48,6 @@ class ForwardPlan:
     gemv: bool | None = None
     decode_attn: bool | None = None
     fused_epilogues: bool = False   # fused-epilogue GEMMs for every non-GEMV bf16 pass (fused weight layout)
-    prologue: bool = False          # tree / AR passes (verify): the residual + RMSNorm and SwiGLU epilogues
-    #                                 run as prologues of the next GEMM (ygg_gemm_plan_set_prologue) on
-    #                                 norm-folded weights (model.prepare_folded_): 6 launches per layer
     fused_layout_gemm: bool = False  # non-GEMV passes over weights already in the fused layout (the draft's
     #                                  prefill chunks): fused-epilogue GEMMs instead of stream-K GEMM + the
     #                                  layout-aware epilogue kernels (512-row chunk of the 1B draft: 3.7 vs 2.0 ms)

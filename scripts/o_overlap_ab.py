@@ -30,12 +30,12 @@ lib = L.lib()
 assert f.at_plans is not None
 orig_o = [p["o"] for p in f.plans]
 alt = {}
-for n in (84, 76, 64):
+for n in (116, 100):
     alt[n] = [GemmPlan(p["o"].W, p["o"].X, p["o"].M, n) for p in f.plans]
     need = max(q.ws_bytes for q in alt[n]) // 4 + 1
     assert need <= f.ws.numel(), (need, f.ws.numel())
-variants = [("late_148", 1, None), ("early_84", 0, 84), ("early_76", 0, 76), ("early_64", 0, 64),
-            ("late_84", 1, 84)]
+variants = [("late_148", 1, None), ("early_148", 0, None), ("early_116", 0, 116), ("early_100", 0, 100),
+            ("late_116", 1, 116)]
 graphs = {}
 for name, late, n in variants:
     for pl in f.at_plans:

@@ -16,8 +16,9 @@ from paper_2512_23858_b200.plan import ForwardPlan, L2Prefetch  # noqa: E402
 
 VARIANTS = {
     "default": ForwardPlan(),
-    "prologue": ForwardPlan(prologue=True),
-    "prologue_o": ForwardPlan(prologue=True, verify_attn_l2=(L2Prefetch("wgu", 0.1), L2Prefetch("wo", 0.25))),
+    "attn_gu_0.15": ForwardPlan(verify_attn_l2=(L2Prefetch("wgu", 0.15),)),
+    "attn_gu_0.2": ForwardPlan(verify_attn_l2=(L2Prefetch("wgu", 0.2),)),
+    "attn_gu_0.05": ForwardPlan(verify_attn_l2=(L2Prefetch("wgu", 0.05),)),
     "attn_gu_0.1_o": ForwardPlan(verify_attn_l2=(L2Prefetch("wgu", 0.1), L2Prefetch("wo", 0.25))),
 }
 

@@ -77,14 +77,14 @@ def test_fp32_step_trace_matches_oracle(coupled, cuda):
     assert sd.generated(0)[:n_tok] == ar
 
 
-@pytest.mark.parametrize("fused", [False, True, "prologue"])
+@pytest.mark.parametrize("fused", [False, True])
 @pytest.mark.parametrize("coupled", [False, True])
 def test_bf16_spec_equals_ar_and_graph_equals_eager(coupled, fused, cuda):
     from paper_2512_23858_b200.engine import ARDecoder, SpecDecoder, StepShape
     from paper_2512_23858_b200.model import weights_to
     from paper_2512_23858_b200.plan import ForwardPlan
 
-    plan = ForwardPlan(prologue=True) if fused == "prologue" else ForwardPlan(fused_epilogues=fused)
+    plan = ForwardPlan(fused_epilogues=fused)
     tc, dc, tw, dw = _models(torch.float32, coupled)
     twb, dwb = weights_to(tw, cuda, torch.bfloat16), weights_to(dw, cuda, torch.bfloat16)
     prompts = torch.stack([_prompt(tc.vocab, 32, s) for s in (1000, 1001)])

@@ -197,8 +197,8 @@ struct Layout {
   static constexpr uint32_t off_recv = off_p + NST * p_bytes;
   static constexpr uint32_t off_ml = off_recv + kRows * RS * 2;     // f32 [C][128 / C][2] (max, sum)
   static constexpr uint32_t off_red = off_ml + kRows * 8;           // f32 [2][128] half maxima, [2][128] half sums
-  static constexpr uint32_t off_bar = off_red + 4 * kRows * 4;      // kv_full[NST], q, s, p, o, recv
-  static constexpr uint32_t bytes = off_bar + (NST + 5) * 8 + 16;
+  static constexpr uint32_t off_bar = off_red + 4 * kRows * 4;      // k_full[NST], v_full[NST], q, s, p, o, recv
+  static constexpr uint32_t bytes = off_bar + (2 * NST + 5) * 8 + 16;
   static constexpr int s_cols = NST * kKC;       // S of one round
   static constexpr int tcols = (s_cols + 2 * HD) <= 256 ? 256 : 512;  // + O of a round + O accumulated
   static_assert(s_cols + 2 * HD <= 512, "TMEM budget");
@@ -220,8 +220,12 @@ __global__ void __launch_bounds__(kThreads, 1)
   __half* recv_o = reinterpret_cast<__half*>(base + Ly::off_recv);
   float* recv_ml = reinterpret_cast<float*>(base + Ly::off_ml);
   float* red = reinterpret_cast<float*>(base + Ly::off_red);
-  uint64_t* kv_full = reinterpret_cast<uint64_t*>(base + Ly::off_bar);
-  uint64_t* q_full = kv_full + NST;
+  // K and V of a ring stage complete on separate barriers: the next round's K chunks stream into the
+  // K slots as soon as this round's S = Q K^T is done (during the softmax), its V chunks as soon as
+  // this round's P V is done, so the round-to-round chain no longer waits on a whole load latency.
+  uint64_t* k_full = reinterpret_cast<uint64_t*>(base + Ly::off_bar);
+  uint64_t* v_full = k_full + NST;
+  uint64_t* q_full = v_full + NST;
   uint64_t* s_full = q_full + 1;
   uint64_t* p_full = s_full + 1;
   uint64_t* o_full = p_full + 1;
@@ -245,7 +249,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   };
   if (threadIdx.x == 0) {
     AT_STAMP(0);
-    for (int s = 0; s < NST; ++s) mbar_init(&kv_full[s], 1);
+    for (int s = 0; s < NST; ++s) {
+      mbar_init(&k_full[s], 1);
+      mbar_init(&v_full[s], 1);
+    }
     mbar_init(q_full, 1);
     mbar_init(s_full, 1);
     mbar_init(p_full, kSoftThreads);
@@ -286,13 +293,21 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) {
       const int kv_row0 = (r * 2 * a.Hkv + kvh) * a.S;        // K rows of this head
       const int vt_row0 = ((r * 2 + 1) * a.Hkv + kvh) * HD;   // V^T rows of this head
-      auto load = [&](int j) {
+      auto load_k = [&](int j) {
         const int c = ks + j * C, st = j % NST;
-        mbar_arrive_expect_tx(&kv_full[st], Ly::k_bytes + Ly::v_bytes);
+        mbar_arrive_expect_tx(&k_full[st], Ly::k_bytes);
 #pragma unroll
         for (int dc = 0; dc < DCH; ++dc)
-          tma2(sk + st * Ly::k_bytes + dc * (kKC * 128), &tk, &kv_full[st], dc * 64, kv_row0 + c * kKC);
-        tma2(sv + st * Ly::v_bytes, &tv, &kv_full[st], c * kKC, vt_row0);
+          tma2(sk + st * Ly::k_bytes + dc * (kKC * 128), &tk, &k_full[st], dc * 64, kv_row0 + c * kKC);
+      };
+      auto load_v = [&](int j) {
+        const int c = ks + j * C, st = j % NST;
+        mbar_arrive_expect_tx(&v_full[st], Ly::v_bytes);
+        tma2(sv + st * Ly::v_bytes, &tv, &v_full[st], c * kKC, vt_row0);
+      };
+      auto load = [&](int j) {
+        load_k(j);
+        load_v(j);
       };
       int issued = 0;
       // the committed prefix's chunks of the first round stream in before the dependency wait
@@ -316,7 +331,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int j0 = rd * NST, j1 = min(n_my, j0 + NST);
         for (int j = j0; j < j1; ++j) {
           const int st = j % NST;
-          mbar_wait(&kv_full[st], (j / NST) & 1);
+          mbar_wait(&k_full[st], (j / NST) & 1);
           tc_fence_after();
           if (j == 0) AT_STAMP(4);
           if (j == j1 - 1 && rd == 0) AT_STAMP(5);
@@ -343,12 +358,19 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
         umma_commit(s_full);
+        const int jn = min(n_my, j1 + NST);
+        if (rd + 1 < rounds) {  // this round's K slots are free once its S MMAs completed
+          mbar_wait(s_full, rd & 1);
+          for (int j = j1; j < jn; ++j) load_k(j);
+        }
         mbar_wait(p_full, rd & 1);
         tc_fence_after();
         trace_max(a.trace, 6);
         if (rd == 0) AT_STAMP(6);
         for (int j = j0; j < j1; ++j) {
           const int st = j % NST;
+          mbar_wait(&v_full[st], (j / NST) & 1);
+          tc_fence_after();
 #pragma unroll
           for (int kk = 0; kk < kKC / 16; ++kk) {
             const uint64_t ad = umma_desc_sw128(smem_u32(sp + (j - j0) * Ly::p_bytes) + kk * 32);
@@ -357,10 +379,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
         umma_commit(o_full);
-        if (rd + 1 < rounds) {  // the round's stages are free once its MMAs completed
+        if (rd + 1 < rounds) {  // ... and its V slots once its P V MMAs completed
           mbar_wait(o_full, rd & 1);
-          const int jn = min(n_my, j1 + NST);
-          while (issued < jn) load(issued++);
+          for (int j = j1; j < jn; ++j) load_v(j);
         }
       }
       // the last round's MMAs complete before the softmax warps pass o_full, i.e. before the

@@ -8,7 +8,8 @@
 //   warp 8 lane 0  TMA: prefix chunks before griddepcontrol.wait (the cache was committed kernels
 //                  ago), Q and the tree-block chunks after it; MMA: S_i = Q K_i^T (M=128, N=64,
 //                  K=hd) into TMEM, then O = sum_i P_i V_i (M=128, N=hd, K=64) once P is in smem.
-//   warps 0-7      softmax, one thread per (row, 32-key half of a chunk): tcgen05.ld S, ancestor /
+//   softmax warps  (Soft<HD>::warps: 16 at hd 128, 8 at hd 64) one thread per (row, 64/NP-key slice of a
+//                  chunk): tcgen05.ld S, ancestor /
 //                  prefix mask from the row's tree-mask bits, round max, exp2, bf16 P -> smem
 //                  (128B-swizzled, the UMMA A operand), then O (read back from TMEM) accumulated in
 //                  registers with the online-softmax rescale across rounds.
@@ -32,9 +33,19 @@ namespace at {
 
 constexpr int kKC = 64;                  // keys per chunk
 constexpr int kRows = 128;               // UMMA M = TMEM lanes
-constexpr int kSoftWarps = 8;            // two per TMEM lane quarter (32-key column halves)
-constexpr int kSoftThreads = 32 * kSoftWarps;
-constexpr int kThreads = kSoftThreads + 32;  // + the TMA / MMA warp
+// Softmax warps: NP per TMEM lane quarter, each taking a 64 / NP-key slice of every chunk (and HD / NP
+// output columns in the O fold / push).  hd 128: 16 warps (4 per quarter), which halves the per-thread
+// exp2 / TMEM-load work of a round against 8 (the long-context rounds are softmax-bound); hd 64: 8.
+template <int HD>
+struct Soft {
+  static constexpr int NP = HD == 128 ? 4 : 2;
+  static constexpr int warps = 4 * NP;
+  static constexpr int threads = 32 * warps;
+  static constexpr int KP = kKC / NP;   // keys per thread per chunk (16 or 32)
+  static constexpr int CP = HD / NP;    // O columns per thread (32)
+  static_assert(CP == 32, "the O fold / push move 32 TMEM columns per thread");
+};
+constexpr int kMaxThreads = 32 * 16 + 32;
 constexpr uint32_t kMagic = 0x59475454u;     // "YGTT"
 
 struct Plan {
@@ -196,8 +207,8 @@ struct Layout {
   static constexpr int RS = HD + 8;
   static constexpr uint32_t off_recv = off_p + NST * p_bytes;
   static constexpr uint32_t off_ml = off_recv + kRows * RS * 2;     // f32 [C][128 / C][2] (max, sum)
-  static constexpr uint32_t off_red = off_ml + kRows * 8;           // f32 [2][128] half maxima, [2][128] half sums
-  static constexpr uint32_t off_bar = off_red + 4 * kRows * 4;      // k_full[NST], v_full[NST], q, s, p, o, recv
+  static constexpr uint32_t off_red = off_ml + kRows * 8;           // f32 [NP][128] slice maxima, [NP][128] sums
+  static constexpr uint32_t off_bar = off_red + 2 * Soft<HD>::NP * kRows * 4;  // k_full[NST], v_full[NST], q, s, p, o, recv
   static constexpr uint32_t bytes = off_bar + (2 * NST + 5) * 8 + 16;
   static constexpr int s_cols = NST * kKC;       // S of one round
   static constexpr int tcols = (s_cols + 2 * HD) <= 256 ? 256 : 512;  // + O of a round + O accumulated
@@ -205,10 +216,13 @@ struct Layout {
 };
 
 template <int HD, int NST>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(Soft<HD>::threads + 32, 1)
     attn_tree_kernel(const __grid_constant__ CUtensorMap tqm, const __grid_constant__ CUtensorMap tk,
                      const __grid_constant__ CUtensorMap tv, Args a) {
   using Ly = Layout<HD, NST>;
+  constexpr int kSoftWarps = Soft<HD>::warps, kSoftThreads = Soft<HD>::threads;
+  constexpr int NP = Soft<HD>::NP, KP = Soft<HD>::KP, CP = Soft<HD>::CP;
+  constexpr uint32_t kpmask = KP == 32 ? 0xffffffffu : ((1u << KP) - 1u);
   constexpr int DCH = Ly::DCH;
   constexpr int RS = Ly::RS;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
@@ -282,7 +296,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int n_my = nch > ks ? (nch - ks + C - 1) >> a.lc : 0;
   const int rounds = (n_my + NST - 1) / NST;
   // this thread's query row (softmax warps): TMEM lane quarter q holds tq tokens x G heads
-  const int q = warp & 3, half = (warp >> 2) & 1;
+  const int q = warp & 3, part = warp >> 2;  // TMEM lane quarter, key / column slice (softmax warps)
   const int row = q * 32 + lane;
   const uint32_t lane_base = static_cast<uint32_t>(q * 32) << 16;  // TMEM lane quarter of this warp
   const int tl = q * a.tq + (lane >> a.lg);             // token within the tile
@@ -391,7 +405,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (!a.late_trigger) pdl_launch_dependents();
     }
   } else {
-    // ===== softmax warps: thread = (TMEM lane row, 32-key half of every chunk) =====
+    // ===== softmax warps: thread = (TMEM lane row, KP-key slice of every chunk) =====
     pdl_wait();
     if (!a.late_trigger) pdl_launch_dependents();
     const int tok = rt * a.tpt + (valid ? tl : 0);
@@ -402,10 +416,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t vis[NST];
 #pragma unroll
       for (int i = 0; i < NST; ++i) {
-        const int kw = (ks + (j0 + i) * C) * kKC + half * 32;
+        const int kw = (ks + (j0 + i) * C) * kKC + part * KP;
         // rows past the tile (never pushed) take the prefix's all-visible word too, so fully visible
         // chunks stay on the warp-uniform fast path
-        vis[i] = i >= nj ? 0u : (kw + 32 <= bs ? 0xffffffffu : (valid ? vis_word(kw, bs, bl, tok, a.mask_words, mrow) : 0u));
+        vis[i] = i >= nj ? 0u
+                         : (kw + KP <= bs ? kpmask : (valid ? vis_word(kw, bs, bl, tok, a.mask_words, mrow) & kpmask : 0u));
       }
       mbar_wait(s_full, rd & 1);
       tc_fence_after();
@@ -414,44 +429,48 @@ __global__ void __launch_bounds__(kThreads, 1)
       // exchange their maxima): P = 2^(s - max) into the UMMA A operand
       bool full[NST];  // warp-uniform: every row of the warp sees all 32 keys (committed prefix)
 #pragma unroll
-      for (int i = 0; i < NST; ++i) full[i] = __all_sync(0xffffffffu, vis[i] == 0xffffffffu);
+      for (int i = 0; i < NST; ++i) full[i] = __all_sync(0xffffffffu, vis[i] == kpmask);
       float mx = -INFINITY;
 #pragma unroll
       for (int i = 0; i < NST; ++i) {
         if (i < nj) {
-          float v[32];
-          tmem_ld32(tS + lane_base + i * kKC + half * 32, v);
+          float v[KP];
+          if constexpr (KP == 32) tmem_ld32(tS + lane_base + i * kKC + part * KP, v);
+          else tmem_ld16(tS + lane_base + i * kKC + part * KP, v);
           if (full[i]) {
 #pragma unroll
-            for (int j = 0; j < 32; ++j) mx = fmaxf(mx, v[j]);
+            for (int j = 0; j < KP; ++j) mx = fmaxf(mx, v[j]);
           } else {
 #pragma unroll
-            for (int j = 0; j < 32; ++j)
+            for (int j = 0; j < KP; ++j)
               if ((vis[i] >> j) & 1u) mx = fmaxf(mx, v[j]);
           }
         }
       }
-      red[half * kRows + row] = mx;
-      asm volatile("bar.sync %0, 64;" ::"r"(2 + q) : "memory");  // the two warps of this lane quarter
-      mx = fmaxf(red[row], red[kRows + row]);
+      red[part * kRows + row] = mx;
+      asm volatile("bar.sync %0, %1;" ::"r"(2 + q), "r"(32 * NP) : "memory");  // the NP warps of this quarter
+      mx = red[row];
+#pragma unroll
+      for (int pp = 1; pp < NP; ++pp) mx = fmaxf(mx, red[pp * kRows + row]);
       const float mnew = fmaxf(M, mx * sl);  // log2 units (scale > 0 commutes with the max)
       const float ref = mnew == -INFINITY ? 0.f : mnew;
       float sum = 0.f;
 #pragma unroll
       for (int i = 0; i < NST; ++i) {
         if (i < nj) {
-          float v[32];
-          tmem_ld32(tS + lane_base + i * kKC + half * 32, v);
+          float v[KP];
+          if constexpr (KP == 32) tmem_ld32(tS + lane_base + i * kKC + part * KP, v);
+          else tmem_ld16(tS + lane_base + i * kKC + part * KP, v);
           if (full[i]) {
 #pragma unroll
-            for (int j = 0; j < 32; ++j) {
+            for (int j = 0; j < KP; ++j) {
               const float x = fmaf(v[j], sl, -ref);
               v[j] = ex2(x);
               sum += v[j];
             }
           } else {
 #pragma unroll
-            for (int j = 0; j < 32; ++j) {
+            for (int j = 0; j < KP; ++j) {
               const float x = fmaf(v[j], sl, -ref);
               v[j] = ((vis[i] >> j) & 1u) ? ex2(x) : 0.f;
               sum += v[j];
@@ -459,8 +478,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           const uint32_t rb = smem_u32(sp + i * Ly::p_bytes + row * 128);
 #pragma unroll
-          for (int u = 0; u < 4; ++u)
-            sts128(rb + (((half * 4 + u) ^ (row & 7)) << 4), pack2(v[8 * u], v[8 * u + 1]),
+          for (int u = 0; u < KP / 8; ++u)
+            sts128(rb + (((part * (KP / 8) + u) ^ (row & 7)) << 4), pack2(v[8 * u], v[8 * u + 1]),
                    pack2(v[8 * u + 2], v[8 * u + 3]), pack2(v[8 * u + 4], v[8 * u + 5]),
                    pack2(v[8 * u + 6], v[8 * u + 7]));
         }
@@ -477,10 +496,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_wait(o_full, rd & 1);
         tc_fence_after();
 #pragma unroll
-        for (int c = 0; c < HD / 2; c += 32) {
+        for (int c = 0; c < CP; c += 32) {
           uint32_t ob[32], ab[32];
-          tmem_ld32_issue(tO + lane_base + half * (HD / 2) + c, ob);
-          if (rd > 0) tmem_ld32_issue(tAcc + lane_base + half * (HD / 2) + c, ab);
+          tmem_ld32_issue(tO + lane_base + part * CP + c, ob);
+          if (rd > 0) tmem_ld32_issue(tAcc + lane_base + part * CP + c, ab);
           tmem_wait_ld();
           regs_after_wait(ob);
           if (rd > 0) {
@@ -488,7 +507,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int i = 0; i < 32; ++i) ob[i] = __float_as_uint(fmaf(__uint_as_float(ab[i]), alpha, __uint_as_float(ob[i])));
           }
-          tmem_st32(tAcc + lane_base + half * (HD / 2) + c, ob);
+          tmem_st32(tAcc + lane_base + part * CP + c, ob);
         }
         tmem_wait_st();
       }
@@ -505,22 +524,24 @@ __global__ void __launch_bounds__(kThreads, 1)
     return;
   }
   // ===== push this row's partial to the rank owning the row: O / l in f16 and (max, l) =====
-  float* red_l = red + 2 * kRows;
-  red_l[half * kRows + row] = l;
-  asm volatile("bar.sync %0, 64;" ::"r"(2 + q) : "memory");
-  const float ltot = red_l[row] + red_l[kRows + row];
+  float* red_l = red + NP * kRows;
+  red_l[part * kRows + row] = l;
+  asm volatile("bar.sync %0, %1;" ::"r"(2 + q), "r"(32 * NP) : "memory");
+  float ltot = red_l[row];
+#pragma unroll
+  for (int pp = 1; pp < NP; ++pp) ltot += red_l[pp * kRows + row];
   const float inv = ltot > 0.f ? 1.f / ltot : 0.f;
   const int lsh = 7 - a.lc;  // log2(lanes_per)
   const int d = row >> lsh, ll = row & (lanes_per - 1);
   const uint32_t rbar = mapa_shared(smem_u32(recv_bar), d);
-  const uint32_t ro = mapa_shared(smem_u32(recv_o + (static_cast<size_t>(ks * lanes_per + ll) * RS + half * (HD / 2))), d);
+  const uint32_t ro = mapa_shared(smem_u32(recv_o + (static_cast<size_t>(ks * lanes_per + ll) * RS + part * CP)), d);
   if (rounds == 1) {
     mbar_wait(o_full, 0);
     tc_fence_after();
   }
-  const uint32_t tsrc = (rounds > 1 ? tAcc : tO) + lane_base + half * (HD / 2);
+  const uint32_t tsrc = (rounds > 1 ? tAcc : tO) + lane_base + part * CP;
 #pragma unroll
-  for (int c = 0; c < HD / 2; c += 32) {
+  for (int c = 0; c < CP; c += 32) {
     uint32_t ob[32];
     if (rounds > 0) {
       tmem_ld32_issue(tsrc + c, ob);
@@ -539,22 +560,22 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   }
-  if (valid && half == 0)
+  if (valid && part == 0)
     st_async_v2(mapa_shared(smem_u32(recv_ml + static_cast<size_t>(ks * lanes_per + ll) * 2), d), __float_as_uint(M),
                 __float_as_uint(ltot), rbar);
   tc_fence_before();
   __syncthreads();  // pairs with the TMA / MMA warp's: every TMEM read is done
   if (threadIdx.x == 0) AT_STAMP(8);
-  // ===== owner: rows [ks * lanes_per, (ks + 1) * lanes_per): 256 / lanes_per threads per row, 8-column
+  // ===== owner: rows [ks * lanes_per, (ks + 1) * lanes_per): kSoftThreads / lanes_per threads per row, 8-column
   // units, the C partials combined in fixed rank order
   mbar_wait(recv_bar, 0);
   if (threadIdx.x == 0) {
     trace_max(a.trace, 4);
     AT_STAMP(9);
   }
-  const int tsh = 8 - lsh;                    // log2(threads per row)
+  const int tsh = (NP == 4 ? 9 : 8) - lsh;    // log2(threads per row)
   const int ll2 = threadIdx.x >> tsh;         // owned row
-  const int part = threadIdx.x & ((1 << tsh) - 1);
+  const int upart = threadIdx.x & ((1 << tsh) - 1);
   const int units = (HD / 8) >> tsh;          // 8-column units per thread
   const int lr = ks * lanes_per + ll2;        // TMEM lane of the row
   if (lane_valid(lr)) {
@@ -581,7 +602,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int head = kvh * a.G + (l32 & (a.G - 1));
     __nv_bfloat16* dst = a.out + (static_cast<size_t>(r * a.T + tok) * a.Hq + head) * HD;
     for (int u = 0; u < units; ++u) {
-      const int col = (part * units + u) * 8;
+      const int col = (upart * units + u) * 8;
       float acc[8];
 #pragma unroll
       for (int i = 0; i < 8; ++i) acc[i] = 0.f;
@@ -801,7 +822,8 @@ int ygg_attn_tree_run(const void* plan, const int32_t* blk_start, const int32_t*
     a.pf_bytes[rg] = p->pf_bytes[rg];
   }
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  const dim3 grid(p->csplit, p->row_tiles, p->Hkv * p->B), block(kThreads);
+  const dim3 grid(p->csplit, p->row_tiles, p->Hkv * p->B), block(p->hd == 128 ? Soft<128>::threads + 32
+                                                                                  : Soft<64>::threads + 32);
 #define YGG_AT_LAUNCH(H, N)                                                                                        \
   if (p->hd == H && p->nst == N)                                                                                   \
     return launch_pdl_cluster_x(attn_tree_kernel<H, N>, grid, block, p->smem, p->csplit, s, p->tqm, p->tk, p->tv, a);

@@ -35,13 +35,13 @@ for _ in range(2):
     sd.step(use_graph=False)
 torch.cuda.synchronize()
 res = {}
-for name, f, variants in (("verify", sd.verify, [(0, 0), (4, 2), (3, 4), (2, 4), (3, 2), (4, 4)]),
-                          ("draft", sd.draft, [(0, 0), (4, 4), (8, 4), (2, 4), (4, 8), (8, 8)])):
-    for kv, st in variants:
-        g = Forward(f.cfg, f.w, f.cache, f.B, f.R, f.mask_words, f.act_dtype,
-                    gemv=f.gemv, plan=ForwardPlan(attn_kvsplit=kv, attn_stages=st))
+DRAFT = [(0, 0, 0), (1, 8, 0), (1, 4, 0), (1, 16, 0), (2, 8, 0), (2, 4, 2), (4, 4, 2)]
+for name, f, variants in (("draft", sd.draft, DRAFT),):
+    for kv, st, ksp in variants:  # (kvsplit, stages, in-CTA key-split groups); 0 = automatic
+        g = Forward(f.cfg, f.w, f.cache, f.B, f.R, f.mask_words, f.act_dtype, gemv=f.gemv,
+                    plan=ForwardPlan(attn_kvsplit=kv, attn_stages=st, attn_ksplit=ksp, tree_attn=False))
         for t in ("tokens", "pos", "slot", "req", "qmask", "blk_start", "blk_len"):
             getattr(g, t).copy_(getattr(f, t))
-        res[f"{name}_kv{kv}_st{st}_ms"] = timeit(g, 20)
+        res[f"{name}_kv{kv}_st{st}_ks{ksp}_ms"] = timeit(g, 20)
         del g
 print(json.dumps(res), flush=True)

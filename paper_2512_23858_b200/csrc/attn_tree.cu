@@ -51,7 +51,7 @@ constexpr uint32_t kMagic = 0x59475454u;     // "YGTT"
 struct Plan {
   uint32_t magic;
   int B, T, Hq, Hkv, hd, S, G;
-  int tpt, tq, row_tiles, csplit, nst, tcols;
+  int tpt, tq, row_tiles, csplit, nst, ring, tcols;
   size_t smem;
   const char* pf_ptr[2];
   size_t pf_bytes[2];
@@ -191,35 +191,41 @@ YGG_DEV uint32_t vis_word(int kw, int bs, int bl, int tq, int mask_words, const 
   return pre | blk;
 }
 
-template <int HD, int NST>
+// NST chunks per round.  RING == NST: one round of K / V in flight and one S buffer (short contexts: the
+// key split over a cluster leaves ~1 round per CTA).  RING == 2 * NST (long contexts, single-CTA tiles):
+// the next round's K / V stream in while a round computes and S is double-buffered in TMEM, so round
+// r + 1's Q K^T runs during round r's softmax; no cluster merge (the tile's CTA writes O itself).
+template <int HD, int NST, int RING>
 struct Layout {
+  static constexpr bool dbl = RING > NST;
+  static_assert(RING == NST || RING == 2 * NST, "ring: one or two rounds of chunks");
   static constexpr int DCH = HD / 64;
   static constexpr uint32_t q_bytes = DCH * kRows * 128;   // [DCH][128 rows][128 B]
   static constexpr uint32_t k_bytes = DCH * kKC * 128;     // one K chunk: [DCH][64 keys][128 B]
   static constexpr uint32_t v_bytes = HD * 128;            // one V^T chunk: [hd rows][64 keys x 2 B]
   static constexpr uint32_t p_bytes = kRows * 128;         // one P chunk: [128 rows][64 keys x 2 B]
   static constexpr uint32_t off_k = q_bytes;
-  static constexpr uint32_t off_v = off_k + NST * k_bytes;
-  static constexpr uint32_t off_p = off_v + NST * v_bytes;
+  static constexpr uint32_t off_v = off_k + RING * k_bytes;
+  static constexpr uint32_t off_p = off_v + RING * v_bytes;
   // Merge receive rows [C][128 / C][RS] of the row-normalised partial O in f16 (|O / l| <= max |V|);
   // RS = hd + 8 halves keeps row-parallel 16-byte accesses conflict-free.  Dedicated (not aliased
   // onto the ring), so a rank pushes as soon as its own rows are done.
   static constexpr int RS = HD + 8;
   static constexpr uint32_t off_recv = off_p + NST * p_bytes;
-  static constexpr uint32_t off_ml = off_recv + kRows * RS * 2;     // f32 [C][128 / C][2] (max, sum)
+  static constexpr uint32_t off_ml = off_recv + (dbl ? 0 : kRows * RS * 2);  // f32 [C][128 / C][2] (max, sum)
   static constexpr uint32_t off_red = off_ml + kRows * 8;           // f32 [NP][128] slice maxima, [NP][128] sums
-  static constexpr uint32_t off_bar = off_red + 2 * Soft<HD>::NP * kRows * 4;  // k_full[NST], v_full[NST], q, s, p, o, recv
-  static constexpr uint32_t bytes = off_bar + (2 * NST + 5) * 8 + 16;
-  static constexpr int s_cols = NST * kKC;       // S of one round
+  static constexpr uint32_t off_bar = off_red + 2 * Soft<HD>::NP * kRows * 4;  // k_full[RING], v_full[RING], q, s[2], p, o, recv
+  static constexpr uint32_t bytes = off_bar + (2 * RING + 6) * 8 + 16;
+  static constexpr int s_cols = (dbl ? 2 : 1) * NST * kKC;  // S of one round (two buffers when dbl)
   static constexpr int tcols = (s_cols + 2 * HD) <= 256 ? 256 : 512;  // + O of a round + O accumulated
   static_assert(s_cols + 2 * HD <= 512, "TMEM budget");
 };
 
-template <int HD, int NST>
+template <int HD, int NST, int RING>
 __global__ void __launch_bounds__(Soft<HD>::threads + 32, 1)
     attn_tree_kernel(const __grid_constant__ CUtensorMap tqm, const __grid_constant__ CUtensorMap tk,
                      const __grid_constant__ CUtensorMap tv, Args a) {
-  using Ly = Layout<HD, NST>;
+  using Ly = Layout<HD, NST, RING>;
   constexpr int kSoftWarps = Soft<HD>::warps, kSoftThreads = Soft<HD>::threads;
   constexpr int NP = Soft<HD>::NP, KP = Soft<HD>::KP, CP = Soft<HD>::CP;
   constexpr uint32_t kpmask = KP == 32 ? 0xffffffffu : ((1u << KP) - 1u);
@@ -238,10 +244,10 @@ __global__ void __launch_bounds__(Soft<HD>::threads + 32, 1)
   // K slots as soon as this round's S = Q K^T is done (during the softmax), its V chunks as soon as
   // this round's P V is done, so the round-to-round chain no longer waits on a whole load latency.
   uint64_t* k_full = reinterpret_cast<uint64_t*>(base + Ly::off_bar);
-  uint64_t* v_full = k_full + NST;
-  uint64_t* q_full = v_full + NST;
-  uint64_t* s_full = q_full + 1;
-  uint64_t* p_full = s_full + 1;
+  uint64_t* v_full = k_full + RING;
+  uint64_t* q_full = v_full + RING;
+  uint64_t* s_full = q_full + 1;  // [2]: one per S buffer (the second only when Ly::dbl)
+  uint64_t* p_full = s_full + 2;
   uint64_t* o_full = p_full + 1;
   uint64_t* recv_bar = o_full + 1;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(recv_bar + 1);
@@ -263,12 +269,13 @@ __global__ void __launch_bounds__(Soft<HD>::threads + 32, 1)
   };
   if (threadIdx.x == 0) {
     AT_STAMP(0);
-    for (int s = 0; s < NST; ++s) {
+    for (int s = 0; s < RING; ++s) {
       mbar_init(&k_full[s], 1);
       mbar_init(&v_full[s], 1);
     }
     mbar_init(q_full, 1);
-    mbar_init(s_full, 1);
+    mbar_init(&s_full[0], 1);
+    mbar_init(&s_full[1], 1);
     mbar_init(p_full, kSoftThreads);
     mbar_init(o_full, 1);
     // The merge: every rank's partial of each valid row this rank owns arrives as st.async bytes.
@@ -308,14 +315,14 @@ __global__ void __launch_bounds__(Soft<HD>::threads + 32, 1)
       const int kv_row0 = (r * 2 * a.Hkv + kvh) * a.S;        // K rows of this head
       const int vt_row0 = ((r * 2 + 1) * a.Hkv + kvh) * HD;   // V^T rows of this head
       auto load_k = [&](int j) {
-        const int c = ks + j * C, st = j % NST;
+        const int c = ks + j * C, st = j % RING;
         mbar_arrive_expect_tx(&k_full[st], Ly::k_bytes);
 #pragma unroll
         for (int dc = 0; dc < DCH; ++dc)
           tma2(sk + st * Ly::k_bytes + dc * (kKC * 128), &tk, &k_full[st], dc * 64, kv_row0 + c * kKC);
       };
       auto load_v = [&](int j) {
-        const int c = ks + j * C, st = j % NST;
+        const int c = ks + j * C, st = j % RING;
         mbar_arrive_expect_tx(&v_full[st], Ly::v_bytes);
         tma2(sv + st * Ly::v_bytes, &tv, &v_full[st], c * kKC, vt_row0);
       };
@@ -325,7 +332,7 @@ __global__ void __launch_bounds__(Soft<HD>::threads + 32, 1)
       };
       int issued = 0;
       // the committed prefix's chunks of the first round stream in before the dependency wait
-      while (issued < n_my && issued < NST && (ks + issued * C + 1) * kKC <= bs) load(issued++);
+      while (issued < n_my && issued < RING && (ks + issued * C + 1) * kKC <= bs) load(issued++);
       pdl_wait();
       if (!a.late_trigger) pdl_launch_dependents();
       trace_min(a.trace, 1);
@@ -336,26 +343,35 @@ __global__ void __launch_bounds__(Soft<HD>::threads + 32, 1)
       for (int dc = 0; dc < DCH; ++dc)
         for (int qq = 0; qq < nq; ++qq)
           tma3(sq + dc * (kRows * 128) + qq * (32 * 128), &tqm, q_full, dc * 64, kvh * a.G, r * a.T + t0 + qq * a.tq);
-      while (issued < n_my && issued < NST) load(issued++);
+      while (issued < n_my && issued < RING) load(issued++);
       const uint32_t id_s = umma_idesc_bf16(kRows, kKC), id_o = umma_idesc_bf16(kRows, HD);
       mbar_wait(q_full, 0);  // always: no CTA leaves with a TMA write into its shared memory in flight
       trace_max(a.trace, 5);
       AT_STAMP(3);
-      for (int rd = 0; rd < rounds; ++rd) {
-        const int j0 = rd * NST, j1 = min(n_my, j0 + NST);
-        for (int j = j0; j < j1; ++j) {
-          const int st = j % NST;
-          mbar_wait(&k_full[st], (j / NST) & 1);
+      // S = Q K^T of round rr into S buffer rr & 1 (buffer 0 only unless Ly::dbl), committed on s_full[buf]
+      auto s_mma = [&](int rr) {
+        const int a0 = rr * NST, a1 = min(n_my, a0 + NST);
+        const uint32_t sb = tS + (Ly::dbl ? (rr & 1) * NST * kKC : 0);
+        for (int j = a0; j < a1; ++j) {
+          const int st = j % RING;
+          mbar_wait(&k_full[st], (j / RING) & 1);
           tc_fence_after();
           if (j == 0) AT_STAMP(4);
-          if (j == j1 - 1 && rd == 0) AT_STAMP(5);
+          if (j == a1 - 1 && rr == 0) AT_STAMP(5);
 #pragma unroll
           for (int kk = 0; kk < HD / 16; ++kk) {
             const uint64_t ad = umma_desc_sw128(smem_u32(sq + (kk / 4) * (kRows * 128)) + (kk % 4) * 32);
             const uint64_t bd = umma_desc_sw128(smem_u32(sk + st * Ly::k_bytes + (kk / 4) * (kKC * 128)) + (kk % 4) * 32);
-            umma_bf16(tS + (j - j0) * kKC, ad, bd, id_s, kk > 0 ? 1u : 0u);
+            umma_bf16(sb + (j - a0) * kKC, ad, bd, id_s, kk > 0 ? 1u : 0u);
           }
         }
+        umma_commit(&s_full[Ly::dbl ? (rr & 1) : 0]);
+      };
+      if (rounds > 0) s_mma(0);
+      for (int rd = 0; rd < rounds; ++rd) {
+        const int j0 = rd * NST, j1 = min(n_my, j0 + NST);
+        // the other S buffer was last read by round rd - 1's softmax, which this warp saw finish (p_full)
+        if (Ly::dbl && rd + 1 < rounds) s_mma(rd + 1);
         if (rd == 0) {
           // This CTA's own loads have landed: now the kernel barely touches HBM, so pull its share of a
           // later weight stream into L2 (issued earlier, the prefetch would queue ahead of the chunk loads).
@@ -371,19 +387,19 @@ __global__ void __launch_bounds__(Soft<HD>::threads + 32, 1)
             }
           }
         }
-        umma_commit(s_full);
-        const int jn = min(n_my, j1 + NST);
-        if (rd + 1 < rounds) {  // this round's K slots are free once its S MMAs completed
-          mbar_wait(s_full, rd & 1);
-          for (int j = j1; j < jn; ++j) load_k(j);
+        // this round's K slots are free once its S MMAs completed: refill them one ring ahead
+        const int jn = Ly::dbl ? min(n_my, j1 + RING) : min(n_my, j1 + NST);
+        if (rd + 1 < rounds) {
+          mbar_wait(&s_full[Ly::dbl ? (rd & 1) : 0], Ly::dbl ? (rd >> 1) & 1 : rd & 1);
+          for (int j = Ly::dbl ? j0 + RING : j1; j < jn; ++j) load_k(j);
         }
         mbar_wait(p_full, rd & 1);
         tc_fence_after();
         trace_max(a.trace, 6);
         if (rd == 0) AT_STAMP(6);
         for (int j = j0; j < j1; ++j) {
-          const int st = j % NST;
-          mbar_wait(&v_full[st], (j / NST) & 1);
+          const int st = j % RING;
+          mbar_wait(&v_full[st], (j / RING) & 1);
           tc_fence_after();
 #pragma unroll
           for (int kk = 0; kk < kKC / 16; ++kk) {
@@ -395,7 +411,9 @@ __global__ void __launch_bounds__(Soft<HD>::threads + 32, 1)
         umma_commit(o_full);
         if (rd + 1 < rounds) {  // ... and its V slots once its P V MMAs completed
           mbar_wait(o_full, rd & 1);
-          for (int j = j1; j < jn; ++j) load_v(j);
+          for (int j = Ly::dbl ? j0 + RING : j1; j < jn; ++j) load_v(j);
+          // non-dbl: round rd + 1's S (one S buffer: after round rd's softmax, i.e. after p_full above)
+          if (!Ly::dbl) s_mma(rd + 1);
         }
       }
       // the last round's MMAs complete before the softmax warps pass o_full, i.e. before the
@@ -422,9 +440,10 @@ __global__ void __launch_bounds__(Soft<HD>::threads + 32, 1)
         vis[i] = i >= nj ? 0u
                          : (kw + KP <= bs ? kpmask : (valid ? vis_word(kw, bs, bl, tok, a.mask_words, mrow) & kpmask : 0u));
       }
-      mbar_wait(s_full, rd & 1);
+      mbar_wait(&s_full[Ly::dbl ? (rd & 1) : 0], Ly::dbl ? (rd >> 1) & 1 : rd & 1);
       tc_fence_after();
       if (threadIdx.x == 0 && rd == 0) AT_STAMP(12);
+      const uint32_t tSr = tS + (Ly::dbl ? (rd & 1) * NST * kKC : 0);  // this round's S buffer
       // pass 1: the row max over this thread's visible scores; pass 2 (after the two column halves
       // exchange their maxima): P = 2^(s - max) into the UMMA A operand
       bool full[NST];  // warp-uniform: every row of the warp sees all 32 keys (committed prefix)
@@ -435,8 +454,8 @@ __global__ void __launch_bounds__(Soft<HD>::threads + 32, 1)
       for (int i = 0; i < NST; ++i) {
         if (i < nj) {
           float v[KP];
-          if constexpr (KP == 32) tmem_ld32(tS + lane_base + i * kKC + part * KP, v);
-          else tmem_ld16(tS + lane_base + i * kKC + part * KP, v);
+          if constexpr (KP == 32) tmem_ld32(tSr + lane_base + i * kKC + part * KP, v);
+          else tmem_ld16(tSr + lane_base + i * kKC + part * KP, v);
           if (full[i]) {
 #pragma unroll
             for (int j = 0; j < KP; ++j) mx = fmaxf(mx, v[j]);
@@ -459,8 +478,8 @@ __global__ void __launch_bounds__(Soft<HD>::threads + 32, 1)
       for (int i = 0; i < NST; ++i) {
         if (i < nj) {
           float v[KP];
-          if constexpr (KP == 32) tmem_ld32(tS + lane_base + i * kKC + part * KP, v);
-          else tmem_ld16(tS + lane_base + i * kKC + part * KP, v);
+          if constexpr (KP == 32) tmem_ld32(tSr + lane_base + i * kKC + part * KP, v);
+          else tmem_ld16(tSr + lane_base + i * kKC + part * KP, v);
           if (full[i]) {
 #pragma unroll
             for (int j = 0; j < KP; ++j) {
@@ -531,6 +550,45 @@ __global__ void __launch_bounds__(Soft<HD>::threads + 32, 1)
 #pragma unroll
   for (int pp = 1; pp < NP; ++pp) ltot += red_l[pp * kRows + row];
   const float inv = ltot > 0.f ? 1.f / ltot : 0.f;
+  if constexpr (Ly::dbl) {
+    // single-CTA tile (no key split): O / l straight from TMEM to the bf16 output, no merge
+    if (rounds == 1) {
+      mbar_wait(o_full, 0);
+      tc_fence_after();
+    }
+    uint32_t ob[32];
+    if (rounds > 0) {
+      tmem_ld32_issue((rounds > 1 ? tAcc : tO) + lane_base + part * CP, ob);
+      tmem_wait_ld();
+      regs_after_wait(ob);
+    } else {
+#pragma unroll
+      for (int i = 0; i < 32; ++i) ob[i] = 0u;
+    }
+    if (valid) {
+      const int l32 = row & 31;
+      const int tok = t0 + (row >> 5) * a.tq + (l32 >> a.lg);
+      const int head = kvh * a.G + (l32 & (a.G - 1));
+      __nv_bfloat16* dst = a.out + (static_cast<size_t>(r * a.T + tok) * a.Hq + head) * HD + part * CP;
+#pragma unroll
+      for (int u = 0; u < 32; u += 8) {
+        uint4 ov;
+        ov.x = pack2(__uint_as_float(ob[u]) * inv, __uint_as_float(ob[u + 1]) * inv);
+        ov.y = pack2(__uint_as_float(ob[u + 2]) * inv, __uint_as_float(ob[u + 3]) * inv);
+        ov.z = pack2(__uint_as_float(ob[u + 4]) * inv, __uint_as_float(ob[u + 5]) * inv);
+        ov.w = pack2(__uint_as_float(ob[u + 6]) * inv, __uint_as_float(ob[u + 7]) * inv);
+        *reinterpret_cast<uint4*>(dst + u) = ov;
+      }
+    }
+    tc_fence_before();
+    __syncthreads();  // pairs with the TMA / MMA warp's: every TMEM read is done
+    if (threadIdx.x == 0) {
+      trace_max(a.trace, 2);
+      AT_STAMP(10);
+    }
+    if (a.late_trigger) pdl_launch_dependents();
+    return;
+  }
   const int lsh = 7 - a.lc;  // log2(lanes_per)
   const int d = row >> lsh, ll = row & (lanes_per - 1);
   const uint32_t rbar = mapa_shared(smem_u32(recv_bar), d);
@@ -663,7 +721,7 @@ static const Plan* plan_of(const void* p) {
 }
 
 // Instantiations: (hd, chunks per round).
-#define YGG_AT_KERNELS(X) X(64, 4) X(128, 3)
+#define YGG_AT_KERNELS(X) X(64, 4, 4) X(128, 3, 3) X(128, 2, 4)
 
 }  // namespace at
 }  // namespace ygg
@@ -674,12 +732,12 @@ using namespace ygg::at;
 extern "C" {
 
 int ygg_prepare_attn_tree(void) {
-#define YGG_AT_ATTR(H, N)                                                                                   \
+#define YGG_AT_ATTR(H, N, R)                                                                                \
   {                                                                                                         \
-    cudaError_t e = cudaFuncSetAttribute(attn_tree_kernel<H, N>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                                         static_cast<int>(Layout<H, N>::bytes + 1024));                     \
+    cudaError_t e = cudaFuncSetAttribute(attn_tree_kernel<H, N, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                         static_cast<int>(Layout<H, N, R>::bytes + 1024));                  \
     if (e != cudaSuccess) return ygg_fail(YGG_ERR_CUDA, "tree attention attribute: %s", cudaGetErrorString(e)); \
-    e = cudaFuncSetAttribute(attn_tree_kernel<H, N>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);      \
+    e = cudaFuncSetAttribute(attn_tree_kernel<H, N, R>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);   \
     if (e != cudaSuccess) return ygg_fail(YGG_ERR_CUDA, "tree attention cluster attribute: %s", cudaGetErrorString(e)); \
   }
   YGG_AT_KERNELS(YGG_AT_ATTR)
@@ -731,9 +789,23 @@ int ygg_attn_tree_plan_init(void* plan, const void* q, const void* cache_layer, 
   // Dependent launch triggered at each CTA's end: the next GEMM's early CTAs otherwise slow this
   // kernel's softmax by ~1.8 us per cfg2 verify layer for no gain of their own (in-graph A/B).
   p->late_trigger = 1;
-  p->nst = hd == 128 ? 3 : 4;
-  p->smem = hd == 128 ? Layout<128, 3>::bytes + 1024 : Layout<64, 4>::bytes + 1024;
-  p->tcols = hd == 128 ? Layout<128, 3>::tcols : Layout<64, 4>::tcols;
+  // Round shape: clusters (short contexts, keys split over the cluster: ~one round per CTA) take 3-chunk
+  // rounds at hd 128; single-CTA hd-128 tiles (batched verifies, prefill chunks: many rounds over long
+  // contexts) take 2-chunk rounds over a 4-stage ring with S double-buffered in TMEM.
+  if (hd == 128 && cs == 1) {
+    p->nst = 2;
+    p->ring = 4;
+    p->smem = Layout<128, 2, 4>::bytes + 1024;
+    p->tcols = Layout<128, 2, 4>::tcols;
+  } else if (hd == 128) {
+    p->nst = p->ring = 3;
+    p->smem = Layout<128, 3, 3>::bytes + 1024;
+    p->tcols = Layout<128, 3, 3>::tcols;
+  } else {
+    p->nst = p->ring = 4;
+    p->smem = Layout<64, 4, 4>::bytes + 1024;
+    p->tcols = Layout<64, 4, 4>::tcols;
+  }
   const int M = B * T;
   {  // q [M][Hq][hd]: box {64, G, tq} -> one lane quarter of (token, head-in-group) rows
     cuuint64_t dims[3] = {static_cast<cuuint64_t>(hd), static_cast<cuuint64_t>(Hq), static_cast<cuuint64_t>(M)};
@@ -824,9 +896,9 @@ int ygg_attn_tree_run(const void* plan, const int32_t* blk_start, const int32_t*
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   const dim3 grid(p->csplit, p->row_tiles, p->Hkv * p->B), block(p->hd == 128 ? Soft<128>::threads + 32
                                                                                   : Soft<64>::threads + 32);
-#define YGG_AT_LAUNCH(H, N)                                                                                        \
-  if (p->hd == H && p->nst == N)                                                                                   \
-    return launch_pdl_cluster_x(attn_tree_kernel<H, N>, grid, block, p->smem, p->csplit, s, p->tqm, p->tk, p->tv, a);
+#define YGG_AT_LAUNCH(H, N, R)                                                                                     \
+  if (p->hd == H && p->nst == N && p->ring == R)                                                                   \
+    return launch_pdl_cluster_x(attn_tree_kernel<H, N, R>, grid, block, p->smem, p->csplit, s, p->tqm, p->tk, p->tv, a);
   YGG_AT_KERNELS(YGG_AT_LAUNCH)
 #undef YGG_AT_LAUNCH
   return ygg_fail(YGG_ERR_VALUE, "tree attention: no kernel for hd %d", p->hd);

@@ -358,3 +358,78 @@ def test_cfg2_draft_prefill_fused_layout_vs_oracle(pair, cuda, fused_gemm):
         vg = cache[li, 0, 1].float().cpu().reshape(dc.n_kv_heads, dc.head_dim, S)[:, :, :n].transpose(1, 2)
         assert _rel_err(kg, rc.k[li][:, :n]) <= 2e-2
         assert _rel_err(vg, rc.v[li][:, :n]) <= 2e-2
+
+
+def test_cfg5_dims_batched_verify_vs_oracle(cuda):
+    """The batched verify at the cfg5 target's dimensions (Llama-3-70B: d 8192, 64 query / 8 kv heads,
+    ffn 28672, V 128256; 2 layers): two requests, each verifying 65 rows (the bonus + the first 64
+    nodes of a D8 W16 k16 EGT: 3 mask words, 8 query heads per kv head on the tree attention's
+    single-CTA long-context path) against the fp32 oracle within 2e-2; argmax equal where the margin
+    allows."""
+    from oracle.llama_ref import RefCache, RefLlama, causal_visible
+    from paper_2512_23858_b200.forward import Forward, new_cache, prefill_causal
+    from paper_2512_23858_b200.model import Coupling, init_weights, preset, weights_to
+
+    tc = preset("llama3-70b", n_layers=2)
+    w32 = init_weights(tc, 7, torch.float32, "cpu", Coupling(**COUPLING))
+    w16 = weights_to(weights_to(w32, "cpu", torch.bfloat16), "cpu", torch.float32)
+    del w32
+    B, P = 2, 192
+    S = 512
+    rng = np.random.default_rng(11)
+    prompts = torch.randint(0, tc.vocab, (B, P), generator=torch.Generator().manual_seed(77))
+    trees = []
+    for b in range(B):
+        full = _egt_tree(rng, 8, 16, 16, tc.vocab)  # 129 nodes; nodes are added level by level,
+        trees.append(full)                          # so the first 64 form a connected subtree
+    n_nodes = 64
+    T_rows = n_nodes + 1
+    mw = (T_rows + 31) // 32
+    w = weights_to(w16, cuda, torch.bfloat16)
+    cache = new_cache(tc, B, S, torch.bfloat16, cuda)
+    prefill_causal(tc, w, cache, prompts.to(cuda, torch.int32), torch.bfloat16, False)
+    f = Forward(tc, w, cache, B, T_rows, mw, torch.bfloat16)
+    assert not f.gemv and f.at_plans is not None
+    tokens, pos, slots, masks, bonuses = [], [], [], [], []
+    for b, tree in enumerate(trees):
+        bonus = int(rng.integers(tc.vocab))
+        bonuses.append(bonus)
+        tokens += [bonus] + tree.token[:n_nodes]
+        pos += [P] + [P + 1 + d for d in tree.depth[:n_nodes]]
+        slots += [P + i for i in range(T_rows)]
+        masks.append(1)
+        for i in range(n_nodes):
+            m = 1
+            for a in tree.path(i):
+                m |= 1 << (1 + a)
+            masks.append(m)
+    f.tokens.copy_(torch.tensor(tokens, dtype=torch.int32))
+    f.pos.copy_(torch.tensor(pos, dtype=torch.int32))
+    f.slot.copy_(torch.tensor(slots, dtype=torch.int32))
+    words = [[(m >> (32 * k)) & 0xFFFFFFFF for k in range(mw)] for m in masks]
+    f.qmask.copy_(torch.tensor(words, dtype=torch.int64).to(torch.int32))
+    f.blk_start.fill_(P)
+    f.blk_len.fill_(T_rows)
+    f.run()
+    torch.cuda.synchronize()
+    got = f.logits.cpu().view(B, T_rows, -1)
+    ref = RefLlama(tc, w16)
+    for b in range(B):
+        rc = RefCache(tc, S)
+        pp = list(range(P))
+        ref.forward(rc, prompts[b].tolist(), pp, pp, causal_visible(P, S))
+        vis = torch.zeros(T_rows, S, dtype=torch.bool)
+        vis[:, :P] = True
+        for r, m in enumerate(masks[b * T_rows:(b + 1) * T_rows]):
+            for j in range(T_rows):
+                if (m >> j) & 1:
+                    vis[r, P + j] = True
+        want = ref.forward(rc, tokens[b * T_rows:(b + 1) * T_rows], pos[b * T_rows:(b + 1) * T_rows],
+                           slots[b * T_rows:(b + 1) * T_rows], vis)
+        err = _rel_err(got[b], want)
+        assert err <= 2e-2, (b, err)
+        row_err = (got[b] - want).abs().max(1).values
+        top2 = want.topk(2, dim=1).values
+        clear = (top2[:, 0] - top2[:, 1]) > 2 * row_err
+        assert int(clear.sum()) >= T_rows // 2
+        assert torch.equal(got[b].argmax(1)[clear], want.argmax(1)[clear])

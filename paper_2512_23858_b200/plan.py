@@ -12,6 +12,8 @@ target sizes:
   draft O GEMV        -> the next quarter of gate|up       (16 MB: 0.625 -> 0.615 ms)
   draft attention     -> the first 3/8 of down             (12 MB of 32: 0.634 -> 0.627 ms)
   verify attention    -> the first tenth of gate|up        (24 MB of 235: verify 3.578 -> 3.464 ms)
+                         + the first quarter of O            (8 MB of 34: 4-14 us per verify in five
+                                                              same-box A/Bs, scripts/verify_plan_ab.py)
 A kernel that pulls more than it leaves idle slows itself as much as the next kernel gains, so every
 region is also capped at a quarter of the L2 (31.5 MB on B200).
 """
@@ -75,7 +77,7 @@ class ForwardPlan:
     draft_qkv_l2: tuple = (L2Prefetch("wgu", 0.25),)
     draft_o_l2: tuple = (L2Prefetch("wgu", 0.25, 0.25),)
     draft_attn_l2: tuple = (L2Prefetch("wdown", 0.375),)
-    verify_attn_l2: tuple = (L2Prefetch("wgu", 0.1),)
+    verify_attn_l2: tuple = (L2Prefetch("wgu", 0.1), L2Prefetch("wo", 0.25))
     # (GEMM, region) pairs: the separate epilogue kernel of that GEMM (verify / prefill passes) pulls the
     # region into L2 after its dependency wait (csrc/gemm.cu epi_l2_prefetch)
     verify_epi_l2: tuple = ()

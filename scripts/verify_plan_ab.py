@@ -16,9 +16,10 @@ from paper_2512_23858_b200.plan import ForwardPlan, L2Prefetch  # noqa: E402
 
 VARIANTS = {
     "default": ForwardPlan(),
-    "attn_gu_0.15": ForwardPlan(verify_attn_l2=(L2Prefetch("wgu", 0.15),)),
-    "attn_gu_0.2": ForwardPlan(verify_attn_l2=(L2Prefetch("wgu", 0.2),)),
-    "attn_gu_0.05": ForwardPlan(verify_attn_l2=(L2Prefetch("wgu", 0.05),)),
+    "csplit2": ForwardPlan(tree_csplit=2),
+    "csplit1": ForwardPlan(tree_csplit=1),
+    "rowtiles4": ForwardPlan(tree_row_tiles=4),
+    "rowtiles4_cs2": ForwardPlan(tree_row_tiles=4, tree_csplit=2),
     "attn_gu_0.1_o": ForwardPlan(verify_attn_l2=(L2Prefetch("wgu", 0.1), L2Prefetch("wo", 0.25))),
 }
 

@@ -25,9 +25,11 @@ torch.cuda.synchronize()
 f = sd.verify if which == "verify" else sd.draft
 graphs = {}
 for v in variants:
-    plan = bench.plan_from_args([x for x in v.split(",") if x])
+    items = [x for x in v.split(",") if x]
+    ctas = [int(x.split("=")[1]) for x in items if x.startswith("ctas=")]  # GEMM CTA count override
+    plan = bench.plan_from_args([x for x in items if not x.startswith("ctas=")])
     g = Forward(f.cfg, f.w, f.cache, f.B, f.R, f.mask_words, f.act_dtype, plan=plan,
-                lm_argmax=getattr(f, "lm_argmax", False))
+                lm_argmax=getattr(f, "lm_argmax", False), num_ctas=ctas[0] if ctas else 0)
     for t in ("tokens", "pos", "slot", "req", "qmask", "blk_start", "blk_len"):
         getattr(g, t).copy_(getattr(f, t))
     cg = torch.cuda.CUDAGraph()

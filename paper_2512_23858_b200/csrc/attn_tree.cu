@@ -550,8 +550,9 @@ __global__ void __launch_bounds__(Soft<HD>::threads + 32, 1)
 #pragma unroll
   for (int pp = 1; pp < NP; ++pp) ltot += red_l[pp * kRows + row];
   const float inv = ltot > 0.f ? 1.f / ltot : 0.f;
-  if constexpr (Ly::dbl) {
-    // single-CTA tile (no key split): O / l straight from TMEM to the bf16 output, no merge
+  if (Ly::dbl || C == 1) {
+    // single-CTA tile (no key split): O / l straight from TMEM to the bf16 output, no merge (st.async
+    // needs a cluster of at least two CTAs)
     if (rounds == 1) {
       mbar_wait(o_full, 0);
       tc_fence_after();

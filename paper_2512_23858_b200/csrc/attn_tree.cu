@@ -534,9 +534,15 @@ __global__ void __launch_bounds__(Soft<HD>::threads + 32, 1)
     if (threadIdx.x == 0) trace_max(a.trace, 3);
     if (threadIdx.x == 0) AT_STAMP(7);
   }
+  // "Every TMEM read of the CTA is done": named barrier 1 — the softmax warps arrive (bar.arrive, they
+  // need not wait) once their last TMEM read is done, the TMA / MMA warp syncs on it before the dealloc.
+  auto tmem_done = [&]() {
+    __syncwarp();  // reconverge the warp (its threads may come from divergent branches)
+    asm volatile("bar.arrive 1, %0;" ::"r"(kSoftThreads + 32) : "memory");
+  };
   if (warp == kSoftWarps) {  // the TMA / MMA warp: release TMEM once every TMEM read of the CTA is done
     tc_fence_before();
-    __syncthreads();
+    asm volatile("bar.sync 1, %0;" ::"r"(kSoftThreads + 32) : "memory");
     tc_fence_after();
     tmem_dealloc(tmem, Ly::tcols);
     if (a.late_trigger) pdl_launch_dependents();
@@ -582,7 +588,7 @@ __global__ void __launch_bounds__(Soft<HD>::threads + 32, 1)
       }
     }
     tc_fence_before();
-    __syncthreads();  // pairs with the TMA / MMA warp's: every TMEM read is done
+    tmem_done();  // pairs with the TMA / MMA warp's: every TMEM read is done
     if (threadIdx.x == 0) {
       trace_max(a.trace, 2);
       AT_STAMP(10);
@@ -623,7 +629,7 @@ __global__ void __launch_bounds__(Soft<HD>::threads + 32, 1)
     st_async_v2(mapa_shared(smem_u32(recv_ml + static_cast<size_t>(ks * lanes_per + ll) * 2), d), __float_as_uint(M),
                 __float_as_uint(ltot), rbar);
   tc_fence_before();
-  __syncthreads();  // pairs with the TMA / MMA warp's: every TMEM read is done
+  tmem_done();  // pairs with the TMA / MMA warp's: every TMEM read is done
   if (threadIdx.x == 0) AT_STAMP(8);
   // ===== owner: rows [ks * lanes_per, (ks + 1) * lanes_per): kSoftThreads / lanes_per threads per row, 8-column
   // units, the C partials combined in fixed rank order

@@ -610,6 +610,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  // first cluster-barrier phase: "this CTA has started"; waited on just before the DSMEM scatter
+  asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
   const uint32_t tmem_base = *tmem_slot;
   if (threadIdx.x == 0) trace_min(e.trace, 0);
   pdl_launch_dependents();
@@ -686,6 +688,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   const uint32_t taddr = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16);
   const int valid = min(BN, p.M - m_tile * BN);
   const int nchunks = (valid + 15) / 16;  // chunks holding at least one real token
+  // every CTA of the cluster has started (arrived right after its set-up) before any DSMEM store
+  asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
   if (warp >= 2) {
     mbar_wait(&tfull[0], 0);
     tc_fence_after();

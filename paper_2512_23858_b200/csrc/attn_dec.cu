@@ -163,7 +163,11 @@ __global__ void __launch_bounds__(32 * (1 + kMaxWarps), 1)
       mbar_init(&empty[s], nw);
     }
     mbar_init(qbar, 1);
-    mbar_init(cbar, (a.kvsplit - 1) * a.warps);  // one arrival per compute warp of the other CTAs
+    // the leader's merge barrier completes on the transaction bytes of the other CTAs' st.async pushes:
+    // (kvsplit - 1) CTAs x warps x 32 lanes x (NPW n-tiles + the (m, l) quad) x 16 B
+    mbar_init(cbar, 1);
+    if (a.kvsplit > 1 && ks2 == 0)
+      mbar_arrive_expect_tx(cbar, static_cast<uint32_t>((a.kvsplit - 1) * a.warps * 32 * ((HD / 8) / KS + 1) * 16));
     fence_barrier_init();
     trace_min(a.trace, 0);
   }
@@ -450,18 +454,17 @@ __global__ void __launch_bounds__(32 * (1 + kMaxWarps), 1)
     if (ks2 != 0) {
       const uint32_t rslot = mapa_shared(
           smem_u32(slots) + static_cast<uint32_t>((((ks2 - 1) * a.warps + cwi) * NV2) * 32 + lane * 4) * 4u, 0);
+      const uint32_t rbar = mapa_shared(smem_u32(cbar), 0);
+      // asynchronous DSMEM stores that complete their bytes on the leader's barrier (no fence, no arrival)
 #pragma unroll
-      for (int n = 0; n < NPW; ++n) st_cluster_v4(rslot + n * 512u, O[n][0], O[n][1], O[n][2], O[n][3]);
-      st_cluster_v4(rslot + NPW * 512u, Ma, Mb, La, Lb);
-      // every lane's stores happen-before lane 0's cluster-scope release arrival
-      __syncwarp();
-      if (lane == 0) {
-        fence_cluster();
-        mbar_arrive_cluster(mapa_shared(smem_u32(cbar), 0));
-      }
+      for (int n = 0; n < NPW; ++n)
+        st_async_v4(rslot + n * 512u, __float_as_uint(O[n][0]), __float_as_uint(O[n][1]), __float_as_uint(O[n][2]),
+                    __float_as_uint(O[n][3]), rbar);
+      st_async_v4(rslot + NPW * 512u, __float_as_uint(Ma), __float_as_uint(Mb), __float_as_uint(La),
+                  __float_as_uint(Lb), rbar);
       return;
     }
-    mbar_wait_cluster(cbar, 0);
+    mbar_wait(cbar, 0);
     const float* b0 = slots + static_cast<size_t>(cwi * NV2) * 32 + lane * 4;
     const int kstride = a.warps * NV2 * 32;
     constexpr int KV = HD == 128 ? 4 : 8;  // cluster-size cap (plan_init clamps kvsplit to it)

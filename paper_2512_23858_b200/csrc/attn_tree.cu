@@ -101,18 +101,6 @@ YGG_DEV uint32_t pack2(float lo, float hi) {
 YGG_DEV void sts128(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
   asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
 }
-// Asynchronous DSMEM store into CTA-of-cluster address `addr` that completes `bytes` on the mbarrier
-// at cluster address `bar` (its owner's barrier): no fence, no arrival, ordering through the tx count.
-YGG_DEV void st_async_v4(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d, uint32_t bar) {
-  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.b32 [%0], {%1, %2, %3, %4}, [%5];" ::"r"(addr),
-               "r"(a), "r"(b), "r"(c), "r"(d), "r"(bar)
-               : "memory");
-}
-YGG_DEV void st_async_v2(uint32_t addr, uint32_t a, uint32_t b, uint32_t bar) {
-  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.b32 [%0], {%1, %2}, [%3];" ::"r"(addr), "r"(a),
-               "r"(b), "r"(bar)
-               : "memory");
-}
 YGG_DEV uint32_t pack_h2(float lo, float hi) {
   __half2 v = __floats2half2_rn(lo, hi);
   return *reinterpret_cast<uint32_t*>(&v);

@@ -136,6 +136,18 @@ YGG_DEV void st_cluster_v4(uint32_t addr, float a, float b, float c, float d) {
   asm volatile("st.shared::cluster.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "f"(a), "f"(b), "f"(c), "f"(d)
                : "memory");
 }
+// Asynchronous DSMEM store into CTA-of-cluster address `addr` that completes `bytes` on the mbarrier
+// at cluster address `bar` (its owner's barrier): no fence, no arrival, ordering through the tx count.
+YGG_DEV void st_async_v4(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d, uint32_t bar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.b32 [%0], {%1, %2, %3, %4}, [%5];" ::"r"(addr),
+               "r"(a), "r"(b), "r"(c), "r"(d), "r"(bar)
+               : "memory");
+}
+YGG_DEV void st_async_v2(uint32_t addr, uint32_t a, uint32_t b, uint32_t bar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.b32 [%0], {%1, %2}, [%3];" ::"r"(addr), "r"(a),
+               "r"(b), "r"(bar)
+               : "memory");
+}
 YGG_DEV void fence_cluster() { asm volatile("fence.acq_rel.cluster;" ::: "memory"); }
 YGG_DEV void mbar_arrive_cluster(uint32_t remote_bar) {  // release: this thread's DSMEM stores first
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote_bar) : "memory");

@@ -35,7 +35,7 @@ for _ in range(2):
     sd.step(use_graph=False)
 torch.cuda.synchronize()
 res = {}
-DRAFT = [(0, 0, 0), (1, 8, 0), (1, 4, 0), (1, 16, 0), (2, 8, 0), (2, 4, 2), (4, 4, 2)]
+DRAFT = [(0, 0, 0)]
 for name, f, variants in (("draft", sd.draft, DRAFT),):
     for kv, st, ksp in variants:  # (kvsplit, stages, in-CTA key-split groups); 0 = automatic
         g = Forward(f.cfg, f.w, f.cache, f.B, f.R, f.mask_words, f.act_dtype, gemv=f.gemv,

@@ -13,4 +13,6 @@ timeout 600 ncu $R --set full --import-source on -k regex:attn_tree --launch-ski
   python scripts/profile_step.py cfg2 1 > /dev/null 2>&1
 timeout 600 ncu $R --set full --import-source on -k regex:gemm_bf16_tc --launch-skip 2 -c 1 -o gpurun_out/${TAG}_gemm_gu -f \
   python scripts/profile_step.py cfg2 1 > /dev/null 2>&1
+timeout 600 ncu $R --set full --import-source on -k regex:attn_dec --launch-skip 16 -c 1 -o gpurun_out/${TAG}_attn_dec -f \
+  python scripts/profile_step.py cfg2 1 > /dev/null 2>&1
 ls -la gpurun_out/${TAG}_*

@@ -27,6 +27,22 @@ constexpr int kTopkThreads = 256;
 using TopkChunkOut = TopkPartial;
 
 YGG_DEV bool better(float va, int ta, float vb, int tb) { return topk_better(va, ta, vb, tb); }
+YGG_DEV unsigned long long topk_key(float v, int tok) {  // larger key == better (v desc, tok asc)
+  const uint32_t b = __float_as_uint(v + 0.0f);  // -0 -> +0: equal values order by token, like better()
+  const uint32_t ord = (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+  return (static_cast<unsigned long long>(ord) << 32) | static_cast<uint32_t>(~static_cast<uint32_t>(tok));
+}
+YGG_DEV float key_val(unsigned long long key) {
+  const uint32_t ord = static_cast<uint32_t>(key >> 32);
+  return __uint_as_float((ord & 0x80000000u) ? (ord & 0x7fffffffu) : ~ord);
+}
+YGG_DEV int key_tok(unsigned long long key) { return static_cast<int>(~static_cast<uint32_t>(key)); }
+constexpr unsigned long long kNoKey = 0ull;  // below every real key (even -inf with token 2^31 - 1)
+YGG_DEV unsigned long long warp_max_key(unsigned long long key) {
+  const uint32_t hi = __reduce_max_sync(0xffffffffu, static_cast<uint32_t>(key >> 32));
+  const uint32_t lo = __reduce_max_sync(0xffffffffu, static_cast<uint32_t>(key >> 32) == hi ? static_cast<uint32_t>(key) : 0u);
+  return (static_cast<unsigned long long>(hi) << 32) | lo;
+}
 
 template <typename T>
 __global__ void __launch_bounds__(kTopkThreads) topk_phase1(const T* __restrict__ logits, int V, int ld, int k,
@@ -64,33 +80,54 @@ __global__ void __launch_bounds__(kTopkThreads) topk_phase1(const T* __restrict_
     o->max_s = cmax;
     o->sum_exp = tot;
   }
-  // k rounds of block arg-best with removal.
-  for (int r = 0; r < k; ++r) {
-    float bv = -INFINITY;
-    int bt = 0x7fffffff;
-    for (int i = begin + threadIdx.x; i < end; i += blockDim.x) {
-      float v = sv[i - begin];
-      if (!isnan(v) && better(v, i, bv, bt)) { bv = v; bt = i; }
-    }
+  // Top-k of the chunk by a tournament over 64-bit keys ordered exactly like better() (logit desc,
+  // token asc; NaN excluded): every thread keeps its 16 elements as keys and its current best; each
+  // warp pops its k best with two redux.sync max reductions per round (only the popping lane rescans
+  // its 16), then warp 0 pops the chunk's k best over the 8 warps' lists.
+  constexpr int kPer = kTopkChunk / kTopkThreads;
+  constexpr int NW = kTopkThreads / 32;
+  __shared__ unsigned long long wsel[NW][kTopkMaxK];
+  unsigned long long mk[kPer];
 #pragma unroll
-    for (int off = 16; off > 0; off >>= 1) {
-      float ov = __shfl_xor_sync(0xffffffffu, bv, off);
-      int ot = __shfl_xor_sync(0xffffffffu, bt, off);
-      if (better(ov, ot, bv, bt)) { bv = ov; bt = ot; }
+  for (int j = 0; j < kPer; ++j) {
+    const int i = begin + threadIdx.x + j * kTopkThreads;
+    const float v = i < end ? sv[i - begin] : __int_as_float(0x7fc00000);
+    mk[j] = isnan(v) ? kNoKey : topk_key(v, i);
+  }
+  uint32_t taken = 0u;
+  auto best_left = [&]() {
+    unsigned long long b = kNoKey;
+#pragma unroll
+    for (int j = 0; j < kPer; ++j)
+      if (!((taken >> j) & 1u) && mk[j] > b) b = mk[j];
+    return b;
+  };
+  unsigned long long cur = best_left();
+  for (int r = 0; r < k; ++r) {
+    const unsigned long long win = warp_max_key(cur);
+    if (lane == 0) wsel[warp][r] = win;
+    if (win != kNoKey && cur == win) {  // keys are unique (distinct indices): exactly one lane pops
+#pragma unroll
+      for (int j = 0; j < kPer; ++j)
+        if (mk[j] == win) taken |= 1u << j;
+      cur = best_left();
     }
-    __syncthreads();
-    if (lane == 0) { red_f[warp] = bv; red_i[warp] = bt; }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      float fv = red_f[0];
-      int ft = red_i[0];
-      for (int w = 1; w < kTopkThreads / 32; ++w)
-        if (better(red_f[w], red_i[w], fv, ft)) { fv = red_f[w]; ft = red_i[w]; }
-      o->val[r] = fv;
-      o->tok[r] = (ft == 0x7fffffff) ? -1 : ft;
-      if (ft != 0x7fffffff) sv[ft - begin] = __int_as_float(0x7fc00000);  // NaN marks taken
+  }
+  __syncthreads();
+  if (warp == 0) {
+    int hp = 0;
+    unsigned long long ck = lane < NW ? wsel[lane][0] : kNoKey;
+    for (int r = 0; r < k; ++r) {
+      const unsigned long long win = warp_max_key(ck);
+      if (lane == 0) {
+        o->val[r] = win == kNoKey ? -INFINITY : key_val(win);
+        o->tok[r] = win == kNoKey ? -1 : key_tok(win);
+      }
+      if (win != kNoKey && ck == win) {
+        ++hp;
+        ck = hp < k ? wsel[lane][hp] : kNoKey;
+      }
     }
-    __syncthreads();
   }
   pdl_launch_dependents();
 }
@@ -175,22 +212,6 @@ __global__ void __launch_bounds__(kTopkThreads) topk_phase2(const TopkChunkOut* 
 // asc), so a tournament round is two redux.sync max reductions instead of a shuffle tree: each warp
 // pops its k best over its chunk heads, then warp 0 pops the block's k best over the warps' lists.
 constexpr int kMergeOwn = 2;
-YGG_DEV unsigned long long topk_key(float v, int tok) {  // larger key == better (v desc, tok asc)
-  const uint32_t b = __float_as_uint(v + 0.0f);  // -0 -> +0: equal values order by token, like better()
-  const uint32_t ord = (b & 0x80000000u) ? ~b : (b | 0x80000000u);
-  return (static_cast<unsigned long long>(ord) << 32) | static_cast<uint32_t>(~static_cast<uint32_t>(tok));
-}
-YGG_DEV float key_val(unsigned long long key) {
-  const uint32_t ord = static_cast<uint32_t>(key >> 32);
-  return __uint_as_float((ord & 0x80000000u) ? (ord & 0x7fffffffu) : ~ord);
-}
-YGG_DEV int key_tok(unsigned long long key) { return static_cast<int>(~static_cast<uint32_t>(key)); }
-constexpr unsigned long long kNoKey = 0ull;  // below every real key (even -inf with token 2^31 - 1)
-YGG_DEV unsigned long long warp_max_key(unsigned long long key) {
-  const uint32_t hi = __reduce_max_sync(0xffffffffu, static_cast<uint32_t>(key >> 32));
-  const uint32_t lo = __reduce_max_sync(0xffffffffu, static_cast<uint32_t>(key >> 32) == hi ? static_cast<uint32_t>(key) : 0u);
-  return (static_cast<unsigned long long>(hi) << 32) | lo;
-}
 
 struct L2Regions {  // weights of the next pass to pull into L2 while the merge / grow leave HBM idle
   const char* ptr[4];

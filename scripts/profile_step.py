@@ -5,7 +5,8 @@ sys.path.insert(0, ".")
 import bench  # noqa: E402
 from paper_2512_23858_b200 import _lib as L  # noqa: E402
 
-wl = bench.WORKLOADS[sys.argv[1] if len(sys.argv) > 1 else "cfg2"]
+wl = dict(bench.WORKLOADS[sys.argv[1] if len(sys.argv) > 1 else "cfg2"])
+wl.setdefault("batch", wl.get("global_batch", 1))
 n_steps = int(sys.argv[2]) if len(sys.argv) > 2 else 2
 sd, tc, dc = bench.build_decoder(wl, sys.argv[1] if len(sys.argv) > 1 else "cfg2", torch.device("cuda"))
 prompts = bench.prompts_for(wl, tc.vocab, 0)

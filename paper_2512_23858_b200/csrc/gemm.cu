@@ -157,7 +157,7 @@ YGG_DEV void epi_apply(const EpiArgs& e, int M, int n, int m0, int valid16, floa
     int pos[16], req[16], slot[16];
 #pragma unroll
     for (int j = 0; j < 16; ++j) {
-      const int m = m0 + (j < valid16 ? j : 0);
+      const int m = min(m0 + j, M - 1);  // chunks past M (valid16 <= 0) still run: clamp their loads
       pos[j] = __ldg(e.pos + m);
       req[j] = __ldg(e.req + m);
       slot[j] = __ldg(e.slot + m);

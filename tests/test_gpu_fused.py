@@ -21,7 +21,10 @@ def _plan(W, X, M, ctas):
 
     if isinstance(ctas, str):
         p = GemmPlan(W, X, M, 0)
-        L.check(L.lib().ygg_gemm_plan_set_cluster(p.handle, int(ctas[1:])))
+        rc = L.lib().ygg_gemm_plan_set_cluster(p.handle, int(ctas[1:]))
+        if rc == L.YGG_ERR_UNSUPPORTED:  # more tiles than co-resident clusters (wide token counts)
+            pytest.skip("cluster shape does not fit one wave")
+        L.check(rc)
         assert L.lib().ygg_gemm_plan_cluster(p.handle) == int(ctas[1:])
         return p
     return GemmPlan(W, X, M, ctas)
@@ -48,7 +51,7 @@ def _epi(kind, counters, **kw):
 
 
 @pytest.mark.parametrize("ctas", [0, 5, 37, "c1", "c2", "c3", "c4"])
-@pytest.mark.parametrize("M", [8, 50, 300])
+@pytest.mark.parametrize("M", [8, 50, 300, 800])
 def test_store_f32_with_rstd(ctas, M, cuda):
     from paper_2512_23858_b200 import _lib as L
 
@@ -77,12 +80,13 @@ def test_store_f32_with_rstd(ctas, M, cuda):
     assert torch.equal(out, first)
 
 
+@pytest.mark.parametrize("M", [40, 800])
 @pytest.mark.parametrize("ctas", [0, 11, "c2", "c4"])
-def test_resid_and_swiglu(ctas, cuda):
+def test_resid_and_swiglu(ctas, M, cuda):
     from paper_2512_23858_b200 import _lib as L
     from paper_2512_23858_b200.model import gate_up_interleave, preset
 
-    M, d, F = 40, 512, 768
+    d, F = 512, 768
     g = torch.Generator(device="cuda").manual_seed(len(str(ctas)) + 3)
     # RESID: resid += X W^T, hb = bf16(resid), ss per 128-feature tile
     X = torch.randn(M, F, device=cuda, generator=g).to(torch.bfloat16)
@@ -113,29 +117,37 @@ def test_resid_and_swiglu(ctas, cuda):
     assert (act.double() - ref2).abs().max() <= 1e-2 * ref2.abs().max()
 
 
+@pytest.mark.parametrize("M", [12, 800])
 @pytest.mark.parametrize("hd,Hq,Hkv", [(64, 4, 2), (128, 8, 2)])
 @pytest.mark.parametrize("ctas", [0, 9, "c3", "c4"])
-def test_qkv_rope_kv_append(hd, Hq, Hkv, ctas, cuda):
+def test_qkv_rope_kv_append(hd, Hq, Hkv, ctas, M, cuda):
     from oracle.llama_ref import rope
     from paper_2512_23858_b200 import _lib as L
-    from paper_2512_23858_b200.model import preset, qkv_row_permutation
+    from paper_2512_23858_b200.model import preset, qkv_row_permutation, rope_table
 
-    M, d, S, B = 12, 256, 64, 2
+    d, B = 256, 2
+    S = 64 if M < 100 else 512
     cfg = preset("tiny-target", d_model=d, n_heads=Hq, n_kv_heads=Hkv, head_dim=hd)
     g = torch.Generator(device="cuda").manual_seed(hd + len(str(ctas)))
     X = torch.randn(M, d, device=cuda, generator=g).to(torch.bfloat16)
     W = (torch.randn(cfg.qkv_dim, d, device=cuda, generator=g) / math.sqrt(d)).to(torch.bfloat16)
     Wp = W[qkv_row_permutation(cfg).to(cuda)].contiguous()
-    pos = torch.randint(0, 1000, (M,), device=cuda, dtype=torch.int32)
-    slot = torch.arange(M, device=cuda, dtype=torch.int32) % (M // B) + 5
-    req = torch.arange(M, device=cuda, dtype=torch.int32) // (M // B)
+    # token metadata as views whose tails are poisoned: a load past row M - 1 (the token tile's rows
+    # beyond M) would index the RoPE table / cache far out of bounds and fault
+    pos = torch.full((M + 64,), 1 << 30, device=cuda, dtype=torch.int32)[:M]
+    pos.copy_(torch.randint(0, 1000, (M,), device=cuda, dtype=torch.int32))
+    slot = torch.full((M + 64,), 1 << 30, device=cuda, dtype=torch.int32)[:M]
+    slot.copy_(torch.arange(M, device=cuda, dtype=torch.int32) % (M // B) + 5)
+    req = torch.full((M + 64,), 1 << 20, device=cuda, dtype=torch.int32)[:M]
+    req.copy_(torch.arange(M, device=cuda, dtype=torch.int32) // (M // B))
+    rope_cs = rope_table(cfg, 1000, cuda) if M >= 100 else None  # the table path (Forward's) and sincos
     q = torch.zeros(M, Hq, hd, dtype=torch.bfloat16, device=cuda)
     cache = torch.zeros(B, 2, Hkv, S, hd, dtype=torch.bfloat16, device=cuda)
     plan = _plan(Wp, X, M, ctas)
     cnt = torch.zeros(plan.tiles, dtype=torch.int32, device=cuda)
     _run(plan, _epi(L.YGG_EPI_QKV_ROPE, cnt, q_out=q.data_ptr(), cache=cache.data_ptr(), S=S, Hq=Hq, Hkv=Hkv,
                     hd=hd, rope_theta=cfg.rope_theta, pos=pos.data_ptr(), slot=slot.data_ptr(),
-                    req=req.data_ptr()), cuda)
+                    req=req.data_ptr(), rope_cs=0 if rope_cs is None else rope_cs.data_ptr()), cuda)
     y = (X.double() @ W.double().T).float().cpu()
     qr = rope(y[:, : Hq * hd].view(M, Hq, hd), pos.cpu(), cfg.rope_theta)
     kr = rope(y[:, Hq * hd : (Hq + Hkv) * hd].view(M, Hkv, hd), pos.cpu(), cfg.rope_theta)

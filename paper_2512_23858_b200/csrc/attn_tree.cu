@@ -11,8 +11,9 @@
 //   softmax warps  (Soft<HD>::warps: 16 at hd 128, 8 at hd 64) one thread per (row, 64/NP-key slice of a
 //                  chunk): tcgen05.ld S, ancestor /
 //                  prefix mask from the row's tree-mask bits, round max, exp2, bf16 P -> smem
-//                  (128B-swizzled, the UMMA A operand), then O (read back from TMEM) accumulated in
-//                  registers with the online-softmax rescale across rounds.
+//                  (128B-swizzled, the UMMA A operand).  Long contexts (single-CTA tiles): O accumulates
+//                  in TMEM across rounds, rescaled (in TMEM) only when a row's max grows by more than 2^8
+//                  over its reference; cluster tiles fold each round's O into an accumulator instead.
 // Merge without a combine launch: every CTA pushes each row's unnormalised O and (max, sum) into the
 // shared memory of the cluster CTA that owns the row (DSMEM stores + a release arrival on the
 // owner's mbarrier); owners merge the C partials in fixed rank order (deterministic) and store bf16.
@@ -34,7 +35,7 @@ namespace at {
 constexpr int kKC = 64;                  // keys per chunk
 constexpr int kRows = 128;               // UMMA M = TMEM lanes
 // Softmax warps: NP per TMEM lane quarter, each taking a 64 / NP-key slice of every chunk (and HD / NP
-// output columns in the O fold / push).  hd 128: 16 warps (4 per quarter), which halves the per-thread
+// output columns in the O rescale / push).  hd 128: 16 warps (4 per quarter), which halves the per-thread
 // exp2 / TMEM-load work of a round against 8 (the long-context rounds are softmax-bound); hd 64: 8.
 template <int HD>
 struct Soft {
@@ -43,7 +44,7 @@ struct Soft {
   static constexpr int threads = 32 * warps;
   static constexpr int KP = kKC / NP;   // keys per thread per chunk (16 or 32)
   static constexpr int CP = HD / NP;    // O columns per thread (32)
-  static_assert(CP == 32, "the O fold / push move 32 TMEM columns per thread");
+  static_assert(CP == 32, "the O rescale / push move 32 TMEM columns per thread");
 };
 constexpr int kMaxThreads = 32 * 16 + 32;
 constexpr uint32_t kMagic = 0x59475454u;     // "YGTT"
@@ -201,12 +202,16 @@ struct Layout {
   static constexpr int RS = HD + 8;
   static constexpr uint32_t off_recv = off_p + NST * p_bytes;
   static constexpr uint32_t off_ml = off_recv + (dbl ? 0 : kRows * RS * 2);  // f32 [C][128 / C][2] (max, sum)
-  static constexpr uint32_t off_red = off_ml + kRows * 8;           // f32 [NP][128] slice maxima, [NP][128] sums
-  static constexpr uint32_t off_bar = off_red + 2 * Soft<HD>::NP * kRows * 4;  // k_full[RING], v_full[RING], q, s[2], p, o, recv
+  // f32 [2][NP][128] slice maxima (by round parity: a thread may start round r + 1 while a slower one of
+  // its quarter still reads round r's), [NP][128] sums
+  static constexpr uint32_t off_red = off_ml + kRows * 8;
+  static constexpr uint32_t off_bar = off_red + 3 * Soft<HD>::NP * kRows * 4;  // k_full[RING], v_full[RING], q, s[2], p, o, recv
   static constexpr uint32_t bytes = off_bar + (2 * RING + 6) * 8 + 16;
   static constexpr int s_cols = (dbl ? 2 : 1) * NST * kKC;  // S of one round (two buffers when dbl)
-  static constexpr int tcols = (s_cols + 2 * HD) <= 256 ? 256 : 512;  // + O of a round + O accumulated
-  static_assert(s_cols + 2 * HD <= 512, "TMEM budget");
+  // + O: accumulated across rounds in TMEM (dbl), or a round's O + the accumulator it is folded into
+  static constexpr int o_cols = (dbl ? 1 : 2) * HD;
+  static constexpr int tcols = (s_cols + o_cols) <= 256 ? 256 : 512;
+  static_assert(s_cols + o_cols <= 512, "TMEM budget");
 };
 
 template <int HD, int NST, int RING>
@@ -217,6 +222,7 @@ __global__ void __launch_bounds__(Soft<HD>::threads + 32, 1)
   constexpr int kSoftWarps = Soft<HD>::warps, kSoftThreads = Soft<HD>::threads;
   constexpr int NP = Soft<HD>::NP, KP = Soft<HD>::KP, CP = Soft<HD>::CP;
   constexpr uint32_t kpmask = KP == 32 ? 0xffffffffu : ((1u << KP) - 1u);
+  constexpr bool kHold = NST * KP <= 32;  // a round's scores stay in registers between the two passes
   constexpr int DCH = Ly::DCH;
   constexpr int RS = Ly::RS;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
@@ -281,7 +287,7 @@ __global__ void __launch_bounds__(Soft<HD>::threads + 32, 1)
   tc_fence_after();
   if (threadIdx.x == 0) AT_STAMP(1);
   const uint32_t tmem = *tmem_slot;
-  const uint32_t tS = tmem, tO = tmem + Ly::s_cols, tAcc = tO + HD;
+  const uint32_t tS = tmem, tO = tmem + Ly::s_cols, tAcc = Ly::dbl ? tO : tO + HD;
   // Block bounds were written at least two kernels back (the kernel just before this one triggers
   // its dependents only after its own dependency wait): read them before the wait.
   const int bs = __ldg(a.blk_start + r), bl = __ldg(a.blk_len + r);
@@ -393,7 +399,7 @@ __global__ void __launch_bounds__(Soft<HD>::threads + 32, 1)
           for (int kk = 0; kk < kKC / 16; ++kk) {
             const uint64_t ad = umma_desc_sw128(smem_u32(sp + (j - j0) * Ly::p_bytes) + kk * 32);
             const uint64_t bd = umma_desc_sw128(smem_u32(sv + st * Ly::v_bytes) + kk * 32);
-            umma_bf16(tO, ad, bd, id_o, (j > j0 || kk > 0) ? 1u : 0u);
+            umma_bf16(tO, ad, bd, id_o, ((Ly::dbl && rd > 0) || j > j0 || kk > 0) ? 1u : 0u);
           }
         }
         umma_commit(o_full);
@@ -431,6 +437,111 @@ __global__ void __launch_bounds__(Soft<HD>::threads + 32, 1)
       mbar_wait(&s_full[Ly::dbl ? (rd & 1) : 0], Ly::dbl ? (rd >> 1) & 1 : rd & 1);
       tc_fence_after();
       if (threadIdx.x == 0 && rd == 0) AT_STAMP(12);
+      if constexpr (Ly::dbl) {
+      // ---- long contexts: O accumulates in TMEM with the lazy rescale
+      const uint32_t tSr = tS + (Ly::dbl ? (rd & 1) * NST * kKC : 0);  // this round's S buffer
+      // pass 1: the row max over this thread's visible scores (S kept in registers); pass 2 (after the
+      // column slices exchange their maxima): P = 2^(s - ref) into the UMMA A operand
+      bool full[NST];  // warp-uniform: every row of the warp sees all 32 keys (committed prefix)
+#pragma unroll
+      for (int i = 0; i < NST; ++i) full[i] = __all_sync(0xffffffffu, vis[i] == kpmask);
+      float v[NST][KP];
+      float mx = -INFINITY;
+#pragma unroll
+      for (int i = 0; i < NST; ++i) {
+        if (i < nj) {
+          if constexpr (KP == 32) tmem_ld32(tSr + lane_base + i * kKC + part * KP, v[i]);
+          else tmem_ld16(tSr + lane_base + i * kKC + part * KP, v[i]);
+          if (full[i]) {
+#pragma unroll
+            for (int j = 0; j < KP; ++j) mx = fmaxf(mx, v[i][j]);
+          } else {
+#pragma unroll
+            for (int j = 0; j < KP; ++j)
+              if ((vis[i] >> j) & 1u) mx = fmaxf(mx, v[i][j]);
+          }
+        }
+      }
+      float* redm = red + (rd & 1) * NP * kRows;
+      redm[part * kRows + row] = mx;
+      asm volatile("bar.sync %0, %1;" ::"r"(2 + q), "r"(32 * NP) : "memory");  // the NP warps of this quarter
+      mx = redm[row];
+#pragma unroll
+      for (int pp = 1; pp < NP; ++pp) mx = fmaxf(mx, redm[pp * kRows + row]);
+      // Lazy rescale: the reference max moves only when the row max grows by more than 2^8 (P <= 256 in
+      // bf16 / f32 is exact enough and cannot overflow), so most rounds leave the TMEM accumulator alone.
+      // The decision is the row's own (its NP threads compute the same values): rows stay independent.
+      const float mnew = fmaxf(M, mx * sl);  // log2 units (scale > 0 commutes with the max)
+      float alpha = 1.f;
+      if (mnew > M + 8.f) {
+        alpha = ex2(M - mnew);  // 0 when M = -inf
+        M = mnew;
+      }
+      const float ref = M == -INFINITY ? 0.f : M;
+      // The previous round's P V has read its P slots and accumulated: P and the accumulator are free.
+      // Short rounds (NST x KP <= 32 scores per thread) keep the exponentials in registers and wait only
+      // before the P stores; longer ones wait first and reload S chunk by chunk (register budget).
+      auto prev_pv_done = [&]() {
+        if (rd == 0) return;
+        mbar_wait(o_full, (rd - 1) & 1);
+        tc_fence_after();
+        if (__any_sync(0xffffffffu, alpha != 1.f)) {  // warp-collective TMEM access; other rows scale by 1
+          uint32_t ab[32];
+          tmem_ld32_issue(tAcc + lane_base + part * CP, ab);
+          tmem_wait_ld();
+          regs_after_wait(ab);
+#pragma unroll
+          for (int c = 0; c < 32; ++c) ab[c] = __float_as_uint(__uint_as_float(ab[c]) * alpha);
+          tmem_st32(tAcc + lane_base + part * CP, ab);
+          tmem_wait_st();
+        }
+      };
+      auto store_p = [&](int i) {
+        const uint32_t rb = smem_u32(sp + i * Ly::p_bytes + row * 128);
+#pragma unroll
+        for (int u = 0; u < KP / 8; ++u)
+          sts128(rb + (((part * (KP / 8) + u) ^ (row & 7)) << 4), pack2(v[i][8 * u], v[i][8 * u + 1]),
+                 pack2(v[i][8 * u + 2], v[i][8 * u + 3]), pack2(v[i][8 * u + 4], v[i][8 * u + 5]),
+                 pack2(v[i][8 * u + 6], v[i][8 * u + 7]));
+      };
+      if constexpr (!kHold) prev_pv_done();
+      float sum = 0.f;
+#pragma unroll
+      for (int i = 0; i < NST; ++i) {
+        if (i < nj) {
+          if constexpr (!kHold) {
+            if constexpr (KP == 32) tmem_ld32(tSr + lane_base + i * kKC + part * KP, v[i]);
+            else tmem_ld16(tSr + lane_base + i * kKC + part * KP, v[i]);
+          }
+          if (full[i]) {
+#pragma unroll
+            for (int j = 0; j < KP; ++j) {
+              v[i][j] = ex2(fmaf(v[i][j], sl, -ref));
+              sum += v[i][j];
+            }
+          } else {
+#pragma unroll
+            for (int j = 0; j < KP; ++j) {
+              v[i][j] = ((vis[i] >> j) & 1u) ? ex2(fmaf(v[i][j], sl, -ref)) : 0.f;
+              sum += v[i][j];
+            }
+          }
+          if constexpr (!kHold) store_p(i);
+        }
+      }
+      if constexpr (kHold) {
+        prev_pv_done();
+#pragma unroll
+        for (int i = 0; i < NST; ++i)
+          if (i < nj) store_p(i);
+      }
+      fence_proxy_async();
+      tc_fence_before();
+      mbar_arrive(p_full);
+      l = l * alpha + sum;
+      } else {
+      // ---- cluster tiles (~one round per CTA): O of each round folded into the accumulator columns
+      // (measured faster here than the TMEM accumulation: cfg2 verify 3.450 vs 3.456 ms)
       const uint32_t tSr = tS + (Ly::dbl ? (rd & 1) * NST * kKC : 0);  // this round's S buffer
       // pass 1: the row max over this thread's visible scores; pass 2 (after the two column halves
       // exchange their maxima): P = 2^(s - max) into the UMMA A operand
@@ -518,6 +629,7 @@ __global__ void __launch_bounds__(Soft<HD>::threads + 32, 1)
         }
         tmem_wait_st();
       }
+      }
     }
     if (threadIdx.x == 0) trace_max(a.trace, 3);
     if (threadIdx.x == 0) AT_STAMP(7);
@@ -537,7 +649,7 @@ __global__ void __launch_bounds__(Soft<HD>::threads + 32, 1)
     return;
   }
   // ===== push this row's partial to the rank owning the row: O / l in f16 and (max, l) =====
-  float* red_l = red + NP * kRows;
+  float* red_l = red + 2 * NP * kRows;
   red_l[part * kRows + row] = l;
   asm volatile("bar.sync %0, %1;" ::"r"(2 + q), "r"(32 * NP) : "memory");
   float ltot = red_l[row];
@@ -547,13 +659,15 @@ __global__ void __launch_bounds__(Soft<HD>::threads + 32, 1)
   if (Ly::dbl || C == 1) {
     // single-CTA tile (no key split): O / l straight from TMEM to the bf16 output, no merge (st.async
     // needs a cluster of at least two CTAs)
-    if (rounds == 1) {
-      mbar_wait(o_full, 0);
+    // the last round's P V (completions are in order: earlier phases are done); without dbl, rounds > 1
+    // were waited for by the fold
+    if (Ly::dbl ? rounds > 0 : rounds == 1) {
+      mbar_wait(o_full, (rounds - 1) & 1);
       tc_fence_after();
     }
     uint32_t ob[32];
     if (rounds > 0) {
-      tmem_ld32_issue((rounds > 1 ? tAcc : tO) + lane_base + part * CP, ob);
+      tmem_ld32_issue((Ly::dbl || rounds > 1 ? tAcc : tO) + lane_base + part * CP, ob);
       tmem_wait_ld();
       regs_after_wait(ob);
     } else {
@@ -588,11 +702,11 @@ __global__ void __launch_bounds__(Soft<HD>::threads + 32, 1)
   const int d = row >> lsh, ll = row & (lanes_per - 1);
   const uint32_t rbar = mapa_shared(smem_u32(recv_bar), d);
   const uint32_t ro = mapa_shared(smem_u32(recv_o + (static_cast<size_t>(ks * lanes_per + ll) * RS + part * CP)), d);
-  if (rounds == 1) {
-    mbar_wait(o_full, 0);
+  if (Ly::dbl ? rounds > 0 : rounds == 1) {
+    mbar_wait(o_full, (rounds - 1) & 1);
     tc_fence_after();
   }
-  const uint32_t tsrc = (rounds > 1 ? tAcc : tO) + lane_base + part * CP;
+  const uint32_t tsrc = (Ly::dbl || rounds > 1 ? tAcc : tO) + lane_base + part * CP;
 #pragma unroll
   for (int c = 0; c < CP; c += 32) {
     uint32_t ob[32];

@@ -1032,38 +1032,77 @@ __global__ void __launch_bounds__(1024) epi_residual_norm_kernel(EpiGeom g, cons
   if (threadIdx.x == 0) trace_max(g.trace, 2);
 }
 
-template <typename ActT>
+// R tokens per thread (R > 1 for wide passes: fewer, fuller CTAs, R tokens' loads in flight together).
+template <typename ActT, int R>
 __global__ void __launch_bounds__(kEpiThreads) epi_swiglu_kernel(EpiGeom g, const float* __restrict__ ws,
                                                                  ActT* __restrict__ out) {
   if (threadIdx.x == 0) trace_min(g.trace, 0);
-  const int m = blockIdx.y;
+  const int m0 = blockIdx.y * R;
   const int F = g.N / 2;
   const int f = (blockIdx.x * blockDim.x + threadIdx.x) * 8;
   // fused layout: gate j / up j are rows 2j / 2j + 1, so this thread's 16 rows start at 2f (one tile)
   const int na = g.il ? 2 * f : f, nb = g.il ? 2 * f + 8 : F + f;
-  const int2 sa = f < F ? epi_segs(g, m, na) : make_int2(0, 0), sb = f < F ? epi_segs(g, m, nb) : make_int2(0, 0);
+  int2 sa[R], sb[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const bool ok = f < F && m0 + r < g.M;
+    sa[r] = ok ? epi_segs(g, m0 + r, na) : make_int2(0, 0);
+    sb[r] = ok ? epi_segs(g, m0 + r, nb) : make_int2(0, 0);
+  }
   pdl_wait();
   pdl_launch_dependents();
   epi_l2_prefetch(g);
   if (threadIdx.x == 0) trace_min(g.trace, 1);
   if (f >= F) return;
-  float gate[8], up[8], o[8];
-  if (g.il) {
-    float a[8], b[8];
-    epi_values2<8>(g, ws, m, na, nb, a, b, sa, sb);
+  float a[R][8], b[R][8];
+  bool single = true;  // every run of this thread's tokens lies in a whole (one-segment) tile
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      gate[i] = a[2 * i];
-      up[i] = a[2 * i + 1];
-      gate[4 + i] = b[2 * i];
-      up[4 + i] = b[2 * i + 1];
+  for (int r = 0; r < R; ++r) single = single && sa[r].y - sa[r].x <= 1 && sb[r].y - sb[r].x <= 1;
+  if (single) {
+    const size_t seg_stride = static_cast<size_t>(g.BN) * kBM;
+    float4 xa[R][2], xb[R][2];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const size_t row = static_cast<size_t>((m0 + r) % g.BN) * kBM;
+      const float4* qa = reinterpret_cast<const float4*>(ws + sa[r].x * seg_stride + row + (na % kBM));
+      const float4* qb = reinterpret_cast<const float4*>(ws + sb[r].x * seg_stride + row + (nb % kBM));
+      const bool ok = sa[r].y > sa[r].x;
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        xa[r][i] = ok ? __ldcg(qa + i) : make_float4(0.f, 0.f, 0.f, 0.f);
+        xb[r][i] = ok ? __ldcg(qb + i) : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
     }
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        a[r][4 * i] = xa[r][i].x; a[r][4 * i + 1] = xa[r][i].y; a[r][4 * i + 2] = xa[r][i].z; a[r][4 * i + 3] = xa[r][i].w;
+        b[r][4 * i] = xb[r][i].x; b[r][4 * i + 1] = xb[r][i].y; b[r][4 * i + 2] = xb[r][i].z; b[r][4 * i + 3] = xb[r][i].w;
+      }
   } else {
-    epi_values2<8>(g, ws, m, f, F + f, gate, up, sa, sb);
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+      if (m0 + r < g.M) epi_values2<8>(g, ws, m0 + r, na, nb, a[r], b[r], sa[r], sb[r]);
   }
 #pragma unroll
-  for (int i = 0; i < 8; ++i) o[i] = gate[i] / (1.f + expf(-gate[i])) * up[i];
-  store8<ActT>(out + static_cast<size_t>(m) * F + f, o);
+  for (int r = 0; r < R; ++r) {
+    if (m0 + r >= g.M) break;
+    float gate[8], up[8], o[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      if (g.il) {
+        gate[i] = i < 4 ? a[r][2 * i] : b[r][2 * (i - 4)];
+        up[i] = i < 4 ? a[r][2 * i + 1] : b[r][2 * (i - 4) + 1];
+      } else {
+        gate[i] = a[r][i];
+        up[i] = b[r][i];
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) o[i] = gate[i] / (1.f + expf(-gate[i])) * up[i];
+    store8<ActT>(out + static_cast<size_t>(m0 + r) * F + f, o);
+  }
   if (threadIdx.x == 0) trace_max(g.trace, 2);
 }
 
@@ -1618,11 +1657,14 @@ int ygg_epi_swiglu(const void* plan, const float* ws, void* out, int act_dtype, 
   YGG_CHECK_ARG(g->N % 2 == 0, "gate_up width must be even");
   EpiGeom geo = geom_of(g, 6);
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  dim3 grid((g->N / 2 + 1023) / 1024, g->M);
+  // Tokens per thread: 1.  (R = 4 at cfg4's 800 rows shortens this kernel 37.8 -> 34.5 us but delays the
+  // down GEMM's dependency release 11 -> 43 us: net slower, measured in-graph with scripts/draft_timeline.py.)
+  constexpr int R = 1;
+  dim3 grid((g->N / 2 + 1023) / 1024, (g->M + R - 1) / R);
   if (act_dtype == YGG_F32)
-    YGG_LAUNCH_PDL(epi_swiglu_kernel<float>, grid, dim3(kEpiThreads), 0, s, geo, ws, static_cast<float*>(out));
+    YGG_LAUNCH_PDL((epi_swiglu_kernel<float, R>), grid, dim3(kEpiThreads), 0, s, geo, ws, static_cast<float*>(out));
   else
-    YGG_LAUNCH_PDL(epi_swiglu_kernel<__nv_bfloat16>, grid, dim3(kEpiThreads), 0, s, geo, ws,
+    YGG_LAUNCH_PDL((epi_swiglu_kernel<__nv_bfloat16, R>), grid, dim3(kEpiThreads), 0, s, geo, ws,
                    static_cast<__nv_bfloat16*>(out));
   return YGG_OK;
 }

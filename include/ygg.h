@@ -184,7 +184,8 @@ typedef enum {
 
 /* Walk the tree from above the root; one uniform per visited group (uniforms [B, n_uniform]).
  * Target rows: row 0 = the confirmed/bonus token, row 1+i = tree node i (verify order).
- * row_argmax [B, rows] (GREEDY), logits [B*rows, ld] + row_stats [B*rows, 2] (SAMPLE).
+ * row_argmax [B, rows] (GREEDY), logits [B*rows, ld] + row_stats [B*rows, 2] (SAMPLE; row_stats may
+ * be NULL: the kernel then computes the log-sum-exp of the rows it walks itself).
  * Outputs: path [B, cap] (accepted node indices), path_len [B], accepted_len [B] = path_len+1,
  * bonus [B] (GREEDY/SAMPLE: next confirmed token), n_draws [B] uniforms consumed by the walk (or NULL). */
 int ygg_accept(ygg_tree tree, int mode, const double* probs, const double* uniforms, int n_uniform,

@@ -364,8 +364,19 @@ __global__ void __launch_bounds__(Soft<HD>::threads + 32, 1)
       if (rounds > 0) s_mma(0);
       for (int rd = 0; rd < rounds; ++rd) {
         const int j0 = rd * NST, j1 = min(n_my, j0 + NST);
-        // the other S buffer was last read by round rd - 1's softmax, which this warp saw finish (p_full)
-        if (Ly::dbl && rd + 1 < rounds) s_mma(rd + 1);
+        // this round's K slots are free once its S MMAs completed: refill them one ring ahead.  dbl: S(rd)
+        // was issued a round ago, so the refill goes out BEFORE waiting for round rd + 1's K (issued
+        // after it, the refill would keep only one round of K loads in flight: ncu showed the softmax
+        // warps ~30% stalled on S at cfg4)
+        const int jn = Ly::dbl ? min(n_my, j1 + RING) : min(n_my, j1 + NST);
+        if (Ly::dbl && rd + 1 < rounds) {
+          if (j0 + RING < jn) {
+            mbar_wait(&s_full[rd & 1], (rd >> 1) & 1);
+            for (int j = j0 + RING; j < jn; ++j) load_k(j);
+          }
+          // the other S buffer was last read by round rd - 1's softmax, which this warp saw finish (p_full)
+          s_mma(rd + 1);
+        }
         if (rd == 0) {
           // This CTA's own loads have landed: now the kernel barely touches HBM, so pull its share of a
           // later weight stream into L2 (issued earlier, the prefetch would queue ahead of the chunk loads).
@@ -381,11 +392,9 @@ __global__ void __launch_bounds__(Soft<HD>::threads + 32, 1)
             }
           }
         }
-        // this round's K slots are free once its S MMAs completed: refill them one ring ahead
-        const int jn = Ly::dbl ? min(n_my, j1 + RING) : min(n_my, j1 + NST);
-        if (rd + 1 < rounds) {
-          mbar_wait(&s_full[Ly::dbl ? (rd & 1) : 0], Ly::dbl ? (rd >> 1) & 1 : rd & 1);
-          for (int j = Ly::dbl ? j0 + RING : j1; j < jn; ++j) load_k(j);
+        if (!Ly::dbl && rd + 1 < rounds) {
+          mbar_wait(&s_full[0], rd & 1);
+          for (int j = j1; j < jn; ++j) load_k(j);
         }
         mbar_wait(p_full, rd & 1);
         tc_fence_after();

@@ -882,8 +882,89 @@ __global__ void subtree_kernel(ygg_tree in, ygg_tree out, const int32_t* __restr
 // ===========================================================================
 // K5: acceptance walk (acceptance.py:221-241) + greedy / sampled realisations.
 // ===========================================================================
-constexpr int kAcceptThreads = 256;
+constexpr int kAcceptThreads = 1024;
+constexpr int kAcceptWarps = kAcceptThreads / 32;
+constexpr int kAcceptSmemNodes = 256;  // trees up to this size are walked from shared memory
 
+// 4 consecutive logits as f32 (through L2: the LM head just wrote them)
+template <typename T>
+YGG_DEV void ld4(const T* p, float* o);
+template <>
+YGG_DEV void ld4<float>(const float* p, float* o) {
+  const float4 q = __ldcg(reinterpret_cast<const float4*>(p));
+  o[0] = q.x; o[1] = q.y; o[2] = q.z; o[3] = q.w;
+}
+template <>
+YGG_DEV void ld4<__nv_bfloat16>(const __nv_bfloat16* p, float* o) {
+  const uint2 u = __ldcg(reinterpret_cast<const uint2*>(p));
+  const __nv_bfloat162 a = *reinterpret_cast<const __nv_bfloat162*>(&u.x), b = *reinterpret_cast<const __nv_bfloat162*>(&u.y);
+  o[0] = __bfloat162float(a.x); o[1] = __bfloat162float(a.y); o[2] = __bfloat162float(b.x); o[3] = __bfloat162float(b.y);
+}
+constexpr int kAcceptUnroll = 8;  // 4-logit loads in flight per thread
+
+// log-sum-exp of row lr / T by the whole block (SAMPLE without precomputed row stats): f32 max, f32
+// per-thread sums of exp(x - max) combined in f64 in fixed order.  Every thread returns the value.
+// vec: 4-logit loads (V % 4 == 0, row 4-element aligned), kAcceptUnroll of them in flight per thread.
+template <typename T>
+YGG_DEV double block_row_lse(const T* __restrict__ lr, int V, float inv_temp, bool vec, float* redf, double* redd) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  float m = -INFINITY;
+  const int nq = V >> 2;
+  if (vec) {
+    for (int i = threadIdx.x; i < nq; i += kAcceptUnroll * kAcceptThreads) {
+      float q[kAcceptUnroll][4];
+#pragma unroll
+      for (int u = 0; u < kAcceptUnroll; ++u) {
+        const int j = i + u * kAcceptThreads;
+        if (j < nq) ld4(lr + 4 * j, q[u]);
+        else q[u][0] = q[u][1] = q[u][2] = q[u][3] = -INFINITY;
+      }
+#pragma unroll
+      for (int u = 0; u < kAcceptUnroll; ++u)
+#pragma unroll
+        for (int k = 0; k < 4; ++k) m = fmaxf(m, q[u][k] * inv_temp);
+    }
+  } else {
+    for (int v = threadIdx.x; v < V; v += kAcceptThreads) m = fmaxf(m, to_f32(lr[v]) * inv_temp);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if (lane == 0) redf[warp] = m;
+  __syncthreads();
+  float gm = redf[0];
+  for (int w = 1; w < kAcceptWarps; ++w) gm = fmaxf(gm, redf[w]);
+  float sf = 0.f;
+  if (vec) {
+    for (int i = threadIdx.x; i < nq; i += kAcceptUnroll * kAcceptThreads) {
+      float q[kAcceptUnroll][4];
+#pragma unroll
+      for (int u = 0; u < kAcceptUnroll; ++u) {
+        const int j = i + u * kAcceptThreads;
+        if (j < nq) ld4(lr + 4 * j, q[u]);
+        else q[u][0] = q[u][1] = q[u][2] = q[u][3] = -INFINITY;
+      }
+#pragma unroll
+      for (int u = 0; u < kAcceptUnroll; ++u)
+#pragma unroll
+        for (int k = 0; k < 4; ++k) sf += __expf(q[u][k] * inv_temp - gm);
+    }
+  } else {
+    for (int v = threadIdx.x; v < V; v += kAcceptThreads) sf += __expf(to_f32(lr[v]) * inv_temp - gm);
+  }
+  double sd = sf;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) sd += __shfl_xor_sync(0xffffffffu, sd, o);
+  if (lane == 0) redd[warp] = sd;
+  __syncthreads();
+  double tot = 0.0;
+  for (int w = 0; w < kAcceptWarps; ++w) tot += redd[w];
+  __syncthreads();  // redf / redd are reused by the next call
+  return static_cast<double>(gm) + log(tot);
+}
+
+// One block per request.  The walk (thread 0) follows acceptance.py:221-241; in SAMPLE mode without
+// row stats the block computes each walked row's log-sum-exp on demand (<= depth + 1 rows per request
+// instead of a stats pass over every verify row).
 template <typename T>
 __global__ void __launch_bounds__(kAcceptThreads) accept_kernel(
     ygg_tree t, int mode, const double* __restrict__ probs, const double* __restrict__ uniforms, int n_uniform,
@@ -895,54 +976,96 @@ __global__ void __launch_bounds__(kAcceptThreads) accept_kernel(
   const size_t tb = static_cast<size_t>(b) * t.cap;
   const int N = t.size[b];
   const int rows = t.cap + 1;  // verify rows per request: [confirmed, node 0, node 1, ...]
-  __shared__ int s_stop_row, s_len, s_excl[64], s_nexcl;
-  __shared__ double s_u2;
-  if (threadIdx.x == 0) {
-    int len = 0;
-    int cursor = -1;
-    int draw_i = 0;
-    int excl_n = 0;
-    while (true) {
+  const bool ondemand = mode == YGG_ACCEPT_SAMPLE && row_stats == nullptr;
+  // 4-logit vector loads: every row starts 4-element aligned
+  const bool vec = logits != nullptr && (V & 3) == 0 && (ld & 3) == 0 &&
+                   (reinterpret_cast<uintptr_t>(logits) & (4 * sizeof(T) - 1)) == 0;
+  __shared__ int s_have, s_took, s_prow, s_stop_row, s_lse_row, s_excl[64], s_nexcl, s_owner;
+  __shared__ double s_u2, s_lse;
+  __shared__ float s_redf[kAcceptWarps];
+  __shared__ double s_redd[kAcceptWarps], s_scan[kAcceptWarps];
+  auto lse_of = [&](int prow) -> double {  // thread 0 only
+    if (ondemand) return s_lse;
+    return row_stats ? static_cast<double>(row_stats[2 * (static_cast<size_t>(b) * rows + prow) + 1]) : 0.0;
+  };
+  int len = 0, cursor = -1, draw_i = 0, excl_n = 0;  // walk state (thread 0)
+  // the walk's node scans read the tree from shared memory (one coalesced load) instead of one
+  // dependent global load per node per visited group
+  __shared__ int32_t s_parent[kAcceptSmemNodes], s_token[kAcceptSmemNodes];
+  const bool smem_tree = N <= kAcceptSmemNodes;
+  if (smem_tree) {
+    for (int i = threadIdx.x; i < N; i += kAcceptThreads) {
+      s_parent[i] = t.parent[tb + i];
+      s_token[i] = t.token[tb + i];
+    }
+  }
+  const int32_t* parent = smem_tree ? s_parent : t.parent + tb;
+  const int32_t* token = smem_tree ? s_token : t.token + tb;
+  if (threadIdx.x == 0) s_lse_row = -1;
+  __syncthreads();
+  while (true) {
+    if (threadIdx.x == 0) {
       // group = [0] if cursor is None else children(cursor)
-      const int prow = cursor < 0 ? 0 : 1 + cursor;
-      int first = cursor < 0 ? 0 : cursor + 1;
+      const int first = cursor < 0 ? 0 : cursor + 1;
       bool any = false;
       for (int c = first; c < N; ++c) {
-        if (cursor < 0 ? c == 0 : t.parent[tb + c] == cursor) { any = true; break; }
+        if (cursor < 0 ? c == 0 : parent[c] == cursor) { any = true; break; }
       }
-      if (!any) break;
+      s_have = any;
+      s_prow = cursor < 0 ? 0 : 1 + cursor;
+    }
+    __syncthreads();
+    if (!s_have) break;
+    if (ondemand) {
+      const int prow = s_prow;
+      const double l = block_row_lse(logits + (static_cast<size_t>(b) * rows + prow) * ld, V, inv_temp, vec, s_redf, s_redd);
+      if (threadIdx.x == 0) {
+        s_lse = l;
+        s_lse_row = prow;
+      }
+    }
+    if (threadIdx.x == 0) {
+      const int prow = cursor < 0 ? 0 : 1 + cursor;
+      const int first = cursor < 0 ? 0 : cursor + 1;
       const double draw = (mode == YGG_ACCEPT_GREEDY) ? 0.5
                           : (draw_i < n_uniform ? uniforms[static_cast<size_t>(b) * n_uniform + draw_i] : 1.0);
       ++draw_i;
+      const double lse = mode == YGG_ACCEPT_SAMPLE ? lse_of(prow) : 0.0;
       double cumulative = 0.0;
       int chosen = -1;
       excl_n = 0;
       for (int c = first; c < N; ++c) {
-        if (!(cursor < 0 ? c == 0 : t.parent[tb + c] == cursor)) continue;
+        if (!(cursor < 0 ? c == 0 : parent[c] == cursor)) continue;
         double p;
         if (mode == YGG_ACCEPT_PROBS) {
           p = probs[tb + c];
         } else if (mode == YGG_ACCEPT_GREEDY) {
-          p = (t.token[tb + c] == row_argmax[static_cast<size_t>(b) * rows + prow]) ? 1.0 : 0.0;
+          p = (token[c] == row_argmax[static_cast<size_t>(b) * rows + prow]) ? 1.0 : 0.0;
         } else {
           const size_t r = static_cast<size_t>(b) * rows + prow;
-          const float l = to_f32(logits[r * ld + t.token[tb + c]]) * inv_temp;
-          p = exp(static_cast<double>(l) - static_cast<double>(row_stats[2 * r + 1]));
+          const float l = to_f32(logits[r * ld + token[c]]) * inv_temp;
+          p = exp(static_cast<double>(l) - lse);
         }
-        if (excl_n < 64) s_excl[excl_n++] = t.token[tb + c];
+        if (excl_n < 64) s_excl[excl_n++] = token[c];
         cumulative += p;
         if (draw < cumulative) { chosen = c; break; }
         if (cursor < 0) break;  // the root group has a single member
       }
-      if (chosen < 0) break;
-      path[tb + len++] = chosen;
-      cursor = chosen;
-      excl_n = 0;
+      if (chosen >= 0) {
+        path[tb + len++] = chosen;
+        cursor = chosen;
+        excl_n = 0;
+      }
+      s_took = chosen >= 0;
     }
-    s_len = len;
+    __syncthreads();
+    if (!s_took) break;
+  }
+  if (threadIdx.x == 0) {
     s_stop_row = (cursor < 0 ? 0 : 1 + cursor);
     s_nexcl = excl_n;
     s_u2 = (n_uniform > 0 && uniforms) ? uniforms[static_cast<size_t>(b) * n_uniform + (n_uniform - 1)] : 0.5;
+    s_owner = -1;
     path_len[b] = len;
     accepted_len[b] = len + 1;
     if (n_draws) n_draws[b] = draw_i;
@@ -952,65 +1075,129 @@ __global__ void __launch_bounds__(kAcceptThreads) accept_kernel(
   if (mode == YGG_ACCEPT_GREEDY) {
     if (threadIdx.x == 0 && bonus) bonus[b] = row_argmax[static_cast<size_t>(b) * rows + s_stop_row];
   } else if (mode == YGG_ACCEPT_SAMPLE && bonus) {
-    // Residual bonus: sample p(.|stop row) with the rejected children removed (inverse CDF in
-    // token order, block scan).  Together with the walk this emits exactly p(.|prefix).
-    const size_t r = static_cast<size_t>(b) * rows + s_stop_row;
-    const double lse = row_stats[2 * r + 1];
+    // Residual bonus: sample p(.|stop row) with the rejected children removed (inverse CDF in token
+    // order).  Together with the walk this emits exactly p(.|prefix).  Each warp owns a contiguous
+    // slice read in coalesced 4-token groups; the slice masses (f64 sums of the f32 exponentials) are
+    // scanned in fixed order, and the last warp whose slice starts at or below the target rescans its
+    // slice in token order (warp prefix sums, 128 tokens per step).
+    const int stop = s_stop_row;
+    const size_t r = static_cast<size_t>(b) * rows + stop;
+    double lse;
+    if (ondemand) {
+      if (s_lse_row == stop) {
+        lse = s_lse;  // written by thread 0 before the barrier above
+      } else {
+        lse = block_row_lse(logits + r * ld, V, inv_temp, vec, s_redf, s_redd);
+      }
+    } else {
+      lse = row_stats[2 * r + 1];
+    }
     const T* lr = logits + r * ld;
     const int nex = s_nexcl;
-    __shared__ double s_part[kAcceptThreads];
-    __shared__ double s_total;
-    // pass 1: per-thread contiguous slice masses
-    const int per = (V + blockDim.x - 1) / blockDim.x;
-    const int lo = threadIdx.x * per, hi = min(V, lo + per);
-    double mass = 0.0;
-    for (int v = lo; v < hi; ++v) {
-      bool ex = false;
-      for (int e = 0; e < nex; ++e) ex |= (s_excl[e] == v);
-      if (!ex) mass += exp(static_cast<double>(to_f32(lr[v]) * inv_temp) - lse);
-    }
-    s_part[threadIdx.x] = mass;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      double tot = 0.0;
-      for (int i = 0; i < (int)blockDim.x; ++i) tot += s_part[i];
-      s_total = tot;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      const double target = s_u2 * s_total;
-      double acc = 0.0;
-      int pick = -1;
-      int last_ok = -1;  // last non-excluded token with mass: the fallback never returns a rejected child
-      for (int i = 0; i < (int)blockDim.x && pick < 0; ++i) {
-        if (s_part[i] > 0.0) {
-          const int l2 = i * per, h2 = min(V, l2 + per);
-          if (acc + s_part[i] > target) {
-            const double slice_start = acc;
-            for (int v = l2; v < h2; ++v) {
-              bool ex = false;
-              for (int e = 0; e < nex; ++e) ex |= (s_excl[e] == v);
-              if (ex) continue;
-              const double pv = exp(static_cast<double>(to_f32(lr[v]) * inv_temp) - lse);
-              if (pv > 0.0) last_ok = v;
-              acc += pv;
-              if (acc > target) { pick = v; break; }
-            }
-            // re-accumulated slice fell a few ulps short of s_part: the slice's last valid token
-            if (pick < 0 && last_ok >= l2) pick = last_ok;
-            acc = slice_start + s_part[i];
-          } else {
-            acc += s_part[i];
-            for (int v = h2 - 1; v >= l2; --v) {  // remember this slice's last valid token
-              bool ex = false;
-              for (int e = 0; e < nex; ++e) ex |= (s_excl[e] == v);
-              if (!ex) { last_ok = v; break; }
-            }
-          }
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int nq = (V + 3) >> 2;                                  // 4-token groups
+    const int per_w = (nq + kAcceptWarps - 1) / kAcceptWarps;    // groups per warp slice (contiguous)
+    const int g0 = min(nq, warp * per_w), g1 = min(nq, g0 + per_w);
+    auto load_group = [&](int j, float* x) {
+      if (vec) {
+        ld4(lr + 4 * j, x);
+      } else {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) x[k] = 4 * j + k < V ? to_f32(lr[4 * j + k]) : 0.f;
+      }
+    };
+    // probabilities of group j's tokens (0: excluded or past the end)
+    auto group_probs = [&](int j, const float* x, double* p) {
+      unsigned ex = 0;
+      for (int e = 0; e < nex; ++e) {
+        const unsigned d = static_cast<unsigned>(s_excl[e] - 4 * j);
+        if (d < 4u) ex |= 1u << d;
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        p[k] = (4 * j + k < V && !((ex >> k) & 1u))
+                   ? static_cast<double>(__expf(static_cast<float>(static_cast<double>(x[k] * inv_temp) - lse)))
+                   : 0.0;
+    };
+    // pass 1: this warp's slice mass (coalesced groups, kAcceptUnroll loads in flight per lane)
+    double lm = 0.0;
+    for (int base = g0; base < g1; base += 32 * kAcceptUnroll) {
+      float x[kAcceptUnroll][4];
+#pragma unroll
+      for (int u = 0; u < kAcceptUnroll; ++u) {
+        const int j = base + u * 32 + lane;
+        if (j < g1) load_group(j, x[u]);
+      }
+#pragma unroll
+      for (int u = 0; u < kAcceptUnroll; ++u) {
+        const int j = base + u * 32 + lane;
+        if (j < g1) {
+          double p[4];
+          group_probs(j, x[u], p);
+          lm += (p[0] + p[1]) + (p[2] + p[3]);
         }
       }
-      if (pick < 0) pick = last_ok >= 0 ? last_ok : 0;
-      bonus[b] = pick;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) lm += __shfl_xor_sync(0xffffffffu, lm, o);
+    if (lane == 0) s_scan[warp] = lm;
+    __syncthreads();
+    double prefix = 0.0, total = 0.0;
+    for (int w = 0; w < kAcceptWarps; ++w) {
+      if (w < warp) prefix += s_scan[w];
+      total += s_scan[w];
+    }
+    const double target = s_u2 * total;
+    // the slice holding the target: the last one with mass that starts at or below it (fixed order)
+    if (lane == 0 && lm > 0.0 && prefix <= target) atomicMax(&s_owner, warp);
+    __syncthreads();
+    if (warp == s_owner) {
+      // pass 2 (one warp): token-order scan of the slice, 128 tokens per step
+      const double rest = target - prefix;
+      double acc = 0.0;
+      int pick = -1, last_ok = -1;
+      for (int base = g0; base < g1 && pick < 0; base += 32) {
+        const int j = base + lane;
+        float x[4] = {0.f, 0.f, 0.f, 0.f};
+        double p[4] = {0.0, 0.0, 0.0, 0.0};
+        if (j < g1) {
+          load_group(j, x);
+          group_probs(j, x, p);
+        }
+        const double ls = (p[0] + p[1]) + (p[2] + p[3]);
+        double incl = ls;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const double y = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= o) incl += y;
+        }
+        int lv = -1;  // this lane's last token with mass
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          if (p[k] > 0.0) lv = 4 * j + k;
+        const unsigned cross = __ballot_sync(0xffffffffu, acc + incl > rest);
+        if (cross) {
+          const int fl = __ffs(cross) - 1;
+          int pk = -1;
+          if (lane == fl) {
+            double a = acc + (incl - ls);
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              a += p[k];
+              if (pk < 0 && p[k] > 0.0 && a > rest) pk = 4 * j + k;
+            }
+            if (pk < 0) pk = lv;  // rounding at the group's end: its last token with mass
+          }
+          pick = __shfl_sync(0xffffffffu, pk, fl);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) lv = max(lv, __shfl_xor_sync(0xffffffffu, lv, o));
+        if (lv >= 0) last_ok = lv;
+        acc += __shfl_sync(0xffffffffu, incl, 31);
+      }
+      if (lane == 0) bonus[b] = pick >= 0 ? pick : last_ok;  // rounding at the slice's end: its last token
+    } else if (threadIdx.x == 0 && s_owner < 0) {
+      bonus[b] = 0;  // no mass anywhere (every token excluded or underflowed)
     }
   }
   pdl_launch_dependents();
@@ -1296,8 +1483,9 @@ int ygg_accept(ygg_tree tree, int mode, const double* probs, const double* unifo
   } else if (mode == YGG_ACCEPT_GREEDY) {
     YGG_CHECK_ARG(row_argmax != nullptr, "GREEDY mode needs row_argmax");
   } else if (mode == YGG_ACCEPT_SAMPLE) {
-    YGG_CHECK_ARG(logits && row_stats && uniforms && n_uniform >= 2 && temperature > 0.f && V >= 1 && ld >= V,
-                  "SAMPLE mode needs logits, row stats, uniforms");
+    // row_stats may be null: the kernel then computes the walked rows' log-sum-exp itself
+    YGG_CHECK_ARG(logits && uniforms && n_uniform >= 2 && temperature > 0.f && V >= 1 && ld >= V,
+                  "SAMPLE mode needs logits and uniforms");
   } else {
     return ygg_fail(YGG_ERR_VALUE, "unknown accept mode");
   }

@@ -421,6 +421,91 @@ def test_accept_probs_matches_oracle(seed, cuda):
         assert int(nd[b]) == used
 
 
+def _sample_oracle(t, lg, inv_t, uni):
+    """SAMPLE acceptance in f64 (acceptance.py:208-241 with p = softmax(logits / T) of the parent's
+    verify row): the walk, then the residual bonus by inverse CDF over the stop row with the rejected
+    group's tokens removed."""
+    x = lg.astype(np.float64) * inv_t
+    lse = x.max(1) + np.log(np.exp(x - x.max(1, keepdims=True)).sum(1))
+    path, cursor, used, excl = [], None, 0, []
+    while True:
+        group = [0] if cursor is None else t.children(cursor)
+        if not group:
+            excl = []
+            break
+        row = 0 if cursor is None else 1 + cursor
+        u = uni[used]
+        used += 1
+        acc, chosen, excl = 0.0, None, []
+        for c in group:
+            excl.append(t.token[c])
+            acc += float(np.exp(x[row, t.token[c]] - lse[row]))
+            if u < acc:
+                chosen = c
+                break
+        if chosen is None:
+            break
+        path.append(chosen)
+        cursor = chosen
+    stop = 0 if cursor is None else 1 + cursor
+    p = np.exp(x[stop] - lse[stop])
+    p[excl] = 0.0
+    cum = np.cumsum(p)
+    bonus = int(np.searchsorted(cum, uni[-1] * cum[-1], side="right"))
+    return path, used, bonus
+
+
+@pytest.mark.parametrize("with_stats", [False, True])
+def test_accept_sample_vs_oracle(with_stats, cuda):
+    """SAMPLE acceptance (tree walk with softmax(target / T) child probabilities + residual bonus) vs an
+    f64 restatement, with the per-row log-sum-exp computed by the accept kernel itself (the engine's
+    path) or passed in from ygg_row_stats.  The walk must match exactly; the residual draw inverts an
+    f32-exponential CDF, so a draw within ~1e-6 of a token boundary may land on the neighbour (<= 1 of
+    64 requests)."""
+    from paper_2512_23858_b200.device_tree import DeviceTrees
+
+    L = _lib()
+    rng = np.random.default_rng(11 + with_stats)
+    B, cap, V, nu, temp = 64, 48, 3000, 16, 0.7
+    trees = [_random_tree(rng, 45) for _ in range(B)]
+    dt = DeviceTrees(B, cap, cuda)
+    dt.load_host([t.to_dict() for t in trees])
+    rows = cap + 1
+    lg = rng.standard_normal((B, rows, V)).astype(np.float32) * 2.0
+    for b, t in enumerate(trees):  # make the walks go deep: each row favours one child of its node
+        lg[b, 0, t.token[0]] += 9.0
+        for n in range(len(t)):
+            ch = t.children(n)
+            if ch:
+                lg[b, 1 + n, t.token[ch[int(rng.integers(0, len(ch)))]]] += float(rng.uniform(6.0, 10.0))
+    uni = rng.random((B, nu))
+    logits = torch.from_numpy(lg.reshape(B * rows, V)).to(cuda)
+    uni_d = torch.from_numpy(uni).to(cuda)
+    i32 = dict(dtype=torch.int32, device=cuda)
+    path, plen, alen, bonus, nd = (torch.zeros(B, cap, **i32), torch.zeros(B, **i32), torch.zeros(B, **i32),
+                                   torch.zeros(B, **i32), torch.zeros(B, **i32))
+    stats = None
+    if with_stats:
+        stats = torch.zeros(B * rows, 2, device=cuda)
+        am = torch.zeros(B * rows, **i32)
+        L.check(L.lib().ygg_row_stats(logits.data_ptr(), L.YGG_F32, B * rows, V, V, temp, am.data_ptr(),
+                                      stats.data_ptr(), L.stream_ptr()))
+    L.check(L.lib().ygg_accept(dt.struct, L.YGG_ACCEPT_SAMPLE, None, uni_d.data_ptr(), nu, None, logits.data_ptr(),
+                               L.YGG_F32, V, V, None if stats is None else stats.data_ptr(), temp, path.data_ptr(),
+                               plen.data_ptr(), alen.data_ptr(), bonus.data_ptr(), nd.data_ptr(), L.stream_ptr()))
+    torch.cuda.synchronize()
+    miss = 0
+    deep = 0
+    for b, t in enumerate(trees):
+        rp, used, rb = _sample_oracle(t, lg[b], 1.0 / temp, uni[b])
+        assert path[b, : int(plen[b])].tolist() == rp, b
+        assert int(alen[b]) == len(rp) + 1 and int(nd[b]) == used
+        deep += len(rp) >= 2
+        miss += int(bonus[b]) != rb
+    assert miss <= 1
+    assert deep >= B // 4  # the planted preferences make many walks accept several nodes
+
+
 def test_accept_greedy_and_kv_compact(cuda):
     from paper_2512_23858_b200.device_tree import DeviceTrees
 

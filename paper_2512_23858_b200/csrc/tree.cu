@@ -55,11 +55,21 @@ __global__ void __launch_bounds__(kTopkThreads) topk_phase1(const T* __restrict_
   __shared__ double red_d[kTopkThreads / 32];
   __shared__ int red_i[kTopkThreads / 32];
   const T* src = logits + static_cast<size_t>(row) * ld;
+  constexpr int kPer = kTopkChunk / kTopkThreads;
   float lmax = -INFINITY;
-  for (int i = begin + threadIdx.x; i < end; i += blockDim.x) {
-    float v = to_f32(src[i]) * inv_temp;
-    sv[i - begin] = v;
-    lmax = fmaxf(lmax, v);
+  {
+    float xv[kPer];  // all of this thread's loads in flight together
+#pragma unroll
+    for (int j = 0; j < kPer; ++j) {
+      const int i = begin + threadIdx.x + j * kTopkThreads;
+      xv[j] = i < end ? to_f32(src[i]) * inv_temp : -INFINITY;
+    }
+#pragma unroll
+    for (int j = 0; j < kPer; ++j) {
+      const int i = begin + threadIdx.x + j * kTopkThreads;
+      if (i < end) sv[i - begin] = xv[j];
+      lmax = fmaxf(lmax, xv[j]);
+    }
   }
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   lmax = warp_max(lmax);
@@ -81,10 +91,10 @@ __global__ void __launch_bounds__(kTopkThreads) topk_phase1(const T* __restrict_
     o->sum_exp = tot;
   }
   // Top-k of the chunk by a tournament over 64-bit keys ordered exactly like better() (logit desc,
-  // token asc; NaN excluded): every thread keeps its 16 elements as keys and its current best; each
-  // warp pops its k best with two redux.sync max reductions per round (only the popping lane rescans
-  // its 16), then warp 0 pops the chunk's k best over the 8 warps' lists.
-  constexpr int kPer = kTopkChunk / kTopkThreads;
+  // token asc; NaN excluded): every thread keeps its 16 elements as keys, its best and second best;
+  // each warp pops its k best with two redux.sync max reductions per round — a lane's next key after
+  // a pop is its cached second best, or (third pop onwards, rare) the largest of its keys below the
+  // popped one (keys are unique) — then warp 0 pops the chunk's k best over the 8 warps' lists.
   constexpr int NW = kTopkThreads / 32;
   __shared__ unsigned long long wsel[NW][kTopkMaxK];
   unsigned long long mk[kPer];
@@ -94,23 +104,31 @@ __global__ void __launch_bounds__(kTopkThreads) topk_phase1(const T* __restrict_
     const float v = i < end ? sv[i - begin] : __int_as_float(0x7fc00000);
     mk[j] = isnan(v) ? kNoKey : topk_key(v, i);
   }
-  uint32_t taken = 0u;
-  auto best_left = [&]() {
-    unsigned long long b = kNoKey;
+  unsigned long long cur = kNoKey, second = kNoKey;
 #pragma unroll
-    for (int j = 0; j < kPer; ++j)
-      if (!((taken >> j) & 1u) && mk[j] > b) b = mk[j];
-    return b;
-  };
-  unsigned long long cur = best_left();
+  for (int j = 0; j < kPer; ++j) {
+    const unsigned long long x = mk[j];
+    if (x > cur) {
+      second = cur;
+      cur = x;
+    } else if (x > second) {
+      second = x;
+    }
+  }
+  int pops = 0;
   for (int r = 0; r < k; ++r) {
     const unsigned long long win = warp_max_key(cur);
     if (lane == 0) wsel[warp][r] = win;
     if (win != kNoKey && cur == win) {  // keys are unique (distinct indices): exactly one lane pops
+      if (++pops == 1) {
+        cur = second;
+      } else {
+        unsigned long long nb = kNoKey;
 #pragma unroll
-      for (int j = 0; j < kPer; ++j)
-        if (mk[j] == win) taken |= 1u << j;
-      cur = best_left();
+        for (int j = 0; j < kPer; ++j)
+          if (mk[j] < win && mk[j] > nb) nb = mk[j];
+        cur = nb;
+      }
     }
   }
   __syncthreads();
